@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py -- 3LC state-change compression throughput on B200.
+
+One step = one pass of the whole hot path over
+one synthetic state-change tensor: tlc_compress (accumulate + global max, quantize +
+residual, quartic encode, zero-run encode) followed by tlc_decompress (ZRE expand,
+quartic decode, dequantize), through the C ABI of include/tlc.h.
+
+Workload at N=1 (BASELINE.json configs[2], the config the metric's "% HBM peak" is
+quoted on -- north_star: ">= 64M-element tensors"): one 268,435,456-element fp32
+tensor, s = 1.75, N(0,1) state changes with the error-accumulation buffer carried
+across steps (steady state), zero-run encoding on.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tlc|reference]
+
+For N > 1 (torchrun, one rank per GPU, NCCL) each rank runs the same workload on its
+own tensor (weak scaling); timing is the max over ranks.  `--impl reference` times
+the CPU oracle (oracle/, the deliberately slow reference) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress+decompress fp32 GB/s per B200 (% HBM peak); bits/value; 8-GPU xchg"
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["tlc", "reference"], default="tlc")
+    ap.add_argument("--n", type=int, default=1 << 28)
+    ap.add_argument("--s", type=float, default=1.75)
+    ap.add_argument("--no-zre", action="store_true")
+    ap.add_argument("--inputs", type=int, default=2, help="rotating state-change tensors")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def workload_name(n, s, zre):
+    return (f"C3: single {n:,}-element fp32 state-change tensor, s={s}, gauss-steady "
+            f"(N(0,1) per step, error buffer carried){'' if zre else ', ZRE off'}")
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def load_traffic(kernel, n):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), if one exists for this n."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(kernel)
+        if e and int(e.get("n", -1)) == n:
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while running."""
+
+    def __init__(self, device, period: float = 0.005):
+        self.period = period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        for k, bit in names.items():
+            if r & bit and k != "gpu_idle":
+                self.reasons.add(k)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.nv:
+            self._stop.set()
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_roundtrips(n_sample: int, s: float, zre: bool, seconds: float = None, reps: int = None):
+    """Time the CPU oracle (as it stands, single thread) on compress+decompress round
+    trips of an n_sample-element tensor of the same workload family."""
+    import numpy as np
+
+    import oracle as O
+    import synth
+
+    ts = [synth.gaussian(n_sample, 3, k) for k in range(2)]
+    buf = np.zeros(n_sample, np.float32)
+    c = O.compress(ts[0], buf, s, zre)         # untimed warm-up (builds/loads the lib)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        c = O.compress(ts[done % 2], buf, s, zre)
+        st, out = O.decompress(c.payload, zre, c.M, n_sample)
+        done += 1
+        el = time.perf_counter() - t0
+        if (reps is not None and done >= reps) or (seconds is not None and el >= seconds):
+            break
+    return {"value": 4.0 * n_sample * done / el / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} compress+decompress round trips of a {n_sample:,}-element N(0,1) fp32 "
+                      f"tensor (same generator, s={s}, error buffer carried), single thread, "
+                      f"{el:.1f} s", "seconds": el, "bits_per_value": 8.0 * c.payload_len / n_sample}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    zre = not args.no_zre
+    for _ in range(args.warmup):
+        oracle_roundtrips(args.cpu_sample, args.s, zre, reps=1)
+    r = oracle_roundtrips(args.cpu_sample, args.s, zre, reps=max(1, args.steps))
+    ms = 1000.0 * r["seconds"] / max(1, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: N(0,1) fp32 state changes (numpy PCG64), error buffer carried",
+        "config": {"workload": workload_name(args.n, args.s, zre) + f"; each step a bounded "
+                   f"{args.cpu_sample:,}-element sample on the host", "n": args.n, "s": args.s},
+        "bits_per_value": r["bits_per_value"],
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ the GPU leg
+def run_tlc(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_07389_b200 as T
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n, s, zre = args.n, float(args.s), not args.no_zre
+    # Inputs: seeded host generator (same module the oracle tests use), copied once
+    # to HBM before any timing; each rank draws its own stream.
+    ts = [torch.from_numpy(synth.gaussian(n, 3, 1000 * rank + k)).to(dev) for k in range(args.inputs)]
+    err = torch.zeros(n, dtype=torch.float32, device=dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    payload = torch.empty(T.tlc_max_payload_bytes(n), dtype=torch.uint8, device=dev)
+    hdr = T.new_header(dev)
+    ws_c = torch.empty(T.tlc_compress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    ws_d = torch.empty(T.tlc_decompress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        T.tlc_compress(ts[k % len(ts)], err, s, zre, payload, hdr, ws_c, stream)
+        T.tlc_decompress(payload, hdr, n, out, T.TLC_MODE_OVERWRITE, ws_d, stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    for k in range(max(3, args.warmup)):
+        step(k)
+    barrier()
+    h = T.parse_header(hdr)
+    if h["status"] != 0:
+        raise RuntimeError(f"compress status {h}")
+
+    # ---------------- timed region (device events on the launching stream)
+    K = args.steps
+    clocks = ClockSampler(dev)
+    T.tlc_prof_collect()
+    launches0 = T.tlc_launch_count()
+    T.tlc_prof_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    clocks.start()
+    e0.record(stream)
+    for k in range(K):
+        step(k)
+    e1.record(stream)
+    barrier()
+    clocks.stop()
+    T.tlc_prof_enable(False)
+    gpu_launches = T.tlc_launch_count() - launches0
+    prof = T.tlc_prof_collect()
+    ms = e0.elapsed_time(e1)
+    h = T.parse_header(hdr)
+    Z = h["payload_len"]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * 4.0 * n * K / (ms / 1e3) / 1e9
+
+    # ---------------- roofline of the dominant kernel (K2) and the per-kernel table
+    peak, peak_src = load_peaks()
+    alg = {  # algorithmic HBM bytes per launch
+        "k1_absmax": 8.0 * n,
+        "k2_quant_qe_zre": 12.0 * n + Z,
+        "k4_zre_scan": float(Z),
+        "k5_expand_dequant": 4.0 * n + Z,
+    }
+    kernels = {}
+    for name, (cnt, tot) in prof.items():
+        avg = tot / max(cnt, 1)
+        b = alg.get(name)
+        kernels[name] = {"launches_per_step": cnt / K, "avg_ms": avg,
+                         "alg_bytes": b, "alg_GBps": (b / (avg / 1e3) / 1e9) if b else None,
+                         "share_of_step": (tot / K) / (ms / K) if ms else None}
+    dom = "k2_quant_qe_zre"
+    dk = kernels.get(dom, {})
+    achieved = dk.get("alg_GBps")
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": load_traffic(dom, n),
+                "peak_source": peak_src,
+                "alg_bytes_per_launch": alg[dom], "alg_bytes_formula": "12n + Z (read t, err; write err, payload)"}
+    step_bytes = sum(alg.values())
+    hbm_frac_step = step_bytes / (ms / K / 1e3) / 1e9 / peak
+
+    # ---------------- end to end through the same C-ABI calls, host buffers
+    e2e = None
+    if not args.no_e2e:
+        th = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        th.copy_(ts[0].cpu())
+        oh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        td = torch.empty_like(ts[0])
+        E = max(1, args.e2e_steps)
+
+        def e2e_step():
+            td.copy_(th, non_blocking=True)
+            T.tlc_compress(td, err, s, zre, payload, hdr, ws_c, stream)
+            T.tlc_decompress(payload, hdr, n, out, T.TLC_MODE_OVERWRITE, ws_d, stream)
+            oh.copy_(out, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(E):
+            e2e_step()
+        f1.record(stream)
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * 4.0 * n * E / (ems / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "steps": E,
+               "ms_per_step": ems / E,
+               "what": "pinned host t -> HBM, tlc_compress, tlc_decompress, HBM -> pinned host out"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_roundtrips(args.cpu_sample, s, zre, seconds=args.cpu_seconds)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: N(0,1) fp32 state changes (numpy PCG64, synth/), "
+                    f"{len(ts)} rotating tensors per rank, error buffer carried across steps",
+            "config": {"workload": workload_name(n, s, zre), "n": n, "s": s, "use_zre": zre,
+                       "family": "gauss-steady",
+                       "l2": "inputs larger than L2 (t, err, out 1 GiB each vs 126 MB L2); no flush",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "bits_per_value": 8.0 * Z / n,
+            "compression_ratio": 4.0 * n / Z if Z else None,
+            "hbm_frac_step": hbm_frac_step,
+            "roofline": roofline,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_tlc(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,160 @@
+/*
+ * tlc.h -- C ABI of the B200-native 3LC state-change compression library
+ * (libtlc.so, built from paper_1802_07389_b200/csrc/).
+ *
+ * The operation is 3LC's compressor (arXiv 1802.07389, Sec. 3, Fig.
+ * "fig:compression"; PAPER.md lines cited as P:n, SPEC.md lines as S:n):
+ *
+ *   (1)  u = err + t                                  P:406-408 (Fig. step 1)
+ *   Eq.1 M = fl(max|u| * s),  1 <= s < 2
+ *   Eq.2 q = round(u / M) in {-1,0,1}, half away       P:379, reading R1
+ *   (a,b) err = u - M*q   (exact, Sterbenz)
+ *   (3)  quartic: B[j] = sum_i 3^(4-i) * (q[iP+j]+1)   P:495-510, P = ceil(n/5)
+ *   (4)  zero-run: runs of 121 -> 243+(k-2), k<=14
+ *
+ * and its inverse (ZRE expand, base-3 decode, Eq.3 T_out = M*q).
+ * The readings R1..R20 the implementation takes where the paper is silent are
+ * listed in DESIGN.md section 3.
+ *
+ * Conventions for every call below:
+ *  - Pointers named t, err, payload, hdr, out, ws are DEVICE pointers (cudaMalloc
+ *    / torch CUDA storage) owned by the caller; the library allocates nothing on
+ *    the hot path.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Calls enqueue work on `stream` and return without synchronizing.
+ *  - Argument errors are returned synchronously (TLC_ERR_ARG / TLC_ERR_CAPACITY /
+ *    TLC_ERR_CUDA).  Data errors are raised ON THE DEVICE into hdr->status
+ *    (NONFINITE, RANGE, FORMAT); the caller reads them after synchronizing.
+ *  - Results are bit-identical to the CPU oracle (oracle/tlc_oracle.c) for
+ *    the same inputs: payload bytes, err, and decompressed values (0 ulp).
+ */
+#ifndef TLC_H
+#define TLC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  S:164 (s out of range is a hard error), S:33/S:70 (NaN/Inf
+ * rejected), S:214/S:235 (malformed payload), reading R6 (M overflow). */
+typedef enum tlc_status {
+    TLC_OK = 0,
+    TLC_ERR_ARG = 1,        /* null pointer, n == 0, s not in [1,2), bad mode      */
+    TLC_ERR_NONFINITE = 2,  /* device: some u = err + t is NaN or +-Inf             */
+    TLC_ERR_RANGE = 3,      /* device: max|u| * s overflows fp32                    */
+    TLC_ERR_FORMAT = 4,     /* device: payload does not decode to exactly P bytes,  */
+                            /*   a literal > 242 without ZRE, or hdr->n != n         */
+    TLC_ERR_CAPACITY = 5,   /* payload_cap < ceil(n/5) or workspace too small       */
+    TLC_ERR_CUDA = 6,       /* a CUDA runtime call failed (launch, memset)          */
+    TLC_ERR_NCCL = 7        /* an NCCL call failed (exchange)                       */
+} tlc_status;
+
+/* Device-resident header of one compressed tensor (32 bytes, naturally
+ * aligned).  Written by tlc_compress, read by tlc_decompress.  This is the
+ * scalar M "sent next to the payload". */
+typedef struct tlc_header {
+    float M;               /* fl(max|u| * s); 0 for an all-zero u (R5)               */
+    uint32_t flags;        /* bit 0: payload is zero-run encoded (TLC_FLAG_ZRE)       */
+    uint64_t n;            /* element count of the state-change tensor               */
+    uint64_t payload_len;  /* payload bytes: Z with ZRE, P = ceil(n/5) without       */
+    uint32_t status;       /* tlc_status raised on the device (0 = OK)               */
+    uint32_t reserved;
+} tlc_header;
+
+#define TLC_FLAG_ZRE 1u
+#define TLC_MODE_OVERWRITE 0   /* out  = M*q                     (Eq. 3)     */
+#define TLC_MODE_ACCUMULATE 1  /* out += M*q where q != 0        (reading R16)      */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int tlc_version(void);
+
+/* Human-readable name of a tlc_status value; never NULL. */
+const char *tlc_status_string(int status);
+
+/* P = ceil(n/5): quartic bytes of an n-element tensor (step 4).   */
+uint64_t tlc_quartic_bytes(uint64_t n);
+
+/* Payload capacity the caller must provide: P (ZRE never expands).    */
+uint64_t tlc_max_payload_bytes(uint64_t n);
+
+/* Workspace bytes (device memory, 256-byte aligned) for one compress /
+ * decompress of n elements.  A workspace may be reused by consecutive calls on
+ * the same stream, never by concurrent calls. */
+size_t tlc_compress_workspace_bytes(uint64_t n);
+size_t tlc_decompress_workspace_bytes(uint64_t n);
+
+/*
+ * tlc_compress -- Fig. "fig:compression" steps (1),(2),(a),(b),(3),(4).
+ *
+ *  t        [in]  fp32[n], the state change T_in (gradient or model delta).
+ *  err      [in/out] fp32[n], the error-accumulation buffer of this tensor's
+ *                 compression context.  Zero-initialised by the
+ *                 caller before the first call (R20); one writer at a time
+ *                 (S:167).  Left unmodified when a data error is raised.
+ *                 Must not alias t or payload.
+ *  n        number of elements, >= 1.
+ *  s        sparsity multiplier, fp32, 1 <= s < 2.
+ *  use_zre  nonzero: apply zero-run encoding (step 4); 0: payload = quartic bytes.
+ *  payload  [out] u8[payload_cap], payload_cap >= tlc_max_payload_bytes(n).
+ *  hdr      [out] device header: M, flags, n, payload_len, status.
+ *  ws       device workspace of >= tlc_compress_workspace_bytes(n) bytes.
+ *  stream   cudaStream_t.
+ *
+ * Returns TLC_OK once enqueued; TLC_ERR_ARG / TLC_ERR_CAPACITY / TLC_ERR_CUDA
+ * synchronously.  Device-side: hdr->status = NONFINITE / RANGE (R6).
+ * Layout: t, err flat row-major fp32; payload bytes in stream order.
+ */
+int tlc_compress(const float *t, float *err, uint64_t n, float s, int use_zre,
+                 uint8_t *payload, uint64_t payload_cap, tlc_header *hdr,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * tlc_decompress -- the reverse path: ZRE expand, quartic decode
+ * (P:512-522), dequantize T_out = M*q (Eq. 3).
+ *
+ *  payload  [in] u8[hdr->payload_len] as written by tlc_compress (or received).
+ *  hdr      [in/out] header of that payload; hdr->status is set to
+ *           TLC_ERR_FORMAT on a malformed payload.  If hdr->status is already
+ *           nonzero the call does nothing on the device.
+ *  n        element count; must equal hdr->n (checked on the device).
+ *  out      [out or in/out] fp32[n].  mode TLC_MODE_OVERWRITE writes M*q;
+ *           TLC_MODE_ACCUMULATE adds M*q only where q != 0 (R16), leaving the
+ *           other elements untouched (used to apply pulled model deltas and
+ *           to aggregate pushes in rank order, R15).
+ *  ws       device workspace of >= tlc_decompress_workspace_bytes(n) bytes.
+ *
+ * On FORMAT no byte outside out[0, n) is written; the contents of out are
+ * then unspecified.
+ */
+int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *out,
+                   int mode, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Instrumentation (host-side, not part of the method).
+ *
+ * tlc_launch_count: number of kernels this library has launched in the
+ *   process so far (bench.py reports the difference over the timed region).
+ * tlc_prof_enable: when on, every library kernel launch is bracketed by a pair
+ *   of CUDA events on its stream.
+ * tlc_prof_collect: synchronizes the recorded events and writes up to `cap`
+ *   entries {kernel name (static string), launches, summed device ms} to
+ *   `out` (host memory); returns the number of distinct kernels seen and
+ *   resets the record.
+ */
+typedef struct tlc_prof_entry {
+    const char *name;
+    unsigned long long launches;
+    double total_ms;
+} tlc_prof_entry;
+
+unsigned long long tlc_launch_count(void);
+void tlc_prof_enable(int on);
+int tlc_prof_collect(tlc_prof_entry *out, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TLC_H */

@@ -1,0 +1,99 @@
+// prof.cu -- launch counting and optional per-kernel CUDA-event timing.
+//
+// Every kernel launch of the library goes through KernelScope, which bumps a
+// global launch counter and, when profiling is enabled (tlc_prof_enable),
+// brackets the launch with a pair of CUDA events recorded on the launching
+// stream.  tlc_prof_collect() synchronizes those events and reports per-kernel
+// launch counts and summed device durations -- bench.py uses it for the live
+// roofline of the dominant kernel.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "tlc_launch.h"
+
+namespace tlc {
+
+static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe_zre", "k4_zre_scan",
+                                            "k5_expand_dequant", "k6_compress_batched",
+                                            "k7_decompress_batched", "k8_scale"};
+
+namespace {
+struct Rec {
+    int id;
+    cudaEvent_t a, b;
+};
+std::atomic<unsigned long long> g_launches{0};
+std::atomic<bool> g_on{false};
+std::mutex g_mu;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t get_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+KernelScope::KernelScope(int id, cudaStream_t st) : id_(id), st_(st), a_(nullptr) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (g_on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        a_ = get_event();
+        cudaEventRecord((cudaEvent_t)a_, st_);
+    }
+}
+
+KernelScope::~KernelScope() {
+    if (a_) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        cudaEvent_t b = get_event();
+        cudaEventRecord(b, st_);
+        g_recs.push_back(Rec{id_, (cudaEvent_t)a_, b});
+    }
+}
+
+}  // namespace tlc
+
+using namespace tlc;
+
+extern "C" {
+
+unsigned long long tlc_launch_count(void) { return g_launches.load(); }
+
+void tlc_prof_enable(int on) { g_on.store(on != 0); }
+
+int tlc_prof_collect(tlc_prof_entry *out, int cap) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    double ms[kNumKernelIds] = {0};
+    unsigned long long cnt[kNumKernelIds] = {0};
+    for (auto &r : g_recs) {
+        float t = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&t, r.a, r.b);
+        ms[r.id] += t;
+        cnt[r.id] += 1;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    int k = 0;
+    for (int i = 0; i < kNumKernelIds; i++) {
+        if (!cnt[i]) continue;
+        if (k < cap && out) {
+            out[k].name = kNames[i];
+            out[k].launches = cnt[i];
+            out[k].total_ms = ms[i];
+        }
+        k++;
+    }
+    return k;
+}
+
+}  // extern "C"

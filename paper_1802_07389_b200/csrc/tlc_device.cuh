@@ -1,0 +1,171 @@
+// tlc_device.cuh -- device-side building blocks shared by the sm_100a kernels.
+//
+// Nothing here is shared with oracle/ (the CPU oracle is an independent
+// transcription of the paper); see DESIGN.md section 5 for the kernel designs.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/tlc.h"
+
+namespace tlc {
+
+// ---------------------------------------------------------------- constants
+constexpr uint8_t kZeroGroup = 121;        // five zero trits
+constexpr uint8_t kFirstRunCode = 243;     // 243+(k-2), 2 <= k <= 14
+constexpr uint32_t kMaxRun = 14;
+
+// Per-call control block at the start of every workspace (zeroed by a
+// cudaMemsetAsync at the start of each call, together with the look-back
+// tile states that follow it).
+struct Ctrl {
+    unsigned int tile_counter;   // dynamic tile ids (forward-progress ordering)
+    unsigned int done_counter;   // K1 last-block detection
+    float M;                     // fl(max|u| * s) (Eq. 1)
+    unsigned int status;         // tlc_status from K1
+    unsigned int maxkey;         // max of (bits(u) & 0x7fffffff)
+    unsigned int pad[59];
+};
+static_assert(sizeof(Ctrl) == 256, "ctrl is one 256-byte block");
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Streaming loads of data read exactly once by this kernel.
+__device__ __forceinline__ float ld_stream(const float *p) { return __ldcs(p); }
+__device__ __forceinline__ float4 ld_stream4(const float4 *p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------- quantizer
+// Eq. 2 with round-half-away (R1) and the residual of steps (a),(b), given
+// M = fl(max|u| * s).  Three uniform regimes (the branch is the same for the
+// whole launch):
+//   M == 0           -> q = 0, err = u                                   (R5)
+//   M >= 2^-125      -> q = sign(u) * [|u| >= M/2]; M/2 is exact, and
+//                       fl(u/M) >= 1/2  <=>  u >= M/2 exactly
+//   0 < M < 2^-125   -> q from the IEEE quotient __fdiv_rn(u, M)          (R4)
+struct Quant {
+    float M, halfM;
+    int mode;  // 0: zero, 1: compare, 2: divide
+    __device__ __forceinline__ Quant(float m) : M(m), halfM(m * 0.5f) {  // exact when used (M >= 2^-125)
+        mode = (m == 0.0f) ? 0 : (m >= 2.350988701644575e-38f /* 2^-125 */ ? 1 : 2);
+    }
+    __device__ __forceinline__ int q(float u) const {
+        if (mode == 1) {
+            return fabsf(u) >= halfM ? (u > 0.0f ? 1 : -1) : 0;
+        } else if (mode == 2) {
+            float x = __fdiv_rn(u, M);
+            return (x >= 0.5f) - (x <= -0.5f);
+        }
+        return 0;
+    }
+    // err = u - M*q (exact by Sterbenz when q != 0; u - (+0) == u otherwise)
+    __device__ __forceinline__ float residual(float u, int q) const {
+        return q == 0 ? u : __fsub_rn(u, q > 0 ? M : -M);
+    }
+};
+
+// ---------------------------------------------------------------- ZRE run summary monoid
+// A stretch of quartic bytes acts on the incoming carry c = (length of the
+// 121-run that ends just before it) mod 14 as
+//     ALL (every byte is 121, length L, `ends` = the run stops right after):
+//         count(c) = floor((c+L)/14) + [ends && (c+L)%14 != 0],  carry' = (c+L)%14
+//     MIX (contains a non-121 byte; leading run lead = 14a + r0, nz = lead>0):
+//         count(c) = cnt + (nz ? ceil((c+r0)/14) : 0),          carry' = tr
+// where count = emitted ZRE bytes (P:545-546 greedy chunks of <= 14, emitted at
+// chunk end) and tr = trailing 121-run length mod 14.  Composition of these
+// transfer functions is associative, which makes the zero-run encoder a
+// single-pass scan with decoupled look-back.
+//
+// Packing (64 bit):  bits 0..43 L|cnt, bit 44 ends|nz, 45..48 r0, 49..52 tr,
+//                    bit 53 kind (1 = MIX), bits 62..63 look-back status.
+struct RunSum {
+    uint64_t v;   // L or cnt
+    uint32_t r0, tr;
+    bool flag;    // ends (ALL) or nz (MIX)
+    bool mix;
+};
+
+constexpr unsigned long long kStatusAgg = 1ull << 62;
+constexpr unsigned long long kStatusPrefix = 2ull << 62;
+constexpr unsigned long long kStatusMask = 3ull << 62;
+
+__host__ __device__ __forceinline__ unsigned long long pack(const RunSum &s) {
+    return (s.v & ((1ull << 44) - 1)) | ((unsigned long long)s.flag << 44) |
+           ((unsigned long long)s.r0 << 45) | ((unsigned long long)s.tr << 49) |
+           ((unsigned long long)s.mix << 53);
+}
+__host__ __device__ __forceinline__ RunSum unpack(unsigned long long w) {
+    RunSum s;
+    s.v = w & ((1ull << 44) - 1);
+    s.flag = (w >> 44) & 1;
+    s.r0 = (w >> 45) & 15;
+    s.tr = (w >> 49) & 15;
+    s.mix = (w >> 53) & 1;
+    return s;
+}
+__host__ __device__ __forceinline__ RunSum run_identity() { return RunSum{0, 0, 0, false, false}; }
+__host__ __device__ __forceinline__ bool is_identity(const RunSum &s) { return !s.mix && s.v == 0; }
+
+// a then b
+__host__ __device__ __forceinline__ RunSum compose(const RunSum &a, const RunSum &b) {
+    if (is_identity(a)) return b;
+    if (is_identity(b)) return a;
+    RunSum r;
+    if (!a.mix) {
+        if (!b.mix) {  // ALL . ALL
+            r = a;
+            r.v = a.v + b.v;
+            r.flag = b.flag;
+            return r;
+        }
+        // ALL . MIX: a's run prefixes b's leading run
+        uint64_t x = a.v + b.r0;
+        r.mix = true;
+        r.flag = true;
+        r.r0 = (uint32_t)(x % kMaxRun);
+        r.v = b.v + x / kMaxRun;
+        r.tr = b.tr;
+        return r;
+    }
+    if (!b.mix) {  // MIX . ALL
+        uint64_t x = a.tr + b.v;
+        r = a;
+        r.v = a.v + x / kMaxRun + ((b.flag && (x % kMaxRun) != 0) ? 1 : 0);
+        r.tr = (uint32_t)(x % kMaxRun);
+        return r;
+    }
+    // MIX . MIX
+    r = a;
+    r.v = a.v + b.v + (b.flag ? (a.tr + b.r0 + kMaxRun - 1) / kMaxRun : 0);
+    r.tr = b.tr;
+    return r;
+}
+
+// (emitted count, carry) of a stretch entered with carry c
+__host__ __device__ __forceinline__ void run_eval(const RunSum &s, uint32_t c, uint64_t &count,
+                                                  uint32_t &carry) {
+    if (!s.mix) {
+        uint64_t x = c + s.v;
+        count = x / kMaxRun + ((s.flag && (x % kMaxRun) != 0) ? 1 : 0);
+        carry = (uint32_t)(x % kMaxRun);
+    } else {
+        count = s.v + (s.flag ? (c + s.r0 + kMaxRun - 1) / kMaxRun : 0);
+        carry = s.tr;
+    }
+}
+
+__device__ __forceinline__ unsigned long long shfl_up64(unsigned long long v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+__device__ __forceinline__ unsigned long long shfl_down64(unsigned long long v, int d) {
+    return __shfl_down_sync(0xffffffffu, v, d);
+}
+
+}  // namespace tlc
