@@ -125,11 +125,10 @@ constexpr int kTile = kK2Threads * kK2BytesPerThread;    // 2048 quartic bytes p
 constexpr int kK2Warps = kK2Threads / 32;
 
 struct K2Smem {
-    alignas(16) uint8_t B[kTile + 16];   // quartic bytes of the tile (+ look-ahead flag slot)
+    alignas(16) uint8_t B[kTile];        // quartic bytes of the tile
     unsigned long long warp_incl[kK2Warps];
     unsigned long long tile_excl;
     unsigned int tile;
-    unsigned int lookahead121;
 };
 
 // One quartic byte from the five strided elements e_i = i*P + j.
@@ -269,42 +268,6 @@ __device__ __forceinline__ void k2_phase_a_vec(const float *__restrict__ t, floa
     }
 }
 
-// Summary of the bytes [0, len) of one thread's segment; next121 tells whether
-// the byte after the segment is a 121 (false at the end of the stream).
-__device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[kK2BytesPerThread], int len,
-                                                  bool next121) {
-    if (len <= 0) return run_identity();
-    int lead = 0;
-    while (lead < len && b[lead] == kZeroGroup) lead++;
-    RunSum s;
-    if (lead == len) {
-        s = run_identity();
-        s.v = (uint64_t)len;
-        s.flag = !next121;
-        return s;
-    }
-    uint64_t cnt = 0;
-    uint32_t o = 0;   // offset inside the current 121-run
-#pragma unroll
-    for (int m = 0; m < kK2BytesPerThread; m++) {
-        if (m < lead || m >= len) continue;
-        if (b[m] != kZeroGroup) {
-            cnt++;
-            o = 0;
-        } else {
-            bool nxt = (m + 1 < len) ? (b[m + 1] == kZeroGroup) : next121;
-            if ((o % kMaxRun) == kMaxRun - 1 || !nxt) cnt++;
-            o++;
-        }
-    }
-    s.mix = true;
-    s.flag = lead > 0;
-    s.r0 = (uint32_t)(lead % kMaxRun);
-    s.v = cnt + lead / kMaxRun;
-    s.tr = o % kMaxRun;
-    return s;
-}
-
 template <bool kVec, bool kZre>
 __global__ void __launch_bounds__(kK2Threads)
 tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
@@ -330,18 +293,6 @@ tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, ui
         else k2_phase_a_scalar<!kZre>(t, err, n, P, j0, tile_len, Q, sm.B, payload);
 
         if (kZre) {
-            // look-ahead: is quartic byte j0 + kTile a 121?  (needs all 5 trits == 0
-            // and no pad position).  Computed by lanes 0..4 of warp 0, err untouched.
-            if (warp == 0) {
-                const uint64_t jn = j0 + kTile;
-                bool zero = false;
-                if (lane < 5 && jn < P) {
-                    const uint64_t e = (uint64_t)lane * P + jn;
-                    if (e < n) zero = Q.q(__fadd_rn(__ldcg(err + e), __ldcg(t + e))) == 0;
-                }
-                unsigned int bal = __ballot_sync(0xffffffffu, zero);
-                if (lane == 0) sm.lookahead121 = (bal & 0x1fu) == 0x1fu;
-            }
             __syncthreads();
 
             // ---------------- phase B: per-thread run summaries, block scan
@@ -355,12 +306,7 @@ tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, ui
 #pragma unroll
                 for (int m = 0; m < 4; m++) b[4 + m] = (w.y >> (8 * m)) & 0xff;
             }
-            const int nxt_pos = sbeg + kK2BytesPerThread;
-            bool next121;
-            if (nxt_pos < tile_len) next121 = sm.B[nxt_pos] == kZeroGroup;
-            else if (tile_len == kTile && nxt_pos == kTile) next121 = sm.lookahead121 != 0;
-            else next121 = false;                                   // end of stream
-            const RunSum mine = segment_summary(b, slen, next121);
+            const RunSum mine = segment_summary(b, slen);
 
             // warp inclusive scan
             unsigned long long x = pack(mine);
@@ -414,7 +360,7 @@ tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, ui
                         uint64_t total;
                         uint32_t carry;
                         run_eval(compose(excl, agg), 0, total, carry);
-                        hdr->payload_len = total;
+                        hdr->payload_len = total + (carry > 0);   // end of stream flushes
                     }
                 }
                 // warp exclusive prefixes for the block: reuse warp_incl as exclusive
@@ -437,21 +383,9 @@ tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, ui
                 uint64_t off;
                 uint32_t c;
                 run_eval(before, 0, off, c);
-#pragma unroll
-                for (int m = 0; m < kK2BytesPerThread; m++) {
-                    if (m >= slen) break;
-                    if (b[m] != kZeroGroup) {
-                        payload[off++] = b[m];
-                        c = 0;
-                    } else {
-                        bool nxt = (m + 1 < slen) ? (b[m + 1] == kZeroGroup) : next121;
-                        if (c == kMaxRun - 1 || !nxt) {
-                            uint32_t L = c + 1;     // chunk length 1..14
-                            payload[off++] = (L == 1) ? kZeroGroup : (uint8_t)(kFirstRunCode + (L - 2));
-                        }
-                        c = (c + 1) % kMaxRun;
-                    }
-                }
+                segment_emit(b, slen, c, payload, off);
+                // the thread holding the last byte of the stream flushes the pending run
+                if (c > 0 && j0 + sbeg + slen == P) payload[off] = run_code(c);
             }
         }
         __syncthreads();   // sm.B / sm.tile reuse

@@ -72,23 +72,26 @@ struct Quant {
 };
 
 // ---------------------------------------------------------------- ZRE run summary monoid
-// A stretch of quartic bytes acts on the incoming carry c = (length of the
-// 121-run that ends just before it) mod 14 as
-//     ALL (every byte is 121, length L, `ends` = the run stops right after):
-//         count(c) = floor((c+L)/14) + [ends && (c+L)%14 != 0],  carry' = (c+L)%14
-//     MIX (contains a non-121 byte; leading run lead = 14a + r0, nz = lead>0):
-//         count(c) = cnt + (nz ? ceil((c+r0)/14) : 0),          carry' = tr
-// where count = emitted ZRE bytes (P:545-546 greedy chunks of <= 14, emitted at
-// chunk end) and tr = trailing 121-run length mod 14.  Composition of these
-// transfer functions is associative, which makes the zero-run encoder a
-// single-pass scan with decoupled look-back.
+// Zero-run encoding (greedy chunks of <= 14 from the run start, R11)
+// is produced left to right with one carry: c = number of 121 bytes seen but
+// not yet emitted (0..13).  A 121 byte increments c and emits 255 when c hits
+// 14; any other byte first flushes a pending chunk (121 if c == 1, else
+// 243+(c-2)) and then emits itself; the end of the stream flushes too.  A
+// stretch of quartic bytes therefore acts on the incoming carry as
+//     ALL (every byte is 121, length L):
+//         count(c) = floor((c+L)/14),                  carry' = (c+L) % 14
+//     MIX (contains a non-121 byte; leading 121-run of length 14a + r0):
+//         count(c) = cnt + ceil((c+r0)/14),            carry' = tr
+// with cnt = a + emissions from the first non-121 byte on, tr = trailing run
+// length mod 14.  Composition of these transfer functions is associative, so
+// the encoder is one scan with decoupled look-back and needs no look-ahead
+// (DESIGN.md section 5.3).
 //
-// Packing (64 bit):  bits 0..43 L|cnt, bit 44 ends|nz, 45..48 r0, 49..52 tr,
-//                    bit 53 kind (1 = MIX), bits 62..63 look-back status.
+// Packing (64 bit): bits 0..43 L|cnt, 45..48 r0, 49..52 tr, bit 53 kind
+// (1 = MIX), bits 62..63 look-back status.
 struct RunSum {
     uint64_t v;   // L or cnt
     uint32_t r0, tr;
-    bool flag;    // ends (ALL) or nz (MIX)
     bool mix;
 };
 
@@ -97,53 +100,45 @@ constexpr unsigned long long kStatusPrefix = 2ull << 62;
 constexpr unsigned long long kStatusMask = 3ull << 62;
 
 __host__ __device__ __forceinline__ unsigned long long pack(const RunSum &s) {
-    return (s.v & ((1ull << 44) - 1)) | ((unsigned long long)s.flag << 44) |
-           ((unsigned long long)s.r0 << 45) | ((unsigned long long)s.tr << 49) |
-           ((unsigned long long)s.mix << 53);
+    return (s.v & ((1ull << 44) - 1)) | ((unsigned long long)s.r0 << 45) |
+           ((unsigned long long)s.tr << 49) | ((unsigned long long)s.mix << 53);
 }
 __host__ __device__ __forceinline__ RunSum unpack(unsigned long long w) {
     RunSum s;
     s.v = w & ((1ull << 44) - 1);
-    s.flag = (w >> 44) & 1;
     s.r0 = (w >> 45) & 15;
     s.tr = (w >> 49) & 15;
     s.mix = (w >> 53) & 1;
     return s;
 }
-__host__ __device__ __forceinline__ RunSum run_identity() { return RunSum{0, 0, 0, false, false}; }
-__host__ __device__ __forceinline__ bool is_identity(const RunSum &s) { return !s.mix && s.v == 0; }
+__host__ __device__ __forceinline__ RunSum run_identity() { return RunSum{0, 0, 0, false}; }
 
 // a then b
 __host__ __device__ __forceinline__ RunSum compose(const RunSum &a, const RunSum &b) {
-    if (is_identity(a)) return b;
-    if (is_identity(b)) return a;
     RunSum r;
     if (!a.mix) {
         if (!b.mix) {  // ALL . ALL
             r = a;
             r.v = a.v + b.v;
-            r.flag = b.flag;
             return r;
         }
-        // ALL . MIX: a's run prefixes b's leading run
-        uint64_t x = a.v + b.r0;
+        // ALL . MIX: a's 121s extend b's leading run
+        const uint64_t x = a.v + b.r0;
         r.mix = true;
-        r.flag = true;
         r.r0 = (uint32_t)(x % kMaxRun);
         r.v = b.v + x / kMaxRun;
         r.tr = b.tr;
         return r;
     }
+    r = a;
     if (!b.mix) {  // MIX . ALL
-        uint64_t x = a.tr + b.v;
-        r = a;
-        r.v = a.v + x / kMaxRun + ((b.flag && (x % kMaxRun) != 0) ? 1 : 0);
+        const uint64_t x = a.tr + b.v;
+        r.v = a.v + x / kMaxRun;
         r.tr = (uint32_t)(x % kMaxRun);
         return r;
     }
-    // MIX . MIX
-    r = a;
-    r.v = a.v + b.v + (b.flag ? (a.tr + b.r0 + kMaxRun - 1) / kMaxRun : 0);
+    // MIX . MIX: b's first non-121 byte flushes the run carried out of a
+    r.v = a.v + b.v + (a.tr + b.r0 + kMaxRun - 1) / kMaxRun;
     r.tr = b.tr;
     return r;
 }
@@ -152,12 +147,67 @@ __host__ __device__ __forceinline__ RunSum compose(const RunSum &a, const RunSum
 __host__ __device__ __forceinline__ void run_eval(const RunSum &s, uint32_t c, uint64_t &count,
                                                   uint32_t &carry) {
     if (!s.mix) {
-        uint64_t x = c + s.v;
-        count = x / kMaxRun + ((s.flag && (x % kMaxRun) != 0) ? 1 : 0);
+        const uint64_t x = c + s.v;
+        count = x / kMaxRun;
         carry = (uint32_t)(x % kMaxRun);
     } else {
-        count = s.v + (s.flag ? (c + s.r0 + kMaxRun - 1) / kMaxRun : 0);
+        count = s.v + (c + s.r0 + kMaxRun - 1) / kMaxRun;
         carry = s.tr;
+    }
+}
+
+// ZRE byte for a pending chunk of c (1..14) zero groups (R12)
+__host__ __device__ __forceinline__ uint8_t run_code(uint32_t c) {
+    return c == 1 ? kZeroGroup : (uint8_t)(kFirstRunCode + (c - 2));
+}
+
+// Run summary of the bytes [0, len) of one segment (len <= N).
+template <int N>
+__host__ __device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[N], int len) {
+    RunSum s = run_identity();
+    if (len <= 0) return s;
+    int lead = 0;
+    while (lead < len && b[lead] == kZeroGroup) lead++;
+    if (lead == len) {
+        s.v = (uint64_t)len;
+        return s;
+    }
+    uint64_t cnt = 0;
+    uint32_t c = 0;   // pending 121s after the first non-121 byte
+#pragma unroll
+    for (int m = 0; m < N; m++) {
+        if (m < lead || m >= len) continue;
+        if (b[m] != kZeroGroup) {
+            cnt += (c > 0) + 1;
+            c = 0;
+        } else if (++c == kMaxRun) {
+            cnt++;
+            c = 0;
+        }
+    }
+    s.mix = true;
+    s.r0 = (uint32_t)(lead % kMaxRun);
+    s.v = cnt + lead / kMaxRun;
+    s.tr = c;
+    return s;
+}
+
+// Emit the ZRE bytes of one segment entered with carry c at payload offset
+// `off`; on return c is the carry out and off the next offset.
+template <int N>
+__host__ __device__ __forceinline__ void segment_emit(const uint8_t (&b)[N], int len, uint32_t &c,
+                                                      uint8_t *payload, uint64_t &off) {
+#pragma unroll
+    for (int m = 0; m < N; m++) {
+        if (m >= len) break;
+        if (b[m] != kZeroGroup) {
+            if (c > 0) payload[off++] = run_code(c);
+            payload[off++] = b[m];
+            c = 0;
+        } else if (++c == kMaxRun) {
+            payload[off++] = run_code(kMaxRun);
+            c = 0;
+        }
     }
 }
 

@@ -1,0 +1,65 @@
+"""CPU test of the GPU zero-run encoder's scan algebra (no GPU needed).
+
+tests/native/zre_scan_host.cu compiles the __host__ __device__ building blocks of
+csrc/tlc_device.cuh as host code and drives them through the K2 decomposition
+(thread segments, warp scans, tile look-back with random aggregate/prefix
+states).  Its output must equal the oracle's zero-run encoding byte for byte."""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "native", "zre_scan_host.cu")
+LIB = os.path.join(ROOT, "tests", "native", "libzre_scan_host.so")
+DEPS = [SRC, os.path.join(ROOT, "paper_1802_07389_b200", "csrc", "tlc_device.cuh")]
+
+
+@pytest.fixture(scope="module")
+def sim():
+    if not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS):
+        subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-O2", "-x", "cu",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", LIB, SRC])
+    L = ctypes.CDLL(LIB)
+    L.zre_scan_sim.restype = ctypes.c_uint64
+    L.zre_scan_sim.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p]
+
+    def run(B, threads, seed=0):
+        B = np.ascontiguousarray(B, dtype=np.uint8)
+        out = np.zeros(B.size + 16, dtype=np.uint8)
+        z = L.zre_scan_sim(B.ctypes.data, B.size, threads, seed, out.ctypes.data)
+        assert z != 2 ** 64 - 1, "tile-aggregate length disagrees with emitted bytes"
+        return out[:z]
+
+    return run
+
+
+def _streams():
+    g = synth.rng(71)
+    yield np.full(1, 121, np.uint8)
+    yield np.array([5], np.uint8)
+    for L in (13, 14, 15, 27, 28, 29, 200, 4096, 4097):
+        yield np.full(L, 121, np.uint8)
+    for p in (0.5, 0.9, 0.97, 0.995):
+        for L in (1, 7, 8, 9, 100, 2047, 2048, 2049, 20000):
+            yield np.where(g.random(L) < p, 121, g.integers(0, 243, L)).astype(np.uint8)
+    # run lengths 1..100 and 14k-1/14k/14k+1 separated by literals
+    menu = list(range(1, 101)) + [14 * k + d for k in range(1, 30) for d in (-1, 0, 1)]
+    parts = []
+    for r in menu:
+        parts += [121] * r + [int(g.integers(0, 121))]
+    yield np.array(parts, np.uint8)
+
+
+@pytest.mark.parametrize("threads", [1, 2, 3, 5, 32, 33, 256])
+def test_scan_matches_oracle_zre(sim, threads):
+    for i, B in enumerate(_streams()):
+        ref = O.zre_encode(B)
+        for seed in (0, 1):
+            got = sim(B, threads, seed + 10 * i)
+            assert got.tolist() == ref.tolist(), (threads, i, B.size)
