@@ -248,6 +248,10 @@ int tlc_o_decompress(const uint8_t *payload, uint64_t len, int zre_flag, float M
 {
     if (n == 0)
         return O_ERR_ARG;
+    /* Eq. 1 makes M = max|T_in| * s a finite (R6) number >= +0: a negative,  */
+    /* -0, NaN or infinite M cannot come from the compressor (R21).           */
+    if (signbit(M) || !isfinite(M))
+        return O_ERR_FORMAT;
     uint64_t P = tlc_o_quartic_len(n);
     uint8_t *B = (uint8_t *)malloc(P);
     int st;

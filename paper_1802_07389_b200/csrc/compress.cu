@@ -3,12 +3,15 @@
 //  K1 tlc_absmax_kernel  (row a1): u = err + t (not stored); grid max of
 //     bits(u) & 0x7fffffff as uint32, which orders |u| and flags NaN/Inf in one
 //     integer max; last CTA turns it into M = fl(a*s) and the header.
-//  K2 tlc_quant_qe_zre_kernel (rows a2-a4): per tile of kTile quartic bytes,
-//     recompute u, quantize (Eq. 2), write err = u - M*q (steps a,b), fold the
-//     five strided trits into quartic bytes (step 3) in shared memory, then
-//     zero-run encode the tile (step 4) as a scan with decoupled look-back over
-//     the run-carry monoid of tlc_device.cuh and write the payload bytes at
-//     their final offsets.  Dynamic tile ids keep the look-back deadlock-free.
+//  K2 tlc_quant_qe_kernel (rows a2-a3): a pure streaming pass -- recompute u,
+//     quantize (Eq. 2), write err = u - M*q (steps a,b) and fold the five
+//     strided trits of each quartic position into its byte (step 3), written
+//     to the payload (no ZRE) or to a P-byte scratch in the workspace.
+//  K3 tlc_zre_kernel (row a4): zero-run encoding (step 4) of the quartic bytes
+//     as one scan over the run-carry monoid of tlc_device.cuh with decoupled
+//     look-back across tiles (dynamic tile ids keep it deadlock-free); each
+//     thread emits its payload bytes at their final offsets and the last tile
+//     writes hdr->payload_len.
 //
 // Paper: P:372-410 (Sec. 3.1), P:495-510 (Sec. 3.2), P:538-548 (Sec. 3.3).
 #include "tlc_device.cuh"
@@ -25,7 +28,7 @@ __device__ __forceinline__ unsigned int absmax_key(float t, float e) {
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(kK1Threads)
+__global__ void __launch_bounds__(kK1Threads, 1)
 tlc_absmax_kernel(const float *__restrict__ t, const float *__restrict__ err, uint64_t n,
                   float s, int use_zre, unsigned int *__restrict__ partial, Ctrl *ctrl,
                   tlc_header *hdr) {
@@ -120,331 +123,290 @@ tlc_absmax_kernel(const float *__restrict__ t, const float *__restrict__ err, ui
 
 // ============================================================== K2
 constexpr int kK2Threads = 256;
-constexpr int kK2BytesPerThread = 8;
-constexpr int kTile = kK2Threads * kK2BytesPerThread;    // 2048 quartic bytes per tile
-constexpr int kK2Warps = kK2Threads / 32;
 
-struct K2Smem {
-    alignas(16) uint8_t B[kTile];        // quartic bytes of the tile
-    unsigned long long warp_incl[kK2Warps];
-    unsigned long long tile_excl;
-    unsigned int tile;
-};
-
-// One quartic byte from the five strided elements e_i = i*P + j.
-// Loads are issued by the caller; this folds digits d_i = q_i + 1 (pad -> 0).
-__device__ __forceinline__ uint32_t fold_byte(const float (&tv)[5], const float (&ev)[5],
-                                              const bool (&ok)[5], const Quant &Q,
-                                              float (&rv)[5]) {
-    uint32_t b = 0;
-#pragma unroll
-    for (int i = 0; i < 5; i++) {
-        float u = __fadd_rn(ev[i], tv[i]);
-        int q = Q.q(u);
-        rv[i] = Q.residual(u, q);
-        uint32_t d = ok[i] ? (uint32_t)(q + 1) : 0u;   // step 4: pad digit 0 (R10)
-        b = b * 3u + d;                                 // step 6: p0*81+...+p4
-    }
-    return b;
-}
-
-// ---- phase A, scalar path: thread handles j = j0 + k*256 + tid, k = 0..7
-template <bool kWritePayload>
-__device__ __forceinline__ void k2_phase_a_scalar(const float *__restrict__ t, float *__restrict__ err,
-                                                  uint64_t n, uint64_t P, uint64_t j0, int tile_len,
-                                                  const Quant &Q, uint8_t *sB,
-                                                  uint8_t *__restrict__ payload) {
-    constexpr int KU = 4;
-#pragma unroll
-    for (int kb = 0; kb < kK2BytesPerThread; kb += KU) {
-        float tv[KU][5], ev[KU][5];
-        bool ok[KU][5];
-#pragma unroll
-        for (int kk = 0; kk < KU; kk++) {
-            const int jl = (kb + kk) * kK2Threads + threadIdx.x;
-            const uint64_t j = j0 + jl;
-#pragma unroll
-            for (int i = 0; i < 5; i++) {
-                const uint64_t e = (uint64_t)i * P + j;
-                ok[kk][i] = (jl < tile_len) && (e < n);
-                tv[kk][i] = ok[kk][i] ? ld_stream(t + e) : 0.0f;
-                ev[kk][i] = ok[kk][i] ? __ldcs(err + e) : 0.0f;
-            }
-        }
-#pragma unroll
-        for (int kk = 0; kk < KU; kk++) {
-            const int jl = (kb + kk) * kK2Threads + threadIdx.x;
-            const uint64_t j = j0 + jl;
-            float rv[5];
-            uint32_t b = fold_byte(tv[kk], ev[kk], ok[kk], Q, rv);
-#pragma unroll
-            for (int i = 0; i < 5; i++)
-                if (ok[kk][i]) __stcs(err + (uint64_t)i * P + j, rv[i]);
-            if (jl < tile_len) {
-                if (kWritePayload) payload[j] = (uint8_t)b;
-                else sB[jl] = (uint8_t)b;
-            }
-        }
-    }
-}
-
-// ---- phase A, vector path (P % 4 == 0, 16-byte aligned t/err): thread handles
-// 4 consecutive j at j0 + 4*tid + 1024*g, g = 0..1, one float4 per partition.
-template <bool kWritePayload>
-__device__ __forceinline__ void k2_phase_a_vec(const float *__restrict__ t, float *__restrict__ err,
-                                               uint64_t n, uint64_t P, uint64_t j0, int tile_len,
-                                               const Quant &Q, uint8_t *sB,
-                                               uint8_t *__restrict__ payload) {
-    constexpr int G = kK2BytesPerThread / 4;   // 2 groups of 4 bytes
-    float4 tv[G][5], ev[G][5];
-    bool full[G][5];
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        const int jl = 4 * threadIdx.x + g * 4 * kK2Threads;
-        const uint64_t j = j0 + jl;
+// ---- vector path (P % 4 == 0, 16-byte aligned t/err/bytes): one thread per
+// group of 4 consecutive quartic positions j..j+3, one float4 per partition.
+__global__ void __launch_bounds__(kK2Threads, 3)
+tlc_quant_qe_vec_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
+                        uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
+    if (ctrl->status != TLC_OK) return;           // K1 raised NONFINITE / RANGE: err untouched
+    const Quant Q(ctrl->M);
+    const uint64_t P = (n + 4) / 5;
+    const uint64_t groups = P / 4;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = 4 * g;
+        float4 tv[5], ev[5];
+        bool full[5];
 #pragma unroll
         for (int i = 0; i < 5; i++) {
             const uint64_t e = (uint64_t)i * P + j;
-            full[g][i] = (jl + 3 < tile_len) && (e + 3 < n);
-            if (full[g][i]) {
-                tv[g][i] = ld_stream4(reinterpret_cast<const float4 *>(t + e));
-                ev[g][i] = __ldcs(reinterpret_cast<const float4 *>(err + e));
+            full[i] = e + 3 < n;                        // only the tail of partition 4 can fail
+            if (full[i]) {
+                tv[i] = ld_stream4(reinterpret_cast<const float4 *>(t + e));
+                ev[i] = __ldcs(reinterpret_cast<const float4 *>(err + e));
             } else {
                 float a[4], b[4];
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
-                    bool ok = (jl + c < tile_len) && (e + c < n);
-                    a[c] = ok ? ld_stream(t + e + c) : 0.0f;
-                    b[c] = ok ? __ldcs(err + e + c) : 0.0f;
+                    a[c] = e + c < n ? ld_stream(t + e + c) : 0.0f;
+                    b[c] = e + c < n ? __ldcs(err + e + c) : 0.0f;
                 }
-                tv[g][i] = make_float4(a[0], a[1], a[2], a[3]);
-                ev[g][i] = make_float4(b[0], b[1], b[2], b[3]);
+                tv[i] = make_float4(a[0], a[1], a[2], a[3]);
+                ev[i] = make_float4(b[0], b[1], b[2], b[3]);
             }
         }
-    }
-#pragma unroll
-    for (int g = 0; g < G; g++) {
-        const int jl = 4 * threadIdx.x + g * 4 * kK2Threads;
-        const uint64_t j = j0 + jl;
-        uint32_t bytes[4] = {0, 0, 0, 0};
+        uint32_t by[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int i = 0; i < 5; i++) {
             const uint64_t e = (uint64_t)i * P + j;
-            const float tt[4] = {tv[g][i].x, tv[g][i].y, tv[g][i].z, tv[g][i].w};
-            const float ee[4] = {ev[g][i].x, ev[g][i].y, ev[g][i].z, ev[g][i].w};
+            const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
+            const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
             float r[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                const bool ok = full[g][i] || ((jl + c < tile_len) && (e + c < n));
-                float u = __fadd_rn(ee[c], tt[c]);
-                int q = Q.q(u);
-                r[c] = Q.residual(u, q);
-                bytes[c] = bytes[c] * 3u + (ok ? (uint32_t)(q + 1) : 0u);
+                const float u = __fadd_rn(ee[c], tt[c]);        // step (1)
+                const int q = Q.q(u);                            // Eq. 2
+                r[c] = Q.residual(u, q);                         // steps (a),(b)
+                const bool ok = full[i] || (e + c < n);
+                by[c] = by[c] * 3u + (ok ? (uint32_t)(q + 1) : 0u);   // steps 1,4,6 (pad digit 0)
             }
-            if (full[g][i]) {
+            if (full[i]) {
                 __stcs(reinterpret_cast<float4 *>(err + e), make_float4(r[0], r[1], r[2], r[3]));
             } else {
 #pragma unroll
                 for (int c = 0; c < 4; c++)
-                    if ((jl + c < tile_len) && (e + c < n)) __stcs(err + e + c, r[c]);
+                    if (e + c < n) __stcs(err + e + c, r[c]);
             }
         }
-        if (jl + 3 < tile_len) {
-            uint32_t w = bytes[0] | (bytes[1] << 8) | (bytes[2] << 16) | (bytes[3] << 24);
-            if (kWritePayload) {
-                // payload + j is 4-aligned when the payload base is (checked on host)
-                *reinterpret_cast<uint32_t *>(payload + j) = w;
-            } else {
-                *reinterpret_cast<uint32_t *>(sB + jl) = w;
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < 4; c++)
-                if (jl + c < tile_len) {
-                    if (kWritePayload) payload[j + c] = (uint8_t)bytes[c];
-                    else sB[jl + c] = (uint8_t)bytes[c];
-                }
-        }
+        *reinterpret_cast<uint32_t *>(bytes + j) = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
     }
 }
 
-template <bool kVec, bool kZre>
+// ---- scalar path (any alignment, any P): one thread per quartic position j.
 __global__ void __launch_bounds__(kK2Threads)
-tlc_quant_qe_zre_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
-                        uint8_t *__restrict__ payload, Ctrl *ctrl, unsigned long long *states,
-                        tlc_header *hdr) {
-    __shared__ K2Smem sm;
-    if (ctrl->status != TLC_OK) return;           // K1 raised NONFINITE / RANGE: err untouched
+tlc_quant_qe_scalar_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
+                           uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
+    if (ctrl->status != TLC_OK) return;
     const Quant Q(ctrl->M);
     const uint64_t P = (n + 4) / 5;
-    const uint64_t num_tiles = (P + kTile - 1) / kTile;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        float tv[5], ev[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + j;
+            tv[i] = e < n ? ld_stream(t + e) : 0.0f;
+            ev[i] = e < n ? __ldcs(err + e) : 0.0f;
+        }
+        uint32_t b = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + j;
+            const float u = __fadd_rn(ev[i], tv[i]);
+            const int q = Q.q(u);
+            if (e < n) __stcs(err + e, Q.residual(u, q));
+            b = b * 3u + (e < n ? (uint32_t)(q + 1) : 0u);
+        }
+        bytes[j] = (uint8_t)b;
+    }
+}
+
+// ============================================================== K3
+constexpr int kK3Threads = 256;
+constexpr int kK3BytesPerThread = 16;
+constexpr int kK3Tile = kK3Threads * kK3BytesPerThread;    // 4096 quartic bytes per tile
+constexpr int kK3Warps = kK3Threads / 32;
+
+__global__ void __launch_bounds__(kK3Threads)
+tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint8_t *__restrict__ payload,
+               Ctrl *ctrl, unsigned long long *states, tlc_header *hdr) {
+    __shared__ unsigned long long s_warp[kK3Warps];
+    __shared__ unsigned long long s_tile_excl;
+    __shared__ unsigned int s_tile;
+    if (ctrl->status != TLC_OK) return;
+    const uint64_t num_tiles = (P + kK3Tile - 1) / kK3Tile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     while (true) {
-        if (threadIdx.x == 0) sm.tile = atomicAdd(&ctrl->tile_counter, 1u);
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->tile_counter, 1u);
         __syncthreads();
-        const uint64_t tile = sm.tile;
+        const uint64_t tile = s_tile;
         if (tile >= num_tiles) break;
-        const uint64_t j0 = tile * kTile;
-        const int tile_len = (int)tmin<uint64_t>(kTile, P - j0);
+        const uint64_t j0 = tile * kK3Tile;
+        const int tile_len = (int)tmin<uint64_t>(kK3Tile, P - j0);
+        const int sbeg = threadIdx.x * kK3BytesPerThread;
+        const int slen = max(0, min(kK3BytesPerThread, tile_len - sbeg));
 
-        // ---------------- phase A: quantize, residual, quartic bytes
-        if (kVec) k2_phase_a_vec<!kZre>(t, err, n, P, j0, tile_len, Q, sm.B, payload);
-        else k2_phase_a_scalar<!kZre>(t, err, n, P, j0, tile_len, Q, sm.B, payload);
-
-        if (kZre) {
-            __syncthreads();
-
-            // ---------------- phase B: per-thread run summaries, block scan
-            const int sbeg = threadIdx.x * kK2BytesPerThread;
-            const int slen = max(0, min(kK2BytesPerThread, tile_len - sbeg));
-            uint8_t b[kK2BytesPerThread];
-            {
-                uint2 w = *reinterpret_cast<const uint2 *>(sm.B + sbeg);
+        uint8_t b[kK3BytesPerThread];
+        if (slen == kK3BytesPerThread) {
+            const uint4 w = __ldcs(reinterpret_cast<const uint4 *>(bytes + j0 + sbeg));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                for (int m = 0; m < 4; m++) b[m] = (w.x >> (8 * m)) & 0xff;
+            for (int k = 0; k < 16; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
+        } else {
 #pragma unroll
-                for (int m = 0; m < 4; m++) b[4 + m] = (w.y >> (8 * m)) & 0xff;
+            for (int k = 0; k < 16; k++) b[k] = k < slen ? bytes[j0 + sbeg + k] : 0;
+        }
+        const RunSum mine = segment_summary(b, slen);
+
+        // block scan: warp inclusive scan, warp totals through shared memory
+        unsigned long long x = pack(mine);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = shfl_up64(x, d);
+            if (lane >= d) x = pack(compose(unpack(y), unpack(x)));
+        }
+        unsigned long long thread_excl = shfl_up64(x, 1);
+        if (lane == 0) thread_excl = pack(run_identity());
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+
+        if (warp == 0) {
+            // tile aggregate and exclusive warp prefixes (lanes 0..7 hold the warp totals)
+            unsigned long long wv = lane < kK3Warps ? s_warp[lane] : pack(run_identity());
+#pragma unroll
+            for (int d = 1; d < kK3Warps; d <<= 1) {
+                const unsigned long long y = shfl_up64(wv, d);
+                if (lane >= d) wv = pack(compose(unpack(y), unpack(wv)));
             }
-            const RunSum mine = segment_summary(b, slen);
+            const RunSum agg = unpack(__shfl_sync(0xffffffffu, wv, kK3Warps - 1));
+            unsigned long long wex = shfl_up64(wv, 1);
+            if (lane == 0) wex = pack(run_identity());
 
-            // warp inclusive scan
-            unsigned long long x = pack(mine);
+            // decoupled look-back over the preceding tiles, 32 at a time
+            RunSum excl = run_identity();
+            if (tile == 0) {
+                if (lane == 0) st_relaxed_u64(states, kStatusPrefix | pack(agg));
+            } else {
+                if (lane == 0) st_relaxed_u64(states + tile, kStatusAgg | pack(agg));
+                int64_t pred = (int64_t)tile - 1;
+                while (true) {
+                    const int64_t idx = pred - lane;
+                    const unsigned long long w =
+                        idx >= 0 ? ld_relaxed_u64(states + idx) : (kStatusPrefix | pack(run_identity()));
+                    const unsigned int st = (unsigned int)(w >> 62);
+                    const unsigned int pref = __ballot_sync(0xffffffffu, st == 2u);
+                    const unsigned int inval = __ballot_sync(0xffffffffu, st == 0u);
+                    const int first = pref ? (__ffs(pref) - 1) : 31;
+                    const unsigned int window = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
+                    if (inval & window) { __nanosleep(20); continue; }
+                    unsigned long long v = (lane <= first) ? (w & ~kStatusMask) : pack(run_identity());
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                unsigned long long y = shfl_up64(x, d);
-                if (lane >= d) x = pack(compose(unpack(y), unpack(x)));
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const unsigned long long o = shfl_down64(v, d);
+                        if (lane + d < 32) v = pack(compose(unpack(o), unpack(v)));
+                    }
+                    excl = compose(unpack(__shfl_sync(0xffffffffu, v, 0)), excl);
+                    if (pref) break;
+                    pred -= 32;
+                }
+                if (lane == 0) st_relaxed_u64(states + tile, kStatusPrefix | pack(compose(excl, agg)));
             }
-            unsigned long long thread_excl = shfl_up64(x, 1);
-            if (lane == 0) thread_excl = pack(run_identity());
-            if (lane == 31) sm.warp_incl[warp] = x;
-            __syncthreads();
-
-            // ---------------- tile aggregate + decoupled look-back (warp 0)
-            if (warp == 0) {
-                RunSum agg = run_identity();
-#pragma unroll
-                for (int w = 0; w < kK2Warps; w++) agg = compose(agg, unpack(sm.warp_incl[w]));
-                RunSum excl = run_identity();
-                if (tile == 0) {
-                    if (lane == 0) st_relaxed_u64(states + tile, kStatusPrefix | pack(agg));
-                } else {
-                    if (lane == 0) st_relaxed_u64(states + tile, kStatusAgg | pack(agg));
-                    int64_t pred = (int64_t)tile - 1;
-                    while (true) {
-                        const int64_t idx = pred - lane;
-                        unsigned long long w =
-                            idx >= 0 ? ld_relaxed_u64(states + idx) : (kStatusPrefix | pack(run_identity()));
-                        const unsigned int st = (unsigned int)(w >> 62);
-                        const unsigned int pref = __ballot_sync(0xffffffffu, st == 2u);
-                        const unsigned int inval = __ballot_sync(0xffffffffu, st == 0u);
-                        const int first = pref ? (__ffs(pref) - 1) : 31;
-                        const unsigned int window = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
-                        if (inval & window) { __nanosleep(32); continue; }
-                        unsigned long long v = (lane <= first) ? (w & ~kStatusMask) : pack(run_identity());
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            unsigned long long o = shfl_down64(v, d);
-                            if (lane + d < 32) v = pack(compose(unpack(o), unpack(v)));
-                        }
-                        v = __shfl_sync(0xffffffffu, v, 0);
-                        excl = compose(unpack(v), excl);
-                        if (pref) break;
-                        pred -= 32;
-                    }
-                    if (lane == 0) st_relaxed_u64(states + tile, kStatusPrefix | pack(compose(excl, agg)));
+            if (lane < kK3Warps) s_warp[lane] = pack(compose(excl, unpack(wex)));
+            if (lane == 0) {
+                s_tile_excl = pack(excl);
+                if (tile == num_tiles - 1) {
+                    uint64_t total;
+                    uint32_t carry;
+                    run_eval(compose(excl, agg), 0, total, carry);
+                    hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
                 }
-                if (lane == 0) {
-                    sm.tile_excl = pack(excl);
-                    if (tile == num_tiles - 1) {
-                        uint64_t total;
-                        uint32_t carry;
-                        run_eval(compose(excl, agg), 0, total, carry);
-                        hdr->payload_len = total + (carry > 0);   // end of stream flushes
-                    }
-                }
-                // warp exclusive prefixes for the block: reuse warp_incl as exclusive
-                __syncwarp();
-                if (lane == 0) {
-                    RunSum acc = run_identity();
-                    for (int w = 0; w < kK2Warps; w++) {
-                        RunSum nx = compose(acc, unpack(sm.warp_incl[w]));
-                        sm.warp_incl[w] = pack(acc);
-                        acc = nx;
-                    }
-                }
-            }
-            __syncthreads();
-
-            // ---------------- emission at final payload offsets
-            if (slen > 0) {
-                RunSum before = compose(unpack(sm.tile_excl),
-                                        compose(unpack(sm.warp_incl[warp]), unpack(thread_excl)));
-                uint64_t off;
-                uint32_t c;
-                run_eval(before, 0, off, c);
-                segment_emit(b, slen, c, payload, off);
-                // the thread holding the last byte of the stream flushes the pending run
-                if (c > 0 && j0 + sbeg + slen == P) payload[off] = run_code(c);
             }
         }
-        __syncthreads();   // sm.B / sm.tile reuse
+        __syncthreads();
+
+        // emission at the final payload offsets
+        if (slen > 0) {
+            const RunSum before = compose(unpack(s_warp[warp]), unpack(thread_excl));
+            uint64_t off;
+            uint32_t c;
+            run_eval(before, 0, off, c);
+            segment_emit(b, slen, c, payload, off);
+            if (c > 0 && j0 + sbeg + slen == P) payload[off] = run_code(c);
+        }
+        __syncthreads();   // s_warp / s_tile reuse
     }
 }
 
 // ============================================================== host launchers
-static int g_k2_blocks_vec = 0, g_k2_blocks_sc = 0;
+struct CompressWs {
+    Ctrl *ctrl;
+    unsigned long long *states;
+    unsigned int *partial;
+    uint8_t *bytes;
+    size_t memset_bytes;
+};
 
-int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
-                    tlc_header *hdr, void *ws, cudaStream_t st) {
+static CompressWs carve_compress_ws(void *ws, uint64_t n) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t num_tiles = (P + kTile - 1) / kTile;
-    Ctrl *ctrl = reinterpret_cast<Ctrl *>(ws);
-    unsigned long long *states = reinterpret_cast<unsigned long long *>((char *)ws + sizeof(Ctrl));
-    unsigned int *partial = reinterpret_cast<unsigned int *>(
-        (char *)ws + sizeof(Ctrl) + align256(num_tiles * sizeof(unsigned long long)));
-
-    const int sms = num_sms();
-    if (cudaMemsetAsync(ws, 0, sizeof(Ctrl) + num_tiles * sizeof(unsigned long long), st) != cudaSuccess)
-        return TLC_ERR_CUDA;
-
-    const bool vec1 = aligned16(t) && aligned16(err);
-    const uint64_t work1 = vec1 ? (n + 3) / 4 : n;
-    int grid1 = (int)tmin<uint64_t>((uint64_t)sms * kK1BlocksPerSm, tmax<uint64_t>(1, (work1 + kK1Threads * 4 - 1) / (kK1Threads * 4)));
-    {
-        KernelScope ks(kK1, st);
-        if (vec1) tlc_absmax_kernel<true><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, partial, ctrl, hdr);
-        else tlc_absmax_kernel<false><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, partial, ctrl, hdr);
-    }
-
-    const bool vec2 = (P % 4 == 0) && aligned16(t) && aligned16(err) && (use_zre || aligned4(payload));
-    int per_sm = 0;
-    if (vec2) {
-        if (!g_k2_blocks_vec)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks_vec, tlc_quant_qe_zre_kernel<true, true>, kK2Threads, 0);
-        per_sm = g_k2_blocks_vec;
-    } else {
-        if (!g_k2_blocks_sc)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks_sc, tlc_quant_qe_zre_kernel<false, true>, kK2Threads, 0);
-        per_sm = g_k2_blocks_sc;
-    }
-    int grid2 = (int)tmin<uint64_t>(num_tiles, (uint64_t)sms * max(1, per_sm));
-    KernelScope ks(kK2, st);
-    if (vec2) {
-        if (use_zre) tlc_quant_qe_zre_kernel<true, true><<<grid2, kK2Threads, 0, st>>>(t, err, n, payload, ctrl, states, hdr);
-        else tlc_quant_qe_zre_kernel<true, false><<<grid2, kK2Threads, 0, st>>>(t, err, n, payload, ctrl, states, hdr);
-    } else {
-        if (use_zre) tlc_quant_qe_zre_kernel<false, true><<<grid2, kK2Threads, 0, st>>>(t, err, n, payload, ctrl, states, hdr);
-        else tlc_quant_qe_zre_kernel<false, false><<<grid2, kK2Threads, 0, st>>>(t, err, n, payload, ctrl, states, hdr);
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+    const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
+    CompressWs w;
+    char *p = reinterpret_cast<char *>(ws);
+    w.ctrl = reinterpret_cast<Ctrl *>(p);
+    w.states = reinterpret_cast<unsigned long long *>(p + sizeof(Ctrl));
+    const size_t o1 = sizeof(Ctrl) + align256(tiles * sizeof(unsigned long long));
+    w.partial = reinterpret_cast<unsigned int *>(p + o1);
+    const size_t o2 = o1 + align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int));
+    w.bytes = reinterpret_cast<uint8_t *>(p + o2);
+    w.memset_bytes = sizeof(Ctrl) + tiles * sizeof(unsigned long long);
+    return w;
 }
 
 size_t compress_workspace_bytes(uint64_t n) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t num_tiles = (P + kTile - 1) / kTile;
-    return sizeof(Ctrl) + align256(num_tiles * sizeof(unsigned long long)) +
-           align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int));
+    const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
+    return sizeof(Ctrl) + align256(tiles * sizeof(unsigned long long)) +
+           align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int)) + align256(P);
+}
+
+static int g_k2_vec_blocks = 0, g_k2_sc_blocks = 0, g_k3_blocks = 0;
+
+int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
+                    tlc_header *hdr, void *ws, cudaStream_t st) {
+    const uint64_t P = (n + 4) / 5;
+    const CompressWs w = carve_compress_ws(ws, n);
+    const int sms = num_sms();
+    if (cudaMemsetAsync(ws, 0, w.memset_bytes, st) != cudaSuccess) return TLC_ERR_CUDA;
+
+    const bool vec1 = aligned16(t) && aligned16(err);
+    const uint64_t work1 = vec1 ? (n + 3) / 4 : n;
+    const int grid1 = (int)tmin<uint64_t>((uint64_t)sms * kK1BlocksPerSm,
+                                          tmax<uint64_t>(1, (work1 + kK1Threads * 4 - 1) / (kK1Threads * 4)));
+    {
+        KernelScope ks(kK1, st);
+        if (vec1) tlc_absmax_kernel<true><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, w.partial, w.ctrl, hdr);
+        else tlc_absmax_kernel<false><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, w.partial, w.ctrl, hdr);
+    }
+
+    uint8_t *bytes = use_zre ? w.bytes : payload;
+    const bool vec2 = (P % 4 == 0) && aligned16(t) && aligned16(err) && aligned4(bytes);
+    {
+        KernelScope ks(kK2, st);
+        if (vec2) {
+            if (!g_k2_vec_blocks)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_vec_blocks, tlc_quant_qe_vec_kernel, kK2Threads, 0);
+            const uint64_t groups = P / 4;
+            const int grid = (int)tmin<uint64_t>((groups + kK2Threads - 1) / kK2Threads,
+                                                 (uint64_t)sms * tmax(1, g_k2_vec_blocks));
+            tlc_quant_qe_vec_kernel<<<tmax(grid, 1), kK2Threads, 0, st>>>(t, err, n, bytes, w.ctrl);
+        } else {
+            if (!g_k2_sc_blocks)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_sc_blocks, tlc_quant_qe_scalar_kernel, kK2Threads, 0);
+            const int grid = (int)tmin<uint64_t>((P + kK2Threads - 1) / kK2Threads,
+                                                 (uint64_t)sms * tmax(1, g_k2_sc_blocks));
+            tlc_quant_qe_scalar_kernel<<<tmax(grid, 1), kK2Threads, 0, st>>>(t, err, n, bytes, w.ctrl);
+        }
+    }
+    if (use_zre) {
+        KernelScope ks(kK3, st);
+        if (!g_k3_blocks)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
+        const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
+        const int grid = (int)tmin<uint64_t>(tiles, (uint64_t)sms * tmax(1, g_k3_blocks));
+        tlc_zre_kernel<<<grid, kK3Threads, 0, st>>>(w.bytes, P, payload, w.ctrl, w.states, hdr);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
 }  // namespace tlc

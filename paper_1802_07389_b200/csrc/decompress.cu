@@ -43,7 +43,10 @@ tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64
     const unsigned int status = hdr->status;
     const uint64_t Z = hdr->payload_len;
     const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
-    const bool valid = status == TLC_OK && hdr->n == n && Z <= P && Z >= 1 && (zre || Z == P);
+    // M = max|u| * s is finite and >= +0 (Eq. 1, R6); anything else is malformed (R21)
+    const uint32_t Mb = __float_as_uint(hdr->M);
+    const bool valid = status == TLC_OK && hdr->n == n && Z <= P && Z >= 1 && (zre || Z == P) &&
+                       (Mb >> 31) == 0 && Mb < 0x7f800000u;
     if (!valid) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && status == TLC_OK) raise_format(hdr);
         return;
@@ -135,15 +138,16 @@ tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64
 // ============================================================== K5
 struct K5Smem {
     alignas(16) uint8_t E[kOutTile];     // expanded quartic bytes of the tile
-    uint16_t lut[256];                   // base-3 digits d0..d4, 2 bits each (d0 highest)
+    uint16_t lut[256];                   // per byte: bit i = (digit_i != 1), bit 8+i = (digit_i == 0)
     unsigned int warp_sum[kK5Threads / 32];
 };
 
-__device__ __forceinline__ float trit_value(float M, uint32_t d) {
-    // Eq. 3: M * q with q = d - 1 in {-1, 0, 1}; the same single fp32 multiply
-    // as T_out = M * T_quantized.
-    const float qf = d == 0 ? -1.0f : (d == 2 ? 1.0f : 0.0f);
-    return __fmul_rn(M, qf);
+// Eq. 3, T_out = M * q, for a valid header (M finite and >= +0, enforced by
+// K4): M*(+1) = M, M*(-1) = -M, M*0 = +0 -- built from M's bit pattern.
+__device__ __forceinline__ uint32_t trit_bits(uint32_t lutv, int i, uint32_t Mb) {
+    const uint32_t nz = (lutv >> i) & 1u;
+    const uint32_t neg = (lutv >> (8 + i)) & 1u;
+    return (0u - nz) & (Mb | (neg << 31));
 }
 
 template <bool kVec, int kMode>
@@ -153,58 +157,86 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
     __shared__ K5Smem sm;
     if (hdr->status != TLC_OK) return;
     const float M = hdr->M;
+    const uint32_t Mb = __float_as_uint(M);
     const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
     const uint64_t Z = hdr->payload_len;
     const uint64_t P = (n + 4) / 5;
     const uint64_t num_tiles = (P + kOutTile - 1) / kOutTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // digit table: step 1 of decoding, "dividing a by a power of 3 and taking
-    // the remainder", precomputed for the 243 byte values.
+    // digit table: decoding step 1, "dividing a by a power of 3 and taking the
+    // remainder", for the 243 byte values (partition 0 = a/81).
     for (int v = threadIdx.x; v < 256; v += kK5Threads) {
         uint32_t w = 0, r = v < 243 ? v : 121;
 #pragma unroll
-        for (int i = 0; i < 5; i++) { w |= (r % 3u) << (2 * i); r /= 3u; }
-        sm.lut[v] = (uint16_t)w;   // bits 2i..2i+1 = digit of partition 4-i
+        for (int i = 4; i >= 0; i--) {
+            const uint32_t d = r % 3u;
+            r /= 3u;
+            w |= (uint32_t)(d != 1) << i;
+            w |= (uint32_t)(d == 0) << (8 + i);
+        }
+        sm.lut[v] = (uint16_t)w;
     }
     bool bad = false;
 
     for (uint64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const uint64_t J0 = tile * kOutTile;
         const int tl = (int)tmin<uint64_t>(kOutTile, P - J0);
-        __syncthreads();   // previous tile's readers of sm.E are done (and lut is built)
+        __syncthreads();   // previous tile's readers of sm.E are done (and the table is built)
         if (zre) {
+            // pre-fill with 121: zero-run codes expand to 121s and need no further writes
+            *reinterpret_cast<uint2 *>(sm.E + 8 * threadIdx.x) = make_uint2(0x79797979u, 0x79797979u);
             const unsigned long long sk = seek[tile];
-            const uint64_t bi = sk >> 4;
-            const uint32_t skip = (uint32_t)(sk & 15);
-            // thread owns window bytes [8*tid, 8*tid+8) of payload[bi, bi + kK5Window)
-            const uint64_t zb = bi + (uint64_t)threadIdx.x * 8;
-            uint8_t b[8];
-            uint32_t len[8], sum = 0;
+            const uint64_t bi = sk >> 4;                      // payload byte covering J0
+            const uint32_t skip = (uint32_t)(sk & 15);        // J0 - (first position of that byte)
+            const uint64_t be = tile + 1 < num_tiles ? (seek[tile + 1] >> 4) : Z - 1;   // last byte needed
+            // thread owns window bytes [w0 + 8*tid, +8), w0 = bi rounded down to 4;
+            // the last thread also owns the 4 bytes after the 2048-byte window so
+            // that the <= 2048 bytes from bi on are always covered.
+            const uint64_t w0 = bi & ~3ull;
+            const uint64_t zb = w0 + 8ull * threadIdx.x;
+            const int nwords = threadIdx.x == kK5Threads - 1 ? 3 : 2;
+            uint32_t wd[3] = {0, 0, 0};
 #pragma unroll
-            for (int m = 0; m < 8; m++) {
-                b[m] = (zb + m < Z) ? payload[zb + m] : 0;
-                len[m] = (zb + m < Z) ? zre_len(b[m]) : 0u;
+            for (int h = 0; h < 3; h++) {
+                const uint64_t a = zb + 4 * h;
+                if (h >= nwords) break;
+                if (a + 3 <= be) {
+                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + a));
+                } else {
+                    uint32_t x = 0;
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if (a + c <= be) x |= (uint32_t)payload[a + c] << (8 * c);
+                    wd[h] = x;
+                }
+            }
+            uint32_t len[12], sum = 0;
+#pragma unroll
+            for (int m = 0; m < 12; m++) {
+                const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+                const uint64_t a = zb + m;
+                len[m] = (m < 4 * nwords && a >= bi && a <= be) ? zre_len(b) : 0u;
                 sum += len[m];
             }
             uint32_t x = sum;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                 if (lane >= d) x += y;
             }
             if (lane == 31) sm.warp_sum[warp] = x;
             __syncthreads();
             uint32_t wofs = 0;
-            for (int w = 0; w < warp; w++) wofs += sm.warp_sum[w];
-            // local position (relative to J0) of this thread's first byte
-            int64_t p = (int64_t)wofs + (x - sum) - (int64_t)skip;
 #pragma unroll
-            for (int m = 0; m < 8; m++) {
-                const int64_t lo = tmax<int64_t>(p, 0), hi = tmin<int64_t>(p + len[m], tl);
-                const uint8_t v = b[m] >= kFirstRunCode ? kZeroGroup : b[m];
-                for (int64_t q = lo; q < hi; q++) sm.E[q] = v;
-                p += len[m];
+            for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? sm.warp_sum[w] : 0u;
+            // position (relative to J0) of this thread's first byte
+            int p = (int)(wofs + x - sum) - (int)skip;
+#pragma unroll
+            for (int m = 0; m < 12; m++) {
+                const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+                if (len[m] == 1 && p >= 0 && p < tl) sm.E[p] = (uint8_t)b;   // literal byte
+                p += (int)len[m];
             }
         } else {
             for (int jl = threadIdx.x; jl < tl; jl += kK5Threads) {
@@ -218,43 +250,40 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
         // ---- base-3 decode + dequantize, 4 consecutive quartic bytes per thread
         for (int jl = 4 * threadIdx.x; jl < tl; jl += 4 * kK5Threads) {
             const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E + jl);
-            uint32_t dg[4];
+            uint32_t L[4];
 #pragma unroll
-            for (int c = 0; c < 4; c++) dg[c] = sm.lut[(w4 >> (8 * c)) & 0xff];
+            for (int c = 0; c < 4; c++) L[c] = sm.lut[(w4 >> (8 * c)) & 0xffu];
             const uint64_t j = J0 + jl;
 #pragma unroll
             for (int i = 0; i < 5; i++) {
-                const int sh = 2 * (4 - i);
-                uint32_t d[4];
-#pragma unroll
-                for (int c = 0; c < 4; c++) d[c] = (dg[c] >> sh) & 3u;
                 const uint64_t e = (uint64_t)i * P + j;
+                float *o = out + e;
                 const bool full = kVec && (jl + 3 < tl) && (e + 3 < n);
                 if (kMode == TLC_MODE_OVERWRITE) {
                     if (full) {
-                        __stcs(reinterpret_cast<float4 *>(out + e),
-                               make_float4(trit_value(M, d[0]), trit_value(M, d[1]),
-                                           trit_value(M, d[2]), trit_value(M, d[3])));
+                        __stcs(reinterpret_cast<uint4 *>(o),
+                               make_uint4(trit_bits(L[0], i, Mb), trit_bits(L[1], i, Mb),
+                                          trit_bits(L[2], i, Mb), trit_bits(L[3], i, Mb)));
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if (jl + c < tl && e + c < n) out[e + c] = trit_value(M, d[c]);
+                            if (jl + c < tl && e + c < n) o[c] = __uint_as_float(trit_bits(L[c], i, Mb));
                     }
                 } else {
-                    const bool any = (d[0] != 1) | (d[1] != 1) | (d[2] != 1) | (d[3] != 1);
-                    if (!any) continue;                       // skip-zero: sector untouched (R16)
+                    const uint32_t nz = ((L[0] | L[1] | L[2] | L[3]) >> i) & 1u;
+                    if (!nz) continue;                           // skip-zero: sector untouched (R16)
                     if (full) {
-                        float4 o = *reinterpret_cast<float4 *>(out + e);
-                        if (d[0] != 1) o.x = __fadd_rn(o.x, trit_value(M, d[0]));
-                        if (d[1] != 1) o.y = __fadd_rn(o.y, trit_value(M, d[1]));
-                        if (d[2] != 1) o.z = __fadd_rn(o.z, trit_value(M, d[2]));
-                        if (d[3] != 1) o.w = __fadd_rn(o.w, trit_value(M, d[3]));
-                        *reinterpret_cast<float4 *>(out + e) = o;
+                        float4 v = *reinterpret_cast<float4 *>(o);
+                        float *vv = reinterpret_cast<float *>(&v);
+#pragma unroll
+                        for (int c = 0; c < 4; c++)
+                            if ((L[c] >> i) & 1u) vv[c] = __fadd_rn(vv[c], __uint_as_float(trit_bits(L[c], i, Mb)));
+                        *reinterpret_cast<float4 *>(o) = v;
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if (jl + c < tl && e + c < n && d[c] != 1)
-                                out[e + c] = __fadd_rn(out[e + c], trit_value(M, d[c]));
+                            if (jl + c < tl && e + c < n && ((L[c] >> i) & 1u))
+                                o[c] = __fadd_rn(o[c], __uint_as_float(trit_bits(L[c], i, Mb)));
                     }
                 }
             }

@@ -14,9 +14,10 @@
 
 namespace tlc {
 
-static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe_zre", "k4_zre_scan",
-                                            "k5_expand_dequant", "k6_compress_batched",
-                                            "k7_decompress_batched", "k8_scale"};
+static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe", "k3_zre",
+                                            "k4_zre_scan", "k5_expand_dequant",
+                                            "k6_compress_batched", "k7_decompress_batched",
+                                            "k8_scale"};
 
 namespace {
 struct Rec {

@@ -167,7 +167,12 @@ __host__ __device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[N]
     RunSum s = run_identity();
     if (len <= 0) return s;
     int lead = 0;
-    while (lead < len && b[lead] == kZeroGroup) lead++;
+    bool in_lead = true;
+#pragma unroll
+    for (int m = 0; m < N; m++) {          // static indices keep b[] in registers
+        if (m < len && in_lead && b[m] == kZeroGroup) lead++;
+        else in_lead = false;
+    }
     if (lead == len) {
         s.v = (uint64_t)len;
         return s;

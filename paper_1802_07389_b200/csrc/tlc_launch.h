@@ -9,7 +9,7 @@
 namespace tlc {
 
 constexpr int kMaxSms = 256;          // workspace sizing bound (B200 has 148)
-constexpr int kK1BlocksPerSm = 4;     // K1 grid = SMs x 4 x 512 threads
+constexpr int kK1BlocksPerSm = 2;     // K1 grid = SMs x 2 x 512 threads (2 waves of 1 CTA/SM)
 
 template <class T> __host__ __device__ inline T tmin(T a, T b) { return a < b ? a : b; }
 template <class T> __host__ __device__ inline T tmax(T a, T b) { return a < b ? b : a; }
@@ -32,7 +32,7 @@ inline int num_sms() {
 }
 
 // Kernel ids for launch counting / profiling (prof.cu).
-enum KernelId { kK1 = 0, kK2 = 1, kK4 = 2, kK5 = 3, kK6 = 4, kK7 = 5, kK8 = 6, kNumKernelIds = 7 };
+enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7, kNumKernelIds = 8 };
 
 // RAII bracket around one kernel launch: counts it and, when profiling is on,
 // records CUDA events before and after it on `st`.

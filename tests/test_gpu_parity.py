@@ -235,6 +235,14 @@ def test_corrupt_payloads_raise_format(tlc):
     assert run(mutate_payload=lambda p: p.__setitem__(slice(0, 50), 255), mutate_hdr=set_len(51)) == T.TLC_ERR_FORMAT
     assert run(n_arg=n - 5) == T.TLC_ERR_FORMAT                      # hdr.n mismatch
 
+    def set_M(v):
+        def f(h):
+            h[0:4] = torch.tensor(list(struct.pack("<f", v)), dtype=torch.uint8)
+        return f
+
+    for bad_M in (-1.0, -0.0, float("nan"), float("inf")):                # R21
+        assert run(mutate_hdr=set_M(bad_M)) == T.TLC_ERR_FORMAT
+
     # no-ZRE stream with a literal > 242
     td2, ed2 = _dev(synth.gaussian(1000, 61)), _dev(np.zeros(1000, f32))
     p2, h2 = T.tlc_compress(td2, ed2, 1.0, False)

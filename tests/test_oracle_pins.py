@@ -383,3 +383,10 @@ def test_s_is_fp32():
     st, M, _ = O.scale(t, 1.9)
     assert struct.pack("<f", M) == struct.pack("<f", 1.9)
     assert float(M) == 1.89999997615814208984375
+
+
+def test_malformed_scale_is_format():
+    """R21: Eq. 1 gives a finite M >= +0; a header with M < 0, -0, NaN or Inf is malformed."""
+    for M in (-1.0, -0.0, float("nan"), float("inf")):
+        st, _ = O.decompress(np.array([175], np.uint8), True, f32(M), 5)
+        assert st == O.ERR_FORMAT
