@@ -213,119 +213,82 @@ tlc_quant_qe_scalar_kernel(const float *__restrict__ t, float *__restrict__ err,
 }
 
 // ============================================================== K3
-constexpr int kK3Threads = 256;
-constexpr int kK3BytesPerThread = 16;
-constexpr int kK3Tile = kK3Threads * kK3BytesPerThread;    // 4096 quartic bytes per tile
-constexpr int kK3Warps = kK3Threads / 32;
+// Chunked single-pass scan: the grid splits the P quartic bytes into one
+// contiguous chunk per CTA (chunk ids taken in order from an atomic counter).
+//   phase 1  each CTA folds its chunk into one run summary and publishes it;
+//   phase 2  it composes the summaries of all preceding chunks (they never
+//            wait on later chunks, so this cannot deadlock) -> its carry-in;
+//   phase 3  it re-reads its chunk (L2-resident: P <= 0.2 n bytes) and emits
+//            every ZRE byte at its final offset.
+// The dependency depth between chunks is one publication, not a chain.
+constexpr int kK3Threads = kScanThreads;
+constexpr int kK3Seg = 16;                                  // bytes per thread per row
+constexpr int kK3Row = kK3Threads * kK3Seg;                 // 4096 quartic bytes per row
+
+__device__ __forceinline__ int load_seg16(const uint8_t *__restrict__ bytes, uint64_t pos, uint64_t hi,
+                                          uint8_t (&b)[kK3Seg]) {
+    const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
+    if (len == kK3Seg && (reinterpret_cast<uintptr_t>(bytes + pos) & 15u) == 0) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(bytes + pos);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < kK3Seg; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kK3Seg; k++) b[k] = k < len ? bytes[pos + k] : 0;
+    }
+    return len;
+}
 
 __global__ void __launch_bounds__(kK3Threads)
-tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint8_t *__restrict__ payload,
-               Ctrl *ctrl, unsigned long long *states, tlc_header *hdr) {
-    __shared__ unsigned long long s_warp[kK3Warps];
-    __shared__ unsigned long long s_tile_excl;
-    __shared__ unsigned int s_tile;
+tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
+               uint8_t *__restrict__ payload, Ctrl *ctrl, unsigned long long *states, tlc_header *hdr) {
+    __shared__ unsigned long long s_warp[kScanWarps];
+    __shared__ unsigned int s_id;
     if (ctrl->status != TLC_OK) return;
-    const uint64_t num_tiles = (P + kK3Tile - 1) / kK3Tile;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t nchunks = (P + chunk - 1) / chunk;
+    if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->tile_counter, 1u);
+    __syncthreads();
+    const uint64_t b = s_id;
+    if (b >= nchunks) return;
+    const uint64_t lo = b * chunk, hi = tmin<uint64_t>(P, lo + chunk);
+    uint8_t seg[kK3Seg];
 
-    while (true) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->tile_counter, 1u);
-        __syncthreads();
-        const uint64_t tile = s_tile;
-        if (tile >= num_tiles) break;
-        const uint64_t j0 = tile * kK3Tile;
-        const int tile_len = (int)tmin<uint64_t>(kK3Tile, P - j0);
-        const int sbeg = threadIdx.x * kK3BytesPerThread;
-        const int slen = max(0, min(kK3BytesPerThread, tile_len - sbeg));
+    // ---- phase 1: run summary of the chunk
+    RunSum agg = run_identity();
+    for (uint64_t row = lo; row < hi; row += kK3Row) {
+        const int len = load_seg16(bytes, row + (uint64_t)kK3Seg * threadIdx.x, hi, seg);
+        agg = compose(agg, block_reduce_runs(segment_summary(seg, len), s_warp));
+    }
+    if (threadIdx.x == 0) st_relaxed_u64(states + b, kReady | pack(agg));
 
-        uint8_t b[kK3BytesPerThread];
-        if (slen == kK3BytesPerThread) {
-            const uint4 w = __ldcs(reinterpret_cast<const uint4 *>(bytes + j0 + sbeg));
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int k = 0; k < 16; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; k++) b[k] = k < slen ? bytes[j0 + sbeg + k] : 0;
-        }
-        const RunSum mine = segment_summary(b, slen);
+    // ---- phase 2: carry-in = composition of all preceding chunk summaries
+    RunSum part = run_identity();
+    const uint64_t per = (b + kK3Threads - 1) / kK3Threads;
+    const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(b, i0 + per);
+    for (uint64_t i = i0; i < i1; i++) part = compose(part, unpack(wait_ready(states + i) & ~kReady));
+    RunSum run = block_reduce_runs(part, s_warp);
+    if (b == nchunks - 1 && threadIdx.x == 0) {
+        uint64_t total;
+        uint32_t carry;
+        run_eval(compose(run, agg), 0, total, carry);
+        hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
+    }
 
-        // block scan: warp inclusive scan, warp totals through shared memory
-        unsigned long long x = pack(mine);
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long y = shfl_up64(x, d);
-            if (lane >= d) x = pack(compose(unpack(y), unpack(x)));
-        }
-        unsigned long long thread_excl = shfl_up64(x, 1);
-        if (lane == 0) thread_excl = pack(run_identity());
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-
-        if (warp == 0) {
-            // tile aggregate and exclusive warp prefixes (lanes 0..7 hold the warp totals)
-            unsigned long long wv = lane < kK3Warps ? s_warp[lane] : pack(run_identity());
-#pragma unroll
-            for (int d = 1; d < kK3Warps; d <<= 1) {
-                const unsigned long long y = shfl_up64(wv, d);
-                if (lane >= d) wv = pack(compose(unpack(y), unpack(wv)));
-            }
-            const RunSum agg = unpack(__shfl_sync(0xffffffffu, wv, kK3Warps - 1));
-            unsigned long long wex = shfl_up64(wv, 1);
-            if (lane == 0) wex = pack(run_identity());
-
-            // decoupled look-back over the preceding tiles, 32 at a time
-            RunSum excl = run_identity();
-            if (tile == 0) {
-                if (lane == 0) st_relaxed_u64(states, kStatusPrefix | pack(agg));
-            } else {
-                if (lane == 0) st_relaxed_u64(states + tile, kStatusAgg | pack(agg));
-                int64_t pred = (int64_t)tile - 1;
-                while (true) {
-                    const int64_t idx = pred - lane;
-                    const unsigned long long w =
-                        idx >= 0 ? ld_relaxed_u64(states + idx) : (kStatusPrefix | pack(run_identity()));
-                    const unsigned int st = (unsigned int)(w >> 62);
-                    const unsigned int pref = __ballot_sync(0xffffffffu, st == 2u);
-                    const unsigned int inval = __ballot_sync(0xffffffffu, st == 0u);
-                    const int first = pref ? (__ffs(pref) - 1) : 31;
-                    const unsigned int window = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
-                    if (inval & window) { __nanosleep(20); continue; }
-                    unsigned long long v = (lane <= first) ? (w & ~kStatusMask) : pack(run_identity());
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const unsigned long long o = shfl_down64(v, d);
-                        if (lane + d < 32) v = pack(compose(unpack(o), unpack(v)));
-                    }
-                    excl = compose(unpack(__shfl_sync(0xffffffffu, v, 0)), excl);
-                    if (pref) break;
-                    pred -= 32;
-                }
-                if (lane == 0) st_relaxed_u64(states + tile, kStatusPrefix | pack(compose(excl, agg)));
-            }
-            if (lane < kK3Warps) s_warp[lane] = pack(compose(excl, unpack(wex)));
-            if (lane == 0) {
-                s_tile_excl = pack(excl);
-                if (tile == num_tiles - 1) {
-                    uint64_t total;
-                    uint32_t carry;
-                    run_eval(compose(excl, agg), 0, total, carry);
-                    hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
-                }
-            }
-        }
-        __syncthreads();
-
-        // emission at the final payload offsets
-        if (slen > 0) {
-            const RunSum before = compose(unpack(s_warp[warp]), unpack(thread_excl));
+    // ---- phase 3: emission at the final payload offsets
+    for (uint64_t row = lo; row < hi; row += kK3Row) {
+        const uint64_t pos = row + (uint64_t)kK3Seg * threadIdx.x;
+        const int len = load_seg16(bytes, pos, hi, seg);
+        RunSum row_total;
+        const RunSum ex = block_excl_scan_runs(segment_summary(seg, len), s_warp, row_total);
+        if (len > 0) {
             uint64_t off;
             uint32_t c;
-            run_eval(before, 0, off, c);
-            segment_emit(b, slen, c, payload, off);
-            if (c > 0 && j0 + sbeg + slen == P) payload[off] = run_code(c);
+            run_eval(compose(run, ex), 0, off, c);
+            segment_emit(seg, len, c, payload, off);
+            if (c > 0 && pos + len == P) payload[off] = run_code(c);
         }
-        __syncthreads();   // s_warp / s_tile reuse
+        run = compose(run, row_total);
     }
 }
 
@@ -340,7 +303,7 @@ struct CompressWs {
 
 static CompressWs carve_compress_ws(void *ws, uint64_t n) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
+    const uint64_t tiles = (uint64_t)kMaxSms * 16;       // K3 chunk summaries
     CompressWs w;
     char *p = reinterpret_cast<char *>(ws);
     w.ctrl = reinterpret_cast<Ctrl *>(p);
@@ -355,7 +318,7 @@ static CompressWs carve_compress_ws(void *ws, uint64_t n) {
 
 size_t compress_workspace_bytes(uint64_t n) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
+    const uint64_t tiles = (uint64_t)kMaxSms * 16;
     return sizeof(Ctrl) + align256(tiles * sizeof(unsigned long long)) +
            align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int)) + align256(P);
 }
@@ -402,9 +365,11 @@ int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre
         KernelScope ks(kK3, st);
         if (!g_k3_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
-        const uint64_t tiles = (P + kK3Tile - 1) / kK3Tile;
-        const int grid = (int)tmin<uint64_t>(tiles, (uint64_t)sms * tmax(1, g_k3_blocks));
-        tlc_zre_kernel<<<grid, kK3Threads, 0, st>>>(w.bytes, P, payload, w.ctrl, w.states, hdr);
+        const uint64_t rows = (P + kK3Row - 1) / kK3Row;
+        const uint64_t grid = tmin<uint64_t>(rows, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks)));
+        const uint64_t chunk = ((P + grid - 1) / grid + kK3Seg - 1) / kK3Seg * kK3Seg;
+        const uint64_t nch = (P + chunk - 1) / chunk;
+        tlc_zre_kernel<<<(unsigned)nch, kK3Threads, 0, st>>>(w.bytes, P, chunk, payload, w.ctrl, w.states, hdr);
     }
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }

@@ -16,10 +16,6 @@
 
 namespace tlc {
 
-constexpr int kK4Threads = 256;
-constexpr int kK4BytesPerThread = 8;
-constexpr int kK4Tile = kK4Threads * kK4BytesPerThread;   // payload bytes per scan tile
-constexpr int kK4Warps = kK4Threads / 32;
 
 constexpr int kK5Threads = 256;
 constexpr int kOutTile = 2048;                             // quartic bytes per output tile
@@ -33,12 +29,37 @@ __device__ __forceinline__ void raise_format(tlc_header *hdr) {
 __device__ __forceinline__ uint32_t zre_len(uint32_t b) { return b >= kFirstRunCode ? b - 241u : 1u; }
 
 // ============================================================== K4
+// Same chunked single-pass scan as K3 (compress.cu), over the sum monoid of
+// expansion lengths: phase 1 sums each chunk, phase 2 adds the preceding
+// chunks' sums, phase 3 re-scans the chunk (L2-resident) and writes the seek
+// entry of every output tile start that falls inside one of its bytes.
+constexpr int kK4Threads = kScanThreads;
+constexpr int kK4Seg = 16;
+constexpr int kK4Row = kK4Threads * kK4Seg;
+
+__device__ __forceinline__ int load_pay16(const uint8_t *__restrict__ p, uint64_t pos, uint64_t hi,
+                                          uint32_t (&len)[kK4Seg]) {
+    const int n = pos < hi ? (int)tmin<uint64_t>(kK4Seg, hi - pos) : 0;
+    uint8_t b[kK4Seg];
+    if (n == kK4Seg && (reinterpret_cast<uintptr_t>(p + pos) & 15u) == 0) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(p + pos));
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < kK4Seg; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kK4Seg; k++) b[k] = k < n ? p[pos + k] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kK4Seg; k++) len[k] = k < n ? zre_len(b[k]) : 0u;
+    return n;
+}
+
 __global__ void __launch_bounds__(kK4Threads)
 tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64_t n, Ctrl *ctrl,
                     unsigned long long *states, unsigned long long *seek) {
-    __shared__ unsigned int s_warp[kK4Warps];
-    __shared__ unsigned long long s_tile_excl;
-    __shared__ unsigned int s_tile;
+    __shared__ unsigned long long s_warp[kScanWarps];
+    __shared__ unsigned int s_id;
     const uint64_t P = (n + 4) / 5;
     const unsigned int status = hdr->status;
     const uint64_t Z = hdr->payload_len;
@@ -52,86 +73,55 @@ tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64
         return;
     }
     if (!zre) return;
-    const uint64_t num_tiles = (Z + kK4Tile - 1) / kK4Tile;
+    // chunk size from the device-side payload length: at most gridDim.x chunks
+    const uint64_t chunk = tmax<uint64_t>(kK4Row, ((Z + gridDim.x - 1) / gridDim.x + kK4Seg - 1) / kK4Seg * kK4Seg);
+    const uint64_t nchunks = (Z + chunk - 1) / chunk;
     const uint64_t num_out_tiles = (P + kOutTile - 1) / kOutTile;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->tile_counter, 1u);
+    __syncthreads();
+    const uint64_t b = s_id;
+    if (b >= nchunks) return;
+    const uint64_t lo = b * chunk, hi = tmin<uint64_t>(Z, lo + chunk);
+    uint32_t len[kK4Seg];
 
-    while (true) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&ctrl->tile_counter, 1u);
-        __syncthreads();
-        const uint64_t tile = s_tile;
-        if (tile >= num_tiles) break;
-        const uint64_t z0 = tile * kK4Tile + (uint64_t)threadIdx.x * kK4BytesPerThread;
-        uint8_t b[kK4BytesPerThread];
-        uint32_t len[kK4BytesPerThread];
+    // ---- phase 1: expansion length of the chunk
+    uint64_t agg = 0;
+    for (uint64_t row = lo; row < hi; row += kK4Row) {
+        load_pay16(payload, row + (uint64_t)kK4Seg * threadIdx.x, hi, len);
         uint32_t sum = 0;
 #pragma unroll
-        for (int m = 0; m < kK4BytesPerThread; m++) {
-            b[m] = (z0 + m < Z) ? payload[z0 + m] : 0;
-            len[m] = (z0 + m < Z) ? zre_len(b[m]) : 0u;
-            sum += len[m];
-        }
-        // block exclusive scan of the per-thread sums
-        uint32_t x = sum;
+        for (int k = 0; k < kK4Seg; k++) sum += len[k];
+        agg += block_reduce_sum(sum, s_warp);
+    }
+    if (threadIdx.x == 0) st_relaxed_u64(states + b, kReady | agg);
+
+    // ---- phase 2: quartic position of the chunk's first byte
+    uint64_t part = 0;
+    const uint64_t per = (b + kK4Threads - 1) / kK4Threads;
+    const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(b, i0 + per);
+    for (uint64_t i = i0; i < i1; i++) part += wait_ready(states + i) & ~kReady;
+    uint64_t run = block_reduce_sum(part, s_warp);
+    if (b == nchunks - 1 && threadIdx.x == 0 && run + agg != P) raise_format(hdr);
+
+    // ---- phase 3: seek entries (payload byte covering J0 = k*kOutTile, offset inside it)
+    for (uint64_t row = lo; row < hi; row += kK4Row) {
+        const uint64_t pos0 = row + (uint64_t)kK4Seg * threadIdx.x;
+        load_pay16(payload, pos0, hi, len);
+        uint32_t sum = 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t agg = 0;
+        for (int k = 0; k < kK4Seg; k++) sum += len[k];
+        uint64_t row_total;
+        uint64_t q = run + block_excl_scan_sum(sum, s_warp, row_total);
 #pragma unroll
-            for (int w = 0; w < kK4Warps; w++) agg += s_warp[w];
-            unsigned long long excl = 0;
-            if (tile == 0) {
-                if (lane == 0) st_relaxed_u64(states, kStatusPrefix | agg);
-            } else {
-                if (lane == 0) st_relaxed_u64(states + tile, kStatusAgg | agg);
-                int64_t pred = (int64_t)tile - 1;
-                while (true) {
-                    const int64_t idx = pred - lane;
-                    unsigned long long w = idx >= 0 ? ld_relaxed_u64(states + idx) : kStatusPrefix;
-                    const unsigned int st = (unsigned int)(w >> 62);
-                    const unsigned int pref = __ballot_sync(0xffffffffu, st == 2u);
-                    const unsigned int inval = __ballot_sync(0xffffffffu, st == 0u);
-                    const int first = pref ? (__ffs(pref) - 1) : 31;
-                    const unsigned int window = (first == 31) ? 0xffffffffu : ((2u << first) - 1u);
-                    if (inval & window) { __nanosleep(32); continue; }
-                    unsigned long long v = (lane <= first) ? (w & kSumMask) : 0ull;
-#pragma unroll
-                    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-                    excl += v;
-                    if (pref) break;
-                    pred -= 32;
-                }
-                if (lane == 0) st_relaxed_u64(states + tile, kStatusPrefix | (excl + agg));
-            }
-            if (lane == 0) {
-                s_tile_excl = excl;
-                if (tile == num_tiles - 1 && excl + agg != P) raise_format(hdr);
-            }
-            __syncwarp();
-            if (lane == 0) {   // exclusive warp offsets
-                uint32_t acc = 0;
-                for (int w = 0; w < kK4Warps; w++) { uint32_t t = s_warp[w]; s_warp[w] = acc; acc += t; }
+        for (int k = 0; k < kK4Seg; k++) {
+            if (len[k]) {
+                const uint64_t kt = (q + kOutTile - 1) / kOutTile;
+                const uint64_t J0 = kt * kOutTile;
+                if (J0 < q + len[k] && kt < num_out_tiles) seek[kt] = ((pos0 + k) << 4) | (J0 - q);
+                q += len[k];
             }
         }
-        __syncthreads();
-        // seek entries: the byte whose expansion [pos, pos+len) contains J0 = k*kOutTile
-        uint64_t pos = s_tile_excl + s_warp[warp] + (x - sum);
-#pragma unroll
-        for (int m = 0; m < kK4BytesPerThread; m++) {
-            if (len[m]) {
-                const uint64_t k = (pos + kOutTile - 1) / kOutTile;
-                const uint64_t J0 = k * kOutTile;
-                if (J0 < pos + len[m] && k < num_out_tiles)
-                    seek[k] = ((z0 + m) << 4) | (J0 - pos);
-                pos += len[m];
-            }
-        }
-        __syncthreads();
+        run += row_total;
     }
 }
 
@@ -295,26 +285,31 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
 // ============================================================== host launchers
 static int g_k5_blocks = 0;
 
+static int g_k4_blocks = 0;
+constexpr int kMaxScanChunks = kMaxSms * 16;
+
 int launch_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *out, int mode,
                       void *ws, cudaStream_t st) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t scan_tiles = (P + kK4Tile - 1) / kK4Tile;
     const uint64_t out_tiles = (P + kOutTile - 1) / kOutTile;
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(ws);
     unsigned long long *states = reinterpret_cast<unsigned long long *>((char *)ws + sizeof(Ctrl));
     unsigned long long *seek = reinterpret_cast<unsigned long long *>(
-        (char *)ws + sizeof(Ctrl) + align256(scan_tiles * sizeof(unsigned long long)));
-    if (cudaMemsetAsync(ws, 0, sizeof(Ctrl) + scan_tiles * sizeof(unsigned long long), st) != cudaSuccess)
+        (char *)ws + sizeof(Ctrl) + align256(kMaxScanChunks * sizeof(unsigned long long)));
+    if (cudaMemsetAsync(ws, 0, sizeof(Ctrl) + kMaxScanChunks * sizeof(unsigned long long), st) != cudaSuccess)
         return TLC_ERR_CUDA;
     const int sms = num_sms();
     if (!g_k5_blocks)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k5_blocks, tlc_expand_dequant_kernel<true, 0>, kK5Threads, 0);
-    const int grid4 = (int)tmin<uint64_t>(scan_tiles, (uint64_t)sms * 8);
+    if (!g_k4_blocks)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k4_blocks, tlc_zre_scan_kernel, kK4Threads, 0);
     {
         KernelScope ks(kK4, st);
+        const uint64_t rows = (P + kK4Row - 1) / kK4Row;
+        const int grid4 = (int)tmax<uint64_t>(1, tmin<uint64_t>(rows, (uint64_t)sms * tmin(16, tmax(1, g_k4_blocks))));
         tlc_zre_scan_kernel<<<grid4, kK4Threads, 0, st>>>(payload, hdr, n, ctrl, states, seek);
     }
-    const int grid5 = (int)tmin<uint64_t>(out_tiles, (uint64_t)sms * max(1, g_k5_blocks));
+    const int grid5 = (int)tmin<uint64_t>(out_tiles, (uint64_t)sms * tmax(1, g_k5_blocks));
     const bool vec = (P % 4 == 0) && aligned16(out);
     KernelScope ks(kK5, st);
     if (mode == TLC_MODE_OVERWRITE) {
@@ -329,9 +324,8 @@ int launch_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float
 
 size_t decompress_workspace_bytes(uint64_t n) {
     const uint64_t P = (n + 4) / 5;
-    const uint64_t scan_tiles = (P + kK4Tile - 1) / kK4Tile;
     const uint64_t out_tiles = (P + kOutTile - 1) / kOutTile;
-    return sizeof(Ctrl) + align256(scan_tiles * sizeof(unsigned long long)) +
+    return sizeof(Ctrl) + align256(kMaxScanChunks * sizeof(unsigned long long)) +
            align256(out_tiles * sizeof(unsigned long long));
 }
 

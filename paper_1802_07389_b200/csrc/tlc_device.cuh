@@ -223,4 +223,97 @@ __device__ __forceinline__ unsigned long long shfl_down64(unsigned long long v, 
     return __shfl_down_sync(0xffffffffu, v, d);
 }
 
+// ---------------------------------------------------------------- block-level helpers
+// (blockDim.x == 256, 8 warps; thread t's item precedes thread t+1's)
+constexpr int kScanThreads = 256;
+constexpr int kScanWarps = kScanThreads / 32;
+
+// In-order reduction of one RunSum per thread; every thread gets the total.
+__device__ __forceinline__ RunSum block_reduce_runs(const RunSum &x, unsigned long long *s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long v = pack(x);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = shfl_down64(v, d);
+        if (lane + d < 32) v = pack(compose(unpack(v), unpack(o)));
+    }
+    if (lane == 0) s_warp[warp] = v;
+    __syncthreads();
+    RunSum r = run_identity();
+#pragma unroll
+    for (int w = 0; w < kScanWarps; w++) r = compose(r, unpack(s_warp[w]));
+    __syncthreads();
+    return r;
+}
+
+// In-order exclusive scan; `total` receives the block aggregate in every thread.
+__device__ __forceinline__ RunSum block_excl_scan_runs(const RunSum &x, unsigned long long *s_warp,
+                                                       RunSum &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long v = pack(x);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = shfl_up64(v, d);
+        if (lane >= d) v = pack(compose(unpack(y), unpack(v)));
+    }
+    unsigned long long ex = shfl_up64(v, 1);
+    if (lane == 0) ex = pack(run_identity());
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+    RunSum pre = run_identity(), tot = run_identity();
+#pragma unroll
+    for (int w = 0; w < kScanWarps; w++) {
+        const RunSum ww = unpack(s_warp[w]);
+        if (w < warp) pre = compose(pre, ww);
+        tot = compose(tot, ww);
+    }
+    __syncthreads();
+    total = tot;
+    return compose(pre, unpack(ex));
+}
+
+// Sum versions for the decoder's expansion lengths.
+__device__ __forceinline__ uint64_t block_reduce_sum(uint64_t x, unsigned long long *s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+    if (lane == 0) s_warp[warp] = x;
+    __syncthreads();
+    uint64_t r = 0;
+#pragma unroll
+    for (int w = 0; w < kScanWarps; w++) r += s_warp[w];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ uint64_t block_excl_scan_sum(uint64_t x, unsigned long long *s_warp,
+                                                        uint64_t &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t v = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += y;
+    }
+    if (lane == 31) s_warp[warp] = v;
+    __syncthreads();
+    uint64_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kScanWarps; w++) {
+        pre += (w < warp) ? s_warp[w] : 0ull;
+        tot += s_warp[w];
+    }
+    __syncthreads();
+    total = tot;
+    return pre + v - x;
+}
+
+constexpr unsigned long long kReady = 1ull << 62;
+
+__device__ __forceinline__ unsigned long long wait_ready(const unsigned long long *p) {
+    unsigned long long w;
+    while (!((w = ld_relaxed_u64(p)) & kReady)) __nanosleep(64);
+    return w;
+}
+
 }  // namespace tlc

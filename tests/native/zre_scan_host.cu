@@ -1,106 +1,103 @@
-// Host-only harness (no GPU): drives the device-side ZRE scan building blocks of
+// Host-only harness (no GPU): drives the device-side ZRE building blocks of
 // paper_1802_07389_b200/csrc/tlc_device.cuh (segment_summary, compose, run_eval,
 // segment_emit -- all __host__ __device__) through the same decomposition the
-// K2 kernel uses: 8-byte thread segments, Hillis-Steele warp scans, per-tile
-// aggregates and a decoupled look-back over windows of 32 predecessors whose
-// publication state (aggregate only / inclusive prefix) is drawn at random.
-// tests/test_zre_scan_host.py compares its output with the oracle's ZRE.
-#include <cstdint>
-#include <array>
+// K3 kernel (compress.cu) uses: `nchunks` contiguous chunks, rows of
+// threads x 16-byte segments, in-order tree reductions (phase 1), the carry-in
+// composed from per-thread partial compositions of the preceding chunk
+// summaries (phase 2), and per-row Hillis-Steele exclusive scans with emission
+// at the final offsets (phase 3).  tests/test_zre_scan_host.py compares the
+// output with the oracle's zero-run encoding.
 #include <algorithm>
+#include <array>
+#include <cstdint>
 #include <cstring>
-#include <random>
 #include <vector>
 
 #include "../../paper_1802_07389_b200/csrc/tlc_device.cuh"
 
 using namespace tlc;
 
-extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int threads, uint64_t seed, uint8_t *out) {
-    constexpr int SEG = 8;
-    const uint64_t T = (uint64_t)threads * SEG;
-    const uint64_t num_tiles = (P + T - 1) / T;
-    std::mt19937_64 rng(seed);
-    std::vector<RunSum> tile_agg(num_tiles), tile_incl(num_tiles);
-    std::vector<int> has_prefix(num_tiles, 0);
+namespace {
+constexpr int SEG = 16;
+
+RunSum tree_reduce(std::vector<RunSum> v) {   // shfl_down-style in-order tree
+    for (size_t d = 1; d < v.size(); d <<= 1)
+        for (size_t l = 0; l + d < v.size(); l += 2 * d) v[l] = compose(v[l], v[l + d]);
+    return v.empty() ? run_identity() : v[0];
+}
+
+int seg_at(const uint8_t *B, uint64_t pos, uint64_t hi, uint8_t (&b)[SEG]) {
+    const int len = pos < hi ? (int)std::min<uint64_t>(SEG, hi - pos) : 0;
+    for (int k = 0; k < SEG; k++) b[k] = k < len ? B[pos + k] : 0;
+    return len;
+}
+}  // namespace
+
+extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int threads, uint64_t nchunks_req, uint8_t *out) {
+    const uint64_t row_bytes = (uint64_t)threads * SEG;
+    uint64_t chunk = (P + nchunks_req - 1) / nchunks_req;
+    chunk = (chunk + SEG - 1) / SEG * SEG;
+    const uint64_t nch = (P + chunk - 1) / chunk;
+    std::vector<RunSum> agg(nch);
+    // phase 1
+    for (uint64_t b = 0; b < nch; b++) {
+        const uint64_t lo = b * chunk, hi = std::min(P, lo + chunk);
+        RunSum a = run_identity();
+        for (uint64_t row = lo; row < hi; row += row_bytes) {
+            std::vector<RunSum> v(threads);
+            for (int t = 0; t < threads; t++) {
+                uint8_t s[SEG];
+                const int len = seg_at(B, row + (uint64_t)SEG * t, hi, s);
+                v[t] = segment_summary(s, len);
+            }
+            a = compose(a, tree_reduce(v));
+        }
+        agg[b] = a;
+    }
     uint64_t total = 0;
-    for (uint64_t tile = 0; tile < num_tiles; tile++) {
-        const uint64_t j0 = tile * T;
-        const int tile_len = (int)std::min<uint64_t>(T, P - j0);
-        std::vector<RunSum> mine(threads);
-        std::vector<std::array<uint8_t, SEG>> segs(threads);
-        std::vector<int> slen(threads);
-        for (int th = 0; th < threads; th++) {
-            uint8_t b[SEG];
-            const int sbeg = th * SEG;
-            slen[th] = std::max(0, std::min(SEG, tile_len - sbeg));
-            for (int m = 0; m < SEG; m++) b[m] = (m < slen[th]) ? B[j0 + sbeg + m] : 0;
-            std::memcpy(segs[th].data(), b, SEG);
-            mine[th] = segment_summary(b, slen[th]);
-        }
-        // warp inclusive scans (Hillis-Steele, as with shfl_up)
-        std::vector<RunSum> incl(mine);
-        const int nw = (threads + 31) / 32;
-        for (int w = 0; w < nw; w++) {
-            const int lo = w * 32, hi = std::min(threads, lo + 32);
-            for (int d = 1; d < 32; d <<= 1) {
-                std::vector<RunSum> nx(incl.begin() + lo, incl.begin() + hi);
-                for (int l = lo; l < hi; l++)
-                    if (l - lo >= d) nx[l - lo] = compose(incl[l - d], incl[l]);
-                std::copy(nx.begin(), nx.end(), incl.begin() + lo);
-            }
-        }
-        std::vector<RunSum> warp_excl(nw);
-        RunSum agg = run_identity();
-        for (int w = 0; w < nw; w++) {
-            warp_excl[w] = agg;
-            agg = compose(agg, incl[std::min(threads, w * 32 + 32) - 1]);
-        }
-        // decoupled look-back over windows of 32 predecessors
-        RunSum excl = run_identity();
-        if (tile > 0) {
-            int64_t pred = (int64_t)tile - 1;
-            while (true) {
-                RunSum v[32];
-                int first = 31;
-                bool found = false;
-                for (int l = 0; l < 32; l++) {
-                    const int64_t idx = pred - l;
-                    if (idx < 0) { v[l] = run_identity(); if (!found) { first = l; found = true; } continue; }
-                    if (has_prefix[idx]) { v[l] = tile_incl[idx]; if (!found) { first = l; found = true; } }
-                    else v[l] = tile_agg[idx];
-                }
-                for (int l = first + 1; l < 32; l++) v[l] = run_identity();
-                for (int d = 1; d < 32; d <<= 1)      // tree reduction as with shfl_down
-                    for (int l = 0; l + d < 32; l++) v[l] = compose(v[l + d], v[l]);
-                excl = compose(v[0], excl);
-                if (found) break;
-                pred -= 32;
-            }
-        }
-        tile_agg[tile] = agg;
-        tile_incl[tile] = compose(excl, agg);
-        has_prefix[tile] = (tile == 0) || (rng() % 3 == 0);   // some tiles publish only aggregates
-        // emission
-        for (int th = 0; th < threads; th++) {
-            if (slen[th] <= 0) continue;
-            const int w = th / 32, l = th % 32;
-            RunSum texcl = l == 0 ? run_identity() : incl[th - 1];
-            RunSum before = compose(excl, compose(warp_excl[w], texcl));
-            uint64_t off;
-            uint32_t c;
-            run_eval(before, 0, off, c);
-            uint8_t b[SEG];
-            std::memcpy(b, segs[th].data(), SEG);
-            segment_emit(b, slen[th], c, out, off);
-            if (c > 0 && j0 + th * SEG + slen[th] == P) out[off++] = run_code(c);
-            total = std::max(total, off);
-        }
-        if (tile == num_tiles - 1) {
+    for (uint64_t b = 0; b < nch; b++) {
+        const uint64_t lo = b * chunk, hi = std::min(P, lo + chunk);
+        // phase 2
+        const uint64_t per = (b + threads - 1) / threads;
+        std::vector<RunSum> part(threads, run_identity());
+        for (int t = 0; t < threads; t++)
+            for (uint64_t i = per * t; i < std::min<uint64_t>(b, per * t + per); i++) part[t] = compose(part[t], agg[i]);
+        RunSum run = tree_reduce(part);
+        if (b == nch - 1) {
             uint64_t cnt;
             uint32_t carry;
-            run_eval(tile_incl[tile], 0, cnt, carry);
-            if (cnt + (carry > 0) != total) return ~0ull;    // header length disagrees
+            run_eval(compose(run, agg[b]), 0, cnt, carry);
+            total = cnt + (carry > 0);
+        }
+        // phase 3
+        for (uint64_t row = lo; row < hi; row += row_bytes) {
+            std::vector<RunSum> v(threads), incl(threads);
+            std::vector<std::array<uint8_t, SEG>> segs(threads);
+            std::vector<int> lens(threads);
+            for (int t = 0; t < threads; t++) {
+                uint8_t s[SEG];
+                lens[t] = seg_at(B, row + (uint64_t)SEG * t, hi, s);
+                std::memcpy(segs[t].data(), s, SEG);
+                v[t] = segment_summary(s, lens[t]);
+            }
+            incl = v;
+            for (int d = 1; d < threads; d <<= 1) {
+                std::vector<RunSum> nx(incl);
+                for (int t = d; t < threads; t++) nx[t] = compose(incl[t - d], incl[t]);
+                incl.swap(nx);
+            }
+            for (int t = 0; t < threads; t++) {
+                if (lens[t] <= 0) continue;
+                const RunSum ex = t == 0 ? run_identity() : incl[t - 1];
+                uint64_t off;
+                uint32_t c;
+                run_eval(compose(run, ex), 0, off, c);
+                uint8_t s[SEG];
+                std::memcpy(s, segs[t].data(), SEG);
+                segment_emit(s, lens[t], c, out, off);
+                if (c > 0 && row + (uint64_t)SEG * t + lens[t] == P) out[off++] = run_code(c);
+            }
+            run = compose(run, incl[threads - 1]);
         }
     }
     return total;

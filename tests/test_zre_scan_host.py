@@ -2,8 +2,8 @@
 
 tests/native/zre_scan_host.cu compiles the __host__ __device__ building blocks of
 csrc/tlc_device.cuh as host code and drives them through the K2 decomposition
-(thread segments, warp scans, tile look-back with random aggregate/prefix
-states).  Its output must equal the oracle's zero-run encoding byte for byte."""
+(chunks, rows of 16-byte thread segments, in-order reductions, carry-in
+composition, per-row exclusive scans).  Its output must equal the oracle's zero-run encoding byte for byte."""
 import ctypes
 import os
 import subprocess
@@ -24,16 +24,17 @@ DEPS = [SRC, os.path.join(ROOT, "paper_1802_07389_b200", "csrc", "tlc_device.cuh
 def sim():
     if not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS):
         subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-std=c++17", "-O2", "-x", "cu",
+                               "-gencode", "arch=compute_100a,code=sm_100a",
                                "-Xcompiler", "-fPIC", "-shared", "-o", LIB, SRC])
     L = ctypes.CDLL(LIB)
     L.zre_scan_sim.restype = ctypes.c_uint64
     L.zre_scan_sim.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p]
 
-    def run(B, threads, seed=0):
+    def run(B, threads, nchunks):
         B = np.ascontiguousarray(B, dtype=np.uint8)
-        out = np.zeros(B.size + 16, dtype=np.uint8)
-        z = L.zre_scan_sim(B.ctypes.data, B.size, threads, seed, out.ctypes.data)
-        assert z != 2 ** 64 - 1, "tile-aggregate length disagrees with emitted bytes"
+        out = np.full(B.size + 16, 0xEE, dtype=np.uint8)
+        z = L.zre_scan_sim(B.ctypes.data, B.size, threads, nchunks, out.ctypes.data)
+        assert np.all(out[z:] == 0xEE), "bytes emitted past the computed payload length"
         return out[:z]
 
     return run
@@ -60,6 +61,6 @@ def _streams():
 def test_scan_matches_oracle_zre(sim, threads):
     for i, B in enumerate(_streams()):
         ref = O.zre_encode(B)
-        for seed in (0, 1):
-            got = sim(B, threads, seed + 10 * i)
-            assert got.tolist() == ref.tolist(), (threads, i, B.size)
+        for nchunks in (1, 2, 3, 7, 64):
+            got = sim(B, threads, nchunks)
+            assert got.tolist() == ref.tolist(), (threads, nchunks, i, B.size)
