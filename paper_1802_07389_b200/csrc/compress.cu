@@ -222,20 +222,30 @@ tlc_quant_qe_scalar_kernel(const float *__restrict__ t, float *__restrict__ err,
 //            every ZRE byte at its final offset.
 // The dependency depth between chunks is one publication, not a chain.
 constexpr int kK3Threads = kScanThreads;
-constexpr int kK3Seg = 16;                                  // bytes per thread per row
-constexpr int kK3Row = kK3Threads * kK3Seg;                 // 4096 quartic bytes per row
+constexpr int kK3Words = 8;                                 // 32 bytes per thread per row
+constexpr int kK3Seg = 4 * kK3Words;
+constexpr int kK3Row = kK3Threads * kK3Seg;                 // 8192 quartic bytes per row
 
-__device__ __forceinline__ int load_seg16(const uint8_t *__restrict__ bytes, uint64_t pos, uint64_t hi,
-                                          uint8_t (&b)[kK3Seg]) {
+// Load the segment [pos, min(pos+32, hi)) as words, padding with 121 (0x79).
+__device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint64_t pos, uint64_t hi,
+                                        uint32_t (&w)[kK3Words]) {
     const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
     if (len == kK3Seg && (reinterpret_cast<uintptr_t>(bytes + pos) & 15u) == 0) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(bytes + pos);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < kK3Seg; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
+        const uint4 a = *reinterpret_cast<const uint4 *>(bytes + pos);
+        const uint4 b = *reinterpret_cast<const uint4 *>(bytes + pos + 16);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
 #pragma unroll
-        for (int k = 0; k < kK3Seg; k++) b[k] = k < len ? bytes[pos + k] : 0;
+        for (int k = 0; k < kK3Words; k++) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int m = 4 * k + c;
+                x |= (uint32_t)(m < len ? bytes[pos + m] : kZeroGroup) << (8 * c);
+            }
+            w[k] = x;
+        }
     }
     return len;
 }
@@ -252,12 +262,12 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     const uint64_t b = s_id;
     if (b >= nchunks) return;
     const uint64_t lo = b * chunk, hi = tmin<uint64_t>(P, lo + chunk);
-    uint8_t seg[kK3Seg];
+    uint32_t seg[kK3Words];
 
     // ---- phase 1: run summary of the chunk
     RunSum agg = run_identity();
     for (uint64_t row = lo; row < hi; row += kK3Row) {
-        const int len = load_seg16(bytes, row + (uint64_t)kK3Seg * threadIdx.x, hi, seg);
+        const int len = load_seg(bytes, row + (uint64_t)kK3Seg * threadIdx.x, hi, seg);
         agg = compose(agg, block_reduce_runs(segment_summary(seg, len), s_warp));
     }
     if (threadIdx.x == 0) st_relaxed_u64(states + b, kReady | pack(agg));
@@ -278,7 +288,7 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     // ---- phase 3: emission at the final payload offsets
     for (uint64_t row = lo; row < hi; row += kK3Row) {
         const uint64_t pos = row + (uint64_t)kK3Seg * threadIdx.x;
-        const int len = load_seg16(bytes, pos, hi, seg);
+        const int len = load_seg(bytes, pos, hi, seg);
         RunSum row_total;
         const RunSum ex = block_excl_scan_runs(segment_summary(seg, len), s_warp, row_total);
         if (len > 0) {

@@ -78,26 +78,23 @@ struct Quant {
 // 14; any other byte first flushes a pending chunk (121 if c == 1, else
 // 243+(c-2)) and then emits itself; the end of the stream flushes too.  A
 // stretch of quartic bytes therefore acts on the incoming carry as
-//     ALL (every byte is 121, length L):
-//         count(c) = floor((c+L)/14),                  carry' = (c+L) % 14
+//     ALL (every byte is 121, length L = 14*div + mod):
+//         count(c) = div + [c+mod >= 14],               carry' = (c+mod) mod 14
 //     MIX (contains a non-121 byte; leading 121-run of length 14a + r0):
-//         count(c) = cnt + ceil((c+r0)/14),            carry' = tr
+//         count(c) = cnt + ceil((c+r0)/14),             carry' = tr
 // with cnt = a + emissions from the first non-121 byte on, tr = trailing run
-// length mod 14.  Composition of these transfer functions is associative, so
-// the encoder is one scan with decoupled look-back and needs no look-ahead
-// (DESIGN.md section 5.3).
+// length mod 14.  Composition of these transfer functions is associative and
+// needs only adds and compares (every sum of residues is < 28), so the encoder
+// is a scan over this monoid.
 //
-// Packing (64 bit): bits 0..43 L|cnt, 45..48 r0, 49..52 tr, bit 53 kind
-// (1 = MIX), bits 62..63 look-back status.
+// Packing (64 bit): bits 0..43 div|cnt, 45..48 mod|r0, 49..52 tr, bit 53 kind
+// (1 = MIX), bit 62 "published" flag of the chunk scans.
 struct RunSum {
-    uint64_t v;   // L or cnt
-    uint32_t r0, tr;
+    uint64_t v;   // ALL: L div 14; MIX: cnt
+    uint32_t r0;  // ALL: L mod 14; MIX: leading run mod 14
+    uint32_t tr;  // MIX: trailing run mod 14
     bool mix;
 };
-
-constexpr unsigned long long kStatusAgg = 1ull << 62;
-constexpr unsigned long long kStatusPrefix = 2ull << 62;
-constexpr unsigned long long kStatusMask = 3ull << 62;
 
 __host__ __device__ __forceinline__ unsigned long long pack(const RunSum &s) {
     return (s.v & ((1ull << 44) - 1)) | ((unsigned long long)s.r0 << 45) |
@@ -106,52 +103,47 @@ __host__ __device__ __forceinline__ unsigned long long pack(const RunSum &s) {
 __host__ __device__ __forceinline__ RunSum unpack(unsigned long long w) {
     RunSum s;
     s.v = w & ((1ull << 44) - 1);
-    s.r0 = (w >> 45) & 15;
-    s.tr = (w >> 49) & 15;
+    s.r0 = (uint32_t)(w >> 45) & 15u;
+    s.tr = (uint32_t)(w >> 49) & 15u;
     s.mix = (w >> 53) & 1;
     return s;
 }
 __host__ __device__ __forceinline__ RunSum run_identity() { return RunSum{0, 0, 0, false}; }
 
+__host__ __device__ __forceinline__ uint32_t mod14(uint32_t x) { return x >= kMaxRun ? x - kMaxRun : x; }  // x < 28
+
 // a then b
 __host__ __device__ __forceinline__ RunSum compose(const RunSum &a, const RunSum &b) {
     RunSum r;
     if (!a.mix) {
-        if (!b.mix) {  // ALL . ALL
-            r = a;
-            r.v = a.v + b.v;
-            return r;
-        }
-        // ALL . MIX: a's 121s extend b's leading run
-        const uint64_t x = a.v + b.r0;
-        r.mix = true;
-        r.r0 = (uint32_t)(x % kMaxRun);
-        r.v = b.v + x / kMaxRun;
+        const uint32_t x = a.r0 + b.r0;          // ALL . ALL, or a's 121s extend b's leading run
+        r.v = a.v + b.v + (x >= kMaxRun);
+        r.r0 = mod14(x);
         r.tr = b.tr;
+        r.mix = b.mix;
         return r;
     }
     r = a;
-    if (!b.mix) {  // MIX . ALL
-        const uint64_t x = a.tr + b.v;
-        r.v = a.v + x / kMaxRun;
-        r.tr = (uint32_t)(x % kMaxRun);
-        return r;
+    const uint32_t x = a.tr + b.r0;
+    if (!b.mix) {                                // MIX . ALL
+        r.v = a.v + b.v + (x >= kMaxRun);
+        r.tr = mod14(x);
+    } else {                                     // MIX . MIX: b's first literal flushes a's tail
+        r.v = a.v + b.v + (x > 0) + (x > kMaxRun);
+        r.tr = b.tr;
     }
-    // MIX . MIX: b's first non-121 byte flushes the run carried out of a
-    r.v = a.v + b.v + (a.tr + b.r0 + kMaxRun - 1) / kMaxRun;
-    r.tr = b.tr;
     return r;
 }
 
 // (emitted count, carry) of a stretch entered with carry c
 __host__ __device__ __forceinline__ void run_eval(const RunSum &s, uint32_t c, uint64_t &count,
                                                   uint32_t &carry) {
+    const uint32_t x = c + s.r0;
     if (!s.mix) {
-        const uint64_t x = c + s.v;
-        count = x / kMaxRun;
-        carry = (uint32_t)(x % kMaxRun);
+        count = s.v + (x >= kMaxRun);
+        carry = mod14(x);
     } else {
-        count = s.v + (c + s.r0 + kMaxRun - 1) / kMaxRun;
+        count = s.v + (x > 0) + (x > kMaxRun);
         carry = s.tr;
     }
 }
@@ -161,28 +153,36 @@ __host__ __device__ __forceinline__ uint8_t run_code(uint32_t c) {
     return c == 1 ? kZeroGroup : (uint8_t)(kFirstRunCode + (c - 2));
 }
 
-// Run summary of the bytes [0, len) of one segment (len <= N).
-template <int N>
-__host__ __device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[N], int len) {
+__host__ __device__ __forceinline__ uint32_t byte_at(const uint32_t *w, int m) {
+    return (w[m >> 2] >> (8 * (m & 3))) & 0xffu;
+}
+
+// Run summary of bytes [0, len) of one segment held as NW little-endian words;
+// bytes at positions >= len must be 121 (the loaders pad with 0x79).
+template <int NW>
+__host__ __device__ __forceinline__ RunSum segment_summary(const uint32_t (&w)[NW], int len) {
+    constexpr int N = 4 * NW;
     RunSum s = run_identity();
     if (len <= 0) return s;
-    int lead = 0;
-    bool in_lead = true;
+    bool all = true;
 #pragma unroll
-    for (int m = 0; m < N; m++) {          // static indices keep b[] in registers
-        if (m < len && in_lead && b[m] == kZeroGroup) lead++;
-        else in_lead = false;
-    }
-    if (lead == len) {
-        s.v = (uint64_t)len;
+    for (int k = 0; k < NW; k++) all &= (w[k] == 0x79797979u);
+    if (all) {
+        s.v = (uint64_t)(len / (int)kMaxRun);
+        s.r0 = (uint32_t)(len % (int)kMaxRun);
         return s;
     }
-    uint64_t cnt = 0;
-    uint32_t c = 0;   // pending 121s after the first non-121 byte
+    uint32_t lead = 0, cnt = 0, c = 0;
+    bool in_lead = true;
 #pragma unroll
     for (int m = 0; m < N; m++) {
-        if (m < lead || m >= len) continue;
-        if (b[m] != kZeroGroup) {
+        if (m >= len) break;
+        const uint32_t b = byte_at(w, m);
+        if (in_lead) {
+            if (b == kZeroGroup) { lead++; continue; }
+            in_lead = false;
+        }
+        if (b != kZeroGroup) {
             cnt += (c > 0) + 1;
             c = 0;
         } else if (++c == kMaxRun) {
@@ -191,7 +191,7 @@ __host__ __device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[N]
         }
     }
     s.mix = true;
-    s.r0 = (uint32_t)(lead % kMaxRun);
+    s.r0 = lead % kMaxRun;
     s.v = cnt + lead / kMaxRun;
     s.tr = c;
     return s;
@@ -199,15 +199,16 @@ __host__ __device__ __forceinline__ RunSum segment_summary(const uint8_t (&b)[N]
 
 // Emit the ZRE bytes of one segment entered with carry c at payload offset
 // `off`; on return c is the carry out and off the next offset.
-template <int N>
-__host__ __device__ __forceinline__ void segment_emit(const uint8_t (&b)[N], int len, uint32_t &c,
+template <int NW>
+__host__ __device__ __forceinline__ void segment_emit(const uint32_t (&w)[NW], int len, uint32_t &c,
                                                       uint8_t *payload, uint64_t &off) {
 #pragma unroll
-    for (int m = 0; m < N; m++) {
+    for (int m = 0; m < 4 * NW; m++) {
         if (m >= len) break;
-        if (b[m] != kZeroGroup) {
+        const uint32_t b = byte_at(w, m);
+        if (b != kZeroGroup) {
             if (c > 0) payload[off++] = run_code(c);
-            payload[off++] = b[m];
+            payload[off++] = (uint8_t)b;
             c = 0;
         } else if (++c == kMaxRun) {
             payload[off++] = run_code(kMaxRun);

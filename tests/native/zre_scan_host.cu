@@ -2,7 +2,7 @@
 // paper_1802_07389_b200/csrc/tlc_device.cuh (segment_summary, compose, run_eval,
 // segment_emit -- all __host__ __device__) through the same decomposition the
 // K3 kernel (compress.cu) uses: `nchunks` contiguous chunks, rows of
-// threads x 16-byte segments, in-order tree reductions (phase 1), the carry-in
+// threads x 32-byte segments, in-order tree reductions (phase 1), the carry-in
 // composed from per-thread partial compositions of the preceding chunk
 // summaries (phase 2), and per-row Hillis-Steele exclusive scans with emission
 // at the final offsets (phase 3).  tests/test_zre_scan_host.py compares the
@@ -18,7 +18,8 @@
 using namespace tlc;
 
 namespace {
-constexpr int SEG = 16;
+constexpr int NW = 8;
+constexpr int SEG = 4 * NW;
 
 RunSum tree_reduce(std::vector<RunSum> v) {   // shfl_down-style in-order tree
     for (size_t d = 1; d < v.size(); d <<= 1)
@@ -26,9 +27,13 @@ RunSum tree_reduce(std::vector<RunSum> v) {   // shfl_down-style in-order tree
     return v.empty() ? run_identity() : v[0];
 }
 
-int seg_at(const uint8_t *B, uint64_t pos, uint64_t hi, uint8_t (&b)[SEG]) {
+int seg_at(const uint8_t *B, uint64_t pos, uint64_t hi, uint32_t (&w)[NW]) {
     const int len = pos < hi ? (int)std::min<uint64_t>(SEG, hi - pos) : 0;
-    for (int k = 0; k < SEG; k++) b[k] = k < len ? B[pos + k] : 0;
+    for (int k = 0; k < NW; k++) {
+        uint32_t x = 0;
+        for (int c = 0; c < 4; c++) x |= (uint32_t)(4 * k + c < len ? B[pos + 4 * k + c] : 121) << (8 * c);
+        w[k] = x;
+    }
     return len;
 }
 }  // namespace
@@ -46,7 +51,7 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int threads, uint
         for (uint64_t row = lo; row < hi; row += row_bytes) {
             std::vector<RunSum> v(threads);
             for (int t = 0; t < threads; t++) {
-                uint8_t s[SEG];
+                uint32_t s[NW];
                 const int len = seg_at(B, row + (uint64_t)SEG * t, hi, s);
                 v[t] = segment_summary(s, len);
             }
@@ -72,12 +77,12 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int threads, uint
         // phase 3
         for (uint64_t row = lo; row < hi; row += row_bytes) {
             std::vector<RunSum> v(threads), incl(threads);
-            std::vector<std::array<uint8_t, SEG>> segs(threads);
+            std::vector<std::array<uint32_t, NW>> segs(threads);
             std::vector<int> lens(threads);
             for (int t = 0; t < threads; t++) {
-                uint8_t s[SEG];
+                uint32_t s[NW];
                 lens[t] = seg_at(B, row + (uint64_t)SEG * t, hi, s);
-                std::memcpy(segs[t].data(), s, SEG);
+                std::memcpy(segs[t].data(), s, sizeof(s));
                 v[t] = segment_summary(s, lens[t]);
             }
             incl = v;
@@ -92,8 +97,8 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int threads, uint
                 uint64_t off;
                 uint32_t c;
                 run_eval(compose(run, ex), 0, off, c);
-                uint8_t s[SEG];
-                std::memcpy(s, segs[t].data(), SEG);
+                uint32_t s[NW];
+                std::memcpy(s, segs[t].data(), sizeof(s));
                 segment_emit(s, lens[t], c, out, off);
                 if (c > 0 && row + (uint64_t)SEG * t + lens[t] == P) out[off++] = run_code(c);
             }
