@@ -124,63 +124,82 @@ tlc_absmax_kernel(const float *__restrict__ t, const float *__restrict__ err, ui
 // ============================================================== K2
 constexpr int kK2Threads = 256;
 
+// One quartic position j, any alignment: the five strided elements e = i*P + j
+// (partition i), residuals stored, byte returned (pad positions -> digit 0).
+__device__ __forceinline__ uint32_t quant_qe_one(const float *__restrict__ t, float *__restrict__ err,
+                                                 uint64_t n, uint64_t P, uint64_t j, const Quant &Q) {
+    float tv[5], ev[5];
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const uint64_t e = (uint64_t)i * P + j;
+        tv[i] = e < n ? ld_stream(t + e) : 0.0f;
+        ev[i] = e < n ? __ldcs(err + e) : 0.0f;
+    }
+    uint32_t b = 0;
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const uint64_t e = (uint64_t)i * P + j;
+        const float u = __fadd_rn(ev[i], tv[i]);            // step (1)
+        const int q = Q.q(u);                                // Eq. 2
+        if (e < n) __stcs(err + e, Q.residual(u, q));       // steps (a),(b)
+        b = b * 3u + (e < n ? (uint32_t)(q + 1) : 0u);       // steps 1,4,6 (pad digit 0)
+    }
+    return b;
+}
+
 // ---- vector path (P % 4 == 0, 16-byte aligned t/err/bytes): one thread per
 // group of 4 consecutive quartic positions j..j+3, one float4 per partition.
+// Groups whose 20 elements all exist run without bounds checks; the few
+// positions of the last group(s) of partition 4 go through quant_qe_one.
+template <class QT>
+__device__ __forceinline__ void quant_qe_groups(const float4 *__restrict__ t4, float4 *__restrict__ e4,
+                                                uint32_t *__restrict__ b4, uint64_t P4,
+                                                uint64_t full_groups, const QT &Q) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < full_groups; g += stride) {
+        float4 tv[5], ev[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            tv[i] = ld_stream4(t4 + g + i * P4);
+            ev[i] = __ldcs(e4 + g + i * P4);
+        }
+        uint32_t by[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            float r[4];
+            const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
+            const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const float u = __fadd_rn(ee[c], tt[c]);    // step (1)
+                const int q = Q.q(u);                        // Eq. 2
+                r[c] = Q.residual(u, q);                     // steps (a),(b)
+                by[c] = by[c] * 3u + (uint32_t)(q + 1);      // steps 1, 6
+            }
+            __stcs(e4 + g + i * P4, make_float4(r[0], r[1], r[2], r[3]));
+        }
+        b4[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
+    }
+}
+
 __global__ void __launch_bounds__(kK2Threads, 3)
 tlc_quant_qe_vec_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
                         uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
     if (ctrl->status != TLC_OK) return;           // K1 raised NONFINITE / RANGE: err untouched
     const Quant Q(ctrl->M);
     const uint64_t P = (n + 4) / 5;
-    const uint64_t groups = P / 4;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
-         g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t j = 4 * g;
-        float4 tv[5], ev[5];
-        bool full[5];
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint64_t e = (uint64_t)i * P + j;
-            full[i] = e + 3 < n;                        // only the tail of partition 4 can fail
-            if (full[i]) {
-                tv[i] = ld_stream4(reinterpret_cast<const float4 *>(t + e));
-                ev[i] = __ldcs(reinterpret_cast<const float4 *>(err + e));
-            } else {
-                float a[4], b[4];
-#pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    a[c] = e + c < n ? ld_stream(t + e + c) : 0.0f;
-                    b[c] = e + c < n ? __ldcs(err + e + c) : 0.0f;
-                }
-                tv[i] = make_float4(a[0], a[1], a[2], a[3]);
-                ev[i] = make_float4(b[0], b[1], b[2], b[3]);
-            }
-        }
-        uint32_t by[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint64_t e = (uint64_t)i * P + j;
-            const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
-            const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
-            float r[4];
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const float u = __fadd_rn(ee[c], tt[c]);        // step (1)
-                const int q = Q.q(u);                            // Eq. 2
-                r[c] = Q.residual(u, q);                         // steps (a),(b)
-                const bool ok = full[i] || (e + c < n);
-                by[c] = by[c] * 3u + (ok ? (uint32_t)(q + 1) : 0u);   // steps 1,4,6 (pad digit 0)
-            }
-            if (full[i]) {
-                __stcs(reinterpret_cast<float4 *>(err + e), make_float4(r[0], r[1], r[2], r[3]));
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    if (e + c < n) __stcs(err + e + c, r[c]);
-            }
-        }
-        *reinterpret_cast<uint32_t *>(bytes + j) = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
-    }
+    const uint64_t P4 = P / 4;                     // partition stride in float4
+    // group g is complete iff 4P + 4g + 3 < n
+    const uint64_t full_groups = n >= 4 * P + 3 ? tmin<uint64_t>(P4, (n - 4 * P) / 4) : 0;
+    const float4 *t4 = reinterpret_cast<const float4 *>(t);
+    float4 *e4 = reinterpret_cast<float4 *>(err);
+    uint32_t *b4 = reinterpret_cast<uint32_t *>(bytes);
+    if (Q.mode == 1) quant_qe_groups(t4, e4, b4, P4, full_groups, QuantCmp(Q));   // uniform branch
+    else quant_qe_groups(t4, e4, b4, P4, full_groups, Q);
+    // tail: quartic positions of the incomplete groups
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t j = 4 * full_groups + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P; j += stride)
+        bytes[j] = (uint8_t)quant_qe_one(t, err, n, P, j, Q);
 }
 
 // ---- scalar path (any alignment, any P): one thread per quartic position j.
@@ -191,44 +210,29 @@ tlc_quant_qe_scalar_kernel(const float *__restrict__ t, float *__restrict__ err,
     const Quant Q(ctrl->M);
     const uint64_t P = (n + 4) / 5;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        float tv[5], ev[5];
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint64_t e = (uint64_t)i * P + j;
-            tv[i] = e < n ? ld_stream(t + e) : 0.0f;
-            ev[i] = e < n ? __ldcs(err + e) : 0.0f;
-        }
-        uint32_t b = 0;
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint64_t e = (uint64_t)i * P + j;
-            const float u = __fadd_rn(ev[i], tv[i]);
-            const int q = Q.q(u);
-            if (e < n) __stcs(err + e, Q.residual(u, q));
-            b = b * 3u + (e < n ? (uint32_t)(q + 1) : 0u);
-        }
-        bytes[j] = (uint8_t)b;
-    }
+         j += (uint64_t)gridDim.x * blockDim.x)
+        bytes[j] = (uint8_t)quant_qe_one(t, err, n, P, j, Q);
 }
 
 // ============================================================== K3
 // Chunked single-pass scan: the grid splits the P quartic bytes into one
-// contiguous chunk per CTA (chunk ids taken in order from an atomic counter).
-//   phase 1  each CTA folds its chunk into one run summary and publishes it;
-//   phase 2  it composes the summaries of all preceding chunks (they never
-//            wait on later chunks, so this cannot deadlock) -> its carry-in;
-//   phase 3  it re-reads its chunk (L2-resident: P <= 0.2 n bytes) and emits
-//            every ZRE byte at its final offset.
+// contiguous chunk per CTA (chunk ids taken in order from an atomic counter),
+// and each CTA splits its chunk into one sub-chunk per warp.
+//   phase 1  each warp folds its sub-chunk (rows of 32 lanes x 32 bytes, each
+//            lane's 32 bytes reduced to a literal bit mask) into a run
+//            summary; the CTA publishes the composition of its 8 warps;
+//   phase 2  the CTA composes the summaries of all preceding chunks (they
+//            never wait on later chunks, so this cannot deadlock) -> carry-in;
+//   phase 3  each warp re-reads its sub-chunk (L2-resident: P <= 0.2 n bytes),
+//            scans it and emits every ZRE byte at its final offset.
 // The dependency depth between chunks is one publication, not a chain.
 constexpr int kK3Threads = kScanThreads;
-constexpr int kK3Words = 8;                                 // 32 bytes per thread per row
-constexpr int kK3Seg = 4 * kK3Words;
-constexpr int kK3Row = kK3Threads * kK3Seg;                 // 8192 quartic bytes per row
+constexpr int kK3Seg = 32;                                   // bytes per lane per row
+constexpr int kK3WarpRow = 32 * kK3Seg;                      // 1 KiB per warp row
 
-// Load the segment [pos, min(pos+32, hi)) as words, padding with 121 (0x79).
+// Load [pos, min(pos+32, hi)) as 8 words, padding with 121 (0x79).
 __device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint64_t pos, uint64_t hi,
-                                        uint32_t (&w)[kK3Words]) {
+                                        uint32_t (&w)[8]) {
     const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
     if (len == kK3Seg && (reinterpret_cast<uintptr_t>(bytes + pos) & 15u) == 0) {
         const uint4 a = *reinterpret_cast<const uint4 *>(bytes + pos);
@@ -237,7 +241,7 @@ __device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint6
         w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
     } else {
 #pragma unroll
-        for (int k = 0; k < kK3Words; k++) {
+        for (int k = 0; k < 8; k++) {
             uint32_t x = 0;
 #pragma unroll
             for (int c = 0; c < 4; c++) {
@@ -254,6 +258,7 @@ __global__ void __launch_bounds__(kK3Threads)
 tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
                uint8_t *__restrict__ payload, Ctrl *ctrl, unsigned long long *states, tlc_header *hdr) {
     __shared__ unsigned long long s_warp[kScanWarps];
+    __shared__ unsigned long long s_wagg[kScanWarps];
     __shared__ unsigned int s_id;
     if (ctrl->status != TLC_OK) return;
     const uint64_t nchunks = (P + chunk - 1) / chunk;
@@ -261,15 +266,23 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     __syncthreads();
     const uint64_t b = s_id;
     if (b >= nchunks) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t lo = b * chunk, hi = tmin<uint64_t>(P, lo + chunk);
-    uint32_t seg[kK3Words];
+    const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
+    const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
+    uint32_t w[8];
 
-    // ---- phase 1: run summary of the chunk
-    RunSum agg = run_identity();
-    for (uint64_t row = lo; row < hi; row += kK3Row) {
-        const int len = load_seg(bytes, row + (uint64_t)kK3Seg * threadIdx.x, hi, seg);
-        agg = compose(agg, block_reduce_runs(segment_summary(seg, len), s_warp));
+    // ---- phase 1: run summary of the warp's sub-chunk, then of the chunk
+    RunSum wagg = run_identity();
+    for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
+        const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
+        wagg = compose(wagg, warp_reduce_runs(mask_summary(literal_mask(w), len)));
     }
+    if (lane == 0) s_wagg[warp] = pack(wagg);
+    __syncthreads();
+    RunSum agg = run_identity();
+#pragma unroll
+    for (int k = 0; k < kScanWarps; k++) agg = compose(agg, unpack(s_wagg[k]));
     if (threadIdx.x == 0) st_relaxed_u64(states + b, kReady | pack(agg));
 
     // ---- phase 2: carry-in = composition of all preceding chunk summaries
@@ -277,25 +290,28 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     const uint64_t per = (b + kK3Threads - 1) / kK3Threads;
     const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(b, i0 + per);
     for (uint64_t i = i0; i < i1; i++) part = compose(part, unpack(wait_ready(states + i) & ~kReady));
-    RunSum run = block_reduce_runs(part, s_warp);
+    const RunSum chunk_in = block_reduce_runs(part, s_warp);
     if (b == nchunks - 1 && threadIdx.x == 0) {
         uint64_t total;
         uint32_t carry;
-        run_eval(compose(run, agg), 0, total, carry);
+        run_eval(compose(chunk_in, agg), 0, total, carry);
         hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
     }
 
     // ---- phase 3: emission at the final payload offsets
-    for (uint64_t row = lo; row < hi; row += kK3Row) {
-        const uint64_t pos = row + (uint64_t)kK3Seg * threadIdx.x;
-        const int len = load_seg(bytes, pos, hi, seg);
+    RunSum run = chunk_in;
+    for (int k = 0; k < warp; k++) run = compose(run, unpack(s_wagg[k]));
+    for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
+        const uint64_t pos = row + (uint64_t)kK3Seg * lane;
+        const int len = load_seg(bytes, pos, whi, w);
+        const uint32_t mask = literal_mask(w);
         RunSum row_total;
-        const RunSum ex = block_excl_scan_runs(segment_summary(seg, len), s_warp, row_total);
+        const RunSum ex = warp_excl_scan_runs(mask_summary(mask, len), row_total);
         if (len > 0) {
             uint64_t off;
             uint32_t c;
             run_eval(compose(run, ex), 0, off, c);
-            segment_emit(seg, len, c, payload, off);
+            mask_emit(w, mask, len, c, payload, off);
             if (c > 0 && pos + len == P) payload[off] = run_code(c);
         }
         run = compose(run, row_total);
@@ -375,8 +391,8 @@ int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre
         KernelScope ks(kK3, st);
         if (!g_k3_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
-        const uint64_t rows = (P + kK3Row - 1) / kK3Row;
-        const uint64_t grid = tmin<uint64_t>(rows, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks)));
+        const uint64_t rows = (P + kScanWarps * kK3WarpRow - 1) / (kScanWarps * kK3WarpRow);
+        const uint64_t grid = tmax<uint64_t>(1, tmin<uint64_t>(rows, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
         const uint64_t chunk = ((P + grid - 1) / grid + kK3Seg - 1) / kK3Seg * kK3Seg;
         const uint64_t nch = (P + chunk - 1) / chunk;
         tlc_zre_kernel<<<(unsigned)nch, kK3Threads, 0, st>>>(w.bytes, P, chunk, payload, w.ctrl, w.states, hdr);

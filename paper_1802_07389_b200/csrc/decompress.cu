@@ -134,10 +134,11 @@ struct K5Smem {
 
 // Eq. 3, T_out = M * q, for a valid header (M finite and >= +0, enforced by
 // K4): M*(+1) = M, M*(-1) = -M, M*0 = +0 -- built from M's bit pattern.
+// lutv bit i = (digit_i != 1), bit 8+i = (digit_i == 0).
 __device__ __forceinline__ uint32_t trit_bits(uint32_t lutv, int i, uint32_t Mb) {
-    const uint32_t nz = (lutv >> i) & 1u;
-    const uint32_t neg = (lutv >> (8 + i)) & 1u;
-    return (0u - nz) & (Mb | (neg << 31));
+    const uint32_t nzm = (uint32_t)((int32_t)(lutv << (31 - i)) >> 31);
+    const uint32_t sgn = (lutv << (23 - i)) & 0x80000000u;
+    return (Mb | sgn) & nzm;
 }
 
 template <bool kVec, int kMode>
@@ -146,13 +147,13 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
                           float *__restrict__ out, const unsigned long long *__restrict__ seek) {
     __shared__ K5Smem sm;
     if (hdr->status != TLC_OK) return;
-    const float M = hdr->M;
-    const uint32_t Mb = __float_as_uint(M);
+    const uint32_t Mb = __float_as_uint(hdr->M);
     const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
     const uint64_t Z = hdr->payload_len;
     const uint64_t P = (n + 4) / 5;
     const uint64_t num_tiles = (P + kOutTile - 1) / kOutTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;   // word loads allowed
 
     // digit table: decoding step 1, "dividing a by a power of 3 and taking the
     // remainder", for the 243 byte values (partition 0 = a/81).
@@ -172,41 +173,50 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
     for (uint64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const uint64_t J0 = tile * kOutTile;
         const int tl = (int)tmin<uint64_t>(kOutTile, P - J0);
+        // valid positions of partition i in this tile: e = i*P + J0 + jl < n
+        int lim[5];
+        float *ob[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e0 = (uint64_t)i * P + J0;
+            lim[i] = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
+            ob[i] = out + e0;
+        }
         __syncthreads();   // previous tile's readers of sm.E are done (and the table is built)
         if (zre) {
             // pre-fill with 121: zero-run codes expand to 121s and need no further writes
             *reinterpret_cast<uint2 *>(sm.E + 8 * threadIdx.x) = make_uint2(0x79797979u, 0x79797979u);
             const unsigned long long sk = seek[tile];
             const uint64_t bi = sk >> 4;                      // payload byte covering J0
-            const uint32_t skip = (uint32_t)(sk & 15);        // J0 - (first position of that byte)
+            const int skip = (int)(sk & 15);                  // J0 - (first position of that byte)
             const uint64_t be = tile + 1 < num_tiles ? (seek[tile + 1] >> 4) : Z - 1;   // last byte needed
-            // thread owns window bytes [w0 + 8*tid, +8), w0 = bi rounded down to 4;
-            // the last thread also owns the 4 bytes after the 2048-byte window so
-            // that the <= 2048 bytes from bi on are always covered.
+            const int wl = (int)(be - bi) + 1;                // <= kOutTile + 1
+            // thread owns window bytes [8*tid, 8*tid+8) relative to w0 = bi rounded down to 4;
+            // the last thread also owns the 4 bytes after them so <= 2048 bytes from bi are covered
             const uint64_t w0 = bi & ~3ull;
-            const uint64_t zb = w0 + 8ull * threadIdx.x;
+            const int sh = (int)(bi - w0);
             const int nwords = threadIdx.x == kK5Threads - 1 ? 3 : 2;
             uint32_t wd[3] = {0, 0, 0};
 #pragma unroll
             for (int h = 0; h < 3; h++) {
-                const uint64_t a = zb + 4 * h;
                 if (h >= nwords) break;
-                if (a + 3 <= be) {
-                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + a));
+                const int r = 8 * threadIdx.x + 4 * h - sh;    // window offset of the word's first byte
+                if (pal && r >= 0 && r + 3 < wl) {
+                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + 2 * threadIdx.x + h);
                 } else {
                     uint32_t x = 0;
 #pragma unroll
                     for (int c = 0; c < 4; c++)
-                        if (a + c <= be) x |= (uint32_t)payload[a + c] << (8 * c);
+                        if (r + c >= 0 && r + c < wl) x |= (uint32_t)payload[bi + r + c] << (8 * c);
                     wd[h] = x;
                 }
             }
             uint32_t len[12], sum = 0;
 #pragma unroll
             for (int m = 0; m < 12; m++) {
+                const int r = 8 * threadIdx.x + m - sh;
                 const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-                const uint64_t a = zb + m;
-                len[m] = (m < 4 * nwords && a >= bi && a <= be) ? zre_len(b) : 0u;
+                len[m] = (m < 4 * nwords && r >= 0 && r < wl) ? zre_len(b) : 0u;
                 sum += len[m];
             }
             uint32_t x = sum;
@@ -220,8 +230,7 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
             uint32_t wofs = 0;
 #pragma unroll
             for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? sm.warp_sum[w] : 0u;
-            // position (relative to J0) of this thread's first byte
-            int p = (int)(wofs + x - sum) - (int)skip;
+            int p = (int)(wofs + x - sum) - skip;   // tile position of this thread's first byte
 #pragma unroll
             for (int m = 0; m < 12; m++) {
                 const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
@@ -238,31 +247,28 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
         __syncthreads();
 
         // ---- base-3 decode + dequantize, 4 consecutive quartic bytes per thread
+#pragma unroll 2
         for (int jl = 4 * threadIdx.x; jl < tl; jl += 4 * kK5Threads) {
             const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E + jl);
             uint32_t L[4];
 #pragma unroll
             for (int c = 0; c < 4; c++) L[c] = sm.lut[(w4 >> (8 * c)) & 0xffu];
-            const uint64_t j = J0 + jl;
 #pragma unroll
             for (int i = 0; i < 5; i++) {
-                const uint64_t e = (uint64_t)i * P + j;
-                float *o = out + e;
-                const bool full = kVec && (jl + 3 < tl) && (e + 3 < n);
+                float *o = ob[i] + jl;
                 if (kMode == TLC_MODE_OVERWRITE) {
-                    if (full) {
+                    if (kVec && jl + 3 < lim[i]) {
                         __stcs(reinterpret_cast<uint4 *>(o),
                                make_uint4(trit_bits(L[0], i, Mb), trit_bits(L[1], i, Mb),
                                           trit_bits(L[2], i, Mb), trit_bits(L[3], i, Mb)));
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if (jl + c < tl && e + c < n) o[c] = __uint_as_float(trit_bits(L[c], i, Mb));
+                            if (jl + c < lim[i]) o[c] = __uint_as_float(trit_bits(L[c], i, Mb));
                     }
                 } else {
-                    const uint32_t nz = ((L[0] | L[1] | L[2] | L[3]) >> i) & 1u;
-                    if (!nz) continue;                           // skip-zero: sector untouched (R16)
-                    if (full) {
+                    if ((((L[0] | L[1] | L[2] | L[3]) >> i) & 1u) == 0) continue;   // skip-zero (R16)
+                    if (kVec && jl + 3 < lim[i]) {
                         float4 v = *reinterpret_cast<float4 *>(o);
                         float *vv = reinterpret_cast<float *>(&v);
 #pragma unroll
@@ -272,7 +278,7 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if (jl + c < tl && e + c < n && ((L[c] >> i) & 1u))
+                            if (jl + c < lim[i] && ((L[c] >> i) & 1u))
                                 o[c] = __fadd_rn(o[c], __uint_as_float(trit_bits(L[c], i, Mb)));
                     }
                 }

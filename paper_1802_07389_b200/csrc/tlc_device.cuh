@@ -50,6 +50,13 @@ __device__ __forceinline__ float4 ld_stream4(const float4 *p) { return __ldcs(p)
 //   M >= 2^-125      -> q = sign(u) * [|u| >= M/2]; M/2 is exact, and
 //                       fl(u/M) >= 1/2  <=>  u >= M/2 exactly
 //   0 < M < 2^-125   -> q from the IEEE quotient __fdiv_rn(u, M)          (R4)
+// IEEE quotient path, out of line: only taken when M < 2^-125 (subnormal M/2),
+// which keeps the division's registers out of the streaming loops.
+static __device__ __noinline__ int quant_div(float u, float M) {
+    const float x = __fdiv_rn(u, M);
+    return (x >= 0.5f) - (x <= -0.5f);
+}
+
 struct Quant {
     float M, halfM;
     int mode;  // 0: zero, 1: compare, 2: divide
@@ -57,15 +64,21 @@ struct Quant {
         mode = (m == 0.0f) ? 0 : (m >= 2.350988701644575e-38f /* 2^-125 */ ? 1 : 2);
     }
     __device__ __forceinline__ int q(float u) const {
-        if (mode == 1) {
-            return fabsf(u) >= halfM ? (u > 0.0f ? 1 : -1) : 0;
-        } else if (mode == 2) {
-            float x = __fdiv_rn(u, M);
-            return (x >= 0.5f) - (x <= -0.5f);
-        }
+        if (mode == 1) return fabsf(u) >= halfM ? (u > 0.0f ? 1 : -1) : 0;
+        if (mode == 2) return quant_div(u, M);
         return 0;
     }
     // err = u - M*q (exact by Sterbenz when q != 0; u - (+0) == u otherwise)
+    __device__ __forceinline__ float residual(float u, int q) const {
+        return q == 0 ? u : __fsub_rn(u, q > 0 ? M : -M);
+    }
+};
+
+// The common regime (M >= 2^-125) only: the compare form of Eq. 2.
+struct QuantCmp {
+    float M, halfM;
+    __device__ __forceinline__ explicit QuantCmp(const Quant &Q) : M(Q.M), halfM(Q.halfM) {}
+    __device__ __forceinline__ int q(float u) const { return fabsf(u) >= halfM ? (u > 0.0f ? 1 : -1) : 0; }
     __device__ __forceinline__ float residual(float u, int q) const {
         return q == 0 ? u : __fsub_rn(u, q > 0 ? M : -M);
     }
@@ -217,11 +230,140 @@ __host__ __device__ __forceinline__ void segment_emit(const uint32_t (&w)[NW], i
     }
 }
 
+// ---------------------------------------------------------------- 32-byte segments as bit masks
+// The zero-run encoder only needs to know which quartic bytes are literals
+// (!= 121): a 32-byte segment becomes a 32-bit mask and its run summary and
+// emission follow from ctz/clz/popc over that mask.
+__host__ __device__ __forceinline__ uint32_t ctz32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return (uint32_t)(__ffs(x) - 1);
+#else
+    return (uint32_t)__builtin_ctz(x);
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t msb32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return 31u - (uint32_t)__clz(x);
+#else
+    return 31u - (uint32_t)__builtin_clz(x);
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t popc32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return (uint32_t)__popc(x);
+#else
+    return (uint32_t)__builtin_popcount(x);
+#endif
+}
+// bit c of the result = (byte c of w != 121)
+__host__ __device__ __forceinline__ uint32_t literal_nibble(uint32_t w) {
+#ifdef __CUDA_ARCH__
+    const uint32_t t = __vcmpne4(w, 0x79797979u) & 0x01010101u;
+#else
+    uint32_t t = 0;
+    for (int c = 0; c < 4; c++) t |= (uint32_t)(((w >> (8 * c)) & 0xffu) != kZeroGroup) << (8 * c);
+#endif
+    return (t * 0x01020408u) >> 24;   // gathers bits 0, 8, 16, 24 into bits 0..3
+}
+__host__ __device__ __forceinline__ uint32_t literal_mask(const uint32_t (&w)[8]) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) m |= literal_nibble(w[k]) << (4 * k);
+    return m;
+}
+
+// Run summary of the first len (1..32) bytes of a segment with literal mask `mask`.
+__host__ __device__ __forceinline__ RunSum mask_summary(uint32_t mask, int len) {
+    RunSum s = run_identity();
+    if (len <= 0) return s;
+    if (len < 32) mask &= (1u << len) - 1u;
+    if (mask == 0) {
+        s.v = (uint64_t)(len / (int)kMaxRun);
+        s.r0 = (uint32_t)(len % (int)kMaxRun);
+        return s;
+    }
+    const uint32_t lead = ctz32(mask), hi = msb32(mask);
+    const uint32_t T = (uint32_t)len - 1u - hi;                       // trailing run
+    uint32_t cnt = popc32(mask);                                       // literals
+    // inner runs between literals: a run of L (1..13) 121s costs one flush byte;
+    // runs of 14 or more (rare) are counted exactly below.
+    const uint32_t inner = hi > lead ? ((~mask) & (((2u << hi) - 1u) ^ ((2u << lead) - 1u))) : 0u;
+    uint32_t y = inner;
+    y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 6;               // bit set at runs >= 14
+    if (y == 0) {
+        cnt += popc32(mask & ~(mask << 1) & (mask - 1u));
+    } else {
+        uint32_t m = mask & (mask - 1u);
+        uint32_t prev = lead;
+        while (m) {
+            const uint32_t p = ctz32(m);
+            m &= m - 1u;
+            const uint32_t L = p - prev - 1u;
+            cnt += L / kMaxRun + (L % kMaxRun != 0);
+            prev = p;
+        }
+    }
+    cnt += T / kMaxRun + lead / kMaxRun;
+    s.mix = true;
+    s.v = cnt;
+    s.r0 = lead % kMaxRun;
+    s.tr = T % kMaxRun;
+    return s;
+}
+
+// Emit the ZRE bytes of the first len bytes of a segment entered with carry c
+// at payload offset `off`; on return c is the carry out and off the next offset.
+__host__ __device__ __forceinline__ void mask_emit(const uint32_t (&w)[8], uint32_t mask, int len,
+                                                   uint32_t &c, uint8_t *payload, uint64_t &off) {
+    if (len <= 0) return;
+    if (len < 32) mask &= (1u << len) - 1u;
+    int prev = -1;
+    while (mask) {
+        const int p = (int)ctz32(mask);
+        mask &= mask - 1u;
+        uint32_t total = (uint32_t)(p - prev - 1) + c;   // pending 121s before this literal
+        c = 0;
+        while (total >= kMaxRun) { payload[off++] = run_code(kMaxRun); total -= kMaxRun; }
+        if (total) payload[off++] = run_code(total);
+        payload[off++] = (uint8_t)byte_at(w, p);
+        prev = p;
+    }
+    uint32_t total = (uint32_t)(len - 1 - prev) + c;
+    while (total >= kMaxRun) { payload[off++] = run_code(kMaxRun); total -= kMaxRun; }
+    c = total;
+}
+
 __device__ __forceinline__ unsigned long long shfl_up64(unsigned long long v, int d) {
     return __shfl_up_sync(0xffffffffu, v, d);
 }
 __device__ __forceinline__ unsigned long long shfl_down64(unsigned long long v, int d) {
     return __shfl_down_sync(0xffffffffu, v, d);
+}
+
+// ---------------------------------------------------------------- warp-level helpers
+// lane l's item precedes lane l+1's
+__device__ __forceinline__ RunSum warp_reduce_runs(const RunSum &x) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long v = pack(x);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = shfl_down64(v, d);
+        if (lane + d < 32) v = pack(compose(unpack(v), unpack(o)));
+    }
+    return unpack(__shfl_sync(0xffffffffu, v, 0));
+}
+
+__device__ __forceinline__ RunSum warp_excl_scan_runs(const RunSum &x, RunSum &total) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long v = pack(x);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = shfl_up64(v, d);
+        if (lane >= d) v = pack(compose(unpack(y), unpack(v)));
+    }
+    total = unpack(__shfl_sync(0xffffffffu, v, 31));
+    const unsigned long long ex = shfl_up64(v, 1);
+    return lane == 0 ? run_identity() : unpack(ex);
 }
 
 // ---------------------------------------------------------------- block-level helpers

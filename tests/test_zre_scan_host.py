@@ -57,8 +57,8 @@ def _streams():
     yield np.array(parts, np.uint8)
 
 
-@pytest.mark.parametrize("threads", [1, 2, 3, 5, 32, 33, 256])
-def test_scan_matches_oracle_zre(sim, threads):
+@pytest.mark.parametrize("threads", [1, 2, 3, 8])
+def test_scan_matches_oracle_zre(sim, threads):  # threads = warps per CTA
     for i, B in enumerate(_streams()):
         ref = O.zre_encode(B)
         for nchunks in (1, 2, 3, 7, 64):
