@@ -182,7 +182,10 @@ __device__ __forceinline__ void quant_qe_groups(const float4 *__restrict__ t4, f
     }
 }
 
-__global__ void __launch_bounds__(kK2Threads, 3)
+#ifndef TLC_K2_MINB
+#define TLC_K2_MINB 3
+#endif
+__global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_vec_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
                         uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
     if (ctrl->status != TLC_OK) return;           // K1 raised NONFINITE / RANGE: err untouched
@@ -327,8 +330,7 @@ struct CompressWs {
     size_t memset_bytes;
 };
 
-static CompressWs carve_compress_ws(void *ws, uint64_t n) {
-    const uint64_t P = (n + 4) / 5;
+static CompressWs carve_compress_ws(void *ws) {
     const uint64_t tiles = (uint64_t)kMaxSms * 16;       // K3 chunk summaries
     CompressWs w;
     char *p = reinterpret_cast<char *>(ws);
@@ -354,7 +356,7 @@ static int g_k2_vec_blocks = 0, g_k2_sc_blocks = 0, g_k3_blocks = 0;
 int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
                     tlc_header *hdr, void *ws, cudaStream_t st) {
     const uint64_t P = (n + 4) / 5;
-    const CompressWs w = carve_compress_ws(ws, n);
+    const CompressWs w = carve_compress_ws(ws);
     const int sms = num_sms();
     if (cudaMemsetAsync(ws, 0, w.memset_bytes, st) != cudaSuccess) return TLC_ERR_CUDA;
 

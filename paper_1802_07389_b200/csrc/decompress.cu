@@ -18,9 +18,7 @@ namespace tlc {
 
 
 constexpr int kK5Threads = 256;
-constexpr int kOutTile = 2048;                             // quartic bytes per output tile
-
-constexpr unsigned long long kSumMask = (1ull << 62) - 1;
+constexpr int kOutTile = 4096;                             // quartic bytes per output tile
 
 __device__ __forceinline__ void raise_format(tlc_header *hdr) {
     atomicCAS(&hdr->status, (unsigned int)TLC_OK, (unsigned int)TLC_ERR_FORMAT);
@@ -126,20 +124,15 @@ tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64
 }
 
 // ============================================================== K5
+constexpr int kK5BytesPerThread = kOutTile / kK5Threads;   // 16 quartic bytes per thread per tile
+constexpr int kK5Words = kK5BytesPerThread / 4;
+
 struct K5Smem {
     alignas(16) uint8_t E[kOutTile];     // expanded quartic bytes of the tile
+    uint32_t V[5][256];                  // Eq. 3 output bits of partition i for byte value b
     uint16_t lut[256];                   // per byte: bit i = (digit_i != 1), bit 8+i = (digit_i == 0)
     unsigned int warp_sum[kK5Threads / 32];
 };
-
-// Eq. 3, T_out = M * q, for a valid header (M finite and >= +0, enforced by
-// K4): M*(+1) = M, M*(-1) = -M, M*0 = +0 -- built from M's bit pattern.
-// lutv bit i = (digit_i != 1), bit 8+i = (digit_i == 0).
-__device__ __forceinline__ uint32_t trit_bits(uint32_t lutv, int i, uint32_t Mb) {
-    const uint32_t nzm = (uint32_t)((int32_t)(lutv << (31 - i)) >> 31);
-    const uint32_t sgn = (lutv << (23 - i)) & 0x80000000u;
-    return (Mb | sgn) & nzm;
-}
 
 template <bool kVec, int kMode>
 __global__ void __launch_bounds__(kK5Threads)
@@ -147,7 +140,7 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
                           float *__restrict__ out, const unsigned long long *__restrict__ seek) {
     __shared__ K5Smem sm;
     if (hdr->status != TLC_OK) return;
-    const uint32_t Mb = __float_as_uint(hdr->M);
+    const float M = hdr->M;
     const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
     const uint64_t Z = hdr->payload_len;
     const uint64_t P = (n + 4) / 5;
@@ -155,8 +148,9 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;   // word loads allowed
 
-    // digit table: decoding step 1, "dividing a by a power of 3 and taking the
-    // remainder", for the 243 byte values (partition 0 = a/81).
+    // Decoding step 1, "dividing a by a power of 3 and taking the remainder"
+    // (P:514-515), tabulated for the 243 byte values, and Eq. 3,
+    // T_out = M * q, tabulated per partition: V[i][b] = M * (digit_i(b) - 1).
     for (int v = threadIdx.x; v < 256; v += kK5Threads) {
         uint32_t w = 0, r = v < 243 ? v : 121;
 #pragma unroll
@@ -165,6 +159,7 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
             r /= 3u;
             w |= (uint32_t)(d != 1) << i;
             w |= (uint32_t)(d == 0) << (8 + i);
+            sm.V[i][v] = __float_as_uint(__fmul_rn(M, (float)((int)d - 1)));
         }
         sm.lut[v] = (uint16_t)w;
     }
@@ -182,27 +177,31 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
             lim[i] = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
             ob[i] = out + e0;
         }
-        __syncthreads();   // previous tile's readers of sm.E are done (and the table is built)
+        __syncthreads();   // previous tile's readers of sm.E are done (and the tables are built)
         if (zre) {
             // pre-fill with 121: zero-run codes expand to 121s and need no further writes
-            *reinterpret_cast<uint2 *>(sm.E + 8 * threadIdx.x) = make_uint2(0x79797979u, 0x79797979u);
+            *reinterpret_cast<uint4 *>(sm.E + kK5BytesPerThread * threadIdx.x) =
+                make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
             const unsigned long long sk = seek[tile];
             const uint64_t bi = sk >> 4;                      // payload byte covering J0
             const int skip = (int)(sk & 15);                  // J0 - (first position of that byte)
             const uint64_t be = tile + 1 < num_tiles ? (seek[tile + 1] >> 4) : Z - 1;   // last byte needed
             const int wl = (int)(be - bi) + 1;                // <= kOutTile + 1
-            // thread owns window bytes [8*tid, 8*tid+8) relative to w0 = bi rounded down to 4;
-            // the last thread also owns the 4 bytes after them so <= 2048 bytes from bi are covered
+            // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
+            // to 4; the last thread also owns the next 4 bytes, so the <= kOutTile bytes
+            // from bi on are always covered
             const uint64_t w0 = bi & ~3ull;
             const int sh = (int)(bi - w0);
-            const int nwords = threadIdx.x == kK5Threads - 1 ? 3 : 2;
-            uint32_t wd[3] = {0, 0, 0};
+            constexpr int NW = kK5Words + 1;
+            const int nwords = threadIdx.x == kK5Threads - 1 ? NW : kK5Words;
+            uint32_t wd[NW];
 #pragma unroll
-            for (int h = 0; h < 3; h++) {
-                if (h >= nwords) break;
-                const int r = 8 * threadIdx.x + 4 * h - sh;    // window offset of the word's first byte
+            for (int h = 0; h < NW; h++) {
+                wd[h] = 0;
+                if (h >= nwords) continue;
+                const int r = kK5BytesPerThread * threadIdx.x + 4 * h - sh;   // window offset of the word
                 if (pal && r >= 0 && r + 3 < wl) {
-                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + 2 * threadIdx.x + h);
+                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + kK5Words * threadIdx.x + h);
                 } else {
                     uint32_t x = 0;
 #pragma unroll
@@ -211,10 +210,10 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
                     wd[h] = x;
                 }
             }
-            uint32_t len[12], sum = 0;
+            uint32_t len[4 * NW], sum = 0;
 #pragma unroll
-            for (int m = 0; m < 12; m++) {
-                const int r = 8 * threadIdx.x + m - sh;
+            for (int m = 0; m < 4 * NW; m++) {
+                const int r = kK5BytesPerThread * threadIdx.x + m - sh;
                 const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
                 len[m] = (m < 4 * nwords && r >= 0 && r < wl) ? zre_len(b) : 0u;
                 sum += len[m];
@@ -232,7 +231,7 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
             for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? sm.warp_sum[w] : 0u;
             int p = (int)(wofs + x - sum) - skip;   // tile position of this thread's first byte
 #pragma unroll
-            for (int m = 0; m < 12; m++) {
+            for (int m = 0; m < 4 * NW; m++) {
                 const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
                 if (len[m] == 1 && p >= 0 && p < tl) sm.E[p] = (uint8_t)b;   // literal byte
                 p += (int)len[m];
@@ -246,40 +245,49 @@ tlc_expand_dequant_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, 
         }
         __syncthreads();
 
-        // ---- base-3 decode + dequantize, 4 consecutive quartic bytes per thread
-#pragma unroll 2
-        for (int jl = 4 * threadIdx.x; jl < tl; jl += 4 * kK5Threads) {
+        // ---- base-3 decode + dequantize, 4 consecutive quartic bytes per step
+#pragma unroll
+        for (int k = 0; k < kK5BytesPerThread / 4; k++) {
+            const int jl = 4 * threadIdx.x + 4 * kK5Threads * k;
+            if (jl >= tl) break;
             const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E + jl);
-            uint32_t L[4];
+            const uint32_t b0 = w4 & 0xffu, b1 = (w4 >> 8) & 0xffu, b2 = (w4 >> 16) & 0xffu, b3 = w4 >> 24;
+            if (kMode == TLC_MODE_OVERWRITE) {
+                const bool zero4 = w4 == 0x79797979u;   // four all-zero groups: 20 x +0
 #pragma unroll
-            for (int c = 0; c < 4; c++) L[c] = sm.lut[(w4 >> (8 * c)) & 0xffu];
-#pragma unroll
-            for (int i = 0; i < 5; i++) {
-                float *o = ob[i] + jl;
-                if (kMode == TLC_MODE_OVERWRITE) {
+                for (int i = 0; i < 5; i++) {
+                    float *o = ob[i] + jl;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if (!zero4) v = make_uint4(sm.V[i][b0], sm.V[i][b1], sm.V[i][b2], sm.V[i][b3]);
                     if (kVec && jl + 3 < lim[i]) {
-                        __stcs(reinterpret_cast<uint4 *>(o),
-                               make_uint4(trit_bits(L[0], i, Mb), trit_bits(L[1], i, Mb),
-                                          trit_bits(L[2], i, Mb), trit_bits(L[3], i, Mb)));
+                        __stcs(reinterpret_cast<uint4 *>(o), v);
                     } else {
+                        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if (jl + c < lim[i]) o[c] = __uint_as_float(trit_bits(L[c], i, Mb));
+                            if (jl + c < lim[i]) o[c] = __uint_as_float(vv[c]);
                     }
-                } else {
-                    if ((((L[0] | L[1] | L[2] | L[3]) >> i) & 1u) == 0) continue;   // skip-zero (R16)
+                }
+            } else {
+                if (w4 == 0x79797979u) continue;         // skip-zero: sectors untouched (R16)
+                const uint32_t L[4] = {sm.lut[b0], sm.lut[b1], sm.lut[b2], sm.lut[b3]};
+                const uint32_t bb[4] = {b0, b1, b2, b3};
+#pragma unroll
+                for (int i = 0; i < 5; i++) {
+                    if ((((L[0] | L[1] | L[2] | L[3]) >> i) & 1u) == 0) continue;
+                    float *o = ob[i] + jl;
                     if (kVec && jl + 3 < lim[i]) {
                         float4 v = *reinterpret_cast<float4 *>(o);
                         float *vv = reinterpret_cast<float *>(&v);
 #pragma unroll
                         for (int c = 0; c < 4; c++)
-                            if ((L[c] >> i) & 1u) vv[c] = __fadd_rn(vv[c], __uint_as_float(trit_bits(L[c], i, Mb)));
+                            if ((L[c] >> i) & 1u) vv[c] = __fadd_rn(vv[c], __uint_as_float(sm.V[i][bb[c]]));
                         *reinterpret_cast<float4 *>(o) = v;
                     } else {
 #pragma unroll
                         for (int c = 0; c < 4; c++)
                             if (jl + c < lim[i] && ((L[c] >> i) & 1u))
-                                o[c] = __fadd_rn(o[c], __uint_as_float(trit_bits(L[c], i, Mb)));
+                                o[c] = __fadd_rn(o[c], __uint_as_float(sm.V[i][bb[c]]));
                     }
                 }
             }
