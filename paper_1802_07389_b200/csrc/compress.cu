@@ -183,7 +183,7 @@ __device__ __forceinline__ void quant_qe_groups(const float4 *__restrict__ t4, f
 }
 
 #ifndef TLC_K2_MINB
-#define TLC_K2_MINB 3
+#define TLC_K2_MINB 2
 #endif
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_vec_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
@@ -275,11 +275,13 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
     uint32_t w[8];
 
-    // ---- phase 1: run summary of the warp's sub-chunk, then of the chunk
+    // ---- phase 1: run summary of the warp's sub-chunk (one per 1 KiB row), then of the chunk
     RunSum wagg = run_identity();
     for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
         const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
-        wagg = compose(wagg, warp_reduce_runs(mask_summary(literal_mask(w), len)));
+        const uint32_t mask = literal_mask(w);
+        const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+        wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
     }
     if (lane == 0) s_wagg[warp] = pack(wagg);
     __syncthreads();
@@ -302,22 +304,32 @@ tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
     }
 
     // ---- phase 3: emission at the final payload offsets
-    RunSum run = chunk_in;
-    for (int k = 0; k < warp; k++) run = compose(run, unpack(s_wagg[k]));
+    RunSum before = chunk_in;
+    for (int k = 0; k < warp; k++) before = compose(before, unpack(s_wagg[k]));
+    uint64_t off;
+    uint32_t carry;
+    run_eval(before, 0, off, carry);              // payload offset and carry at the sub-chunk start
     for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
         const uint64_t pos = row + (uint64_t)kK3Seg * lane;
         const int len = load_seg(bytes, pos, whi, w);
         const uint32_t mask = literal_mask(w);
-        RunSum row_total;
-        const RunSum ex = warp_excl_scan_runs(mask_summary(mask, len), row_total);
-        if (len > 0) {
-            uint64_t off;
-            uint32_t c;
-            run_eval(compose(run, ex), 0, off, c);
-            mask_emit(w, mask, len, c, payload, off);
-            if (c > 0 && pos + len == P) payload[off] = run_code(c);
+        const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+        const WarpRow r = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
+        uint32_t ex = r.count;                    // exclusive prefix of the lane counts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
+            if (lane >= d) ex += y;
         }
-        run = compose(run, row_total);
+        ex -= r.count;
+        if (len > 0) {
+            uint64_t o = off + ex;
+            uint32_t c = r.carry_in;
+            mask_emit(w, mask, len, c, payload, o);
+            if (c > 0 && pos + len == P) payload[o] = run_code(c);
+        }
+        off += r.row_count;
+        carry = r.carry_out;
     }
 }
 

@@ -366,6 +366,79 @@ __device__ __forceinline__ RunSum warp_excl_scan_runs(const RunSum &x, RunSum &t
     return lane == 0 ? run_identity() : unpack(ex);
 }
 
+// ---------------------------------------------------------------- warp rows of 32 x 32 bytes
+// A warp row: lane l holds the bytes [32 l, 32 l + len_l) of a row (len_l = 32
+// except at the end of a stream), reduced to its literal mask.  The carry a
+// lane enters with is fixed by where the last literal before it sits (or by the
+// row's incoming carry c_row if there is none), so per-lane carries need one
+// ballot and one shuffle instead of a scan over the run monoid.  The three
+// formulas below are __host__ __device__ so tests/native can drive them.
+
+// carry entering lane `lane`; lp = row position of the last literal before it
+__host__ __device__ __forceinline__ uint32_t lane_carry_in(uint32_t lane, bool has_before, uint32_t lp,
+                                                           uint32_t c_row) {
+    return (has_before ? (32u * lane - lp - 1u) : (c_row + 32u * lane)) % kMaxRun;
+}
+// carry leaving a row of row_len bytes; lp_all = position of its last literal
+__host__ __device__ __forceinline__ uint32_t row_carry_out(bool any, uint32_t lp_all, uint32_t c_row,
+                                                           uint32_t row_len) {
+    return (any ? (row_len - lp_all - 1u) : (c_row + row_len)) % kMaxRun;
+}
+// run summary of a row from its count and carry-out at c_row = 0 and its leading run
+__host__ __device__ __forceinline__ RunSum row_summary(bool any, uint32_t lead, uint32_t count0,
+                                                       uint32_t carry_out0, uint32_t row_len) {
+    RunSum s = run_identity();
+    if (!any) {
+        s.v = row_len / kMaxRun;
+        s.r0 = row_len % kMaxRun;
+        return s;
+    }
+    s.mix = true;
+    s.r0 = lead % kMaxRun;
+    s.v = count0 - (s.r0 > 0);             // count(c) = v + ceil((c + r0)/14)
+    s.tr = carry_out0;
+    return s;
+}
+
+struct WarpRow {
+    uint32_t carry_in;    // this lane's incoming carry
+    uint32_t count;       // ZRE bytes this lane emits (given carry_in)
+    uint32_t row_count;   // all lanes: ZRE bytes the whole row emits
+    uint32_t carry_out;   // all lanes: carry leaving the row
+    uint32_t mixbal;      // lanes holding a literal
+};
+
+__device__ __forceinline__ WarpRow warp_row(uint32_t mask, int len, const RunSum &lane_sum, uint32_t c_row,
+                                            uint32_t row_len) {
+    const uint32_t lane = threadIdx.x & 31;
+    WarpRow r;
+    r.mixbal = __ballot_sync(0xffffffffu, mask != 0);
+    const uint32_t lastpos = 32u * lane + (mask ? msb32(mask) : 0u);
+    const uint32_t before = r.mixbal & ((1u << lane) - 1u);
+    const uint32_t lp = __shfl_sync(0xffffffffu, lastpos, before ? (int)msb32(before) : 0);
+    r.carry_in = lane_carry_in(lane, before != 0, lp, c_row);
+    uint64_t cnt;
+    uint32_t co;
+    run_eval(lane_sum, r.carry_in, cnt, co);
+    r.count = len > 0 ? (uint32_t)cnt : 0u;
+    uint32_t tot = r.count;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+    r.row_count = tot;
+    const uint32_t lp_all = __shfl_sync(0xffffffffu, lastpos, r.mixbal ? (int)msb32(r.mixbal) : 0);
+    r.carry_out = row_carry_out(r.mixbal != 0, lp_all, c_row, row_len);
+    return r;
+}
+
+// Run summary of a whole warp row (as a function of its incoming carry).
+__device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const RunSum &lane_sum,
+                                                   uint32_t row_len) {
+    const WarpRow r = warp_row(mask, len, lane_sum, 0u, row_len);
+    const uint32_t k0 = r.mixbal ? ctz32(r.mixbal) : 0u;
+    const uint32_t lead = __shfl_sync(0xffffffffu, mask ? ctz32(mask) : 0u, (int)k0) + 32u * k0;
+    return row_summary(r.mixbal != 0, lead, r.row_count, r.carry_out, row_len);
+}
+
 // ---------------------------------------------------------------- block-level helpers
 // (blockDim.x == 256, 8 warps; thread t's item precedes thread t+1's)
 constexpr int kScanThreads = 256;

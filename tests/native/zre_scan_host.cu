@@ -1,11 +1,12 @@
 // Host-only harness (no GPU): drives the device-side ZRE building blocks of
 // paper_1802_07389_b200/csrc/tlc_device.cuh (literal_mask, mask_summary,
-// mask_emit, compose, run_eval -- all __host__ __device__) through the same
-// decomposition as the K3 kernel (compress.cu): `nchunks` contiguous chunks,
-// each split into `warps` sub-chunks scanned in rows of 32 lanes x 32 bytes;
-// in-order tree reductions (phase 1), the carry-in composed from per-thread
-// partial compositions of the preceding chunk summaries (phase 2), per-row
-// Hillis-Steele exclusive scans and emission at final offsets (phase 3).
+// mask_emit, lane_carry_in, row_carry_out, row_summary, compose, run_eval --
+// all __host__ __device__) through the same decomposition as the K3 kernel
+// (compress.cu): `nchunks` contiguous chunks, each split into `warps`
+// sub-chunks scanned in warp rows of 32 lanes x 32 bytes (ballots and shuffles
+// emulated serially); phase 1 composes row summaries, phase 2 composes the
+// preceding chunk summaries from per-thread partials, phase 3 tracks
+// (offset, carry) across rows and emits at the final offsets.
 // tests/test_zre_scan_host.py compares the output with the oracle's ZRE.
 #include <algorithm>
 #include <cstdint>
@@ -34,6 +35,48 @@ int seg_at(const uint8_t *B, uint64_t pos, uint64_t hi, uint32_t (&w)[8]) {
     }
     return len;
 }
+
+struct Row {
+    uint32_t w[LANES][8], mask[LANES];
+    int len[LANES];
+    RunSum ls[LANES];
+    uint32_t carry_in[LANES], count[LANES], row_count, carry_out, row_len;
+    bool any;
+    uint32_t lead;
+};
+
+// serial emulation of warp_row (ballot + shuffles)
+void warp_row_host(Row &r, uint32_t c_row) {
+    uint32_t mixbal = 0, lastpos[LANES];
+    for (int l = 0; l < LANES; l++) {
+        mixbal |= (uint32_t)(r.mask[l] != 0) << l;
+        lastpos[l] = 32u * l + (r.mask[l] ? msb32(r.mask[l]) : 0u);
+    }
+    r.row_count = 0;
+    for (int l = 0; l < LANES; l++) {
+        const uint32_t before = mixbal & ((1u << l) - 1u);
+        const uint32_t lp = lastpos[before ? msb32(before) : 0];
+        r.carry_in[l] = lane_carry_in(l, before != 0, lp, c_row);
+        uint64_t cnt;
+        uint32_t co;
+        run_eval(r.ls[l], r.carry_in[l], cnt, co);
+        r.count[l] = r.len[l] > 0 ? (uint32_t)cnt : 0u;
+        r.row_count += r.count[l];
+    }
+    r.any = mixbal != 0;
+    r.carry_out = row_carry_out(r.any, lastpos[r.any ? msb32(mixbal) : 0], c_row, r.row_len);
+    const uint32_t k0 = r.any ? ctz32(mixbal) : 0u;
+    r.lead = (r.mask[k0] ? ctz32(r.mask[k0]) : 0u) + 32u * k0;
+}
+
+void load_row(const uint8_t *B, uint64_t row, uint64_t whi, Row &r) {
+    r.row_len = (uint32_t)std::min<uint64_t>((uint64_t)LANES * SEG, whi - row);
+    for (int l = 0; l < LANES; l++) {
+        r.len[l] = seg_at(B, row + (uint64_t)SEG * l, whi, r.w[l]);
+        r.mask[l] = literal_mask(r.w[l]);
+        r.ls[l] = mask_summary(r.mask[l], r.len[l]);
+    }
+}
 }  // namespace
 
 extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out) {
@@ -48,6 +91,7 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
         wlo = std::min(hi, lo + w * sub);
         whi = std::min(hi, wlo + sub);
     };
+    static Row r;
     for (uint64_t b = 0; b < nch; b++) {                 // phase 1
         RunSum a = run_identity();
         for (int w = 0; w < warps; w++) {
@@ -55,13 +99,9 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
             bounds(b, w, wlo, whi);
             RunSum x = run_identity();
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
-                std::vector<RunSum> v(LANES);
-                for (int l = 0; l < LANES; l++) {
-                    uint32_t s[8];
-                    const int len = seg_at(B, row + (uint64_t)SEG * l, whi, s);
-                    v[l] = mask_summary(literal_mask(s), len);
-                }
-                x = compose(x, tree_reduce(v));
+                load_row(B, row, whi, r);
+                warp_row_host(r, 0);
+                x = compose(x, row_summary(r.any, r.lead, r.row_count, r.carry_out, r.row_len));
             }
             wagg[b][w] = x;
             a = compose(a, x);
@@ -83,38 +123,28 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
             total = cnt + (carry > 0);
         }
         for (int w = 0; w < warps; w++) {                  // phase 3
-            RunSum run = chunk_in;
-            for (int k = 0; k < w; k++) run = compose(run, wagg[b][k]);
+            RunSum before = chunk_in;
+            for (int k = 0; k < w; k++) before = compose(before, wagg[b][k]);
+            uint64_t off;
+            uint32_t carry;
+            run_eval(before, 0, off, carry);
             uint64_t wlo, whi;
             bounds(b, w, wlo, whi);
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
-                std::vector<RunSum> v(LANES);
-                std::vector<std::vector<uint32_t>> segs(LANES, std::vector<uint32_t>(8));
-                std::vector<int> lens(LANES);
+                load_row(B, row, whi, r);
+                warp_row_host(r, carry);
+                uint32_t ex = 0;
                 for (int l = 0; l < LANES; l++) {
-                    uint32_t s[8];
-                    lens[l] = seg_at(B, row + (uint64_t)SEG * l, whi, s);
-                    std::memcpy(segs[l].data(), s, sizeof(s));
-                    v[l] = mask_summary(literal_mask(s), lens[l]);
+                    if (r.len[l] > 0) {
+                        uint64_t o = off + ex;
+                        uint32_t c = r.carry_in[l];
+                        mask_emit(r.w[l], r.mask[l], r.len[l], c, out, o);
+                        if (c > 0 && row + (uint64_t)SEG * l + r.len[l] == P) out[o++] = run_code(c);
+                    }
+                    ex += r.count[l];
                 }
-                std::vector<RunSum> incl(v);
-                for (int d = 1; d < LANES; d <<= 1) {
-                    std::vector<RunSum> nx(incl);
-                    for (int l = d; l < LANES; l++) nx[l] = compose(incl[l - d], incl[l]);
-                    incl.swap(nx);
-                }
-                for (int l = 0; l < LANES; l++) {
-                    if (lens[l] <= 0) continue;
-                    const RunSum ex = l == 0 ? run_identity() : incl[l - 1];
-                    uint64_t off;
-                    uint32_t c;
-                    run_eval(compose(run, ex), 0, off, c);
-                    uint32_t s[8];
-                    std::memcpy(s, segs[l].data(), sizeof(s));
-                    mask_emit(s, literal_mask(s), lens[l], c, out, off);
-                    if (c > 0 && row + (uint64_t)SEG * l + lens[l] == P) out[off++] = run_code(c);
-                }
-                run = compose(run, incl[LANES - 1]);
+                off += r.row_count;
+                carry = r.carry_out;
             }
         }
     }
