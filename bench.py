@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the ResNet-110 (configs[1]) side measurement")
     ap.add_argument("--e2e-steps", type=int, default=10)
     return ap.parse_args()
 
@@ -196,6 +197,52 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ C2: ResNet-110 set
+def measure_resnet110(T, dev, s, steps=200, warmup=10):
+    """BASELINE configs[1]: the 110 per-layer ResNet-110 gradient tensors (1,719,856 values),
+    compress + decompress through the batched launches, captured in one CUDA graph."""
+    import torch
+
+    import synth
+
+    sizes = synth.RESNET110_SIZES
+    mus = synth.layer_means(sizes, 2, 110)
+    tsets = [[torch.from_numpy(synth.layer_gradient(n, mus[k], 2, 0, k, step)).to(dev)
+              for k, n in enumerate(sizes)] for step in range(2)]
+    outs = [torch.empty(n, dtype=torch.float32, device=dev) for n in sizes]
+    ctx = T.TensorSet(sizes, dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for k in range(warmup):                     # error feedback reaches steady state
+            ctx.compress(tsets[k % 2], s, True, stream)
+            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream)
+    torch.cuda.synchronize(dev)
+    graphs = []
+    for k in range(2):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            ctx._cdesc = None
+            ctx.compress(tsets[k], s, True, stream)
+            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream)
+        graphs.append(g)
+    torch.cuda.synchronize(dev)
+    l0 = T.tlc_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(steps):
+        graphs[k % 2].replay()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    N = sum(sizes)
+    Z = sum(h["payload_len"] for h in ctx.headers())
+    return {"workload": "C2: ResNet-110 gradient set, 110 tensors, 1,719,856 values, batched K6/K7 "
+                        "launches in a CUDA graph, error feedback carried", "s": s,
+            "value": 4.0 * N / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+            "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 2,
+            "host_launch_calls_during_replay": T.tlc_launch_count() - l0}
+
+
 # ------------------------------------------------------------------ the GPU leg
 def run_tlc(args):
     import numpy as np
@@ -328,6 +375,10 @@ def run_tlc(args):
                "ms_per_step": ems / E,
                "what": "pinned host t -> HBM, tlc_compress, tlc_decompress, HBM -> pinned host out"}
 
+    c2 = None
+    if rank == 0 and not args.no_c2:
+        c2 = [measure_resnet110(T, dev, sv) for sv in (1.0, 1.75, 1.9)]
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = oracle_roundtrips(args.cpu_sample, s, zre, seconds=args.cpu_seconds)
@@ -352,6 +403,7 @@ def run_tlc(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
+            "c2_resnet110": c2,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

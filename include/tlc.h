@@ -132,6 +132,33 @@ int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *o
                    int mode, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Batched small tensors (SURVEY 8(a) "small-tensor regime"; BASELINE configs[1],
+ * the 110 per-layer gradient tensors of ResNet-110).  One kernel launch
+ * compresses (decompresses) a whole list of independent tensors, one CTA per
+ * tensor, each with its own error buffer, payload and header -- the same
+ * per-tensor operation and results as tlc_compress / tlc_decompress.
+ *
+ * `descs` is a DEVICE array of `count` descriptors (so the call can be captured
+ * in a CUDA graph).  Every tensor must have 1 <= n <= tlc_batched_max_elements();
+ * a tensor violating that gets hdr->status = TLC_ERR_ARG (compress) or
+ * TLC_ERR_FORMAT (decompress) on the device and is otherwise skipped.
+ * Fields used by compress: t, err, payload (capacity >= ceil(n/5)), hdr, n.
+ * Fields used by decompress: payload, hdr, out, n (mode as tlc_decompress).
+ */
+typedef struct tlc_tensor_desc {
+    const float *t;
+    float *err;
+    float *out;
+    uint8_t *payload;
+    tlc_header *hdr;
+    uint64_t n;
+} tlc_tensor_desc;
+
+uint64_t tlc_batched_max_elements(void);
+int tlc_compress_batched(int count, const tlc_tensor_desc *descs, float s, int use_zre, void *stream);
+int tlc_decompress_batched(int count, const tlc_tensor_desc *descs, int mode, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation (host-side, not part of the method).
  *
  * tlc_launch_count: number of kernels this library has launched in the

@@ -46,6 +46,9 @@ def _load():
         "tlc_decompress_workspace_bytes": (SZ, [U64]),
         "tlc_compress": (I, [P, P, U64, F, I, P, U64, P, P, SZ, P]),
         "tlc_decompress": (I, [P, P, U64, P, I, P, SZ, P]),
+        "tlc_batched_max_elements": (U64, []),
+        "tlc_compress_batched": (I, [I, P, F, I, P]),
+        "tlc_decompress_batched": (I, [I, P, I, P]),
         "tlc_launch_count": (ctypes.c_ulonglong, []),
         "tlc_prof_enable": (None, [I]),
         "tlc_prof_collect": (I, [P, I]),
@@ -173,6 +176,93 @@ def tlc_decompress(payload: torch.Tensor, hdr: torch.Tensor, n: int, out: torch.
     if rc != TLC_OK:
         raise TlcError(rc, "tlc_decompress")
     return out
+
+
+# ------------------------------------------------------------------ batched small tensors
+DESC_BYTES = 48   # struct tlc_tensor_desc: t, err, out, payload, hdr (pointers), n (uint64)
+
+
+def tlc_batched_max_elements() -> int:
+    return int(_lib.tlc_batched_max_elements())
+
+
+def pack_descs(rows, device) -> torch.Tensor:
+    """rows: iterable of (t, err, out, payload, hdr, n) with tensors or None -> a device
+    array of struct tlc_tensor_desc (uint8 tensor)."""
+    import struct
+
+    buf = bytearray()
+    for t, e, o, pl, h, n in rows:
+        ptr = [x.data_ptr() if isinstance(x, torch.Tensor) else int(x or 0) for x in (t, e, o, pl, h)]
+        buf += struct.pack("<QQQQQQ", *ptr, int(n))
+    host = torch.frombuffer(buf if buf else bytearray(DESC_BYTES), dtype=torch.uint8)
+    return host.to(device)
+
+
+def tlc_compress_batched(descs: torch.Tensor, count: int, s: float, use_zre: bool = True, stream=None):
+    _check_dev("descs", descs, torch.uint8)
+    rc = _lib.tlc_compress_batched(int(count), descs.data_ptr(), ctypes.c_float(s), int(bool(use_zre)),
+                                   _stream_ptr(stream))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_compress_batched")
+
+
+def tlc_decompress_batched(descs: torch.Tensor, count: int, mode: int = TLC_MODE_OVERWRITE, stream=None):
+    _check_dev("descs", descs, torch.uint8)
+    rc = _lib.tlc_decompress_batched(int(count), descs.data_ptr(), int(mode), _stream_ptr(stream))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_decompress_batched")
+
+
+class TensorSet:
+    """Compression contexts for a list of tensors (one error buffer, payload and
+    header each -- the paper's per-tensor contexts).  Tensors up to
+    tlc_batched_max_elements() go through one batched launch; larger ones through
+    tlc_compress / tlc_decompress.  Marshalling only: all arithmetic is on the GPU."""
+
+    def __init__(self, sizes, device=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device, self.sizes = dev, [int(n) for n in sizes]
+        self.errs = [torch.zeros(n, dtype=torch.float32, device=dev) for n in self.sizes]
+        self.payloads = [torch.empty(max(1, tlc_max_payload_bytes(n)), dtype=torch.uint8, device=dev)
+                         for n in self.sizes]
+        self.hdrs = torch.zeros(len(self.sizes), HEADER_BYTES, dtype=torch.uint8, device=dev)
+        lim = tlc_batched_max_elements()
+        self.small = [i for i, n in enumerate(self.sizes) if n <= lim]
+        self.large = [i for i, n in enumerate(self.sizes) if n > lim]
+        self._cdesc = None
+        self._dkey = None
+
+    def compress(self, ts, s: float, use_zre: bool = True, stream=None):
+        if self._cdesc is None or self._cdesc[1] is not ts:
+            rows = [(ts[i], self.errs[i], None, self.payloads[i], self.hdrs[i], self.sizes[i]) for i in self.small]
+            self._cdesc = (pack_descs(rows, self.device), ts)
+        if self.small:
+            tlc_compress_batched(self._cdesc[0], len(self.small), s, use_zre, stream)
+        for i in self.large:
+            tlc_compress(ts[i], self.errs[i], s, use_zre, self.payloads[i], self.hdrs[i], stream=stream)
+
+    def decompress(self, outs, mode: int = TLC_MODE_OVERWRITE, stream=None, payloads=None, hdrs=None):
+        payloads = self.payloads if payloads is None else payloads
+        hdrs = self.hdrs if hdrs is None else hdrs
+        key = (id(outs), id(payloads), id(hdrs))
+        if self._dkey != key:
+            rows = [(None, None, outs[i], payloads[i], hdrs[i], self.sizes[i]) for i in self.small]
+            self._ddesc, self._dkey = pack_descs(rows, self.device), key
+        if self.small:
+            tlc_decompress_batched(self._ddesc, len(self.small), mode, stream)
+        for i in self.large:
+            tlc_decompress(payloads[i], hdrs[i], self.sizes[i], outs[i], mode, stream=stream)
+
+    def headers(self):
+        import struct
+
+        raw = self.hdrs.cpu().numpy().tobytes()
+        out = []
+        for k in range(len(self.sizes)):
+            M, flags, n, plen, status, _ = struct.unpack("<fIQQII", raw[32 * k: 32 * k + 32])
+            out.append({"M": M, "flags": flags, "n": n, "payload_len": plen, "status": status})
+        return out
 
 
 # ------------------------------------------------------------------ instrumentation

@@ -20,11 +20,6 @@ namespace tlc {
 constexpr int kK5Threads = 256;
 constexpr int kOutTile = 4096;                             // quartic bytes per output tile
 
-__device__ __forceinline__ void raise_format(tlc_header *hdr) {
-    atomicCAS(&hdr->status, (unsigned int)TLC_OK, (unsigned int)TLC_ERR_FORMAT);
-}
-
-__device__ __forceinline__ uint32_t zre_len(uint32_t b) { return b >= kFirstRunCode ? b - 241u : 1u; }
 
 // ============================================================== K4
 // Same chunked single-pass scan as K3 (compress.cu), over the sum monoid of
@@ -62,10 +57,7 @@ tlc_zre_scan_kernel(const uint8_t *__restrict__ payload, tlc_header *hdr, uint64
     const unsigned int status = hdr->status;
     const uint64_t Z = hdr->payload_len;
     const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
-    // M = max|u| * s is finite and >= +0 (Eq. 1, R6); anything else is malformed (R21)
-    const uint32_t Mb = __float_as_uint(hdr->M);
-    const bool valid = status == TLC_OK && hdr->n == n && Z <= P && Z >= 1 && (zre || Z == P) &&
-                       (Mb >> 31) == 0 && Mb < 0x7f800000u;
+    const bool valid = header_valid(hdr, n);
     if (!valid) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && status == TLC_OK) raise_format(hdr);
         return;

@@ -325,7 +325,10 @@ __host__ __device__ __forceinline__ void mask_emit(const uint32_t (&w)[8], uint3
         c = 0;
         while (total >= kMaxRun) { payload[off++] = run_code(kMaxRun); total -= kMaxRun; }
         if (total) payload[off++] = run_code(total);
-        payload[off++] = (uint8_t)byte_at(w, p);
+        uint32_t word = w[0];                    // select, not a dynamic index: w stays in registers
+#pragma unroll
+        for (int k = 1; k < 8; k++) word = (k == (p >> 2)) ? w[k] : word;
+        payload[off++] = (uint8_t)(word >> (8 * (p & 3)));
         prev = p;
     }
     uint32_t total = (uint32_t)(len - 1 - prev) + c;
@@ -437,6 +440,25 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
     const uint32_t k0 = r.mixbal ? ctz32(r.mixbal) : 0u;
     const uint32_t lead = __shfl_sync(0xffffffffu, mask ? ctz32(mask) : 0u, (int)k0) + 32u * k0;
     return row_summary(r.mixbal != 0, lead, r.row_count, r.carry_out, row_len);
+}
+
+// ---------------------------------------------------------------- decoder helpers
+__device__ __forceinline__ void raise_format(tlc_header *hdr) {
+    atomicCAS(&hdr->status, (unsigned int)TLC_OK, (unsigned int)TLC_ERR_FORMAT);
+}
+
+// expansion length of a payload byte (inverse of P:545-546)
+__host__ __device__ __forceinline__ uint32_t zre_len(uint32_t b) { return b >= kFirstRunCode ? b - 241u : 1u; }
+
+// Header checks of the decoder: compressor status OK, n matches, 1 <= Z <= P,
+// Z == P without ZRE, and M finite and >= +0 (Eq. 1, R6; anything else R21).
+__device__ __forceinline__ bool header_valid(const tlc_header *hdr, uint64_t n) {
+    const uint64_t P = (n + 4) / 5;
+    const uint64_t Z = hdr->payload_len;
+    const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
+    const uint32_t Mb = __float_as_uint(hdr->M);
+    return hdr->status == TLC_OK && hdr->n == n && Z <= P && Z >= 1 && (zre || Z == P) &&
+           (Mb >> 31) == 0 && Mb < 0x7f800000u;
 }
 
 // ---------------------------------------------------------------- block-level helpers

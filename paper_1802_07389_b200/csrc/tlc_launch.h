@@ -50,6 +50,10 @@ int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre
                     tlc_header *hdr, void *ws, cudaStream_t st);
 size_t compress_workspace_bytes(uint64_t n);
 
+constexpr uint64_t kBatchMaxN = 5 * 32768;   // P <= 32 KiB of shared memory per CTA
+int launch_compress_batched(int count, const tlc_tensor_desc *d_descs, float s, int use_zre, cudaStream_t st);
+int launch_decompress_batched(int count, const tlc_tensor_desc *d_descs, int mode, cudaStream_t st);
+
 int launch_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *out, int mode,
                       void *ws, cudaStream_t st);
 size_t decompress_workspace_bytes(uint64_t n);
