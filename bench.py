@@ -217,13 +217,15 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
             ctx.compress(tsets[k % 2], s, True, stream)
             ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream)
     torch.cuda.synchronize(dev)
+    cdescs = [ctx.compress_descs(tsets[k]) for k in range(2)]
+    ddesc = ctx.decompress_descs(outs)
+    torch.cuda.synchronize(dev)
     graphs = []
     for k in range(2):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            ctx._cdesc = None
-            ctx.compress(tsets[k], s, True, stream)
-            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream)
+            ctx.compress(tsets[k], s, True, stream, descs=cdescs[k])
+            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream, descs=ddesc)
         graphs.append(g)
     torch.cuda.synchronize(dev)
     l0 = T.tlc_launch_count()

@@ -233,24 +233,39 @@ class TensorSet:
         self._cdesc = None
         self._dkey = None
 
-    def compress(self, ts, s: float, use_zre: bool = True, stream=None):
-        if self._cdesc is None or self._cdesc[1] is not ts:
-            rows = [(ts[i], self.errs[i], None, self.payloads[i], self.hdrs[i], self.sizes[i]) for i in self.small]
-            self._cdesc = (pack_descs(rows, self.device), ts)
+    def compress_descs(self, ts) -> torch.Tensor:
+        """Device descriptor array for compressing `ts` (build once, reuse; needed
+        before capturing the call in a CUDA graph)."""
+        rows = [(ts[i], self.errs[i], None, self.payloads[i], self.hdrs[i], self.sizes[i]) for i in self.small]
+        return pack_descs(rows, self.device)
+
+    def decompress_descs(self, outs, payloads=None, hdrs=None) -> torch.Tensor:
+        payloads = self.payloads if payloads is None else payloads
+        hdrs = self.hdrs if hdrs is None else hdrs
+        rows = [(None, None, outs[i], payloads[i], hdrs[i], self.sizes[i]) for i in self.small]
+        return pack_descs(rows, self.device)
+
+    def compress(self, ts, s: float, use_zre: bool = True, stream=None, descs=None):
+        if descs is None:
+            if self._cdesc is None or self._cdesc[1] is not ts:
+                self._cdesc = (self.compress_descs(ts), ts)
+            descs = self._cdesc[0]
         if self.small:
-            tlc_compress_batched(self._cdesc[0], len(self.small), s, use_zre, stream)
+            tlc_compress_batched(descs, len(self.small), s, use_zre, stream)
         for i in self.large:
             tlc_compress(ts[i], self.errs[i], s, use_zre, self.payloads[i], self.hdrs[i], stream=stream)
 
-    def decompress(self, outs, mode: int = TLC_MODE_OVERWRITE, stream=None, payloads=None, hdrs=None):
+    def decompress(self, outs, mode: int = TLC_MODE_OVERWRITE, stream=None, payloads=None, hdrs=None,
+                   descs=None):
         payloads = self.payloads if payloads is None else payloads
         hdrs = self.hdrs if hdrs is None else hdrs
-        key = (id(outs), id(payloads), id(hdrs))
-        if self._dkey != key:
-            rows = [(None, None, outs[i], payloads[i], hdrs[i], self.sizes[i]) for i in self.small]
-            self._ddesc, self._dkey = pack_descs(rows, self.device), key
+        if descs is None:
+            key = (id(outs), id(payloads), id(hdrs))
+            if self._dkey != key:
+                self._ddesc, self._dkey = self.decompress_descs(outs, payloads, hdrs), key
+            descs = self._ddesc
         if self.small:
-            tlc_decompress_batched(self._ddesc, len(self.small), mode, stream)
+            tlc_decompress_batched(descs, len(self.small), mode, stream)
         for i in self.large:
             tlc_decompress(payloads[i], hdrs[i], self.sizes[i], outs[i], mode, stream=stream)
 
