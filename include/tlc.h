@@ -159,6 +159,69 @@ int tlc_compress_batched(int count, const tlc_tensor_desc *descs, float s, int u
 int tlc_decompress_batched(int count, const tlc_tensor_desc *descs, int mode, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Parameter-server exchange over NCCL.
+ *
+ * The paper's data-parallel architecture: workers push compressed
+ * state changes, servers aggregate ("average the gradients") and
+ * update, workers pull compressed model deltas which the server compresses ONCE
+ * and shares.  Here every rank is a worker and the owner (server)
+ * of a shard of the compression contexts given by the plan (reading R17).
+ *
+ * tlc_comm_unique_id  writes a 128-byte NCCL unique id to `out` (host memory);
+ *                     rank 0 creates it and the caller broadcasts it (e.g. with
+ *                     torch.distributed).
+ * tlc_comm_init       creates the library's NCCL communicator on `device`.
+ * tlc_plan_count / tlc_plan_compute  the deterministic plan (R17) for `world`
+ *                     ranks over host `sizes[num_tensors]`: context k covers
+ *                     elements [lo[k], hi[k]) of tensor[k] and is owned by
+ *                     owner[k].  Pure host computation (no GPU).
+ * tlc_exchange_create allocates every buffer of the exchange for the tensor
+ *                     list (error buffers zeroed, R20): push error buffers for
+ *                     all contexts, the owned (aggregate / delta) buffer and
+ *                     pull error buffers for this rank's contexts, send/receive
+ *                     regions in capacity layout (ceil(n/5) bytes per context).
+ * tlc_exchange_push   grads: host array of num_tensors DEVICE pointers (fp32,
+ *                     the local state changes).  Compresses every context with
+ *                     its push error buffer, sends each owner its payloads and
+ *                     headers, and leaves in the owned buffer (see
+ *                     tlc_exchange_owned_buffer) the mean over ranks of the
+ *                     decompressed pushes: rank-ordered sum from +0, zero trits
+ *                     skipped, then / world in fp32 (R15).  The caller may turn
+ *                     that mean into a model delta in place (R18) before pull.
+ * tlc_exchange_pull   compresses this rank's owned buffer once with its pull
+ *                     error buffers, all-gathers every owner's payloads, and
+ *                     adds the decompressed delta (where q != 0, R16) into
+ *                     outs: host array of num_tensors DEVICE pointers to
+ *                     full-size fp32 tensors.
+ * tlc_exchange_status synchronizes `stream` and returns the worst device status
+ *                     over all received headers (NONFINITE/RANGE from a peer).
+ * Push/pull enqueue on `stream`, allocate nothing and do not synchronize the
+ * host (a descriptor upload happens when the grads/outs pointers change).
+ */
+typedef struct tlc_comm tlc_comm;
+typedef struct tlc_exchange tlc_exchange;
+
+int tlc_comm_unique_id(void *out);
+int tlc_comm_init(tlc_comm **comm, const void *unique_id, int rank, int world, int device);
+int tlc_comm_destroy(tlc_comm *comm);
+int tlc_plan_count(int num_tensors, const uint64_t *sizes, int world);
+int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap, int32_t *tensor,
+                     uint64_t *lo, uint64_t *hi, int32_t *owner);
+int tlc_exchange_create(tlc_exchange **x, tlc_comm *comm, int num_tensors, const uint64_t *sizes);
+int tlc_exchange_destroy(tlc_exchange *x);
+int tlc_exchange_num_contexts(const tlc_exchange *x);
+int tlc_exchange_context(const tlc_exchange *x, int k, int32_t *tensor, uint64_t *lo, uint64_t *hi,
+                         int32_t *owner, uint64_t *elem_off, uint64_t *owned_off);
+uint64_t tlc_exchange_owned_elements(const tlc_exchange *x);
+float *tlc_exchange_owned_buffer(tlc_exchange *x);
+float *tlc_exchange_push_error(tlc_exchange *x);
+float *tlc_exchange_pull_error(tlc_exchange *x);
+uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction /* 0 push, 1 pull */);
+int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream);
+int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream);
+int tlc_exchange_status(tlc_exchange *x, unsigned int *status, void *stream);
+
+/* ---------------------------------------------------------------------------
  * Instrumentation (host-side, not part of the method).
  *
  * tlc_launch_count: number of kernels this library has launched in the

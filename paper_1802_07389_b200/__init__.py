@@ -49,6 +49,23 @@ def _load():
         "tlc_batched_max_elements": (U64, []),
         "tlc_compress_batched": (I, [I, P, F, I, P]),
         "tlc_decompress_batched": (I, [I, P, I, P]),
+        "tlc_comm_unique_id": (I, [P]),
+        "tlc_comm_init": (I, [P, P, I, I, I]),
+        "tlc_comm_destroy": (I, [P]),
+        "tlc_plan_count": (I, [I, P, I]),
+        "tlc_plan_compute": (I, [I, P, I, I, P, P, P, P]),
+        "tlc_exchange_create": (I, [P, P, I, P]),
+        "tlc_exchange_destroy": (I, [P]),
+        "tlc_exchange_num_contexts": (I, [P]),
+        "tlc_exchange_context": (I, [P, I, P, P, P, P, P, P]),
+        "tlc_exchange_owned_elements": (U64, [P]),
+        "tlc_exchange_owned_buffer": (P, [P]),
+        "tlc_exchange_push_error": (P, [P]),
+        "tlc_exchange_pull_error": (P, [P]),
+        "tlc_exchange_wire_bytes": (U64, [P, I]),
+        "tlc_exchange_push": (I, [P, P, F, I, P]),
+        "tlc_exchange_pull": (I, [P, P, F, I, P]),
+        "tlc_exchange_status": (I, [P, P, P]),
         "tlc_launch_count": (ctypes.c_ulonglong, []),
         "tlc_prof_enable": (None, [I]),
         "tlc_prof_collect": (I, [P, I]),
@@ -278,6 +295,141 @@ class TensorSet:
             M, flags, n, plen, status, _ = struct.unpack("<fIQQII", raw[32 * k: 32 * k + 32])
             out.append({"M": M, "flags": flags, "n": n, "payload_len": plen, "status": status})
         return out
+
+
+# ------------------------------------------------------------------ parameter-server exchange
+def tlc_plan(sizes, world: int):
+    """The exchange plan (R17) computed by the library on the host:
+    list of (tensor, lo, hi, owner)."""
+    import numpy as np
+
+    sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
+    k = _lib.tlc_plan_count(len(sz), sz.ctypes.data, int(world))
+    if k < 0:
+        raise TlcError(TLC_ERR_ARG, "tlc_plan_count")
+    t = np.zeros(max(k, 1), np.int32)
+    lo = np.zeros(max(k, 1), np.uint64)
+    hi = np.zeros(max(k, 1), np.uint64)
+    ow = np.zeros(max(k, 1), np.int32)
+    rc = _lib.tlc_plan_compute(len(sz), sz.ctypes.data, int(world), k, t.ctypes.data, lo.ctypes.data,
+                               hi.ctypes.data, ow.ctypes.data)
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_plan_compute")
+    return [(int(t[i]), int(lo[i]), int(hi[i]), int(ow[i])) for i in range(k)]
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory (fp32)."""
+
+    def __init__(self, ptr, n, device):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+        self.device = device
+
+
+def _as_tensor(ptr, n, device):
+    if n == 0:
+        return torch.zeros(0, dtype=torch.float32, device=device)
+    return torch.as_tensor(_DevArray(ptr, n, device), device=device)
+
+
+class Comm:
+    """The library's NCCL communicator.  The 128-byte unique id is created on rank 0
+    and broadcast through torch.distributed (plumbing only)."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device=None, group=None):
+        import torch.distributed as dist
+
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        uid = (ctypes.c_ubyte * 128)()
+        if rank == 0:
+            rc = _lib.tlc_comm_unique_id(ctypes.cast(uid, ctypes.c_void_p))
+            if rc != TLC_OK:
+                raise TlcError(rc, "tlc_comm_unique_id")
+        if world > 1:
+            backend = dist.get_backend(group)
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev if backend == "nccl" else "cpu")
+            dist.broadcast(t, src=0, group=group)
+            ctypes.memmove(uid, bytes(t.cpu().tolist()), 128)
+        self._c = ctypes.c_void_p()
+        rc = _lib.tlc_comm_init(ctypes.byref(self._c), ctypes.cast(uid, ctypes.c_void_p), int(rank), int(world),
+                                int(dev.index))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_comm_init")
+        self.rank, self.world, self.device = rank, world, dev
+
+    def close(self):
+        if self._c:
+            _lib.tlc_comm_destroy(self._c)
+            self._c = ctypes.c_void_p()
+
+
+class Exchange:
+    """3LC parameter-server push/pull for a fixed tensor list (include/tlc.h)."""
+
+    def __init__(self, comm: Comm, sizes):
+        import numpy as np
+
+        self.comm, self.sizes = comm, [int(n) for n in sizes]
+        sz = np.ascontiguousarray(np.asarray(self.sizes, dtype=np.uint64))
+        self._x = ctypes.c_void_p()
+        rc = _lib.tlc_exchange_create(ctypes.byref(self._x), comm._c, len(sz), sz.ctypes.data)
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_create")
+        self.device = comm.device
+        self.num_contexts = _lib.tlc_exchange_num_contexts(self._x)
+        self.owned_elements = int(_lib.tlc_exchange_owned_elements(self._x))
+        self.owned = _as_tensor(_lib.tlc_exchange_owned_buffer(self._x), self.owned_elements, self.device)
+        self.pull_err = _as_tensor(_lib.tlc_exchange_pull_error(self._x), self.owned_elements, self.device)
+        self.push_err = _as_tensor(_lib.tlc_exchange_push_error(self._x), sum(self.sizes), self.device)
+
+    def contexts(self):
+        out = []
+        t, o = ctypes.c_int32(), ctypes.c_int32()
+        lo, hi, eo, oo = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        for k in range(self.num_contexts):
+            _lib.tlc_exchange_context(self._x, k, ctypes.byref(t), ctypes.byref(lo), ctypes.byref(hi),
+                                      ctypes.byref(o), ctypes.byref(eo), ctypes.byref(oo))
+            out.append({"tensor": t.value, "lo": lo.value, "hi": hi.value, "owner": o.value,
+                        "elem_off": eo.value, "owned_off": None if oo.value == 2 ** 64 - 1 else oo.value})
+        return out
+
+    def wire_bytes(self, direction: int) -> int:
+        return int(_lib.tlc_exchange_wire_bytes(self._x, int(direction)))
+
+    @staticmethod
+    def _ptrs(ts):
+        return (ctypes.c_void_p * len(ts))(*[x.data_ptr() for x in ts])
+
+    def push(self, grads, s: float, use_zre: bool = True, stream=None):
+        for g in grads:
+            _check_dev("grad", g, torch.float32)
+        self._g = self._ptrs(grads)
+        rc = _lib.tlc_exchange_push(self._x, ctypes.cast(self._g, ctypes.c_void_p), ctypes.c_float(s),
+                                    int(bool(use_zre)), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_push")
+
+    def pull(self, outs, s: float, use_zre: bool = True, stream=None):
+        for o in outs:
+            _check_dev("out", o, torch.float32)
+        self._o = self._ptrs(outs)
+        rc = _lib.tlc_exchange_pull(self._x, ctypes.cast(self._o, ctypes.c_void_p), ctypes.c_float(s),
+                                    int(bool(use_zre)), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_pull")
+
+    def status(self, stream=None) -> int:
+        st = ctypes.c_uint()
+        rc = _lib.tlc_exchange_status(self._x, ctypes.byref(st), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_status")
+        return int(st.value)
+
+    def close(self):
+        if self._x:
+            _lib.tlc_exchange_destroy(self._x)
+            self._x = ctypes.c_void_p()
 
 
 # ------------------------------------------------------------------ instrumentation

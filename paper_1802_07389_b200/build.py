@@ -13,10 +13,22 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtlc.so")
-SOURCES = ["api.cu", "compress.cu", "decompress.cu", "batched.cu", "prof.cu"]
+SOURCES = ["api.cu", "compress.cu", "decompress.cu", "batched.cu", "exchange.cu", "prof.cu"]
 HEADERS = ["tlc_device.cuh", "tlc_launch.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    """The NCCL that torch loads (nvidia-nccl wheel), so one libnccl.so.2 is in the process."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = list(spec.submodule_search_locations)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-fmad=false", "-prec-div=true",
          "-ftz=false", "-prec-sqrt=true", "--expt-relaxed-constexpr"]
@@ -44,14 +56,16 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     for s in SOURCES:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-               "-c", os.path.join(CSRC, s), "-o", o]
+               "-I", os.path.join(_nccl_dir(), "include"), "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)
         objs.append(o)
     tmp = out + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
+    nlib = os.path.join(_nccl_dir(), "lib")
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", nlib, "-l:libnccl.so.2",
+                           "-Xlinker", "-rpath", "-Xlinker", nlib])
     os.replace(tmp, out)
     return out
 

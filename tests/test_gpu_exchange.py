@@ -1,0 +1,118 @@
+"""The NCCL exchange (tlc_exchange_push / tlc_exchange_pull) vs the W-virtual-rank
+oracle (oracle/exchange.py, X1-X6): owners' means, every rank's outputs and every
+push / pull error buffer, bit for bit.  W = 1 runs in-process; W = 2, 4 spawn one
+process per GPU when the box has them."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+f32 = np.float32
+
+SIZES = [432, 2304, 9216, 36864, 640, 200_003, 1_000_000]
+S, STEPS = 1.75, 3
+
+
+def _grads(r, step, sizes=SIZES):
+    import synth
+
+    return [synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
+
+
+def _run_rank(rank, world, steps, sizes=SIZES):
+    """One rank's exchange; returns per-step means (owned flat) and final state."""
+    import torch
+
+    import paper_1802_07389_b200 as T
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comm = T.Comm(rank, world, dev)
+    x = T.Exchange(comm, sizes)
+    outs = [torch.zeros(n, device=dev) for n in sizes]
+    owned_per_step = []
+    for step in range(steps):
+        g = [torch.from_numpy(a).to(dev) for a in _grads(rank, step, sizes)]
+        x.push(g, S)
+        torch.cuda.synchronize()
+        owned_per_step.append(x.owned.cpu().numpy().copy())
+        x.pull(outs, S)          # delta = mean (R18)
+        torch.cuda.synchronize()
+    assert x.status() == 0
+    res = {"ctx": x.contexts(), "owned": owned_per_step, "outs": [o.cpu().numpy() for o in outs],
+           "push_err": x.push_err.cpu().numpy().copy(), "pull_err": x.pull_err.cpu().numpy().copy()}
+    x.close()
+    comm.close()
+    return res
+
+
+def _check(world, results, sizes=SIZES, steps=STEPS):
+    from oracle import exchange as X
+
+    ps = X.VirtualPS(sizes, world)
+    outs = [[np.zeros(n, f32) for n in sizes] for _ in range(world)]
+    means_steps = []
+    for step in range(steps):
+        means, _, _ = ps.push([_grads(r, step, sizes) for r in range(world)], S)
+        ps.pull(means, outs, S)
+        means_steps.append(means)
+    for r in range(world):
+        res = results[r]
+        for c, cx in enumerate(res["ctx"]):
+            assert (cx["tensor"], cx["lo"], cx["hi"], cx["owner"]) == ps.ctx[c]
+            n = cx["hi"] - cx["lo"]
+            pe = res["push_err"][cx["elem_off"]: cx["elem_off"] + n]
+            assert np.array_equal(pe.view(np.uint32), ps.push_err[r][c].view(np.uint32)), ("push_err", r, c)
+            if cx["owner"] == r:
+                for step in range(steps):
+                    m = res["owned"][step][cx["owned_off"]: cx["owned_off"] + n]
+                    assert np.array_equal(m.view(np.uint32), means_steps[step][c].view(np.uint32)), ("mean", r, c)
+                pl = res["pull_err"][cx["owned_off"]: cx["owned_off"] + n]
+                assert np.array_equal(pl.view(np.uint32), ps.pull_err[c].view(np.uint32)), ("pull_err", r, c)
+        for t in range(len(sizes)):
+            assert np.array_equal(res["outs"][t].view(np.uint32), outs[r][t].view(np.uint32)), ("out", r, t)
+
+
+def test_exchange_w1_in_process():
+    import torch
+
+    assert torch.cuda.is_available()
+    _check(1, [_run_rank(0, 1, STEPS)])
+
+
+def _mp_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        res = _run_rank(rank, world, STEPS)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_exchange_multi_gpu(world):
+    import torch
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    _check(world, results)
