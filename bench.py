@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the ResNet-110 (configs[1]) side measurement")
+    ap.add_argument("--mode", choices=["auto", "codec", "exchange"], default="auto",
+                    help="auto: codec step at N=1, parameter-server exchange step at N>1")
+    ap.add_argument("--model", default="bert-large", help="tensor list of the exchange workload")
+    ap.add_argument("--xs", type=float, default=1.9, help="s of the exchange workload (configs[4])")
+    ap.add_argument("--no-xchg-w1", action="store_true", help="skip the N=1 exchange side measurement")
     ap.add_argument("--e2e-steps", type=int, default=10)
     return ap.parse_args()
 
@@ -262,6 +267,73 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
             "host_launch_calls_during_replay": T.tlc_launch_count() - l0}
 
 
+# ------------------------------------------------------------------ exchange step (row e)
+NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
+
+
+def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None):
+    """BASELINE configs[4]: the model's ndim>=2 gradient tensors exchanged through
+    the parameter-server push/pull (tlc_exchange_push + tlc_exchange_pull, delta =
+    mean) on `world` ranks; every rank holds its own full state change (weak
+    scaling).  Returns the rank-local timings; the caller takes the max over ranks."""
+    import torch
+
+    import synth
+
+    sizes = synth.MODELS[model]
+    N = sum(sizes)
+    grads = [synth.model_step_torch(model, k, rank, dev) for k in range(2)]
+    outs = [torch.zeros(n, dtype=torch.float32, device=dev) for n in sizes]
+    comm = T.Comm(rank, world, dev)
+    x = T.Exchange(comm, sizes)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(k):
+        x.push(grads[k % 2], s, True, stream)
+        x.pull(outs, s, True, stream)
+
+    for k in range(max(3, warmup)):
+        step(k)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    T.tlc_prof_collect()
+    T.tlc_prof_enable(True)
+    l0 = T.tlc_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(steps):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    T.tlc_prof_enable(False)
+    launches = T.tlc_launch_count() - l0
+    prof = T.tlc_prof_collect()
+    ms = e0.elapsed_time(e1) / steps
+    status = x.status(stream)
+    wire = x.wire_bytes(0) + x.wire_bytes(1)
+    kern_ms = sum(tot for (_, tot) in prof.values()) / steps
+    x.close()
+    comm.close()
+    return {"ms": ms, "kernel_ms": kern_ms, "launches": launches, "wire": wire, "N": N, "status": status,
+            "contexts": len(T.tlc_plan(sizes, world)),
+            "kernels": {k: {"launches_per_step": c / steps, "ms_per_step": t / steps} for k, (c, t) in prof.items()}}
+
+
+def run_exchange_leg(args, T, dev, world, rank, dist):
+    import torch
+
+    r = measure_exchange(T, dev, world, rank, args.model, args.xs, args.steps, args.warmup,
+                         dist if world > 1 else None)
+    ms = r["ms"]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * 4.0 * r["N"] / (ms / 1e3) / 1e9
+    return r, ms, value
+
+
 # ------------------------------------------------------------------ the GPU leg
 def run_tlc(args):
     import numpy as np
@@ -278,6 +350,10 @@ def run_tlc(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+
+    mode = args.mode if args.mode != "auto" else ("codec" if world == 1 else "exchange")
+    if mode == "exchange":
+        return run_exchange_main(args, T, dev, world, rank, dist)
 
     n, s, zre = args.n, float(args.s), not args.no_zre
     # Inputs: seeded host generator (same module the oracle tests use), copied once
@@ -394,6 +470,13 @@ def run_tlc(args):
                "ms_per_step": ems / E,
                "what": "pinned host t -> HBM, tlc_compress, tlc_decompress, HBM -> pinned host out"}
 
+    xw1 = None
+    if world == 1 and not args.no_xchg_w1:
+        r, xms, xval = run_exchange_leg(args, T, dev, 1, 0, None)
+        xw1 = {"workload": f"configs[4]: {args.model} gradient exchange (push+pull) at s={args.xs}, W=1",
+               "value": xval, "unit": "GB/s", "ms_per_step": xms, "kernel_ms_per_step": r["kernel_ms"],
+               "status": r["status"]}
+
     c2 = None
     if rank == 0 and not args.no_c2:
         c2 = [measure_resnet110(T, dev, sv) for sv in (1.0, 1.75, 1.9)]
@@ -423,11 +506,50 @@ def run_tlc(args):
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "c2_resnet110": c2,
+            "xchg_w1": xw1,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_exchange_main(args, T, dev, world, rank, dist):
+    """N > 1: the parameter-server exchange step of configs[4] (weak scaling)."""
+    import torch
+
+    clocks = ClockSampler(dev)
+    clocks.start()
+    r, ms, value = run_exchange_leg(args, T, dev, world, rank, dist)
+    clocks.stop()
+    if rank == 0:
+        pct_nvlink = r["wire"] / 2 / (ms / 1e3) / 1e9 / NVLINK_GBS   # per direction
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic: {args.model} ndim>=2 gradient shapes, g = mu_l + N(0,1) per layer "
+                    "(torch Philox on device, synth/), 2 rotating steps per rank",
+            "config": {"workload": f"configs[4]: {args.model} gradient exchange, parameter-server push "
+                                   f"(compress, NCCL to owners, rank-ordered aggregate / W) + shared pull "
+                                   f"(owner compresses once, NCCL all-gather, apply) at s={args.xs}, "
+                                   f"{r['N']:,} values per rank",
+                       "n_per_rank": r["N"], "s": args.xs, "contexts": r["contexts"],
+                       "l2": "inputs larger than L2 (1.34 GB of state changes per rank); no flush",
+                       "parallelism": f"ps{world} (sharded parameter server over NCCL, NVLink)"},
+            "value_definition": "world x 4 x values-per-rank / step time (effective fp32 GB/s exchanged)",
+            "wire_bytes_per_rank_per_step": r["wire"],
+            "nvlink_frac": pct_nvlink,
+            "kernel_ms_per_step_rank0": r["kernel_ms"],
+            "kernels_rank0": r["kernels"],
+            "gpu_launches": r["launches"],
+            "exchange_status": r["status"],
+            "e2e": None,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

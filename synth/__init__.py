@@ -84,6 +84,25 @@ def model_step(model: str, step: int, rank: int = 0, cfg: int = 2):
     return [layer_gradient(n, mus[l], cfg, rank, l, step) for l, n in enumerate(sizes)]
 
 
+def model_step_torch(model: str, step: int, rank: int, device, cfg: int = 5):
+    """Device-side draw of one (rank, step) state change for every tensor of
+    ``model``: g = mu_l + z with torch's seeded Philox generator on ``device``
+    (bench-only, for the 336M-value BERT-large lists; same distribution as
+    model_step, different stream)."""
+    import torch
+
+    sizes = MODELS[model]
+    mus = layer_means(sizes, cfg, 10_000 + len(sizes))
+    g = torch.Generator(device=device)
+    g.manual_seed(int(np.random.SeedSequence([cfg, rank, step]).generate_state(1)[0]))
+    out = []
+    for l, n in enumerate(sizes):
+        x = torch.randn(n, generator=g, device=device, dtype=torch.float32)
+        x += float(mus[l])
+        out.append(x)
+    return out
+
+
 def zeros(n: int) -> np.ndarray:
     """'zeros' family: every state change is 0 (P:546-548's all-zero tensor)."""
     return np.zeros(n, dtype=np.float32)
