@@ -222,15 +222,15 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
             ctx.compress(tsets[k % 2], s, True, stream)
             ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream)
     torch.cuda.synchronize(dev)
-    cdescs = [ctx.compress_descs(tsets[k]) for k in range(2)]
-    ddesc = ctx.decompress_descs(outs)
+    cb = [ctx.compress_batch(tsets[k]) for k in range(2)]
+    db = ctx.decompress_batch(outs)
     torch.cuda.synchronize(dev)
     graphs = []
     for k in range(2):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            ctx.compress(tsets[k], s, True, stream, descs=cdescs[k])
-            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream, descs=ddesc)
+            ctx.compress(tsets[k], s, True, stream, batch=cb[k])
+            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream, batch=db)
         graphs.append(g)
     torch.cuda.synchronize(dev)
     l0 = T.tlc_launch_count()
@@ -257,13 +257,13 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
     del flush
     N = sum(sizes)
     Z = sum(h["payload_len"] for h in ctx.headers())
-    return {"workload": "C2: ResNet-110 gradient set, 110 tensors, 1,719,856 values, batched K6/K7 "
-                        "launches in a CUDA graph, error feedback carried", "s": s,
+    return {"workload": "C2: ResNet-110 gradient set, 110 tensors, 1,719,856 values, one tlc_batch "
+                        "(K1-K5 over a 110-segment table) in a CUDA graph, error feedback carried", "s": s,
             "value": 4.0 * N / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "l2": "flushed (512 MiB write) before every timed step",
             "warm": {"value": 4.0 * N / (ms_warm / 1e3) / 1e9, "ms_per_step": ms_warm,
                      "l2": "back-to-back replays, working set L2-resident"},
-            "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 2,
+            "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 5,
             "host_launch_calls_during_replay": T.tlc_launch_count() - l0}
 
 

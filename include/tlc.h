@@ -132,18 +132,23 @@ int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *o
                    int mode, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
- * Batched small tensors (SURVEY 8(a) "small-tensor regime"; BASELINE configs[1],
- * the 110 per-layer gradient tensors of ResNet-110).  One kernel launch
- * compresses (decompresses) a whole list of independent tensors, one CTA per
- * tensor, each with its own error buffer, payload and header -- the same
- * per-tensor operation and results as tlc_compress / tlc_decompress.
+ * Batches of tensors (SURVEY 8(a) "small-tensor regime"; BASELINE configs[1]
+ * and [4]: the per-layer gradient tensors of ResNet-110 / ResNet-50 /
+ * BERT-large).  A batch is a fixed list of independent tensors, each with its
+ * own error buffer, payload and header -- the per-tensor compression contexts
+ * of the paper -- compressed (decompressed) by one set of kernel
+ * launches over all of them, with results identical to one tlc_compress /
+ * tlc_decompress call per tensor.
  *
- * `descs` is a DEVICE array of `count` descriptors (so the call can be captured
- * in a CUDA graph).  Every tensor must have 1 <= n <= tlc_batched_max_elements();
- * a tensor violating that gets hdr->status = TLC_ERR_ARG (compress) or
- * TLC_ERR_FORMAT (decompress) on the device and is otherwise skipped.
- * Fields used by compress: t, err, payload (capacity >= ceil(n/5)), hdr, n.
- * Fields used by decompress: payload, hdr, out, n (mode as tlc_decompress).
+ * tlc_batch_create    `descs` is a HOST array of `count` descriptors (device
+ *                     pointers inside); the batch uploads its tensor table and
+ *                     allocates its own device workspace once.  Fields used by
+ *                     compress: t, err, payload (capacity >= ceil(n/5)), hdr,
+ *                     n; by decompress: payload, hdr, out, n.  1 <= n < 2^42.
+ * tlc_batch_update    replaces the pointers (same n's); synchronous upload.
+ * tlc_batch_compress  / tlc_batch_decompress enqueue on `stream`, no host
+ *                     traffic, no allocation (CUDA-graph capturable); per-tensor
+ *                     data errors land in each tensor's hdr->status.
  */
 typedef struct tlc_tensor_desc {
     const float *t;
@@ -154,9 +159,14 @@ typedef struct tlc_tensor_desc {
     uint64_t n;
 } tlc_tensor_desc;
 
-uint64_t tlc_batched_max_elements(void);
-int tlc_compress_batched(int count, const tlc_tensor_desc *descs, float s, int use_zre, void *stream);
-int tlc_decompress_batched(int count, const tlc_tensor_desc *descs, int mode, void *stream);
+typedef struct tlc_batch tlc_batch;
+
+int tlc_batch_create(tlc_batch **batch, int count, const tlc_tensor_desc *descs);
+int tlc_batch_update(tlc_batch *batch, const tlc_tensor_desc *descs);
+int tlc_batch_destroy(tlc_batch *batch);
+size_t tlc_batch_workspace_bytes(const tlc_batch *batch);
+int tlc_batch_compress(tlc_batch *batch, float s, int use_zre, void *stream);
+int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Parameter-server exchange over NCCL.

@@ -46,9 +46,12 @@ def _load():
         "tlc_decompress_workspace_bytes": (SZ, [U64]),
         "tlc_compress": (I, [P, P, U64, F, I, P, U64, P, P, SZ, P]),
         "tlc_decompress": (I, [P, P, U64, P, I, P, SZ, P]),
-        "tlc_batched_max_elements": (U64, []),
-        "tlc_compress_batched": (I, [I, P, F, I, P]),
-        "tlc_decompress_batched": (I, [I, P, I, P]),
+        "tlc_batch_create": (I, [P, I, P]),
+        "tlc_batch_update": (I, [P, P]),
+        "tlc_batch_destroy": (I, [P]),
+        "tlc_batch_workspace_bytes": (SZ, [P]),
+        "tlc_batch_compress": (I, [P, F, I, P]),
+        "tlc_batch_decompress": (I, [P, I, P]),
         "tlc_comm_unique_id": (I, [P]),
         "tlc_comm_init": (I, [P, P, I, I, I]),
         "tlc_comm_destroy": (I, [P]),
@@ -195,47 +198,66 @@ def tlc_decompress(payload: torch.Tensor, hdr: torch.Tensor, n: int, out: torch.
     return out
 
 
-# ------------------------------------------------------------------ batched small tensors
-DESC_BYTES = 48   # struct tlc_tensor_desc: t, err, out, payload, hdr (pointers), n (uint64)
+# ------------------------------------------------------------------ batches of tensors
+class TensorDesc(ctypes.Structure):
+    """struct tlc_tensor_desc (include/tlc.h)."""
+    _fields_ = [("t", ctypes.c_void_p), ("err", ctypes.c_void_p), ("out", ctypes.c_void_p),
+                ("payload", ctypes.c_void_p), ("hdr", ctypes.c_void_p), ("n", ctypes.c_uint64)]
 
 
-def tlc_batched_max_elements() -> int:
-    return int(_lib.tlc_batched_max_elements())
+def _descs(rows):
+    arr = (TensorDesc * len(rows))()
+    for k, (t, e, o, pl, h, n) in enumerate(rows):
+        arr[k] = TensorDesc(*[x.data_ptr() if isinstance(x, torch.Tensor) else (x or None) for x in (t, e, o, pl, h)],
+                            int(n))
+    return arr
 
 
-def pack_descs(rows, device) -> torch.Tensor:
-    """rows: iterable of (t, err, out, payload, hdr, n) with tensors or None -> a device
-    array of struct tlc_tensor_desc (uint8 tensor)."""
-    import struct
+class Batch:
+    """tlc_batch: a fixed list of tensors compressed / decompressed by one set of
+    kernel launches (device-resident table and workspace)."""
 
-    buf = bytearray()
-    for t, e, o, pl, h, n in rows:
-        ptr = [x.data_ptr() if isinstance(x, torch.Tensor) else int(x or 0) for x in (t, e, o, pl, h)]
-        buf += struct.pack("<QQQQQQ", *ptr, int(n))
-    host = torch.frombuffer(buf if buf else bytearray(DESC_BYTES), dtype=torch.uint8)
-    return host.to(device)
+    def __init__(self, rows):
+        self.rows = list(rows)
+        self._b = ctypes.c_void_p()
+        arr = _descs(self.rows)
+        rc = _lib.tlc_batch_create(ctypes.byref(self._b), len(self.rows), ctypes.cast(arr, ctypes.c_void_p))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_batch_create")
 
+    def update(self, rows):
+        self.rows = list(rows)
+        arr = _descs(self.rows)
+        rc = _lib.tlc_batch_update(self._b, ctypes.cast(arr, ctypes.c_void_p))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_batch_update")
 
-def tlc_compress_batched(descs: torch.Tensor, count: int, s: float, use_zre: bool = True, stream=None):
-    _check_dev("descs", descs, torch.uint8)
-    rc = _lib.tlc_compress_batched(int(count), descs.data_ptr(), ctypes.c_float(s), int(bool(use_zre)),
-                                   _stream_ptr(stream))
-    if rc != TLC_OK:
-        raise TlcError(rc, "tlc_compress_batched")
+    def compress(self, s: float, use_zre: bool = True, stream=None):
+        rc = _lib.tlc_batch_compress(self._b, ctypes.c_float(s), int(bool(use_zre)), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_batch_compress")
 
+    def decompress(self, mode: int = TLC_MODE_OVERWRITE, stream=None):
+        rc = _lib.tlc_batch_decompress(self._b, int(mode), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_batch_decompress")
 
-def tlc_decompress_batched(descs: torch.Tensor, count: int, mode: int = TLC_MODE_OVERWRITE, stream=None):
-    _check_dev("descs", descs, torch.uint8)
-    rc = _lib.tlc_decompress_batched(int(count), descs.data_ptr(), int(mode), _stream_ptr(stream))
-    if rc != TLC_OK:
-        raise TlcError(rc, "tlc_decompress_batched")
+    def close(self):
+        if self._b:
+            _lib.tlc_batch_destroy(self._b)
+            self._b = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class TensorSet:
     """Compression contexts for a list of tensors (one error buffer, payload and
-    header each -- the paper's per-tensor contexts).  Tensors up to
-    tlc_batched_max_elements() go through one batched launch; larger ones through
-    tlc_compress / tlc_decompress.  Marshalling only: all arithmetic is on the GPU."""
+    header each -- the paper's per-tensor contexts), compressed and
+    decompressed through tlc_batch objects.  Marshalling only."""
 
     def __init__(self, sizes, device=None):
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -244,47 +266,32 @@ class TensorSet:
         self.payloads = [torch.empty(max(1, tlc_max_payload_bytes(n)), dtype=torch.uint8, device=dev)
                          for n in self.sizes]
         self.hdrs = torch.zeros(len(self.sizes), HEADER_BYTES, dtype=torch.uint8, device=dev)
-        lim = tlc_batched_max_elements()
-        self.small = [i for i, n in enumerate(self.sizes) if n <= lim]
-        self.large = [i for i, n in enumerate(self.sizes) if n > lim]
-        self._cdesc = None
-        self._dkey = None
+        self._cb = self._db = None
+        self._ckey = self._dkey = None
 
-    def compress_descs(self, ts) -> torch.Tensor:
-        """Device descriptor array for compressing `ts` (build once, reuse; needed
-        before capturing the call in a CUDA graph)."""
-        rows = [(ts[i], self.errs[i], None, self.payloads[i], self.hdrs[i], self.sizes[i]) for i in self.small]
-        return pack_descs(rows, self.device)
+    def compress_batch(self, ts) -> Batch:
+        return Batch([(ts[i], self.errs[i], None, self.payloads[i], self.hdrs[i], n) for i, n in enumerate(self.sizes)])
 
-    def decompress_descs(self, outs, payloads=None, hdrs=None) -> torch.Tensor:
+    def decompress_batch(self, outs, payloads=None, hdrs=None) -> Batch:
         payloads = self.payloads if payloads is None else payloads
         hdrs = self.hdrs if hdrs is None else hdrs
-        rows = [(None, None, outs[i], payloads[i], hdrs[i], self.sizes[i]) for i in self.small]
-        return pack_descs(rows, self.device)
+        return Batch([(None, None, outs[i], payloads[i], hdrs[i], n) for i, n in enumerate(self.sizes)])
 
-    def compress(self, ts, s: float, use_zre: bool = True, stream=None, descs=None):
-        if descs is None:
-            if self._cdesc is None or self._cdesc[1] is not ts:
-                self._cdesc = (self.compress_descs(ts), ts)
-            descs = self._cdesc[0]
-        if self.small:
-            tlc_compress_batched(descs, len(self.small), s, use_zre, stream)
-        for i in self.large:
-            tlc_compress(ts[i], self.errs[i], s, use_zre, self.payloads[i], self.hdrs[i], stream=stream)
+    def compress(self, ts, s: float, use_zre: bool = True, stream=None, batch: Batch | None = None):
+        if batch is None:
+            key = tuple(t.data_ptr() for t in ts)
+            if self._ckey != key:
+                self._cb, self._ckey = self.compress_batch(ts), key
+            batch = self._cb
+        batch.compress(s, use_zre, stream)
 
-    def decompress(self, outs, mode: int = TLC_MODE_OVERWRITE, stream=None, payloads=None, hdrs=None,
-                   descs=None):
-        payloads = self.payloads if payloads is None else payloads
-        hdrs = self.hdrs if hdrs is None else hdrs
-        if descs is None:
-            key = (id(outs), id(payloads), id(hdrs))
+    def decompress(self, outs, mode: int = TLC_MODE_OVERWRITE, stream=None, batch: Batch | None = None):
+        if batch is None:
+            key = tuple(o.data_ptr() for o in outs)
             if self._dkey != key:
-                self._ddesc, self._dkey = self.decompress_descs(outs, payloads, hdrs), key
-            descs = self._ddesc
-        if self.small:
-            tlc_decompress_batched(descs, len(self.small), mode, stream)
-        for i in self.large:
-            tlc_decompress(payloads[i], hdrs[i], self.sizes[i], outs[i], mode, stream=stream)
+                self._db, self._dkey = self.decompress_batch(outs), key
+            batch = self._db
+        batch.decompress(mode, stream)
 
     def headers(self):
         import struct

@@ -59,18 +59,4 @@ int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *o
     return launch_decompress(payload, hdr, n, out, mode, ws, reinterpret_cast<cudaStream_t>(stream));
 }
 
-uint64_t tlc_batched_max_elements(void) { return kBatchMaxN; }
-
-int tlc_compress_batched(int count, const tlc_tensor_desc *descs, float s, int use_zre, void *stream) {
-    if (count < 0 || (count > 0 && !descs)) return TLC_ERR_ARG;
-    if (!(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
-    return launch_compress_batched(count, descs, s, use_zre ? 1 : 0, reinterpret_cast<cudaStream_t>(stream));
-}
-
-int tlc_decompress_batched(int count, const tlc_tensor_desc *descs, int mode, void *stream) {
-    if (count < 0 || (count > 0 && !descs)) return TLC_ERR_ARG;
-    if (mode != TLC_MODE_OVERWRITE && mode != TLC_MODE_ACCUMULATE) return TLC_ERR_ARG;
-    return launch_decompress_batched(count, descs, mode, reinterpret_cast<cudaStream_t>(stream));
-}
-
 }  // extern "C"

@@ -1,19 +1,24 @@
-// compress.cu -- the 3LC compressor on sm_100a: two HBM passes.
+// compress.cu -- the 3LC compressor on sm_100a over a table of tensors
+// ("segments", tlc_launch.h): a single tlc_compress call is a one-segment table,
+// a batch of per-layer tensors is a device table, and every kernel covers all
+// segments in one launch.
 //
-//  K1 tlc_absmax_kernel  (row a1): u = err + t (not stored); grid max of
-//     bits(u) & 0x7fffffff as uint32, which orders |u| and flags NaN/Inf in one
-//     integer max; last CTA turns it into M = fl(a*s) and the header.
-//  K2 tlc_quant_qe_kernel (rows a2-a3): a pure streaming pass -- recompute u,
-//     quantize (Eq. 2), write err = u - M*q (steps a,b) and fold the five
-//     strided trits of each quartic position into its byte (step 3), written
-//     to the payload (no ZRE) or to a P-byte scratch in the workspace.
+//  K1 tlc_absmax_kernel  (row a1): u = err + t (not stored); max of
+//     bits(u) & 0x7fffffff as uint32 per segment, which orders |u| and flags
+//     NaN/Inf in one integer max (atomicMax per CTA and segment).
+//  K2 tlc_quant_qe_kernel (rows a2-a3): a streaming pass -- recompute u,
+//     M = fl(max|u| * s) (Eq. 1) from the segment's key, quantize (Eq. 2),
+//     write err = u - M*q (steps a,b) and fold the five strided trits of each
+//     quartic position into its byte (step 3), written to the payload (no ZRE)
+//     or to the quartic scratch.  The CTA owning a segment's first tile writes
+//     its header.
 //  K3 tlc_zre_kernel (row a4): zero-run encoding (step 4) of the quartic bytes
-//     as one scan over the run-carry monoid of tlc_device.cuh with decoupled
-//     look-back across tiles (dynamic tile ids keep it deadlock-free); each
-//     thread emits its payload bytes at their final offsets and the last tile
-//     writes hdr->payload_len.
+//     as a chunked single-pass scan over the run-carry monoid of
+//     tlc_device.cuh (section 5.3 of DESIGN.md).
 //
 // Paper: P:372-410 (Sec. 3.1), P:495-510 (Sec. 3.2), P:538-548 (Sec. 3.3).
+#include <algorithm>
+
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
 
@@ -27,98 +32,68 @@ __device__ __forceinline__ unsigned int absmax_key(float t, float e) {
     return __float_as_uint(u) & 0x7fffffffu;         // |u| as ordered uint; NaN > Inf
 }
 
-template <bool kVec>
-__global__ void __launch_bounds__(kK1Threads, 1)
-tlc_absmax_kernel(const float *__restrict__ t, const float *__restrict__ err, uint64_t n,
-                  float s, int use_zre, unsigned int *__restrict__ partial, Ctrl *ctrl,
-                  tlc_header *hdr) {
-    unsigned int m = 0;
-    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint64_t tail_start = 0;
-    if (kVec) {
-        const uint64_t n4 = n / 4;
-        const float4 *t4 = reinterpret_cast<const float4 *>(t);
-        const float4 *e4 = reinterpret_cast<const float4 *>(err);
-        constexpr int U = 4;
-        uint64_t i = gtid;
-        for (; i + (U - 1) * stride < n4; i += U * stride) {
-            float4 a[U], b[U];
-#pragma unroll
-            for (int k = 0; k < U; k++) {
-                a[k] = ld_stream4(t4 + i + k * stride);
-                b[k] = __ldcg(e4 + i + k * stride);
-            }
-#pragma unroll
-            for (int k = 0; k < U; k++) {
-                m = max(m, absmax_key(a[k].x, b[k].x));
-                m = max(m, absmax_key(a[k].y, b[k].y));
-                m = max(m, absmax_key(a[k].z, b[k].z));
-                m = max(m, absmax_key(a[k].w, b[k].w));
-            }
-        }
-        for (; i < n4; i += stride) {
-            float4 a = ld_stream4(t4 + i), b = __ldcg(e4 + i);
-            m = max(m, absmax_key(a.x, b.x));
-            m = max(m, absmax_key(a.y, b.y));
-            m = max(m, absmax_key(a.z, b.z));
-            m = max(m, absmax_key(a.w, b.w));
-        }
-        tail_start = n4 * 4;
-    }
-    for (uint64_t i = tail_start + gtid; i < n; i += stride)
-        m = max(m, absmax_key(ld_stream(t + i), __ldcg(err + i)));
-
-    // block reduction: warp redux, then one warp over the warp maxima
-    __shared__ unsigned int s_warp[kK1Threads / 32];
-    __shared__ bool s_last;
+__device__ __forceinline__ void k1_flush(unsigned int m, unsigned int *maxkey, int si, unsigned int *s_warp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     m = __reduce_max_sync(0xffffffffu, m);
     if (lane == 0) s_warp[warp] = m;
     __syncthreads();
     if (warp == 0) {
-        m = lane < (kK1Threads / 32) ? s_warp[lane] : 0u;
+        m = lane < kK1Threads / 32 ? s_warp[lane] : 0u;
         m = __reduce_max_sync(0xffffffffu, m);
-        if (lane == 0) {
-            partial[blockIdx.x] = m;
-            __threadfence();
-            unsigned int ticket = atomicAdd(&ctrl->done_counter, 1u);
-            s_last = (ticket == gridDim.x - 1);
-        }
+        if (lane == 0) atomicMax(maxkey + si, m);
     }
     __syncthreads();
-    if (!s_last) return;
+}
 
-    // last CTA: reduce the per-CTA maxima, derive M (Eq. 1) and the status
-    __threadfence();
-    m = 0;
-    for (unsigned int i = threadIdx.x; i < gridDim.x; i += blockDim.x)
-        m = max(m, __ldcg(partial + i));
-    m = __reduce_max_sync(0xffffffffu, m);
-    if (lane == 0) s_warp[warp] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned int key = 0;
-        for (int w = 0; w < kK1Threads / 32; w++) key = max(key, s_warp[w]);
-        unsigned int status = TLC_OK;
-        float M = 0.0f;
-        if (key >= 0x7f800000u) {
-            status = TLC_ERR_NONFINITE;                       // NaN or Inf in u (R6)
-        } else {
-            M = __fmul_rn(__uint_as_float(key), s);           // Eq. 1
-            if (isinf(M)) { status = TLC_ERR_RANGE; M = 0.0f; }
+__global__ void __launch_bounds__(kK1Threads, 1)
+tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
+    __shared__ unsigned int s_warp[kK1Threads / 32];
+    unsigned int m = 0;
+    int cur = -1;
+    for (uint64_t tile = blockIdx.x; tile < T.n1; tile += gridDim.x) {
+        const int si = find_seg<1>(T, tile);
+        if (si != cur) {                                  // uniform: flush the previous segment
+            if (cur >= 0) k1_flush(m, maxkey, cur, s_warp);
+            m = 0;
+            cur = si;
         }
-        ctrl->maxkey = key;
-        ctrl->M = M;
-        ctrl->status = status;
-        const uint64_t P = (n + 4) / 5;
-        hdr->M = M;
-        hdr->flags = use_zre ? TLC_FLAG_ZRE : 0u;
-        hdr->n = n;
-        hdr->payload_len = (status == TLC_OK && !use_zre) ? P : 0;
-        hdr->status = status;
-        hdr->reserved = 0;
+        const Seg S = get_seg(T, si);
+        const uint64_t lo = (tile - S.k1) * kT1, hi = tmin<uint64_t>(S.n, lo + kT1);
+        uint64_t tail = lo;
+        if (S.flags & kSegVec1) {
+            const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
+            const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
+            const uint64_t a = lo / 4, b = hi / 4;             // lo is a multiple of 4
+            constexpr int U = 4;
+            uint64_t i = a + threadIdx.x;
+            for (; i + (U - 1) * kK1Threads < b; i += U * kK1Threads) {
+                float4 x[U], y[U];
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    x[k] = ld_stream4(t4 + i + k * kK1Threads);
+                    y[k] = __ldcg(e4 + i + k * kK1Threads);
+                }
+#pragma unroll
+                for (int k = 0; k < U; k++) {
+                    m = max(m, absmax_key(x[k].x, y[k].x));
+                    m = max(m, absmax_key(x[k].y, y[k].y));
+                    m = max(m, absmax_key(x[k].z, y[k].z));
+                    m = max(m, absmax_key(x[k].w, y[k].w));
+                }
+            }
+            for (; i < b; i += kK1Threads) {
+                const float4 x = ld_stream4(t4 + i), y = __ldcg(e4 + i);
+                m = max(m, absmax_key(x.x, y.x));
+                m = max(m, absmax_key(x.y, y.y));
+                m = max(m, absmax_key(x.z, y.z));
+                m = max(m, absmax_key(x.w, y.w));
+            }
+            tail = 4 * b;
+        }
+        for (uint64_t i = tail + threadIdx.x; i < hi; i += kK1Threads)
+            m = max(m, absmax_key(ld_stream(S.t + i), __ldcg(S.err + i)));
     }
+    if (cur >= 0) k1_flush(m, maxkey, cur, s_warp);
 }
 
 // ============================================================== K2
@@ -126,8 +101,9 @@ constexpr int kK2Threads = 256;
 
 // One quartic position j, any alignment: the five strided elements e = i*P + j
 // (partition i), residuals stored, byte returned (pad positions -> digit 0).
+template <class QT>
 __device__ __forceinline__ uint32_t quant_qe_one(const float *__restrict__ t, float *__restrict__ err,
-                                                 uint64_t n, uint64_t P, uint64_t j, const Quant &Q) {
+                                                 uint64_t n, uint64_t P, uint64_t j, const QT &Q) {
     float tv[5], ev[5];
 #pragma unroll
     for (int i = 0; i < 5; i++) {
@@ -147,38 +123,53 @@ __device__ __forceinline__ uint32_t quant_qe_one(const float *__restrict__ t, fl
     return b;
 }
 
-// ---- vector path (P % 4 == 0, 16-byte aligned t/err/bytes): one thread per
-// group of 4 consecutive quartic positions j..j+3, one float4 per partition.
-// Groups whose 20 elements all exist run without bounds checks; the few
-// positions of the last group(s) of partition 4 go through quant_qe_one.
+// One group of 4 consecutive quartic positions 4g..4g+3 whose 20 elements all
+// exist: one float4 of t and of err per partition.
 template <class QT>
-__device__ __forceinline__ void quant_qe_groups(const float4 *__restrict__ t4, float4 *__restrict__ e4,
-                                                uint32_t *__restrict__ b4, uint64_t P4,
-                                                uint64_t full_groups, const QT &Q) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < full_groups; g += stride) {
-        float4 tv[5], ev[5];
+__device__ __forceinline__ void quant_qe_group(const float4 *__restrict__ t4, float4 *__restrict__ e4,
+                                               uint32_t *__restrict__ b4, uint64_t P4, uint64_t g,
+                                               const QT &Q) {
+    float4 tv[5], ev[5];
 #pragma unroll
-        for (int i = 0; i < 5; i++) {
-            tv[i] = ld_stream4(t4 + g + i * P4);
-            ev[i] = __ldcs(e4 + g + i * P4);
+    for (int i = 0; i < 5; i++) {
+        tv[i] = ld_stream4(t4 + g + i * P4);
+        ev[i] = __ldcs(e4 + g + i * P4);
+    }
+    uint32_t by[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        float r[4];
+        const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
+        const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const float u = __fadd_rn(ee[c], tt[c]);        // step (1)
+            const int q = Q.q(u);                            // Eq. 2
+            r[c] = Q.residual(u, q);                         // steps (a),(b)
+            by[c] = by[c] * 3u + (uint32_t)(q + 1);          // steps 1, 6
         }
-        uint32_t by[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            float r[4];
-            const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
-            const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const float u = __fadd_rn(ee[c], tt[c]);    // step (1)
-                const int q = Q.q(u);                        // Eq. 2
-                r[c] = Q.residual(u, q);                     // steps (a),(b)
-                by[c] = by[c] * 3u + (uint32_t)(q + 1);      // steps 1, 6
-            }
-            __stcs(e4 + g + i * P4, make_float4(r[0], r[1], r[2], r[3]));
-        }
-        b4[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
+        __stcs(e4 + g + i * P4, make_float4(r[0], r[1], r[2], r[3]));
+    }
+    b4[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
+}
+
+template <class QT>
+__device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, const QT &Q) {
+    const uint64_t P = S.P, n = S.n;
+    const uint64_t jend = tmin<uint64_t>(P, j0 + kT2);
+    if (S.flags & kSegVec2) {
+        // groups g with 4P + 4g + 3 < n are complete in all five partitions
+        const uint64_t full = n >= 4 * P + 3 ? tmin<uint64_t>(P / 4, (n - 4 * P) / 4) : 0;
+        const uint64_t g0 = j0 / 4, g1 = tmax<uint64_t>(g0, tmin<uint64_t>(jend / 4, full));
+        const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
+        float4 *e4 = reinterpret_cast<float4 *>(S.err);
+        uint32_t *b4 = reinterpret_cast<uint32_t *>(bytes);
+        for (uint64_t g = g0 + threadIdx.x; g < g1; g += kK2Threads) quant_qe_group(t4, e4, b4, P / 4, g, Q);
+        for (uint64_t j = 4 * g1 + threadIdx.x; j < jend; j += kK2Threads)
+            bytes[j] = (uint8_t)quant_qe_one(S.t, S.err, n, P, j, Q);
+    } else {
+        for (uint64_t j = j0 + threadIdx.x; j < jend; j += kK2Threads)
+            bytes[j] = (uint8_t)quant_qe_one(S.t, S.err, n, P, j, Q);
     }
 }
 
@@ -186,49 +177,42 @@ __device__ __forceinline__ void quant_qe_groups(const float4 *__restrict__ t4, f
 #define TLC_K2_MINB 2
 #endif
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
-tlc_quant_qe_vec_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
-                        uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
-    if (ctrl->status != TLC_OK) return;           // K1 raised NONFINITE / RANGE: err untouched
-    const Quant Q(ctrl->M);
-    const uint64_t P = (n + 4) / 5;
-    const uint64_t P4 = P / 4;                     // partition stride in float4
-    // group g is complete iff 4P + 4g + 3 < n
-    const uint64_t full_groups = n >= 4 * P + 3 ? tmin<uint64_t>(P4, (n - 4 * P) / 4) : 0;
-    const float4 *t4 = reinterpret_cast<const float4 *>(t);
-    float4 *e4 = reinterpret_cast<float4 *>(err);
-    uint32_t *b4 = reinterpret_cast<uint32_t *>(bytes);
-    if (Q.mode == 1) quant_qe_groups(t4, e4, b4, P4, full_groups, QuantCmp(Q));   // uniform branch
-    else quant_qe_groups(t4, e4, b4, P4, full_groups, Q);
-    // tail: quartic positions of the incomplete groups
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t j = 4 * full_groups + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P; j += stride)
-        bytes[j] = (uint8_t)quant_qe_one(t, err, n, P, j, Q);
-}
-
-// ---- scalar path (any alignment, any P): one thread per quartic position j.
-__global__ void __launch_bounds__(kK2Threads)
-tlc_quant_qe_scalar_kernel(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
-                           uint8_t *__restrict__ bytes, const Ctrl *__restrict__ ctrl) {
-    if (ctrl->status != TLC_OK) return;
-    const Quant Q(ctrl->M);
-    const uint64_t P = (n + 4) / 5;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < P;
-         j += (uint64_t)gridDim.x * blockDim.x)
-        bytes[j] = (uint8_t)quant_qe_one(t, err, n, P, j, Q);
+tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
+                    uint8_t *__restrict__ scratch) {
+    for (uint64_t tile = blockIdx.x; tile < T.n2; tile += gridDim.x) {
+        const int si = find_seg<2>(T, tile);
+        const Seg S = get_seg(T, si);
+        float M;
+        const unsigned int status = scale_from_key(maxkey[si], s, M);   // Eq. 1, R6
+        const uint64_t lt = tile - S.k2;
+        if (lt == 0 && threadIdx.x == 0) {
+            tlc_header *h = S.hdr;
+            h->M = M;
+            h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+            h->n = S.n;
+            h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;   // ZRE: set by K3
+            h->status = status;
+            h->reserved = 0;
+        }
+        if (status != TLC_OK) continue;                  // err untouched (R6)
+        uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
+        const Quant Q(M);
+        if (Q.mode == 1) quant_qe_tile(S, bytes, lt * kT2, QuantCmp(Q));   // uniform branch
+        else quant_qe_tile(S, bytes, lt * kT2, Q);
+    }
 }
 
 // ============================================================== K3
-// Chunked single-pass scan: the grid splits the P quartic bytes into one
-// contiguous chunk per CTA (chunk ids taken in order from an atomic counter),
-// and each CTA splits its chunk into one sub-chunk per warp.
-//   phase 1  each warp folds its sub-chunk (rows of 32 lanes x 32 bytes, each
-//            lane's 32 bytes reduced to a literal bit mask) into a run
-//            summary; the CTA publishes the composition of its 8 warps;
-//   phase 2  the CTA composes the summaries of all preceding chunks (they
-//            never wait on later chunks, so this cannot deadlock) -> carry-in;
-//   phase 3  each warp re-reads its sub-chunk (L2-resident: P <= 0.2 n bytes),
-//            scans it and emits every ZRE byte at its final offset.
-// The dependency depth between chunks is one publication, not a chain.
+// Chunked single-pass scan over chunks of kCH3 quartic bytes, numbered globally
+// segment after segment and taken in order from an atomic counter.  Each chunk
+// is split into one sub-range per warp.
+//   phase 1  each warp folds its sub-range (rows of 32 lanes x 32 bytes, each
+//            lane's bytes reduced to a literal bit mask) into a run summary; the
+//            CTA publishes the composition of its 8 warps;
+//   phase 2  it composes the summaries of the segment's preceding chunks (taken
+//            earlier, never waiting on a later one: no deadlock) -> carry-in;
+//   phase 3  each warp re-reads its sub-range (L2-resident) and writes every ZRE
+//            byte at its final offset; the segment's last chunk writes the length.
 constexpr int kK3Threads = kScanThreads;
 constexpr int kK3Seg = 32;                                   // bytes per lane per row
 constexpr int kK3WarpRow = 32 * kK3Seg;                      // 1 KiB per warp row
@@ -258,160 +242,133 @@ __device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint6
 }
 
 __global__ void __launch_bounds__(kK3Threads)
-tlc_zre_kernel(const uint8_t *__restrict__ bytes, uint64_t P, uint64_t chunk,
-               uint8_t *__restrict__ payload, Ctrl *ctrl, unsigned long long *states, tlc_header *hdr) {
+tlc_zre_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s,
+               const uint8_t *__restrict__ scratch, Ctrl *ctrl, unsigned long long *states) {
     __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wagg[kScanWarps];
-    __shared__ unsigned int s_id;
-    if (ctrl->status != TLC_OK) return;
-    const uint64_t nchunks = (P + chunk - 1) / chunk;
-    if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->tile_counter, 1u);
-    __syncthreads();
-    const uint64_t b = s_id;
-    if (b >= nchunks) return;
+    __shared__ unsigned long long s_id;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t lo = b * chunk, hi = tmin<uint64_t>(P, lo + chunk);
-    const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
-    const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
     uint32_t w[8];
+    while (true) {
+        if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k3_counter, 1ull);
+        __syncthreads();
+        const uint64_t id = s_id;
+        __syncthreads();
+        if (id >= T.n3) break;
+        const int si = find_seg<3>(T, id);
+        const Seg S = get_seg(T, si);
+        float M;
+        if (scale_from_key(maxkey[si], s, M) != TLC_OK) continue;      // segment failed in K1
+        const uint8_t *bytes = scratch + S.bytes_off;
+        const uint64_t P = S.P, lc = id - S.k3, nch = (P + kCH3 - 1) / kCH3;
+        const uint64_t lo = lc * kCH3, hi = tmin<uint64_t>(P, lo + kCH3);
+        const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
+        const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
 
-    // ---- phase 1: run summary of the warp's sub-chunk (one per 1 KiB row), then of the chunk
-    RunSum wagg = run_identity();
-    for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
-        const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
-        const uint32_t mask = literal_mask(w);
-        const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-        wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
-    }
-    if (lane == 0) s_wagg[warp] = pack(wagg);
-    __syncthreads();
-    RunSum agg = run_identity();
+        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row), then of the chunk
+        RunSum wagg = run_identity();
+        for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
+            const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
+            const uint32_t mask = literal_mask(w);
+            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+            wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
+        }
+        if (lane == 0) s_wagg[warp] = pack(wagg);
+        __syncthreads();
+        RunSum agg = run_identity();
 #pragma unroll
-    for (int k = 0; k < kScanWarps; k++) agg = compose(agg, unpack(s_wagg[k]));
-    if (threadIdx.x == 0) st_relaxed_u64(states + b, kReady | pack(agg));
+        for (int k = 0; k < kScanWarps; k++) agg = compose(agg, unpack(s_wagg[k]));
+        if (threadIdx.x == 0) st_relaxed_u64(states + id, kReady | pack(agg));
 
-    // ---- phase 2: carry-in = composition of all preceding chunk summaries
-    RunSum part = run_identity();
-    const uint64_t per = (b + kK3Threads - 1) / kK3Threads;
-    const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(b, i0 + per);
-    for (uint64_t i = i0; i < i1; i++) part = compose(part, unpack(wait_ready(states + i) & ~kReady));
-    const RunSum chunk_in = block_reduce_runs(part, s_warp);
-    if (b == nchunks - 1 && threadIdx.x == 0) {
-        uint64_t total;
+        // ---- phase 2: carry-in = composition of the segment's preceding chunk summaries
+        RunSum part = run_identity();
+        const uint64_t per = (lc + kK3Threads - 1) / kK3Threads;
+        const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(lc, i0 + per);
+        for (uint64_t i = i0; i < i1; i++) part = compose(part, unpack(wait_ready(states + S.k3 + i) & ~kReady));
+        const RunSum chunk_in = block_reduce_runs(part, s_warp);
+        if (lc == nch - 1 && threadIdx.x == 0) {
+            uint64_t total;
+            uint32_t carry;
+            run_eval(compose(chunk_in, agg), 0, total, carry);
+            S.hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
+        }
+
+        // ---- phase 3: emission at the final payload offsets
+        RunSum before = chunk_in;
+        for (int k = 0; k < warp; k++) before = compose(before, unpack(s_wagg[k]));
+        uint64_t off;
         uint32_t carry;
-        run_eval(compose(chunk_in, agg), 0, total, carry);
-        hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
-    }
-
-    // ---- phase 3: emission at the final payload offsets
-    RunSum before = chunk_in;
-    for (int k = 0; k < warp; k++) before = compose(before, unpack(s_wagg[k]));
-    uint64_t off;
-    uint32_t carry;
-    run_eval(before, 0, off, carry);              // payload offset and carry at the sub-chunk start
-    for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
-        const uint64_t pos = row + (uint64_t)kK3Seg * lane;
-        const int len = load_seg(bytes, pos, whi, w);
-        const uint32_t mask = literal_mask(w);
-        const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-        const WarpRow r = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
-        uint32_t ex = r.count;                    // exclusive prefix of the lane counts
+        run_eval(before, 0, off, carry);              // payload offset and carry at the sub-range start
+        for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
+            const uint64_t pos = row + (uint64_t)kK3Seg * lane;
+            const int len = load_seg(bytes, pos, whi, w);
+            const uint32_t mask = literal_mask(w);
+            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+            const WarpRow r = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
+            uint32_t ex = r.count;                    // exclusive prefix of the lane counts
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
-            if (lane >= d) ex += y;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
+                if (lane >= d) ex += y;
+            }
+            ex -= r.count;
+            if (len > 0) {
+                uint64_t o = off + ex;
+                uint32_t c = r.carry_in;
+                mask_emit(w, mask, len, c, S.payload, o);
+                if (c > 0 && pos + len == P) S.payload[o] = run_code(c);
+            }
+            off += r.row_count;
+            carry = r.carry_out;
         }
-        ex -= r.count;
-        if (len > 0) {
-            uint64_t o = off + ex;
-            uint32_t c = r.carry_in;
-            mask_emit(w, mask, len, c, payload, o);
-            if (c > 0 && pos + len == P) payload[o] = run_code(c);
-        }
-        off += r.row_count;
-        carry = r.carry_out;
     }
 }
 
-// ============================================================== host launchers
-struct CompressWs {
-    Ctrl *ctrl;
-    unsigned long long *states;
-    unsigned int *partial;
-    uint8_t *bytes;
-    size_t memset_bytes;
-};
+// ============================================================== host side
+static int g_k2_blocks = 0, g_k3_blocks = 0;
 
-static CompressWs carve_compress_ws(void *ws) {
-    const uint64_t tiles = (uint64_t)kMaxSms * 16;       // K3 chunk summaries
-    CompressWs w;
-    char *p = reinterpret_cast<char *>(ws);
-    w.ctrl = reinterpret_cast<Ctrl *>(p);
-    w.states = reinterpret_cast<unsigned long long *>(p + sizeof(Ctrl));
-    const size_t o1 = sizeof(Ctrl) + align256(tiles * sizeof(unsigned long long));
-    w.partial = reinterpret_cast<unsigned int *>(p + o1);
-    const size_t o2 = o1 + align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int));
-    w.bytes = reinterpret_cast<uint8_t *>(p + o2);
-    w.memset_bytes = sizeof(Ctrl) + tiles * sizeof(unsigned long long);
-    return w;
-}
-
-size_t compress_workspace_bytes(uint64_t n) {
-    const uint64_t P = (n + 4) / 5;
-    const uint64_t tiles = (uint64_t)kMaxSms * 16;
-    return sizeof(Ctrl) + align256(tiles * sizeof(unsigned long long)) +
-           align256((size_t)kMaxSms * kK1BlocksPerSm * sizeof(unsigned int)) + align256(P);
-}
-
-static int g_k2_vec_blocks = 0, g_k2_sc_blocks = 0, g_k3_blocks = 0;
-
-int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
-                    tlc_header *hdr, void *ws, cudaStream_t st) {
-    const uint64_t P = (n + 4) / 5;
-    const CompressWs w = carve_compress_ws(ws);
+int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+    const WsLayout L = ws_layout(T, 0);
+    char *base = reinterpret_cast<char *>(ws);
+    Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
+    unsigned int *maxkey = reinterpret_cast<unsigned int *>(base + L.maxkey);
+    unsigned long long *states = reinterpret_cast<unsigned long long *>(base + L.k3st);
+    uint8_t *scratch = reinterpret_cast<uint8_t *>(base + L.bytes);
     const int sms = num_sms();
-    if (cudaMemsetAsync(ws, 0, w.memset_bytes, st) != cudaSuccess) return TLC_ERR_CUDA;
-
-    const bool vec1 = aligned16(t) && aligned16(err);
-    const uint64_t work1 = vec1 ? (n + 3) / 4 : n;
-    const int grid1 = (int)tmin<uint64_t>((uint64_t)sms * kK1BlocksPerSm,
-                                          tmax<uint64_t>(1, (work1 + kK1Threads * 4 - 1) / (kK1Threads * 4)));
+    if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
     {
         KernelScope ks(kK1, st);
-        if (vec1) tlc_absmax_kernel<true><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, w.partial, w.ctrl, hdr);
-        else tlc_absmax_kernel<false><<<grid1, kK1Threads, 0, st>>>(t, err, n, s, use_zre, w.partial, w.ctrl, hdr);
+        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n1, (uint64_t)sms * kK1BlocksPerSm));
+        tlc_absmax_kernel<<<grid, kK1Threads, 0, st>>>(T, maxkey);
     }
-
-    uint8_t *bytes = use_zre ? w.bytes : payload;
-    const bool vec2 = (P % 4 == 0) && aligned16(t) && aligned16(err) && aligned4(bytes);
     {
         KernelScope ks(kK2, st);
-        if (vec2) {
-            if (!g_k2_vec_blocks)
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_vec_blocks, tlc_quant_qe_vec_kernel, kK2Threads, 0);
-            const uint64_t groups = P / 4;
-            const int grid = (int)tmin<uint64_t>((groups + kK2Threads - 1) / kK2Threads,
-                                                 (uint64_t)sms * tmax(1, g_k2_vec_blocks));
-            tlc_quant_qe_vec_kernel<<<tmax(grid, 1), kK2Threads, 0, st>>>(t, err, n, bytes, w.ctrl);
-        } else {
-            if (!g_k2_sc_blocks)
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_sc_blocks, tlc_quant_qe_scalar_kernel, kK2Threads, 0);
-            const int grid = (int)tmin<uint64_t>((P + kK2Threads - 1) / kK2Threads,
-                                                 (uint64_t)sms * tmax(1, g_k2_sc_blocks));
-            tlc_quant_qe_scalar_kernel<<<tmax(grid, 1), kK2Threads, 0, st>>>(t, err, n, bytes, w.ctrl);
-        }
+        if (!g_k2_blocks)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
+        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2, (uint64_t)sms * tmax(1, g_k2_blocks)));
+        tlc_quant_qe_kernel<<<grid, kK2Threads, 0, st>>>(T, maxkey, s, use_zre, scratch);
     }
     if (use_zre) {
         KernelScope ks(kK3, st);
         if (!g_k3_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
-        const uint64_t rows = (P + kScanWarps * kK3WarpRow - 1) / (kScanWarps * kK3WarpRow);
-        const uint64_t grid = tmax<uint64_t>(1, tmin<uint64_t>(rows, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
-        const uint64_t chunk = ((P + grid - 1) / grid + kK3Seg - 1) / kK3Seg * kK3Seg;
-        const uint64_t nch = (P + chunk - 1) / chunk;
-        tlc_zre_kernel<<<(unsigned)nch, kK3Threads, 0, st>>>(w.bytes, P, chunk, payload, w.ctrl, w.states, hdr);
+        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
+        tlc_zre_kernel<<<grid, kK3Threads, 0, st>>>(T, maxkey, s, scratch, ctrl, states);
     }
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
+                    tlc_header *hdr, void *ws, cudaStream_t st) {
+    uint64_t scratch = 0;
+    const SegTable T = single_table(t, err, nullptr, payload, hdr, n, scratch);
+    return launch_compress_table(T, s, use_zre, ws, st);
+}
+
+size_t compress_workspace_bytes(uint64_t n) {
+    uint64_t scratch = 0;
+    const SegTable T = single_table(nullptr, nullptr, nullptr, nullptr, nullptr, n, scratch);
+    return ws_layout(T, scratch).total;
 }
 
 }  // namespace tlc

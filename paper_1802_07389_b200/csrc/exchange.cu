@@ -7,8 +7,8 @@
 // NVSwitch box every rank is both a worker and the server ("owner") of a shard
 // of the compression contexts (plan R17):
 //
-//   push   compress every context with this rank's push error buffer (batched
-//          launch for small contexts, K1-K3 for large ones) straight into a send
+//   push   compress every context with this rank's push error buffer (one
+//          segment-table launch of K1-K3 for all contexts) straight into a send
 //          buffer laid out by owner; one grouped ncclSend/ncclRecv per peer moves
 //          each owner's region (capacity layout: ceil(n/5) bytes per context, so
 //          no host-side size exchange is needed) plus the headers; the owner
@@ -126,12 +126,11 @@ struct tlc_exchange {
     uint8_t *push_send = nullptr, *push_recv = nullptr, *pull_buf = nullptr;
     tlc_header *push_hdr_send = nullptr, *push_hdr_recv = nullptr, *pull_hdr = nullptr;
     unsigned int *d_status = nullptr;
-    void *ws_c = nullptr, *ws_d = nullptr;
-    size_t ws_c_bytes = 0, ws_d_bytes = 0;
-    // batched descriptors (device) and the contexts they cover
-    std::vector<int> small_all, large_all, small_own, large_own;
-    tlc_tensor_desc *d_push = nullptr, *d_agg = nullptr, *d_pullc = nullptr, *d_apply = nullptr;
-    tlc_tensor_desc *h_push = nullptr, *h_apply = nullptr;   // pinned staging
+    void *agg_ws = nullptr;
+    // segment tables: push compress (all contexts), aggregation (owned contexts, one
+    // per source rank, sharing agg_ws), pull compress (owned), apply (all contexts)
+    Table push_tab, pullc_tab, apply_tab;
+    std::vector<Table> agg_tab;
     std::vector<const float *> last_grads;
     std::vector<float *> last_outs;
 };
@@ -195,12 +194,13 @@ int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap,
 int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
     void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
-                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->ws_c, x->ws_d,
-                   x->d_push, x->d_agg, x->d_pullc, x->d_apply};
+                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->agg_ws};
     for (void *p : dev)
         if (p) cudaFree(p);
-    if (x->h_push) cudaFreeHost(x->h_push);
-    if (x->h_apply) cudaFreeHost(x->h_apply);
+    x->push_tab.release();
+    x->pullc_tab.release();
+    x->apply_tab.release();
+    for (Table &t : x->agg_tab) t.release();
     delete x;
     return TLC_OK;
 }
@@ -246,14 +246,6 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
         oe += x->ctx[k].n;
     }
     x->owned_elems = oe;
-    const uint64_t lim = kBatchMaxN;
-    uint64_t max_large = 0;
-    for (int k = 0; k < C; k++) {
-        (x->ctx[k].n <= lim ? x->small_all : x->large_all).push_back(k);
-        if (x->ctx[k].n > lim) max_large = std::max(max_large, x->ctx[k].n);
-    }
-    for (int k : x->owned[x->me]) (x->ctx[k].n <= lim ? x->small_own : x->large_own).push_back(k);
-
     const int nown = (int)x->owned[x->me].size();
     const size_t own_region = x->region_bytes[x->me];
     int rc = TLC_OK;
@@ -270,48 +262,43 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     alloc((void **)&x->push_hdr_recv, (size_t)x->W * nown * sizeof(tlc_header));
     alloc((void **)&x->pull_hdr, (size_t)C * sizeof(tlc_header));
     alloc((void **)&x->d_status, 256);
-    x->ws_c_bytes = max_large ? compress_workspace_bytes(max_large) : 0;
-    x->ws_d_bytes = max_large ? decompress_workspace_bytes(max_large) : 0;
-    alloc(&x->ws_c, x->ws_c_bytes);
-    alloc(&x->ws_d, x->ws_d_bytes);
-    alloc((void **)&x->d_push, x->small_all.size() * sizeof(tlc_tensor_desc));
-    alloc((void **)&x->d_apply, x->small_all.size() * sizeof(tlc_tensor_desc));
-    alloc((void **)&x->d_agg, (size_t)x->W * x->small_own.size() * sizeof(tlc_tensor_desc));
-    alloc((void **)&x->d_pullc, x->small_own.size() * sizeof(tlc_tensor_desc));
-    if (rc == TLC_OK && cudaMallocHost((void **)&x->h_push, std::max<size_t>(1, x->small_all.size()) * sizeof(tlc_tensor_desc)) != cudaSuccess) rc = TLC_ERR_CUDA;
-    if (rc == TLC_OK && cudaMallocHost((void **)&x->h_apply, std::max<size_t>(1, x->small_all.size()) * sizeof(tlc_tensor_desc)) != cudaSuccess) rc = TLC_ERR_CUDA;
     if (rc == TLC_OK) {
         // error buffers start at zero (R20)
         rc = cuda_ok(cudaMemset(x->push_err, 0, std::max<size_t>(x->total_elems * sizeof(float), 256)));
         if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->pull_err, 0, std::max<size_t>(x->owned_elems * sizeof(float), 256)));
     }
-    if (rc == TLC_OK) {
-        // descriptors that only point at exchange-owned memory are built once
-        std::vector<tlc_tensor_desc> agg, pullc;
-        for (int w = 0; w < x->W; w++)
-            for (int k : x->small_own) {
-                const Ctx &c = x->ctx[k];
-                tlc_tensor_desc d{};
-                d.payload = x->push_recv + (size_t)w * own_region + c.region_off;
-                d.hdr = x->push_hdr_recv + (size_t)w * nown + c.slot;
-                d.out = x->owned_buf + c.owned_off;
-                d.n = c.n;
-                agg.push_back(d);
-            }
-        for (int k : x->small_own) {
-            const Ctx &c = x->ctx[k];
-            tlc_tensor_desc d{};
+    if (rc == TLC_OK && nown) {
+        // tables that only point at exchange-owned memory are built once
+        std::vector<tlc_tensor_desc> agg(nown), pullc(nown);
+        for (int q = 0; q < nown; q++) {
+            const Ctx &c = x->ctx[x->owned[x->me][q]];
+            tlc_tensor_desc &d = pullc[q];
+            d = tlc_tensor_desc{};
             d.t = x->owned_buf + c.owned_off;
             d.err = x->pull_err + c.owned_off;
             d.payload = x->pull_buf + x->region_start[x->me] + c.region_off;
             d.hdr = x->pull_hdr + x->hdr_start[x->me] + c.slot;
             d.n = c.n;
-            pullc.push_back(d);
         }
-        if (!agg.empty())
-            rc = cuda_ok(cudaMemcpy(x->d_agg, agg.data(), agg.size() * sizeof(tlc_tensor_desc), cudaMemcpyHostToDevice));
-        if (rc == TLC_OK && !pullc.empty())
-            rc = cuda_ok(cudaMemcpy(x->d_pullc, pullc.data(), pullc.size() * sizeof(tlc_tensor_desc), cudaMemcpyHostToDevice));
+        rc = x->pullc_tab.create(pullc.data(), nown, true, nullptr);
+        x->agg_tab.resize(x->W);
+        for (int w = 0; rc == TLC_OK && w < x->W; w++) {
+            for (int q = 0; q < nown; q++) {
+                const Ctx &c = x->ctx[x->owned[x->me][q]];
+                tlc_tensor_desc &d = agg[q];
+                d = tlc_tensor_desc{};
+                d.payload = x->push_recv + (size_t)w * own_region + c.region_off;
+                d.hdr = x->push_hdr_recv + (size_t)w * nown + c.slot;
+                d.out = x->owned_buf + c.owned_off;
+                d.n = c.n;
+            }
+            if (w == 0) {
+                rc = x->agg_tab[0].create(agg.data(), nown, false, nullptr);
+                if (rc == TLC_OK) x->agg_ws = nullptr;   // table 0 owns the shared workspace
+            } else {
+                rc = x->agg_tab[w].create(agg.data(), nown, false, x->agg_tab[0].ws);
+            }
+        }
     }
     if (rc != TLC_OK) {
         tlc_exchange_destroy(x);
@@ -360,41 +347,30 @@ uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction) {
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream) {
     if (!x || !grads || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int T = (int)x->tensor_sizes.size();
+    const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
     for (int i = 0; i < T; i++)
         if (!grads[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
     int rc = TLC_OK;
     // (1) compress every context with this rank's push error buffer into the send layout
     bool same = x->last_grads.size() == (size_t)T;
     for (int i = 0; same && i < T; i++) same = x->last_grads[i] == grads[i];
-    if (!same && !x->small_all.empty()) {
-        cudaStreamSynchronize(st);   // staging may still be in use by a previous copy
-        for (size_t q = 0; q < x->small_all.size(); q++) {
-            const Ctx &c = x->ctx[x->small_all[q]];
-            tlc_tensor_desc d{};
-            d.t = grads[c.tensor] + c.lo;
-            d.err = x->push_err + c.elem_off;
-            d.payload = x->push_send + x->region_start[c.owner] + c.region_off;
-            d.hdr = x->push_hdr_send + x->hdr_start[c.owner] + c.slot;
-            d.n = c.n;
-            x->h_push[q] = d;
+    if (!same) {
+        std::vector<tlc_tensor_desc> d(C);
+        for (int k = 0; k < C; k++) {
+            const Ctx &c = x->ctx[k];
+            d[k] = tlc_tensor_desc{};
+            d[k].t = grads[c.tensor] + c.lo;
+            d[k].err = x->push_err + c.elem_off;
+            d[k].payload = x->push_send + x->region_start[c.owner] + c.region_off;
+            d[k].hdr = x->push_hdr_send + x->hdr_start[c.owner] + c.slot;
+            d[k].n = c.n;
         }
-        rc = cuda_ok(cudaMemcpyAsync(x->d_push, x->h_push, x->small_all.size() * sizeof(tlc_tensor_desc),
-                                     cudaMemcpyHostToDevice, st));
+        if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;   // table may be in use
+        rc = x->push_tab.d ? x->push_tab.update(d.data()) : x->push_tab.create(d.data(), C, true, nullptr);
         if (rc != TLC_OK) return rc;
+        x->last_grads.assign(grads, grads + T);
     }
-    x->last_grads.assign(grads, grads + T);
-    if (!x->small_all.empty()) {
-        rc = launch_compress_batched((int)x->small_all.size(), x->d_push, s, use_zre ? 1 : 0, st);
-        if (rc != TLC_OK) return rc;
-    }
-    for (int k : x->large_all) {
-        const Ctx &c = x->ctx[k];
-        rc = launch_compress(grads[c.tensor] + c.lo, x->push_err + c.elem_off, c.n, s, use_zre ? 1 : 0,
-                             x->push_send + x->region_start[c.owner] + c.region_off,
-                             x->push_hdr_send + x->hdr_start[c.owner] + c.slot, x->ws_c, st);
-        if (rc != TLC_OK) return rc;
-    }
+    if ((rc = launch_compress_table(x->push_tab.T, s, use_zre ? 1 : 0, x->push_tab.ws, st)) != TLC_OK) return rc;
     // (2) every owner receives its contexts' payloads and headers from every rank
     const int nown = (int)x->owned[x->me].size();
     const size_t own_region = x->region_bytes[x->me];
@@ -415,18 +391,8 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
     if (x->owned_elems) {
         if ((rc = cuda_ok(cudaMemsetAsync(x->owned_buf, 0, x->owned_elems * sizeof(float), st))) != TLC_OK) return rc;
         for (int w = 0; w < x->W; w++) {
-            if (!x->small_own.empty()) {
-                rc = launch_decompress_batched((int)x->small_own.size(), x->d_agg + (size_t)w * x->small_own.size(),
-                                               TLC_MODE_ACCUMULATE, st);
-                if (rc != TLC_OK) return rc;
-            }
-            for (int k : x->large_own) {
-                const Ctx &c = x->ctx[k];
-                rc = launch_decompress(x->push_recv + (size_t)w * own_region + c.region_off,
-                                       x->push_hdr_recv + (size_t)w * nown + c.slot, c.n,
-                                       x->owned_buf + c.owned_off, TLC_MODE_ACCUMULATE, x->ws_d, st);
-                if (rc != TLC_OK) return rc;
-            }
+            rc = launch_decompress_table(x->agg_tab[w].T, TLC_MODE_ACCUMULATE, x->agg_tab[w].ws, st);
+            if (rc != TLC_OK) return rc;
         }
         KernelScope ks(kK8, st);
         const int grid = (int)std::min<uint64_t>((x->owned_elems + 255) / 256, (uint64_t)num_sms() * 8);
@@ -439,22 +405,14 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream) {
     if (!x || !outs || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int T = (int)x->tensor_sizes.size();
+    const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
     for (int i = 0; i < T; i++)
         if (!outs[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
     int rc = TLC_OK;
     // (1) the owner compresses its shard of the model delta ONCE (shared pull)
-    if (!x->small_own.empty()) {
-        rc = launch_compress_batched((int)x->small_own.size(), x->d_pullc, s, use_zre ? 1 : 0, st);
-        if (rc != TLC_OK) return rc;
-    }
-    for (int k : x->large_own) {
-        const Ctx &c = x->ctx[k];
-        rc = launch_compress(x->owned_buf + c.owned_off, x->pull_err + c.owned_off, c.n, s, use_zre ? 1 : 0,
-                             x->pull_buf + x->region_start[x->me] + c.region_off,
-                             x->pull_hdr + x->hdr_start[x->me] + c.slot, x->ws_c, st);
-        if (rc != TLC_OK) return rc;
-    }
+    if (x->owned_elems &&
+        (rc = launch_compress_table(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st)) != TLC_OK)
+        return rc;
     // (2) all-gather of the owners' regions (grouped send/recv, sizes differ per owner)
     ncclComm_t nc = x->comm->nccl;
     if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
@@ -473,34 +431,22 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
     // (3) every rank applies every context to its full-size output (ACCUMULATE, R16)
     bool same = x->last_outs.size() == (size_t)T;
     for (int i = 0; same && i < T; i++) same = x->last_outs[i] == outs[i];
-    if (!same && !x->small_all.empty()) {
-        cudaStreamSynchronize(st);
-        for (size_t q = 0; q < x->small_all.size(); q++) {
-            const Ctx &c = x->ctx[x->small_all[q]];
-            tlc_tensor_desc d{};
-            d.out = outs[c.tensor] + c.lo;
-            d.payload = x->pull_buf + x->region_start[c.owner] + c.region_off;
-            d.hdr = x->pull_hdr + x->hdr_start[c.owner] + c.slot;
-            d.n = c.n;
-            x->h_apply[q] = d;
+    if (!same) {
+        std::vector<tlc_tensor_desc> d(C);
+        for (int k = 0; k < C; k++) {
+            const Ctx &c = x->ctx[k];
+            d[k] = tlc_tensor_desc{};
+            d[k].out = outs[c.tensor] + c.lo;
+            d[k].payload = x->pull_buf + x->region_start[c.owner] + c.region_off;
+            d[k].hdr = x->pull_hdr + x->hdr_start[c.owner] + c.slot;
+            d[k].n = c.n;
         }
-        rc = cuda_ok(cudaMemcpyAsync(x->d_apply, x->h_apply, x->small_all.size() * sizeof(tlc_tensor_desc),
-                                     cudaMemcpyHostToDevice, st));
+        if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;
+        rc = x->apply_tab.d ? x->apply_tab.update(d.data()) : x->apply_tab.create(d.data(), C, false, nullptr);
         if (rc != TLC_OK) return rc;
+        x->last_outs.assign(outs, outs + T);
     }
-    x->last_outs.assign(outs, outs + T);
-    if (!x->small_all.empty()) {
-        rc = launch_decompress_batched((int)x->small_all.size(), x->d_apply, TLC_MODE_ACCUMULATE, st);
-        if (rc != TLC_OK) return rc;
-    }
-    for (int k : x->large_all) {
-        const Ctx &c = x->ctx[k];
-        rc = launch_decompress(x->pull_buf + x->region_start[c.owner] + c.region_off,
-                               x->pull_hdr + x->hdr_start[c.owner] + c.slot, c.n, outs[c.tensor] + c.lo,
-                               TLC_MODE_ACCUMULATE, x->ws_d, st);
-        if (rc != TLC_OK) return rc;
-    }
-    return TLC_OK;
+    return launch_decompress_table(x->apply_tab.T, TLC_MODE_ACCUMULATE, x->apply_tab.ws, st);
 }
 
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream) {

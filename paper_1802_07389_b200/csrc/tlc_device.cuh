@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/tlc.h"
+#include "tlc_launch.h"
 
 namespace tlc {
 
@@ -20,12 +21,9 @@ constexpr uint32_t kMaxRun = 14;
 // cudaMemsetAsync at the start of each call, together with the look-back
 // tile states that follow it).
 struct Ctrl {
-    unsigned int tile_counter;   // dynamic tile ids (forward-progress ordering)
-    unsigned int done_counter;   // K1 last-block detection
-    float M;                     // fl(max|u| * s) (Eq. 1)
-    unsigned int status;         // tlc_status from K1
-    unsigned int maxkey;         // max of (bits(u) & 0x7fffffff)
-    unsigned int pad[59];
+    unsigned long long k3_counter;   // dynamic K3 chunk ids (forward-progress ordering)
+    unsigned long long k4_counter;   // dynamic K4 chunk ids
+    unsigned int pad[60];
 };
 static_assert(sizeof(Ctrl) == 256, "ctrl is one 256-byte block");
 
@@ -440,6 +438,34 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
     const uint32_t k0 = r.mixbal ? ctz32(r.mixbal) : 0u;
     const uint32_t lead = __shfl_sync(0xffffffffu, mask ? ctz32(mask) : 0u, (int)k0) + 32u * k0;
     return row_summary(r.mixbal != 0, lead, r.row_count, r.carry_out, row_len);
+}
+
+// ---------------------------------------------------------------- segment lookup
+template <int F>
+__device__ __forceinline__ uint64_t seg_first(const Seg &s) {
+    return F == 1 ? s.k1 : F == 2 ? s.k2 : F == 3 ? s.k3 : F == 4 ? s.k4 : s.k5;
+}
+// segment holding global item `item` of kernel F
+template <int F>
+__device__ __forceinline__ int find_seg(const SegTable &T, uint64_t item) {
+    if (T.count == 1) return 0;
+    int lo = 0, hi = T.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (seg_first<F>(T.d[mid]) <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+__device__ __forceinline__ Seg get_seg(const SegTable &T, int i) { return T.count == 1 ? T.one : T.d[i]; }
+
+// M and the compressor status of a segment from its max key (Eq. 1, R6)
+__device__ __forceinline__ unsigned int scale_from_key(unsigned int key, float s, float &M) {
+    M = 0.0f;
+    if (key >= 0x7f800000u) return TLC_ERR_NONFINITE;      // NaN or Inf in u
+    M = __fmul_rn(__uint_as_float(key), s);
+    if (isinf(M)) { M = 0.0f; return TLC_ERR_RANGE; }
+    return TLC_OK;
 }
 
 // ---------------------------------------------------------------- decoder helpers

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "../../include/tlc.h"
@@ -34,6 +35,8 @@ inline int num_sms() {
 // Kernel ids for launch counting / profiling (prof.cu).
 enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7, kNumKernelIds = 8 };
 
+struct Ctrl;
+
 // RAII bracket around one kernel launch: counts it and, when profiling is on,
 // records CUDA events before and after it on `st`.
 class KernelScope {
@@ -46,16 +49,72 @@ class KernelScope {
     void *a_;
 };
 
+// ---------------------------------------------------------------- segments
+// Every kernel works on a table of independent tensors ("segments"): a single
+// tlc_compress call is a one-segment table passed by value (no upload), a batch
+// (tlc_batch_*) is a device-resident table.  Work items of each kernel are
+// numbered globally, segment after segment; a CTA maps an item to its segment by
+// a binary search over the per-segment first-item numbers.
+constexpr uint64_t kT1 = 65536;     // K1 tile: elements
+constexpr uint64_t kT2 = 4096;      // K2 tile: quartic positions (1024 groups of 4)
+constexpr uint64_t kCH3 = 32768;    // K3 chunk: quartic bytes (8 warps x 4 rows of 1 KiB)
+constexpr uint64_t kCH4 = 16384;    // K4 chunk: payload bytes (capacity based)
+constexpr uint64_t kT5 = 4096;      // K5 tile: quartic positions per output tile
+
+enum SegFlags : uint32_t { kSegVec2 = 1u, kSegVec5 = 2u, kSegVec1 = 4u };
+
+struct Seg {
+    const float *t;
+    float *err;
+    float *out;
+    uint8_t *payload;
+    tlc_header *hdr;
+    uint64_t n, P;
+    uint64_t k1, k2, k3, k4, k5;    // first global item of each kernel
+    uint64_t bytes_off;             // quartic scratch offset (compress with ZRE)
+    uint32_t flags, pad;
+};
+
+struct SegTable {
+    const Seg *d;                   // device table when count > 1
+    Seg one;                        // the segment when count == 1
+    int count;
+    uint64_t n1, n2, n3, n4, n5;    // total items per kernel
+};
+
+// Workspace layout of one table: control block, per-segment max keys, K3 / K4
+// chunk states, K5 seek entries, quartic scratch.
+struct WsLayout {
+    size_t ctrl, maxkey, k3st, k4st, seek, bytes, memset_c, memset_d, total;
+};
+
+WsLayout ws_layout(const SegTable &T, uint64_t scratch_bytes);
+void seg_items(Seg &s, uint64_t &c1, uint64_t &c2, uint64_t &c3, uint64_t &c4, uint64_t &c5);
+SegTable single_table(const float *t, float *err, float *out, uint8_t *payload, tlc_header *hdr, uint64_t n,
+                      uint64_t &scratch);
+int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st);
 int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
                     tlc_header *hdr, void *ws, cudaStream_t st);
 size_t compress_workspace_bytes(uint64_t n);
-
-constexpr uint64_t kBatchMaxN = 5 * 32768;   // P <= 32 KiB of shared memory per CTA
-int launch_compress_batched(int count, const tlc_tensor_desc *d_descs, float s, int use_zre, cudaStream_t st);
-int launch_decompress_batched(int count, const tlc_tensor_desc *d_descs, int mode, cudaStream_t st);
-
 int launch_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *out, int mode,
                       void *ws, cudaStream_t st);
 size_t decompress_workspace_bytes(uint64_t n);
+uint32_t seg_flags(const Seg &s);
+
+// A device-resident segment table with its workspace (batches, exchange).
+struct Table {
+    int count = 0;
+    std::vector<Seg> host;
+    Seg *d = nullptr;
+    SegTable T{};
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    bool own_ws = false;
+    int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);
+    int update(const tlc_tensor_desc *descs);
+    int upload();
+    void release();
+};
+int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t st);
 
 }  // namespace tlc

@@ -1,5 +1,5 @@
-"""Batched small-tensor path (K6/K7, tlc_compress_batched / tlc_decompress_batched)
-vs the CPU oracle, tensor by tensor, bit for bit (BASELINE configs[1]: ResNet-110)."""
+"""Batches of tensors (tlc_batch_*, segment tables through K1-K5) vs the CPU
+oracle, tensor by tensor, bit for bit (BASELINE configs[1]: ResNet-110)."""
 import numpy as np
 import pytest
 
@@ -59,9 +59,8 @@ def test_resnet110_batched(T, s):
     _run_steps(T, sizes, 3, s, True, lambda k, n, step: synth.layer_gradient(n, mus[k], 2, 0, k, step))
 
 
-def test_mixed_sizes_and_large_fallback(T):
-    lim = T.tlc_batched_max_elements()
-    sizes = list(range(1, 12)) + [69, 70, 71, 1000, 5 * 2048 + 3, lim, lim + 1, 400_003]
+def test_mixed_sizes(T):
+    sizes = list(range(1, 12)) + [69, 70, 71, 1000, 5 * 2048 + 3, 163_840, 163_841, 400_003, 5 * 65536 + 7]
     for use_zre in (True, False):
         _run_steps(T, sizes, 2, 1.5, use_zre, lambda k, n, step: synth.runs_adversarial(n, 1.0, 5, k, step)
                    if k % 2 else synth.gaussian(n, 6, k, step))

@@ -54,7 +54,7 @@ def _check(world, results, sizes=SIZES, steps=STEPS):
     outs = [[np.zeros(n, f32) for n in sizes] for _ in range(world)]
     means_steps = []
     for step in range(steps):
-        means, _, _ = ps.push([_grads(r, step, sizes) for r in range(world)], S)
+        means, _ = ps.push([_grads(r, step, sizes) for r in range(world)], S)
         ps.pull(means, outs, S)
         means_steps.append(means)
     for r in range(world):
