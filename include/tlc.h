@@ -185,7 +185,7 @@ int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
  *                     ranks over host `sizes[num_tensors]`: context k covers
  *                     elements [lo[k], hi[k]) of tensor[k] and is owned by
  *                     owner[k].  Pure host computation (no GPU).
- * tlc_exchange_create allocates every buffer of the exchange for the tensor
+ * tlc_exchange_create (world <= 8) allocates every buffer of the exchange for the tensor
  *                     list (error buffers zeroed, R20): push error buffers for
  *                     all contexts, the owned (aggregate / delta) buffer and
  *                     pull error buffers for this rank's contexts, send/receive
@@ -196,7 +196,8 @@ int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
  *                     headers, and leaves in the owned buffer (see
  *                     tlc_exchange_owned_buffer) the mean over ranks of the
  *                     decompressed pushes: rank-ordered sum from +0, zero trits
- *                     skipped, then / world in fp32 (R15).  The caller may turn
+ *                     skipped, then / world in fp32 (R15) -- one fused
+ *                     decompress-aggregate pass over the W received payloads.  The caller may turn
  *                     that mean into a model delta in place (R18) before pull.
  * tlc_exchange_pull   compresses this rank's owned buffer once with its pull
  *                     error buffers, all-gathers every owner's payloads, and

@@ -124,11 +124,89 @@ struct K5Smem {
     unsigned int warp_sum[kK5Threads / 32];
 };
 
+// Expand the payload bytes covering output tile lt (positions [J0, J0+tl)) into
+// E[0, tl): 121 prefill, then only the literal bytes are written at their scanned
+// positions (zero-run codes expand to 121s).  seek points at the segment's seek
+// entries.  Without ZRE the bytes are copied (a literal > 242 returns true:
+// FORMAT).  Ends with E complete and visible to the whole block.
+__device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, const uint8_t *__restrict__ payload,
+                                            bool zre, uint64_t Z, const unsigned long long *__restrict__ seek,
+                                            uint64_t lt, uint64_t ntiles, uint64_t J0, int tl) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bool bad = false;
+    if (zre) {
+        *reinterpret_cast<uint4 *>(E + kK5BytesPerThread * threadIdx.x) =
+            make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
+        const unsigned long long sk = seek[lt];
+        const uint64_t bi = sk >> 4;                      // payload byte covering J0
+        const int skip = (int)(sk & 15);                  // J0 - (first position of that byte)
+        const uint64_t be = lt + 1 < ntiles ? (seek[lt + 1] >> 4) : Z - 1;   // last byte needed
+        const int wl = (int)(be - bi) + 1;                // <= kT5 + 1
+        // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
+        // to 4; the last thread also owns the next 4 bytes, so the <= kT5 bytes from bi
+        // on are always covered
+        const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;
+        const uint64_t w0 = bi & ~3ull;
+        const int sh = (int)(bi - w0);
+        constexpr int NW = kK5Words + 1;
+        const int nwords = threadIdx.x == kK5Threads - 1 ? NW : kK5Words;
+        uint32_t wd[NW];
+#pragma unroll
+        for (int h = 0; h < NW; h++) {
+            wd[h] = 0;
+            if (h >= nwords) continue;
+            const int r = kK5BytesPerThread * threadIdx.x + 4 * h - sh;   // window offset of the word
+            if (pal && r >= 0 && r + 3 < wl) {
+                wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + kK5Words * threadIdx.x + h);
+            } else {
+                uint32_t x = 0;
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (r + c >= 0 && r + c < wl) x |= (uint32_t)payload[bi + r + c] << (8 * c);
+                wd[h] = x;
+            }
+        }
+        uint32_t len[4 * NW], sum = 0;
+#pragma unroll
+        for (int m = 0; m < 4 * NW; m++) {
+            const int r = kK5BytesPerThread * threadIdx.x + m - sh;
+            const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+            len[m] = (m < 4 * nwords && r >= 0 && r < wl) ? zre_len(b) : 0u;
+            sum += len[m];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) warp_sum[warp] = x;
+        __syncthreads();
+        uint32_t wofs = 0;
+#pragma unroll
+        for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? warp_sum[w] : 0u;
+        int p = (int)(wofs + x - sum) - skip;   // tile position of this thread's first byte
+#pragma unroll
+        for (int m = 0; m < 4 * NW; m++) {
+            const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+            if (len[m] == 1 && p >= 0 && p < tl) E[p] = (uint8_t)b;   // literal byte
+            p += (int)len[m];
+        }
+        __syncthreads();                                  // warp_sum reuse; E complete
+    } else {
+        for (int jl = threadIdx.x; jl < tl; jl += kK5Threads) {
+            uint8_t v = payload[J0 + jl];
+            if (v > 242) { bad = true; v = kZeroGroup; }
+            E[jl] = v;
+        }
+    }
+    return __syncthreads_or(bad);
+}
+
 template <int kMode>
 __global__ void __launch_bounds__(kK5Threads)
 tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict__ seek) {
     __shared__ K5Smem sm;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n5; tile += gridDim.x) {
         const int si = find_seg<5>(T, tile);
@@ -169,74 +247,8 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict
             lim[i] = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
             ob[i] = S.out + e0;
         }
-        bool bad = false;
-        if (zre) {
-            // pre-fill with 121: zero-run codes expand to 121s and need no further writes
-            *reinterpret_cast<uint4 *>(sm.E + kK5BytesPerThread * threadIdx.x) =
-                make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
-            const unsigned long long sk = seek[S.k5 + lt];
-            const uint64_t bi = sk >> 4;                      // payload byte covering J0
-            const int skip = (int)(sk & 15);                  // J0 - (first position of that byte)
-            const uint64_t be = lt + 1 < ntiles ? (seek[S.k5 + lt + 1] >> 4) : Z - 1;   // last byte needed
-            const int wl = (int)(be - bi) + 1;                // <= kT5 + 1
-            // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
-            // to 4; the last thread also owns the next 4 bytes, so the <= kT5 bytes from
-            // bi on are always covered
-            const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;
-            const uint64_t w0 = bi & ~3ull;
-            const int sh = (int)(bi - w0);
-            constexpr int NW = kK5Words + 1;
-            const int nwords = threadIdx.x == kK5Threads - 1 ? NW : kK5Words;
-            uint32_t wd[NW];
-#pragma unroll
-            for (int h = 0; h < NW; h++) {
-                wd[h] = 0;
-                if (h >= nwords) continue;
-                const int r = kK5BytesPerThread * threadIdx.x + 4 * h - sh;   // window offset of the word
-                if (pal && r >= 0 && r + 3 < wl) {
-                    wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + kK5Words * threadIdx.x + h);
-                } else {
-                    uint32_t x = 0;
-#pragma unroll
-                    for (int c = 0; c < 4; c++)
-                        if (r + c >= 0 && r + c < wl) x |= (uint32_t)payload[bi + r + c] << (8 * c);
-                    wd[h] = x;
-                }
-            }
-            uint32_t len[4 * NW], sum = 0;
-#pragma unroll
-            for (int m = 0; m < 4 * NW; m++) {
-                const int r = kK5BytesPerThread * threadIdx.x + m - sh;
-                const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-                len[m] = (m < 4 * nwords && r >= 0 && r < wl) ? zre_len(b) : 0u;
-                sum += len[m];
-            }
-            uint32_t x = sum;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-                if (lane >= d) x += y;
-            }
-            if (lane == 31) sm.warp_sum[warp] = x;
-            __syncthreads();
-            uint32_t wofs = 0;
-#pragma unroll
-            for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? sm.warp_sum[w] : 0u;
-            int p = (int)(wofs + x - sum) - skip;   // tile position of this thread's first byte
-#pragma unroll
-            for (int m = 0; m < 4 * NW; m++) {
-                const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-                if (len[m] == 1 && p >= 0 && p < tl) sm.E[p] = (uint8_t)b;   // literal byte
-                p += (int)len[m];
-            }
-        } else {
-            for (int jl = threadIdx.x; jl < tl; jl += kK5Threads) {
-                uint8_t v = payload[J0 + jl];
-                if (v > 242) { bad = true; v = kZeroGroup; }
-                sm.E[jl] = v;
-            }
-        }
-        if (__syncthreads_or(bad)) {                       // literal > 242 without ZRE
+        const bool bad = expand_tile(sm.E, sm.warp_sum, payload, zre, Z, seek + S.k5, lt, ntiles, J0, tl);
+        if (bad) {                                         // literal > 242 without ZRE
             if (threadIdx.x == 0) raise_format(S.hdr);
             continue;
         }
@@ -290,6 +302,135 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict
             }
         }
     }
+}
+
+// ============================================================== K5m (exchange aggregation)
+// The owner's fused decompress-aggregate of W pushed payloads per owned
+// context (row a6, multi-source variant; reading R15): for each output element
+// acc = +0, then for w = 0..W-1 in rank order acc = fl(acc + M_w*q_w) where
+// q_w != 0, then mean = fl(acc / W) -- written once.  A = owned contexts (out,
+// n); X = the W x |A| received (payload, header) rows, row w*|A| + q, whose
+// seek entries K4 wrote.  A source whose header is not OK contributes nothing.
+constexpr int kMaxSources = 8;
+
+struct K5mSmem {
+    alignas(16) uint8_t E[kMaxSources][kT5];
+    uint16_t lut[256];                   // bit i = (digit_i != 1), bit 8+i = (digit_i == 0)
+    float M[kMaxSources];
+    int ok[kMaxSources];
+    unsigned int warp_sum[kK5Threads / 32];
+};
+
+__global__ void __launch_bounds__(kK5Threads)
+tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *__restrict__ seek) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    K5mSmem &sm = *reinterpret_cast<K5mSmem *>(smem_raw);
+    for (int v = threadIdx.x; v < 256; v += kK5Threads) {
+        uint32_t w = 0, r = v < 243 ? v : 121;
+#pragma unroll
+        for (int i = 4; i >= 0; i--) {
+            const uint32_t d = r % 3u;
+            r /= 3u;
+            w |= (uint32_t)(d != 1) << i;
+            w |= (uint32_t)(d == 0) << (8 + i);
+        }
+        sm.lut[v] = (uint16_t)w;
+    }
+    const float Wf = (float)W;
+    for (uint64_t tile = blockIdx.x; tile < A.n5; tile += gridDim.x) {
+        const int q = find_seg<5>(A, tile);
+        const Seg S = get_seg(A, q);
+        const uint64_t P = S.P, n = S.n, lt = tile - S.k5, ntiles = (P + kT5 - 1) / kT5;
+        const uint64_t J0 = lt * kT5;
+        const int tl = (int)tmin<uint64_t>(kT5, P - J0);
+        __syncthreads();                                   // previous tile's readers are done
+        for (int w = 0; w < W; w++) {
+            const Seg R = get_seg(X, w * A.count + q);
+            const tlc_header *h = R.hdr;
+            const bool ok = h->status == TLC_OK;           // uniform
+            if (threadIdx.x == 0) { sm.ok[w] = ok; sm.M[w] = h->M; }
+            if (!ok) continue;
+            const bool bad = expand_tile(sm.E[w], sm.warp_sum, R.payload, (h->flags & TLC_FLAG_ZRE) != 0,
+                                         h->payload_len, seek + R.k5, lt, ntiles, J0, tl);
+            if (bad && threadIdx.x == 0) { raise_format(R.hdr); sm.ok[w] = 0; }
+        }
+        __syncthreads();
+        int lim[5];
+        float *ob[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e0 = (uint64_t)i * P + J0;
+            lim[i] = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
+            ob[i] = S.out + e0;
+        }
+        const bool vec = (S.flags & kSegVec5) != 0;
+#pragma unroll
+        for (int k = 0; k < kK5BytesPerThread / 4; k++) {
+            const int jl = 4 * threadIdx.x + 4 * kK5Threads * k;
+            if (jl >= tl) break;
+            float acc[5][4];
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0
+            for (int w = 0; w < W; w++) {                          // rank order
+                if (!sm.ok[w]) continue;
+                const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E[w] + jl);
+                if (w4 == 0x79797979u) continue;                   // all trits zero: nothing to add
+                const float Mw = sm.M[w];
+                uint32_t L[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) L[c] = sm.lut[(w4 >> (8 * c)) & 0xffu];
+#pragma unroll
+                for (int i = 0; i < 5; i++)
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if ((L[c] >> i) & 1u)
+                            acc[i][c] = __fadd_rn(acc[i][c], ((L[c] >> (8 + i)) & 1u) ? -Mw : Mw);
+            }
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                float r[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) r[c] = __fdiv_rn(acc[i][c], Wf);     // R15
+                float *o = ob[i] + jl;
+                if (vec && jl + 3 < lim[i]) {
+                    __stcs(reinterpret_cast<float4 *>(o), make_float4(r[0], r[1], r[2], r[3]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if (jl + c < lim[i]) o[c] = r[c];
+                }
+            }
+        }
+    }
+}
+
+int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st) {
+    // X: K4 over every received payload (validation + seek entries), then one fused pass
+    if (W < 1 || W > kMaxSources) return TLC_ERR_ARG;
+    const WsLayout L = ws_layout(X, 0);
+    char *base = reinterpret_cast<char *>(xws);
+    Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
+    unsigned long long *states = reinterpret_cast<unsigned long long *>(base + L.k4st);
+    unsigned long long *seek = reinterpret_cast<unsigned long long *>(base + L.seek);
+    if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
+    if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
+    const int sms = num_sms();
+    {
+        KernelScope ks(kK4, st);
+        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(X.n4, (uint64_t)sms * 8));
+        tlc_zre_scan_kernel<<<grid, kK4Threads, 0, st>>>(X, ctrl, states, seek);
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K5mSmem));
+        attr = true;
+    }
+    KernelScope ks(kK6, st);
+    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * 4));
+    tlc_aggregate_kernel<<<grid, kK5Threads, sizeof(K5mSmem), st>>>(A, X, W, seek);
+    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
 // ============================================================== host side

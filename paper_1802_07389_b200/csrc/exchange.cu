@@ -50,13 +50,6 @@ struct Ctx {
     size_t owned_off;   // offset in the owner's flat owned buffer (valid on the owner)
 };
 
-// mean = sum / W in fp32 (R15), in place over the owner's flat buffer
-__global__ void tlc_scale_kernel(float *__restrict__ x, uint64_t n, float W) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        x[i] = __fdiv_rn(x[i], W);
-}
-
 // worst (largest) status over a header array -> *out (atomicMax)
 __global__ void tlc_status_kernel(const tlc_header *__restrict__ h, int count, unsigned int *out) {
     unsigned int m = 0;
@@ -126,11 +119,9 @@ struct tlc_exchange {
     uint8_t *push_send = nullptr, *push_recv = nullptr, *pull_buf = nullptr;
     tlc_header *push_hdr_send = nullptr, *push_hdr_recv = nullptr, *pull_hdr = nullptr;
     unsigned int *d_status = nullptr;
-    void *agg_ws = nullptr;
-    // segment tables: push compress (all contexts), aggregation (owned contexts, one
-    // per source rank, sharing agg_ws), pull compress (owned), apply (all contexts)
-    Table push_tab, pullc_tab, apply_tab;
-    std::vector<Table> agg_tab;
+    // segment tables: push compress (all contexts), aggregation (owned contexts A and
+    // the W x |A| received payloads X), pull compress (owned), apply (all contexts)
+    Table push_tab, pullc_tab, apply_tab, a_tab, x_tab;
     std::vector<const float *> last_grads;
     std::vector<float *> last_outs;
 };
@@ -194,19 +185,21 @@ int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap,
 int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
     void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
-                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->agg_ws};
+                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status};
     for (void *p : dev)
         if (p) cudaFree(p);
     x->push_tab.release();
     x->pullc_tab.release();
     x->apply_tab.release();
-    for (Table &t : x->agg_tab) t.release();
+    x->a_tab.release();
+    x->x_tab.release();
     delete x;
     return TLC_OK;
 }
 
 int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, const uint64_t *sizes) {
     if (!out || !comm || num_tensors < 1 || !sizes) return TLC_ERR_ARG;
+    if (comm->world > 8) return TLC_ERR_ARG;   // the fused aggregation holds <= 8 sources per tile
     auto *x = new tlc_exchange{};
     x->comm = comm;
     x->W = comm->world;
@@ -281,24 +274,24 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
             d.n = c.n;
         }
         rc = x->pullc_tab.create(pullc.data(), nown, true, nullptr);
-        x->agg_tab.resize(x->W);
-        for (int w = 0; rc == TLC_OK && w < x->W; w++) {
-            for (int q = 0; q < nown; q++) {
-                const Ctx &c = x->ctx[x->owned[x->me][q]];
-                tlc_tensor_desc &d = agg[q];
-                d = tlc_tensor_desc{};
-                d.payload = x->push_recv + (size_t)w * own_region + c.region_off;
-                d.hdr = x->push_hdr_recv + (size_t)w * nown + c.slot;
-                d.out = x->owned_buf + c.owned_off;
-                d.n = c.n;
-            }
-            if (w == 0) {
-                rc = x->agg_tab[0].create(agg.data(), nown, false, nullptr);
-                if (rc == TLC_OK) x->agg_ws = nullptr;   // table 0 owns the shared workspace
-            } else {
-                rc = x->agg_tab[w].create(agg.data(), nown, false, x->agg_tab[0].ws);
+        std::vector<tlc_tensor_desc> xs((size_t)x->W * nown);
+        for (int q = 0; q < nown; q++) {
+            const Ctx &c = x->ctx[x->owned[x->me][q]];
+            tlc_tensor_desc &d = agg[q];
+            d = tlc_tensor_desc{};
+            d.out = x->owned_buf + c.owned_off;
+            d.hdr = x->push_hdr_recv + c.slot;      // only n / out are used through A
+            d.n = c.n;
+            for (int w = 0; w < x->W; w++) {
+                tlc_tensor_desc &e = xs[(size_t)w * nown + q];
+                e = tlc_tensor_desc{};
+                e.payload = x->push_recv + (size_t)w * own_region + c.region_off;
+                e.hdr = x->push_hdr_recv + (size_t)w * nown + c.slot;
+                e.n = c.n;
             }
         }
+        if (rc == TLC_OK) rc = x->a_tab.create(agg.data(), nown, false, nullptr);
+        if (rc == TLC_OK) rc = x->x_tab.create(xs.data(), x->W * nown, false, nullptr);
     }
     if (rc != TLC_OK) {
         tlc_exchange_destroy(x);
@@ -387,18 +380,11 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
             ncclRecv(x->push_hdr_recv + (size_t)w * nown, nown * sizeof(tlc_header), ncclUint8, w, nc, st);
         }
     if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
-    // (3) owner: rank-ordered sum of the W decompressed pushes, then / W (R15)
-    if (x->owned_elems) {
-        if ((rc = cuda_ok(cudaMemsetAsync(x->owned_buf, 0, x->owned_elems * sizeof(float), st))) != TLC_OK) return rc;
-        for (int w = 0; w < x->W; w++) {
-            rc = launch_decompress_table(x->agg_tab[w].T, TLC_MODE_ACCUMULATE, x->agg_tab[w].ws, st);
-            if (rc != TLC_OK) return rc;
-        }
-        KernelScope ks(kK8, st);
-        const int grid = (int)std::min<uint64_t>((x->owned_elems + 255) / 256, (uint64_t)num_sms() * 8);
-        tlc_scale_kernel<<<grid, 256, 0, st>>>(x->owned_buf, x->owned_elems, (float)x->W);
-        if ((rc = cuda_ok(cudaPeekAtLastError())) != TLC_OK) return rc;
-    }
+    // (3) owner: fused decompress-aggregate of the W pushes of every owned context,
+    //     rank-ordered sum from +0 of the nonzero trits, then / W (R15), written once
+    if (x->owned_elems &&
+        (rc = launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st)) != TLC_OK)
+        return rc;
     return TLC_OK;
 }
 

@@ -116,5 +116,6 @@ struct Table {
     void release();
 };
 int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t st);
+int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st);
 
 }  // namespace tlc
