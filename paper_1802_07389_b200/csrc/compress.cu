@@ -153,6 +153,41 @@ __device__ __forceinline__ void quant_qe_group(const float4 *__restrict__ t4, fl
     b4[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
 }
 
+// Four quartic positions j + 256k (k = 0..3), any alignment: all 40 loads are
+// issued before any arithmetic so that 160 bytes per thread are in flight.
+template <class QT>
+__device__ __forceinline__ void quant_qe_four(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
+                                              uint64_t P, uint64_t j, uint64_t jend, uint8_t *__restrict__ bytes,
+                                              const QT &Q) {
+    float tv[4][5], ev[4][5];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint64_t jj = j + (uint64_t)k * kK2Threads;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + jj;
+            const bool ok = jj < jend && e < n;
+            tv[k][i] = ok ? ld_stream(t + e) : 0.0f;
+            ev[k][i] = ok ? __ldcs(err + e) : 0.0f;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint64_t jj = j + (uint64_t)k * kK2Threads;
+        if (jj >= jend) break;
+        uint32_t b = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + jj;
+            const float u = __fadd_rn(ev[k][i], tv[k][i]);      // step (1)
+            const int q = Q.q(u);                                // Eq. 2
+            if (e < n) __stcs(err + e, Q.residual(u, q));       // steps (a),(b)
+            b = b * 3u + (e < n ? (uint32_t)(q + 1) : 0u);       // steps 1,4,6 (pad digit 0)
+        }
+        bytes[jj] = (uint8_t)b;
+    }
+}
+
 template <class QT>
 __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, const QT &Q) {
     const uint64_t P = S.P, n = S.n;
@@ -168,8 +203,8 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
         for (uint64_t j = 4 * g1 + threadIdx.x; j < jend; j += kK2Threads)
             bytes[j] = (uint8_t)quant_qe_one(S.t, S.err, n, P, j, Q);
     } else {
-        for (uint64_t j = j0 + threadIdx.x; j < jend; j += kK2Threads)
-            bytes[j] = (uint8_t)quant_qe_one(S.t, S.err, n, P, j, Q);
+        for (uint64_t j = j0 + threadIdx.x; j < jend; j += 4 * kK2Threads)
+            quant_qe_four(S.t, S.err, n, P, j, jend, bytes, Q);
     }
 }
 

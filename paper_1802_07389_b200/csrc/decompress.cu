@@ -254,6 +254,29 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict
         }
         const bool vec = (S.flags & kSegVec5) != 0;
 
+        if (kMode == TLC_MODE_OVERWRITE && !vec && (reinterpret_cast<uintptr_t>(S.out) & 3u) == 0) {
+            // Partitions not 16-byte aligned (P % 4 != 0 or an offset view): shift each
+            // partition's groups of four so every float4 store is aligned; the bytes of a
+            // group come from shared memory at any offset.
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                float *base = ob[i];
+                const int sh = (int)((4u - ((reinterpret_cast<uintptr_t>(base) >> 2) & 3u)) & 3u);  // first aligned jl
+                if ((int)threadIdx.x < sh && (int)threadIdx.x < lim[i])
+                    base[threadIdx.x] = __uint_as_float(sm.V[i][sm.E[threadIdx.x]]);
+                for (int jl = sh + 4 * (int)threadIdx.x; jl < lim[i]; jl += 4 * kK5Threads) {
+                    if (jl + 3 < lim[i]) {
+                        __stcs(reinterpret_cast<uint4 *>(base + jl),
+                               make_uint4(sm.V[i][sm.E[jl]], sm.V[i][sm.E[jl + 1]], sm.V[i][sm.E[jl + 2]],
+                                          sm.V[i][sm.E[jl + 3]]));
+                    } else {
+                        for (int c = 0; jl + c < lim[i]; c++) base[jl + c] = __uint_as_float(sm.V[i][sm.E[jl + c]]);
+                    }
+                }
+            }
+            continue;
+        }
+
         // ---- base-3 decode + dequantize, 4 consecutive quartic bytes per step
 #pragma unroll
         for (int k = 0; k < kK5BytesPerThread / 4; k++) {
