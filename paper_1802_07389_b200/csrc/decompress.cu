@@ -338,28 +338,32 @@ constexpr int kMaxSources = 8;
 
 struct K5mSmem {
     alignas(16) uint8_t E[kMaxSources][kT5];
-    uint16_t lut[256];                   // bit i = (digit_i != 1), bit 8+i = (digit_i == 0)
-    float M[kMaxSources];
+    uint32_t V[kMaxSources][5][256];     // V[w][i][b] = M_w * (digit_i(b) - 1): +0 for a zero trit
     int ok[kMaxSources];
     unsigned int warp_sum[kK5Threads / 32];
 };
+
+// One source's Eq. 3 table (the same single fp32 multiply as the decoder).
+__device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
+    for (int v = threadIdx.x; v < 256; v += kK5Threads) {
+        uint32_t r = v < 243 ? v : 121;
+#pragma unroll
+        for (int i = 4; i >= 0; i--) {
+            V[i][v] = __float_as_uint(__fmul_rn(M, (float)((int)(r % 3u) - 1)));
+            r /= 3u;
+        }
+    }
+}
 
 __global__ void __launch_bounds__(kK5Threads)
 tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *__restrict__ seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K5mSmem &sm = *reinterpret_cast<K5mSmem *>(smem_raw);
-    for (int v = threadIdx.x; v < 256; v += kK5Threads) {
-        uint32_t w = 0, r = v < 243 ? v : 121;
-#pragma unroll
-        for (int i = 4; i >= 0; i--) {
-            const uint32_t d = r % 3u;
-            r /= 3u;
-            w |= (uint32_t)(d != 1) << i;
-            w |= (uint32_t)(d == 0) << (8 + i);
-        }
-        sm.lut[v] = (uint16_t)w;
-    }
-    const float Wf = (float)W;
+    // acc / W: for W a power of two the division is the exact scaling acc * (1/W),
+    // bitwise equal to the IEEE quotient; otherwise divide
+    const bool pow2 = (W & (W - 1)) == 0;
+    const float Wf = (float)W, rW = 1.0f / (float)W;
+    int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < A.n5; tile += gridDim.x) {
         const int q = find_seg<5>(A, tile);
         const Seg S = get_seg(A, q);
@@ -371,12 +375,14 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
             const Seg R = get_seg(X, w * A.count + q);
             const tlc_header *h = R.hdr;
             const bool ok = h->status == TLC_OK;           // uniform
-            if (threadIdx.x == 0) { sm.ok[w] = ok; sm.M[w] = h->M; }
+            if (threadIdx.x == 0) sm.ok[w] = ok;
             if (!ok) continue;
+            if (q != cur) build_values(sm.V[w], h->M);
             const bool bad = expand_tile(sm.E[w], sm.warp_sum, R.payload, (h->flags & TLC_FLAG_ZRE) != 0,
                                          h->payload_len, seek + R.k5, lt, ntiles, J0, tl);
             if (bad && threadIdx.x == 0) { raise_format(R.hdr); sm.ok[w] = 0; }
         }
+        cur = q;
         __syncthreads();
         int lim[5];
         float *ob[5];
@@ -395,27 +401,26 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
 #pragma unroll
             for (int i = 0; i < 5; i++)
 #pragma unroll
-                for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0
+                for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0 (R15)
+            bool any = false;
             for (int w = 0; w < W; w++) {                          // rank order
-                if (!sm.ok[w]) continue;
                 const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E[w] + jl);
-                if (w4 == 0x79797979u) continue;                   // all trits zero: nothing to add
-                const float Mw = sm.M[w];
-                uint32_t L[4];
-#pragma unroll
-                for (int c = 0; c < 4; c++) L[c] = sm.lut[(w4 >> (8 * c)) & 0xffu];
+                if (!sm.ok[w] || w4 == 0x79797979u) continue;      // all trits zero: adds +0 only
+                any = true;
+                const uint32_t b[4] = {w4 & 0xffu, (w4 >> 8) & 0xffu, (w4 >> 16) & 0xffu, w4 >> 24};
+                // acc is never -0, so adding the +0 of a zero trit leaves it bitwise unchanged:
+                // this equals "add M_w*q_w only where q_w != 0"
 #pragma unroll
                 for (int i = 0; i < 5; i++)
 #pragma unroll
-                    for (int c = 0; c < 4; c++)
-                        if ((L[c] >> i) & 1u)
-                            acc[i][c] = __fadd_rn(acc[i][c], ((L[c] >> (8 + i)) & 1u) ? -Mw : Mw);
+                    for (int c = 0; c < 4; c++) acc[i][c] = __fadd_rn(acc[i][c], __uint_as_float(sm.V[w][i][b[c]]));
             }
 #pragma unroll
             for (int i = 0; i < 5; i++) {
                 float r[4];
 #pragma unroll
-                for (int c = 0; c < 4; c++) r[c] = __fdiv_rn(acc[i][c], Wf);     // R15
+                for (int c = 0; c < 4; c++)
+                    r[c] = !any ? 0.0f : (pow2 ? __fmul_rn(acc[i][c], rW) : __fdiv_rn(acc[i][c], Wf));
                 float *o = ob[i] + jl;
                 if (vec && jl + 3 < lim[i]) {
                     __stcs(reinterpret_cast<float4 *>(o), make_float4(r[0], r[1], r[2], r[3]));
