@@ -336,12 +336,15 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict
 // seek entries K4 wrote.  A source whose header is not OK contributes nothing.
 constexpr int kMaxSources = 8;
 
-struct K5mSmem {
-    alignas(16) uint8_t E[kMaxSources][kT5];
-    uint32_t V[kMaxSources][5][256];     // V[w][i][b] = M_w * (digit_i(b) - 1): +0 for a zero trit
+// Dynamic shared memory, sized for W sources: E[W][kT5] bytes, then
+// V[W][5][256] words (V[w][i][b] = M_w * (digit_i(b) - 1): +0 for a zero trit).
+struct K5mHead {
     int ok[kMaxSources];
     unsigned int warp_sum[kK5Threads / 32];
 };
+__host__ __device__ constexpr size_t k5m_smem_bytes(int W) {
+    return sizeof(K5mHead) + (size_t)W * kT5 + (size_t)W * 5 * 256 * sizeof(uint32_t);
+}
 
 // One source's Eq. 3 table (the same single fp32 multiply as the decoder).
 __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
@@ -355,10 +358,12 @@ __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
     }
 }
 
-__global__ void __launch_bounds__(kK5Threads)
+__global__ void __launch_bounds__(kK5Threads, 3)
 tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *__restrict__ seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    K5mSmem &sm = *reinterpret_cast<K5mSmem *>(smem_raw);
+    K5mHead &sm = *reinterpret_cast<K5mHead *>(smem_raw);
+    uint8_t(*E)[kT5] = reinterpret_cast<uint8_t(*)[kT5]>(smem_raw + sizeof(K5mHead));
+    uint32_t(*V)[5][256] = reinterpret_cast<uint32_t(*)[5][256]>(smem_raw + sizeof(K5mHead) + (size_t)W * kT5);
     // acc / W: for W a power of two the division is the exact scaling acc * (1/W),
     // bitwise equal to the IEEE quotient; otherwise divide
     const bool pow2 = (W & (W - 1)) == 0;
@@ -377,8 +382,8 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
             const bool ok = h->status == TLC_OK;           // uniform
             if (threadIdx.x == 0) sm.ok[w] = ok;
             if (!ok) continue;
-            if (q != cur) build_values(sm.V[w], h->M);
-            const bool bad = expand_tile(sm.E[w], sm.warp_sum, R.payload, (h->flags & TLC_FLAG_ZRE) != 0,
+            if (q != cur) build_values(V[w], h->M);
+            const bool bad = expand_tile(E[w], sm.warp_sum, R.payload, (h->flags & TLC_FLAG_ZRE) != 0,
                                          h->payload_len, seek + R.k5, lt, ntiles, J0, tl);
             if (bad && threadIdx.x == 0) { raise_format(R.hdr); sm.ok[w] = 0; }
         }
@@ -404,7 +409,7 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
                 for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0 (R15)
             bool any = false;
             for (int w = 0; w < W; w++) {                          // rank order
-                const uint32_t w4 = *reinterpret_cast<const uint32_t *>(sm.E[w] + jl);
+                const uint32_t w4 = *reinterpret_cast<const uint32_t *>(E[w] + jl);
                 if (!sm.ok[w] || w4 == 0x79797979u) continue;      // all trits zero: adds +0 only
                 any = true;
                 const uint32_t b[4] = {w4 & 0xffu, (w4 >> 8) & 0xffu, (w4 >> 16) & 0xffu, w4 >> 24};
@@ -413,7 +418,7 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
 #pragma unroll
                 for (int i = 0; i < 5; i++)
 #pragma unroll
-                    for (int c = 0; c < 4; c++) acc[i][c] = __fadd_rn(acc[i][c], __uint_as_float(sm.V[w][i][b[c]]));
+                    for (int c = 0; c < 4; c++) acc[i][c] = __fadd_rn(acc[i][c], __uint_as_float(V[w][i][b[c]]));
             }
 #pragma unroll
             for (int i = 0; i < 5; i++) {
@@ -452,12 +457,15 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
     }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K5mSmem));
+        cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k5m_smem_bytes(kMaxSources));
         attr = true;
     }
     KernelScope ks(kK6, st);
-    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * 4));
-    tlc_aggregate_kernel<<<grid, kK5Threads, sizeof(K5mSmem), st>>>(A, X, W, seek);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_kernel, kK5Threads, k5m_smem_bytes(W));
+    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * tmax(1, per_sm)));
+    tlc_aggregate_kernel<<<grid, kK5Threads, k5m_smem_bytes(W), st>>>(A, X, W, seek);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
