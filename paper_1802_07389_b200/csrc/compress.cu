@@ -18,6 +18,7 @@
 //
 // Paper: P:372-410 (Sec. 3.1), P:495-510 (Sec. 3.2), P:538-548 (Sec. 3.3).
 #include <algorithm>
+#include <cstdlib>
 
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
@@ -213,8 +214,8 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
 #endif
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
-                    uint8_t *__restrict__ scratch) {
-    for (uint64_t tile = blockIdx.x; tile < T.n2; tile += gridDim.x) {
+                    uint8_t *__restrict__ scratch, uint64_t tile_begin) {
+    for (uint64_t tile = tile_begin + blockIdx.x; tile < T.n2; tile += gridDim.x) {
         const int si = find_seg<2>(T, tile);
         const Seg S = get_seg(T, si);
         float M;
@@ -234,6 +235,120 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, f
         const Quant Q(M);
         if (Q.mode == 1) quant_qe_tile(S, bytes, lt * kT2, QuantCmp(Q));   // uniform branch
         else quant_qe_tile(S, bytes, lt * kT2, Q);
+    }
+}
+
+// ---- K2 bulk path: the same computation on tiles staged in shared memory by the
+// Blackwell bulk-copy (TMA) engine.  One CTA per SM keeps kBulkStages tiles of
+// t and err (10 contiguous 4 KiB partition segments each) in flight behind
+// mbarrier transaction counts, so the memory system never waits for a thread;
+// threads read their four positions per partition with 128-bit shared loads
+// and store err and the quartic bytes straight to global memory.  Used for the
+// complete tiles of a single aligned tensor (P % 4 == 0); the ragged tail and
+// tensor batches go through tlc_quant_qe_kernel.
+constexpr int kBulkPos = 1024;                                   // quartic positions per tile
+constexpr int kBulkStages = 4;
+constexpr uint32_t kBulkPart = kBulkPos * 4;                     // bytes per partition segment
+constexpr uint32_t kBulkStageBytes = 10 * kBulkPart;             // t and err, five partitions
+
+struct BulkSmem {
+    float buf[kBulkStages][10][kBulkPos];
+    unsigned long long bar[kBulkStages];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TLC_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra TLC_WAIT_%=;\n\t}" ::"r"(smem_addr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+
+template <class QT>
+__device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, const Seg &S, uint64_t j0,
+                                             uint8_t *bytes, const QT &Q) {
+    const int g = threadIdx.x;                       // group: positions j0 + 4g .. j0 + 4g + 3
+    const uint64_t P = S.P;
+    uint32_t by[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i][4 * g]);
+        const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][5 + i][4 * g]);
+        const float tt[4] = {tv.x, tv.y, tv.z, tv.w};
+        const float ee[4] = {ev.x, ev.y, ev.z, ev.w};
+        float r[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const float u = __fadd_rn(ee[c], tt[c]);        // step (1)
+            const int q = Q.q(u);                            // Eq. 2
+            r[c] = Q.residual(u, q);                         // steps (a),(b)
+            by[c] = by[c] * 3u + (uint32_t)(q + 1);          // steps 1, 6
+        }
+        __stcs(reinterpret_cast<float4 *>(S.err + (uint64_t)i * P + j0) + g, make_float4(r[0], r[1], r[2], r[3]));
+    }
+    reinterpret_cast<uint32_t *>(bytes + j0)[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
+}
+
+__global__ void __launch_bounds__(kK2Threads, 1)
+tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
+                         uint8_t *__restrict__ scratch, uint64_t nbulk) {
+    static_assert(kBulkPos == 4 * kK2Threads, "one group of four positions per thread");
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    BulkSmem &sm = *reinterpret_cast<BulkSmem *>(smem_raw);
+    const Seg S = T.one;
+    float M;
+    const unsigned int status = scale_from_key(maxkey[0], s, M);   // Eq. 1, R6
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        tlc_header *h = S.hdr;
+        h->M = M;
+        h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+        h->n = S.n;
+        h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;
+        h->status = status;
+        h->reserved = 0;
+    }
+    if (status != TLC_OK) return;
+    uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
+    const uint64_t P = S.P;
+    const uint64_t mine = nbulk > blockIdx.x ? (nbulk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t k) {
+        const int st = (int)(k % kBulkStages);
+        const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
+        mbar_expect_tx(&sm.bar[st], kBulkStageBytes);
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            bulk_load(sm.buf[st][i], S.t + (uint64_t)i * P + j0, kBulkPart, &sm.bar[st]);
+            bulk_load(sm.buf[st][5 + i], S.err + (uint64_t)i * P + j0, kBulkPart, &sm.bar[st]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t k = 0; k < mine && k < kBulkStages; k++) issue(k);
+    const Quant Q(M);
+    for (uint64_t k = 0; k < mine; k++) {
+        const int st = (int)(k % kBulkStages);
+        mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
+        const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
+        if (Q.mode == 1) bulk_compute(sm, st, S, j0, bytes, QuantCmp(Q));
+        else bulk_compute(sm, st, S, j0, bytes, Q);
+        __syncthreads();                                 // every thread is done with this stage
+        if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
     }
 }
 
@@ -362,6 +477,27 @@ tlc_zre_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float 
 // ============================================================== host side
 static int g_k2_blocks = 0, g_k3_blocks = 0;
 
+// Complete bulk tiles of a one-segment table: positions j < min(P, n - 4P) have all five
+// elements; the bulk kernel takes whole K2 tiles of them (kT2 = 4 bulk tiles).
+static uint64_t bulk_tiles(const SegTable &T, int use_zre) {
+    if (T.count != 1) return 0;
+    const Seg &S = T.one;
+    if (!(S.flags & kSegVec2) || S.P % 4 != 0) return 0;
+    if (!use_zre && !aligned4(S.payload)) return 0;
+    const uint64_t complete = S.n >= 4 * S.P ? tmin<uint64_t>(S.P, S.n - 4 * S.P) : 0;
+    return (complete / kT2) * (kT2 / kBulkPos);
+}
+
+// TLC_NO_BULK=1 disables the bulk-copy K2 path (A/B measurements)
+static bool use_bulk() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_NO_BULK");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
     const WsLayout L = ws_layout(T, 0);
     char *base = reinterpret_cast<char *>(ws);
@@ -378,10 +514,25 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
     }
     {
         KernelScope ks(kK2, st);
-        if (!g_k2_blocks)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
-        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2, (uint64_t)sms * tmax(1, g_k2_blocks)));
-        tlc_quant_qe_kernel<<<grid, kK2Threads, 0, st>>>(T, maxkey, s, use_zre, scratch);
+        const uint64_t nbulk = use_bulk() ? bulk_tiles(T, use_zre) : 0;
+        uint64_t tile_begin = 0;
+        if (nbulk) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(BulkSmem));
+                attr = true;
+            }
+            const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);
+            tlc_quant_qe_bulk_kernel<<<grid, kK2Threads, sizeof(BulkSmem), st>>>(T, maxkey, s, use_zre, scratch, nbulk);
+            tile_begin = nbulk * kBulkPos / kT2;
+        }
+        if (tile_begin < T.n2) {
+            if (!g_k2_blocks)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
+            const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2 - tile_begin, (uint64_t)sms * tmax(1, g_k2_blocks)));
+            tlc_quant_qe_kernel<<<grid, kK2Threads, 0, st>>>(T, maxkey, s, use_zre, scratch, tile_begin);
+        }
     }
     if (use_zre) {
         KernelScope ks(kK3, st);
