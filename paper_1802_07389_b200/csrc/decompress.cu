@@ -25,7 +25,6 @@ namespace tlc {
 // ============================================================== K4
 constexpr int kK4Threads = kScanThreads;
 constexpr int kK4Seg = 16;
-constexpr int kK4Row = kK4Threads * kK4Seg;
 
 __device__ __forceinline__ int load_pay16(const uint8_t *__restrict__ p, uint64_t pos, uint64_t hi,
                                           uint32_t (&len)[kK4Seg]) {
@@ -48,6 +47,7 @@ __device__ __forceinline__ int load_pay16(const uint8_t *__restrict__ p, uint64_
 __global__ void __launch_bounds__(kK4Threads)
 tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, unsigned long long *seek) {
     __shared__ unsigned long long s_warp[kScanWarps];
+    __shared__ unsigned long long s_wsum[kScanWarps];
     __shared__ unsigned long long s_id;
     uint32_t len[kK4Seg];
     while (true) {
@@ -70,14 +70,30 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         if (lo >= Z) continue;                            // past the payload: nothing to scan
         const uint64_t num_out_tiles = (P + kT5 - 1) / kT5;
 
-        // ---- phase 1: expansion length of the chunk
-        uint64_t agg = 0;
-        for (uint64_t row = lo; row < hi; row += kK4Row) {
-            load_pay16(S.payload, row + (uint64_t)kK4Seg * threadIdx.x, hi, len);
+        // the chunk is split into one sub-range per warp, scanned in warp rows of 32 x 16 bytes
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        constexpr uint64_t kWRow = 32 * kK4Seg;
+        const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK4Seg - 1) / kK4Seg * kK4Seg;
+        const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
+
+        // ---- phase 1: expansion length of each warp's sub-range, then of the chunk
+        uint64_t wsum = 0;
+        for (uint64_t row = wlo; row < whi; row += kWRow) {
+            load_pay16(S.payload, row + (uint64_t)kK4Seg * lane, whi, len);
             uint32_t sum = 0;
 #pragma unroll
             for (int k = 0; k < kK4Seg; k++) sum += len[k];
-            agg += block_reduce_sum(sum, s_warp);
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+            wsum += sum;
+        }
+        if (lane == 0) s_wsum[warp] = wsum;
+        __syncthreads();
+        uint64_t agg = 0, before = 0;
+#pragma unroll
+        for (int k = 0; k < kScanWarps; k++) {
+            before += k < warp ? s_wsum[k] : 0ull;
+            agg += s_wsum[k];
         }
         if (threadIdx.x == 0) st_relaxed_u64(states + id, kReady | agg);
 
@@ -86,18 +102,24 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         const uint64_t per = (lc + kK4Threads - 1) / kK4Threads;
         const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(lc, i0 + per);
         for (uint64_t i = i0; i < i1; i++) part += wait_ready(states + S.k4 + i) & ~kReady;
-        uint64_t run = block_reduce_sum(part, s_warp);
+        const uint64_t run = block_reduce_sum(part, s_warp);
         if (hi == Z && threadIdx.x == 0 && run + agg != P) raise_format(hdr);
 
         // ---- phase 3: seek entries (payload byte covering J0 = k*kT5, offset inside it)
-        for (uint64_t row = lo; row < hi; row += kK4Row) {
-            const uint64_t pos0 = row + (uint64_t)kK4Seg * threadIdx.x;
-            load_pay16(S.payload, pos0, hi, len);
+        uint64_t q0 = run + before;                       // position of the warp's first byte
+        for (uint64_t row = wlo; row < whi; row += kWRow) {
+            const uint64_t pos0 = row + (uint64_t)kK4Seg * lane;
+            load_pay16(S.payload, pos0, whi, len);
             uint32_t sum = 0;
 #pragma unroll
             for (int k = 0; k < kK4Seg; k++) sum += len[k];
-            uint64_t row_total;
-            uint64_t q = run + block_excl_scan_sum(sum, s_warp, row_total);
+            uint32_t x = sum;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            uint64_t q = q0 + (x - sum);
 #pragma unroll
             for (int k = 0; k < kK4Seg; k++) {
                 if (len[k]) {
@@ -107,7 +129,7 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
                     q += len[k];
                 }
             }
-            run += row_total;
+            q0 += __shfl_sync(0xffffffffu, x, 31);
         }
     }
 }
