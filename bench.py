@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--model", default="bert-large", help="tensor list of the exchange workload")
     ap.add_argument("--xs", type=float, default=1.9, help="s of the exchange workload (configs[4])")
     ap.add_argument("--no-xchg-w1", action="store_true", help="skip the N=1 exchange side measurement")
+    ap.add_argument("--xchg", choices=["p2p", "nccl"], default="p2p",
+                    help="exchange transport: peer-memory kernels over NVLink, or NCCL send/recv")
     ap.add_argument("--e2e-steps", type=int, default=10)
     return ap.parse_args()
 
@@ -271,7 +273,7 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
 NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
 
 
-def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None):
+def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True):
     """BASELINE configs[4]: the model's ndim>=2 gradient tensors exchanged through
     the parameter-server push/pull (tlc_exchange_push + tlc_exchange_pull, delta =
     mean) on `world` ranks; every rank holds its own full state change (weak
@@ -285,7 +287,7 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None):
     grads = [synth.model_step_torch(model, k, rank, dev) for k in range(2)]
     outs = [torch.zeros(n, dtype=torch.float32, device=dev) for n in sizes]
     comm = T.Comm(rank, world, dev)
-    x = T.Exchange(comm, sizes)
+    x = T.Exchange(comm, sizes, p2p=p2p)
     stream = torch.cuda.current_stream(dev)
 
     def step(k):
@@ -311,7 +313,7 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None):
     prof = T.tlc_prof_collect()
     ms = e0.elapsed_time(e1) / steps
     status = x.status(stream)
-    wire = x.wire_bytes(0) + x.wire_bytes(1)
+    wire = sum(x.traffic())
     kern_ms = sum(tot for (_, tot) in prof.values()) / steps
     x.close()
     comm.close()
@@ -324,7 +326,7 @@ def run_exchange_leg(args, T, dev, world, rank, dist):
     import torch
 
     r = measure_exchange(T, dev, world, rank, args.model, args.xs, args.steps, args.warmup,
-                         dist if world > 1 else None)
+                         dist if world > 1 else None, p2p=args.xchg == "p2p")
     ms = r["ms"]
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -532,14 +534,17 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             "data": f"synthetic: {args.model} ndim>=2 gradient shapes, g = mu_l + N(0,1) per layer "
                     "(torch Philox on device, synth/), 2 rotating steps per rank",
             "config": {"workload": f"configs[4]: {args.model} gradient exchange, parameter-server push "
-                                   f"(compress, NCCL to owners, rank-ordered aggregate / W) + shared pull "
-                                   f"(owner compresses once, NCCL all-gather, apply) at s={args.xs}, "
-                                   f"{r['N']:,} values per rank",
+                                   f"(compress, owners' fused aggregate of the W payloads / W) + shared pull "
+                                   f"(owner compresses once, every rank applies) at s={args.xs}, "
+                                   f"{r['N']:,} values per rank; transport: "
+                                   + ("kernels read peers' payloads over NVLink (CUDA IPC), flag barriers"
+                                      if args.xchg == "p2p" else "NCCL grouped send/recv"),
                        "n_per_rank": r["N"], "s": args.xs, "contexts": r["contexts"],
                        "l2": "inputs larger than L2 (1.34 GB of state changes per rank); no flush",
-                       "parallelism": f"ps{world} (sharded parameter server over NCCL, NVLink)"},
+                       "parallelism": f"ps{world} (sharded parameter server, {args.xchg})"},
             "value_definition": "world x 4 x values-per-rank / step time (effective fp32 GB/s exchanged)",
             "wire_bytes_per_rank_per_step": r["wire"],
+            "wire_definition": "bytes rank 0 received from other ranks per step (push + pull)",
             "nvlink_frac": pct_nvlink,
             "kernel_ms_per_step_rank0": r["kernel_ms"],
             "kernels_rank0": r["kernels"],

@@ -232,6 +232,23 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream);
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status, void *stream);
 
+/* Peer-memory mode (one rank per GPU on an NVLink/NVSwitch box).  After
+ * tlc_exchange_create, every rank calls tlc_exchange_ipc_handles (writes 5 x 64
+ * bytes of CUDA IPC handles of its send / pull buffers and flag slots to host
+ * memory `out`), the caller all-gathers them in rank order (W x 320 bytes) and
+ * every rank calls tlc_exchange_ipc_open.  From then on push/pull move no data
+ * with NCCL: a flag barrier over peer memory orders the phases, and the owner's
+ * scan + fused aggregation kernels (and every rank's apply kernels) read the
+ * compressed payloads -- exactly their payload_len bytes -- straight from the
+ * producing GPU over NVLink.  Results are identical to the NCCL mode. */
+int tlc_exchange_ipc_handles(tlc_exchange *x, void *out);
+int tlc_exchange_ipc_open(tlc_exchange *x, const void *all);
+
+/* Bytes this rank received from other ranks in the last push (out[0]) and pull
+ * (out[1]): capacity regions + headers with NCCL; exactly the payload_len (+
+ * header) bytes read over NVLink in peer-memory mode.  Synchronizes the device. */
+int tlc_exchange_traffic(tlc_exchange *x, uint64_t *out);
+
 /* ---------------------------------------------------------------------------
  * Instrumentation (host-side, not part of the method).
  *

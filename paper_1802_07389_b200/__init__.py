@@ -69,6 +69,9 @@ def _load():
         "tlc_exchange_push": (I, [P, P, F, I, P]),
         "tlc_exchange_pull": (I, [P, P, F, I, P]),
         "tlc_exchange_status": (I, [P, P, P]),
+        "tlc_exchange_ipc_handles": (I, [P, P]),
+        "tlc_exchange_ipc_open": (I, [P, P]),
+        "tlc_exchange_traffic": (I, [P, P]),
         "tlc_launch_count": (ctypes.c_ulonglong, []),
         "tlc_prof_enable": (None, [I]),
         "tlc_prof_collect": (I, [P, I]),
@@ -374,7 +377,10 @@ class Comm:
 class Exchange:
     """3LC parameter-server push/pull for a fixed tensor list (include/tlc.h)."""
 
-    def __init__(self, comm: Comm, sizes):
+    def __init__(self, comm: Comm, sizes, p2p: bool = False, group=None):
+        """p2p=True: peer-memory mode -- the compressed payloads are read by the consuming
+        kernels straight from the producing GPU over NVLink (CUDA IPC mappings set up
+        here through torch.distributed); otherwise NCCL send/recv moves them."""
         import numpy as np
 
         self.comm, self.sizes = comm, [int(n) for n in sizes]
@@ -389,6 +395,22 @@ class Exchange:
         self.owned = _as_tensor(_lib.tlc_exchange_owned_buffer(self._x), self.owned_elements, self.device)
         self.pull_err = _as_tensor(_lib.tlc_exchange_pull_error(self._x), self.owned_elements, self.device)
         self.push_err = _as_tensor(_lib.tlc_exchange_push_error(self._x), sum(self.sizes), self.device)
+        self.p2p = bool(p2p)
+        if self.p2p:
+            mine = (ctypes.c_ubyte * 320)()
+            rc = _lib.tlc_exchange_ipc_handles(self._x, ctypes.cast(mine, ctypes.c_void_p))
+            if rc != TLC_OK:
+                raise TlcError(rc, "tlc_exchange_ipc_handles")
+            blobs = [bytes(mine)]
+            if comm.world > 1:
+                import torch.distributed as dist
+
+                blobs = [None] * comm.world
+                dist.all_gather_object(blobs, bytes(mine), group=group)
+            allh = (ctypes.c_ubyte * (320 * comm.world)).from_buffer_copy(b"".join(blobs))
+            rc = _lib.tlc_exchange_ipc_open(self._x, ctypes.cast(allh, ctypes.c_void_p))
+            if rc != TLC_OK:
+                raise TlcError(rc, "tlc_exchange_ipc_open")
 
     def contexts(self):
         out = []
@@ -400,6 +422,14 @@ class Exchange:
             out.append({"tensor": t.value, "lo": lo.value, "hi": hi.value, "owner": o.value,
                         "elem_off": eo.value, "owned_off": None if oo.value == 2 ** 64 - 1 else oo.value})
         return out
+
+    def traffic(self):
+        """(push bytes, pull bytes) this rank received from other ranks in the last step."""
+        out = (ctypes.c_uint64 * 2)()
+        rc = _lib.tlc_exchange_traffic(self._x, ctypes.cast(out, ctypes.c_void_p))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_traffic")
+        return int(out[0]), int(out[1])
 
     def wire_bytes(self, direction: int) -> int:
         return int(_lib.tlc_exchange_wire_bytes(self._x, int(direction)))

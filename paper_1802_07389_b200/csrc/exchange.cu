@@ -22,6 +22,7 @@
 // Buffers are allocated once by tlc_exchange_create; push/pull allocate nothing
 // and never synchronize the host.
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <nccl.h>
 #include <vector>
@@ -56,6 +57,23 @@ __global__ void tlc_status_kernel(const tlc_header *__restrict__ h, int count, u
     for (int i = threadIdx.x; i < count; i += blockDim.x) m = max(m, h[i].status);
     m = __reduce_max_sync(0xffffffffu, m);
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+// Cross-GPU flag barrier over peer memory (one rank per GPU): after a system
+// fence, write `epoch` into this rank's slot on every rank, then wait until every
+// rank has written it here.  Ordered after the kernels that produced the data.
+__global__ void tlc_flag_barrier_kernel(unsigned long long *const *peer_flags, unsigned long long *mine, int me,
+                                        int W, int slot, unsigned long long epoch) {
+    const int w = threadIdx.x;
+    if (w < W) {
+        __threadfence_system();
+        unsigned long long *dst = peer_flags[w] + (size_t)slot * W + me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + (size_t)slot * W + w) : "memory");
+        } while (v < epoch);
+    }
+    __syncthreads();
 }
 }  // namespace
 
@@ -122,6 +140,15 @@ struct tlc_exchange {
     // segment tables: push compress (all contexts), aggregation (owned contexts A and
     // the W x |A| received payloads X), pull compress (owned), apply (all contexts)
     Table push_tab, pullc_tab, apply_tab, a_tab, x_tab;
+    // peer-memory mode (tlc_exchange_ipc_*): the owner's kernels read the pushed
+    // payloads and every rank reads the pulled payloads straight from the producing
+    // rank's buffers over NVLink; two flag barriers per step order the phases
+    int p2p = 0;
+    unsigned long long *flags = nullptr;             // 2 x W epoch slots (local)
+    unsigned long long **d_peer_flags = nullptr;     // device array: every rank's flag slots
+    std::vector<void *> opened;                      // peer mappings to close
+    std::vector<std::array<void *, 5>> peer;         // per rank: push_send, push_hdr, pull_buf, pull_hdr, flags
+    unsigned long long epoch = 0;
     std::vector<const float *> last_grads;
     std::vector<float *> last_outs;
 };
@@ -184,8 +211,9 @@ int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap,
 
 int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
+    for (void *p : x->opened) cudaIpcCloseMemHandle(p);
     void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
-                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status};
+                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags};
     for (void *p : dev)
         if (p) cudaFree(p);
     x->push_tab.release();
@@ -255,6 +283,9 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     alloc((void **)&x->push_hdr_recv, (size_t)x->W * nown * sizeof(tlc_header));
     alloc((void **)&x->pull_hdr, (size_t)C * sizeof(tlc_header));
     alloc((void **)&x->d_status, 256);
+    alloc((void **)&x->flags, 2 * x->W * sizeof(unsigned long long));
+    alloc((void **)&x->d_peer_flags, x->W * sizeof(unsigned long long *));
+    if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->flags, 0, 2 * x->W * sizeof(unsigned long long)));
     if (rc == TLC_OK) {
         // error buffers start at zero (R20)
         rc = cuda_ok(cudaMemset(x->push_err, 0, std::max<size_t>(x->total_elems * sizeof(float), 256)));
@@ -298,6 +329,105 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
         return rc;
     }
     *out = x;
+    return TLC_OK;
+}
+
+// ------------------------------------------------------------------ peer-memory mode
+int tlc_exchange_ipc_handles(tlc_exchange *x, void *out) {
+    // five cudaIpcMemHandle_t (64 bytes each): push_send, push headers, pull buffer,
+    // pull headers, flag slots
+    if (!x || !out) return TLC_ERR_ARG;
+    void *bufs[5] = {x->push_send, x->push_hdr_send, x->pull_buf, x->pull_hdr, x->flags};
+    for (int k = 0; k < 5; k++) {
+        cudaIpcMemHandle_t h;
+        if (cudaIpcGetMemHandle(&h, bufs[k]) != cudaSuccess) return TLC_ERR_CUDA;
+        std::memcpy(static_cast<char *>(out) + 64 * k, &h, 64);
+    }
+    return TLC_OK;
+}
+
+int tlc_exchange_ipc_open(tlc_exchange *x, const void *all) {
+    // all: W x 5 handles in rank order (the all-gather of tlc_exchange_ipc_handles)
+    if (!x || !all || x->p2p) return TLC_ERR_ARG;
+    const int W = x->W, me = x->me;
+    x->peer.assign(W, {});
+    void *mine[5] = {x->push_send, x->push_hdr_send, x->pull_buf, x->pull_hdr, x->flags};
+    for (int w = 0; w < W; w++)
+        for (int k = 0; k < 5; k++) {
+            if (w == me) { x->peer[w][k] = mine[k]; continue; }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const char *>(all) + 64 * (5 * w + k), 64);
+            void *p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return TLC_ERR_CUDA;
+            x->opened.push_back(p);
+            x->peer[w][k] = p;
+        }
+    std::vector<unsigned long long *> pf(W);
+    for (int w = 0; w < W; w++) pf[w] = static_cast<unsigned long long *>(x->peer[w][4]);
+    int rc = cuda_ok(cudaMemcpy(x->d_peer_flags, pf.data(), W * sizeof(void *), cudaMemcpyHostToDevice));
+    // the owner's aggregation reads row w*|A|+q straight from rank w's send buffer
+    const int nown = (int)x->owned[me].size();
+    if (rc == TLC_OK && nown) {
+        std::vector<tlc_tensor_desc> xs((size_t)W * nown);
+        for (int q = 0; q < nown; q++) {
+            const Ctx &c = x->ctx[x->owned[me][q]];
+            for (int w = 0; w < W; w++) {
+                tlc_tensor_desc &e = xs[(size_t)w * nown + q];
+                e = tlc_tensor_desc{};
+                e.payload = static_cast<uint8_t *>(x->peer[w][0]) + x->region_start[me] + c.region_off;
+                e.hdr = static_cast<tlc_header *>(x->peer[w][1]) + x->hdr_start[me] + c.slot;
+                e.n = c.n;
+            }
+        }
+        rc = x->x_tab.update(xs.data());
+    }
+    if (rc == TLC_OK) {
+        x->p2p = 1;
+        x->last_outs.clear();   // the apply table is rebuilt with peer pointers
+    }
+    return rc;
+}
+
+static int flag_barrier(tlc_exchange *x, int slot, cudaStream_t st) {
+    x->epoch++;
+    KernelScope ks(kK7, st);
+    tlc_flag_barrier_kernel<<<1, 32 * ((x->W + 31) / 32), 0, st>>>(x->d_peer_flags, x->flags, x->me, x->W, slot,
+                                                                    x->epoch);
+    return cuda_ok(cudaPeekAtLastError());
+}
+
+int tlc_exchange_traffic(tlc_exchange *x, uint64_t *out) {
+    // bytes this rank received in the last push (out[0]) and pull (out[1]) from other
+    // ranks: capacity regions with NCCL, exactly the payload (+ header) bytes the
+    // consuming kernels read in peer-memory mode.  Synchronizes the device.
+    if (!x || !out) return TLC_ERR_ARG;
+    if (cudaDeviceSynchronize() != cudaSuccess) return TLC_ERR_CUDA;
+    const int W = x->W, me = x->me;
+    const int nown = (int)x->owned[me].size();
+    if (!x->p2p) {
+        out[0] = (uint64_t)(W - 1) * (x->region_bytes[me] + nown * sizeof(tlc_header));
+        uint64_t b = 0;
+        for (int o = 0; o < W; o++)
+            if (o != me) b += x->region_bytes[o] + x->owned[o].size() * sizeof(tlc_header);
+        out[1] = b;
+        return TLC_OK;
+    }
+    uint64_t push = 0, pull = 0;
+    std::vector<tlc_header> h;
+    for (int w = 0; w < W; w++) {
+        if (w == me) continue;
+        h.resize(nown);
+        if (nown && cudaMemcpy(h.data(), static_cast<tlc_header *>(x->peer[w][1]) + x->hdr_start[me],
+                               nown * sizeof(tlc_header), cudaMemcpyDefault) != cudaSuccess) return TLC_ERR_CUDA;
+        for (auto &e : h) push += e.payload_len + sizeof(tlc_header);
+        const int no = (int)x->owned[w].size();
+        h.resize(no);
+        if (no && cudaMemcpy(h.data(), static_cast<tlc_header *>(x->peer[w][3]) + x->hdr_start[w],
+                             no * sizeof(tlc_header), cudaMemcpyDefault) != cudaSuccess) return TLC_ERR_CUDA;
+        for (auto &e : h) pull += e.payload_len + sizeof(tlc_header);
+    }
+    out[0] = push;
+    out[1] = pull;
     return TLC_OK;
 }
 
@@ -368,6 +498,15 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
     const int nown = (int)x->owned[x->me].size();
     const size_t own_region = x->region_bytes[x->me];
     ncclComm_t nc = x->comm->nccl;
+    if (x->p2p) {
+        // peer memory: no copy -- once every rank's pushes are written, the owner's
+        // scan and aggregation kernels read them from the producing GPU over NVLink
+        if ((rc = flag_barrier(x, 0, st)) != TLC_OK) return rc;
+        if (x->owned_elems &&
+            (rc = launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st)) != TLC_OK)
+            return rc;
+        return TLC_OK;
+    }
     if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
     for (int o = 0; o < x->W; o++) {
         if (x->region_bytes[o] == 0) continue;
@@ -399,8 +538,12 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
     if (x->owned_elems &&
         (rc = launch_compress_table(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st)) != TLC_OK)
         return rc;
-    // (2) all-gather of the owners' regions (grouped send/recv, sizes differ per owner)
+    // (2) all-gather of the owners' regions (grouped send/recv, sizes differ per owner);
+    //     in peer-memory mode a barrier, then the apply kernels read the owners' regions
     ncclComm_t nc = x->comm->nccl;
+    if (x->p2p) {
+        if ((rc = flag_barrier(x, 1, st)) != TLC_OK) return rc;
+    } else {
     if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
     for (int o = 0; o < x->W; o++) {
         if (o == x->me) continue;
@@ -414,6 +557,7 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
         }
     }
     if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
+    }
     // (3) every rank applies every context to its full-size output (ACCUMULATE, R16)
     bool same = x->last_outs.size() == (size_t)T;
     for (int i = 0; same && i < T; i++) same = x->last_outs[i] == outs[i];
@@ -423,8 +567,10 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
             const Ctx &c = x->ctx[k];
             d[k] = tlc_tensor_desc{};
             d[k].out = outs[c.tensor] + c.lo;
-            d[k].payload = x->pull_buf + x->region_start[c.owner] + c.region_off;
-            d[k].hdr = x->pull_hdr + x->hdr_start[c.owner] + c.slot;
+            uint8_t *pb = x->p2p ? static_cast<uint8_t *>(x->peer[c.owner][2]) : x->pull_buf;
+            tlc_header *ph = x->p2p ? static_cast<tlc_header *>(x->peer[c.owner][3]) : x->pull_hdr;
+            d[k].payload = pb + x->region_start[c.owner] + c.region_off;
+            d[k].hdr = ph + x->hdr_start[c.owner] + c.slot;
             d[k].n = c.n;
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;
@@ -441,7 +587,9 @@ int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream)
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     int rc = cuda_ok(cudaMemsetAsync(x->d_status, 0, sizeof(unsigned int), st));
     const int nown = (int)x->owned[x->me].size();
-    if (rc == TLC_OK && nown) tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_recv, x->W * nown, x->d_status);
+    if (rc == TLC_OK && nown && !x->p2p) tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_recv, x->W * nown, x->d_status);
+    if (rc == TLC_OK && x->p2p && !x->ctx.empty())   // peer-memory mode: this rank's own pushes
+        tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_send, (int)x->ctx.size(), x->d_status);
     if (rc == TLC_OK && !x->ctx.empty()) tlc_status_kernel<<<1, 256, 0, st>>>(x->pull_hdr, (int)x->ctx.size(), x->d_status);
     if (rc == TLC_OK) rc = cuda_ok(cudaMemcpyAsync(status_out, x->d_status, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     if (rc == TLC_OK) rc = cuda_ok(cudaStreamSynchronize(st));

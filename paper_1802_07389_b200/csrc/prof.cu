@@ -16,7 +16,7 @@ namespace tlc {
 
 static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe", "k3_zre",
                                             "k4_zre_scan", "k5_expand_dequant",
-                                            "k5m_aggregate", "k7_unused",
+                                            "k5m_aggregate", "k9_flag_barrier",
                                             "k8_scale_mean"};
 
 namespace {

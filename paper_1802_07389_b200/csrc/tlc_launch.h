@@ -57,7 +57,7 @@ class KernelScope {
 // a binary search over the per-segment first-item numbers.
 constexpr uint64_t kT1 = 65536;     // K1 tile: elements
 constexpr uint64_t kT2 = 4096;      // K2 tile: quartic positions (1024 groups of 4)
-constexpr uint64_t kCH3 = 65536;    // K3 chunk: quartic bytes (8 warps x 8 rows of 1 KiB)
+constexpr uint64_t kCH3 = 32768;    // K3 chunk: quartic bytes (8 warps x 4 rows of 1 KiB)
 constexpr uint64_t kCH4 = 16384;    // K4 chunk: payload bytes (capacity based)
 constexpr uint64_t kT5 = 4096;      // K5 tile: quartic positions per output tile
 

@@ -21,7 +21,7 @@ def _grads(r, step, sizes=SIZES):
     return [synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
 
 
-def _run_rank(rank, world, steps, sizes=SIZES):
+def _run_rank(rank, world, steps, sizes=SIZES, p2p=False):
     """One rank's exchange; returns per-step means (owned flat) and final state."""
     import torch
 
@@ -29,7 +29,7 @@ def _run_rank(rank, world, steps, sizes=SIZES):
 
     dev = torch.device("cuda", torch.cuda.current_device())
     comm = T.Comm(rank, world, dev)
-    x = T.Exchange(comm, sizes)
+    x = T.Exchange(comm, sizes, p2p=p2p)
     outs = [torch.zeros(n, device=dev) for n in sizes]
     owned_per_step = []
     for step in range(steps):
@@ -74,14 +74,15 @@ def _check(world, results, sizes=SIZES, steps=STEPS):
             assert np.array_equal(res["outs"][t].view(np.uint32), outs[r][t].view(np.uint32)), ("out", r, t)
 
 
-def test_exchange_w1_in_process():
+@pytest.mark.parametrize("p2p", [False, True])
+def test_exchange_w1_in_process(p2p):
     import torch
 
     assert torch.cuda.is_available()
-    _check(1, [_run_rank(0, 1, STEPS)])
+    _check(1, [_run_rank(0, 1, STEPS, p2p=p2p)])
 
 
-def _mp_worker(rank, world, port, q):
+def _mp_worker(rank, world, port, q, p2p):
     import torch
     import torch.distributed as dist
 
@@ -89,14 +90,15 @@ def _mp_worker(rank, world, port, q):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        res = _run_rank(rank, world, STEPS)
+        res = _run_rank(rank, world, STEPS, p2p=p2p)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("world", [2, 4])
-def test_exchange_multi_gpu(world):
+def test_exchange_multi_gpu(world, p2p):
     import torch
     import torch.multiprocessing as mp
 
@@ -108,7 +110,7 @@ def test_exchange_multi_gpu(world):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
