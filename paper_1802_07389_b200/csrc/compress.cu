@@ -59,7 +59,7 @@ tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
             cur = si;
         }
         const Seg S = get_seg(T, si);
-        const uint64_t lo = (tile - S.k1) * kT1, hi = tmin<uint64_t>(S.n, lo + kT1);
+        const uint64_t lo = (tile - S.k1) * T.sz.t1, hi = tmin<uint64_t>(S.n, lo + T.sz.t1);
         uint64_t tail = lo;
         if (S.flags & kSegVec1) {
             const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
@@ -190,9 +190,9 @@ __device__ __forceinline__ void quant_qe_four(const float *__restrict__ t, float
 }
 
 template <class QT>
-__device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, const QT &Q) {
+__device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, uint64_t t2, const QT &Q) {
     const uint64_t P = S.P, n = S.n;
-    const uint64_t jend = tmin<uint64_t>(P, j0 + kT2);
+    const uint64_t jend = tmin<uint64_t>(P, j0 + t2);
     if (S.flags & kSegVec2) {
         // groups g with 4P + 4g + 3 < n are complete in all five partitions
         const uint64_t full = n >= 4 * P + 3 ? tmin<uint64_t>(P / 4, (n - 4 * P) / 4) : 0;
@@ -233,8 +233,8 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, f
         if (status != TLC_OK) continue;                  // err untouched (R6)
         uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
         const Quant Q(M);
-        if (Q.mode == 1) quant_qe_tile(S, bytes, lt * kT2, QuantCmp(Q));   // uniform branch
-        else quant_qe_tile(S, bytes, lt * kT2, Q);
+        if (Q.mode == 1) quant_qe_tile(S, bytes, lt * T.sz.t2, T.sz.t2, QuantCmp(Q));   // uniform branch
+        else quant_qe_tile(S, bytes, lt * T.sz.t2, T.sz.t2, Q);
     }
 }
 
@@ -410,8 +410,8 @@ tlc_zre_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float 
         float M;
         if (scale_from_key(maxkey[si], s, M) != TLC_OK) continue;      // segment failed in K1
         const uint8_t *bytes = scratch + S.bytes_off;
-        const uint64_t P = S.P, lc = id - S.k3, nch = (P + kCH3 - 1) / kCH3;
-        const uint64_t lo = lc * kCH3, hi = tmin<uint64_t>(P, lo + kCH3);
+        const uint64_t P = S.P, lc = id - S.k3, nch = (P + T.sz.c3 - 1) / T.sz.c3;
+        const uint64_t lo = lc * T.sz.c3, hi = tmin<uint64_t>(P, lo + T.sz.c3);
         const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
         const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
 
@@ -485,7 +485,7 @@ static uint64_t bulk_tiles(const SegTable &T, int use_zre) {
     if (!(S.flags & kSegVec2) || S.P % 4 != 0) return 0;
     if (!use_zre && !aligned4(S.payload)) return 0;
     const uint64_t complete = S.n >= 4 * S.P ? tmin<uint64_t>(S.P, S.n - 4 * S.P) : 0;
-    return (complete / kT2) * (kT2 / kBulkPos);
+    return (complete / T.sz.t2) * (T.sz.t2 / kBulkPos);
 }
 
 // TLC_NO_BULK=1 disables the bulk-copy K2 path (A/B measurements)
@@ -525,7 +525,7 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
             }
             const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);
             tlc_quant_qe_bulk_kernel<<<grid, kK2Threads, sizeof(BulkSmem), st>>>(T, maxkey, s, use_zre, scratch, nbulk);
-            tile_begin = nbulk * kBulkPos / kT2;
+            tile_begin = nbulk * kBulkPos / T.sz.t2;
         }
         if (tile_begin < T.n2) {
             if (!g_k2_blocks)

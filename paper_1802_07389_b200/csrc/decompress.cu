@@ -66,7 +66,7 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         }
         if (!(hdr->flags & TLC_FLAG_ZRE)) continue;       // K5 reads the quartic bytes directly
         const uint64_t P = S.P, Z = hdr->payload_len;
-        const uint64_t lo = lc * kCH4, hi = tmin<uint64_t>(Z, lo + kCH4);
+        const uint64_t lo = lc * T.sz.c4, hi = tmin<uint64_t>(Z, lo + T.sz.c4);
         if (lo >= Z) continue;                            // past the payload: nothing to scan
         const uint64_t num_out_tiles = (P + kT5 - 1) / kT5;
 

@@ -10,12 +10,12 @@
 
 namespace tlc {
 
-void seg_items(Seg &s, uint64_t &c1, uint64_t &c2, uint64_t &c3, uint64_t &c4, uint64_t &c5) {
+void seg_items(Seg &s, const ItemSizes &z, uint64_t &c1, uint64_t &c2, uint64_t &c3, uint64_t &c4, uint64_t &c5) {
     s.P = (s.n + 4) / 5;
-    s.k1 = c1; c1 += (s.n + kT1 - 1) / kT1;
-    s.k2 = c2; c2 += (s.P + kT2 - 1) / kT2;
-    s.k3 = c3; c3 += (s.P + kCH3 - 1) / kCH3;
-    s.k4 = c4; c4 += (s.P + kCH4 - 1) / kCH4;
+    s.k1 = c1; c1 += (s.n + z.t1 - 1) / z.t1;
+    s.k2 = c2; c2 += (s.P + z.t2 - 1) / z.t2;
+    s.k3 = c3; c3 += (s.P + z.c3 - 1) / z.c3;
+    s.k4 = c4; c4 += (s.P + z.c4 - 1) / z.c4;
     s.k5 = c5; c5 += (s.P + kT5 - 1) / kT5;
 }
 
@@ -34,7 +34,8 @@ SegTable single_table(const float *t, float *err, float *out, uint8_t *payload, 
     Seg &s = T.one;
     s = Seg{};
     s.t = t; s.err = err; s.out = out; s.payload = payload; s.hdr = hdr; s.n = n;
-    seg_items(s, T.n1, T.n2, T.n3, T.n4, T.n5);
+    T.sz = item_sizes(n);
+    seg_items(s, T.sz, T.n1, T.n2, T.n3, T.n4, T.n5);
     s.bytes_off = 0;
     s.flags = seg_flags(s);
     scratch = (s.P + 15) & ~uint64_t(15);
@@ -60,17 +61,20 @@ WsLayout ws_layout(const SegTable &T, uint64_t scratch_bytes) {
 int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws) {
     count = cnt;
     host.assign(cnt, Seg{});
-    uint64_t c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, scratch = 0;
+    uint64_t c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, scratch = 0, total = 0;
+    for (int i = 0; i < cnt; i++) total += descs[i].n;
+    const ItemSizes z = item_sizes(total);
     for (int i = 0; i < cnt; i++) {
         const tlc_tensor_desc &d = descs[i];
         if (d.n == 0 || d.n >= (1ull << 42) || !d.hdr) return TLC_ERR_ARG;
         Seg &s = host[i];
         s.t = d.t; s.err = d.err; s.out = d.out; s.payload = d.payload; s.hdr = d.hdr; s.n = d.n;
-        seg_items(s, c1, c2, c3, c4, c5);
+        seg_items(s, z, c1, c2, c3, c4, c5);
         s.bytes_off = scratch;
         scratch += (s.P + 15) & ~uint64_t(15);
     }
     T = SegTable{};
+    T.sz = z;
     T.count = cnt;
     T.n1 = c1; T.n2 = c2; T.n3 = c3; T.n4 = c4; T.n5 = c5;
     ws_bytes = ws_layout(T, with_scratch ? scratch : 0).total;

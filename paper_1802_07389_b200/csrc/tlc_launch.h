@@ -55,10 +55,17 @@ class KernelScope {
 // (tlc_batch_*) is a device-resident table.  Work items of each kernel are
 // numbered globally, segment after segment; a CTA maps an item to its segment by
 // a binary search over the per-segment first-item numbers.
-constexpr uint64_t kT1 = 65536;     // K1 tile: elements
-constexpr uint64_t kT2 = 4096;      // K2 tile: quartic positions (1024 groups of 4)
-constexpr uint64_t kCH3 = 32768;    // K3 chunk: quartic bytes (8 warps x 4 rows of 1 KiB)
-constexpr uint64_t kCH4 = 16384;    // K4 chunk: payload bytes (capacity based)
+// Work-item sizes of a table: large tables favour long streams per item, small ones
+// (e.g. the 1.7M values of ResNet-110) more items so that every SM gets work.
+struct ItemSizes {
+    uint64_t t1;    // K1 tile: elements
+    uint64_t t2;    // K2 tile: quartic positions
+    uint64_t c3;    // K3 chunk: quartic bytes (8 warps x rows of 1 KiB)
+    uint64_t c4;    // K4 chunk: payload bytes (capacity based)
+};
+constexpr ItemSizes kLargeItems{65536, 4096, 32768, 16384};
+constexpr ItemSizes kSmallItems{8192, 1024, 8192, 4096};
+constexpr uint64_t kSmallTableElems = 32ull << 20;   // tables below 32M values use kSmallItems
 constexpr uint64_t kT5 = 4096;      // K5 tile: quartic positions per output tile
 
 enum SegFlags : uint32_t { kSegVec2 = 1u, kSegVec5 = 2u, kSegVec1 = 4u };
@@ -80,6 +87,7 @@ struct SegTable {
     Seg one;                        // the segment when count == 1
     int count;
     uint64_t n1, n2, n3, n4, n5;    // total items per kernel
+    ItemSizes sz;
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -89,7 +97,8 @@ struct WsLayout {
 };
 
 WsLayout ws_layout(const SegTable &T, uint64_t scratch_bytes);
-void seg_items(Seg &s, uint64_t &c1, uint64_t &c2, uint64_t &c3, uint64_t &c4, uint64_t &c5);
+void seg_items(Seg &s, const ItemSizes &z, uint64_t &c1, uint64_t &c2, uint64_t &c3, uint64_t &c4, uint64_t &c5);
+inline ItemSizes item_sizes(uint64_t total_elems) { return total_elems < kSmallTableElems ? kSmallItems : kLargeItems; }
 SegTable single_table(const float *t, float *err, float *out, uint8_t *payload, tlc_header *hdr, uint64_t n,
                       uint64_t &scratch);
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st);
