@@ -256,6 +256,17 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
             evs[k][1].record(stream)
     torch.cuda.synchronize(dev)
     ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    # per-kernel device times of the same step (outside the graph, library CUDA events)
+    T.tlc_prof_collect()
+    T.tlc_prof_enable(True)
+    with torch.cuda.stream(stream):
+        for k in range(20):
+            flush.fill_(k & 0xff)
+            ctx.compress(tsets[k % 2], s, True, stream, batch=cb[k % 2])
+            ctx.decompress(outs, T.TLC_MODE_OVERWRITE, stream, batch=db)
+    torch.cuda.synchronize(dev)
+    T.tlc_prof_enable(False)
+    kern = {k: round(t / c * 1e3, 2) for k, (c, t) in T.tlc_prof_collect().items()}
     del flush
     N = sum(sizes)
     Z = sum(h["payload_len"] for h in ctx.headers())
@@ -265,7 +276,7 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
             "l2": "flushed (512 MiB write) before every timed step",
             "warm": {"value": 4.0 * N / (ms_warm / 1e3) / 1e9, "ms_per_step": ms_warm,
                      "l2": "back-to-back replays, working set L2-resident"},
-            "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 5,
+            "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 5, "kernel_us_cold": kern,
             "host_launch_calls_during_replay": T.tlc_launch_count() - l0}
 
 
