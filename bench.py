@@ -399,9 +399,7 @@ def run_tlc(args):
     # ---------------- timed region (device events on the launching stream)
     K = args.steps
     clocks = ClockSampler(dev)
-    T.tlc_prof_collect()
     launches0 = T.tlc_launch_count()
-    T.tlc_prof_enable(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     clocks.start()
@@ -411,9 +409,7 @@ def run_tlc(args):
     e1.record(stream)
     barrier()
     clocks.stop()
-    T.tlc_prof_enable(False)
     gpu_launches = T.tlc_launch_count() - launches0
-    prof = T.tlc_prof_collect()
     ms = e0.elapsed_time(e1)
     h = T.parse_header(hdr)
     Z = h["payload_len"]
@@ -422,6 +418,22 @@ def run_tlc(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * 4.0 * n * K / (ms / 1e3) / 1e9
+
+    # ---------------- the same K steps again with a CUDA-event pair around every library
+    # kernel launch on its stream (per-kernel durations for the roofline; the events
+    # break the programmatic-dependent-launch overlap, so this pass is a bit slower)
+    T.tlc_prof_collect()
+    T.tlc_prof_enable(True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    p0.record(stream)
+    for k in range(K):
+        step(k)
+    p1.record(stream)
+    barrier()
+    T.tlc_prof_enable(False)
+    prof = T.tlc_prof_collect()
+    ms_prof = p0.elapsed_time(p1)
 
     # ---------------- roofline of the dominant kernel (K2) and the per-kernel table
     peak, peak_src = load_peaks()
@@ -439,7 +451,7 @@ def run_tlc(args):
         b = alg.get(name)
         kernels[name] = {"launches_per_step": cnt / K, "avg_ms": avg,
                          "alg_bytes": b, "alg_GBps": (b / (avg / 1e3) / 1e9) if b else None,
-                         "share_of_step": (tot / K) / (ms / K) if ms else None}
+                         "share_of_step": (tot / K) / (ms_prof / K) if ms_prof else None}
     dom = "k2_quant_qe"
     dk = kernels.get(dom, {})
     achieved = dk.get("alg_GBps")
@@ -502,7 +514,8 @@ def run_tlc(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
-            "warmup": max(3, args.warmup), "ms_per_step": ms / K, "higher_is_better": True,
+            "warmup": max(3, args.warmup), "ms_per_step": ms / K, "ms_per_step_profiled_pass": ms_prof / K,
+            "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: N(0,1) fp32 state changes (numpy PCG64, synth/), "
                     f"{len(ts)} rotating tensors per rank, error buffer carried across steps",

@@ -49,6 +49,7 @@ __device__ __forceinline__ void k1_flush(unsigned int m, unsigned int *maxkey, i
 __global__ void __launch_bounds__(kK1Threads, 1)
 tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
     __shared__ unsigned int s_warp[kK1Threads / 32];
+    pdl_trigger();
     unsigned int m = 0;
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n1; tile += gridDim.x) {
@@ -215,6 +216,8 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
                     uint8_t *__restrict__ scratch, uint64_t tile_begin) {
+    pdl_trigger();
+    pdl_wait();                                          // K1's max keys (or the bulk kernel's tiles)
     for (uint64_t tile = tile_begin + blockIdx.x; tile < T.n2; tile += gridDim.x) {
         const int si = find_seg<2>(T, tile);
         const Seg S = get_seg(T, si);
@@ -307,6 +310,12 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *__restrict__ maxk
     static_assert(kBulkPos == 4 * kK2Threads, "one group of four positions per thread");
     extern __shared__ __align__(128) uint8_t smem_raw[];
     BulkSmem &sm = *reinterpret_cast<BulkSmem *>(smem_raw);
+    pdl_trigger();
+    if (threadIdx.x == 0) {                              // barrier setup overlaps K1's tail
+        for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait();                                          // K1's max keys
     const Seg S = T.one;
     float M;
     const unsigned int status = scale_from_key(maxkey[0], s, M);   // Eq. 1, R6
@@ -323,10 +332,6 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *__restrict__ maxk
     uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
     const uint64_t P = S.P;
     const uint64_t mine = nbulk > blockIdx.x ? (nbulk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     __syncthreads();
     auto issue = [&](uint64_t k) {
         const int st = (int)(k % kBulkStages);
@@ -399,6 +404,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float 
     __shared__ unsigned long long s_id;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t w[8];
+    pdl_wait();                                          // K2's quartic bytes and headers
     while (true) {
         if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k3_counter, 1ull);
         __syncthreads();
@@ -524,14 +530,15 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
                 attr = true;
             }
             const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);
-            tlc_quant_qe_bulk_kernel<<<grid, kK2Threads, sizeof(BulkSmem), st>>>(T, maxkey, s, use_zre, scratch, nbulk);
+            launch_pdl(tlc_quant_qe_bulk_kernel, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s, use_zre, scratch,
+                       nbulk);
             tile_begin = nbulk * kBulkPos / T.sz.t2;
         }
         if (tile_begin < T.n2) {
             if (!g_k2_blocks)
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
             const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2 - tile_begin, (uint64_t)sms * tmax(1, g_k2_blocks)));
-            tlc_quant_qe_kernel<<<grid, kK2Threads, 0, st>>>(T, maxkey, s, use_zre, scratch, tile_begin);
+            launch_pdl(tlc_quant_qe_kernel, grid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin);
         }
     }
     if (use_zre) {
@@ -539,7 +546,7 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
         if (!g_k3_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
-        tlc_zre_kernel<<<grid, kK3Threads, 0, st>>>(T, maxkey, s, scratch, ctrl, states);
+        launch_pdl(tlc_zre_kernel, grid, kK3Threads, 0, st, T, maxkey, s, scratch, ctrl, states);
     }
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }

@@ -50,6 +50,7 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
     __shared__ unsigned long long s_wsum[kScanWarps];
     __shared__ unsigned long long s_id;
     uint32_t len[kK4Seg];
+    pdl_trigger();
     while (true) {
         if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k4_counter, 1ull);
         __syncthreads();
@@ -229,6 +230,7 @@ template <int kMode>
 __global__ void __launch_bounds__(kK5Threads)
 tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict__ seek) {
     __shared__ K5Smem sm;
+    pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n5; tile += gridDim.x) {
         const int si = find_seg<5>(T, tile);
@@ -383,6 +385,7 @@ __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
 __global__ void __launch_bounds__(kK5Threads, 3)
 tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *__restrict__ seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
+    pdl_wait();                                          // K4's seek entries
     K5mHead &sm = *reinterpret_cast<K5mHead *>(smem_raw);
     uint8_t(*E)[kT5] = reinterpret_cast<uint8_t(*)[kT5]>(smem_raw + sizeof(K5mHead));
     uint32_t(*V)[5][256] = reinterpret_cast<uint32_t(*)[5][256]>(smem_raw + sizeof(K5mHead) + (size_t)W * kT5);
@@ -487,7 +490,7 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_kernel, kK5Threads, k5m_smem_bytes(W));
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * tmax(1, per_sm)));
-    tlc_aggregate_kernel<<<grid, kK5Threads, k5m_smem_bytes(W), st>>>(A, X, W, seek);
+    launch_pdl(tlc_aggregate_kernel, grid, kK5Threads, k5m_smem_bytes(W), st, A, X, W, seek);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
@@ -514,8 +517,8 @@ int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t 
     if (!g_k5_blocks)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k5_blocks, tlc_expand_dequant_kernel<0>, kK5Threads, 0);
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n5, (uint64_t)sms * tmax(1, g_k5_blocks)));
-    if (mode == TLC_MODE_OVERWRITE) tlc_expand_dequant_kernel<0><<<grid, kK5Threads, 0, st>>>(T, seek);
-    else tlc_expand_dequant_kernel<1><<<grid, kK5Threads, 0, st>>>(T, seek);
+    if (mode == TLC_MODE_OVERWRITE) launch_pdl(tlc_expand_dequant_kernel<0>, grid, kK5Threads, 0, st, T, seek);
+    else launch_pdl(tlc_expand_dequant_kernel<1>, grid, kK5Threads, 0, st, T, seek);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 

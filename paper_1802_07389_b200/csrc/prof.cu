@@ -7,6 +7,7 @@
 // launch counts and summed device durations -- bench.py uses it for the live
 // roofline of the dominant kernel.
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -58,6 +59,16 @@ KernelScope::~KernelScope() {
         cudaEventRecord(b, st_);
         g_recs.push_back(Rec{id_, (cudaEvent_t)a_, b});
     }
+}
+
+// TLC_NO_PDL=1 launches every kernel without programmatic dependent launch
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_NO_PDL");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 }  // namespace tlc

@@ -32,6 +32,26 @@ inline int num_sms() {
     return sms[dev];
 }
 
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor drains; it must execute pdl_wait() (griddepcontrol.wait) before
+// touching the predecessor's results.  Launch overhead of the chain overlaps.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Kernel ids for launch counting / profiling (prof.cu).
 enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7, kNumKernelIds = 8 };
 
