@@ -214,7 +214,7 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
 #define TLC_K2_MINB 2
 #endif
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
-tlc_quant_qe_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
+tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
                     uint8_t *__restrict__ scratch, uint64_t tile_begin) {
     pdl_trigger();
     pdl_wait();                                          // K1's max keys (or the bulk kernel's tiles)
@@ -305,7 +305,7 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
 }
 
 __global__ void __launch_bounds__(kK2Threads, 1)
-tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s, int use_zre,
+tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
                          uint8_t *__restrict__ scratch, uint64_t nbulk) {
     static_assert(kBulkPos == 4 * kK2Threads, "one group of four positions per thread");
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -373,7 +373,7 @@ constexpr int kK3Seg = 32;                                   // bytes per lane p
 constexpr int kK3WarpRow = 32 * kK3Seg;                      // 1 KiB per warp row
 
 // Load [pos, min(pos+32, hi)) as 8 words, padding with 121 (0x79).
-__device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint64_t pos, uint64_t hi,
+__device__ __forceinline__ int load_seg(const uint8_t *bytes, uint64_t pos, uint64_t hi,
                                         uint32_t (&w)[8]) {
     const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
     if (len == kK3Seg && (reinterpret_cast<uintptr_t>(bytes + pos) & 15u) == 0) {
@@ -397,8 +397,8 @@ __device__ __forceinline__ int load_seg(const uint8_t *__restrict__ bytes, uint6
 }
 
 __global__ void __launch_bounds__(kK3Threads)
-tlc_zre_kernel(const SegTable T, const unsigned int *__restrict__ maxkey, float s,
-               const uint8_t *__restrict__ scratch, Ctrl *ctrl, unsigned long long *states) {
+tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
+               const uint8_t *scratch, Ctrl *ctrl, unsigned long long *states) {
     __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wagg[kScanWarps];
     __shared__ unsigned long long s_id;

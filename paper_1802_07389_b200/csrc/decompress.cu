@@ -152,8 +152,8 @@ struct K5Smem {
 // positions (zero-run codes expand to 121s).  seek points at the segment's seek
 // entries.  Without ZRE the bytes are copied (a literal > 242 returns true:
 // FORMAT).  Ends with E complete and visible to the whole block.
-__device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, const uint8_t *__restrict__ payload,
-                                            bool zre, uint64_t Z, const unsigned long long *__restrict__ seek,
+__device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, const uint8_t *payload,
+                                            bool zre, uint64_t Z, const unsigned long long *seek,
                                             uint64_t lt, uint64_t ntiles, uint64_t J0, int tl) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     bool bad = false;
@@ -228,7 +228,7 @@ __device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, 
 
 template <int kMode>
 __global__ void __launch_bounds__(kK5Threads)
-tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *__restrict__ seek) {
+tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     __shared__ K5Smem sm;
     pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
@@ -383,7 +383,7 @@ __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
 }
 
 __global__ void __launch_bounds__(kK5Threads, 3)
-tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *__restrict__ seek) {
+tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     pdl_wait();                                          // K4's seek entries
     K5mHead &sm = *reinterpret_cast<K5mHead *>(smem_raw);
