@@ -49,11 +49,13 @@ __device__ __forceinline__ void k1_flush(unsigned int m, unsigned int *maxkey, i
 __global__ void __launch_bounds__(kK1Threads, 1)
 tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
     __shared__ unsigned int s_warp[kK1Threads / 32];
+    __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
+    seg_index_load<1>(T, s_first);
     unsigned int m = 0;
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n1; tile += gridDim.x) {
-        const int si = find_seg<1>(T, tile);
+        const int si = find_seg_c<1>(T, tile, s_first);
         if (si != cur) {                                  // uniform: flush the previous segment
             if (cur >= 0) k1_flush(m, maxkey, cur, s_warp);
             m = 0;
@@ -216,10 +218,12 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
                     uint8_t *__restrict__ scratch, uint64_t tile_begin) {
+    __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
+    seg_index_load<2>(T, s_first);
     pdl_wait();                                          // K1's max keys (or the bulk kernel's tiles)
     for (uint64_t tile = tile_begin + blockIdx.x; tile < T.n2; tile += gridDim.x) {
-        const int si = find_seg<2>(T, tile);
+        const int si = find_seg_c<2>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         float M;
         const unsigned int status = scale_from_key(maxkey[si], s, M);   // Eq. 1, R6
@@ -372,6 +376,14 @@ constexpr int kK3Threads = kScanThreads;
 constexpr int kK3Seg = 32;                                   // bytes per lane per row
 constexpr int kK3WarpRow = 32 * kK3Seg;                      // 1 KiB per warp row
 
+// true if the lane's 32 bytes are all 121 (padding included)
+__device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) x |= w[k] ^ 0x79797979u;
+    return x == 0;
+}
+
 // Load [pos, min(pos+32, hi)) as 8 words, padding with 121 (0x79).
 __device__ __forceinline__ int load_seg(const uint8_t *bytes, uint64_t pos, uint64_t hi,
                                         uint32_t (&w)[8]) {
@@ -402,8 +414,12 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
     __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wagg[kScanWarps];
     __shared__ unsigned long long s_id;
+    __shared__ uint16_t s_lit[kScanWarps][kK3WarpRow];              // literal positions of a warp row
+    __shared__ __align__(16) uint8_t s_rowb[kScanWarps][kK3WarpRow]; // the row's bytes
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t w[8];
+    __shared__ uint64_t s_first[kSegCache];
+    seg_index_load<3>(T, s_first);
     pdl_wait();                                          // K2's quartic bytes and headers
     while (true) {
         if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k3_counter, 1ull);
@@ -411,7 +427,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         const uint64_t id = s_id;
         __syncthreads();
         if (id >= T.n3) break;
-        const int si = find_seg<3>(T, id);
+        const int si = find_seg_c<3>(T, id, s_first);
         const Seg S = get_seg(T, si);
         float M;
         if (scale_from_key(maxkey[si], s, M) != TLC_OK) continue;      // segment failed in K1
@@ -425,8 +441,12 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         RunSum wagg = run_identity();
         for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
             const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
-            const uint32_t mask = literal_mask(w);
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+            if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal in the row: one ALL run
+                wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
+                continue;
+            }
+            const uint32_t mask = literal_mask(w);
             wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
         }
         if (lane == 0) s_wagg[warp] = pack(wagg);
@@ -434,14 +454,18 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         RunSum agg = run_identity();
 #pragma unroll
         for (int k = 0; k < kScanWarps; k++) agg = compose(agg, unpack(s_wagg[k]));
-        if (threadIdx.x == 0) st_relaxed_u64(states + id, kReady | pack(agg));
+        if (threadIdx.x == 0) st_relaxed_u64(states + id, (lc == 0 ? kPrefix : kReady) | pack(agg));
 
-        // ---- phase 2: carry-in = composition of the segment's preceding chunk summaries
-        RunSum part = run_identity();
-        const uint64_t per = (lc + kK3Threads - 1) / kK3Threads;
-        const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(lc, i0 + per);
-        for (uint64_t i = i0; i < i1; i++) part = compose(part, unpack(wait_ready(states + S.k3 + i) & ~kReady));
-        const RunSum chunk_in = block_reduce_runs(part, s_warp);
+        // ---- phase 2: carry-in = composition of the segment's preceding chunks (look-back)
+        if (warp == 0) {
+            const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
+            if (lane == 0) {
+                if (lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, pack(agg)));
+                s_warp[0] = ex;
+            }
+        }
+        __syncthreads();
+        const RunSum chunk_in = unpack(s_warp[0]);
         if (lc == nch - 1 && threadIdx.x == 0) {
             uint64_t total;
             uint32_t carry;
@@ -458,24 +482,80 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
             const uint64_t pos = row + (uint64_t)kK3Seg * lane;
             const int len = load_seg(bytes, pos, whi, w);
-            const uint32_t mask = literal_mask(w);
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-            const WarpRow r = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
-            uint32_t ex = r.count;                    // exclusive prefix of the lane counts
+            if (__all_sync(0xffffffffu, plain_lane(w))) {
+                // no literal in the row: the pending run grows by row_len and a
+                // full chunk (code 255) is emitted every 14 zero groups
+                const uint32_t x = carry + row_len, cnt = x / kMaxRun;
+                warp_fill_full_chunks(S.payload, off, off + cnt);
+                carry = x - cnt * kMaxRun;
+                off += cnt;
+                if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
+                continue;
+            }
+            // literal list of the row (positions in row order) and its bytes, in shared memory;
+            // load_seg pads with 121, so bits past the end of the stream are clear
+            const uint32_t mask = literal_mask(w);
+            const uint32_t nl = popc32(mask);
+            uint32_t b = nl;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, ex, d);
-                if (lane >= d) ex += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, b, d);
+                if (lane >= d) b += y;
             }
-            ex -= r.count;
-            if (len > 0) {
-                uint64_t o = off + ex;
-                uint32_t c = r.carry_in;
-                mask_emit(w, mask, len, c, S.payload, o);
-                if (c > 0 && pos + len == P) S.payload[o] = run_code(c);
+            const uint32_t L = __shfl_sync(0xffffffffu, b, 31);
+            b -= nl;
+            uint16_t *lit = s_lit[warp];
+            uint4 *rb = reinterpret_cast<uint4 *>(s_rowb[warp] + kK3Seg * lane);
+            rb[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            rb[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = (uint16_t)(kK3Seg * lane + ctz32(m));
+            __syncwarp();
+            // literal k (one per lane and round) is preceded by R 121s: R/14 full chunks
+            // (code 255), one flush code if R%14 > 0, then the literal itself
+            const uint32_t c_row = carry;
+            const uint32_t Rt = row_len - 1u - lit[L - 1];           // trailing 121s of the row
+            uint32_t rsum = 0;
+            if (L > 32) {                                            // dense row: count first
+                for (uint32_t k = lane; k < L; k += 32) {
+                    const uint32_t R = lit[k] - (k ? lit[k - 1] + 1u : 0u) + (k ? 0u : c_row);
+                    rsum += R / kMaxRun + (R % kMaxRun != 0) + 1u;
+                }
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, d);
             }
-            off += r.row_count;
-            carry = r.carry_out;
+            uint32_t base = 0;
+            for (uint32_t k0 = 0; k0 < L; k0 += 32) {
+                const uint32_t k = k0 + lane;
+                uint32_t R = 0, cost = 0, p = 0;
+                if (k < L) {
+                    p = lit[k];
+                    R = p - (k ? lit[k - 1] + 1u : 0u) + (k ? 0u : c_row);
+                    cost = R / kMaxRun + (R % kMaxRun != 0) + 1u;
+                }
+                uint32_t x = cost;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                    if (lane >= d) x += y;
+                }
+                const uint32_t round_total = __shfl_sync(0xffffffffu, x, 31);
+                if (k0 == 0) {                                       // 255s before any literal store
+                    const uint32_t row_count = (L > 32 ? rsum : round_total) + Rt / kMaxRun;
+                    warp_fill_full_chunks(S.payload, off, off + row_count);
+                    __syncwarp();
+                }
+                if (k < L) {
+                    uint64_t o = off + base + (x - cost) + R / kMaxRun;
+                    if (R % kMaxRun) S.payload[o++] = run_code(R % kMaxRun);
+                    S.payload[o] = s_rowb[warp][p];
+                }
+                base += round_total;
+            }
+            off += base + Rt / kMaxRun;
+            carry = Rt % kMaxRun;
+            if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
+            __syncwarp();                                            // s_lit / s_rowb reused
         }
     }
 }

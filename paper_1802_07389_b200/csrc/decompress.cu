@@ -50,25 +50,37 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
     __shared__ unsigned long long s_wsum[kScanWarps];
     __shared__ unsigned long long s_id;
     uint32_t len[kK4Seg];
+    __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
+    seg_index_load<4>(T, s_first);
     while (true) {
         if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k4_counter, 1ull);
         __syncthreads();
         const uint64_t id = s_id;
         __syncthreads();
         if (id >= T.n4) break;
-        const int si = find_seg<4>(T, id);
+        const int si = find_seg_c<4>(T, id, s_first);
         const Seg S = get_seg(T, si);
         const uint64_t lc = id - S.k4;
         tlc_header *hdr = S.hdr;
+        // Chunks are sized by P (Z is only known on the device); once a chunk of a
+        // segment has nothing to scan, neither have the segment's later ones, and
+        // no chunk with work waits on them: advance the counter past the segment.
+        const uint64_t seg_end = S.k4 + (S.P + T.sz.c4 - 1) / T.sz.c4;
         if (!header_valid(hdr, S.n)) {                    // uniform over the CTA
-            if (lc == 0 && threadIdx.x == 0 && hdr->status == TLC_OK) raise_format(hdr);
+            if (threadIdx.x == 0) {
+                if (lc == 0 && hdr->status == TLC_OK) raise_format(hdr);
+                atomicMax(&ctrl->k4_counter, (unsigned long long)seg_end);
+            }
             continue;
         }
-        if (!(hdr->flags & TLC_FLAG_ZRE)) continue;       // K5 reads the quartic bytes directly
         const uint64_t P = S.P, Z = hdr->payload_len;
         const uint64_t lo = lc * T.sz.c4, hi = tmin<uint64_t>(Z, lo + T.sz.c4);
-        if (lo >= Z) continue;                            // past the payload: nothing to scan
+        if (!(hdr->flags & TLC_FLAG_ZRE) || lo >= Z) {    // no ZRE (K5 reads the quartic bytes
+            if (threadIdx.x == 0)                         // directly) or past the payload
+                atomicMax(&ctrl->k4_counter, (unsigned long long)seg_end);
+            continue;
+        }
         const uint64_t num_out_tiles = (P + kT5 - 1) / kT5;
 
         // the chunk is split into one sub-range per warp, scanned in warp rows of 32 x 16 bytes
@@ -96,14 +108,18 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
             before += k < warp ? s_wsum[k] : 0ull;
             agg += s_wsum[k];
         }
-        if (threadIdx.x == 0) st_relaxed_u64(states + id, kReady | agg);
+        if (threadIdx.x == 0) st_relaxed_u64(states + id, (lc == 0 ? kPrefix : kReady) | agg);
 
-        // ---- phase 2: quartic position of the chunk's first byte
-        uint64_t part = 0;
-        const uint64_t per = (lc + kK4Threads - 1) / kK4Threads;
-        const uint64_t i0 = per * threadIdx.x, i1 = tmin<uint64_t>(lc, i0 + per);
-        for (uint64_t i = i0; i < i1; i++) part += wait_ready(states + S.k4 + i) & ~kReady;
-        const uint64_t run = block_reduce_sum(part, s_warp);
+        // ---- phase 2: quartic position of the chunk's first byte (look-back)
+        if (warp == 0) {
+            const unsigned long long ex = warp_lookback<SumOp>(states + S.k4, lc);
+            if (lane == 0) {
+                if (lc > 0) st_relaxed_u64(states + id, kPrefix | (ex + agg));
+                s_warp[0] = ex;
+            }
+        }
+        __syncthreads();
+        const uint64_t run = s_warp[0];
         if (hi == Z && threadIdx.x == 0 && run + agg != P) raise_format(hdr);
 
         // ---- phase 3: seek entries (payload byte covering J0 = k*kT5, offset inside it)
@@ -230,10 +246,12 @@ template <int kMode>
 __global__ void __launch_bounds__(kK5Threads)
 tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     __shared__ K5Smem sm;
+    __shared__ uint64_t s_first[kSegCache];
+    seg_index_load<5>(T, s_first);
     pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n5; tile += gridDim.x) {
-        const int si = find_seg<5>(T, tile);
+        const int si = find_seg_c<5>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         const tlc_header *hdr = S.hdr;
         if (hdr->status != TLC_OK) continue;             // uniform: FORMAT from K4 or a failed compress
@@ -366,6 +384,7 @@ struct K5mHead {
     int ok[kMaxSources];
     unsigned int warp_sum[kK5Threads / 32];
 };
+constexpr int kK5mSegCache = 128;
 __host__ __device__ constexpr size_t k5m_smem_bytes(int W) {
     return sizeof(K5mHead) + (size_t)W * kT5 + (size_t)W * 5 * 256 * sizeof(uint32_t);
 }
@@ -385,6 +404,8 @@ __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
 __global__ void __launch_bounds__(kK5Threads, 3)
 tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ uint64_t s_first[kK5mSegCache];         // owned contexts: few per rank
+    seg_index_load<5, kK5mSegCache>(A, s_first);
     pdl_wait();                                          // K4's seek entries
     K5mHead &sm = *reinterpret_cast<K5mHead *>(smem_raw);
     uint8_t(*E)[kT5] = reinterpret_cast<uint8_t(*)[kT5]>(smem_raw + sizeof(K5mHead));
@@ -395,7 +416,7 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
     const float Wf = (float)W, rW = 1.0f / (float)W;
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < A.n5; tile += gridDim.x) {
-        const int q = find_seg<5>(A, tile);
+        const int q = find_seg_c<5, kK5mSegCache>(A, tile, s_first);
         const Seg S = get_seg(A, q);
         const uint64_t P = S.P, n = S.n, lt = tile - S.k5, ntiles = (P + kT5 - 1) / kT5;
         const uint64_t J0 = lt * kT5;

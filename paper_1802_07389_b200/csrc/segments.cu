@@ -79,6 +79,17 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
     T.n1 = c1; T.n2 = c2; T.n3 = c3; T.n4 = c4; T.n5 = c5;
     ws_bytes = ws_layout(T, with_scratch ? scratch : 0).total;
     if (cudaMalloc((void **)&d, cnt * sizeof(Seg)) != cudaSuccess) return TLC_ERR_CUDA;
+    if (cudaMalloc((void **)&d_first, 5 * (size_t)cnt * sizeof(uint64_t)) != cudaSuccess) return TLC_ERR_CUDA;
+    {
+        std::vector<uint64_t> f(5 * (size_t)cnt);
+        for (int i = 0; i < cnt; i++) {
+            f[0 * cnt + i] = host[i].k1; f[1 * cnt + i] = host[i].k2; f[2 * cnt + i] = host[i].k3;
+            f[3 * cnt + i] = host[i].k4; f[4 * cnt + i] = host[i].k5;
+        }
+        if (cudaMemcpy(d_first, f.data(), f.size() * sizeof(uint64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+            return TLC_ERR_CUDA;
+        for (int k = 0; k < 5; k++) T.first[k] = d_first + (size_t)k * cnt;
+    }
     if (shared_ws) {
         ws = shared_ws;
     } else {
@@ -109,6 +120,8 @@ int Table::update(const tlc_tensor_desc *descs) {
 
 void Table::release() {
     if (d) cudaFree(d);
+    if (d_first) cudaFree(d_first);
+    d_first = nullptr;
     if (own_ws && ws) cudaFree(ws);
     d = nullptr;
     ws = nullptr;

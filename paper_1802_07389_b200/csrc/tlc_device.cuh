@@ -313,31 +313,6 @@ __host__ __device__ __forceinline__ RunSum mask_summary(uint32_t mask, int len) 
     return s;
 }
 
-// Emit the ZRE bytes of the first len bytes of a segment entered with carry c
-// at payload offset `off`; on return c is the carry out and off the next offset.
-__host__ __device__ __forceinline__ void mask_emit(const uint32_t (&w)[8], uint32_t mask, int len,
-                                                   uint32_t &c, uint8_t *payload, uint64_t &off) {
-    if (len <= 0) return;
-    if (len < 32) mask &= (1u << len) - 1u;
-    int prev = -1;
-    while (mask) {
-        const int p = (int)ctz32(mask);
-        mask &= mask - 1u;
-        uint32_t total = (uint32_t)(p - prev - 1) + c;   // pending 121s before this literal
-        c = 0;
-        while (total >= kMaxRun) { payload[off++] = run_code(kMaxRun); total -= kMaxRun; }
-        if (total) payload[off++] = run_code(total);
-        uint32_t word = w[0];                    // select, not a dynamic index: w stays in registers
-#pragma unroll
-        for (int k = 1; k < 8; k++) word = (k == (p >> 2)) ? w[k] : word;
-        payload[off++] = (uint8_t)(word >> (8 * (p & 3)));
-        prev = p;
-    }
-    uint32_t total = (uint32_t)(len - 1 - prev) + c;
-    while (total >= kMaxRun) { payload[off++] = run_code(kMaxRun); total -= kMaxRun; }
-    c = total;
-}
-
 __device__ __forceinline__ unsigned long long shfl_up64(unsigned long long v, int d) {
     return __shfl_up_sync(0xffffffffu, v, d);
 }
@@ -444,6 +419,20 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
     return row_summary(r.mixbal != 0, lead, r.row_count, r.carry_out, row_len);
 }
 
+// A warp stores code 255 to payload[a, b): head and tail bytes singly, the
+// 16-byte-aligned middle with vector stores.  Callers __syncwarp() before
+// overwriting any of these bytes.
+__device__ __forceinline__ void warp_fill_full_chunks(uint8_t *payload, uint64_t a, uint64_t b) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(payload + a), hi = reinterpret_cast<uintptr_t>(payload + b);
+    const uintptr_t lo16 = tmin<uintptr_t>(hi, (lo + 15) & ~uintptr_t(15));
+    const uintptr_t hi16 = tmax<uintptr_t>(lo16, hi & ~uintptr_t(15));
+    if (lo + lane < lo16) *reinterpret_cast<uint8_t *>(lo + lane) = 0xff;
+    if (hi16 + lane < hi) *reinterpret_cast<uint8_t *>(hi16 + lane) = 0xff;
+    for (uintptr_t q = lo16 + 16 * lane; q < hi16; q += 16 * 32)
+        *reinterpret_cast<uint4 *>(q) = make_uint4(~0u, ~0u, ~0u, ~0u);
+}
+
 // ---------------------------------------------------------------- segment lookup
 template <int F>
 __device__ __forceinline__ uint64_t seg_first(const Seg &s) {
@@ -462,6 +451,30 @@ __device__ __forceinline__ int find_seg(const SegTable &T, uint64_t item) {
     return lo;
 }
 __device__ __forceinline__ Seg get_seg(const SegTable &T, int i) { return T.count == 1 ? T.one : T.d[i]; }
+
+// Per-CTA shared-memory copy of a kernel's first-item array (tables of up to
+// kSegCache segments): the per-item segment search then costs shared loads, not
+// a chain of dependent global loads.
+constexpr int kSegCache = 512;
+template <int F, int C = kSegCache>
+__device__ __forceinline__ void seg_index_load(const SegTable &T, uint64_t *sf) {
+    if (T.count > 1 && T.count <= C) {
+        for (int i = threadIdx.x; i < T.count; i += blockDim.x) sf[i] = T.first[F - 1][i];
+    }
+    __syncthreads();
+}
+template <int F, int C = kSegCache>
+__device__ __forceinline__ int find_seg_c(const SegTable &T, uint64_t item, const uint64_t *sf) {
+    if (T.count == 1) return 0;
+    if (T.count > C) return find_seg<F>(T, item);
+    int lo = 0, hi = T.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sf[mid] <= item) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
 
 // M and the compressor status of a segment from its max key (Eq. 1, R6)
 __device__ __forceinline__ unsigned int scale_from_key(unsigned int key, float s, float &M) {
@@ -578,10 +591,52 @@ __device__ __forceinline__ uint64_t block_excl_scan_sum(uint64_t x, unsigned lon
 
 constexpr unsigned long long kReady = 1ull << 62;
 
+constexpr unsigned long long kPrefix = 1ull << 63;   // the state holds the inclusive prefix
+constexpr unsigned long long kStateFlags = kReady | kPrefix;
+
 __device__ __forceinline__ unsigned long long wait_ready(const unsigned long long *p) {
     unsigned long long w;
-    while (!((w = ld_relaxed_u64(p)) & kReady)) __nanosleep(64);
+    while (!((w = ld_relaxed_u64(p)) & kStateFlags)) __nanosleep(64);
     return w;
+}
+
+// Monoids of the chunked scans, on packed 62-bit values (identity packs to 0).
+struct SumOp {
+    __device__ __forceinline__ static unsigned long long combine(unsigned long long a, unsigned long long b) {
+        return a + b;
+    }
+};
+struct RunOp {   // a then b
+    __device__ __forceinline__ static unsigned long long combine(unsigned long long a, unsigned long long b) {
+        return pack(compose(unpack(a), unpack(b)));
+    }
+};
+
+// Decoupled look-back by one full warp: the composition of chunk states
+// st[0..lc), each published as kReady|aggregate or kPrefix|inclusive prefix.
+// The warp reads 32 predecessors at a time (newest in lane 0), stops at the
+// newest inclusive prefix and reduces the window in order.
+template <class Op>
+__device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long *st, uint64_t lc) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long excl = 0;
+    int64_t j = (int64_t)lc - 1;
+    while (j >= 0) {
+        const int64_t idx = j - lane;
+        const unsigned long long w = idx >= 0 ? wait_ready(st + idx) : kPrefix;
+        const uint32_t pre = __ballot_sync(0xffffffffu, (w & kPrefix) != 0);
+        const int first = pre ? __ffs(pre) - 1 : 31;          // newest prefix in the window
+        unsigned long long v = lane <= first ? (w & ~kStateFlags) : 0ull;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {                    // lane L + d is older than lane L
+            const unsigned long long o = __shfl_down_sync(0xffffffffu, v, d);
+            if (lane + d < 32) v = Op::combine(o, v);
+        }
+        excl = Op::combine(__shfl_sync(0xffffffffu, v, 0), excl);
+        if (pre) break;
+        j -= 32;
+    }
+    return excl;
 }
 
 }  // namespace tlc

@@ -108,6 +108,7 @@ struct SegTable {
     int count;
     uint64_t n1, n2, n3, n4, n5;    // total items per kernel
     ItemSizes sz;
+    const uint64_t *first[5];       // device: first item of every segment, per kernel (count > 1)
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -135,6 +136,7 @@ struct Table {
     int count = 0;
     std::vector<Seg> host;
     Seg *d = nullptr;
+    uint64_t *d_first = nullptr;    // 5 x count first-item arrays
     SegTable T{};
     void *ws = nullptr;
     size_t ws_bytes = 0;

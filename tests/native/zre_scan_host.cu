@@ -1,12 +1,12 @@
 // Host-only harness (no GPU): drives the device-side ZRE building blocks of
 // paper_1802_07389_b200/csrc/tlc_device.cuh (literal_mask, mask_summary,
-// mask_emit, lane_carry_in, row_carry_out, row_summary, compose, run_eval --
+// lane_carry_in, row_carry_out, row_summary, compose, run_eval --
 // all __host__ __device__) through the same decomposition as the K3 kernel
 // (compress.cu): `nchunks` contiguous chunks, each split into `warps`
 // sub-chunks scanned in warp rows of 32 lanes x 32 bytes (ballots and shuffles
 // emulated serially); phase 1 composes row summaries, phase 2 composes the
-// preceding chunk summaries from per-thread partials, phase 3 tracks
-// (offset, carry) across rows and emits at the final offsets.
+// preceding chunk summaries, phase 3 tracks (offset, carry) across rows and
+// emits each row from its literal list at the final offsets.
 // tests/test_zre_scan_host.py compares the output with the oracle's ZRE.
 #include <algorithm>
 #include <cstdint>
@@ -67,6 +67,48 @@ void warp_row_host(Row &r, uint32_t c_row) {
     r.carry_out = row_carry_out(r.any, lastpos[r.any ? msb32(mixbal) : 0], c_row, r.row_len);
     const uint32_t k0 = r.any ? ctz32(mixbal) : 0u;
     r.lead = (r.mask[k0] ? ctz32(r.mask[k0]) : 0u) + 32u * k0;
+}
+
+// K3 phase 3 for one warp row (serial form of the device code): a row without
+// literals emits (carry + row_len)/14 full chunks; otherwise the row's literal
+// list is walked, literal k preceded by R 121s emitting R/14 codes 255 (the
+// prefilled range), a flush code if R%14 > 0 and the literal.
+void emit_row_list(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint8_t *out, uint64_t &off) {
+    std::vector<uint32_t> lit;
+    uint8_t bytes[LANES * SEG];
+    for (int l = 0; l < LANES; l++)
+        for (int m = 0; m < SEG; m++) {
+            bytes[SEG * l + m] = (uint8_t)byte_at(r.w[l], m);
+            if ((r.mask[l] >> m) & 1u) lit.push_back(SEG * l + m);
+        }
+    if (lit.empty()) {
+        const uint32_t x = carry + r.row_len, cnt = x / kMaxRun;
+        for (uint32_t k = 0; k < cnt; k++) out[off + k] = 0xff;
+        carry = x - cnt * kMaxRun;
+        off += cnt;
+        if (carry > 0 && row + r.row_len == P) out[off] = run_code(carry);
+        return;
+    }
+    const uint32_t L = (uint32_t)lit.size(), Rt = r.row_len - 1u - lit[L - 1];
+    uint32_t total = 0;
+    std::vector<uint32_t> R(L), cost(L);
+    for (uint32_t k = 0; k < L; k++) {
+        R[k] = lit[k] - (k ? lit[k - 1] + 1u : 0u) + (k ? 0u : carry);
+        cost[k] = R[k] / kMaxRun + (R[k] % kMaxRun != 0) + 1u;
+        total += cost[k];
+    }
+    const uint32_t row_count = total + Rt / kMaxRun;
+    for (uint32_t k = 0; k < row_count; k++) out[off + k] = 0xff;
+    uint64_t ex = 0;
+    for (uint32_t k = 0; k < L; k++) {
+        uint64_t o = off + ex + R[k] / kMaxRun;
+        if (R[k] % kMaxRun) out[o++] = run_code(R[k] % kMaxRun);
+        out[o] = bytes[lit[k]];
+        ex += cost[k];
+    }
+    off += row_count;
+    carry = Rt % kMaxRun;
+    if (carry > 0 && row + r.row_len == P) out[off] = run_code(carry);
 }
 
 void load_row(const uint8_t *B, uint64_t row, uint64_t whi, Row &r) {
@@ -133,18 +175,7 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
                 load_row(B, row, whi, r);
                 warp_row_host(r, carry);
-                uint32_t ex = 0;
-                for (int l = 0; l < LANES; l++) {
-                    if (r.len[l] > 0) {
-                        uint64_t o = off + ex;
-                        uint32_t c = r.carry_in[l];
-                        mask_emit(r.w[l], r.mask[l], r.len[l], c, out, o);
-                        if (c > 0 && row + (uint64_t)SEG * l + r.len[l] == P) out[o++] = run_code(c);
-                    }
-                    ex += r.count[l];
-                }
-                off += r.row_count;
-                carry = r.carry_out;
+                emit_row_list(r, row, P, carry, out, off);
             }
         }
     }
