@@ -467,22 +467,52 @@ def run_tlc(args):
     if not args.no_e2e:
         th = torch.empty(n, dtype=torch.float32, pin_memory=True)
         th.copy_(ts[0].cpu())
-        oh = torch.empty(n, dtype=torch.float32, pin_memory=True)
-        td = torch.empty_like(ts[0])
+        ohb = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        tdb = [torch.empty_like(ts[0]) for _ in range(2)]
+        outb = [out, torch.empty_like(out)]
         E = max(1, args.e2e_steps)
+        # Step k: H2D of its input (copy stream 1), compress + decompress (the
+        # codec stream), D2H of its output (copy stream 2).  Double buffers let
+        # step k+1's H2D and step k's D2H run concurrently (full-duplex PCIe)
+        # while every step still moves its whole input in and its output out.
+        h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        for b in range(2):
+            ev_done[b].record(stream)
+            ev_out[b].record(stream)
 
-        def e2e_step():
-            td.copy_(th, non_blocking=True)
-            T.tlc_compress(td, err, s, zre, payload, hdr, ws_c, stream)
-            T.tlc_decompress(payload, hdr, n, out, T.TLC_MODE_OVERWRITE, ws_d, stream)
-            oh.copy_(out, non_blocking=True)
+        def e2e_step(k):
+            b = k % 2
+            h2d.wait_event(ev_done[b])                 # tdb[b] no longer read by step k-2
+            with torch.cuda.stream(h2d):
+                tdb[b].copy_(th, non_blocking=True)
+            ev_in[b].record(h2d)
+            stream.wait_event(ev_in[b])
+            stream.wait_event(ev_out[b])               # outb[b] drained by step k-2's D2H
+            T.tlc_compress(tdb[b], err, s, zre, payload, hdr, ws_c, stream)
+            T.tlc_decompress(payload, hdr, n, outb[b], T.TLC_MODE_OVERWRITE, ws_d, stream)
+            ev_done[b].record(stream)
+            d2h.wait_event(ev_done[b])
+            with torch.cuda.stream(d2h):
+                ohb[b].copy_(outb[b], non_blocking=True)
+            ev_out[b].record(d2h)
 
-        e2e_step()
+        for k in range(2):
+            e2e_step(k)
+        stream.wait_event(ev_out[0])
+        stream.wait_event(ev_out[1])
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for _ in range(E):
-            e2e_step()
+        for b in range(2):                             # the timed steps start after f0
+            ev_done[b].record(stream)
+            ev_out[b].record(stream)
+        for k in range(E):
+            e2e_step(k)
+        stream.wait_event(ev_out[0])
+        stream.wait_event(ev_out[1])
         f1.record(stream)
         barrier()
         ems = f0.elapsed_time(f1)
@@ -493,7 +523,8 @@ def run_tlc(args):
         e2e = {"value": world * 4.0 * n * E / (ems / 1e3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "steps": E,
                "ms_per_step": ems / E,
-               "what": "pinned host t -> HBM, tlc_compress, tlc_decompress, HBM -> pinned host out"}
+               "what": "per step: pinned host t -> HBM, tlc_compress, tlc_decompress, HBM -> pinned host out; "
+                       "H2D, codec and D2H on three streams, double-buffered across steps"}
 
     xw1 = None
     if world == 1 and not args.no_xchg_w1:

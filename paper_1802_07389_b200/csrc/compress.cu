@@ -384,6 +384,36 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
     return x == 0;
 }
 
+struct K3Smem {
+    uint8_t chunk[kLargeItems.c3];                      // the chunk's quartic bytes
+    uint16_t lit[kScanWarps][kK3WarpRow];                // literal positions of a warp row
+    unsigned long long bar;
+};
+
+// Load chunk bytes [rel, min(rel+32, rhi)) from shared memory as 8 words,
+// padding with 121 (0x79); rel is a multiple of 32.
+__device__ __forceinline__ int load_seg_s(const uint8_t *c, uint32_t rel, uint32_t rhi, uint32_t (&w)[8]) {
+    const int len = rel < rhi ? (int)tmin<uint32_t>(kK3Seg, rhi - rel) : 0;
+    if (len == kK3Seg) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(c + rel);
+        const uint4 b = *reinterpret_cast<const uint4 *>(c + rel + 16);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int m = 4 * k + q;
+                x |= (uint32_t)(m < len ? c[rel + m] : kZeroGroup) << (8 * q);
+            }
+            w[k] = x;
+        }
+    }
+    return len;
+}
+
 // Load [pos, min(pos+32, hi)) as 8 words, padding with 121 (0x79).
 __device__ __forceinline__ int load_seg(const uint8_t *bytes, uint64_t pos, uint64_t hi,
                                         uint32_t (&w)[8]) {
@@ -414,12 +444,17 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
     __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wagg[kScanWarps];
     __shared__ unsigned long long s_id;
-    __shared__ uint16_t s_lit[kScanWarps][kK3WarpRow];              // literal positions of a warp row
-    __shared__ __align__(16) uint8_t s_rowb[kScanWarps][kK3WarpRow]; // the row's bytes
+    extern __shared__ __align__(128) uint8_t k3_smem_raw[];
+    K3Smem &sm = *reinterpret_cast<K3Smem *>(k3_smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t w[8];
     __shared__ uint64_t s_first[kSegCache];
-    seg_index_load<3>(T, s_first);
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    seg_index_load<3>(T, s_first);                       // (ends with __syncthreads)
+    uint32_t parity = 0;
     pdl_wait();                                          // K2's quartic bytes and headers
     while (true) {
         if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k3_counter, 1ull);
@@ -436,11 +471,22 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         const uint64_t lo = lc * T.sz.c3, hi = tmin<uint64_t>(P, lo + T.sz.c3);
         const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
         const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
+        const uint32_t rwhi = (uint32_t)(whi - lo);
+
+        // the chunk's bytes to shared memory with one bulk copy (16-byte multiple:
+        // a segment's scratch is padded to 16 bytes; the loaders pad past whi)
+        if (threadIdx.x == 0) {
+            const uint32_t nb = (uint32_t)((hi - lo + 15) & ~uint64_t(15));
+            mbar_expect_tx(&sm.bar, nb);
+            bulk_load(sm.chunk, bytes + lo, nb, &sm.bar);
+        }
+        mbar_wait(&sm.bar, parity);
+        parity ^= 1u;
 
         // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row), then of the chunk
         RunSum wagg = run_identity();
         for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
-            const int len = load_seg(bytes, row + (uint64_t)kK3Seg * lane, whi, w);
+            const int len = load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
             if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal in the row: one ALL run
                 wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
@@ -458,7 +504,11 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
 
         // ---- phase 2: carry-in = composition of the segment's preceding chunks (look-back)
         if (warp == 0) {
+#ifdef TLC_EXP_NO_LOOKBACK                               // timing experiment only: wrong output
+            const unsigned long long ex = 0;
+#else
             const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
+#endif
             if (lane == 0) {
                 if (lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, pack(agg)));
                 s_warp[0] = ex;
@@ -479,9 +529,11 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         uint64_t off;
         uint32_t carry;
         run_eval(before, 0, off, carry);              // payload offset and carry at the sub-range start
+#ifdef TLC_EXP_NO_PHASE3                                 // timing experiment only: wrong output
+        if (wlo < whi) continue;
+#endif
         for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
-            const uint64_t pos = row + (uint64_t)kK3Seg * lane;
-            const int len = load_seg(bytes, pos, whi, w);
+            load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
             if (__all_sync(0xffffffffu, plain_lane(w))) {
                 // no literal in the row: the pending run grows by row_len and a
@@ -505,10 +557,8 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
             }
             const uint32_t L = __shfl_sync(0xffffffffu, b, 31);
             b -= nl;
-            uint16_t *lit = s_lit[warp];
-            uint4 *rb = reinterpret_cast<uint4 *>(s_rowb[warp] + kK3Seg * lane);
-            rb[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            rb[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            uint16_t *lit = sm.lit[warp];
+            const uint8_t *rowb = sm.chunk + (row - lo);
             for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = (uint16_t)(kK3Seg * lane + ctz32(m));
             __syncwarp();
             // literal k (one per lane and round) is preceded by R 121s: R/14 full chunks
@@ -548,14 +598,14 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 if (k < L) {
                     uint64_t o = off + base + (x - cost) + R / kMaxRun;
                     if (R % kMaxRun) S.payload[o++] = run_code(R % kMaxRun);
-                    S.payload[o] = s_rowb[warp][p];
+                    S.payload[o] = rowb[p];
                 }
                 base += round_total;
             }
             off += base + Rt / kMaxRun;
             carry = Rt % kMaxRun;
             if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
-            __syncwarp();                                            // s_lit / s_rowb reused
+            __syncwarp();                                            // sm.lit reused
         }
     }
 }
@@ -623,10 +673,12 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
     }
     if (use_zre) {
         KernelScope ks(kK3, st);
-        if (!g_k3_blocks)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, 0);
+        if (!g_k3_blocks) {
+            cudaFuncSetAttribute(tlc_zre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K3Smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, sizeof(K3Smem));
+        }
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
-        launch_pdl(tlc_zre_kernel, grid, kK3Threads, 0, st, T, maxkey, s, scratch, ctrl, states);
+        launch_pdl(tlc_zre_kernel, grid, kK3Threads, sizeof(K3Smem), st, T, maxkey, s, scratch, ctrl, states);
     }
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
