@@ -384,11 +384,58 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
     return x == 0;
 }
 
+constexpr int kK3RowsPerWarp = (int)(kLargeItems.c3 / kScanWarps / kK3WarpRow);   // rows of a sub-range
+constexpr int kK3LitCap = 1024;            // literal-list entries a warp keeps between phases 1 and 3
+constexpr uint32_t kRowNotKept = 1u << 31;
+
 struct K3Smem {
     uint8_t chunk[kLargeItems.c3];                      // the chunk's quartic bytes
-    uint16_t lit[kScanWarps][kK3WarpRow];                // literal positions of a warp row
+    uint16_t lit[kScanWarps][kK3LitCap];                 // literal positions (row-relative), row after row
+    uint32_t rowmeta[kScanWarps][kK3RowsPerWarp];        // per row: L | base << 16, or kRowNotKept | L
     unsigned long long bar;
 };
+
+// Literal list of a warp row held as 32 bytes per lane: the row positions of
+// its bytes != 121 in ascending order, written to lit[0..L) if `store`
+// (load_seg_s pads with 121, so positions past the end of the data are clear).
+// Returns L in all lanes.
+__device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint16_t *lit, uint32_t cap,
+                                                 bool &stored) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t mask = literal_mask(w);
+    const uint32_t nl = popc32(mask);
+    uint32_t b = nl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, b, d);
+        if (lane >= d) b += y;
+    }
+    const uint32_t L = __shfl_sync(0xffffffffu, b, 31);
+    stored = L <= cap;
+    if (stored) {
+        b -= nl;
+        for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = (uint16_t)(kK3Seg * lane + ctz32(m));
+    }
+    __syncwarp();
+    return L;
+}
+
+// ZRE bytes of a literal preceded by R zero groups: R/14 full
+// chunks, one flush code if R % 14 > 0, the literal itself.
+__device__ __forceinline__ uint32_t lit_cost(uint32_t R) { return R / kMaxRun + (R % kMaxRun != 0) + 1u; }
+
+// Code 255 (a full chunk of 14 zero groups) to payload[a, b) by the whole CTA:
+// single bytes at the ends, 16-byte stores in between.
+__device__ __forceinline__ void cta_fill_full_chunks(uint8_t *payload, uint64_t a, uint64_t b) {
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(payload + a), hi = reinterpret_cast<uintptr_t>(payload + b);
+    const uintptr_t lo16 = tmin<uintptr_t>(hi, (lo + 15) & ~uintptr_t(15));
+    const uintptr_t hi16 = tmax<uintptr_t>(lo16, hi & ~uintptr_t(15));
+    const uint32_t t = threadIdx.x;
+    if (t < 16 && lo + t < lo16) *reinterpret_cast<uint8_t *>(lo + t) = 0xff;
+    if (t >= 16 && t < 32 && hi16 + (t - 16) < hi) *reinterpret_cast<uint8_t *>(hi16 + (t - 16)) = 0xff;
+    for (uintptr_t q = lo16 + 16 * (uintptr_t)t; q < hi16; q += 16 * (uintptr_t)blockDim.x)
+        *reinterpret_cast<uint4 *>(q) = make_uint4(~0u, ~0u, ~0u, ~0u);
+}
 
 // Load chunk bytes [rel, min(rel+32, rhi)) from shared memory as 8 words,
 // padding with 121 (0x79); rel is a multiple of 32.
@@ -483,17 +530,42 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         mbar_wait(&sm.bar, parity);
         parity ^= 1u;
 
-        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row), then of the chunk
+        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row), then of the chunk.
+        // A row's literal list is kept for phase 3 while the warp's list space lasts.
         RunSum wagg = run_identity();
-        for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
+        uint16_t *lit = sm.lit[warp];
+        uint32_t used = 0;
+        bool keep = true;
+        int r = 0;
+        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
             const int len = load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
             if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal in the row: one ALL run
                 wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
+                if (lane == 0) sm.rowmeta[warp][r] = 0u;
                 continue;
             }
-            const uint32_t mask = literal_mask(w);
-            wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
+            bool stored = false;
+            const uint32_t L = row_literals(w, lit + used, keep ? kK3LitCap - used : 0u, stored);
+            if (!stored) {                                        // list space exhausted: mask form
+                keep = false;
+                const uint32_t mask = literal_mask(w);
+                wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
+                if (lane == 0) sm.rowmeta[warp][r] = kRowNotKept | L;
+                continue;
+            }
+            // count with carry 0: the first literal costs 1 + lead/14 (its flush code
+            // depends on the carry: RunSum r0), literal k > 0 lit_cost(R_k)
+            const uint16_t *rl = lit + used;
+            uint32_t part = 0;
+            for (uint32_t k = lane; k < L; k += 32)
+                part += k ? lit_cost((uint32_t)rl[k] - rl[k - 1] - 1u) : 1u + rl[0] / kMaxRun;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+            const uint32_t Rt = row_len - 1u - rl[L - 1];               // trailing zero groups
+            wagg = compose(wagg, RunSum{part + Rt / kMaxRun, (uint32_t)rl[0] % kMaxRun, Rt % kMaxRun, true});
+            if (lane == 0) sm.rowmeta[warp][r] = L | (used << 16);
+            used += L;
         }
         if (lane == 0) s_wagg[warp] = pack(wagg);
         __syncthreads();
@@ -504,11 +576,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
 
         // ---- phase 2: carry-in = composition of the segment's preceding chunks (look-back)
         if (warp == 0) {
-#ifdef TLC_EXP_NO_LOOKBACK                               // timing experiment only: wrong output
-            const unsigned long long ex = 0;
-#else
             const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
-#endif
             if (lane == 0) {
                 if (lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, pack(agg)));
                 s_warp[0] = ex;
@@ -516,72 +584,50 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         }
         __syncthreads();
         const RunSum chunk_in = unpack(s_warp[0]);
-        if (lc == nch - 1 && threadIdx.x == 0) {
-            uint64_t total;
-            uint32_t carry;
-            run_eval(compose(chunk_in, agg), 0, total, carry);
-            S.hdr->payload_len = total + (carry > 0);   // the end of the stream flushes
-        }
+        uint64_t o_begin, o_end;
+        uint32_t c_tmp;
+        run_eval(chunk_in, 0, o_begin, c_tmp);
+        run_eval(compose(chunk_in, agg), 0, o_end, c_tmp);
+        if (lc == nch - 1 && threadIdx.x == 0) S.hdr->payload_len = o_end + (c_tmp > 0);   // the end flushes
 
-        // ---- phase 3: emission at the final payload offsets
+        // ---- phase 3: every byte of the chunk's output that is not a flush code or a
+        // literal is a full chunk (255): fill the range, then store the sparse rest
+        cta_fill_full_chunks(S.payload, o_begin, o_end);
+        __syncthreads();
         RunSum before = chunk_in;
         for (int k = 0; k < warp; k++) before = compose(before, unpack(s_wagg[k]));
         uint64_t off;
         uint32_t carry;
         run_eval(before, 0, off, carry);              // payload offset and carry at the sub-range start
-#ifdef TLC_EXP_NO_PHASE3                                 // timing experiment only: wrong output
-        if (wlo < whi) continue;
-#endif
-        for (uint64_t row = wlo; row < whi; row += kK3WarpRow) {
-            load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
+        r = 0;
+        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-            if (__all_sync(0xffffffffu, plain_lane(w))) {
-                // no literal in the row: the pending run grows by row_len and a
-                // full chunk (code 255) is emitted every 14 zero groups
-                const uint32_t x = carry + row_len, cnt = x / kMaxRun;
-                warp_fill_full_chunks(S.payload, off, off + cnt);
-                carry = x - cnt * kMaxRun;
-                off += cnt;
+            const uint32_t meta = sm.rowmeta[warp][r];
+            uint32_t L = meta & 0xffffu;
+            if (L == 0) {                             // no literal: the run grows by row_len
+                const uint32_t x = carry + row_len;
+                off += x / kMaxRun;
+                carry = x % kMaxRun;
                 if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
                 continue;
             }
-            // literal list of the row (positions in row order) and its bytes, in shared memory;
-            // load_seg pads with 121, so bits past the end of the stream are clear
-            const uint32_t mask = literal_mask(w);
-            const uint32_t nl = popc32(mask);
-            uint32_t b = nl;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, b, d);
-                if (lane >= d) b += y;
+            const uint16_t *rl = lit + (meta >> 16);
+            if (meta & kRowNotKept) {                 // rebuild the list (kept rows are consumed)
+                load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
+                bool stored;
+                L = row_literals(w, lit, kK3WarpRow, stored);
+                rl = lit;
             }
-            const uint32_t L = __shfl_sync(0xffffffffu, b, 31);
-            b -= nl;
-            uint16_t *lit = sm.lit[warp];
             const uint8_t *rowb = sm.chunk + (row - lo);
-            for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = (uint16_t)(kK3Seg * lane + ctz32(m));
-            __syncwarp();
-            // literal k (one per lane and round) is preceded by R 121s: R/14 full chunks
-            // (code 255), one flush code if R%14 > 0, then the literal itself
-            const uint32_t c_row = carry;
-            const uint32_t Rt = row_len - 1u - lit[L - 1];           // trailing 121s of the row
-            uint32_t rsum = 0;
-            if (L > 32) {                                            // dense row: count first
-                for (uint32_t k = lane; k < L; k += 32) {
-                    const uint32_t R = lit[k] - (k ? lit[k - 1] + 1u : 0u) + (k ? 0u : c_row);
-                    rsum += R / kMaxRun + (R % kMaxRun != 0) + 1u;
-                }
-#pragma unroll
-                for (int d = 16; d >= 1; d >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, d);
-            }
+            uint8_t *out = S.payload + off;
             uint32_t base = 0;
-            for (uint32_t k0 = 0; k0 < L; k0 += 32) {
+            for (uint32_t k0 = 0; k0 < L; k0 += 32) {             // literal k0 + lane
                 const uint32_t k = k0 + lane;
                 uint32_t R = 0, cost = 0, p = 0;
                 if (k < L) {
-                    p = lit[k];
-                    R = p - (k ? lit[k - 1] + 1u : 0u) + (k ? 0u : c_row);
-                    cost = R / kMaxRun + (R % kMaxRun != 0) + 1u;
+                    p = rl[k];
+                    R = k ? p - rl[k - 1] - 1u : p + carry;
+                    cost = lit_cost(R);
                 }
                 uint32_t x = cost;
 #pragma unroll
@@ -589,23 +635,18 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                     if (lane >= d) x += y;
                 }
-                const uint32_t round_total = __shfl_sync(0xffffffffu, x, 31);
-                if (k0 == 0) {                                       // 255s before any literal store
-                    const uint32_t row_count = (L > 32 ? rsum : round_total) + Rt / kMaxRun;
-                    warp_fill_full_chunks(S.payload, off, off + row_count);
-                    __syncwarp();
-                }
                 if (k < L) {
-                    uint64_t o = off + base + (x - cost) + R / kMaxRun;
-                    if (R % kMaxRun) S.payload[o++] = run_code(R % kMaxRun);
-                    S.payload[o] = rowb[p];
+                    uint32_t o = base + (x - cost) + R / kMaxRun;
+                    if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
+                    out[o] = rowb[p];
                 }
-                base += round_total;
+                base += __shfl_sync(0xffffffffu, x, 31);
             }
+            const uint32_t Rt = row_len - 1u - rl[L - 1];
             off += base + Rt / kMaxRun;
             carry = Rt % kMaxRun;
             if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
-            __syncwarp();                                            // sm.lit reused
+            __syncwarp();                             // a rebuilt list is overwritten by the next one
         }
     }
 }

@@ -614,27 +614,49 @@ struct RunOp {   // a then b
 
 // Decoupled look-back by one full warp: the composition of chunk states
 // st[0..lc), each published as kReady|aggregate or kPrefix|inclusive prefix.
-// The warp reads 32 predecessors at a time (newest in lane 0), stops at the
-// newest inclusive prefix and reduces the window in order.
+// Each round reads the 4*32 newest unread predecessors (lane l holds four
+// consecutive ones, lane 0 the newest), stops at the newest inclusive prefix
+// and reduces the window in order.
 template <class Op>
 __device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long *st, uint64_t lc) {
+    constexpr int V = 4;
     const int lane = threadIdx.x & 31;
     unsigned long long excl = 0;
     int64_t j = (int64_t)lc - 1;
     while (j >= 0) {
-        const int64_t idx = j - lane;
-        const unsigned long long w = idx >= 0 ? wait_ready(st + idx) : kPrefix;
-        const uint32_t pre = __ballot_sync(0xffffffffu, (w & kPrefix) != 0);
-        const int first = pre ? __ffs(pre) - 1 : 31;          // newest prefix in the window
-        unsigned long long v = lane <= first ? (w & ~kStateFlags) : 0ull;
+        unsigned long long w[V];                            // w[0] newest
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {                    // lane L + d is older than lane L
+        for (int k = 0; k < V; k++) {
+            const int64_t idx = j - (int64_t)(V * lane + k);
+            w[k] = idx >= 0 ? ld_relaxed_u64(st + idx) : kPrefix;
+        }
+#pragma unroll
+        for (int k = 0; k < V; k++)
+            while (!(w[k] & kStateFlags)) {
+                __nanosleep(64);
+                w[k] = ld_relaxed_u64(st + (j - (int64_t)(V * lane + k)));
+            }
+        int kp = V;                                         // newest prefix in this lane
+#pragma unroll
+        for (int k = V - 1; k >= 0; k--)
+            if (w[k] & kPrefix) kp = k;
+        const uint32_t pre = __ballot_sync(0xffffffffu, kp < V);
+        const int first = pre ? __ffs(pre) - 1 : 31;       // lane of the newest prefix
+        unsigned long long v = 0;                            // this lane's part, oldest first
+        if (lane <= first) {
+            const int kmax = lane == first && pre ? kp : V - 1;
+#pragma unroll
+            for (int k = V - 1; k >= 0; k--)
+                if (k <= kmax) v = Op::combine(v, w[k] & ~kStateFlags);
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {                 // lane L + d is older than lane L
             const unsigned long long o = __shfl_down_sync(0xffffffffu, v, d);
             if (lane + d < 32) v = Op::combine(o, v);
         }
         excl = Op::combine(__shfl_sync(0xffffffffu, v, 0), excl);
         if (pre) break;
-        j -= 32;
+        j -= 32 * V;
     }
     return excl;
 }
