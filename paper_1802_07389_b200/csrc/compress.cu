@@ -385,21 +385,25 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
 }
 
 constexpr int kK3RowsPerWarp = (int)(kLargeItems.c3 / kScanWarps / kK3WarpRow);   // rows of a sub-range
-constexpr int kK3LitCap = 1024;            // literal-list entries a warp keeps between phases 1 and 3
+constexpr int kK3LitCap = 512;             // list entries a warp keeps between phases 1 and 3
 constexpr uint32_t kRowNotKept = 1u << 31;
 
+// A kept list entry of literal k > 0 of a row: its position p (bits 0-11), the
+// flush code remainder R_k % 14 (bits 12-15) and its output offset relative to
+// the end of literal 0's bytes (bits 16-31); literal 0's entry holds p only,
+// its bytes depend on the carry entering the row.
 struct K3Smem {
     uint8_t chunk[kLargeItems.c3];                      // the chunk's quartic bytes
-    uint16_t lit[kScanWarps][kK3LitCap];                 // literal positions (row-relative), row after row
-    uint32_t rowmeta[kScanWarps][kK3RowsPerWarp];        // per row: L | base << 16, or kRowNotKept | L
+    uint32_t lit[kScanWarps][kK3LitCap];                 // literal lists, row after row
+    uint2 rowmeta[kScanWarps][kK3RowsPerWarp];           // per row: (L | base << 16, rest | cout << 16)
     unsigned long long bar;
 };
 
 // Literal list of a warp row held as 32 bytes per lane: the row positions of
-// its bytes != 121 in ascending order, written to lit[0..L) if `store`
+// its bytes != 121 in ascending order, written to lit[0..L) if L <= cap
 // (load_seg_s pads with 121, so positions past the end of the data are clear).
 // Returns L in all lanes.
-__device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint16_t *lit, uint32_t cap,
+__device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint32_t *lit, uint32_t cap,
                                                  bool &stored) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t mask = literal_mask(w);
@@ -414,7 +418,7 @@ __device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint16_
     stored = L <= cap;
     if (stored) {
         b -= nl;
-        for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = (uint16_t)(kK3Seg * lane + ctz32(m));
+        for (uint32_t m = mask; m; m &= m - 1u) lit[b++] = kK3Seg * lane + ctz32(m);
     }
     __syncwarp();
     return L;
@@ -461,35 +465,12 @@ __device__ __forceinline__ int load_seg_s(const uint8_t *c, uint32_t rel, uint32
     return len;
 }
 
-// Load [pos, min(pos+32, hi)) as 8 words, padding with 121 (0x79).
-__device__ __forceinline__ int load_seg(const uint8_t *bytes, uint64_t pos, uint64_t hi,
-                                        uint32_t (&w)[8]) {
-    const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
-    if (len == kK3Seg && (reinterpret_cast<uintptr_t>(bytes + pos) & 15u) == 0) {
-        const uint4 a = *reinterpret_cast<const uint4 *>(bytes + pos);
-        const uint4 b = *reinterpret_cast<const uint4 *>(bytes + pos + 16);
-        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-    } else {
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            uint32_t x = 0;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const int m = 4 * k + c;
-                x |= (uint32_t)(m < len ? bytes[pos + m] : kZeroGroup) << (8 * c);
-            }
-            w[k] = x;
-        }
-    }
-    return len;
-}
-
 __global__ void __launch_bounds__(kK3Threads)
 tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                const uint8_t *scratch, Ctrl *ctrl, unsigned long long *states) {
-    __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wagg[kScanWarps];
+    __shared__ unsigned long long s_off[kScanWarps + 1];    // offset entering each warp's sub-range, end
+    __shared__ uint32_t s_carry[kScanWarps + 1];
     __shared__ unsigned long long s_id;
     extern __shared__ __align__(128) uint8_t k3_smem_raw[];
     K3Smem &sm = *reinterpret_cast<K3Smem *>(k3_smem_raw);
@@ -530,10 +511,11 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         mbar_wait(&sm.bar, parity);
         parity ^= 1u;
 
-        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row), then of the chunk.
-        // A row's literal list is kept for phase 3 while the warp's list space lasts.
+        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row).  Rows'
+        // literal lists, with each literal's output offset, are kept for phase 3 while
+        // the warp's list space lasts.
         RunSum wagg = run_identity();
-        uint16_t *lit = sm.lit[warp];
+        uint32_t *lit = sm.lit[warp];
         uint32_t used = 0;
         bool keep = true;
         int r = 0;
@@ -542,7 +524,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
             const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
             if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal in the row: one ALL run
                 wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
-                if (lane == 0) sm.rowmeta[warp][r] = 0u;
+                if (lane == 0) sm.rowmeta[warp][r] = make_uint2(0u, 0u);
                 continue;
             }
             bool stored = false;
@@ -551,82 +533,23 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 keep = false;
                 const uint32_t mask = literal_mask(w);
                 wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
-                if (lane == 0) sm.rowmeta[warp][r] = kRowNotKept | L;
+                if (lane == 0) sm.rowmeta[warp][r] = make_uint2(kRowNotKept | L, 0u);
                 continue;
             }
-            // count with carry 0: the first literal costs 1 + lead/14 (its flush code
-            // depends on the carry: RunSum r0), literal k > 0 lit_cost(R_k)
-            const uint16_t *rl = lit + used;
-            uint32_t part = 0;
-            for (uint32_t k = lane; k < L; k += 32)
-                part += k ? lit_cost((uint32_t)rl[k] - rl[k - 1] - 1u) : 1u + rl[0] / kMaxRun;
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
-            const uint32_t Rt = row_len - 1u - rl[L - 1];               // trailing zero groups
-            wagg = compose(wagg, RunSum{part + Rt / kMaxRun, (uint32_t)rl[0] % kMaxRun, Rt % kMaxRun, true});
-            if (lane == 0) sm.rowmeta[warp][r] = L | (used << 16);
-            used += L;
-        }
-        if (lane == 0) s_wagg[warp] = pack(wagg);
-        __syncthreads();
-        RunSum agg = run_identity();
-#pragma unroll
-        for (int k = 0; k < kScanWarps; k++) agg = compose(agg, unpack(s_wagg[k]));
-        if (threadIdx.x == 0) st_relaxed_u64(states + id, (lc == 0 ? kPrefix : kReady) | pack(agg));
-
-        // ---- phase 2: carry-in = composition of the segment's preceding chunks (look-back)
-        if (warp == 0) {
-            const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
-            if (lane == 0) {
-                if (lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, pack(agg)));
-                s_warp[0] = ex;
-            }
-        }
-        __syncthreads();
-        const RunSum chunk_in = unpack(s_warp[0]);
-        uint64_t o_begin, o_end;
-        uint32_t c_tmp;
-        run_eval(chunk_in, 0, o_begin, c_tmp);
-        run_eval(compose(chunk_in, agg), 0, o_end, c_tmp);
-        if (lc == nch - 1 && threadIdx.x == 0) S.hdr->payload_len = o_end + (c_tmp > 0);   // the end flushes
-
-        // ---- phase 3: every byte of the chunk's output that is not a flush code or a
-        // literal is a full chunk (255): fill the range, then store the sparse rest
-        cta_fill_full_chunks(S.payload, o_begin, o_end);
-        __syncthreads();
-        RunSum before = chunk_in;
-        for (int k = 0; k < warp; k++) before = compose(before, unpack(s_wagg[k]));
-        uint64_t off;
-        uint32_t carry;
-        run_eval(before, 0, off, carry);              // payload offset and carry at the sub-range start
-        r = 0;
-        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
-            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-            const uint32_t meta = sm.rowmeta[warp][r];
-            uint32_t L = meta & 0xffffu;
-            if (L == 0) {                             // no literal: the run grows by row_len
-                const uint32_t x = carry + row_len;
-                off += x / kMaxRun;
-                carry = x % kMaxRun;
-                if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
-                continue;
-            }
-            const uint16_t *rl = lit + (meta >> 16);
-            if (meta & kRowNotKept) {                 // rebuild the list (kept rows are consumed)
-                load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
-                bool stored;
-                L = row_literals(w, lit, kK3WarpRow, stored);
-                rl = lit;
-            }
-            const uint8_t *rowb = sm.chunk + (row - lo);
-            uint8_t *out = S.payload + off;
-            uint32_t base = 0;
-            for (uint32_t k0 = 0; k0 < L; k0 += 32) {             // literal k0 + lane
+            // literal k > 0 is preceded by R_k = p_k - p_{k-1} - 1 zero groups and costs
+            // lit_cost(R_k) bytes; literal 0's cost depends on the row's carry
+            uint32_t *e = lit + used;
+            uint32_t run = 0, plast = 0, p0 = 0;
+            for (uint32_t k0 = 0; k0 < L; k0 += 32) {
                 const uint32_t k = k0 + lane;
-                uint32_t R = 0, cost = 0, p = 0;
-                if (k < L) {
-                    p = rl[k];
-                    R = k ? p - rl[k - 1] - 1u : p + carry;
+                const uint32_t p = k < L ? e[k] : 0u;
+                uint32_t pp = __shfl_up_sync(0xffffffffu, p, 1);
+                if (lane == 0) pp = plast;
+                plast = __shfl_sync(0xffffffffu, p, (int)tmin<uint32_t>(31u, L - 1u - k0));
+                if (k0 == 0) p0 = __shfl_sync(0xffffffffu, p, 0);
+                uint32_t R = 0, cost = 0;
+                if (k > 0 && k < L) {
+                    R = p - pp - 1u;
                     cost = lit_cost(R);
                 }
                 uint32_t x = cost;
@@ -635,18 +558,139 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                     if (lane >= d) x += y;
                 }
-                if (k < L) {
-                    uint32_t o = base + (x - cost) + R / kMaxRun;
-                    if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
-                    out[o] = rowb[p];
-                }
-                base += __shfl_sync(0xffffffffu, x, 31);
+                if (k > 0 && k < L) e[k] = p | ((R % kMaxRun) << 12) | ((run + x - cost + R / kMaxRun) << 16);
+                run += __shfl_sync(0xffffffffu, x, 31);
             }
-            const uint32_t Rt = row_len - 1u - rl[L - 1];
-            off += base + Rt / kMaxRun;
-            carry = Rt % kMaxRun;
+            const uint32_t Rt = row_len - 1u - plast;                 // trailing zero groups
+            const uint32_t rest = run + Rt / kMaxRun;                 // bytes after literal 0's
+            wagg = compose(wagg, RunSum{1u + p0 / kMaxRun + rest, p0 % kMaxRun, Rt % kMaxRun, true});
+            if (lane == 0) sm.rowmeta[warp][r] = make_uint2(L | (used << 16), rest | ((Rt % kMaxRun) << 16));
+            used += L;
+        }
+        if (lane == 0) s_wagg[warp] = pack(wagg);
+        __syncthreads();
+
+        // ---- phase 2 (warp 0): publish the chunk aggregate, look back for the carry-in,
+        // publish the inclusive prefix; offsets and carries entering every warp's sub-range
+        if (warp == 0) {
+            RunSum incl = run_identity();                           // lane l: warps 0..l
+#pragma unroll
+            for (int k = 0; k < kScanWarps; k++)
+                if (k <= lane) incl = compose(incl, unpack(s_wagg[k]));
+            const unsigned long long agg = __shfl_sync(0xffffffffu, pack(incl), kScanWarps - 1);
+            const unsigned long long prev = __shfl_up_sync(0xffffffffu, pack(incl), 1);
+            if (lane == 0) st_relaxed_u64(states + id, (lc == 0 ? kPrefix : kReady) | agg);
+            const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
+            if (lane == 0 && lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, agg));
+            RunSum bw = unpack(ex);
+            if (lane > 0 && lane < kScanWarps) bw = compose(bw, unpack(prev));
+            if (lane == kScanWarps) bw = compose(bw, unpack(agg));
+            uint64_t o;
+            uint32_t c;
+            run_eval(bw, 0, o, c);
+            if (lane <= kScanWarps) {
+                s_off[lane] = o;
+                s_carry[lane] = c;
+            }
+        }
+        __syncthreads();
+        const uint64_t o_begin = s_off[0], o_end = s_off[kScanWarps];
+        if (lc == nch - 1 && threadIdx.x == 0)
+            S.hdr->payload_len = o_end + (s_carry[kScanWarps] > 0);     // the end of the stream flushes
+
+        // ---- phase 3: every byte of the chunk's output that is not a flush code or a
+        // literal is a full chunk (255): fill the range, then store the sparse rest
+        cta_fill_full_chunks(S.payload, o_begin, o_end);
+        __syncthreads();
+        uint64_t off = s_off[warp];
+        uint32_t carry = s_carry[warp];
+        r = 0;
+        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
+            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
+            const uint2 meta = sm.rowmeta[warp][r];
+            const uint32_t L = meta.x & 0xffffu;
+            const uint8_t *rowb = sm.chunk + (row - lo);
+            uint8_t *out = S.payload + off;
+            if (L == 0) {                             // no literal: the run grows by row_len
+                const uint32_t x = carry + row_len;
+                off += x / kMaxRun;
+                carry = x % kMaxRun;
+            } else if (!(meta.x & kRowNotKept)) {     // kept list: offsets known up to literal 0's cost
+                const uint32_t *e = lit + (meta.x >> 16);
+                const uint32_t R0 = (e[0] & 0xfffu) + carry;
+                const uint32_t cost0 = lit_cost(R0);
+                for (uint32_t k = lane; k < L; k += 32) {
+                    const uint32_t u = e[k];
+                    uint32_t o, rem;
+                    if (k == 0) {
+                        o = R0 / kMaxRun;
+                        rem = R0 % kMaxRun;
+                    } else {
+                        o = cost0 + (u >> 16);
+                        rem = (u >> 12) & 0xfu;
+                    }
+                    if (rem) out[o++] = run_code(rem);
+                    out[o] = rowb[u & 0xfffu];
+                }
+                off += cost0 + (meta.y & 0xffffu);
+                carry = meta.y >> 16;
+            } else {                                  // rebuild the list (kept rows are consumed)
+                const int len = load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
+                bool stored;
+                const uint32_t L2 = row_literals(w, lit, kK3LitCap, stored);
+                if (!stored) {                        // denser than the list space: per-lane emission
+                    const uint32_t mask = literal_mask(w);
+                    const WarpRow wr = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
+                    uint32_t x = wr.count;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    uint32_t o = x - wr.count, c = wr.carry_in;
+                    int prev = -1;
+                    for (uint32_t m = mask; m; m &= m - 1u) {
+                        const int q = (int)ctz32(m);
+                        const uint32_t R = (uint32_t)(q - prev - 1) + c;
+                        c = 0;
+                        o += R / kMaxRun;
+                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
+                        out[o++] = rowb[kK3Seg * lane + q];
+                        prev = q;
+                    }
+                    off += wr.row_count;
+                    carry = wr.carry_out;
+                    if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
+                    continue;
+                }
+                uint32_t base = 0;
+                for (uint32_t k0 = 0; k0 < L2; k0 += 32) {         // literal k0 + lane
+                    const uint32_t k = k0 + lane;
+                    uint32_t R = 0, cost = 0, p = 0;
+                    if (k < L2) {
+                        p = lit[k];
+                        R = k ? p - lit[k - 1] - 1u : p + carry;
+                        cost = lit_cost(R);
+                    }
+                    uint32_t x = cost;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    if (k < L2) {
+                        uint32_t o = base + (x - cost) + R / kMaxRun;
+                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
+                        out[o] = rowb[p];
+                    }
+                    base += __shfl_sync(0xffffffffu, x, 31);
+                }
+                const uint32_t Rt = row_len - 1u - lit[L2 - 1];
+                off += base + Rt / kMaxRun;
+                carry = Rt % kMaxRun;
+                __syncwarp();                         // the list is overwritten by the next rebuild
+            }
             if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
-            __syncwarp();                             // a rebuilt list is overwritten by the next one
         }
     }
 }
