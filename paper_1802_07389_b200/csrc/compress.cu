@@ -372,7 +372,23 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
 //            earlier, never waiting on a later one: no deadlock) -> carry-in;
 //   phase 3  each warp re-reads its sub-range (L2-resident) and writes every ZRE
 //            byte at its final offset; the segment's last chunk writes the length.
-constexpr int kK3Threads = kScanThreads;
+#ifdef TLC_K3_TRACE
+// development instrumentation: %globaltimer at phase boundaries of every K3 chunk
+__device__ unsigned long long g_k3_trace[1 << 14][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define K3_TRACE(slot) \
+    do { if ((threadIdx.x & 31) == 0 && id < (1u << 14)) g_k3_trace[id][slot] = gtimer(); } while (0)
+#else
+#define K3_TRACE(slot) do {} while (0)
+#endif
+
+constexpr int kK3Workers = kScanWarps;                       // warps scanning the chunk
+constexpr int kK3LookWarp = kK3Workers;                      // + one warp for the look-back
+constexpr int kK3Threads = 32 * (kK3Workers + 1);
 constexpr int kK3Seg = 32;                                   // bytes per lane per row
 constexpr int kK3WarpRow = 32 * kK3Seg;                      // 1 KiB per warp row
 
@@ -385,17 +401,20 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
 }
 
 constexpr int kK3RowsPerWarp = (int)(kLargeItems.c3 / kScanWarps / kK3WarpRow);   // rows of a sub-range
-constexpr int kK3LitCap = 512;             // list entries a warp keeps between phases 1 and 3
+constexpr int kK3LitCap = 256;             // list entries a warp keeps per chunk between phases 1 and 3
 constexpr uint32_t kRowNotKept = 1u << 31;
 
-// A kept list entry of literal k > 0 of a row: its position p (bits 0-11), the
-// flush code remainder R_k % 14 (bits 12-15) and its output offset relative to
-// the end of literal 0's bytes (bits 16-31); literal 0's entry holds p only,
-// its bytes depend on the carry entering the row.
+// K3 is software-pipelined over the chunks a CTA takes: phase 1 of chunk j runs
+// while the look-back warp resolves the carry-in of the previous chunk i, whose
+// phase 3 then works from its kept literal lists alone (the chunk buffer already
+// holds j).  A kept entry of literal k of a row: the literal byte (bits 8-15)
+// and, for k > 0, the flush code remainder R_k % 14 (bits 0-3) and the output
+// offset relative to the end of literal 0's bytes (bits 16-31); literal 0's
+// position is in the row's metadata, its bytes depend on the row's carry.
 struct K3Smem {
-    uint8_t chunk[kLargeItems.c3];                      // the chunk's quartic bytes
-    uint32_t lit[kScanWarps][kK3LitCap];                 // literal lists, row after row
-    uint2 rowmeta[kScanWarps][kK3RowsPerWarp];           // per row: (L | base << 16, rest | cout << 16)
+    uint8_t chunk[kLargeItems.c3];                       // the chunk's quartic bytes
+    uint32_t lit[2][kScanWarps][kK3LitCap];               // literal lists, row after row
+    uint4 rowmeta[2][kScanWarps][kK3RowsPerWarp];         // (L | base << 16, rest | cout << 16, p0, -)
     unsigned long long bar;
 };
 
@@ -428,17 +447,20 @@ __device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint32_
 // chunks, one flush code if R % 14 > 0, the literal itself.
 __device__ __forceinline__ uint32_t lit_cost(uint32_t R) { return R / kMaxRun + (R % kMaxRun != 0) + 1u; }
 
-// Code 255 (a full chunk of 14 zero groups) to payload[a, b) by the whole CTA:
-// single bytes at the ends, 16-byte stores in between.
-__device__ __forceinline__ void cta_fill_full_chunks(uint8_t *payload, uint64_t a, uint64_t b) {
-    const uintptr_t lo = reinterpret_cast<uintptr_t>(payload + a), hi = reinterpret_cast<uintptr_t>(payload + b);
-    const uintptr_t lo16 = tmin<uintptr_t>(hi, (lo + 15) & ~uintptr_t(15));
-    const uintptr_t hi16 = tmax<uintptr_t>(lo16, hi & ~uintptr_t(15));
-    const uint32_t t = threadIdx.x;
-    if (t < 16 && lo + t < lo16) *reinterpret_cast<uint8_t *>(lo + t) = 0xff;
-    if (t >= 16 && t < 32 && hi16 + (t - 16) < hi) *reinterpret_cast<uint8_t *>(hi16 + (t - 16)) = 0xff;
-    for (uintptr_t q = lo16 + 16 * (uintptr_t)t; q < hi16; q += 16 * (uintptr_t)blockDim.x)
-        *reinterpret_cast<uint4 *>(q) = make_uint4(~0u, ~0u, ~0u, ~0u);
+// Load [pos, min(pos+32, hi)) from global memory as 8 words, padding with 121.
+__device__ __forceinline__ int load_seg_g(const uint8_t *bytes, uint64_t pos, uint64_t hi, uint32_t (&w)[8]) {
+    const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int m = 4 * k + q;
+            x |= (uint32_t)(m < len ? bytes[pos + m] : kZeroGroup) << (8 * q);
+        }
+        w[k] = x;
+    }
+    return len;
 }
 
 // Load chunk bytes [rel, min(rel+32, rhi)) from shared memory as 8 words,
@@ -465,16 +487,45 @@ __device__ __forceinline__ int load_seg_s(const uint8_t *c, uint32_t rel, uint32
     return len;
 }
 
+// Geometry of chunk `id` of a K3 launch as seen by warp `warp`.
+struct K3Chunk {
+    uint64_t id, lc, nch, lo, hi, wlo, whi, P;
+    int si;
+    bool ok;
+};
+__device__ __forceinline__ K3Chunk k3_chunk(const SegTable &T, uint64_t id, const uint64_t *s_first,
+                                            const unsigned int *maxkey, float s, int warp) {
+    K3Chunk c{};
+    c.id = id;
+    c.ok = id < T.n3;
+    if (!c.ok) return c;
+    c.si = find_seg_c<3>(T, id, s_first);
+    const Seg S = get_seg(T, c.si);
+    float M;
+    c.ok = scale_from_key(maxkey[c.si], s, M) == TLC_OK;     // else the segment failed in K1
+    c.P = S.P;
+    c.lc = id - S.k3;
+    c.nch = (S.P + T.sz.c3 - 1) / T.sz.c3;
+    c.lo = c.lc * T.sz.c3;
+    c.hi = tmin<uint64_t>(S.P, c.lo + T.sz.c3);
+    const uint64_t sub = ((c.hi - c.lo + kK3Workers - 1) / kK3Workers + kK3Seg - 1) / kK3Seg * kK3Seg;
+    c.wlo = warp < kK3Workers ? tmin<uint64_t>(c.hi, c.lo + warp * sub) : c.hi;
+    c.whi = tmin<uint64_t>(c.hi, c.wlo + sub);
+    return c;
+}
+
 __global__ void __launch_bounds__(kK3Threads)
 tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                const uint8_t *scratch, Ctrl *ctrl, unsigned long long *states) {
-    __shared__ unsigned long long s_wagg[kScanWarps];
-    __shared__ unsigned long long s_off[kScanWarps + 1];    // offset entering each warp's sub-range, end
-    __shared__ uint32_t s_carry[kScanWarps + 1];
+    __shared__ unsigned long long s_wagg[kK3Workers];
+    __shared__ unsigned long long s_incl[2][kK3Workers];  // warps 0..w of a chunk composed
+    __shared__ unsigned long long s_off[kK3Workers + 1];  // offset entering each warp's sub-range, end
+    __shared__ uint32_t s_carry[kK3Workers + 1];
     __shared__ unsigned long long s_id;
     extern __shared__ __align__(128) uint8_t k3_smem_raw[];
     K3Smem &sm = *reinterpret_cast<K3Smem *>(k3_smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wk = tmin(warp, kK3Workers - 1);
     uint32_t w[8];
     __shared__ uint64_t s_first[kSegCache];
     if (threadIdx.x == 0) {
@@ -484,192 +535,105 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
     seg_index_load<3>(T, s_first);                       // (ends with __syncthreads)
     uint32_t parity = 0;
     pdl_wait();                                          // K2's quartic bytes and headers
-    while (true) {
-        if (threadIdx.x == 0) s_id = atomicAdd(&ctrl->k3_counter, 1ull);
+    uint64_t pend_id = ~0ull;                            // chunk awaiting phase 3 (~0: none)
+    int jb = 0;                                          // buffer of the new chunk
+    bool more = true;
+    while (more || pend_id != ~0ull) {
+        if (threadIdx.x == 0) s_id = more ? atomicAdd(&ctrl->k3_counter, 1ull) : ~0ull;
         __syncthreads();
-        const uint64_t id = s_id;
+        const uint64_t jid = s_id;
         __syncthreads();
-        if (id >= T.n3) break;
-        const int si = find_seg_c<3>(T, id, s_first);
-        const Seg S = get_seg(T, si);
-        float M;
-        if (scale_from_key(maxkey[si], s, M) != TLC_OK) continue;      // segment failed in K1
-        const uint8_t *bytes = scratch + S.bytes_off;
-        const uint64_t P = S.P, lc = id - S.k3, nch = (P + T.sz.c3 - 1) / T.sz.c3;
-        const uint64_t lo = lc * T.sz.c3, hi = tmin<uint64_t>(P, lo + T.sz.c3);
-        const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK3Seg - 1) / kK3Seg * kK3Seg;
-        const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
-        const uint32_t rwhi = (uint32_t)(whi - lo);
+        more = jid < T.n3;
+        const int ib = jb ^ 1;
 
-        // the chunk's bytes to shared memory with one bulk copy (16-byte multiple:
-        // a segment's scratch is padded to 16 bytes; the loaders pad past whi)
-        if (threadIdx.x == 0) {
-            const uint32_t nb = (uint32_t)((hi - lo + 15) & ~uint64_t(15));
-            mbar_expect_tx(&sm.bar, nb);
-            bulk_load(sm.chunk, bytes + lo, nb, &sm.bar);
-        }
-        mbar_wait(&sm.bar, parity);
-        parity ^= 1u;
-
-        // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row).  Rows'
-        // literal lists, with each literal's output offset, are kept for phase 3 while
-        // the warp's list space lasts.
-        RunSum wagg = run_identity();
-        uint32_t *lit = sm.lit[warp];
-        uint32_t used = 0;
-        bool keep = true;
-        int r = 0;
-        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
-            const int len = load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
-            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-            if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal in the row: one ALL run
-                wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
-                if (lane == 0) sm.rowmeta[warp][r] = make_uint2(0u, 0u);
-                continue;
-            }
-            bool stored = false;
-            const uint32_t L = row_literals(w, lit + used, keep ? kK3LitCap - used : 0u, stored);
-            if (!stored) {                                        // list space exhausted: mask form
-                keep = false;
-                const uint32_t mask = literal_mask(w);
-                wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
-                if (lane == 0) sm.rowmeta[warp][r] = make_uint2(kRowNotKept | L, 0u);
-                continue;
-            }
-            // literal k > 0 is preceded by R_k = p_k - p_{k-1} - 1 zero groups and costs
-            // lit_cost(R_k) bytes; literal 0's cost depends on the row's carry
-            uint32_t *e = lit + used;
-            uint32_t run = 0, plast = 0, p0 = 0;
-            for (uint32_t k0 = 0; k0 < L; k0 += 32) {
-                const uint32_t k = k0 + lane;
-                const uint32_t p = k < L ? e[k] : 0u;
-                uint32_t pp = __shfl_up_sync(0xffffffffu, p, 1);
-                if (lane == 0) pp = plast;
-                plast = __shfl_sync(0xffffffffu, p, (int)tmin<uint32_t>(31u, L - 1u - k0));
-                if (k0 == 0) p0 = __shfl_sync(0xffffffffu, p, 0);
-                uint32_t R = 0, cost = 0;
-                if (k > 0 && k < L) {
-                    R = p - pp - 1u;
-                    cost = lit_cost(R);
+        if (warp == kK3LookWarp) {
+            // ---- phase 2 of the pending chunk, concurrent with phase 1 of the new one
+            const K3Chunk pend = k3_chunk(T, pend_id, s_first, maxkey, s, warp);
+            unsigned long long ex = 0;
+            if (pend.ok) ex = warp_lookback<RunOp>(states + get_seg(T, pend.si).k3, pend.lc);
+            __syncthreads();                                         // B1: phase 1 of cj done
+            if (pend.ok) {
+                const Seg S = get_seg(T, pend.si);
+                RunSum bw = unpack(ex);
+                if (lane > 0 && lane <= kK3Workers) bw = compose(bw, unpack(s_incl[ib][lane - 1]));
+                const unsigned long long agg = s_incl[ib][kK3Workers - 1];
+                if (lane == 0 && pend.lc > 0) st_relaxed_u64(states + pend.id, kPrefix | RunOp::combine(ex, agg));
+                uint64_t o;
+                uint32_t c;
+                run_eval(bw, 0, o, c);
+                if (lane <= kK3Workers) {
+                    s_off[lane] = o;
+                    s_carry[lane] = c;
                 }
-                uint32_t x = cost;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-                    if (lane >= d) x += y;
-                }
-                if (k > 0 && k < L) e[k] = p | ((R % kMaxRun) << 12) | ((run + x - cost + R / kMaxRun) << 16);
-                run += __shfl_sync(0xffffffffu, x, 31);
+                const uint64_t o_begin = __shfl_sync(0xffffffffu, o, 0);
+                const uint64_t o_end = __shfl_sync(0xffffffffu, o, kK3Workers);
+                const uint32_t c_end = __shfl_sync(0xffffffffu, c, kK3Workers);
+                if (pend.lc == pend.nch - 1 && lane == 0) S.hdr->payload_len = o_end + (c_end > 0);
+                // every byte of the chunk's output that is not a flush code or a literal
+                // is a full chunk (255): fill the range before phase 3 stores the rest
+                warp_fill_full_chunks(S.payload, o_begin, o_end);
             }
-            const uint32_t Rt = row_len - 1u - plast;                 // trailing zero groups
-            const uint32_t rest = run + Rt / kMaxRun;                 // bytes after literal 0's
-            wagg = compose(wagg, RunSum{1u + p0 / kMaxRun + rest, p0 % kMaxRun, Rt % kMaxRun, true});
-            if (lane == 0) sm.rowmeta[warp][r] = make_uint2(L | (used << 16), rest | ((Rt % kMaxRun) << 16));
-            used += L;
+            __syncthreads();                                         // B2
+            pend_id = jid;
+            jb ^= 1;
+            continue;
         }
-        if (lane == 0) s_wagg[warp] = pack(wagg);
-        __syncthreads();
 
-        // ---- phase 2 (warp 0): publish the chunk aggregate, look back for the carry-in,
-        // publish the inclusive prefix; offsets and carries entering every warp's sub-range
-        if (warp == 0) {
-            RunSum incl = run_identity();                           // lane l: warps 0..l
-#pragma unroll
-            for (int k = 0; k < kScanWarps; k++)
-                if (k <= lane) incl = compose(incl, unpack(s_wagg[k]));
-            const unsigned long long agg = __shfl_sync(0xffffffffu, pack(incl), kScanWarps - 1);
-            const unsigned long long prev = __shfl_up_sync(0xffffffffu, pack(incl), 1);
-            if (lane == 0) st_relaxed_u64(states + id, (lc == 0 ? kPrefix : kReady) | agg);
-            const unsigned long long ex = warp_lookback<RunOp>(states + S.k3, lc);
-            if (lane == 0 && lc > 0) st_relaxed_u64(states + id, kPrefix | RunOp::combine(ex, agg));
-            RunSum bw = unpack(ex);
-            if (lane > 0 && lane < kScanWarps) bw = compose(bw, unpack(prev));
-            if (lane == kScanWarps) bw = compose(bw, unpack(agg));
-            uint64_t o;
-            uint32_t c;
-            run_eval(bw, 0, o, c);
-            if (lane <= kScanWarps) {
-                s_off[lane] = o;
-                s_carry[lane] = c;
+        {
+            const K3Chunk cj = k3_chunk(T, jid, s_first, maxkey, s, warp);
+            if (cj.ok) {
+            // the chunk's bytes to shared memory with one bulk copy (16-byte multiple:
+            // a segment's scratch is padded to 16 bytes; the loaders pad past whi)
+            const Seg S = get_seg(T, cj.si);
+            const uint32_t rwhi = (uint32_t)(cj.whi - cj.lo);
+            if (threadIdx.x == 0) {
+                const uint32_t nb = (uint32_t)((cj.hi - cj.lo + 15) & ~uint64_t(15));
+                mbar_expect_tx(&sm.bar, nb);
+                bulk_load(sm.chunk, scratch + S.bytes_off + cj.lo, nb, &sm.bar);
             }
-        }
-        __syncthreads();
-        const uint64_t o_begin = s_off[0], o_end = s_off[kScanWarps];
-        if (lc == nch - 1 && threadIdx.x == 0)
-            S.hdr->payload_len = o_end + (s_carry[kScanWarps] > 0);     // the end of the stream flushes
+            mbar_wait(&sm.bar, parity);
+            parity ^= 1u;
 
-        // ---- phase 3: every byte of the chunk's output that is not a flush code or a
-        // literal is a full chunk (255): fill the range, then store the sparse rest
-        cta_fill_full_chunks(S.payload, o_begin, o_end);
-        __syncthreads();
-        uint64_t off = s_off[warp];
-        uint32_t carry = s_carry[warp];
-        r = 0;
-        for (uint64_t row = wlo; row < whi; row += kK3WarpRow, r++) {
-            const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, whi - row);
-            const uint2 meta = sm.rowmeta[warp][r];
-            const uint32_t L = meta.x & 0xffffu;
-            const uint8_t *rowb = sm.chunk + (row - lo);
-            uint8_t *out = S.payload + off;
-            if (L == 0) {                             // no literal: the run grows by row_len
-                const uint32_t x = carry + row_len;
-                off += x / kMaxRun;
-                carry = x % kMaxRun;
-            } else if (!(meta.x & kRowNotKept)) {     // kept list: offsets known up to literal 0's cost
-                const uint32_t *e = lit + (meta.x >> 16);
-                const uint32_t R0 = (e[0] & 0xfffu) + carry;
-                const uint32_t cost0 = lit_cost(R0);
-                for (uint32_t k = lane; k < L; k += 32) {
-                    const uint32_t u = e[k];
-                    uint32_t o, rem;
-                    if (k == 0) {
-                        o = R0 / kMaxRun;
-                        rem = R0 % kMaxRun;
-                    } else {
-                        o = cost0 + (u >> 16);
-                        rem = (u >> 12) & 0xfu;
-                    }
-                    if (rem) out[o++] = run_code(rem);
-                    out[o] = rowb[u & 0xfffu];
-                }
-                off += cost0 + (meta.y & 0xffffu);
-                carry = meta.y >> 16;
-            } else {                                  // rebuild the list (kept rows are consumed)
-                const int len = load_seg_s(sm.chunk, (uint32_t)(row - lo) + kK3Seg * lane, rwhi, w);
-                bool stored;
-                const uint32_t L2 = row_literals(w, lit, kK3LitCap, stored);
-                if (!stored) {                        // denser than the list space: per-lane emission
-                    const uint32_t mask = literal_mask(w);
-                    const WarpRow wr = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
-                    uint32_t x = wr.count;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-                        if (lane >= d) x += y;
-                    }
-                    uint32_t o = x - wr.count, c = wr.carry_in;
-                    int prev = -1;
-                    for (uint32_t m = mask; m; m &= m - 1u) {
-                        const int q = (int)ctz32(m);
-                        const uint32_t R = (uint32_t)(q - prev - 1) + c;
-                        c = 0;
-                        o += R / kMaxRun;
-                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
-                        out[o++] = rowb[kK3Seg * lane + q];
-                        prev = q;
-                    }
-                    off += wr.row_count;
-                    carry = wr.carry_out;
-                    if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
+            // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row); rows'
+            // literal lists with their output offsets are kept while the list space lasts
+            RunSum wagg = run_identity();
+            uint32_t *lit = sm.lit[jb][wk];
+            uint32_t used = 0;
+            bool keep = true;
+            int r = 0;
+            for (uint64_t row = cj.wlo; row < cj.whi; row += kK3WarpRow, r++) {
+                const uint32_t rel = (uint32_t)(row - cj.lo);
+                const int len = load_seg_s(sm.chunk, rel + kK3Seg * lane, rwhi, w);
+                const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, cj.whi - row);
+                if (__all_sync(0xffffffffu, plain_lane(w))) {        // no literal: one ALL run
+                    wagg = compose(wagg, RunSum{row_len / kMaxRun, row_len % kMaxRun, 0u, false});
+                    if (lane == 0) sm.rowmeta[jb][wk][r] = make_uint4(0u, 0u, 0u, 0u);
                     continue;
                 }
-                uint32_t base = 0;
-                for (uint32_t k0 = 0; k0 < L2; k0 += 32) {         // literal k0 + lane
+                bool stored = false;
+                const uint32_t L = row_literals(w, lit + used, keep ? kK3LitCap - used : 0u, stored);
+                if (!stored) {                                        // list space exhausted: mask form
+                    keep = false;
+                    const uint32_t mask = literal_mask(w);
+                    wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
+                    if (lane == 0) sm.rowmeta[jb][wk][r] = make_uint4(kRowNotKept | L, 0u, 0u, 0u);
+                    continue;
+                }
+                // literal k > 0 is preceded by R_k = p_k - p_{k-1} - 1 zero groups and costs
+                // lit_cost(R_k) bytes; literal 0's cost depends on the row's carry
+                const uint8_t *rowb = sm.chunk + rel;
+                uint32_t *e = lit + used;
+                uint32_t run = 0, plast = 0, p0 = 0;
+                for (uint32_t k0 = 0; k0 < L; k0 += 32) {
                     const uint32_t k = k0 + lane;
-                    uint32_t R = 0, cost = 0, p = 0;
-                    if (k < L2) {
-                        p = lit[k];
-                        R = k ? p - lit[k - 1] - 1u : p + carry;
+                    const uint32_t p = k < L ? e[k] : 0u;
+                    uint32_t pp = __shfl_up_sync(0xffffffffu, p, 1);
+                    if (lane == 0) pp = plast;
+                    plast = __shfl_sync(0xffffffffu, p, (int)tmin<uint32_t>(31u, L - 1u - k0));
+                    if (k0 == 0) p0 = __shfl_sync(0xffffffffu, p, 0);
+                    uint32_t R = 0, cost = 0;
+                    if (k > 0 && k < L) {
+                        R = p - pp - 1u;
                         cost = lit_cost(R);
                     }
                     uint32_t x = cost;
@@ -678,20 +642,103 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                         if (lane >= d) x += y;
                     }
-                    if (k < L2) {
-                        uint32_t o = base + (x - cost) + R / kMaxRun;
-                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
-                        out[o] = rowb[p];
-                    }
-                    base += __shfl_sync(0xffffffffu, x, 31);
+                    if (k < L)
+                        e[k] = ((uint32_t)rowb[p] << 8) |
+                               (k ? (R % kMaxRun) | ((run + x - cost + R / kMaxRun) << 16) : 0u);
+                    run += __shfl_sync(0xffffffffu, x, 31);
                 }
-                const uint32_t Rt = row_len - 1u - lit[L2 - 1];
-                off += base + Rt / kMaxRun;
-                carry = Rt % kMaxRun;
-                __syncwarp();                         // the list is overwritten by the next rebuild
+                const uint32_t Rt = row_len - 1u - plast;                 // trailing zero groups
+                const uint32_t rest = run + Rt / kMaxRun;                 // bytes after literal 0's
+                wagg = compose(wagg, RunSum{1u + p0 / kMaxRun + rest, p0 % kMaxRun, Rt % kMaxRun, true});
+                if (lane == 0)
+                    sm.rowmeta[jb][wk][r] = make_uint4(L | (used << 16), rest | ((Rt % kMaxRun) << 16), p0, 0u);
+                used += L;
             }
-            if (lane == 0 && carry > 0 && row + row_len == P) S.payload[off] = run_code(carry);
+            if (lane == 0) s_wagg[warp] = pack(wagg);
+            asm volatile("bar.sync 1, %0;" ::"r"(32 * kK3Workers) : "memory");   // the scanning warps
+            if (warp == 0) {                                 // publish the chunk aggregate at once
+                RunSum incl = run_identity();
+#pragma unroll
+                for (int k = 0; k < kK3Workers; k++)
+                    if (k <= lane) incl = compose(incl, unpack(s_wagg[k]));
+                if (lane < kK3Workers) s_incl[jb][lane] = pack(incl);
+                if (lane == 31) st_relaxed_u64(states + cj.id, (cj.lc == 0 ? kPrefix : kReady) | pack(incl));
+            }
+            }
         }
+        __syncthreads();                                     // B1
+        __syncthreads();                                     // B2: pending chunk's offsets known, 255s filled
+
+        const K3Chunk pend = k3_chunk(T, pend_id, s_first, maxkey, s, warp);
+        if (pend.ok) {
+            // ---- phase 3 of the pending chunk: the sparse stores (flush codes and literals)
+            const Seg S = get_seg(T, pend.si);
+            const uint8_t *bytes = scratch + S.bytes_off;
+            const uint32_t *lit = sm.lit[ib][wk];
+            uint64_t off = s_off[warp];
+            uint32_t carry = s_carry[warp];
+            int r = 0;
+            for (uint64_t row = pend.wlo; row < pend.whi; row += kK3WarpRow, r++) {
+                const uint32_t row_len = (uint32_t)tmin<uint64_t>(kK3WarpRow, pend.whi - row);
+                const uint4 meta = sm.rowmeta[ib][wk][r];
+                const uint32_t L = meta.x & 0xffffu;
+                uint8_t *out = S.payload + off;
+                if (L == 0) {                             // no literal: the run grows by row_len
+                    const uint32_t x = carry + row_len;
+                    off += x / kMaxRun;
+                    carry = x % kMaxRun;
+                } else if (!(meta.x & kRowNotKept)) {     // kept list: offsets known up to literal 0's cost
+                    const uint32_t *e = lit + (meta.x >> 16);
+                    const uint32_t R0 = meta.z + carry;
+                    const uint32_t cost0 = lit_cost(R0);
+                    for (uint32_t k = lane; k < L; k += 32) {
+                        const uint32_t u = e[k];
+                        uint32_t o, rem;
+                        if (k == 0) {
+                            o = R0 / kMaxRun;
+                            rem = R0 % kMaxRun;
+                        } else {
+                            o = cost0 + (u >> 16);
+                            rem = u & 0xfu;
+                        }
+                        if (rem) out[o++] = run_code(rem);
+                        out[o] = (uint8_t)(u >> 8);
+                    }
+                    off += cost0 + (meta.y & 0xffffu);
+                    carry = meta.y >> 16;
+                } else {                                  // not kept: per-lane emission from the bytes
+                    const int len = load_seg_g(bytes, row + kK3Seg * lane, pend.whi, w);
+                    const uint32_t mask = literal_mask(w);
+                    const WarpRow wr = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
+                    uint32_t x = wr.count;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    uint32_t o = x - wr.count;
+                    uint32_t c = wr.carry_in;
+                    int prev = -1;
+                    for (uint32_t m = mask; m; m &= m - 1u) {
+                        const int q = (int)ctz32(m);
+                        const uint32_t R = (uint32_t)(q - prev - 1) + c;
+                        c = 0;
+                        o += R / kMaxRun;
+                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
+                        uint32_t word = w[0];             // select, not a dynamic index
+#pragma unroll
+                        for (int k = 1; k < 8; k++) word = (k == (q >> 2)) ? w[k] : word;
+                        out[o++] = (uint8_t)(word >> (8 * (q & 3)));
+                        prev = q;
+                    }
+                    off += wr.row_count;
+                    carry = wr.carry_out;
+                }
+                if (lane == 0 && carry > 0 && row + row_len == pend.P) S.payload[off] = run_code(carry);
+            }
+        }
+        pend_id = jid;
+        jb ^= 1;
     }
 }
 
@@ -782,3 +829,9 @@ size_t compress_workspace_bytes(uint64_t n) {
 }
 
 }  // namespace tlc
+
+#ifdef TLC_K3_TRACE
+extern "C" int tlc_debug_k3_trace(void *host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, tlc::g_k3_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif

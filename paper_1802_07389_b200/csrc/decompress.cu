@@ -26,22 +26,36 @@ namespace tlc {
 constexpr int kK4Threads = kScanThreads;
 constexpr int kK4Seg = 16;
 
-__device__ __forceinline__ int load_pay16(const uint8_t *__restrict__ p, uint64_t pos, uint64_t hi,
-                                          uint32_t (&len)[kK4Seg]) {
-    const int n = pos < hi ? (int)tmin<uint64_t>(kK4Seg, hi - pos) : 0;
-    uint8_t b[kK4Seg];
+// Expansion length of the 4 payload bytes of a word: each byte b counts
+// len(b) = b >= 243 ? b - 241 : 1.  Bytes >= 243 are the ones whose low seven
+// bits plus 13 carry into bit 7 while bit 7 is set (SWAR, no cross-byte carry).
+__device__ __forceinline__ uint32_t word_len(uint32_t w) {
+    const uint32_t hi = w & ((w & 0x7f7f7f7fu) + 0x0d0d0d0du) & 0x80808080u;   // bit 7 of codes >= 243
+    const uint32_t m = (hi >> 7) * 0xffu;                                        // their bytes
+    return 4u + __dp4a(w & m, 0x01010101u, 0u) - 242u * (uint32_t)__popc(hi);
+}
+
+// Payload bytes [pos, min(pos+16, hi)) as 4 words and their total expansion
+// length; n = the number of bytes present.
+__device__ __forceinline__ uint32_t pay16(const uint8_t *__restrict__ p, uint64_t pos, uint64_t hi,
+                                          uint32_t (&w)[4], int &n) {
+    n = pos < hi ? (int)tmin<uint64_t>(kK4Seg, hi - pos) : 0;
     if (n == kK4Seg && (reinterpret_cast<uintptr_t>(p + pos) & 15u) == 0) {
-        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(p + pos));
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < kK4Seg; k++) b[k] = (ws[k >> 2] >> (8 * (k & 3))) & 0xff;
-    } else {
-#pragma unroll
-        for (int k = 0; k < kK4Seg; k++) b[k] = k < n ? p[pos + k] : 0;
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p + pos));
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        return word_len(w[0]) + word_len(w[1]) + word_len(w[2]) + word_len(w[3]);
     }
+    uint32_t sum = 0;
 #pragma unroll
-    for (int k = 0; k < kK4Seg; k++) len[k] = k < n ? zre_len(b[k]) : 0u;
-    return n;
+    for (int k = 0; k < 4; k++) w[k] = 0;
+#pragma unroll
+    for (int k = 0; k < kK4Seg; k++)
+        if (k < n) {
+            const uint32_t b = p[pos + k];
+            w[k >> 2] |= b << (8 * (k & 3));
+            sum += zre_len(b);
+        }
+    return sum;
 }
 
 __global__ void __launch_bounds__(kK4Threads)
@@ -49,7 +63,6 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
     __shared__ unsigned long long s_warp[kScanWarps];
     __shared__ unsigned long long s_wsum[kScanWarps];
     __shared__ unsigned long long s_id;
-    uint32_t len[kK4Seg];
     __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
     seg_index_load<4>(T, s_first);
@@ -91,11 +104,10 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
 
         // ---- phase 1: expansion length of each warp's sub-range, then of the chunk
         uint64_t wsum = 0;
+        uint32_t wv[4];
+        int nb;
         for (uint64_t row = wlo; row < whi; row += kWRow) {
-            load_pay16(S.payload, row + (uint64_t)kK4Seg * lane, whi, len);
-            uint32_t sum = 0;
-#pragma unroll
-            for (int k = 0; k < kK4Seg; k++) sum += len[k];
+            uint32_t sum = pay16(S.payload, row + (uint64_t)kK4Seg * lane, whi, wv, nb);
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
             wsum += sum;
@@ -122,14 +134,12 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         const uint64_t run = s_warp[0];
         if (hi == Z && threadIdx.x == 0 && run + agg != P) raise_format(hdr);
 
-        // ---- phase 3: seek entries (payload byte covering J0 = k*kT5, offset inside it)
+        // ---- phase 3: seek entries (payload byte covering J0 = k*kT5, offset inside it).  A
+        // lane's 16 bytes expand to at most 16*14 < kT5 positions: at most one J0 falls in them.
         uint64_t q0 = run + before;                       // position of the warp's first byte
         for (uint64_t row = wlo; row < whi; row += kWRow) {
             const uint64_t pos0 = row + (uint64_t)kK4Seg * lane;
-            load_pay16(S.payload, pos0, whi, len);
-            uint32_t sum = 0;
-#pragma unroll
-            for (int k = 0; k < kK4Seg; k++) sum += len[k];
+            const uint32_t sum = pay16(S.payload, pos0, whi, wv, nb);
             uint32_t x = sum;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -137,13 +147,17 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
                 if (lane >= d) x += y;
             }
             uint64_t q = q0 + (x - sum);
+            const uint64_t kt = (q + kT5 - 1) / kT5, J0 = kt * kT5;
+            if (J0 < q + sum && kt < num_out_tiles) {
 #pragma unroll
-            for (int k = 0; k < kK4Seg; k++) {
-                if (len[k]) {
-                    const uint64_t kt = (q + kT5 - 1) / kT5;
-                    const uint64_t J0 = kt * kT5;
-                    if (J0 < q + len[k] && kt < num_out_tiles) seek[S.k5 + kt] = ((pos0 + k) << 4) | (J0 - q);
-                    q += len[k];
+                for (int k = 0; k < kK4Seg; k++) {
+                    if (k >= nb) break;
+                    const uint32_t len = zre_len((wv[k >> 2] >> (8 * (k & 3))) & 0xffu);
+                    if (J0 < q + len) {
+                        seek[S.k5 + kt] = ((pos0 + k) << 4) | (J0 - q);
+                        break;
+                    }
+                    q += len;
                 }
             }
             q0 += __shfl_sync(0xffffffffu, x, 31);

@@ -20,7 +20,7 @@ class Ent(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("launches", ctypes.c_ulonglong), ("total_ms", ctypes.c_double)]
 
 
-def run(path, n=1 << 28, s=1.75, steps=30, warm=45):
+def run(path, n=1 << 28, s=1.75, steps=30, warm=45, keep=False):
     L = ctypes.CDLL(path)
     P, U64, SZ = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t
     L.tlc_compress.argtypes = [P, P, U64, ctypes.c_float, ctypes.c_int, P, U64, P, P, SZ, P]
@@ -60,6 +60,8 @@ def run(path, n=1 << 28, s=1.75, steps=30, warm=45):
     k = L.tlc_prof_collect(ctypes.cast(arr, P), 16)
     ms = e0.elapsed_time(e1) / steps
     per = {arr[i].name.decode(): arr[i].total_ms / arr[i].launches for i in range(k)}
+    if keep:
+        return L
     print(os.path.basename(path), f"step {ms:.4f} ms  fp32-in {4 * n / ms / 1e6:.1f} GB/s  ",
           "  ".join(f"{a}={b:.4f}" for a, b in per.items()), flush=True)
 
