@@ -284,7 +284,7 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
 NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
 
 
-def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True):
+def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True, e2e_steps=0):
     """BASELINE configs[4]: the model's ndim>=2 gradient tensors exchanged through
     the parameter-server push/pull (tlc_exchange_push + tlc_exchange_pull, delta =
     mean) on `world` ranks; every rank holds its own full state change (weak
@@ -326,24 +326,76 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2
     status = x.status(stream)
     wire = sum(x.traffic())
     kern_ms = sum(tot for (_, tot) in prof.values()) / steps
+
+    e2e = None
+    if e2e_steps:
+        # End to end through the same public calls: every step copies its gradient set
+        # (N fp32 values) from pinned host memory, runs push + pull and reads the
+        # exchange status back to pinned host memory (the step's result; the model
+        # update stays in HBM).  H2D on its own stream, double-buffered, so step k+1's
+        # copy overlaps step k's exchange.
+        gflat = [torch.empty(N, dtype=torch.float32, device=dev) for _ in range(2)]
+        gv = [list(torch.split(g, sizes)) for g in gflat]
+        hin = torch.empty(N, dtype=torch.float32, pin_memory=True)
+        hin.copy_(torch.cat(grads[0]).cpu())
+        hst = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        h2d = torch.cuda.Stream(device=dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+
+        def e2e_step(k):
+            b = k % 2
+            h2d.wait_event(ev_done[b])
+            with torch.cuda.stream(h2d):
+                gflat[b].copy_(hin, non_blocking=True)
+            ev_in[b].record(h2d)
+            stream.wait_event(ev_in[b])
+            x.push(gv[b], s, True, stream)
+            x.pull(outs, s, True, stream)
+            x.status_async(hst[b:b + 1], stream)
+            ev_done[b].record(stream)
+
+        for b in range(2):
+            ev_done[b].record(stream)
+        for k in range(2):
+            e2e_step(k)
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for b in range(2):
+            ev_done[b].record(stream)
+        for k in range(e2e_steps):
+            e2e_step(k)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e = {"ms": f0.elapsed_time(f1) / e2e_steps, "h2d": 4 * N, "d2h": 4, "steps": e2e_steps,
+               "status": int(hst.max())}
     x.close()
     comm.close()
     return {"ms": ms, "kernel_ms": kern_ms, "launches": launches, "wire": wire, "N": N, "status": status,
-            "contexts": len(T.tlc_plan(sizes, world)),
+            "contexts": len(T.tlc_plan(sizes, world)), "e2e": e2e,
             "kernels": {k: {"launches_per_step": c / steps, "ms_per_step": t / steps} for k, (c, t) in prof.items()}}
 
 
-def run_exchange_leg(args, T, dev, world, rank, dist):
+def run_exchange_leg(args, T, dev, world, rank, dist, e2e_steps=None):
     import torch
 
     r = measure_exchange(T, dev, world, rank, args.model, args.xs, args.steps, args.warmup,
-                         dist if world > 1 else None, p2p=args.xchg == "p2p")
+                         dist if world > 1 else None, p2p=args.xchg == "p2p",
+                         e2e_steps=e2e_steps if e2e_steps is not None else (0 if args.no_e2e else args.e2e_steps))
     ms = r["ms"]
+    ems = r["e2e"]["ms"] if r["e2e"] else None
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, ems or 0.0], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(t[0].item())
+        ems = float(t[1].item()) if r["e2e"] else None
     value = world * 4.0 * r["N"] / (ms / 1e3) / 1e9
+    if r["e2e"]:
+        r["e2e"]["value"] = world * 4.0 * r["N"] / (ems / 1e3) / 1e9
+        r["e2e"]["ms"] = ems
     return r, ms, value
 
 
@@ -528,7 +580,7 @@ def run_tlc(args):
 
     xw1 = None
     if world == 1 and not args.no_xchg_w1:
-        r, xms, xval = run_exchange_leg(args, T, dev, 1, 0, None)
+        r, xms, xval = run_exchange_leg(args, T, dev, 1, 0, None, e2e_steps=0)
         xw1 = {"workload": f"configs[4]: {args.model} gradient exchange (push+pull) at s={args.xs}, W=1",
                "value": xval, "unit": "GB/s", "ms_per_step": xms, "kernel_ms_per_step": r["kernel_ms"],
                "status": r["status"]}
@@ -605,7 +657,12 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             "kernels_rank0": r["kernels"],
             "gpu_launches": r["launches"],
             "exchange_status": r["status"],
-            "e2e": None,
+            "e2e": ({"value": r["e2e"]["value"], "unit": "GB/s", "h2d_bytes_per_step": r["e2e"]["h2d"],
+                     "d2h_bytes_per_step": r["e2e"]["d2h"], "steps": r["e2e"]["steps"], "ms_per_step": r["e2e"]["ms"],
+                     "status": r["e2e"]["status"],
+                     "what": "per step and rank: pinned host gradient set -> HBM (own stream, double-buffered), "
+                             "tlc_exchange_push + tlc_exchange_pull, exchange status -> pinned host"}
+                    if r["e2e"] else None),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -206,6 +206,9 @@ int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
  *                     full-size fp32 tensors.
  * tlc_exchange_status synchronizes `stream` and returns the worst device status
  *                     over all received headers (NONFINITE/RANGE from a peer).
+ * tlc_exchange_status_async  the same worst status, written by an async copy
+ *                     enqueued on `stream` to `dst` (pinned host or device
+ *                     memory, 4 bytes, owned by the caller); no host sync.
  * Push/pull enqueue on `stream`, allocate nothing and do not synchronize the
  * host (a descriptor upload happens when the grads/outs pointers change).
  */
@@ -231,6 +234,7 @@ uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction /* 0 push,
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream);
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream);
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status, void *stream);
+int tlc_exchange_status_async(tlc_exchange *x, unsigned int *dst, void *stream);
 
 /* Peer-memory mode (one rank per GPU on an NVLink/NVSwitch box).  After
  * tlc_exchange_create, every rank calls tlc_exchange_ipc_handles (writes 5 x 64

@@ -69,6 +69,7 @@ def _load():
         "tlc_exchange_push": (I, [P, P, F, I, P]),
         "tlc_exchange_pull": (I, [P, P, F, I, P]),
         "tlc_exchange_status": (I, [P, P, P]),
+        "tlc_exchange_status_async": (I, [P, P, P]),
         "tlc_exchange_ipc_handles": (I, [P, P]),
         "tlc_exchange_ipc_open": (I, [P, P]),
         "tlc_exchange_traffic": (I, [P, P]),
@@ -462,6 +463,13 @@ class Exchange:
         if rc != TLC_OK:
             raise TlcError(rc, "tlc_exchange_status")
         return int(st.value)
+
+    def status_async(self, dst, stream=None):
+        """Enqueue the worst status into `dst` (a 1-element uint32/int32 tensor, pinned
+        host or device) without synchronizing."""
+        rc = _lib.tlc_exchange_status_async(self._x, ctypes.c_void_p(dst.data_ptr()), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_status_async")
 
     def close(self):
         if self._x:

@@ -581,19 +581,30 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
     return launch_decompress_table(x->apply_tab.T, TLC_MODE_ACCUMULATE, x->apply_tab.ws, st);
 }
 
-int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream) {
-    // worst device status over every received header (push and pull); synchronizes `stream`
-    if (!x || !status_out) return TLC_ERR_ARG;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+static int exchange_status_enqueue(tlc_exchange *x, unsigned int *dst, cudaStream_t st) {
+    // worst device status over every received header (push and pull)
     int rc = cuda_ok(cudaMemsetAsync(x->d_status, 0, sizeof(unsigned int), st));
     const int nown = (int)x->owned[x->me].size();
     if (rc == TLC_OK && nown && !x->p2p) tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_recv, x->W * nown, x->d_status);
     if (rc == TLC_OK && x->p2p && !x->ctx.empty())   // peer-memory mode: this rank's own pushes
         tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_send, (int)x->ctx.size(), x->d_status);
     if (rc == TLC_OK && !x->ctx.empty()) tlc_status_kernel<<<1, 256, 0, st>>>(x->pull_hdr, (int)x->ctx.size(), x->d_status);
-    if (rc == TLC_OK) rc = cuda_ok(cudaMemcpyAsync(status_out, x->d_status, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    if (rc == TLC_OK) rc = cuda_ok(cudaMemcpyAsync(dst, x->d_status, sizeof(unsigned int), cudaMemcpyDefault, st));
+    return rc;
+}
+
+int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream) {
+    // synchronizes `stream`
+    if (!x || !status_out) return TLC_ERR_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int rc = exchange_status_enqueue(x, status_out, st);
     if (rc == TLC_OK) rc = cuda_ok(cudaStreamSynchronize(st));
     return rc;
+}
+
+int tlc_exchange_status_async(tlc_exchange *x, unsigned int *dst, void *stream) {
+    if (!x || !dst) return TLC_ERR_ARG;
+    return exchange_status_enqueue(x, dst, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
