@@ -514,7 +514,7 @@ __device__ __forceinline__ K3Chunk k3_chunk(const SegTable &T, uint64_t id, cons
     return c;
 }
 
-__global__ void __launch_bounds__(kK3Threads)
+__global__ void __launch_bounds__(kK3Threads, 4)
 tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                const uint8_t *scratch, Ctrl *ctrl, unsigned long long *states) {
     __shared__ unsigned long long s_wagg[kK3Workers];
@@ -631,20 +631,17 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     if (lane == 0) pp = plast;
                     plast = __shfl_sync(0xffffffffu, p, (int)tmin<uint32_t>(31u, L - 1u - k0));
                     if (k0 == 0) p0 = __shfl_sync(0xffffffffu, p, 0);
-                    uint32_t R = 0, cost = 0;
-                    if (k > 0 && k < L) {
-                        R = p - pp - 1u;
-                        cost = lit_cost(R);
-                    }
+                    const bool inner = k > 0 && k < L;
+                    const uint32_t R = inner ? p - pp - 1u : 0u;
+                    const uint32_t q = R / kMaxRun, rem = R - q * kMaxRun;
+                    const uint32_t cost = inner ? q + (rem != 0) + 1u : 0u;
                     uint32_t x = cost;
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                         if (lane >= d) x += y;
                     }
-                    if (k < L)
-                        e[k] = ((uint32_t)rowb[p] << 8) |
-                               (k ? (R % kMaxRun) | ((run + x - cost + R / kMaxRun) << 16) : 0u);
+                    if (k < L) e[k] = ((uint32_t)rowb[p] << 8) | (inner ? rem | ((run + x - cost + q) << 16) : 0u);
                     run += __shfl_sync(0xffffffffu, x, 31);
                 }
                 const uint32_t Rt = row_len - 1u - plast;                 // trailing zero groups
