@@ -28,6 +28,18 @@ namespace tlc {
 // ============================================================== K1
 constexpr int kK1Threads = 512;
 
+#ifdef TLC_K1_L2HINT
+__device__ __forceinline__ float4 ld_l2hint4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+#endif
+#ifndef TLC_K1_U
+#define TLC_K1_U 4
+#endif
+
 __device__ __forceinline__ unsigned int absmax_key(float t, float e) {
     float u = __fadd_rn(e, t);                       // step (1): u = buffer + T_in
     return __float_as_uint(u) & 0x7fffffffu;         // |u| as ordered uint; NaN > Inf
@@ -68,14 +80,19 @@ tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
             const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
             const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
             const uint64_t a = lo / 4, b = hi / 4;             // lo is a multiple of 4
-            constexpr int U = 4;
+            constexpr int U = TLC_K1_U;
             uint64_t i = a + threadIdx.x;
             for (; i + (U - 1) * kK1Threads < b; i += U * kK1Threads) {
                 float4 x[U], y[U];
 #pragma unroll
                 for (int k = 0; k < U; k++) {
+#ifdef TLC_K1_L2HINT
+                    x[k] = ld_l2hint4(t4 + i + k * kK1Threads);
+                    y[k] = ld_l2hint4(e4 + i + k * kK1Threads);
+#else
                     x[k] = ld_stream4(t4 + i + k * kK1Threads);
                     y[k] = __ldcg(e4 + i + k * kK1Threads);
+#endif
                 }
 #pragma unroll
                 for (int k = 0; k < U; k++) {
