@@ -392,15 +392,16 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
 #ifdef TLC_K3_TRACE
 // development instrumentation: %globaltimer at phase boundaries of every K3 chunk
 __device__ unsigned long long g_k3_trace[1 << 14][8];
+__device__ unsigned long long g_k3_cta[4096][2];           // per CTA: entry, exit
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-#define K3_TRACE(slot) \
-    do { if ((threadIdx.x & 31) == 0 && id < (1u << 14)) g_k3_trace[id][slot] = gtimer(); } while (0)
+#define K3_TRACE(id, slot) \
+    do { if ((threadIdx.x & 31) == 0 && (id) < (1u << 14)) g_k3_trace[(id)][slot] = gtimer(); } while (0)
 #else
-#define K3_TRACE(slot) do {} while (0)
+#define K3_TRACE(id, slot) do {} while (0)
 #endif
 
 constexpr int kK3Workers = kScanWarps;                       // warps scanning the chunk
@@ -418,7 +419,10 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
 }
 
 constexpr int kK3RowsPerWarp = (int)(kLargeItems.c3 / kScanWarps / kK3WarpRow);   // rows of a sub-range
-constexpr int kK3LitCap = 256;             // list entries a warp keeps per chunk between phases 1 and 3
+#ifndef TLC_K3_LITCAP
+#define TLC_K3_LITCAP 512
+#endif
+constexpr int kK3LitCap = TLC_K3_LITCAP;   // list entries a warp keeps per chunk between phases 1 and 3
 constexpr uint32_t kRowNotKept = 1u << 31;
 
 // K3 is software-pipelined over the chunks a CTA takes: phase 1 of chunk j runs
@@ -531,7 +535,10 @@ __device__ __forceinline__ K3Chunk k3_chunk(const SegTable &T, uint64_t id, cons
     return c;
 }
 
-__global__ void __launch_bounds__(kK3Threads, 4)
+#ifndef TLC_K3_MINB
+#define TLC_K3_MINB 4
+#endif
+__global__ void __launch_bounds__(kK3Threads, TLC_K3_MINB)
 tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                const uint8_t *scratch, Ctrl *ctrl, unsigned long long *states) {
     __shared__ unsigned long long s_wagg[kK3Workers];
@@ -545,6 +552,9 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
     const int wk = tmin(warp, kK3Workers - 1);
     uint32_t w[8];
     __shared__ uint64_t s_first[kSegCache];
+#ifdef TLC_K3_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_k3_cta[blockIdx.x][0] = gtimer();
+#endif
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -562,12 +572,21 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
         __syncthreads();
         more = jid < T.n3;
         const int ib = jb ^ 1;
+        if (threadIdx.x == 0) {
+            K3_TRACE(jid, 0);
+#ifdef TLC_K3_TRACE
+            unsigned int smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            if (jid < (1u << 14)) { g_k3_trace[jid][6] = smid; g_k3_trace[jid][7] = blockIdx.x; }
+#endif
+        }
 
         if (warp == kK3LookWarp) {
             // ---- phase 2 of the pending chunk, concurrent with phase 1 of the new one
             const K3Chunk pend = k3_chunk(T, pend_id, s_first, maxkey, s, warp);
             unsigned long long ex = 0;
             if (pend.ok) ex = warp_lookback<RunOp>(states + get_seg(T, pend.si).k3, pend.lc);
+            if (pend.ok) K3_TRACE(pend.id, 1);
             __syncthreads();                                         // B1: phase 1 of cj done
             if (pend.ok) {
                 const Seg S = get_seg(T, pend.si);
@@ -589,6 +608,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 // every byte of the chunk's output that is not a flush code or a literal
                 // is a full chunk (255): fill the range before phase 3 stores the rest
                 warp_fill_full_chunks(S.payload, o_begin, o_end);
+                K3_TRACE(pend.id, 4);
             }
             __syncthreads();                                         // B2
             pend_id = jid;
@@ -610,6 +630,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
             }
             mbar_wait(&sm.bar, parity);
             parity ^= 1u;
+            if (threadIdx.x == 0) K3_TRACE(cj.id, 2);
 
             // ---- phase 1: run summary of the warp's sub-range (one per 1 KiB row); rows'
             // literal lists with their output offsets are kept while the list space lasts
@@ -677,6 +698,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     if (k <= lane) incl = compose(incl, unpack(s_wagg[k]));
                 if (lane < kK3Workers) s_incl[jb][lane] = pack(incl);
                 if (lane == 31) st_relaxed_u64(states + cj.id, (cj.lc == 0 ? kPrefix : kReady) | pack(incl));
+                K3_TRACE(cj.id, 3);
             }
             }
         }
@@ -750,10 +772,14 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 }
                 if (lane == 0 && carry > 0 && row + row_len == pend.P) S.payload[off] = run_code(carry);
             }
+            if (warp == 0) K3_TRACE(pend.id, 5);
         }
         pend_id = jid;
         jb ^= 1;
     }
+#ifdef TLC_K3_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_k3_cta[blockIdx.x][1] = gtimer();
+#endif
 }
 
 // ============================================================== host side
@@ -847,5 +873,8 @@ size_t compress_workspace_bytes(uint64_t n) {
 #ifdef TLC_K3_TRACE
 extern "C" int tlc_debug_k3_trace(void *host, size_t bytes) {
     return cudaMemcpyFromSymbol(host, tlc::g_k3_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+extern "C" int tlc_debug_k3_cta(void *host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, tlc::g_k3_cta, bytes) == cudaSuccess ? 0 : 1;
 }
 #endif

@@ -61,6 +61,7 @@ def run(path, n=1 << 28, s=1.75, steps=30, warm=45, keep=False):
     ms = e0.elapsed_time(e1) / steps
     per = {arr[i].name.decode(): arr[i].total_ms / arr[i].launches for i in range(k)}
     if keep:
+        print("events:", "  ".join(f"{a}={b * 1e3:.1f}us" for a, b in per.items()), flush=True)
         return L
     print(os.path.basename(path), f"step {ms:.4f} ms  fp32-in {4 * n / ms / 1e6:.1f} GB/s  ",
           "  ".join(f"{a}={b:.4f}" for a, b in per.items()), flush=True)
