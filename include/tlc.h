@@ -211,6 +211,10 @@ int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
  *                     memory, 4 bytes, owned by the caller); no host sync.
  * Push/pull enqueue on `stream`, allocate nothing and do not synchronize the
  * host (a descriptor upload happens when the grads/outs pointers change).
+ * CUDA graphs: in peer-memory mode a push or pull may be captured (stream
+ * capture) once the grads/outs pointers have been seen by an eager call; the
+ * flag-barrier epochs are counted on the device, so replays stay ordered.  The
+ * NCCL transport returns TLC_ERR_ARG when called on a capturing stream.
  */
 typedef struct tlc_comm tlc_comm;
 typedef struct tlc_exchange tlc_exchange;

@@ -62,7 +62,16 @@ __global__ void tlc_status_kernel(const tlc_header *__restrict__ h, int count, u
 // fence, write `epoch` into this rank's slot on every rank, then wait until every
 // rank has written it here.  Ordered after the kernels that produced the data.
 __global__ void tlc_flag_barrier_kernel(unsigned long long *const *peer_flags, unsigned long long *mine, int me,
-                                        int W, int slot, unsigned long long epoch) {
+                                        int W, int slot, unsigned long long *epoch_ctr) {
+    // the epoch is counted on the device (every rank runs the same barrier sequence),
+    // so a captured CUDA graph replays with fresh epochs
+    __shared__ unsigned long long s_epoch;
+    if (threadIdx.x == 0) {
+        s_epoch = *epoch_ctr + 1;
+        *epoch_ctr = s_epoch;
+    }
+    __syncthreads();
+    const unsigned long long epoch = s_epoch;
     const int w = threadIdx.x;
     if (w < W) {
         __threadfence_system();
@@ -148,7 +157,7 @@ struct tlc_exchange {
     unsigned long long **d_peer_flags = nullptr;     // device array: every rank's flag slots
     std::vector<void *> opened;                      // peer mappings to close
     std::vector<std::array<void *, 5>> peer;         // per rank: push_send, push_hdr, pull_buf, pull_hdr, flags
-    unsigned long long epoch = 0;
+    unsigned long long *d_epoch = nullptr;           // barrier epochs issued (device counter)
     std::vector<const float *> last_grads;
     std::vector<float *> last_outs;
 };
@@ -213,7 +222,8 @@ int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
     for (void *p : x->opened) cudaIpcCloseMemHandle(p);
     void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
-                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags};
+                   x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags,
+                   x->d_epoch};
     for (void *p : dev)
         if (p) cudaFree(p);
     x->push_tab.release();
@@ -284,6 +294,8 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     alloc((void **)&x->pull_hdr, (size_t)C * sizeof(tlc_header));
     alloc((void **)&x->d_status, 256);
     alloc((void **)&x->flags, 2 * x->W * sizeof(unsigned long long));
+    alloc((void **)&x->d_epoch, sizeof(unsigned long long));
+    if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->d_epoch, 0, sizeof(unsigned long long)));
     alloc((void **)&x->d_peer_flags, x->W * sizeof(unsigned long long *));
     if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->flags, 0, 2 * x->W * sizeof(unsigned long long)));
     if (rc == TLC_OK) {
@@ -388,11 +400,18 @@ int tlc_exchange_ipc_open(tlc_exchange *x, const void *all) {
     return rc;
 }
 
+// Stream capture (CUDA graphs) is supported by the peer-memory transport only;
+// the NCCL transport refuses it instead of hanging in capture.
+static int capture_ok(const tlc_exchange *x, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return TLC_ERR_CUDA;
+    return (cs != cudaStreamCaptureStatusNone && !x->p2p) ? TLC_ERR_ARG : TLC_OK;
+}
+
 static int flag_barrier(tlc_exchange *x, int slot, cudaStream_t st) {
-    x->epoch++;
     KernelScope ks(kK7, st);
     tlc_flag_barrier_kernel<<<1, 32 * ((x->W + 31) / 32), 0, st>>>(x->d_peer_flags, x->flags, x->me, x->W, slot,
-                                                                    x->epoch);
+                                                                    x->d_epoch);
     return cuda_ok(cudaPeekAtLastError());
 }
 
@@ -470,6 +489,7 @@ uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction) {
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream) {
     if (!x || !grads || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc0 = capture_ok(x, st)) return rc0;
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
     for (int i = 0; i < T; i++)
         if (!grads[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
@@ -530,6 +550,7 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream) {
     if (!x || !outs || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc0 = capture_ok(x, st)) return rc0;
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
     for (int i = 0; i < T; i++)
         if (!outs[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;

@@ -1,7 +1,8 @@
 """The NCCL exchange (tlc_exchange_push / tlc_exchange_pull) vs the W-virtual-rank
 oracle (oracle/exchange.py, X1-X6): owners' means, every rank's outputs and every
-push / pull error buffer, bit for bit.  W = 1 runs in-process; W = 2, 4 spawn one
-process per GPU when the box has them."""
+push / pull error buffer, bit for bit, eagerly and (peer-memory transport) replayed
+from CUDA graphs.  W = 1 runs in-process; W = 2, 4 spawn one process per GPU when the
+box has them."""
 import os
 import socket
 
@@ -21,8 +22,10 @@ def _grads(r, step, sizes=SIZES):
     return [synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
 
 
-def _run_rank(rank, world, steps, sizes=SIZES, p2p=False):
-    """One rank's exchange; returns per-step means (owned flat) and final state."""
+def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False):
+    """One rank's exchange; returns per-step means (owned flat) and final state.
+    graph=True: step 0 runs eagerly (it uploads the descriptor tables), then push and
+    pull are captured once as CUDA graphs over fixed gradient buffers and replayed."""
     import torch
 
     import paper_1802_07389_b200 as T
@@ -31,14 +34,29 @@ def _run_rank(rank, world, steps, sizes=SIZES, p2p=False):
     comm = T.Comm(rank, world, dev)
     x = T.Exchange(comm, sizes, p2p=p2p)
     outs = [torch.zeros(n, device=dev) for n in sizes]
+    gs = [torch.empty(n, device=dev) for n in sizes]
     owned_per_step = []
+    gpush = gpull = None
     for step in range(steps):
-        g = [torch.from_numpy(a).to(dev) for a in _grads(rank, step, sizes)]
-        x.push(g, S)
+        for b, a in zip(gs, _grads(rank, step, sizes)):
+            b.copy_(torch.from_numpy(a))
+        if gpush is None:
+            x.push(gs, S)
+        else:
+            gpush.replay()
         torch.cuda.synchronize()
         owned_per_step.append(x.owned.cpu().numpy().copy())
-        x.pull(outs, S)          # delta = mean (R18)
+        if gpull is None:
+            x.pull(outs, S)      # delta = mean (R18)
+        else:
+            gpull.replay()
         torch.cuda.synchronize()
+        if graph and gpush is None:
+            gpush, gpull = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gpush, capture_error_mode="thread_local"):
+                x.push(gs, S)
+            with torch.cuda.graph(gpull, capture_error_mode="thread_local"):
+                x.pull(outs, S)
     assert x.status() == 0
     res = {"ctx": x.contexts(), "owned": owned_per_step, "outs": [o.cpu().numpy() for o in outs],
            "push_err": x.push_err.cpu().numpy().copy(), "pull_err": x.pull_err.cpu().numpy().copy()}
@@ -74,15 +92,15 @@ def _check(world, results, sizes=SIZES, steps=STEPS):
             assert np.array_equal(res["outs"][t].view(np.uint32), outs[r][t].view(np.uint32)), ("out", r, t)
 
 
-@pytest.mark.parametrize("p2p", [False, True])
-def test_exchange_w1_in_process(p2p):
+@pytest.mark.parametrize("p2p,graph", [(False, False), (True, False), (True, True)])
+def test_exchange_w1_in_process(p2p, graph):
     import torch
 
     assert torch.cuda.is_available()
-    _check(1, [_run_rank(0, 1, STEPS, p2p=p2p)])
+    _check(1, [_run_rank(0, 1, STEPS, p2p=p2p, graph=graph)])
 
 
-def _mp_worker(rank, world, port, q, p2p):
+def _mp_worker(rank, world, port, q, p2p, graph=False):
     import torch
     import torch.distributed as dist
 
@@ -90,15 +108,15 @@ def _mp_worker(rank, world, port, q, p2p):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        res = _run_rank(rank, world, STEPS, p2p=p2p)
+        res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("p2p,graph", [(False, False), (True, False), (True, True)])
 @pytest.mark.parametrize("world", [2, 4])
-def test_exchange_multi_gpu(world, p2p):
+def test_exchange_multi_gpu(world, p2p, graph):
     import torch
     import torch.multiprocessing as mp
 
@@ -110,7 +128,7 @@ def test_exchange_multi_gpu(world, p2p):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p)) for r in range(world)]
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
@@ -118,3 +136,24 @@ def test_exchange_multi_gpu(world, p2p):
         p.join(timeout=120)
         assert p.exitcode == 0
     _check(world, results)
+
+
+def test_nccl_transport_refuses_capture():
+    """The NCCL transport returns TLC_ERR_ARG on a capturing stream (no hang)."""
+    import torch
+
+    import paper_1802_07389_b200 as T
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comm = T.Comm(0, 1, dev)
+    x = T.Exchange(comm, SIZES, p2p=False)
+    gs = [torch.zeros(n, device=dev) for n in SIZES]
+    x.push(gs, S)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(T.TlcError):
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            x.push(gs, S)
+    torch.cuda.synchronize()
+    x.close()
+    comm.close()
