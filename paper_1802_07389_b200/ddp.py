@@ -54,7 +54,7 @@ class TLCHookState:
         self.comm.close()
 
 
-def tlc_hook(state: TLCHookState, bucket) -> torch.futures.Future:
+def tlc_hook(state: TLCHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP comm hook: 3LC-compressed parameter-server exchange of one bucket."""
     grad = bucket.buffer()
     if grad.dtype != torch.float32 or not grad.is_cuda:
