@@ -26,15 +26,6 @@ namespace tlc {
 constexpr int kK4Threads = kScanThreads;
 constexpr int kK4Seg = 16;
 
-// Expansion length of the 4 payload bytes of a word: each byte b counts
-// len(b) = b >= 243 ? b - 241 : 1.  Bytes >= 243 are the ones whose low seven
-// bits plus 13 carry into bit 7 while bit 7 is set (SWAR, no cross-byte carry).
-__device__ __forceinline__ uint32_t word_len(uint32_t w) {
-    const uint32_t hi = w & ((w & 0x7f7f7f7fu) + 0x0d0d0d0du) & 0x80808080u;   // bit 7 of codes >= 243
-    const uint32_t m = (hi >> 7) * 0xffu;                                        // their bytes
-    return 4u + __dp4a(w & m, 0x01010101u, 0u) - 242u * (uint32_t)__popc(hi);
-}
-
 // Payload bytes [pos, min(pos+16, hi)) as 4 words and their total expansion
 // length; n = the number of bytes present.
 __device__ __forceinline__ uint32_t pay16(const uint8_t *__restrict__ p, uint64_t pos, uint64_t hi,

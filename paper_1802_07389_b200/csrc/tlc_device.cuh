@@ -172,66 +172,6 @@ __host__ __device__ __forceinline__ uint32_t byte_at(const uint32_t *w, int m) {
     return (w[m >> 2] >> (8 * (m & 3))) & 0xffu;
 }
 
-// Run summary of bytes [0, len) of one segment held as NW little-endian words;
-// bytes at positions >= len must be 121 (the loaders pad with 0x79).
-template <int NW>
-__host__ __device__ __forceinline__ RunSum segment_summary(const uint32_t (&w)[NW], int len) {
-    constexpr int N = 4 * NW;
-    RunSum s = run_identity();
-    if (len <= 0) return s;
-    bool all = true;
-#pragma unroll
-    for (int k = 0; k < NW; k++) all &= (w[k] == 0x79797979u);
-    if (all) {
-        s.v = (uint64_t)(len / (int)kMaxRun);
-        s.r0 = (uint32_t)(len % (int)kMaxRun);
-        return s;
-    }
-    uint32_t lead = 0, cnt = 0, c = 0;
-    bool in_lead = true;
-#pragma unroll
-    for (int m = 0; m < N; m++) {
-        if (m >= len) break;
-        const uint32_t b = byte_at(w, m);
-        if (in_lead) {
-            if (b == kZeroGroup) { lead++; continue; }
-            in_lead = false;
-        }
-        if (b != kZeroGroup) {
-            cnt += (c > 0) + 1;
-            c = 0;
-        } else if (++c == kMaxRun) {
-            cnt++;
-            c = 0;
-        }
-    }
-    s.mix = true;
-    s.r0 = lead % kMaxRun;
-    s.v = cnt + lead / kMaxRun;
-    s.tr = c;
-    return s;
-}
-
-// Emit the ZRE bytes of one segment entered with carry c at payload offset
-// `off`; on return c is the carry out and off the next offset.
-template <int NW>
-__host__ __device__ __forceinline__ void segment_emit(const uint32_t (&w)[NW], int len, uint32_t &c,
-                                                      uint8_t *payload, uint64_t &off) {
-#pragma unroll
-    for (int m = 0; m < 4 * NW; m++) {
-        if (m >= len) break;
-        const uint32_t b = byte_at(w, m);
-        if (b != kZeroGroup) {
-            if (c > 0) payload[off++] = run_code(c);
-            payload[off++] = (uint8_t)b;
-            c = 0;
-        } else if (++c == kMaxRun) {
-            payload[off++] = run_code(kMaxRun);
-            c = 0;
-        }
-    }
-}
-
 // ---------------------------------------------------------------- 32-byte segments as bit masks
 // The zero-run encoder only needs to know which quartic bytes are literals
 // (!= 121): a 32-byte segment becomes a 32-bit mask and its run summary and
@@ -313,38 +253,6 @@ __host__ __device__ __forceinline__ RunSum mask_summary(uint32_t mask, int len) 
     return s;
 }
 
-__device__ __forceinline__ unsigned long long shfl_up64(unsigned long long v, int d) {
-    return __shfl_up_sync(0xffffffffu, v, d);
-}
-__device__ __forceinline__ unsigned long long shfl_down64(unsigned long long v, int d) {
-    return __shfl_down_sync(0xffffffffu, v, d);
-}
-
-// ---------------------------------------------------------------- warp-level helpers
-// lane l's item precedes lane l+1's
-__device__ __forceinline__ RunSum warp_reduce_runs(const RunSum &x) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long v = pack(x);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = shfl_down64(v, d);
-        if (lane + d < 32) v = pack(compose(unpack(v), unpack(o)));
-    }
-    return unpack(__shfl_sync(0xffffffffu, v, 0));
-}
-
-__device__ __forceinline__ RunSum warp_excl_scan_runs(const RunSum &x, RunSum &total) {
-    const int lane = threadIdx.x & 31;
-    unsigned long long v = pack(x);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long y = shfl_up64(v, d);
-        if (lane >= d) v = pack(compose(unpack(y), unpack(v)));
-    }
-    total = unpack(__shfl_sync(0xffffffffu, v, 31));
-    const unsigned long long ex = shfl_up64(v, 1);
-    return lane == 0 ? run_identity() : unpack(ex);
-}
 
 // ---------------------------------------------------------------- warp rows of 32 x 32 bytes
 // A warp row: lane l holds the bytes [32 l, 32 l + len_l) of a row (len_l = 32
@@ -493,6 +401,20 @@ __device__ __forceinline__ void raise_format(tlc_header *hdr) {
 // expansion length of a payload byte (inverse of P:545-546)
 __host__ __device__ __forceinline__ uint32_t zre_len(uint32_t b) { return b >= kFirstRunCode ? b - 241u : 1u; }
 
+// Expansion length of the 4 payload bytes of a word, SWAR: bytes >= 243 are the
+// ones whose low seven bits plus 13 carry into bit 7 while bit 7 is set (no carry
+// crosses a byte: 127 + 13 < 256); their excess b - 242 is summed with one dp4a.
+__host__ __device__ __forceinline__ uint32_t word_len(uint32_t w) {
+    const uint32_t hi = w & ((w & 0x7f7f7f7fu) + 0x0d0d0d0du) & 0x80808080u;   // bit 7 of codes >= 243
+    const uint32_t x = w & ((hi >> 7) * 0xffu);                                   // their bytes
+#ifdef __CUDA_ARCH__
+    return 4u + __dp4a(x, 0x01010101u, 0u) - 242u * (uint32_t)__popc(hi);
+#else
+    const uint32_t sum = (x & 0xffu) + ((x >> 8) & 0xffu) + ((x >> 16) & 0xffu) + (x >> 24);
+    return 4u + sum - 242u * (uint32_t)__builtin_popcount(hi);
+#endif
+}
+
 // Header checks of the decoder: compressor status OK, n matches, 1 <= Z <= P,
 // Z == P without ZRE, and M finite and >= +0 (Eq. 1, R6; anything else R21).
 __device__ __forceinline__ bool header_valid(const tlc_header *hdr, uint64_t n) {
@@ -504,101 +426,14 @@ __device__ __forceinline__ bool header_valid(const tlc_header *hdr, uint64_t n) 
            (Mb >> 31) == 0 && Mb < 0x7f800000u;
 }
 
-// ---------------------------------------------------------------- block-level helpers
-// (blockDim.x == 256, 8 warps; thread t's item precedes thread t+1's)
-constexpr int kScanThreads = 256;
+// ---------------------------------------------------------------- chunked scans
+constexpr int kScanThreads = 256;                   // K4's block; K3 has 8 scanning warps + 1
 constexpr int kScanWarps = kScanThreads / 32;
-
-// In-order reduction of one RunSum per thread; every thread gets the total.
-__device__ __forceinline__ RunSum block_reduce_runs(const RunSum &x, unsigned long long *s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long v = pack(x);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = shfl_down64(v, d);
-        if (lane + d < 32) v = pack(compose(unpack(v), unpack(o)));
-    }
-    if (lane == 0) s_warp[warp] = v;
-    __syncthreads();
-    RunSum r = run_identity();
-#pragma unroll
-    for (int w = 0; w < kScanWarps; w++) r = compose(r, unpack(s_warp[w]));
-    __syncthreads();
-    return r;
-}
-
-// In-order exclusive scan; `total` receives the block aggregate in every thread.
-__device__ __forceinline__ RunSum block_excl_scan_runs(const RunSum &x, unsigned long long *s_warp,
-                                                       RunSum &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long v = pack(x);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long y = shfl_up64(v, d);
-        if (lane >= d) v = pack(compose(unpack(y), unpack(v)));
-    }
-    unsigned long long ex = shfl_up64(v, 1);
-    if (lane == 0) ex = pack(run_identity());
-    if (lane == 31) s_warp[warp] = v;
-    __syncthreads();
-    RunSum pre = run_identity(), tot = run_identity();
-#pragma unroll
-    for (int w = 0; w < kScanWarps; w++) {
-        const RunSum ww = unpack(s_warp[w]);
-        if (w < warp) pre = compose(pre, ww);
-        tot = compose(tot, ww);
-    }
-    __syncthreads();
-    total = tot;
-    return compose(pre, unpack(ex));
-}
-
-// Sum versions for the decoder's expansion lengths.
-__device__ __forceinline__ uint64_t block_reduce_sum(uint64_t x, unsigned long long *s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
-    if (lane == 0) s_warp[warp] = x;
-    __syncthreads();
-    uint64_t r = 0;
-#pragma unroll
-    for (int w = 0; w < kScanWarps; w++) r += s_warp[w];
-    __syncthreads();
-    return r;
-}
-
-__device__ __forceinline__ uint64_t block_excl_scan_sum(uint64_t x, unsigned long long *s_warp,
-                                                        uint64_t &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t v = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += y;
-    }
-    if (lane == 31) s_warp[warp] = v;
-    __syncthreads();
-    uint64_t pre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kScanWarps; w++) {
-        pre += (w < warp) ? s_warp[w] : 0ull;
-        tot += s_warp[w];
-    }
-    __syncthreads();
-    total = tot;
-    return pre + v - x;
-}
 
 constexpr unsigned long long kReady = 1ull << 62;
 
 constexpr unsigned long long kPrefix = 1ull << 63;   // the state holds the inclusive prefix
 constexpr unsigned long long kStateFlags = kReady | kPrefix;
-
-__device__ __forceinline__ unsigned long long wait_ready(const unsigned long long *p) {
-    unsigned long long w;
-    while (!((w = ld_relaxed_u64(p)) & kStateFlags)) __nanosleep(64);
-    return w;
-}
 
 // Monoids of the chunked scans, on packed 62-bit values (identity packs to 0).
 struct SumOp {

@@ -181,3 +181,6 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
     }
     return total;
 }
+
+// K4's SWAR expansion length of a payload word (tlc_device.cuh word_len), host form
+extern "C" uint32_t tlc_word_len(uint32_t w) { return word_len(w); }

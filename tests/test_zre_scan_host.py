@@ -37,6 +37,7 @@ def sim():
         assert np.all(out[z:] == 0xEE), "bytes emitted past the computed payload length"
         return out[:z]
 
+    run.lib = L
     return run
 
 
@@ -64,3 +65,28 @@ def test_scan_matches_oracle_zre(sim, threads):  # threads = warps per CTA
         for nchunks in (1, 2, 3, 7, 64):
             got = sim(B, threads, nchunks)
             assert got.tolist() == ref.tolist(), (threads, nchunks, i, B.size)
+
+
+def test_word_len_swar_matches_bytewise(sim):
+    """K4 sums expansion lengths four bytes at a time (word_len): every byte value in
+    every lane position, and random words, against the per-byte definition
+    len(b) = b >= 243 ? b - 241 : 1 (inverse of P:545-546)."""
+    import ctypes
+
+    L = sim.lib
+    L.tlc_word_len.restype = ctypes.c_uint32
+    L.tlc_word_len.argtypes = [ctypes.c_uint32]
+
+    def ref(w):
+        return sum((b - 241 if b >= 243 else 1) for b in ((w >> (8 * i)) & 0xFF for i in range(4)))
+
+    for b in range(256):
+        for fill in (0, 121, 242, 243, 255):
+            for pos in range(4):
+                w = 0
+                for i in range(4):
+                    w |= (b if i == pos else fill) << (8 * i)
+                assert L.tlc_word_len(w) == ref(w), (b, fill, pos)
+    g = np.random.default_rng(5)
+    for w in g.integers(0, 2**32, 20000, dtype=np.uint64):
+        assert L.tlc_word_len(int(w)) == ref(int(w))
