@@ -22,9 +22,9 @@ def declared_symbols():
 
 @pytest.fixture(scope="module")
 def T():
-    from paper_1802_07389_b200 import build as B
+    import __graft_entry__
 
-    B.build()
+    __graft_entry__.build()        # builds libtlc.so on a fresh checkout (no package import first)
     import paper_1802_07389_b200 as T
 
     return T
