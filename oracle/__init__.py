@@ -56,6 +56,12 @@ def lib():
             "tlc_o_zre_decode": (I, [P, U64, P, U64]),
             "tlc_o_compress": (I, [P, P, U64, F, I, P, U64, P, P]),
             "tlc_o_decompress": (I, [P, U64, I, F, U64, P, I]),
+            "tlc_o_philox4x32_10": (None, [P, P, P]),
+            "tlc_o_stoch_word": (ctypes.c_uint32, [U64, U64, U64]),
+            "tlc_o_stoch_quantize": (I, [P, U64, U64, U64, P, P]),
+            "tlc_o_stoch_compress": (I, [P, U64, U64, U64, I, P, U64, P, P]),
+            "tlc_o_int8_compress": (I, [P, U64, P, P]),
+            "tlc_o_int8_decompress": (None, [P, U64, F, P, I]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -190,3 +196,60 @@ def roundtrip(t, buf, s, use_zre=True):
     c = compress(t, buf, s, use_zre)
     st, out = decompress(c.payload, use_zre, c.M, c.n)
     return c, out
+
+
+# --------------------------------------------------------------------------- compared designs (Sec. 5.1)
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 block (Random123): four 32-bit counter words, two key words."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.empty(4, dtype=np.uint32)
+    lib().tlc_o_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def stoch_word(seed: int, step: int, e: int) -> int:
+    """The random word of element e at (seed, step) (reading R22)."""
+    return int(lib().tlc_o_stoch_word(seed, step, e))
+
+
+def stoch_quantize(t, seed: int, step: int):
+    """Stochastic 3-value quantization; returns (status, m, q)."""
+    t = _f32(t)
+    q = np.empty(t.size, dtype=np.int8)
+    m = ctypes.c_float(0)
+    st = lib().tlc_o_stoch_quantize(_p(t), t.size, seed, step, _p(q), ctypes.byref(m))
+    return st, np.float32(m.value), q
+
+
+def stoch_compress(t, seed: int, step: int, use_zre=False):
+    """"Stoch 3-value + QE": stochastic trits, quartic encoding, optional ZRE.
+    Decoded by decompress(payload, use_zre, M, n)."""
+    t = _f32(t)
+    n = t.size
+    cap = max(quartic_len(n), 1)
+    payload = np.empty(cap, dtype=np.uint8)
+    M, ln = ctypes.c_float(0), ctypes.c_uint64(0)
+    st = lib().tlc_o_stoch_compress(_p(t), n, seed, step, int(bool(use_zre)), _p(payload), cap,
+                                    ctypes.byref(M), ctypes.byref(ln))
+    if st != OK:
+        return Compressed(st, np.float32(0), n, use_zre, payload[:0].copy())
+    return Compressed(st, np.float32(M.value), n, use_zre, payload[: ln.value].copy())
+
+
+def int8_compress(t):
+    """"8-bit int"; returns (status, scale, codes int8[n])."""
+    t = _f32(t)
+    codes = np.empty(max(t.size, 1), dtype=np.int8)
+    sc = ctypes.c_float(0)
+    st = lib().tlc_o_int8_compress(_p(t), t.size, _p(codes), ctypes.byref(sc))
+    return st, np.float32(sc.value), codes[: t.size].copy()
+
+
+def int8_decompress(codes, scale, out=None, accumulate=False):
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    if out is None:
+        out = np.zeros(codes.size, dtype=np.float32)
+    assert out.dtype == np.float32 and out.flags.c_contiguous and out.size == codes.size
+    lib().tlc_o_int8_decompress(_p(codes), codes.size, ctypes.c_float(scale), _p(out), int(bool(accumulate)))
+    return out

@@ -281,3 +281,159 @@ int tlc_o_decompress(const uint8_t *payload, uint64_t len, int zre_flag, float M
     free(B);
     return st;
 }
+
+/* ========================================================================= */
+/* Compared designs of Sec. 5.1 that share the 3LC kernels        */
+/* (SURVEY 8(f) NEXT-3): "Stoch 3-value + QE" and "8-bit int".  Same rules as */
+/* above: fp32, one IEEE operation per source operation, whole-tensor steps.  */
+/* ========================================================================= */
+
+/* Philox4x32-10, the counter-based generator of Salmon, Moraes, Dror, Shaw,  */
+/* "Parallel random numbers: as easy as 1, 2, 3" (SC'11), Random123 reference:*/
+/* ten rounds of                                                              */
+/*   (c0,c1,c2,c3) <- (hi(B*c2)^c1^k0, lo(B*c2), hi(A*c0)^c3^k1, lo(A*c0))    */
+/* with A = 0xD2511F53, B = 0xCD9E8D57, the key bumped by (0x9E3779B9,        */
+/* 0xBB67AE85) after every round.  Pinned by the Random123 known-answer       */
+/* vectors (tests/golden/philox_kat.json) and by triton's Philox.             */
+void tlc_o_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; r++) {
+        uint64_t pa = (uint64_t)0xD2511F53u * c0;
+        uint64_t pb = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t n0 = (uint32_t)(pb >> 32) ^ c1 ^ k0;
+        uint32_t n1 = (uint32_t)pb;
+        uint32_t n2 = (uint32_t)(pa >> 32) ^ c3 ^ k1;
+        uint32_t n3 = (uint32_t)pa;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* The random word drawn for element e of a tensor at (seed, step) -- reading */
+/* R22: word e mod 4 of Philox4x32-10 at counter (e/4 as two 32-bit halves,   */
+/* step as two halves) under key (seed low half, seed high half).             */
+uint32_t tlc_o_stoch_word(uint64_t seed, uint64_t step, uint64_t e)
+{
+    uint64_t b = e / 4;
+    uint32_t ctr[4] = {(uint32_t)b, (uint32_t)(b >> 32), (uint32_t)step, (uint32_t)(step >> 32)};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    tlc_o_philox4x32_10(ctr, key, out);
+    return out[e % 4];
+}
+
+/* Stochastic 3-value quantization ("outputs randomized quantization */
+/* values whose expectation matches their input value"; "similar to */
+/* TernGrad (but without gradient clipping)", no sparsity multiplier and no   */
+/* error accumulation buffer).  m = max|t|; element x becomes sign(x) with    */
+/* probability |x|/m, else 0.  The draw (R22): U = (w >> 8)*2^-24 */
+/* in [0,1) from the element's word w, p = fl(|x| / m), q = sign(x) iff U < p.*/
+/* E[m*q] = x up to the 2^-24 grid of U.  m == 0 gives all zeros.             */
+int tlc_o_stoch_quantize(const float *t, uint64_t n, uint64_t seed, uint64_t step, int8_t *q, float *m_out)
+{
+    float m = 0.0f;
+    for (uint64_t i = 0; i < n; i++) {
+        if (isnan(t[i]) || isinf(t[i]))
+            return O_ERR_NONFINITE;
+        if (fabsf(t[i]) > m)
+            m = fabsf(t[i]);
+    }
+    for (uint64_t i = 0; i < n; i++) {
+        if (m == 0.0f) {
+            q[i] = 0;
+            continue;
+        }
+        uint32_t w = tlc_o_stoch_word(seed, step, i);
+        float U = (float)(w >> 8) * 0x1p-24f;
+        float p = fabsf(t[i]) / m;
+        if (U < p)
+            q[i] = t[i] > 0.0f ? 1 : -1;
+        else
+            q[i] = 0;
+    }
+    *m_out = m;
+    return O_OK;
+}
+
+/* "Stoch 3-value + QE": the ternary tensor goes through the same */
+/* quartic encoding (Sec. 3.2), optionally followed by zero-run encoding; the */
+/* receiver decodes it with tlc_o_decompress (M = m).                         */
+int tlc_o_stoch_compress(const float *t, uint64_t n, uint64_t seed, uint64_t step, int use_zre,
+                         uint8_t *payload, uint64_t cap, float *M_out, uint64_t *len_out)
+{
+    if (n == 0)
+        return O_ERR_ARG;
+    uint64_t P = tlc_o_quartic_len(n);
+    if (cap < P)
+        return O_ERR_ARG;
+    int8_t *q = (int8_t *)malloc(n);
+    float m = 0.0f;
+    int st = tlc_o_stoch_quantize(t, n, seed, step, q, &m);
+    if (st != O_OK) {
+        free(q);
+        return st;
+    }
+    uint8_t *B = (uint8_t *)malloc(P);
+    tlc_o_quartic_encode(q, n, B);
+    uint64_t len;
+    if (use_zre) {
+        len = tlc_o_zre_encode(B, P, payload);
+    } else {
+        memcpy(payload, B, P);
+        len = P;
+    }
+    *M_out = m;
+    *len_out = len;
+    free(B);
+    free(q);
+    return O_OK;
+}
+
+/* "8-bit int": "255 distinct values ([-127,127], leaving -128    */
+/* unused)".  S:346-354: scale = max|t| / 127 (0 if max = 0), codes =         */
+/* round(t / scale) clamped to [-127,127], dequant = scale * code.  round()   */
+/* is half away from zero as in Eq. 2 (R1); a scale that underflows to 0 (max */
+/* below 127 * 2^-150) gives all-zero codes, like max = 0 (R23).              */
+int tlc_o_int8_compress(const float *t, uint64_t n, int8_t *codes, float *scale_out)
+{
+    if (n == 0)
+        return O_ERR_ARG;
+    float a = 0.0f;
+    for (uint64_t i = 0; i < n; i++) {
+        if (isnan(t[i]) || isinf(t[i]))
+            return O_ERR_NONFINITE;
+        if (fabsf(t[i]) > a)
+            a = fabsf(t[i]);
+    }
+    float scale = a / 127.0f;
+    for (uint64_t i = 0; i < n; i++) {
+        if (scale == 0.0f) {
+            codes[i] = 0;
+            continue;
+        }
+        float c = roundf(t[i] / scale);
+        if (c > 127.0f)
+            c = 127.0f;
+        if (c < -127.0f)
+            c = -127.0f;
+        codes[i] = (int8_t)c;
+    }
+    *scale_out = scale;
+    return O_OK;
+}
+
+/* 8-bit dequantization: mode 0 writes scale * code; mode 1 adds it where     */
+/* code != 0 (the accumulate rule R16 of the 3LC decoder).                    */
+void tlc_o_int8_decompress(const int8_t *codes, uint64_t n, float scale, float *out, int mode)
+{
+    for (uint64_t i = 0; i < n; i++) {
+        if (mode == 0)
+            out[i] = scale * (float)codes[i];
+        else if (codes[i] != 0)
+            out[i] = out[i] + scale * (float)codes[i];
+    }
+}
