@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--xchg", choices=["p2p", "nccl"], default="p2p",
                     help="exchange transport: peer-memory kernels over NVLink, or NCCL send/recv")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-codecs", action="store_true",
+                    help="skip the compared-design codecs side measurement (Stoch 3-value + QE, 8-bit int)")
     return ap.parse_args()
 
 
@@ -282,6 +284,82 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
 
 # ------------------------------------------------------------------ exchange step (row e)
 NVLINK_GBS = 770.0   # measured peer copy per direction per GPU (B200_PROFILING.md)
+
+
+def measure_codecs(T, dev, ts, steps=20, warmup=3):
+    """Side measurement: the paper's compared designs that share the 3LC
+    kernels, on the same n-element N(0,1) tensors as the headline: "Stoch 3-value + QE"
+    (QE only as in the paper, and with ZRE) and "8-bit int".  A step
+    is one compress + decompress; value = fp32-input GB/s.  Per-kernel device times come from
+    the library's CUDA events on the launching stream (a second, profiled pass)."""
+    import torch
+
+    n = ts[0].numel()
+    P = (n + 4) // 5
+    stream = torch.cuda.current_stream(dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    payload = torch.empty(T.tlc_max_payload_bytes(n), dtype=torch.uint8, device=dev)
+    hdr = T.new_header(dev)
+    ws_c = torch.empty(T.tlc_compress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    ws_d = torch.empty(T.tlc_decompress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    codes = torch.empty(n, dtype=torch.int8, device=dev)
+    ws_8 = torch.empty(T.tlc_int8_workspace_bytes(n), dtype=torch.uint8, device=dev)
+
+    def stoch_step(k, zre):
+        T.tlc_stoch_compress(ts[k % len(ts)], 7, k, zre, payload, hdr, ws_c, stream)
+        T.tlc_decompress(payload, hdr, n, out, T.TLC_MODE_OVERWRITE, ws_d, stream)
+
+    def int8_step(k):
+        T.tlc_int8_compress(ts[k % len(ts)], codes, hdr, ws_8, stream)
+        T.tlc_int8_decompress(codes, hdr, n, out, T.TLC_MODE_OVERWRITE, stream)
+
+    def timed(fn):
+        for k in range(warmup):
+            fn(k)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(steps):
+            fn(k)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        T.tlc_prof_collect()
+        T.tlc_prof_enable(True)
+        for k in range(steps):
+            fn(k)
+        T.tlc_prof_enable(False)
+        prof = T.tlc_prof_collect()
+        h = T.parse_header(hdr)
+        return ms, {k: v[1] / max(v[0], 1) for k, v in prof.items()}, h
+
+    peak, _ = load_peaks()
+    res = []
+    for zre in (False, True):
+        ms, kern, h = timed(lambda k: stoch_step(k, zre))
+        Z = h["payload_len"]
+        alg = {"k1_absmax": 4.0 * n, "k2s_stoch_qe": 4.0 * n + P, "k3_zre": float(P + Z) if zre else 0.0,
+               "k4_zre_scan": float(Z), "k5_expand_dequant": 4.0 * n + Z}
+        dom = "k2s_stoch_qe"
+        ach = alg[dom] / (kern[dom] / 1e3) / 1e9
+        res.append({"design": "Stoch 3-value + QE" + (" + ZRE" if zre else ""), "cite": "P:629-632, R22",
+                    "value": 4.0 * n / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+                    "bits_per_value": 8.0 * Z / n, "status": h["status"],
+                    "kernel_ms": {k: round(v, 5) for k, v in kern.items()},
+                    "roofline": {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                 "frac": ach / peak, "alg_bytes_formula": "4n + ceil(n/5)"}})
+    ms, kern, h = timed(int8_step)
+    alg = {"k1_absmax": 4.0 * n, "kq8_int8_quant": 5.0 * n, "kd8_int8_dequant": 5.0 * n}
+    doms = {k: alg[k] / (kern[k] / 1e3) / 1e9 for k in ("kq8_int8_quant", "kd8_int8_dequant")}
+    res.append({"design": "8-bit int", "cite": "P:624-627, R23", "value": 4.0 * n / (ms / 1e3) / 1e9,
+                "unit": "GB/s", "ms_per_step": ms, "bits_per_value": 8.0, "status": h["status"],
+                "kernel_ms": {k: round(v, 5) for k, v in kern.items()},
+                "roofline": {"kernel": "kq8_int8_quant", "bound": "hbm", "achieved": doms["kq8_int8_quant"],
+                             "peak": peak, "unit": "GB/s", "frac": doms["kq8_int8_quant"] / peak,
+                             "alg_bytes_formula": "5n (read t, write codes)",
+                             "dequant_achieved": doms["kd8_int8_dequant"]}})
+    return {"workload": f"n = {n:,} N(0,1) fp32 (same tensors as the headline), compress + decompress per step",
+            "steps": steps, "designs": res}
 
 
 def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True, e2e_steps=0):
@@ -626,6 +704,10 @@ def run_tlc(args):
                "value": xval, "unit": "GB/s", "ms_per_step": xms, "kernel_ms_per_step": r["kernel_ms"],
                "status": r["status"]}
 
+    codecs = None
+    if rank == 0 and world == 1 and not args.no_codecs:
+        codecs = measure_codecs(T, dev, ts)
+
     c2 = None
     if rank == 0 and not args.no_c2:
         c2 = [measure_resnet110(T, dev, sv) for sv in (1.0, 1.75, 1.9)]
@@ -657,6 +739,7 @@ def run_tlc(args):
             "gpu_launches": gpu_launches,
             "c2_resnet110": c2,
             "xchg_w1": xw1,
+            "next3_codecs": codecs,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -64,6 +64,7 @@ typedef struct tlc_header {
 } tlc_header;
 
 #define TLC_FLAG_ZRE 1u
+#define TLC_FLAG_INT8 2u       /* payload is 8-bit int codes (tlc_int8_compress)  */
 #define TLC_MODE_OVERWRITE 0   /* out  = M*q                     (Eq. 3)     */
 #define TLC_MODE_ACCUMULATE 1  /* out += M*q where q != 0        (reading R16)      */
 
@@ -130,6 +131,38 @@ int tlc_compress(const float *t, float *err, uint64_t n, float s, int use_zre,
  */
 int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *out,
                    int mode, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Compared designs of the paper's evaluation (Sec. 5.1) that share
+ * the 3LC kernels.  Same conventions as above.
+ *
+ * tlc_stoch_compress -- "Stoch 3-value + QE": stochastic 3-value
+ *   quantization "similar to TernGrad (but without gradient clipping)" -- each
+ *   element x becomes sign(x) with probability |x|/m, m = max|t| (P:412-416,
+ *   expectation = input), no sparsity multiplier, no error buffer -- then the
+ *   3LC quartic encoding (1.6 bits/value) and, if use_zre, zero-run encoding.
+ *   The draws are a pure function of (seed, step, element index): reading R22
+ *   of DESIGN.md (Philox4x32-10, counter (e/4, step), key seed, word e%4;
+ *   q = sign(x) iff (w>>8)*2^-24 < fl(|x|/m)).  Decode with tlc_decompress
+ *   (hdr->M = m).  t: fp32[n] in; payload: u8[payload_cap >= ceil(n/5)] out;
+ *   hdr out (status NONFINITE on NaN/Inf in t); ws >= tlc_compress_workspace_bytes(n).
+ *
+ * tlc_int8_compress -- "8-bit int": 255 values [-127,127], -128
+ *   unused.  scale = fl(max|t|/127), code = clamp(round_half_away(fl(t/scale)))
+ *   (reading R23).  codes: int8[n] out; hdr->M = scale, hdr->flags =
+ *   TLC_FLAG_INT8, hdr->payload_len = n; ws >= tlc_int8_workspace_bytes(n).
+ * tlc_int8_decompress -- out = scale*code (mode OVERWRITE) or out += scale*code
+ *   where code != 0 (mode ACCUMULATE).  FORMAT in hdr->status if the header is
+ *   not an int8 header of n elements with a finite scale >= +0.
+ */
+int tlc_stoch_compress(const float *t, uint64_t n, uint64_t seed, uint64_t step, int use_zre,
+                       uint8_t *payload, uint64_t payload_cap, tlc_header *hdr,
+                       void *ws, size_t ws_bytes, void *stream);
+size_t tlc_int8_workspace_bytes(uint64_t n);
+int tlc_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr,
+                      void *ws, size_t ws_bytes, void *stream);
+int tlc_int8_decompress(const int8_t *codes, tlc_header *hdr, uint64_t n, float *out, int mode,
+                        void *stream);
 
 /* ---------------------------------------------------------------------------
  * Batches of tensors (SURVEY 8(a) "small-tensor regime"; BASELINE configs[1]

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libtlc.so")
 TLC_OK, TLC_ERR_ARG, TLC_ERR_NONFINITE, TLC_ERR_RANGE, TLC_ERR_FORMAT, TLC_ERR_CAPACITY, \
     TLC_ERR_CUDA, TLC_ERR_NCCL = range(8)
 TLC_FLAG_ZRE = 1
+TLC_FLAG_INT8 = 2
 TLC_MODE_OVERWRITE, TLC_MODE_ACCUMULATE = 0, 1
 HEADER_BYTES = 32
 
@@ -73,6 +74,10 @@ def _load():
         "tlc_exchange_ipc_handles": (I, [P, P]),
         "tlc_exchange_ipc_open": (I, [P, P]),
         "tlc_exchange_traffic": (I, [P, P]),
+        "tlc_stoch_compress": (I, [P, U64, U64, U64, I, P, U64, P, P, SZ, P]),
+        "tlc_int8_workspace_bytes": (SZ, [U64]),
+        "tlc_int8_compress": (I, [P, U64, P, P, P, SZ, P]),
+        "tlc_int8_decompress": (I, [P, P, U64, P, I, P]),
         "tlc_launch_count": (ctypes.c_ulonglong, []),
         "tlc_prof_enable": (None, [I]),
         "tlc_prof_collect": (I, [P, I]),
@@ -499,3 +504,65 @@ def tlc_prof_collect() -> dict:
 
 compress = tlc_compress
 decompress = tlc_decompress
+
+
+# ------------------------------------------------------------------ compared designs (Sec. 5.1)
+def tlc_stoch_compress(t: torch.Tensor, seed: int, step: int, use_zre: bool = False,
+                       payload: torch.Tensor | None = None, hdr: torch.Tensor | None = None,
+                       ws: torch.Tensor | None = None, stream=None):
+    """"Stoch 3-value + QE": stochastic trits (draws keyed by seed, step and
+    element index; reading R22), quartic encoding, optional ZRE.  Decode with tlc_decompress."""
+    _check_dev("t", t, torch.float32)
+    n = t.numel()
+    cap = tlc_max_payload_bytes(n)
+    if payload is None:
+        payload = torch.empty(max(cap, 1), dtype=torch.uint8, device=t.device)
+    if hdr is None:
+        hdr = new_header(t.device)
+    if ws is None:
+        ws = workspace(tlc_compress_workspace_bytes(n), t.device, "compress")
+    rc = _lib.tlc_stoch_compress(t.data_ptr(), n, int(seed) & (2 ** 64 - 1), int(step) & (2 ** 64 - 1),
+                                 int(bool(use_zre)), payload.data_ptr(), payload.numel(), hdr.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), _stream_ptr(stream))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_stoch_compress")
+    return payload, hdr
+
+
+def tlc_int8_workspace_bytes(n: int) -> int:
+    return int(_lib.tlc_int8_workspace_bytes(n))
+
+
+def tlc_int8_compress(t: torch.Tensor, codes: torch.Tensor | None = None, hdr: torch.Tensor | None = None,
+                      ws: torch.Tensor | None = None, stream=None):
+    """"8-bit int": codes in [-127,127], hdr M = scale (reading R23)."""
+    _check_dev("t", t, torch.float32)
+    n = t.numel()
+    if codes is None:
+        codes = torch.empty(n, dtype=torch.int8, device=t.device)
+    _check_dev("codes", codes, torch.int8)
+    if codes.numel() < n:
+        raise ValueError("codes must hold n elements")
+    if hdr is None:
+        hdr = new_header(t.device)
+    if ws is None:
+        ws = workspace(tlc_int8_workspace_bytes(n), t.device, "int8")
+    rc = _lib.tlc_int8_compress(t.data_ptr(), n, codes.data_ptr(), hdr.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _stream_ptr(stream))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_int8_compress")
+    return codes, hdr
+
+
+def tlc_int8_decompress(codes: torch.Tensor, hdr: torch.Tensor, n: int, out: torch.Tensor | None = None,
+                        mode: int = TLC_MODE_OVERWRITE, stream=None):
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=codes.device)
+    _check_dev("out", out, torch.float32)
+    _check_dev("codes", codes, torch.int8)
+    _check_dev("hdr", hdr, torch.uint8)
+    rc = _lib.tlc_int8_decompress(codes.data_ptr(), hdr.data_ptr(), n, out.data_ptr(), int(mode),
+                                  _stream_ptr(stream))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_int8_decompress")
+    return out

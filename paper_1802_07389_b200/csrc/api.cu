@@ -59,4 +59,40 @@ int tlc_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float *o
     return launch_decompress(payload, hdr, n, out, mode, ws, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int tlc_stoch_compress(const float *t, uint64_t n, uint64_t seed, uint64_t step, int use_zre, uint8_t *payload,
+                       uint64_t payload_cap, tlc_header *hdr, void *ws, size_t ws_bytes, void *stream) {
+    if (!t || !payload || !hdr || !ws || n == 0) return TLC_ERR_ARG;
+    if (n >= (1ull << 42)) return TLC_ERR_ARG;
+    if (payload_cap < tlc_max_payload_bytes(n)) return TLC_ERR_CAPACITY;
+    if (ws_bytes < compress_workspace_bytes(n)) return TLC_ERR_CAPACITY;
+    if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return TLC_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(hdr) & 7u) != 0) return TLC_ERR_ARG;
+    uint64_t scratch = 0;
+    const SegTable T = single_table(t, nullptr, nullptr, payload, hdr, n, scratch);
+    return launch_stoch_compress_table(T, seed, step, use_zre ? 1 : 0, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t tlc_int8_workspace_bytes(uint64_t n) {
+    uint64_t scratch = 0;
+    const SegTable T = single_table(nullptr, nullptr, nullptr, nullptr, nullptr, n ? n : 1, scratch);
+    return ws_layout(T, 0).memset_c;
+}
+
+int tlc_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr, void *ws, size_t ws_bytes,
+                      void *stream) {
+    if (!t || !codes || !hdr || !ws || n == 0) return TLC_ERR_ARG;
+    if (n >= (1ull << 42)) return TLC_ERR_ARG;
+    if (ws_bytes < tlc_int8_workspace_bytes(n)) return TLC_ERR_CAPACITY;
+    if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return TLC_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(hdr) & 7u) != 0) return TLC_ERR_ARG;
+    return launch_int8_compress(t, n, codes, hdr, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tlc_int8_decompress(const int8_t *codes, tlc_header *hdr, uint64_t n, float *out, int mode, void *stream) {
+    if (!codes || !hdr || !out || n == 0) return TLC_ERR_ARG;
+    if (mode != TLC_MODE_OVERWRITE && mode != TLC_MODE_ACCUMULATE) return TLC_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(hdr) & 7u) != 0) return TLC_ERR_ARG;
+    return launch_int8_decompress(codes, hdr, n, out, mode, reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

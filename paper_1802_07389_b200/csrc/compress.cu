@@ -58,6 +58,15 @@ __device__ __forceinline__ void k1_flush(unsigned int m, unsigned int *maxkey, i
     __syncthreads();
 }
 
+// kErr = false: the codecs without an error buffer (stochastic 3-value, 8-bit
+// int) take max|t| -- the same key without the add.
+template <bool kErr>
+__device__ __forceinline__ unsigned int k1_key(float t, float e) {
+    if constexpr (kErr) return absmax_key(t, e);
+    else return __float_as_uint(t) & 0x7fffffffu;
+}
+
+template <bool kErr>
 __global__ void __launch_bounds__(kK1Threads, 1)
 tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
     __shared__ unsigned int s_warp[kK1Threads / 32];
@@ -91,28 +100,31 @@ tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
                     y[k] = ld_l2hint4(e4 + i + k * kK1Threads);
 #else
                     x[k] = ld_stream4(t4 + i + k * kK1Threads);
-                    y[k] = __ldcg(e4 + i + k * kK1Threads);
+                    if constexpr (kErr) y[k] = __ldcg(e4 + i + k * kK1Threads);
+                    else y[k] = x[k];
 #endif
                 }
 #pragma unroll
                 for (int k = 0; k < U; k++) {
-                    m = max(m, absmax_key(x[k].x, y[k].x));
-                    m = max(m, absmax_key(x[k].y, y[k].y));
-                    m = max(m, absmax_key(x[k].z, y[k].z));
-                    m = max(m, absmax_key(x[k].w, y[k].w));
+                    m = max(m, k1_key<kErr>(x[k].x, y[k].x));
+                    m = max(m, k1_key<kErr>(x[k].y, y[k].y));
+                    m = max(m, k1_key<kErr>(x[k].z, y[k].z));
+                    m = max(m, k1_key<kErr>(x[k].w, y[k].w));
                 }
             }
             for (; i < b; i += kK1Threads) {
-                const float4 x = ld_stream4(t4 + i), y = __ldcg(e4 + i);
-                m = max(m, absmax_key(x.x, y.x));
-                m = max(m, absmax_key(x.y, y.y));
-                m = max(m, absmax_key(x.z, y.z));
-                m = max(m, absmax_key(x.w, y.w));
+                const float4 x = ld_stream4(t4 + i);
+                float4 y = x;
+                if constexpr (kErr) y = __ldcg(e4 + i);
+                m = max(m, k1_key<kErr>(x.x, y.x));
+                m = max(m, k1_key<kErr>(x.y, y.y));
+                m = max(m, k1_key<kErr>(x.z, y.z));
+                m = max(m, k1_key<kErr>(x.w, y.w));
             }
             tail = 4 * b;
         }
         for (uint64_t i = tail + threadIdx.x; i < hi; i += kK1Threads)
-            m = max(m, absmax_key(ld_stream(S.t + i), __ldcg(S.err + i)));
+            m = max(m, k1_key<kErr>(ld_stream(S.t + i), kErr ? __ldcg(S.err + i) : 0.0f));
     }
     if (cur >= 0) k1_flush(m, maxkey, cur, s_warp);
 }
@@ -806,7 +818,17 @@ static bool use_bulk() {
     return v == 1;
 }
 
-int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+void launch_absmax(const SegTable &T, unsigned int *maxkey, bool has_err, cudaStream_t st) {
+    KernelScope ks(kK1, st);
+    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n1, (uint64_t)num_sms() * kK1BlocksPerSm));
+    if (has_err) tlc_absmax_kernel<true><<<grid, kK1Threads, 0, st>>>(T, maxkey);
+    else tlc_absmax_kernel<false><<<grid, kK1Threads, 0, st>>>(T, maxkey);
+}
+
+// K1 (max key), then `k2` (the quantizer + quartic pass of the codec), then K3 (ZRE).
+template <class K2Launch>
+static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_err, void *ws, cudaStream_t st,
+                             const K2Launch &k2) {
     const WsLayout L = ws_layout(T, 0);
     char *base = reinterpret_cast<char *>(ws);
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
@@ -815,12 +837,23 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
     uint8_t *scratch = reinterpret_cast<uint8_t *>(base + L.bytes);
     const int sms = num_sms();
     if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
-    {
-        KernelScope ks(kK1, st);
-        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n1, (uint64_t)sms * kK1BlocksPerSm));
-        tlc_absmax_kernel<<<grid, kK1Threads, 0, st>>>(T, maxkey);
+    launch_absmax(T, maxkey, has_err, st);
+    k2(maxkey, scratch);
+    if (use_zre) {
+        KernelScope ks(kK3, st);
+        if (!g_k3_blocks) {
+            cudaFuncSetAttribute(tlc_zre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K3Smem));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, sizeof(K3Smem));
+        }
+        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
+        launch_pdl(tlc_zre_kernel, grid, kK3Threads, sizeof(K3Smem), st, T, maxkey, s, scratch, ctrl, states);
     }
-    {
+    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+    const int sms = num_sms();
+    return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
         KernelScope ks(kK2, st);
         const uint64_t nbulk = use_bulk() ? bulk_tiles(T, use_zre) : 0;
         uint64_t tile_begin = 0;
@@ -842,17 +875,16 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
             const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2 - tile_begin, (uint64_t)sms * tmax(1, g_k2_blocks)));
             launch_pdl(tlc_quant_qe_kernel, grid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin);
         }
-    }
-    if (use_zre) {
-        KernelScope ks(kK3, st);
-        if (!g_k3_blocks) {
-            cudaFuncSetAttribute(tlc_zre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K3Smem));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, sizeof(K3Smem));
-        }
-        const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
-        launch_pdl(tlc_zre_kernel, grid, kK3Threads, sizeof(K3Smem), st, T, maxkey, s, scratch, ctrl, states);
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+    });
+}
+
+// "Stoch 3-value + QE": K1 over t alone (m = max|t|, s = 1), the
+// stochastic quantizer + quartic pass of stoch.cu, K3 when ZRE is asked for.
+int launch_stoch_compress_table(const SegTable &T, uint64_t seed, uint64_t step, int use_zre, void *ws,
+                                cudaStream_t st) {
+    return compress_pipeline(T, 1.0f, use_zre, false, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
+        launch_stoch_qe(T, maxkey, seed, step, use_zre, scratch, st);
+    });
 }
 
 int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,

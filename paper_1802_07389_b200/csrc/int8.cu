@@ -1,0 +1,146 @@
+// int8.cu -- "8-bit int", a compared design of the paper (Sec. 5.1):
+// "255 distinct values ([-127,127], leaving -128 unused)".  Reading R23:
+// scale = fl(max|t| / 127); code = clamp(round_half_away(fl(t / scale)), -127, 127);
+// dequant = fl(scale * code).  No error buffer.
+//
+// Kq8 tlc_int8_quant_kernel: after K1<no err> (max|t|), one streaming pass:
+//     16 elements per thread and step (four 128-bit loads, one 128-bit store of
+//     codes).  Algorithmic bytes 4n read + n written.
+// Kd8 tlc_int8_dequant_kernel: 16 codes per thread (one 128-bit load, four
+//     128-bit stores): n read + 4n written (accumulate: + 4n read).
+// Both are plain HBM streams; grid = SMs x resident CTAs, grid-stride.
+#include "tlc_device.cuh"
+#include "tlc_launch.h"
+
+namespace tlc {
+
+constexpr int kI8Threads = 256;
+
+__device__ __forceinline__ int8_t int8_code(float x, float scale) {
+    if (scale == 0.0f) return 0;                          // max = 0 or an underflowed scale (R23)
+    float c = roundf(__fdiv_rn(x, scale));                // half away from zero (R1)
+    c = fminf(fmaxf(c, -127.0f), 127.0f);                 // -128 unused
+    return (int8_t)(int)c;
+}
+
+__device__ __forceinline__ uint32_t pack4(float4 v, float scale) {
+    return (uint32_t)(uint8_t)int8_code(v.x, scale) | ((uint32_t)(uint8_t)int8_code(v.y, scale) << 8) |
+           ((uint32_t)(uint8_t)int8_code(v.z, scale) << 16) | ((uint32_t)(uint8_t)int8_code(v.w, scale) << 24);
+}
+
+__global__ void __launch_bounds__(kI8Threads)
+tlc_int8_quant_kernel(const float *__restrict__ t, uint64_t n, int8_t *__restrict__ codes, tlc_header *hdr,
+                      const unsigned int *maxkey, int vec) {
+    const unsigned int key = maxkey[0];
+    const unsigned int status = key >= 0x7f800000u ? (unsigned int)TLC_ERR_NONFINITE : (unsigned int)TLC_OK;
+    const float scale = status == TLC_OK ? __fdiv_rn(__uint_as_float(key), 127.0f) : 0.0f;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        hdr->M = scale;
+        hdr->flags = TLC_FLAG_INT8;
+        hdr->n = n;
+        hdr->payload_len = status == TLC_OK ? n : 0;
+        hdr->status = status;
+        hdr->reserved = 0;
+    }
+    if (status != TLC_OK) return;
+    const uint64_t stride = (uint64_t)gridDim.x * kI8Threads;
+    uint64_t head = 0;
+    if (vec) {
+        const uint64_t n16 = n / 16;
+        const float4 *t4 = reinterpret_cast<const float4 *>(t);
+        uint4 *c16 = reinterpret_cast<uint4 *>(codes);
+        for (uint64_t g = (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; g < n16; g += stride) {
+            float4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) v[k] = ld_stream4(t4 + 4 * g + k);
+            __stcs(c16 + g, make_uint4(pack4(v[0], scale), pack4(v[1], scale), pack4(v[2], scale), pack4(v[3], scale)));
+        }
+        head = 16 * n16;
+    }
+    for (uint64_t i = head + (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; i < n; i += stride)
+        codes[i] = int8_code(ld_stream(t + i), scale);
+}
+
+__device__ __forceinline__ float dq(int8_t c, float scale) { return __fmul_rn(scale, (float)c); }
+
+__device__ __forceinline__ float4 dq4(uint32_t w, float scale, float4 o, int mode) {
+    const int8_t c0 = (int8_t)(w & 0xff), c1 = (int8_t)((w >> 8) & 0xff), c2 = (int8_t)((w >> 16) & 0xff),
+                 c3 = (int8_t)(w >> 24);
+    if (mode == TLC_MODE_OVERWRITE) return make_float4(dq(c0, scale), dq(c1, scale), dq(c2, scale), dq(c3, scale));
+    // accumulate: add only where code != 0 (R16); other elements keep their bits
+    return make_float4(c0 ? __fadd_rn(o.x, dq(c0, scale)) : o.x, c1 ? __fadd_rn(o.y, dq(c1, scale)) : o.y,
+                       c2 ? __fadd_rn(o.z, dq(c2, scale)) : o.z, c3 ? __fadd_rn(o.w, dq(c3, scale)) : o.w);
+}
+
+__global__ void __launch_bounds__(kI8Threads)
+tlc_int8_dequant_kernel(const int8_t *__restrict__ codes, tlc_header *hdr, uint64_t n, float *__restrict__ out,
+                        int mode, int vec) {
+    // header checks: the producer's n, the int8 flag, a finite scale >= +0 (R21, R23)
+    const float scale = hdr->M;
+    const bool ok = hdr->status == TLC_OK && hdr->n == n && (hdr->flags & TLC_FLAG_INT8) &&
+                    hdr->payload_len == n && !signbit(scale) && isfinite(scale);
+    if (!ok) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && hdr->status == TLC_OK) raise_format(hdr);
+        return;
+    }
+    const uint64_t stride = (uint64_t)gridDim.x * kI8Threads;
+    uint64_t head = 0;
+    if (vec) {
+        const uint64_t n16 = n / 16;
+        const uint4 *c16 = reinterpret_cast<const uint4 *>(codes);
+        float4 *o4 = reinterpret_cast<float4 *>(out);
+        for (uint64_t g = (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; g < n16; g += stride) {
+            const uint4 w = __ldcs(c16 + g);
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const float4 o = mode == TLC_MODE_OVERWRITE ? make_float4(0, 0, 0, 0) : o4[4 * g + k];
+                __stcs(o4 + 4 * g + k, dq4(ww[k], scale, o, mode));
+            }
+        }
+        head = 16 * n16;
+    }
+    for (uint64_t i = head + (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; i < n; i += stride) {
+        const int8_t c = codes[i];
+        if (mode == TLC_MODE_OVERWRITE) out[i] = dq(c, scale);
+        else if (c) out[i] = __fadd_rn(out[i], dq(c, scale));
+    }
+}
+
+template <class K>
+static int grid_for(K kernel, uint64_t work) {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, kI8Threads, 0);
+    return (int)tmax<uint64_t>(1, tmin<uint64_t>((work + kI8Threads - 1) / kI8Threads,
+                                                 (uint64_t)num_sms() * tmax(1, blocks)));
+}
+
+int launch_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr, void *ws, cudaStream_t st) {
+    uint64_t scratch = 0;
+    const SegTable T = single_table(t, nullptr, nullptr, nullptr, hdr, n, scratch);
+    const WsLayout L = ws_layout(T, 0);
+    unsigned int *maxkey = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ws) + L.maxkey);
+    if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
+    launch_absmax(T, maxkey, false, st);
+    {
+        KernelScope ks(kKq8, st);
+        static int grid = 0;
+        if (!grid) grid = grid_for(tlc_int8_quant_kernel, ~0ull >> 8);
+        const int vec = aligned16(t) && aligned16(codes);
+        const int g = (int)tmin<uint64_t>((uint64_t)grid, tmax<uint64_t>(1, (n / 16 + kI8Threads - 1) / kI8Threads));
+        tlc_int8_quant_kernel<<<g, kI8Threads, 0, st>>>(t, n, codes, hdr, maxkey, vec);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+int launch_int8_decompress(const int8_t *codes, tlc_header *hdr, uint64_t n, float *out, int mode, cudaStream_t st) {
+    KernelScope ks(kKd8, st);
+    static int grid = 0;
+    if (!grid) grid = grid_for(tlc_int8_dequant_kernel, ~0ull >> 8);
+    const int vec = aligned16(codes) && aligned16(out);
+    const int g = (int)tmin<uint64_t>((uint64_t)grid, tmax<uint64_t>(1, (n / 16 + kI8Threads - 1) / kI8Threads));
+    tlc_int8_dequant_kernel<<<g, kI8Threads, 0, st>>>(codes, hdr, n, out, mode, vec);
+    return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+}  // namespace tlc

@@ -1,0 +1,136 @@
+// stoch.cu -- "Stoch 3-value + QE", a compared design of the paper (Sec. 5.1,
+// P:629-632): TernGrad-like stochastic 3-value quantization ("outputs
+// randomized quantization values whose expectation matches their input value")
+// without gradient clipping, sparsity multiplier or error buffer, followed by
+// the same quartic encoding (and optionally zero-run encoding) as 3LC.
+//
+// K2s tlc_stoch_qe_kernel: m = max|t| from K1's key; element x of the tensor
+// becomes sign(x) with probability |x|/m, drawn from a counter-based generator
+// (reading R22): the element's word is word e%4 of Philox4x32-10 at counter
+// (e/4, step) under key seed, U = (w >> 8) * 2^-24, p = fl(|x| / m) (IEEE
+// division), q = sign(x) iff U < p.  The result depends only on (t, seed,
+// step), never on the launch shape.
+//
+// Layout: a tile of t2 quartic positions [j0, j1) needs the elements
+// [i*P + j0, i*P + j1) of each partition i.  Philox blocks are aligned to the
+// ELEMENT index (four elements e = 4b..4b+3 per block), so a thread takes
+// whole blocks: one 128-bit load of t (16-byte aligned for any P), one Philox
+// evaluation, four digits -- written to a shared-memory digit plane at their
+// quartic position.  After a barrier every thread folds the five planes of four
+// positions into four quartic bytes with one SWAR multiply-add chain
+// (each byte <= 242, no carries between bytes) and one 32-bit store.
+#include "tlc_device.cuh"
+#include "tlc_launch.h"
+
+namespace tlc {
+
+constexpr int kK2sThreads = 256;
+constexpr int kK2sMaxTile = 4096;            // >= every ItemSizes::t2
+
+struct PhiloxKey {
+    uint32_t k0, k1;
+};
+
+// Philox4x32-10 (Salmon et al., SC'11): ten rounds of two 32x32->64 multiplies.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey k) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.k0, lo1, hi0 ^ c.w ^ k.k1, lo0);
+        k.k0 += 0x9E3779B9u;
+        k.k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// digit (q + 1) of element x under word w: U = (w >> 8) 2^-24 < fl(|x| / m) -> sign(x)
+__device__ __forceinline__ uint32_t stoch_digit(float x, uint32_t w, float m) {
+    const float p = __fdiv_rn(fabsf(x), m);
+    const float U = __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
+    return U < p ? (x > 0.0f ? 2u : 0u) : 1u;
+}
+
+__global__ void __launch_bounds__(kK2sThreads)
+tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_lo, uint32_t seed_hi,
+                    uint32_t step_lo, uint32_t step_hi, int use_zre, uint8_t *__restrict__ scratch) {
+    __shared__ __align__(16) uint8_t dig[5][kK2sMaxTile];
+    __shared__ uint64_t s_first[kSegCache];
+    pdl_trigger();
+    seg_index_load<2>(T, s_first);
+    pdl_wait();                                          // K1's max keys
+    const PhiloxKey key{seed_lo, seed_hi};
+    for (uint64_t tile = blockIdx.x; tile < T.n2; tile += gridDim.x) {
+        const int si = find_seg_c<2>(T, tile, s_first);
+        const Seg S = get_seg(T, si);
+        float m;
+        const unsigned int status = scale_from_key(maxkey[si], 1.0f, m);   // m = max|t| (no s)
+        const uint64_t lt = tile - S.k2;
+        if (lt == 0 && threadIdx.x == 0) {
+            tlc_header *h = S.hdr;
+            h->M = m;
+            h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+            h->n = S.n;
+            h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;   // ZRE: set by K3
+            h->status = status;
+            h->reserved = 0;
+        }
+        if (status != TLC_OK) continue;                  // uniform per tile
+        const uint64_t P = S.P, n = S.n;
+        const uint64_t j0 = lt * T.sz.t2, j1 = tmin<uint64_t>(P, j0 + T.sz.t2);
+        const bool vec = aligned16(S.t);
+        // phase A: digit planes, one Philox block (4 elements) per thread and step
+#pragma unroll 1
+        for (int i = 0; i < 5; i++) {
+            const uint64_t lo = (uint64_t)i * P + j0, hi = (uint64_t)i * P + j1;
+            const uint64_t b0 = lo / 4, b1 = (hi - 1) / 4;
+            for (uint64_t b = b0 + threadIdx.x; b <= b1; b += kK2sThreads) {
+                const uint64_t e0 = 4 * b;
+                float x[4];
+                if (vec && e0 + 3 < n) {
+                    const float4 v = ld_stream4(reinterpret_cast<const float4 *>(S.t) + b);
+                    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; c++) x[c] = (e0 + c < n && e0 + c >= lo && e0 + c < hi) ? ld_stream(S.t + e0 + c) : 0.0f;
+                }
+                const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const uint64_t e = e0 + c;
+                    if (e >= lo && e < hi)               // pad positions (e >= n): digit 0
+                        dig[i][e - lo] = e < n ? (uint8_t)stoch_digit(x[c], ww[c], m) : (uint8_t)0;
+                }
+            }
+        }
+        __syncthreads();
+        // phase B: B = 81 d0 + 27 d1 + 9 d2 + 3 d3 + d4, four positions per thread
+        uint8_t *bytes = (use_zre ? scratch + S.bytes_off : S.payload) + j0;
+        const uint32_t len = (uint32_t)(j1 - j0);
+        const bool word_ok = use_zre || aligned4(S.payload);
+        for (uint32_t g = threadIdx.x; 4 * g < len; g += kK2sThreads) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int i = 0; i < 5; i++) v = v * 3u + reinterpret_cast<const uint32_t *>(dig[i])[g];
+            if (word_ok && 4 * g + 4 <= len) {
+                reinterpret_cast<uint32_t *>(bytes)[g] = v;
+            } else {
+                for (uint32_t c = 0; c < 4 && 4 * g + c < len; c++) bytes[4 * g + c] = (uint8_t)(v >> (8 * c));
+            }
+        }
+        __syncthreads();                                 // planes are reused by the next tile
+    }
+}
+
+void launch_stoch_qe(const SegTable &T, const unsigned int *maxkey, uint64_t seed, uint64_t step, int use_zre,
+                     uint8_t *scratch, cudaStream_t st) {
+    static int blocks = 0;
+    if (!blocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tlc_stoch_qe_kernel, kK2sThreads, 0);
+    KernelScope ks(kK2s, st);
+    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2, (uint64_t)num_sms() * tmax(1, blocks)));
+    launch_pdl(tlc_stoch_qe_kernel, grid, kK2sThreads, 0, st, T, maxkey, (uint32_t)seed, (uint32_t)(seed >> 32),
+               (uint32_t)step, (uint32_t)(step >> 32), use_zre, scratch);
+}
+
+}  // namespace tlc

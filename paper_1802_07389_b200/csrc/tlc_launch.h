@@ -16,8 +16,8 @@ template <class T> __host__ __device__ inline T tmin(T a, T b) { return a < b ? 
 template <class T> __host__ __device__ inline T tmax(T a, T b) { return a < b ? b : a; }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-inline bool aligned4(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+__host__ __device__ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+__host__ __device__ inline bool aligned4(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
 
 inline int num_sms() {
     static int sms[64] = {0};
@@ -53,7 +53,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 // Kernel ids for launch counting / profiling (prof.cu).
-enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7, kNumKernelIds = 8 };
+enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7,
+                kK2s = 8, kKq8 = 9, kKd8 = 10, kNumKernelIds = 11 };
 
 struct Ctrl;
 
@@ -147,6 +148,16 @@ struct Table {
     void release();
 };
 int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t st);
+
+// K1 alone: per-segment max key of |err + t| (has_err) or |t| into maxkey[].
+void launch_absmax(const SegTable &T, unsigned int *maxkey, bool has_err, cudaStream_t st);
+// Compared designs of Sec. 5.1 (stoch.cu, int8.cu).
+void launch_stoch_qe(const SegTable &T, const unsigned int *maxkey, uint64_t seed, uint64_t step, int use_zre,
+                     uint8_t *scratch, cudaStream_t st);
+int launch_stoch_compress_table(const SegTable &T, uint64_t seed, uint64_t step, int use_zre, void *ws,
+                                cudaStream_t st);
+int launch_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr, void *ws, cudaStream_t st);
+int launch_int8_decompress(const int8_t *codes, tlc_header *hdr, uint64_t n, float *out, int mode, cudaStream_t st);
 int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st);
 
 }  // namespace tlc
