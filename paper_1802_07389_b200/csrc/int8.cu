@@ -4,10 +4,11 @@
 // dequant = fl(scale * code).  No error buffer.
 //
 // Kq8 tlc_int8_quant_kernel: after K1<no err> (max|t|), one streaming pass:
-//     16 elements per thread and step (four 128-bit loads, one 128-bit store of
-//     codes).  Algorithmic bytes 4n read + n written.
-// Kd8 tlc_int8_dequant_kernel: 16 codes per thread (one 128-bit load, four
-//     128-bit stores): n read + 4n written (accumulate: + 4n read).
+//     per warp step 512 elements, lane l taking float4 number base + l + 32k
+//     (k = 0..3, four coalesced 512-byte loads in flight) and storing its 4 codes
+//     as one 32-bit word (coalesced 128-byte stores).  4n read + n written.
+// Kd8 tlc_int8_dequant_kernel: the mirror image, 32-bit code loads and float4
+//     stores with the same lane mapping: n read + 4n written (accumulate: + 4n).
 // Both are plain HBM streams; grid = SMs x resident CTAs, grid-stride.
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
@@ -46,16 +47,21 @@ tlc_int8_quant_kernel(const float *__restrict__ t, uint64_t n, int8_t *__restric
     const uint64_t stride = (uint64_t)gridDim.x * kI8Threads;
     uint64_t head = 0;
     if (vec) {
-        const uint64_t n16 = n / 16;
+        // warp step ws covers float4 numbers 128 ws + 32 k + lane, k = 0..3
+        const uint64_t n4 = n / 4;
         const float4 *t4 = reinterpret_cast<const float4 *>(t);
-        uint4 *c16 = reinterpret_cast<uint4 *>(codes);
-        for (uint64_t g = (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; g < n16; g += stride) {
+        uint32_t *c32 = reinterpret_cast<uint32_t *>(codes);
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint64_t nw = n4 / 128;                                         // 128 float4 per warp step
+        const uint64_t wstride = (uint64_t)gridDim.x * (kI8Threads / 32);
+        for (uint64_t ws = (uint64_t)blockIdx.x * (kI8Threads / 32) + warp; ws < nw; ws += wstride) {
             float4 v[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) v[k] = ld_stream4(t4 + 4 * g + k);
-            __stcs(c16 + g, make_uint4(pack4(v[0], scale), pack4(v[1], scale), pack4(v[2], scale), pack4(v[3], scale)));
+            for (int k = 0; k < 4; k++) v[k] = ld_stream4(t4 + 128 * ws + 32 * k + lane);
+#pragma unroll
+            for (int k = 0; k < 4; k++) __stcs(c32 + 128 * ws + 32 * k + lane, pack4(v[k], scale));
         }
-        head = 16 * n16;
+        head = 4 * 128 * nw;
     }
     for (uint64_t i = head + (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; i < n; i += stride)
         codes[i] = int8_code(ld_stream(t + i), scale);
@@ -86,19 +92,23 @@ tlc_int8_dequant_kernel(const int8_t *__restrict__ codes, tlc_header *hdr, uint6
     const uint64_t stride = (uint64_t)gridDim.x * kI8Threads;
     uint64_t head = 0;
     if (vec) {
-        const uint64_t n16 = n / 16;
-        const uint4 *c16 = reinterpret_cast<const uint4 *>(codes);
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint64_t nw = n / 512;                                          // 128 code words per warp step
+        const uint64_t wstride = (uint64_t)gridDim.x * (kI8Threads / 32);
+        const uint32_t *c32 = reinterpret_cast<const uint32_t *>(codes);
         float4 *o4 = reinterpret_cast<float4 *>(out);
-        for (uint64_t g = (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; g < n16; g += stride) {
-            const uint4 w = __ldcs(c16 + g);
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+        for (uint64_t ws = (uint64_t)blockIdx.x * (kI8Threads / 32) + warp; ws < nw; ws += wstride) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) w[k] = __ldcs(c32 + 128 * ws + 32 * k + lane);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                const float4 o = mode == TLC_MODE_OVERWRITE ? make_float4(0, 0, 0, 0) : o4[4 * g + k];
-                __stcs(o4 + 4 * g + k, dq4(ww[k], scale, o, mode));
+                float4 *dst = o4 + 128 * ws + 32 * k + lane;
+                const float4 o = mode == TLC_MODE_OVERWRITE ? make_float4(0, 0, 0, 0) : *dst;
+                __stcs(dst, dq4(w[k], scale, o, mode));
             }
         }
-        head = 16 * n16;
+        head = 512 * nw;
     }
     for (uint64_t i = head + (uint64_t)blockIdx.x * kI8Threads + threadIdx.x; i < n; i += stride) {
         const int8_t c = codes[i];

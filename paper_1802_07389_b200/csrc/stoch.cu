@@ -15,10 +15,11 @@
 // [i*P + j0, i*P + j1) of each partition i.  Philox blocks are aligned to the
 // ELEMENT index (four elements e = 4b..4b+3 per block), so a thread takes
 // whole blocks: one 128-bit load of t (16-byte aligned for any P), one Philox
-// evaluation, four digits -- written to a shared-memory digit plane at their
-// quartic position.  After a barrier every thread folds the five planes of four
-// positions into four quartic bytes with one SWAR multiply-add chain
-// (each byte <= 242, no carries between bytes) and one 32-bit store.
+// evaluation, four digits packed in one 32-bit word of a shared-memory digit
+// plane (partition i's tile starts at byte lo_i mod 4 of its plane).  After a
+// barrier every thread funnel-shifts the five planes' words of four positions
+// into place and folds them into four quartic bytes with one SWAR multiply-add
+// chain (each byte <= 242, no carries between bytes) and one 32-bit store.
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
 
@@ -44,17 +45,36 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey k) {
     return c;
 }
 
-// digit (q + 1) of element x under word w: U = (w >> 8) 2^-24 < fl(|x| / m) -> sign(x)
-__device__ __forceinline__ uint32_t stoch_digit(float x, uint32_t w, float m) {
-    const float p = __fdiv_rn(fabsf(x), m);
-    const float U = __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
-    return U < p ? (x > 0.0f ? 2u : 0u) : 1u;
-}
+// Digit (q + 1) of element x under word w: q = sign(x) iff U = (w >> 8) 2^-24 < fl(|x| / m).
+// Fast form (2^-125 <= m <= 2^125): r = fl(|x| * fl(1/m)) is within 2^-22 of fl(|x|/m)
+// (three roundings of a quotient <= 1), so whenever |r - U| > 2^-21 the comparison of U
+// with r decides exactly as with the IEEE quotient; the remaining draws (probability
+// ~2^-20) and every other m take the IEEE division.
+struct StochQ {
+    float m, inv_m;
+    bool fast;
+    __device__ __forceinline__ explicit StochQ(float mm)
+        : m(mm), inv_m(0.0f), fast(mm >= 0x1p-125f && mm <= 0x1p125f) {
+        if (fast) inv_m = __frcp_rn(mm);
+    }
+    __device__ __forceinline__ uint32_t digit(float x, uint32_t w) const {
+        const float a = fabsf(x);
+        const float U = __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
+        bool take;
+        const float d = __fsub_rn(__fmul_rn(a, inv_m), U);
+        if (fast && fabsf(d) > 0x1p-21f) take = d > 0.0f;
+        else take = U < __fdiv_rn(a, m);
+        return take ? (x > 0.0f ? 2u : 0u) : 1u;
+    }
+};
 
 __global__ void __launch_bounds__(kK2sThreads)
 tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_lo, uint32_t seed_hi,
                     uint32_t step_lo, uint32_t step_hi, int use_zre, uint8_t *__restrict__ scratch) {
-    __shared__ __align__(16) uint8_t dig[5][kK2sMaxTile];
+    // digit planes: element e of partition i lands at byte e - 4*floor(lo_i/4), so every
+    // Philox block writes one aligned 32-bit word; the tile's first position sits at
+    // byte sh_i = lo_i mod 4 of plane i.
+    __shared__ __align__(16) uint32_t dig[5][kK2sMaxTile / 4 + 4];
     __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
     seg_index_load<2>(T, s_first);
@@ -79,29 +99,32 @@ tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_
         const uint64_t P = S.P, n = S.n;
         const uint64_t j0 = lt * T.sz.t2, j1 = tmin<uint64_t>(P, j0 + T.sz.t2);
         const bool vec = aligned16(S.t);
-        // phase A: digit planes, one Philox block (4 elements) per thread and step
+        const StochQ Q(m);
+        // phase A: one Philox block (4 elements, one 128-bit load) per thread and step
 #pragma unroll 1
         for (int i = 0; i < 5; i++) {
             const uint64_t lo = (uint64_t)i * P + j0, hi = (uint64_t)i * P + j1;
-            const uint64_t b0 = lo / 4, b1 = (hi - 1) / 4;
-            for (uint64_t b = b0 + threadIdx.x; b <= b1; b += kK2sThreads) {
-                const uint64_t e0 = 4 * b;
+            const uint64_t b0 = lo / 4;
+            const uint32_t nb = (uint32_t)((hi - 1) / 4 - b0 + 1);
+            for (uint32_t lb = threadIdx.x; lb < nb; lb += kK2sThreads) {
+                const uint64_t b = b0 + lb, e0 = 4 * b;
                 float x[4];
+                uint32_t d;
+                const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
                 if (vec && e0 + 3 < n) {
                     const float4 v = ld_stream4(reinterpret_cast<const float4 *>(S.t) + b);
-                    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-                } else {
+                    d = Q.digit(v.x, w.x) | (Q.digit(v.y, w.y) << 8) | (Q.digit(v.z, w.z) << 16) |
+                        (Q.digit(v.w, w.w) << 24);
+                } else {                                 // tensor end or unaligned t
 #pragma unroll
-                    for (int c = 0; c < 4; c++) x[c] = (e0 + c < n && e0 + c >= lo && e0 + c < hi) ? ld_stream(S.t + e0 + c) : 0.0f;
-                }
-                const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
-                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+                    for (int c = 0; c < 4; c++) x[c] = e0 + c < n ? ld_stream(S.t + e0 + c) : 0.0f;
+                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+                    d = 0;
 #pragma unroll
-                for (int c = 0; c < 4; c++) {
-                    const uint64_t e = e0 + c;
-                    if (e >= lo && e < hi)               // pad positions (e >= n): digit 0
-                        dig[i][e - lo] = e < n ? (uint8_t)stoch_digit(x[c], ww[c], m) : (uint8_t)0;
+                    for (int c = 0; c < 4; c++)          // pad positions (e >= n): digit 0
+                        d |= (e0 + c < n ? Q.digit(x[c], ww[c]) : 0u) << (8 * c);
                 }
+                dig[i][lb] = d;
             }
         }
         __syncthreads();
@@ -112,7 +135,10 @@ tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_
         for (uint32_t g = threadIdx.x; 4 * g < len; g += kK2sThreads) {
             uint32_t v = 0;
 #pragma unroll
-            for (int i = 0; i < 5; i++) v = v * 3u + reinterpret_cast<const uint32_t *>(dig[i])[g];
+            for (int i = 0; i < 5; i++) {
+                const uint32_t sh = (uint32_t)(((uint64_t)i * P + j0) & 3);     // lo_i mod 4
+                v = v * 3u + __funnelshift_r(dig[i][g], dig[i][g + 1], 8 * sh);
+            }
             if (word_ok && 4 * g + 4 <= len) {
                 reinterpret_cast<uint32_t *>(bytes)[g] = v;
             } else {

@@ -157,3 +157,23 @@ def family(name: str, n: int, s: float, seed: int = 3) -> np.ndarray:
     if name == "runs":
         return runs_adversarial(n, 1.0, seed, 2)
     raise ValueError(name)
+
+
+def blobs(n_train: int, n_test: int, dim: int, classes: int, std: float, *key: int):
+    """Desk-scale classification task of the training simulator (the
+    stand-in for CIFAR-10): class c is centred at a seeded random unit-norm vector
+    scaled by 2.0, points are centre + std * N(0, 1).  Returns fp32 (x_train,
+    y_train, x_test, y_test); labels are stratified (n/classes per class)."""
+    g = rng(*(key or (9, 0)))
+    centers = g.standard_normal((classes, dim))
+    centers = (2.0 * centers / np.linalg.norm(centers, axis=1, keepdims=True)).astype(np.float32)
+
+    def draw(n):
+        y = np.arange(n) % classes
+        g.shuffle(y)
+        x = centers[y] + np.float32(std) * g.standard_normal((n, dim)).astype(np.float32)
+        return x.astype(np.float32), y.astype(np.int64)
+
+    xtr, ytr = draw(n_train)
+    xte, yte = draw(n_test)
+    return xtr, ytr, xte, yte
