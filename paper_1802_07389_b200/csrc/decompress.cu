@@ -238,10 +238,25 @@ __device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, 
         }
         __syncthreads();                                  // warp_sum reuse; E complete
     } else {
-        for (int jl = threadIdx.x; jl < tl; jl += kK5Threads) {
-            uint8_t v = payload[J0 + jl];
-            if (v > 242) { bad = true; v = kZeroGroup; }
-            E[jl] = v;
+        // quartic bytes as sent: 16 per thread (one 128-bit load when aligned); a byte
+        // > 242 is not a quartic code -> FORMAT, replaced by 121 meanwhile
+        const uint8_t *src = payload + J0;
+        const int j = kK5BytesPerThread * threadIdx.x;
+        if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && j + kK5BytesPerThread <= tl) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + j));
+            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t m = __vcmpgtu4(w[c], 0xf2f2f2f2u);   // bytes > 242
+                if (m) { bad = true; w[c] = (w[c] & ~m) | (0x79797979u & m); }
+            }
+            *reinterpret_cast<uint4 *>(E + j) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+            for (int jl = j; jl < j + kK5BytesPerThread && jl < tl; jl++) {
+                uint8_t v = src[jl];
+                if (v > 242) { bad = true; v = kZeroGroup; }
+                E[jl] = v;
+            }
         }
     }
     return __syncthreads_or(bad);

@@ -24,10 +24,38 @@ __device__ __forceinline__ int8_t int8_code(float x, float scale) {
     return (int8_t)(int)c;
 }
 
-__device__ __forceinline__ uint32_t pack4(float4 v, float scale) {
-    return (uint32_t)(uint8_t)int8_code(v.x, scale) | ((uint32_t)(uint8_t)int8_code(v.y, scale) << 8) |
-           ((uint32_t)(uint8_t)int8_code(v.z, scale) << 16) | ((uint32_t)(uint8_t)int8_code(v.w, scale) << 24);
-}
+// The same codes without the XU pipe (the IEEE quotient costs MUFU.RCP, roundf FRND, the
+// cast F2I: three quarter-rate XU ops per element): for 2^-100 <= scale <= 2^100,
+// r = fl(x * fl(1/scale)) lies within 3 * 2^-24 |x/scale| <= 2^-15 of fl(x/scale)
+// (|x/scale| <= 127 (1 + 2^-23)), so unless r is within 2^-14 of a half-integer both
+// round to the same integer -- computed by adding 1.5 * 2^23 (the sum's last mantissa bit
+// is the units place, any rounding of a non-tie lands on the nearest integer).  Near a
+// half-integer the IEEE form decides (probability ~2^-13 per element).
+struct Int8Q {
+    float scale, inv;
+    bool fast;
+    __device__ __forceinline__ explicit Int8Q(float sc)
+        : scale(sc), inv(0.0f), fast(sc >= 0x1p-100f && sc <= 0x1p100f) {
+        if (fast) inv = __frcp_rn(sc);
+    }
+    // code of x as a byte; `unsure` set when the IEEE form must decide
+    __device__ __forceinline__ uint32_t code_fast(float x, bool &unsure) const {
+        const float r = __fmul_rn(x, inv);
+        const float y = __fadd_rn(r, 12582912.0f);                     // 1.5 * 2^23
+        const float k = __fsub_rn(y, 12582912.0f);                     // nearest integer (exact)
+        unsure |= !(fabsf(__fsub_rn(r, k)) < 0.5f - 0x1p-14f);
+        const int c = max(-127, min(127, (int)(__float_as_uint(y) - 0x4b400000u)));
+        return (uint32_t)c & 0xffu;
+    }
+    __device__ __forceinline__ uint32_t pack4(float4 v) const {
+        bool unsure = !fast;
+        const uint32_t w = code_fast(v.x, unsure) | (code_fast(v.y, unsure) << 8) | (code_fast(v.z, unsure) << 16) |
+                           (code_fast(v.w, unsure) << 24);
+        if (!unsure) return w;
+        return (uint32_t)(uint8_t)int8_code(v.x, scale) | ((uint32_t)(uint8_t)int8_code(v.y, scale) << 8) |
+               ((uint32_t)(uint8_t)int8_code(v.z, scale) << 16) | ((uint32_t)(uint8_t)int8_code(v.w, scale) << 24);
+    }
+};
 
 __global__ void __launch_bounds__(kI8Threads)
 tlc_int8_quant_kernel(const float *__restrict__ t, uint64_t n, int8_t *__restrict__ codes, tlc_header *hdr,
@@ -44,6 +72,7 @@ tlc_int8_quant_kernel(const float *__restrict__ t, uint64_t n, int8_t *__restric
         hdr->reserved = 0;
     }
     if (status != TLC_OK) return;
+    const Int8Q Q(scale);
     const uint64_t stride = (uint64_t)gridDim.x * kI8Threads;
     uint64_t head = 0;
     if (vec) {
@@ -59,7 +88,7 @@ tlc_int8_quant_kernel(const float *__restrict__ t, uint64_t n, int8_t *__restric
 #pragma unroll
             for (int k = 0; k < 4; k++) v[k] = ld_stream4(t4 + 128 * ws + 32 * k + lane);
 #pragma unroll
-            for (int k = 0; k < 4; k++) __stcs(c32 + 128 * ws + 32 * k + lane, pack4(v[k], scale));
+            for (int k = 0; k < 4; k++) __stcs(c32 + 128 * ws + 32 * k + lane, Q.pack4(v[k]));
         }
         head = 4 * 128 * nw;
     }

@@ -46,27 +46,43 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey k) {
 }
 
 // Digit (q + 1) of element x under word w: q = sign(x) iff U = (w >> 8) 2^-24 < fl(|x| / m).
-// Fast form (2^-125 <= m <= 2^125): r = fl(|x| * fl(1/m)) is within 2^-22 of fl(|x|/m)
-// (three roundings of a quotient <= 1), so whenever |r - U| > 2^-21 the comparison of U
-// with r decides exactly as with the IEEE quotient; the remaining draws (probability
-// ~2^-20) and every other m take the IEEE division.
+// Fast form (2^-100 <= m <= 2^100): r = fl(|x| * fl(1/m)) lies within 2^-22 of fl(|x|/m)
+// (three roundings of a quotient <= 1), so whenever |r - U| > 2^-21 comparing U with r
+// decides exactly as the IEEE quotient does.  Both sides are kept scaled by 2^24 (exact:
+// inv24 = fl(1/m) 2^24 stays normal): d = fl(|x| inv24) - (w >> 8).  The rare draws with
+// |d| <= 8 (probability ~2^-20 each) and every other m take the IEEE division, once per
+// block of four elements, out of line.
 struct StochQ {
-    float m, inv_m;
+    float m, inv24;
     bool fast;
     __device__ __forceinline__ explicit StochQ(float mm)
-        : m(mm), inv_m(0.0f), fast(mm >= 0x1p-125f && mm <= 0x1p125f) {
-        if (fast) inv_m = __frcp_rn(mm);
+        : m(mm), inv24(0.0f), fast(mm >= 0x1p-100f && mm <= 0x1p100f) {
+        if (fast) inv24 = __fmul_rn(__frcp_rn(mm), 0x1p24f);
     }
-    __device__ __forceinline__ uint32_t digit(float x, uint32_t w) const {
-        const float a = fabsf(x);
+    __device__ __forceinline__ static uint32_t code(bool take, float x) {
+        return take ? (signbit(x) ? 0u : 2u) : 1u;            // take implies x != 0
+    }
+    // fast digit; sets `unsure` when the exact quotient must decide
+    __device__ __forceinline__ uint32_t digit_fast(float x, uint32_t w, bool &unsure) const {
+        const float d = __fsub_rn(__fmul_rn(fabsf(x), inv24), __uint2float_rn(w >> 8));
+        unsure |= !(fabsf(d) > 8.0f);
+        return code(d > 0.0f, x);
+    }
+    __device__ __forceinline__ uint32_t digit_exact(float x, uint32_t w) const {
         const float U = __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
-        bool take;
-        const float d = __fsub_rn(__fmul_rn(a, inv_m), U);
-        if (fast && fabsf(d) > 0x1p-21f) take = d > 0.0f;
-        else take = U < __fdiv_rn(a, m);
-        return take ? (x > 0.0f ? 2u : 0u) : 1u;
+        return code(U < __fdiv_rn(fabsf(x), m), x);
     }
 };
+
+__device__ __noinline__ uint32_t stoch_block_exact(const StochQ &Q, float4 v, uint4 w, uint32_t valid) {
+    const float x[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+    uint32_t d = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+        d |= (c < (int)valid ? Q.digit_exact(x[c], ww[c]) : 0u) << (8 * c);   // pad: digit 0
+    return d;
+}
 
 __global__ void __launch_bounds__(kK2sThreads)
 tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_lo, uint32_t seed_hi,
@@ -106,25 +122,39 @@ tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_
             const uint64_t lo = (uint64_t)i * P + j0, hi = (uint64_t)i * P + j1;
             const uint64_t b0 = lo / 4;
             const uint32_t nb = (uint32_t)((hi - 1) / 4 - b0 + 1);
-            for (uint32_t lb = threadIdx.x; lb < nb; lb += kK2sThreads) {
-                const uint64_t b = b0 + lb, e0 = 4 * b;
-                float x[4];
-                uint32_t d;
-                const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
-                if (vec && e0 + 3 < n) {
-                    const float4 v = ld_stream4(reinterpret_cast<const float4 *>(S.t) + b);
-                    d = Q.digit(v.x, w.x) | (Q.digit(v.y, w.y) << 8) | (Q.digit(v.z, w.z) << 16) |
-                        (Q.digit(v.w, w.w) << 24);
-                } else {                                 // tensor end or unaligned t
+            // kU blocks per thread and step: their loads are all in flight before the
+            // first Philox round, so each thread keeps 16 kU bytes of t outstanding
+            constexpr int kU = 4;
+            for (uint32_t lb0 = threadIdx.x; lb0 < nb; lb0 += kU * kK2sThreads) {
+                float4 v[kU];
+                uint32_t valid[kU];
 #pragma unroll
-                    for (int c = 0; c < 4; c++) x[c] = e0 + c < n ? ld_stream(S.t + e0 + c) : 0.0f;
-                    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-                    d = 0;
-#pragma unroll
-                    for (int c = 0; c < 4; c++)          // pad positions (e >= n): digit 0
-                        d |= (e0 + c < n ? Q.digit(x[c], ww[c]) : 0u) << (8 * c);
+                for (int u = 0; u < kU; u++) {
+                    const uint32_t lb = lb0 + u * kK2sThreads;
+                    const uint64_t e0 = 4 * (b0 + lb);
+                    valid[u] = lb >= nb ? 0u : e0 + 3 < n ? 4u : (uint32_t)(n - tmin<uint64_t>(n, e0));
+                    v[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    if (vec && valid[u] == 4) {
+                        v[u] = ld_stream4(reinterpret_cast<const float4 *>(S.t) + (b0 + lb));
+                    } else {                             // tensor end or unaligned t
+                        if (valid[u] > 0) v[u].x = ld_stream(S.t + e0);
+                        if (valid[u] > 1) v[u].y = ld_stream(S.t + e0 + 1);
+                        if (valid[u] > 2) v[u].z = ld_stream(S.t + e0 + 2);
+                        if (valid[u] > 3) v[u].w = ld_stream(S.t + e0 + 3);
+                    }
                 }
-                dig[i][lb] = d;
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    const uint32_t lb = lb0 + u * kK2sThreads;
+                    if (lb >= nb) break;
+                    const uint64_t b = b0 + lb;
+                    const uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
+                    bool unsure = !Q.fast || valid[u] != 4;
+                    uint32_t d = Q.digit_fast(v[u].x, w.x, unsure) | (Q.digit_fast(v[u].y, w.y, unsure) << 8) |
+                                 (Q.digit_fast(v[u].z, w.z, unsure) << 16) | (Q.digit_fast(v[u].w, w.w, unsure) << 24);
+                    if (unsure) d = stoch_block_exact(Q, v[u], w, valid[u]);
+                    dig[i][lb] = d;
+                }
             }
         }
         __syncthreads();
