@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtlc.so")
-SOURCES = ["api.cu", "compress.cu", "decompress.cu", "segments.cu", "exchange.cu", "prof.cu", "stoch.cu", "int8.cu"]
+SOURCES = ["api.cu", "compress.cu", "decompress.cu", "segments.cu", "exchange.cu", "prof.cu", "stoch.cu", "int8.cu", "small.cu"]
 HEADERS = ["tlc_device.cuh", "tlc_launch.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

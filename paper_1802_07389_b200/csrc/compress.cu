@@ -852,6 +852,7 @@ static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_e
 }
 
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+    if (small_table(T)) return launch_small_compress(T, s, use_zre, st);    // one launch, on chip
     const int sms = num_sms();
     return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
         KernelScope ks(kK2, st);

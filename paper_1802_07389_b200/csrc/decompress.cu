@@ -539,6 +539,7 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
 static int g_k4_blocks = 0, g_k5_blocks = 0;
 
 int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t st) {
+    if (small_table(T)) return launch_small_decompress(T, mode, st);         // one launch, on chip
     const WsLayout L = ws_layout(T, 0);
     char *base = reinterpret_cast<char *>(ws);
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);

@@ -19,7 +19,8 @@ static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe", "k3_zre"
                                             "k4_zre_scan", "k5_expand_dequant",
                                             "k5m_aggregate", "k9_flag_barrier",
                                             "k8_scale_mean", "k2s_stoch_qe",
-                                            "kq8_int8_quant", "kd8_int8_dequant"};
+                                            "kq8_int8_quant", "kd8_int8_dequant",
+                                            "k6_small_compress", "k7_small_decompress"};
 
 namespace {
 struct Rec {

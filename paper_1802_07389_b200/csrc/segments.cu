@@ -35,6 +35,7 @@ SegTable single_table(const float *t, float *err, float *out, uint8_t *payload, 
     s = Seg{};
     s.t = t; s.err = err; s.out = out; s.payload = payload; s.hdr = hdr; s.n = n;
     T.sz = item_sizes(n);
+    T.max_n = n;
     seg_items(s, T.sz, T.n1, T.n2, T.n3, T.n4, T.n5);
     s.bytes_off = 0;
     s.flags = seg_flags(s);
@@ -77,6 +78,7 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
     T.sz = z;
     T.count = cnt;
     T.n1 = c1; T.n2 = c2; T.n3 = c3; T.n4 = c4; T.n5 = c5;
+    for (int i = 0; i < cnt; i++) T.max_n = tmax<uint64_t>(T.max_n, host[i].n);
     ws_bytes = ws_layout(T, with_scratch ? scratch : 0).total;
     if (cudaMalloc((void **)&d, cnt * sizeof(Seg)) != cudaSuccess) return TLC_ERR_CUDA;
     if (cudaMalloc((void **)&d_first, 5 * (size_t)cnt * sizeof(uint64_t)) != cudaSuccess) return TLC_ERR_CUDA;

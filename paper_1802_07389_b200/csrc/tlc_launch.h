@@ -54,7 +54,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // Kernel ids for launch counting / profiling (prof.cu).
 enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7,
-                kK2s = 8, kKq8 = 9, kKd8 = 10, kNumKernelIds = 11 };
+                kK2s = 8, kKq8 = 9, kKd8 = 10, kK6s = 11, kK7s = 12, kNumKernelIds = 13 };
 
 struct Ctrl;
 
@@ -88,6 +88,9 @@ constexpr ItemSizes kLargeItems{65536, 4096, 32768, 16384};
 constexpr ItemSizes kSmallItems{8192, 1024, 8192, 4096};
 constexpr uint64_t kSmallTableElems = 32ull << 20;   // tables below 32M values use kSmallItems
 constexpr uint64_t kT5 = 4096;      // K5 tile: quartic positions per output tile
+// Tables whose tensors all have at most kSmallMaxN values (P <= 8192 quartic bytes) take
+// the fused one-CTA-per-tensor kernels of small.cu (u staged in 160 KiB of shared memory).
+constexpr uint64_t kSmallMaxN = 40960;
 
 enum SegFlags : uint32_t { kSegVec2 = 1u, kSegVec5 = 2u, kSegVec1 = 4u };
 
@@ -110,6 +113,7 @@ struct SegTable {
     uint64_t n1, n2, n3, n4, n5;    // total items per kernel
     ItemSizes sz;
     const uint64_t *first[5];       // device: first item of every segment, per kernel (count > 1)
+    uint64_t max_n;                 // largest segment
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -148,6 +152,12 @@ struct Table {
     void release();
 };
 int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t st);
+
+// Small tensors (small.cu): one CTA per tensor, one launch per direction.
+bool small_enabled();
+bool small_table(const SegTable &T);
+int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st);
+int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st);
 
 // K1 alone: per-segment max key of |err + t| (has_err) or |t| into maxkey[].
 void launch_absmax(const SegTable &T, unsigned int *maxkey, bool has_err, cudaStream_t st);
