@@ -86,15 +86,16 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
             const uint32_t n4 = n / 4;
             const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
             const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
-            for (uint32_t g0 = threadIdx.x; g0 < n4; g0 += 4 * kSmThreads) {
-                float4 tv[4], ev[4];
+            constexpr int kU = 8;                            // 256 bytes of t and err in flight per thread
+            for (uint32_t g0 = threadIdx.x; g0 < n4; g0 += kU * kSmThreads) {
+                float4 tv[kU], ev[kU];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < kU; k++) {
                     const uint32_t g = g0 + k * kSmThreads;
                     if (g < n4) { tv[k] = ld_stream4(t4 + g); ev[k] = __ldcs(e4 + g); }
                 }
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
+                for (int k = 0; k < kU; k++) {
                     const uint32_t g = g0 + k * kSmThreads;
                     if (g >= n4) break;
                     const float4 x = make_float4(__fadd_rn(ev[k].x, tv[k].x), __fadd_rn(ev[k].y, tv[k].y),
@@ -204,27 +205,38 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
     }
 }
 
+// A tensor's decode is split into parts of kSmPart quartic positions, one CTA each (the
+// 36,864-value ResNet-110 tensors would otherwise keep one SM busy while most idle): every
+// part scans the whole payload (<= P bytes, on chip) and expands / decodes only its range.
+constexpr uint32_t kSmPart = 2048;
+
 template <int kMode>
-__global__ void __launch_bounds__(kSmThreads, 1)
-tlc_small_decompress_kernel(const SegTable T) {
+__global__ void __launch_bounds__(kSmThreads)
+tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
     extern __shared__ __align__(16) uint8_t sm_raw[];
     __shared__ uint32_t V[5][256];
     __shared__ uint16_t lut[256];
     __shared__ uint32_t s_wsum[kSmWarps + 1];
     __shared__ int s_bad;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int si = blockIdx.x; si < T.count; si += gridDim.x) {
+    const uint64_t items = (uint64_t)T.count * parts;
+    for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const int si = (int)(item / parts);
+        const uint32_t part = (uint32_t)(item % parts);
         const Seg S = get_seg(T, si);
         tlc_header *hdr = S.hdr;
+        const uint32_t jr0 = part * kSmPart;
+        if (jr0 >= S.P) continue;                                // no positions in this part
         if (!header_valid(hdr, S.n)) {                           // uniform over the CTA
-            if (threadIdx.x == 0 && hdr->status == TLC_OK) raise_format(hdr);
+            if (threadIdx.x == 0 && part == 0 && hdr->status == TLC_OK) raise_format(hdr);
             continue;
         }
         const uint32_t n = (uint32_t)S.n, P = (uint32_t)S.P, Z = (uint32_t)hdr->payload_len;
+        const uint32_t jr1 = min(P, jr0 + kSmPart), pl = jr1 - jr0;
         const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
         const float M = hdr->M;
-        uint8_t *E = sm_raw;                                     // the P quartic bytes
-        uint8_t *Y = sm_raw + ((P + 15) & ~15u);                 // the payload (ZRE)
+        uint8_t *E = sm_raw;                                     // quartic bytes [jr0, jr1)
+        uint8_t *Y = sm_raw + kSmPart;                           // the payload (ZRE)
         if (threadIdx.x == 0) s_bad = 0;
         // value table: Eq. 3 per partition, V[i][b] = M * (digit_i(b) - 1)
         for (int v = threadIdx.x; v < 256; v += kSmThreads) {
@@ -256,10 +268,10 @@ tlc_small_decompress_kernel(const SegTable T) {
                 if (lane >= d) x += y;
             }
             if (lane == 31) s_wsum[warp] = x;
-            for (uint32_t q = 16 * threadIdx.x; q < P; q += 16 * kSmThreads) {   // 121 prefill
-                if (q + 16 <= P) *reinterpret_cast<uint4 *>(E + q) = make_uint4(0x79797979u, 0x79797979u,
-                                                                                0x79797979u, 0x79797979u);
-                else for (uint32_t r = q; r < P; r++) E[r] = kZeroGroup;
+            for (uint32_t q = 16 * threadIdx.x; q < pl; q += 16 * kSmThreads) {   // 121 prefill
+                if (q + 16 <= pl) *reinterpret_cast<uint4 *>(E + q) = make_uint4(0x79797979u, 0x79797979u,
+                                                                                 0x79797979u, 0x79797979u);
+                else for (uint32_t r = q; r < pl; r++) E[r] = kZeroGroup;
             }
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -270,21 +282,21 @@ tlc_small_decompress_kernel(const SegTable T) {
             }
             __syncthreads();
             if (s_bad) {
-                if (threadIdx.x == 0) raise_format(hdr);
+                if (threadIdx.x == 0 && part == 0) raise_format(hdr);
                 __syncthreads();
                 continue;
             }
             uint32_t p = s_wsum[warp] + x - lens;
 #pragma unroll
             for (int k = 0; k < kPer; k++) {
-                if (b0 + k >= Z) break;
+                if (b0 + k >= Z || p >= jr1) break;
                 const uint32_t b = Y[b0 + k];
-                if (b < kFirstRunCode) E[p] = (uint8_t)b;        // literal
+                if (b < kFirstRunCode && p >= jr0) E[p - jr0] = (uint8_t)b;   // literal
                 p += zre_len(b);
             }
         } else {
-            for (uint32_t q = threadIdx.x; q < P; q += kSmThreads) {
-                const uint8_t b = S.payload[q];
+            for (uint32_t q = threadIdx.x; q < pl; q += kSmThreads) {
+                const uint8_t b = S.payload[jr0 + q];
                 if (b > 242) s_bad = 1;
                 E[q] = b;
             }
@@ -297,12 +309,12 @@ tlc_small_decompress_kernel(const SegTable T) {
         }
         __syncthreads();
         // ---- decoding steps 1-4 and Eq. 3
-        for (uint32_t j = threadIdx.x; j < P; j += kSmThreads) {
-            const uint32_t b = E[j];
+        for (uint32_t jl = threadIdx.x; jl < pl; jl += kSmThreads) {
+            const uint32_t b = E[jl];
             const uint32_t nz = lut[b];
 #pragma unroll
             for (int i = 0; i < 5; i++) {
-                const uint32_t e = (uint32_t)(i * P) + j;
+                const uint32_t e = (uint32_t)(i * P) + jr0 + jl;
                 if (e >= n) break;
                 const float v = __uint_as_float(V[i][b]);
                 if (kMode == TLC_MODE_OVERWRITE) __stcs(S.out + e, v);
@@ -318,7 +330,7 @@ static size_t small_smem_compress(uint64_t max_n) {
 }
 static size_t small_smem_decompress(uint64_t max_n) {
     const uint64_t P = (max_n + 4) / 5;
-    return 2 * ((P + 15) & ~15ull);
+    return kSmPart + ((P + 15) & ~15ull);
 }
 
 // TLC_NO_SMALL=1 routes small tables through K1-K5 (A/B measurements)
@@ -356,10 +368,11 @@ int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
         attr = true;
     }
     KernelScope ks(kK7s, st);
-    const int grid = (int)tmin<uint64_t>((uint64_t)T.count, 65535);
+    const uint32_t parts = (uint32_t)(((T.max_n + 4) / 5 + kSmPart - 1) / kSmPart);
+    const int grid = (int)tmin<uint64_t>((uint64_t)T.count * parts, 65535);
     const size_t smem = small_smem_decompress(T.max_n);
-    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T);
-    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T);
+    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T, parts);
+    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T, parts);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
