@@ -168,6 +168,31 @@ struct K5Smem {
     unsigned int warp_sum[kK5Threads / 32];
 };
 
+// Without ZRE: the quartic bytes as sent, 16 per thread (one 128-bit load when aligned); a
+// byte > 242 is not a quartic code -> FORMAT, replaced by 121 meanwhile.  Out of
+// line so that the ZRE path's register allocation (and K5's occupancy) is unaffected.
+__device__ __noinline__ bool copy_quartic(uint8_t *E, const uint8_t *src, int tl) {
+    bool bad = false;
+    const int j = kK5BytesPerThread * threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && j + kK5BytesPerThread <= tl) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + j));
+        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const uint32_t m = __vcmpgtu4(w[c], 0xf2f2f2f2u);   // bytes > 242
+            if (m) { bad = true; w[c] = (w[c] & ~m) | (0x79797979u & m); }
+        }
+        *reinterpret_cast<uint4 *>(E + j) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+        for (int jl = j; jl < j + kK5BytesPerThread && jl < tl; jl++) {
+            uint8_t v = src[jl];
+            if (v > 242) { bad = true; v = kZeroGroup; }
+            E[jl] = v;
+        }
+    }
+    return bad;
+}
+
 // Expand the payload bytes covering output tile lt (positions [J0, J0+tl)) into
 // E[0, tl): 121 prefill, then only the literal bytes are written at their scanned
 // positions (zero-run codes expand to 121s).  seek points at the segment's seek
@@ -238,32 +263,16 @@ __device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, 
         }
         __syncthreads();                                  // warp_sum reuse; E complete
     } else {
-        // quartic bytes as sent: 16 per thread (one 128-bit load when aligned); a byte
-        // > 242 is not a quartic code -> FORMAT, replaced by 121 meanwhile
-        const uint8_t *src = payload + J0;
-        const int j = kK5BytesPerThread * threadIdx.x;
-        if ((reinterpret_cast<uintptr_t>(src) & 15u) == 0 && j + kK5BytesPerThread <= tl) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src + j));
-            uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const uint32_t m = __vcmpgtu4(w[c], 0xf2f2f2f2u);   // bytes > 242
-                if (m) { bad = true; w[c] = (w[c] & ~m) | (0x79797979u & m); }
-            }
-            *reinterpret_cast<uint4 *>(E + j) = make_uint4(w[0], w[1], w[2], w[3]);
-        } else {
-            for (int jl = j; jl < j + kK5BytesPerThread && jl < tl; jl++) {
-                uint8_t v = src[jl];
-                if (v > 242) { bad = true; v = kZeroGroup; }
-                E[jl] = v;
-            }
-        }
+        bad = copy_quartic(E, payload + J0, tl);
     }
     return __syncthreads_or(bad);
 }
 
+#ifndef TLC_K5_MINB
+#define TLC_K5_MINB 3
+#endif
 template <int kMode>
-__global__ void __launch_bounds__(kK5Threads)
+__global__ void __launch_bounds__(kK5Threads, TLC_K5_MINB)   // <= 85 registers: 3 CTAs per SM
 tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     __shared__ K5Smem sm;
     __shared__ uint64_t s_first[kSegCache];
