@@ -126,6 +126,31 @@ tlc_stoch_qe_kernel(const SegTable T, const unsigned int *maxkey, uint32_t seed_
             // first Philox round, so each thread keeps 16 kU bytes of t outstanding
             constexpr int kU = 4;
             for (uint32_t lb0 = threadIdx.x; lb0 < nb; lb0 += kU * kK2sThreads) {
+                const uint32_t lbl = lb0 + (kU - 1) * kK2sThreads;
+                if (vec && Q.fast && lbl < nb && 4 * (b0 + lbl) + 3 < n) {
+                    // all kU blocks exist and are aligned: no per-block guards
+                    float4 v[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; u++)
+                        v[u] = ld_stream4(reinterpret_cast<const float4 *>(S.t) + (b0 + lb0 + u * kK2sThreads));
+                    uint32_t d[kU];
+                    uint4 w[kU];
+                    bool unsure = false;
+#pragma unroll
+                    for (int u = 0; u < kU; u++) {
+                        const uint64_t b = b0 + lb0 + u * kK2sThreads;
+                        w[u] = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), step_lo, step_hi), key);
+                        d[u] = Q.digit_fast(v[u].x, w[u].x, unsure) | (Q.digit_fast(v[u].y, w[u].y, unsure) << 8) |
+                               (Q.digit_fast(v[u].z, w[u].z, unsure) << 16) | (Q.digit_fast(v[u].w, w[u].w, unsure) << 24);
+                    }
+                    if (unsure) {                        // rare: the IEEE quotient decides
+#pragma unroll
+                        for (int u = 0; u < kU; u++) d[u] = stoch_block_exact(Q, v[u], w[u], 4u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; u++) dig[i][lb0 + u * kK2sThreads] = d[u];
+                    continue;
+                }
                 float4 v[kU];
                 uint32_t valid[kU];
 #pragma unroll
