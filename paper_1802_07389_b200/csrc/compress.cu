@@ -284,11 +284,12 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int u
 // tensor batches go through tlc_quant_qe_kernel.
 constexpr int kBulkPos = 1024;                                   // quartic positions per tile
 constexpr int kBulkStages = 4;
+constexpr int kBulkRow = kBulkPos + 4;                          // + up to 3 leading elements (alignment)
 constexpr uint32_t kBulkPart = kBulkPos * 4;                     // bytes per partition segment
-constexpr uint32_t kBulkStageBytes = 10 * kBulkPart;             // t and err, five partitions
+constexpr uint32_t kBulkPartU = kBulkRow * 4;                    // ... of an unaligned partition (superset)
 
 struct BulkSmem {
-    float buf[kBulkStages][10][kBulkPos];
+    float buf[kBulkStages][10][kBulkRow];
     unsigned long long bar[kBulkStages];
 };
 
@@ -312,7 +313,10 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                  ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
 }
 
-template <class QT>
+// kAligned: P % 4 == 0, every partition segment starts 16-byte aligned.  Otherwise the
+// copy engine fetched the aligned superset starting sh_i = (i P) mod 4 elements early:
+// shared reads are scalar at offset sh_i and err goes back with 32-bit stores.
+template <bool kAligned, class QT>
 __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, const Seg &S, uint64_t j0,
                                              uint8_t *bytes, const QT &Q) {
     const int g = threadIdx.x;                       // group: positions j0 + 4g .. j0 + 4g + 3
@@ -320,10 +324,20 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
     uint32_t by[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 5; i++) {
-        const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i][4 * g]);
-        const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][5 + i][4 * g]);
-        const float tt[4] = {tv.x, tv.y, tv.z, tv.w};
-        const float ee[4] = {ev.x, ev.y, ev.z, ev.w};
+        const int sh = kAligned ? 0 : (int)(((uint64_t)i * P) & 3);
+        float tt[4], ee[4];
+        if (kAligned) {
+            const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i][4 * g]);
+            const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][5 + i][4 * g]);
+            tt[0] = tv.x; tt[1] = tv.y; tt[2] = tv.z; tt[3] = tv.w;
+            ee[0] = ev.x; ee[1] = ev.y; ee[2] = ev.z; ee[3] = ev.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                tt[c] = sm.buf[stage][i][sh + 4 * g + c];
+                ee[c] = sm.buf[stage][5 + i][sh + 4 * g + c];
+            }
+        }
         float r[4];
 #pragma unroll
         for (int c = 0; c < 4; c++) {
@@ -332,7 +346,13 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
             r[c] = Q.residual(u, q);                         // steps (a),(b)
             by[c] = by[c] * 3u + (uint32_t)(q + 1);          // steps 1, 6
         }
-        __stcs(reinterpret_cast<float4 *>(S.err + (uint64_t)i * P + j0) + g, make_float4(r[0], r[1], r[2], r[3]));
+        float *eo = S.err + (uint64_t)i * P + j0 + 4 * g;
+        if (kAligned) {
+            __stcs(reinterpret_cast<float4 *>(eo), make_float4(r[0], r[1], r[2], r[3]));
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; c++) __stcs(eo + c, r[c]);
+        }
     }
     reinterpret_cast<uint32_t *>(bytes + j0)[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
 }
@@ -366,14 +386,17 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
     const uint64_t P = S.P;
     const uint64_t mine = nbulk > blockIdx.x ? (nbulk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     __syncthreads();
+    const bool aligned = (P & 3) == 0;
+    const uint32_t part = aligned ? kBulkPart : kBulkPartU;
     auto issue = [&](uint64_t k) {
         const int st = (int)(k % kBulkStages);
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
-        mbar_expect_tx(&sm.bar[st], kBulkStageBytes);
+        mbar_expect_tx(&sm.bar[st], 10 * part);
 #pragma unroll
         for (int i = 0; i < 5; i++) {
-            bulk_load(sm.buf[st][i], S.t + (uint64_t)i * P + j0, kBulkPart, &sm.bar[st]);
-            bulk_load(sm.buf[st][5 + i], S.err + (uint64_t)i * P + j0, kBulkPart, &sm.bar[st]);
+            const uint64_t a = ((uint64_t)i * P + j0) & ~uint64_t(3);   // 16-byte aligned start
+            bulk_load(sm.buf[st][i], S.t + a, part, &sm.bar[st]);
+            bulk_load(sm.buf[st][5 + i], S.err + a, part, &sm.bar[st]);
         }
     };
     if (threadIdx.x == 0)
@@ -383,8 +406,13 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
-        if (Q.mode == 1) bulk_compute(sm, st, S, j0, bytes, QuantCmp(Q));
-        else bulk_compute(sm, st, S, j0, bytes, Q);
+        if (aligned) {
+            if (Q.mode == 1) bulk_compute<true>(sm, st, S, j0, bytes, QuantCmp(Q));
+            else bulk_compute<true>(sm, st, S, j0, bytes, Q);
+        } else {
+            if (Q.mode == 1) bulk_compute<false>(sm, st, S, j0, bytes, QuantCmp(Q));
+            else bulk_compute<false>(sm, st, S, j0, bytes, Q);
+        }
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
     }
@@ -799,12 +827,16 @@ static int g_k2_blocks = 0, g_k3_blocks = 0;
 
 // Complete bulk tiles of a one-segment table: positions j < min(P, n - 4P) have all five
 // elements; the bulk kernel takes whole K2 tiles of them (kT2 = 4 bulk tiles).
+// Complete bulk tiles of a one-segment table (aligned t and err): tiles of positions whose
+// five elements exist, with 4 elements of slack at the end of the last partition (an
+// unaligned partition is fetched as an aligned superset of up to 3 more elements); the
+// bulk kernel takes whole K2 tiles of them (kT2 = 4 bulk tiles).
 static uint64_t bulk_tiles(const SegTable &T, int use_zre) {
     if (T.count != 1) return 0;
     const Seg &S = T.one;
-    if (!(S.flags & kSegVec2) || S.P % 4 != 0) return 0;
+    if (!aligned16(S.t) || !aligned16(S.err)) return 0;
     if (!use_zre && !aligned4(S.payload)) return 0;
-    const uint64_t complete = S.n >= 4 * S.P ? tmin<uint64_t>(S.P, S.n - 4 * S.P) : 0;
+    const uint64_t complete = S.n >= 4 * S.P + 4 ? tmin<uint64_t>(S.P, S.n - 4 * S.P - 4) : 0;
     return (complete / T.sz.t2) * (T.sz.t2 / kBulkPos);
 }
 

@@ -112,6 +112,22 @@ def test_parity_misaligned(tlc, offset):
         check_case(tlc, t, err0, 1.0, False, offset=offset)
 
 
+@pytest.mark.parametrize("pmod", [0, 1, 2, 3])
+def test_parity_bulk_partition_alignment(tlc, pmod):
+    """Single tensors large enough for the bulk-copy (TMA) K2 path, with P = ceil(n/5) in every
+    residue mod 4: P % 4 != 0 makes every partition after the first start off a 16-byte
+    boundary (aligned-superset copies shifted by (i P) mod 4)."""
+    for base in (5 * 4096 * 4, 5 * 4096 * 37, 1 << 22):
+        P = -(-base // 5)
+        P += (pmod - P) % 4
+        for k in (0, 3):
+            n = 5 * P - k
+            t = synth.gaussian(n, 8, n)
+            err0 = (0.4 * synth.gaussian(n, 9, n)).astype(f32)
+            check_case(tlc, t, err0, 1.75, True)
+            check_case(tlc, t, err0, 1.0, False)
+
+
 def test_parity_runs_many_tiles(tlc):
     """Runs of 121 bytes (lengths 1..100, 14k+-1) crossing many tile edges."""
     for n in (5 * 2048 * 7 + 3, 5 * 2048 * 64, 999_999, 3_000_001):
