@@ -246,12 +246,15 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
 #endif
 __global__ void __launch_bounds__(kK2Threads, TLC_K2_MINB)
 tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
-                    uint8_t *__restrict__ scratch, uint64_t tile_begin) {
+                    uint8_t *__restrict__ scratch, uint64_t tile_begin, int skip_bulk) {
     __shared__ uint64_t s_first[kSegCache];
     pdl_trigger();
     seg_index_load<2>(T, s_first);
     pdl_wait();                                          // K1's max keys (or the bulk kernel's tiles)
-    for (uint64_t tile = tile_begin + blockIdx.x; tile < T.n2; tile += gridDim.x) {
+    // skip_bulk: the bulk kernel took the tiles of T.bulk_list; this kernel takes T.rest_list
+    const uint64_t nwork = skip_bulk ? T.n_rest : T.n2 - tile_begin;
+    for (uint64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const uint64_t tile = skip_bulk ? T.rest_list[w] : tile_begin + w;
         const int si = find_seg_c<2>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         float M;
@@ -412,6 +415,97 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
         } else {
             if (Q.mode == 1) bulk_compute<false>(sm, st, S, j0, bytes, QuantCmp(Q));
             else bulk_compute<false>(sm, st, S, j0, bytes, Q);
+        }
+        __syncthreads();                                 // every thread is done with this stage
+        if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
+    }
+}
+
+// The bulk kernel over a segment table: work item q is bulk tile q % per of K2 tile
+// list[q / per], per = t2 / 1024 (tiles chosen on the host by bulk_tile_ok;
+// tlc_quant_qe_kernel skips them).
+// Thread 0 resolves each item's segment when it issues the copies and leaves what the
+// compute needs in shared memory for that stage.
+struct BulkItem {
+    Seg S;
+    uint64_t j0;
+    int si, first;
+};
+
+__global__ void __launch_bounds__(kK2Threads, 1)
+tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
+                               uint8_t *__restrict__ scratch) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    BulkSmem &sm = *reinterpret_cast<BulkSmem *>(smem_raw);
+    __shared__ BulkItem s_item[kBulkStages];
+    __shared__ uint64_t s_first[kSegCache];
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    seg_index_load<2>(T, s_first);                       // (ends with __syncthreads)
+    pdl_wait();                                          // K1's max keys
+    // a CTA takes a contiguous run of items, so consecutive items mostly share a segment and
+    // thread 0 re-reads the segment's descriptor from global memory only when it changes
+    const uint32_t per = (uint32_t)(T.sz.t2 / kBulkPos);           // bulk tiles per K2 tile
+    const uint64_t nitems = per * T.n_bulk;
+    const uint64_t chunk = (nitems + gridDim.x - 1) / gridDim.x;
+    const uint64_t q0 = blockIdx.x * chunk;
+    const uint64_t mine = q0 < nitems ? tmin<uint64_t>(chunk, nitems - q0) : 0;
+    int cur_si = -1;
+    Seg cur{};
+    auto issue = [&](uint64_t k) {                       // thread 0
+        const int st = (int)(k % kBulkStages);
+        const uint64_t q = q0 + k;
+        const uint64_t tile = T.bulk_list[q / per];
+        const int si = (cur_si >= 0 && tile >= cur.k2 && tile < cur.k2 + (cur.P + T.sz.t2 - 1) / T.sz.t2)
+                           ? cur_si : find_seg_c<2>(T, tile, s_first);
+        if (si != cur_si) { cur = get_seg(T, si); cur_si = si; }
+        BulkItem &it = s_item[st];
+        it.si = si;
+        it.S = cur;
+        const uint64_t lt = tile - cur.k2;
+        it.j0 = lt * T.sz.t2 + (q % per) * (uint64_t)kBulkPos;
+        it.first = lt == 0 && (q % per) == 0;
+        const uint64_t P = cur.P;
+        const uint32_t part = (P & 3) == 0 ? kBulkPart : kBulkPartU;
+        mbar_expect_tx(&sm.bar[st], 10 * part);
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t a = ((uint64_t)i * P + it.j0) & ~uint64_t(3);   // 16-byte aligned start
+            bulk_load(sm.buf[st][i], cur.t + a, part, &sm.bar[st]);
+            bulk_load(sm.buf[st][5 + i], cur.err + a, part, &sm.bar[st]);
+        }
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t k = 0; k < mine && k < kBulkStages; k++) issue(k);
+    for (uint64_t k = 0; k < mine; k++) {
+        const int st = (int)(k % kBulkStages);
+        mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
+        const BulkItem &it = s_item[st];
+        const Seg &S = it.S;
+        float M;
+        const unsigned int status = scale_from_key(maxkey[it.si], s, M);   // Eq. 1, R6
+        if (it.first && threadIdx.x == 0) {
+            tlc_header *h = S.hdr;
+            h->M = M;
+            h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+            h->n = S.n;
+            h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;
+            h->status = status;
+            h->reserved = 0;
+        }
+        if (status == TLC_OK) {                          // else err untouched (R6)
+            uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
+            const Quant Q(M);
+            if ((S.P & 3) == 0) {
+                if (Q.mode == 1) bulk_compute<true>(sm, st, S, it.j0, bytes, QuantCmp(Q));
+                else bulk_compute<true>(sm, st, S, it.j0, bytes, Q);
+            } else {
+                if (Q.mode == 1) bulk_compute<false>(sm, st, S, it.j0, bytes, QuantCmp(Q));
+                else bulk_compute<false>(sm, st, S, it.j0, bytes, Q);
+            }
         }
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
@@ -890,23 +984,36 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
         KernelScope ks(kK2, st);
         const uint64_t nbulk = use_bulk() ? bulk_tiles(T, use_zre) : 0;
         uint64_t tile_begin = 0;
+        int skip_bulk = 0;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BulkSmem));
+            cudaFuncSetAttribute(tlc_quant_qe_bulk_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BulkSmem));
+            attr = true;
+        }
         if (nbulk) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(BulkSmem));
-                attr = true;
-            }
             const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);
             launch_pdl(tlc_quant_qe_bulk_kernel, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s, use_zre, scratch,
                        nbulk);
             tile_begin = nbulk * kBulkPos / T.sz.t2;
+        } else if (use_bulk() && T.count > 1 && T.n_bulk && (use_zre || T.bulk_nozre_ok) &&
+                   T.sz.t2 == kLargeItems.t2) {
+            // large tables only: below 32M values (ResNet-50) the register kernel at 2 CTAs/SM
+            // measured faster (0.44 vs 0.49 ms per W=1 exchange step) than the 1-CTA/SM bulk one
+            const int grid = (int)tmin<uint64_t>(T.n_bulk * (T.sz.t2 / kBulkPos), (uint64_t)sms);
+            launch_pdl(tlc_quant_qe_bulk_table_kernel, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s, use_zre,
+                       scratch);
+            skip_bulk = 1;
         }
-        if (tile_begin < T.n2) {
+        const uint64_t nreg = skip_bulk ? T.n_rest : T.n2 - tile_begin;
+        if (nreg > 0) {
             if (!g_k2_blocks)
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
-            const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n2 - tile_begin, (uint64_t)sms * tmax(1, g_k2_blocks)));
-            launch_pdl(tlc_quant_qe_kernel, grid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin);
+            const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(nreg, (uint64_t)sms * tmax(1, g_k2_blocks)));
+            launch_pdl(tlc_quant_qe_kernel, grid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin,
+                       skip_bulk);
         }
     });
 }

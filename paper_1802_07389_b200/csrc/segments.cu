@@ -105,6 +105,32 @@ int Table::upload() {
     for (Seg &s : host) s.flags = seg_flags(s);
     T.d = d;
     if (count == 1) T.one = host[0];
+    // the K2 tiles the bulk-copy kernel takes (count > 1; one tensor uses a tile range)
+    std::vector<uint64_t> list, rest;
+    bool nozre_ok = true;
+    if (count > 1) {
+        for (const Seg &s : host) {
+            const uint64_t nt = (s.P + T.sz.t2 - 1) / T.sz.t2;
+            bool any = false;
+            for (uint64_t lt = 0; lt < nt; lt++) {
+                if (bulk_tile_ok(s, lt, T.sz.t2)) { list.push_back(s.k2 + lt); any = true; }
+                else rest.push_back(s.k2 + lt);
+            }
+            if (any && !aligned4(s.payload)) nozre_ok = false;
+        }
+    }
+    if (d_bulk) { cudaFree(d_bulk); d_bulk = nullptr; }
+    if (!list.empty()) {
+        list.insert(list.end(), rest.begin(), rest.end());
+        if (cudaMalloc((void **)&d_bulk, list.size() * sizeof(uint64_t)) != cudaSuccess) return TLC_ERR_CUDA;
+        if (cudaMemcpy(d_bulk, list.data(), list.size() * sizeof(uint64_t), cudaMemcpyHostToDevice) != cudaSuccess)
+            return TLC_ERR_CUDA;
+    }
+    T.bulk_list = d_bulk;
+    T.n_bulk = list.size() - rest.size();
+    T.rest_list = d_bulk ? d_bulk + T.n_bulk : nullptr;
+    T.n_rest = d_bulk ? rest.size() : 0;
+    T.bulk_nozre_ok = nozre_ok ? 1 : 0;
     return cudaMemcpy(d, host.data(), host.size() * sizeof(Seg), cudaMemcpyHostToDevice) == cudaSuccess
                ? TLC_OK : TLC_ERR_CUDA;
 }
@@ -124,6 +150,8 @@ void Table::release() {
     if (d) cudaFree(d);
     if (d_first) cudaFree(d_first);
     d_first = nullptr;
+    if (d_bulk) cudaFree(d_bulk);
+    d_bulk = nullptr;
     if (own_ws && ws) cudaFree(ws);
     d = nullptr;
     ws = nullptr;

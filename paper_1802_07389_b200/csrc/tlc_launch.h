@@ -114,6 +114,11 @@ struct SegTable {
     ItemSizes sz;
     const uint64_t *first[5];       // device: first item of every segment, per kernel (count > 1)
     uint64_t max_n;                 // largest segment
+    const uint64_t *bulk_list;      // device: K2 tiles taken by the bulk (TMA) kernel (count > 1)
+    uint64_t n_bulk;                // entries of bulk_list
+    const uint64_t *rest_list;      // device: the other K2 tiles (the register kernel's, when bulk runs)
+    uint64_t n_rest;
+    int bulk_nozre_ok;              // every listed segment's payload is 4-byte aligned
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -135,6 +140,14 @@ int launch_decompress(const uint8_t *payload, tlc_header *hdr, uint64_t n, float
                       void *ws, cudaStream_t st);
 size_t decompress_workspace_bytes(uint64_t n);
 uint32_t seg_flags(const Seg &s);
+// K2 tile lt (t2 positions) of segment s can go through the bulk-copy kernel: t and err
+// 16-byte aligned, and all positions of the tile have their five elements with 4 elements
+// of slack at the end (unaligned partitions are fetched as aligned supersets).
+__host__ __device__ inline bool bulk_tile_ok(const Seg &s, uint64_t lt, uint64_t t2) {
+    if (!aligned16(s.t) || !aligned16(s.err)) return false;
+    const uint64_t complete = s.n >= 4 * s.P + 4 ? (s.P < s.n - 4 * s.P - 4 ? s.P : s.n - 4 * s.P - 4) : 0;
+    return (lt + 1) * t2 <= complete;
+}
 
 // A device-resident segment table with its workspace (batches, exchange).
 struct Table {
@@ -142,6 +155,7 @@ struct Table {
     std::vector<Seg> host;
     Seg *d = nullptr;
     uint64_t *d_first = nullptr;    // 5 x count first-item arrays
+    uint64_t *d_bulk = nullptr;     // eligible K2 tiles of the bulk kernel, then the rest
     SegTable T{};
     void *ws = nullptr;
     size_t ws_bytes = 0;

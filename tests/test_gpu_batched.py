@@ -96,3 +96,13 @@ def test_batched_format_error_writes_nothing(T):
     hs = ts.headers()
     assert hs[0]["status"] == 0 and hs[1]["status"] == T.TLC_ERR_FORMAT
     assert torch.all(outs[1] == 7.0)
+
+
+@pytest.mark.parametrize("use_zre", [True, False])
+def test_large_table_bulk_path(T, use_zre):
+    """A table of >= 32M values (large work items, like BERT-large's): its complete K2 tiles go
+    through the table form of the bulk-copy kernel, the rest through the register kernel;
+    partitions of every alignment (P mod 4 = 0..3), a tiny tensor, two error-feedback steps."""
+    sizes = [(1 << 24) + 3, (1 << 23) + 1, 1 << 22, (1 << 22) + 10, 1000, 70_001, (1 << 21) + 15]
+    assert sum(sizes) >= 32 << 20
+    _run_steps(T, sizes, 2, 1.75, use_zre, lambda k, n, step: synth.gaussian(n, 10, k, step))
