@@ -291,8 +291,10 @@ constexpr int kBulkRow = kBulkPos + 4;                          // + up to 3 lea
 constexpr uint32_t kBulkPart = kBulkPos * 4;                     // bytes per partition segment
 constexpr uint32_t kBulkPartU = kBulkRow * 4;                    // ... of an unaligned partition (superset)
 
+// A stage holds the ten partition segments (t, err) back to back, kBulkPos floats apart for
+// aligned partitions and kBulkRow apart for supersets (row(i) below).
 struct BulkSmem {
-    float buf[kBulkStages][10][kBulkRow];
+    float buf[kBulkStages][10 * kBulkRow];
     unsigned long long bar[kBulkStages];
 };
 
@@ -330,15 +332,15 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
         const int sh = kAligned ? 0 : (int)(((uint64_t)i * P) & 3);
         float tt[4], ee[4];
         if (kAligned) {
-            const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i][4 * g]);
-            const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][5 + i][4 * g]);
+            const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i * kBulkPos + 4 * g]);
+            const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][(5 + i) * kBulkPos + 4 * g]);
             tt[0] = tv.x; tt[1] = tv.y; tt[2] = tv.z; tt[3] = tv.w;
             ee[0] = ev.x; ee[1] = ev.y; ee[2] = ev.z; ee[3] = ev.w;
         } else {
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                tt[c] = sm.buf[stage][i][sh + 4 * g + c];
-                ee[c] = sm.buf[stage][5 + i][sh + 4 * g + c];
+                tt[c] = sm.buf[stage][i * kBulkRow + sh + 4 * g + c];
+                ee[c] = sm.buf[stage][(5 + i) * kBulkRow + sh + 4 * g + c];
             }
         }
         float r[4];
@@ -360,6 +362,7 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
     reinterpret_cast<uint32_t *>(bytes + j0)[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
 }
 
+template <bool kAligned>                                // P % 4 == 0: no superset, no shifts
 __global__ void __launch_bounds__(kK2Threads, 1)
 tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
                          uint8_t *__restrict__ scratch, uint64_t nbulk) {
@@ -389,17 +392,17 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
     const uint64_t P = S.P;
     const uint64_t mine = nbulk > blockIdx.x ? (nbulk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     __syncthreads();
-    const bool aligned = (P & 3) == 0;
-    const uint32_t part = aligned ? kBulkPart : kBulkPartU;
+    constexpr uint32_t part = kAligned ? kBulkPart : kBulkPartU;
+    constexpr int row = kAligned ? kBulkPos : kBulkRow;
     auto issue = [&](uint64_t k) {
         const int st = (int)(k % kBulkStages);
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
         mbar_expect_tx(&sm.bar[st], 10 * part);
 #pragma unroll
         for (int i = 0; i < 5; i++) {
-            const uint64_t a = ((uint64_t)i * P + j0) & ~uint64_t(3);   // 16-byte aligned start
-            bulk_load(sm.buf[st][i], S.t + a, part, &sm.bar[st]);
-            bulk_load(sm.buf[st][5 + i], S.err + a, part, &sm.bar[st]);
+            const uint64_t a = kAligned ? (uint64_t)i * P + j0 : ((uint64_t)i * P + j0) & ~uint64_t(3);
+            bulk_load(&sm.buf[st][i * row], S.t + a, part, &sm.bar[st]);
+            bulk_load(&sm.buf[st][(5 + i) * row], S.err + a, part, &sm.bar[st]);
         }
     };
     if (threadIdx.x == 0)
@@ -409,13 +412,8 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
-        if (aligned) {
-            if (Q.mode == 1) bulk_compute<true>(sm, st, S, j0, bytes, QuantCmp(Q));
-            else bulk_compute<true>(sm, st, S, j0, bytes, Q);
-        } else {
-            if (Q.mode == 1) bulk_compute<false>(sm, st, S, j0, bytes, QuantCmp(Q));
-            else bulk_compute<false>(sm, st, S, j0, bytes, Q);
-        }
+        if (Q.mode == 1) bulk_compute<kAligned>(sm, st, S, j0, bytes, QuantCmp(Q));
+        else bulk_compute<kAligned>(sm, st, S, j0, bytes, Q);
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
     }
@@ -474,8 +472,9 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
 #pragma unroll
         for (int i = 0; i < 5; i++) {
             const uint64_t a = ((uint64_t)i * P + it.j0) & ~uint64_t(3);   // 16-byte aligned start
-            bulk_load(sm.buf[st][i], cur.t + a, part, &sm.bar[st]);
-            bulk_load(sm.buf[st][5 + i], cur.err + a, part, &sm.bar[st]);
+            const int row = (P & 3) == 0 ? kBulkPos : kBulkRow;
+            bulk_load(&sm.buf[st][i * row], cur.t + a, part, &sm.bar[st]);
+            bulk_load(&sm.buf[st][(5 + i) * row], cur.err + a, part, &sm.bar[st]);
         }
     };
     if (threadIdx.x == 0)
@@ -987,7 +986,9 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
         int skip_bulk = 0;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(BulkSmem));
+            cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BulkSmem));
             cudaFuncSetAttribute(tlc_quant_qe_bulk_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BulkSmem));
@@ -995,8 +996,12 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
         }
         if (nbulk) {
             const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);
-            launch_pdl(tlc_quant_qe_bulk_kernel, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s, use_zre, scratch,
-                       nbulk);
+            if ((T.one.P & 3) == 0)
+                launch_pdl(tlc_quant_qe_bulk_kernel<true>, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s,
+                           use_zre, scratch, nbulk);
+            else
+                launch_pdl(tlc_quant_qe_bulk_kernel<false>, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s,
+                           use_zre, scratch, nbulk);
             tile_begin = nbulk * kBulkPos / T.sz.t2;
         } else if (use_bulk() && T.count > 1 && T.n_bulk && (use_zre || T.bulk_nozre_ok) &&
                    T.sz.t2 == kLargeItems.t2) {
