@@ -193,6 +193,82 @@ __device__ __noinline__ bool copy_quartic(uint8_t *E, const uint8_t *src, int tl
     return bad;
 }
 
+// The ZRE expansion of a tile in two halves, so that a caller with several payloads (K5m)
+// can have every source's loads in flight before the first scan:
+//  expand_load  -- this thread's window words of the payload bytes covering the tile
+//                  (seek entries -> payload: two dependent global accesses);
+//  expand_scan  -- 121 prefill, expansion-length scan over the block, literal scatter.
+constexpr int kK5NW = kK5Words + 1;
+struct ExpandWin {
+    uint32_t wd[kK5NW];
+    int skip, wl, sh;
+};
+
+__device__ __forceinline__ void expand_load(ExpandWin &X, const uint8_t *payload, uint64_t Z,
+                                            const unsigned long long *seek, uint64_t lt, uint64_t ntiles) {
+    const unsigned long long sk = seek[lt];
+    const uint64_t bi = sk >> 4;                          // payload byte covering J0
+    X.skip = (int)(sk & 15);                              // J0 - (first position of that byte)
+    const uint64_t be = lt + 1 < ntiles ? (seek[lt + 1] >> 4) : Z - 1;   // last byte needed
+    X.wl = (int)(be - bi) + 1;                            // <= kT5 + 1
+    // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
+    // to 4; the last thread also owns the next 4 bytes, so the <= kT5 bytes from bi
+    // on are always covered
+    const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;
+    const uint64_t w0 = bi & ~3ull;
+    X.sh = (int)(bi - w0);
+    const int nwords = threadIdx.x == kK5Threads - 1 ? kK5NW : kK5Words;
+#pragma unroll
+    for (int h = 0; h < kK5NW; h++) {
+        X.wd[h] = 0;
+        if (h >= nwords) continue;
+        const int r = kK5BytesPerThread * threadIdx.x + 4 * h - X.sh;   // window offset of the word
+        if (pal && r >= 0 && r + 3 < X.wl) {
+            X.wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + kK5Words * threadIdx.x + h);
+        } else {
+            uint32_t x = 0;
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                if (r + c >= 0 && r + c < X.wl) x |= (uint32_t)payload[bi + r + c] << (8 * c);
+            X.wd[h] = x;
+        }
+    }
+}
+
+__device__ __forceinline__ void expand_scan(uint8_t *E, unsigned int *warp_sum, const ExpandWin &X, int tl) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    *reinterpret_cast<uint4 *>(E + kK5BytesPerThread * threadIdx.x) =
+        make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
+    const int nwords = threadIdx.x == kK5Threads - 1 ? kK5NW : kK5Words;
+    uint32_t len[4 * kK5NW], sum = 0;
+#pragma unroll
+    for (int m = 0; m < 4 * kK5NW; m++) {
+        const int r = kK5BytesPerThread * threadIdx.x + m - X.sh;
+        const uint32_t b = (X.wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+        len[m] = (m < 4 * nwords && r >= 0 && r < X.wl) ? zre_len(b) : 0u;
+        sum += len[m];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) warp_sum[warp] = x;
+    __syncthreads();
+    uint32_t wofs = 0;
+#pragma unroll
+    for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? warp_sum[w] : 0u;
+    int p = (int)(wofs + x - sum) - X.skip;   // tile position of this thread's first byte
+#pragma unroll
+    for (int m = 0; m < 4 * kK5NW; m++) {
+        const uint32_t b = (X.wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+        if (len[m] == 1 && p >= 0 && p < tl) E[p] = (uint8_t)b;   // literal byte
+        p += (int)len[m];
+    }
+    __syncthreads();                                      // warp_sum reuse; E complete
+}
+
 // Expand the payload bytes covering output tile lt (positions [J0, J0+tl)) into
 // E[0, tl): 121 prefill, then only the literal bytes are written at their scanned
 // positions (zero-run codes expand to 121s).  seek points at the segment's seek
@@ -201,67 +277,11 @@ __device__ __noinline__ bool copy_quartic(uint8_t *E, const uint8_t *src, int tl
 __device__ __forceinline__ bool expand_tile(uint8_t *E, unsigned int *warp_sum, const uint8_t *payload,
                                             bool zre, uint64_t Z, const unsigned long long *seek,
                                             uint64_t lt, uint64_t ntiles, uint64_t J0, int tl) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     bool bad = false;
     if (zre) {
-        *reinterpret_cast<uint4 *>(E + kK5BytesPerThread * threadIdx.x) =
-            make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
-        const unsigned long long sk = seek[lt];
-        const uint64_t bi = sk >> 4;                      // payload byte covering J0
-        const int skip = (int)(sk & 15);                  // J0 - (first position of that byte)
-        const uint64_t be = lt + 1 < ntiles ? (seek[lt + 1] >> 4) : Z - 1;   // last byte needed
-        const int wl = (int)(be - bi) + 1;                // <= kT5 + 1
-        // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
-        // to 4; the last thread also owns the next 4 bytes, so the <= kT5 bytes from bi
-        // on are always covered
-        const bool pal = (reinterpret_cast<uintptr_t>(payload) & 3u) == 0;
-        const uint64_t w0 = bi & ~3ull;
-        const int sh = (int)(bi - w0);
-        constexpr int NW = kK5Words + 1;
-        const int nwords = threadIdx.x == kK5Threads - 1 ? NW : kK5Words;
-        uint32_t wd[NW];
-#pragma unroll
-        for (int h = 0; h < NW; h++) {
-            wd[h] = 0;
-            if (h >= nwords) continue;
-            const int r = kK5BytesPerThread * threadIdx.x + 4 * h - sh;   // window offset of the word
-            if (pal && r >= 0 && r + 3 < wl) {
-                wd[h] = __ldg(reinterpret_cast<const uint32_t *>(payload + w0) + kK5Words * threadIdx.x + h);
-            } else {
-                uint32_t x = 0;
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    if (r + c >= 0 && r + c < wl) x |= (uint32_t)payload[bi + r + c] << (8 * c);
-                wd[h] = x;
-            }
-        }
-        uint32_t len[4 * NW], sum = 0;
-#pragma unroll
-        for (int m = 0; m < 4 * NW; m++) {
-            const int r = kK5BytesPerThread * threadIdx.x + m - sh;
-            const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-            len[m] = (m < 4 * nwords && r >= 0 && r < wl) ? zre_len(b) : 0u;
-            sum += len[m];
-        }
-        uint32_t x = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        if (lane == 31) warp_sum[warp] = x;
-        __syncthreads();
-        uint32_t wofs = 0;
-#pragma unroll
-        for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? warp_sum[w] : 0u;
-        int p = (int)(wofs + x - sum) - skip;   // tile position of this thread's first byte
-#pragma unroll
-        for (int m = 0; m < 4 * NW; m++) {
-            const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-            if (len[m] == 1 && p >= 0 && p < tl) E[p] = (uint8_t)b;   // literal byte
-            p += (int)len[m];
-        }
-        __syncthreads();                                  // warp_sum reuse; E complete
+        ExpandWin X;
+        expand_load(X, payload, Z, seek, lt, ntiles);
+        expand_scan(E, warp_sum, X, tl);
     } else {
         bad = copy_quartic(E, payload + J0, tl);
     }
@@ -406,6 +426,10 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
 // n); X = the W x |A| received (payload, header) rows, row w*|A| + q, whose
 // seek entries K4 wrote.  A source whose header is not OK contributes nothing.
 constexpr int kMaxSources = 8;
+#ifndef TLC_K5M_G
+#define TLC_K5M_G 1
+#endif
+constexpr int kK5mG = TLC_K5M_G;                    // sources whose loads are in flight together
 
 // Dynamic shared memory, sized for W sources: E[W][kT5] bytes, then
 // V[W][5][256] words (V[w][i][b] = M_w * (digit_i(b) - 1): +0 for a zero trit).
@@ -413,7 +437,7 @@ struct K5mHead {
     int ok[kMaxSources];
     unsigned int warp_sum[kK5Threads / 32];
 };
-constexpr int kK5mSegCache = 128;
+constexpr int kK5mSegCache = kSegCache;               // owned contexts (all 150 of BERT-large at W = 1)
 __host__ __device__ constexpr size_t k5m_smem_bytes(int W) {
     return sizeof(K5mHead) + (size_t)W * kT5 + (size_t)W * 5 * 256 * sizeof(uint32_t);
 }
@@ -451,16 +475,37 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
         const uint64_t J0 = lt * kT5;
         const int tl = (int)tmin<uint64_t>(kT5, P - J0);
         __syncthreads();                                   // previous tile's readers are done
-        for (int w = 0; w < W; w++) {
-            const Seg R = get_seg(X, w * A.count + q);
-            const tlc_header *h = R.hdr;
-            const bool ok = h->status == TLC_OK;           // uniform
-            if (threadIdx.x == 0) sm.ok[w] = ok;
-            if (!ok) continue;
-            if (q != cur) build_values(V[w], h->M);
-            const bool bad = expand_tile(E[w], sm.warp_sum, R.payload, (h->flags & TLC_FLAG_ZRE) != 0,
-                                         h->payload_len, seek + R.k5, lt, ntiles, J0, tl);
-            if (bad && threadIdx.x == 0) { raise_format(R.hdr); sm.ok[w] = 0; }
+        // sources in groups of kK5mG: every source's header, seek and payload-window loads of a
+        // group are in flight together (in peer-memory mode they cross NVLink), then the scans
+        for (int w0 = 0; w0 < W; w0 += kK5mG) {
+            ExpandWin Xw[kK5mG];
+            bool okw[kK5mG], zw[kK5mG];
+            const uint8_t *pw[kK5mG];
+            tlc_header *hw[kK5mG];
+#pragma unroll
+            for (int g = 0; g < kK5mG; g++) {
+                const int w = w0 + g;
+                okw[g] = false;
+                if (w >= W) continue;
+                const Seg R = get_seg(X, w * A.count + q);
+                hw[g] = R.hdr;
+                pw[g] = R.payload;
+                okw[g] = R.hdr->status == TLC_OK;          // uniform
+                zw[g] = (R.hdr->flags & TLC_FLAG_ZRE) != 0;
+                if (okw[g] && zw[g]) expand_load(Xw[g], R.payload, R.hdr->payload_len, seek + R.k5, lt, ntiles);
+            }
+#pragma unroll
+            for (int g = 0; g < kK5mG; g++) {
+                const int w = w0 + g;
+                if (w >= W) continue;
+                if (threadIdx.x == 0) sm.ok[w] = okw[g];
+                if (!okw[g]) continue;
+                if (q != cur) build_values(V[w], hw[g]->M);
+                bool bad = false;
+                if (zw[g]) expand_scan(E[w], sm.warp_sum, Xw[g], tl);
+                else bad = __syncthreads_or(copy_quartic(E[w], pw[g] + J0, tl));
+                if (bad && threadIdx.x == 0) { raise_format(hw[g]); sm.ok[w] = 0; }
+            }
         }
         cur = q;
         __syncthreads();
