@@ -322,10 +322,9 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // copy engine fetched the aligned superset starting sh_i = (i P) mod 4 elements early:
 // shared reads are scalar at offset sh_i and err goes back with 32-bit stores.
 template <bool kAligned, class QT>
-__device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, const Seg &S, uint64_t j0,
+__device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, float *err, uint64_t P, uint64_t j0,
                                              uint8_t *bytes, const QT &Q) {
     const int g = threadIdx.x;                       // group: positions j0 + 4g .. j0 + 4g + 3
-    const uint64_t P = S.P;
     uint32_t by[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 5; i++) {
@@ -351,10 +350,10 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, cons
             r[c] = Q.residual(u, q);                         // steps (a),(b)
             by[c] = by[c] * 3u + (uint32_t)(q + 1);          // steps 1, 6
         }
-        float *eo = S.err + (uint64_t)i * P + j0 + 4 * g;
         if (kAligned) {
-            __stcs(reinterpret_cast<float4 *>(eo), make_float4(r[0], r[1], r[2], r[3]));
-        } else {
+            __stcs(reinterpret_cast<float4 *>(err + (uint64_t)i * P + j0 + 4 * g), make_float4(r[0], r[1], r[2], r[3]));
+        } else {                                     // 32-bit stores (a lane-shuffled realignment
+            float *eo = err + (uint64_t)i * P + j0 + 4 * g;   // to 16-byte stores measured slower)
 #pragma unroll
             for (int c = 0; c < 4; c++) __stcs(eo + c, r[c]);
         }
@@ -412,23 +411,35 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
-        if (Q.mode == 1) bulk_compute<kAligned>(sm, st, S, j0, bytes, QuantCmp(Q));
-        else bulk_compute<kAligned>(sm, st, S, j0, bytes, Q);
+        if (Q.mode == 1) bulk_compute<kAligned>(sm, st, S.err, P, j0, bytes, QuantCmp(Q));
+        else bulk_compute<kAligned>(sm, st, S.err, P, j0, bytes, Q);
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
     }
 }
 
-// The bulk kernel over a segment table: work item q is bulk tile q % per of K2 tile
-// list[q / per], per = t2 / 1024 (tiles chosen on the host by bulk_tile_ok;
-// tlc_quant_qe_kernel skips them).
+// The bulk kernel over a segment table: work item q is bulk tile q % kBulkPer of K2 tile
+// list[q / kBulkPer] (tiles of kLargeItems.t2 positions, chosen on the host by
+// bulk_tile_ok; tlc_quant_qe_kernel skips them).
 // Thread 0 resolves each item's segment when it issues the copies and leaves what the
-// compute needs in shared memory for that stage.
+// compute needs in shared memory for that stage.  Everything on that thread's per-item path
+// is shared-memory reads and shifts: the other warps wait for it at the stage barrier.
 struct BulkItem {
-    Seg S;
-    uint64_t j0;
-    int si, first;
+    float *err;
+    uint8_t *bytes;                                      // quartic bytes: payload or ZRE scratch
+    tlc_header *hdr;
+    uint64_t n, P, j0;
+    float M;
+    unsigned int status;
+    int first;
 };
+constexpr uint64_t kBulkT2 = kLargeItems.t2;             // the launch requires T.sz.t2 == kBulkT2
+constexpr uint32_t kBulkPer = (uint32_t)(kBulkT2 / kBulkPos);   // bulk tiles per K2 tile
+static_assert(kBulkT2 % kBulkPos == 0, "K2 tile of whole bulk tiles");
+// K2 tiles of a CTA's contiguous run of items held in shared memory (BERT-large: ~111 per
+// CTA), loaded before K1 finishes: the per-item list read from global memory was a dependent
+// load on every item's critical path (0.78 -> 0.73 ms per BERT-large K2)
+constexpr int kBulkTileCache = 1024;
 
 __global__ void __launch_bounds__(kK2Threads, 1)
 tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
@@ -437,43 +448,56 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
     BulkSmem &sm = *reinterpret_cast<BulkSmem *>(smem_raw);
     __shared__ BulkItem s_item[kBulkStages];
     __shared__ uint64_t s_first[kSegCache];
+    __shared__ uint64_t s_tiles[kBulkTileCache];
     pdl_trigger();
     if (threadIdx.x == 0) {
         for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    seg_index_load<2>(T, s_first);                       // (ends with __syncthreads)
-    pdl_wait();                                          // K1's max keys
     // a CTA takes a contiguous run of items, so consecutive items mostly share a segment and
-    // thread 0 re-reads the segment's descriptor from global memory only when it changes
-    const uint32_t per = (uint32_t)(T.sz.t2 / kBulkPos);           // bulk tiles per K2 tile
-    const uint64_t nitems = per * T.n_bulk;
+    // thread 0 re-reads the segment's descriptor and max key only when it changes
+    const uint64_t nitems = kBulkPer * T.n_bulk;
     const uint64_t chunk = (nitems + gridDim.x - 1) / gridDim.x;
     const uint64_t q0 = blockIdx.x * chunk;
     const uint64_t mine = q0 < nitems ? tmin<uint64_t>(chunk, nitems - q0) : 0;
-    int cur_si = -1;
-    Seg cur{};
+    const uint64_t tl0 = q0 / kBulkPer;                  // first list entry of the run
+    const uint64_t ntl = mine ? (q0 + mine - 1) / kBulkPer - tl0 + 1 : 0;
+    for (uint64_t i = threadIdx.x; i < ntl && i < kBulkTileCache; i += blockDim.x) s_tiles[i] = T.bulk_list[tl0 + i];
+    seg_index_load<2>(T, s_first);                       // (ends with __syncthreads)
+    pdl_wait();                                          // K1's max keys
+    uint64_t cur_k2 = 1, cur_end = 0;                    // K2 tiles [cur_k2, cur_end) of the current segment
+    BulkItem cur{};
+    const float *cur_t = nullptr;
     auto issue = [&](uint64_t k) {                       // thread 0
         const int st = (int)(k % kBulkStages);
         const uint64_t q = q0 + k;
-        const uint64_t tile = T.bulk_list[q / per];
-        const int si = (cur_si >= 0 && tile >= cur.k2 && tile < cur.k2 + (cur.P + T.sz.t2 - 1) / T.sz.t2)
-                           ? cur_si : find_seg_c<2>(T, tile, s_first);
-        if (si != cur_si) { cur = get_seg(T, si); cur_si = si; }
-        BulkItem &it = s_item[st];
-        it.si = si;
-        it.S = cur;
-        const uint64_t lt = tile - cur.k2;
-        it.j0 = lt * T.sz.t2 + (q % per) * (uint64_t)kBulkPos;
-        it.first = lt == 0 && (q % per) == 0;
+        const uint64_t e = q / kBulkPer - tl0;
+        const uint64_t tile = e < kBulkTileCache ? s_tiles[e] : T.bulk_list[q / kBulkPer];
+        if (tile < cur_k2 || tile >= cur_end) {          // segment change: global reads
+            const int si = find_seg_c<2>(T, tile, s_first);
+            const Seg S = get_seg(T, si);
+            cur_t = S.t;
+            cur.err = S.err;
+            cur.bytes = use_zre ? scratch + S.bytes_off : S.payload;
+            cur.hdr = S.hdr;
+            cur.n = S.n;
+            cur.P = S.P;
+            cur.status = scale_from_key(maxkey[si], s, cur.M);   // Eq. 1, R6
+            cur_k2 = S.k2;
+            cur_end = S.k2 + (S.P + kBulkT2 - 1) / kBulkT2;
+        }
+        const uint64_t lt = tile - cur_k2;
+        cur.j0 = lt * kBulkT2 + (q % kBulkPer) * (uint64_t)kBulkPos;
+        cur.first = lt == 0 && (q % kBulkPer) == 0;
+        s_item[st] = cur;
         const uint64_t P = cur.P;
         const uint32_t part = (P & 3) == 0 ? kBulkPart : kBulkPartU;
+        const int row = (P & 3) == 0 ? kBulkPos : kBulkRow;
         mbar_expect_tx(&sm.bar[st], 10 * part);
 #pragma unroll
         for (int i = 0; i < 5; i++) {
-            const uint64_t a = ((uint64_t)i * P + it.j0) & ~uint64_t(3);   // 16-byte aligned start
-            const int row = (P & 3) == 0 ? kBulkPos : kBulkRow;
-            bulk_load(&sm.buf[st][i * row], cur.t + a, part, &sm.bar[st]);
+            const uint64_t a = ((uint64_t)i * P + cur.j0) & ~uint64_t(3);   // 16-byte aligned start
+            bulk_load(&sm.buf[st][i * row], cur_t + a, part, &sm.bar[st]);
             bulk_load(&sm.buf[st][(5 + i) * row], cur.err + a, part, &sm.bar[st]);
         }
     };
@@ -483,27 +507,25 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
         const BulkItem &it = s_item[st];
-        const Seg &S = it.S;
-        float M;
-        const unsigned int status = scale_from_key(maxkey[it.si], s, M);   // Eq. 1, R6
+        const float M = it.M;
+        const unsigned int status = it.status;
         if (it.first && threadIdx.x == 0) {
-            tlc_header *h = S.hdr;
+            tlc_header *h = it.hdr;
             h->M = M;
             h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
-            h->n = S.n;
-            h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;
+            h->n = it.n;
+            h->payload_len = (status == TLC_OK && !use_zre) ? it.P : 0;
             h->status = status;
             h->reserved = 0;
         }
         if (status == TLC_OK) {                          // else err untouched (R6)
-            uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
             const Quant Q(M);
-            if ((S.P & 3) == 0) {
-                if (Q.mode == 1) bulk_compute<true>(sm, st, S, it.j0, bytes, QuantCmp(Q));
-                else bulk_compute<true>(sm, st, S, it.j0, bytes, Q);
+            if ((it.P & 3) == 0) {
+                if (Q.mode == 1) bulk_compute<true>(sm, st, it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
+                else bulk_compute<true>(sm, st, it.err, it.P, it.j0, it.bytes, Q);
             } else {
-                if (Q.mode == 1) bulk_compute<false>(sm, st, S, it.j0, bytes, QuantCmp(Q));
-                else bulk_compute<false>(sm, st, S, it.j0, bytes, Q);
+                if (Q.mode == 1) bulk_compute<false>(sm, st, it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
+                else bulk_compute<false>(sm, st, it.err, it.P, it.j0, it.bytes, Q);
             }
         }
         __syncthreads();                                 // every thread is done with this stage

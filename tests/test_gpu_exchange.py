@@ -16,13 +16,24 @@ SIZES = [432, 2304, 9216, 36864, 640, 200_003, 1_000_000]
 S, STEPS = 1.75, 3
 
 
-def _grads(r, step, sizes=SIZES):
+def _grads(r, step, sizes=SIZES, kind="gauss"):
     import synth
 
+    if kind == "sparse":
+        # zero tiles next to nonzero ones in every payload: runs of zero groups crossing
+        # decoder tiles, an all-zero tensor, and a gaussian one (owners skip zero windows)
+        def block_sparse(n, t):
+            g = synth.gaussian(n, 95, r, t, step)
+            j = np.arange(n) % -(-n // 5)              # quartic position of each element
+            g[(j // 10000) % 2 == 1] = 0.0              # zero groups in blocks over two tiles wide
+            return g
+
+        return [synth.zeros(n) if t % 3 == 1 else block_sparse(n, t) if t % 3 == 0 else
+                synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
     return [synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
 
 
-def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False):
+def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False, kind="gauss"):
     """One rank's exchange; returns per-step means (owned flat) and final state.
     graph=True: step 0 runs eagerly (it uploads the descriptor tables), then push and
     pull are captured once as CUDA graphs over fixed gradient buffers and replayed."""
@@ -38,7 +49,7 @@ def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False):
     owned_per_step = []
     gpush = gpull = None
     for step in range(steps):
-        for b, a in zip(gs, _grads(rank, step, sizes)):
+        for b, a in zip(gs, _grads(rank, step, sizes, kind)):
             b.copy_(torch.from_numpy(a))
         if gpush is None:
             x.push(gs, S)
@@ -65,14 +76,14 @@ def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False):
     return res
 
 
-def _check(world, results, sizes=SIZES, steps=STEPS):
+def _check(world, results, sizes=SIZES, steps=STEPS, kind="gauss"):
     from oracle import exchange as X
 
     ps = X.VirtualPS(sizes, world)
     outs = [[np.zeros(n, f32) for n in sizes] for _ in range(world)]
     means_steps = []
     for step in range(steps):
-        means, _ = ps.push([_grads(r, step, sizes) for r in range(world)], S)
+        means, _ = ps.push([_grads(r, step, sizes, kind) for r in range(world)], S)
         ps.pull(means, outs, S)
         means_steps.append(means)
     for r in range(world):
@@ -100,7 +111,13 @@ def test_exchange_w1_in_process(p2p, graph):
     _check(1, [_run_rank(0, 1, STEPS, p2p=p2p, graph=graph)])
 
 
-def _mp_worker(rank, world, port, q, p2p, graph=False):
+def test_exchange_w1_sparse_gradients():
+    """Payloads with all-zero decoder tiles between nonzero ones (the owners' aggregate and
+    the pull's skip-zero apply skip those tiles' expansion), W = 1 in process."""
+    _check(1, [_run_rank(0, 1, STEPS, p2p=True, kind="sparse")], kind="sparse")
+
+
+def _mp_worker(rank, world, port, q, p2p, graph=False, kind="gauss"):
     import torch
     import torch.distributed as dist
 
@@ -108,15 +125,16 @@ def _mp_worker(rank, world, port, q, p2p, graph=False):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph)
+        res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph, kind=kind)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("p2p,graph", [(False, False), (True, False), (True, True)])
+@pytest.mark.parametrize("p2p,graph,kind", [(False, False, "gauss"), (True, False, "gauss"), (True, True, "gauss"),
+                                            (True, False, "sparse")])
 @pytest.mark.parametrize("world", [2, 4])
-def test_exchange_multi_gpu(world, p2p, graph):
+def test_exchange_multi_gpu(world, p2p, graph, kind):
     import torch
     import torch.multiprocessing as mp
 
@@ -128,14 +146,14 @@ def test_exchange_multi_gpu(world, p2p, graph):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph)) for r in range(world)]
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph, kind)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    _check(world, results)
+    _check(world, results, kind=kind)
 
 
 def test_nccl_transport_refuses_capture():
