@@ -286,7 +286,10 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int u
 // complete tiles of a single aligned tensor (P % 4 == 0); the ragged tail and
 // tensor batches go through tlc_quant_qe_kernel.
 constexpr int kBulkPos = 1024;                                   // quartic positions per tile
-constexpr int kBulkStages = 4;
+#ifndef TLC_K2_STAGES
+#define TLC_K2_STAGES 4                                  // 5 measured slower (C3 K2 0.518 -> 0.523 ms)
+#endif
+constexpr int kBulkStages = TLC_K2_STAGES;
 constexpr int kBulkRow = kBulkPos + 4;                          // + up to 3 leading elements (alignment)
 constexpr uint32_t kBulkPart = kBulkPos * 4;                     // bytes per partition segment
 constexpr uint32_t kBulkPartU = kBulkRow * 4;                    // ... of an unaligned partition (superset)

@@ -249,36 +249,50 @@ __device__ __forceinline__ bool window_nonzero(const ExpandWin &X) {
     return nz;
 }
 
+// kWarpSkip: warps whose bytes all lie past the window only prefill.  Used by the ACCUMULATE
+// decoder, which is instruction-bound on sparse tiles (pull apply 0.201 -> 0.185 ms per
+// BERT-large W = 1 step); the store-bound OVERWRITE decoder measured 2 % slower with it.
+template <bool kWarpSkip = false>
 __device__ __forceinline__ void expand_scan(uint8_t *E, unsigned int *warp_sum, const ExpandWin &X, int tl) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     *reinterpret_cast<uint4 *>(E + kK5BytesPerThread * threadIdx.x) =
         make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
     const int nwords = threadIdx.x == kK5Threads - 1 ? kK5NW : kK5Words;
-    uint32_t len[4 * kK5NW], sum = 0;
-#pragma unroll
-    for (int m = 0; m < 4 * kK5NW; m++) {
+    // warp-uniform: does any of the warp's bytes fall in the window?  A sparse tile's window is
+    // a few hundred bytes, so most warps only prefill (their bytes would all have length 0)
+    const bool wact = !kWarpSkip || kK5BytesPerThread * 32 * warp - X.sh < X.wl;
+    // expansion length of window byte m of this thread (0 outside the window); recomputed in
+    // the scatter below rather than kept live across the barrier (that spilled)
+    auto len = [&](int m) -> uint32_t {
         const int r = kK5BytesPerThread * threadIdx.x + m - X.sh;
         const uint32_t b = (X.wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-        len[m] = (m < 4 * nwords && r >= 0 && r < X.wl) ? zre_len(b) : 0u;
-        sum += len[m];
-    }
-    uint32_t x = sum;
+        return (m < 4 * nwords && r >= 0 && r < X.wl) ? zre_len(b) : 0u;
+    };
+    uint32_t sum = 0, x = 0;
+    if (wact) {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += y;
+        for (int m = 0; m < 4 * kK5NW; m++) sum += len(m);
+        x = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
     }
     if (lane == 31) warp_sum[warp] = x;
     __syncthreads();
-    uint32_t wofs = 0;
+    if (wact) {
+        uint32_t wofs = 0;
 #pragma unroll
-    for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? warp_sum[w] : 0u;
-    int p = (int)(wofs + x - sum) - X.skip;   // tile position of this thread's first byte
+        for (int w = 0; w < kK5Threads / 32; w++) wofs += (w < warp) ? warp_sum[w] : 0u;
+        int p = (int)(wofs + x - sum) - X.skip;   // tile position of this thread's first byte
 #pragma unroll
-    for (int m = 0; m < 4 * kK5NW; m++) {
-        const uint32_t b = (X.wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
-        if (len[m] == 1 && p >= 0 && p < tl) E[p] = (uint8_t)b;   // literal byte
-        p += (int)len[m];
+        for (int m = 0; m < 4 * kK5NW; m++) {
+            const uint32_t b = (X.wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+            const uint32_t l = len(m);
+            if (l == 1 && p >= 0 && p < tl) E[p] = (uint8_t)b;   // literal byte
+            p += (int)l;
+        }
     }
     __syncthreads();                                      // warp_sum reuse; E complete
 }
@@ -358,7 +372,7 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
             ExpandWin X;
             expand_load(X, payload, Z, seek + S.k5, lt, ntiles);
             if (!__syncthreads_or(window_nonzero(X))) continue;
-            expand_scan(sm.E, sm.warp_sum, X, tl);
+            expand_scan<true>(sm.E, sm.warp_sum, X, tl);
         }
         const bool bad = (kMode != TLC_MODE_OVERWRITE && zre)
                              ? false : expand_tile(sm.E, sm.warp_sum, payload, zre, Z, seek + S.k5, lt, ntiles, J0, tl);
