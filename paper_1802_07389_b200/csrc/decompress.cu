@@ -492,7 +492,10 @@ __device__ __forceinline__ void build_values(uint32_t (*V)[256], float M) {
     }
 }
 
-__global__ void __launch_bounds__(kK5Threads, 3)
+#ifndef TLC_K5M_MINB
+#define TLC_K5M_MINB 4                                   // 4 CTAs/SM (64 registers, 28 B spilled): K5m 0.298 -> 0.287 ms at N = 2, 0.370 -> 0.355 at W = 1; 2: 0.43
+#endif
+__global__ void __launch_bounds__(kK5Threads, TLC_K5M_MINB)
 tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint64_t s_first[kK5mSegCache];         // owned contexts: few per rank
