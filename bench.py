@@ -452,8 +452,14 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2
                "status": int(hst.max())}
     x.close()
     comm.close()
+    plan = T.tlc_plan(sizes, world)
+    # K2's algorithmic bytes per step on this rank: 12 n_c + ceil(n_c / 5) per compressed
+    # context (read t, err; write err, quartic bytes) -- every context in the push, the
+    # contexts this rank owns in the pull (the owner re-compresses the model delta)
+    k2_push = sum(12 * (hi - lo) + (hi - lo + 4) // 5 for (_, lo, hi, _) in plan)
+    k2_pull = sum(12 * (hi - lo) + (hi - lo + 4) // 5 for (_, lo, hi, ow) in plan if ow == rank)
     return {"ms": ms, "kernel_ms": kern_ms, "launches": launches, "wire": wire, "N": N, "status": status,
-            "contexts": len(T.tlc_plan(sizes, world)), "e2e": e2e,
+            "contexts": len(plan), "e2e": e2e, "k2_alg_bytes_per_step": k2_push + k2_pull,
             "kernels": {k: {"launches_per_step": c / steps, "ms_per_step": t / steps} for k, (c, t) in prof.items()}}
 
 
@@ -516,6 +522,23 @@ def run_exchange_leg(args, T, dev, world, rank, dist, e2e_steps=None):
         r["e2e"]["value"] = world * 4.0 * r["N"] / (ems / 1e3) / 1e9
         r["e2e"]["ms"] = ems
     return r, ms, value
+
+
+def exchange_roofline(r):
+    """roofline object of the exchange step's dominant kernel (K2 over the segment table,
+    push + pull launches) on this rank: algorithmic bytes per step / its device time per step."""
+    dom = "k2_quant_qe"
+    k = r["kernels"].get(dom)
+    if not k or not k["ms_per_step"]:
+        return None
+    peak, peak_src = load_peaks()
+    achieved = r["k2_alg_bytes_per_step"] / (k["ms_per_step"] / 1e3) / 1e9
+    return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+            "launches_per_step": k["launches_per_step"],
+            "alg_bytes_per_launch": r["k2_alg_bytes_per_step"] / k["launches_per_step"],
+            "alg_bytes_formula": "sum over compressed contexts of 12 n_c + ceil(n_c/5): all contexts (push) "
+                                 "+ the contexts this rank owns (pull), per step; rank 0"}
 
 
 # ------------------------------------------------------------------ the GPU leg
@@ -702,7 +725,7 @@ def run_tlc(args):
         r, xms, xval = run_exchange_leg(args, T, dev, 1, 0, None, e2e_steps=0)
         xw1 = {"workload": f"configs[4]: {args.model} gradient exchange (push+pull) at s={args.xs}, W=1",
                "value": xval, "unit": "GB/s", "ms_per_step": xms, "kernel_ms_per_step": r["kernel_ms"],
-               "status": r["status"]}
+               "roofline": exchange_roofline(r), "status": r["status"]}
 
     codecs = None
     if rank == 0 and world == 1 and not args.no_codecs:
@@ -787,6 +810,7 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             "wire_bytes_per_rank_per_step": r["wire"],
             "wire_definition": "bytes rank 0 received from other ranks per step (push + pull)",
             "nvlink_frac": pct_nvlink,
+            "roofline": exchange_roofline(r),
             "kernel_ms_per_step_rank0": r["kernel_ms"],
             "kernels_rank0": r["kernels"],
             "gpu_launches": r["launches"],
