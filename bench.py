@@ -347,7 +347,10 @@ def measure_codecs(T, dev, ts, steps=20, warmup=3):
                     "bits_per_value": 8.0 * Z / n, "status": h["status"],
                     "kernel_ms": {k: round(v, 5) for k, v in kern.items()},
                     "roofline": {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                                 "frac": ach / peak, "alg_bytes_formula": "4n + ceil(n/5)"}})
+                                 "frac": ach / peak, "alg_bytes_formula": "4n + ceil(n/5)",
+                                 "limiter": "instruction issue, not HBM: Philox4x32-10 (20 IMAD.WIDE + 20 LOP3 "
+                                            "per 4 values) + the exact-comparison digit, ~36 thread-instr per "
+                                            "value at ~60 % issue busy (ncu, profiles/r01_ncu_summary.md)"}})
     ms, kern, h = timed(int8_step)
     alg = {"k1_absmax": 4.0 * n, "kq8_int8_quant": 5.0 * n, "kd8_int8_dequant": 5.0 * n}
     doms = {k: alg[k] / (kern[k] / 1e3) / 1e9 for k in ("kq8_int8_quant", "kd8_int8_dequant")}
