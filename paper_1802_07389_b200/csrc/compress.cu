@@ -444,7 +444,19 @@ static_assert(kBulkT2 % kBulkPos == 0, "K2 tile of whole bulk tiles");
 // load on every item's critical path (0.78 -> 0.73 ms per BERT-large K2)
 constexpr int kBulkTileCache = 1024;
 
-__global__ void __launch_bounds__(kK2Threads, 1)
+// TLC_K2T_WS (default; -DTLC_K2T_NO_WS for the single-role kernel): a ninth (producer) warp
+// issues the copies; consumers release a stage by arriving on its `empty` mbarrier instead of
+// a block barrier, so they never wait for the issuing thread (40 % of the stall samples were
+// at that barrier: BERT-large W = 1 K2 1.415 -> 1.368 ms per step, tools/k2t_ws_check.sh).
+#if !defined(TLC_K2T_WS) && !defined(TLC_K2T_NO_WS)
+#define TLC_K2T_WS 1
+#endif
+#ifdef TLC_K2T_WS
+constexpr int kK2TThreads = kK2Threads + 32;
+#else
+constexpr int kK2TThreads = kK2Threads;
+#endif
+__global__ void __launch_bounds__(kK2TThreads, 1)
 tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, float s, int use_zre,
                                uint8_t *__restrict__ scratch) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -452,9 +464,15 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
     __shared__ BulkItem s_item[kBulkStages];
     __shared__ uint64_t s_first[kSegCache];
     __shared__ uint64_t s_tiles[kBulkTileCache];
+#ifdef TLC_K2T_WS
+    __shared__ unsigned long long s_empty[kBulkStages];
+#endif
     pdl_trigger();
     if (threadIdx.x == 0) {
         for (int st = 0; st < kBulkStages; st++) mbar_init(&sm.bar[st], 1);
+#ifdef TLC_K2T_WS
+        for (int st = 0; st < kBulkStages; st++) mbar_init(&s_empty[st], kK2Threads / 32);
+#endif
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // a CTA takes a contiguous run of items, so consecutive items mostly share a segment and
@@ -504,8 +522,20 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
             bulk_load(&sm.buf[st][(5 + i) * row], cur.err + a, part, &sm.bar[st]);
         }
     };
+#ifdef TLC_K2T_WS
+    if (threadIdx.x >= kK2Threads) {                     // producer warp
+        if (threadIdx.x == kK2Threads)
+            for (uint64_t k = 0; k < mine; k++) {
+                if (k >= kBulkStages)                    // consumers released the stage's last use
+                    mbar_wait(&s_empty[k % kBulkStages], (uint32_t)(((k / kBulkStages) - 1) & 1));
+                issue(k);
+            }
+        return;
+    }
+#else
     if (threadIdx.x == 0)
         for (uint64_t k = 0; k < mine && k < kBulkStages; k++) issue(k);
+#endif
     for (uint64_t k = 0; k < mine; k++) {
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
@@ -531,8 +561,14 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
                 else bulk_compute<false>(sm, st, it.err, it.P, it.j0, it.bytes, Q);
             }
         }
+#ifdef TLC_K2T_WS
+        __syncwarp();                                    // the warp is done with this stage
+        if ((threadIdx.x & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&s_empty[st])) : "memory");
+#else
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
+#endif
     }
 }
 
@@ -1033,7 +1069,7 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
             // large tables only: below 32M values (ResNet-50) the register kernel at 2 CTAs/SM
             // measured faster (0.44 vs 0.49 ms per W=1 exchange step) than the 1-CTA/SM bulk one
             const int grid = (int)tmin<uint64_t>(T.n_bulk * (T.sz.t2 / kBulkPos), (uint64_t)sms);
-            launch_pdl(tlc_quant_qe_bulk_table_kernel, grid, kK2Threads, sizeof(BulkSmem), st, T, maxkey, s, use_zre,
+            launch_pdl(tlc_quant_qe_bulk_table_kernel, grid, kK2TThreads, sizeof(BulkSmem), st, T, maxkey, s, use_zre,
                        scratch);
             skip_bulk = 1;
         }
