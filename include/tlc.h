@@ -238,12 +238,25 @@ int tlc_batch_decompress(tlc_batch *batch, int mode, void *stream);
  *                     outs: host array of num_tensors DEVICE pointers to
  *                     full-size fp32 tensors.
  * tlc_exchange_status synchronizes `stream` and returns the worst device status
- *                     over all received headers (NONFINITE/RANGE from a peer).
+ *                     of the last step: this rank's own pushes and every
+ *                     context's shared pull (which carries any rank's push
+ *                     failure, R24); with NCCL also the received pushes.
  * tlc_exchange_status_async  the same worst status, written by an async copy
  *                     enqueued on `stream` to `dst` (pinned host or device
  *                     memory, 4 bytes, owned by the caller); no host sync.
  * Push/pull enqueue on `stream`, allocate nothing and do not synchronize the
  * host (a descriptor upload happens when the grads/outs pointers change).
+ * Ordering: push and pull strictly alternate (push, pull, push, ...); a call out
+ * of turn returns TLC_ERR_ARG.  Every rank must issue its pushes and pulls on
+ * one stream: in peer-memory mode the two flag barriers of a step order both the
+ * reads of a rank's send/pull buffers by the other ranks and that rank's next
+ * overwrite of them, which holds only if nothing of the next phase can start
+ * before this rank's barrier kernel (stream order).
+ * Failed pushes (reading R24): if any rank's push of a context fails (NaN/Inf
+ * in u, M overflow, malformed payload), the owner's mean of that context is NaN
+ * (owned buffer), its pull compression then raises NONFINITE, and every rank's
+ * apply leaves that context's outputs untouched; tlc_exchange_status on every
+ * rank reports it.
  * CUDA graphs: in peer-memory mode a push or pull may be captured (stream
  * capture) once the grads/outs pointers have been seen by an eager call; the
  * flag-barrier epochs are counted on the device, so replays stay ordered.  The
@@ -284,6 +297,27 @@ int tlc_exchange_status_async(tlc_exchange *x, unsigned int *dst, void *stream);
  * producing GPU over NVLink.  Results are identical to the NCCL mode. */
 int tlc_exchange_ipc_handles(tlc_exchange *x, void *out);
 int tlc_exchange_ipc_open(tlc_exchange *x, const void *all);
+
+/* Loopback group (single GPU): `world` (1..8) virtual ranks of one exchange in
+ * one process on `device`, for testing and profiling the multi-source path on
+ * one B200.  Each virtual rank is a full tlc_exchange (tlc_loopback_rank: its
+ * error buffers, owned buffer and contexts through the tlc_exchange_* queries;
+ * tlc_exchange_push/pull on it return TLC_ERR_ARG) whose peers' buffers are
+ * plain device pointers.  tlc_loopback_push takes `grads`, a host array of
+ * world x num_tensors DEVICE pointers (rank-major: grads[r*num_tensors + i]),
+ * and runs every rank's push compression, then every owner's K4 + fused
+ * aggregation reading all ranks' payloads; tlc_loopback_pull likewise takes
+ * outs[r*num_tensors + i] and runs every owner's pull compression, then every
+ * rank's apply reading all owners' payloads.  Stream order replaces the flag
+ * barriers; results are those of a world-GPU exchange, bit for bit.  Push and
+ * pull alternate (TLC_ERR_ARG otherwise).  The group owns its ranks; destroy
+ * the group, not the ranks. */
+typedef struct tlc_loopback tlc_loopback;
+int tlc_loopback_create(tlc_loopback **group, int world, int num_tensors, const uint64_t *sizes, int device);
+int tlc_loopback_destroy(tlc_loopback *group);
+tlc_exchange *tlc_loopback_rank(tlc_loopback *group, int rank);
+int tlc_loopback_push(tlc_loopback *group, const float *const *grads, float s, int use_zre, void *stream);
+int tlc_loopback_pull(tlc_loopback *group, float *const *outs, float s, int use_zre, void *stream);
 
 /* Bytes this rank received from other ranks in the last push (out[0]) and pull
  * (out[1]): capacity regions + headers with NCCL; exactly the payload_len (+

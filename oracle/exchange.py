@@ -9,11 +9,13 @@ X1  plan: contexts (tensor, lo, hi, owner) -- reading R17, written here
 X2  every rank r compresses every context c with push_err[r][c] (Fig. steps 1-4).
 X3  the owner sums the W decompressed pushes in rank order starting from +0,
     adding M_w*q_w only where q_w != 0 (R15, R16), then divides by W in fp32
-    ("average the gradients", P:184-185).
+    ("average the gradients").  A context with a failed push (status
+    not OK: NaN/Inf in a rank's u, or M overflow) has a NaN mean (reading R24).
 X4  delta = mean (identity update in benchmarks, R18).
 X5  the owner compresses delta[c] ONCE with pull_err[c] (shared pull).
 X6  every rank applies every owner's payload to its full-size output with
-    decompress-ACCUMULATE; all ranks end bit-identical.
+    decompress-ACCUMULATE; all ranks end bit-identical.  A context whose shared
+    pull failed (R24: its NaN mean raises NONFINITE) is left untouched.
 """
 from __future__ import annotations
 
@@ -70,10 +72,12 @@ class VirtualPS:
                  for c, (t, lo, hi, _) in enumerate(self.ctx)] for r in range(W)]
         means = []
         for c, (t, lo, hi, owner) in enumerate(self.ctx):
+            if any(sent[w][c].status != 0 for w in range(W)):    # R24
+                means.append(np.full(hi - lo, np.nan, f32))
+                continue
             acc = np.zeros(hi - lo, f32)                     # +0
             for w in range(W):                                # rank order
                 p = sent[w][c]
-                assert p.status == 0, p.status
                 st, acc = decompress(p.payload, use_zre, p.M, hi - lo, out=acc, accumulate=True)
                 assert st == 0
             means.append((acc / f32(W)).astype(f32))          # IEEE fp32 division
@@ -86,6 +90,8 @@ class VirtualPS:
         for r in range(self.W):
             for c, (t, lo, hi, owner) in enumerate(self.ctx):
                 p = shared[c]
+                if p.status != 0:                             # R24: nothing to apply
+                    continue
                 view = outs[r][t][lo:hi].copy()
                 st, view = decompress(p.payload, use_zre, p.M, hi - lo, out=view, accumulate=True)
                 assert st == 0

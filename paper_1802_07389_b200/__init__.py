@@ -74,6 +74,11 @@ def _load():
         "tlc_exchange_ipc_handles": (I, [P, P]),
         "tlc_exchange_ipc_open": (I, [P, P]),
         "tlc_exchange_traffic": (I, [P, P]),
+        "tlc_loopback_create": (I, [P, I, I, P, I]),
+        "tlc_loopback_destroy": (I, [P]),
+        "tlc_loopback_rank": (P, [P, I]),
+        "tlc_loopback_push": (I, [P, P, F, I, P]),
+        "tlc_loopback_pull": (I, [P, P, F, I, P]),
         "tlc_stoch_compress": (I, [P, U64, U64, U64, I, P, U64, P, P, SZ, P]),
         "tlc_int8_workspace_bytes": (SZ, [U64]),
         "tlc_int8_compress": (I, [P, U64, P, P, P, SZ, P]),
@@ -197,6 +202,10 @@ def tlc_decompress(payload: torch.Tensor, hdr: torch.Tensor, n: int, out: torch.
     _check_dev("out", out, torch.float32)
     _check_dev("payload", payload, torch.uint8)
     _check_dev("hdr", hdr, torch.uint8)
+    if out.numel() < n:
+        raise ValueError(f"out holds {out.numel()} elements, n = {n}")
+    if hdr.numel() < HEADER_BYTES:
+        raise ValueError("hdr must hold 32 bytes")
     need = tlc_decompress_workspace_bytes(n)
     if ws is None:
         ws = workspace(need, out.device, "decompress")
@@ -380,29 +389,49 @@ class Comm:
             self._c = ctypes.c_void_p()
 
 
+def _check_list(name, ts, sizes, device):
+    """The C ABI reads one pointer per configured tensor and that many elements through
+    it: check the list length, each tensor's dtype / contiguity / numel and device."""
+    if len(ts) != len(sizes):
+        raise ValueError(f"{name}: {len(ts)} tensors given, the exchange was created for {len(sizes)}")
+    for i, (x, n) in enumerate(zip(ts, sizes)):
+        _check_dev(f"{name}[{i}]", x, torch.float32)
+        if x.numel() != n:
+            raise ValueError(f"{name}[{i}] has {x.numel()} elements, expected {n}")
+        if x.device != device:
+            raise ValueError(f"{name}[{i}] is on {x.device}, the exchange on {device}")
+
+
 class Exchange:
     """3LC parameter-server push/pull for a fixed tensor list (include/tlc.h)."""
 
-    def __init__(self, comm: Comm, sizes, p2p: bool = False, group=None):
+    def __init__(self, comm: Comm | None, sizes, p2p: bool = False, group=None, _handle=None, _device=None):
         """p2p=True: peer-memory mode -- the compressed payloads are read by the consuming
         kernels straight from the producing GPU over NVLink (CUDA IPC mappings set up
-        here through torch.distributed); otherwise NCCL send/recv moves them."""
+        here through torch.distributed); otherwise NCCL send/recv moves them.
+        (_handle: a virtual rank of a Loopback group, owned by the group.)"""
         import numpy as np
 
         self.comm, self.sizes = comm, [int(n) for n in sizes]
-        sz = np.ascontiguousarray(np.asarray(self.sizes, dtype=np.uint64))
-        self._x = ctypes.c_void_p()
-        rc = _lib.tlc_exchange_create(ctypes.byref(self._x), comm._c, len(sz), sz.ctypes.data)
-        if rc != TLC_OK:
-            raise TlcError(rc, "tlc_exchange_create")
-        self.device = comm.device
+        self._owned_handle = _handle is None
+        if _handle is None:
+            sz = np.ascontiguousarray(np.asarray(self.sizes, dtype=np.uint64))
+            self._x = ctypes.c_void_p()
+            rc = _lib.tlc_exchange_create(ctypes.byref(self._x), comm._c, len(sz), sz.ctypes.data)
+            if rc != TLC_OK:
+                raise TlcError(rc, "tlc_exchange_create")
+            self.device = comm.device
+        else:
+            self._x = ctypes.c_void_p(_handle)
+            self.device = _device
+            p2p = False                   # the group has already mapped its peers
         self.num_contexts = _lib.tlc_exchange_num_contexts(self._x)
         self.owned_elements = int(_lib.tlc_exchange_owned_elements(self._x))
         self.owned = _as_tensor(_lib.tlc_exchange_owned_buffer(self._x), self.owned_elements, self.device)
         self.pull_err = _as_tensor(_lib.tlc_exchange_pull_error(self._x), self.owned_elements, self.device)
         self.push_err = _as_tensor(_lib.tlc_exchange_push_error(self._x), sum(self.sizes), self.device)
-        self.p2p = bool(p2p)
-        if self.p2p:
+        self.p2p = bool(p2p) or _handle is not None
+        if p2p:
             mine = (ctypes.c_ubyte * 320)()
             rc = _lib.tlc_exchange_ipc_handles(self._x, ctypes.cast(mine, ctypes.c_void_p))
             if rc != TLC_OK:
@@ -445,8 +474,7 @@ class Exchange:
         return (ctypes.c_void_p * len(ts))(*[x.data_ptr() for x in ts])
 
     def push(self, grads, s: float, use_zre: bool = True, stream=None):
-        for g in grads:
-            _check_dev("grad", g, torch.float32)
+        _check_list("grads", grads, self.sizes, self.device)
         self._g = self._ptrs(grads)
         rc = _lib.tlc_exchange_push(self._x, ctypes.cast(self._g, ctypes.c_void_p), ctypes.c_float(s),
                                     int(bool(use_zre)), _stream_ptr(stream))
@@ -454,8 +482,7 @@ class Exchange:
             raise TlcError(rc, "tlc_exchange_push")
 
     def pull(self, outs, s: float, use_zre: bool = True, stream=None):
-        for o in outs:
-            _check_dev("out", o, torch.float32)
+        _check_list("outs", outs, self.sizes, self.device)
         self._o = self._ptrs(outs)
         rc = _lib.tlc_exchange_pull(self._x, ctypes.cast(self._o, ctypes.c_void_p), ctypes.c_float(s),
                                     int(bool(use_zre)), _stream_ptr(stream))
@@ -477,9 +504,67 @@ class Exchange:
             raise TlcError(rc, "tlc_exchange_status_async")
 
     def close(self):
-        if self._x:
+        if self._x and self._owned_handle:
             _lib.tlc_exchange_destroy(self._x)
-            self._x = ctypes.c_void_p()
+        self._x = ctypes.c_void_p()
+
+
+class Loopback:
+    """W virtual ranks of one exchange on one GPU (tlc_loopback_*): the multi-source push /
+    aggregate / pull kernels run exactly as across W GPUs, with plain device pointers for
+    the peers' buffers and stream order for the barriers.  ``ranks[r]`` is rank r's view
+    (an Exchange: push_err, pull_err, owned, contexts(), status())."""
+
+    def __init__(self, world: int, sizes, device=None):
+        import numpy as np
+
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.world, self.sizes, self.device = int(world), [int(n) for n in sizes], dev
+        sz = np.ascontiguousarray(np.asarray(self.sizes, dtype=np.uint64))
+        self._g = ctypes.c_void_p()
+        rc = _lib.tlc_loopback_create(ctypes.byref(self._g), self.world, len(sz), sz.ctypes.data, int(dev.index))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_loopback_create")
+        self.ranks = [Exchange(None, self.sizes, _handle=_lib.tlc_loopback_rank(self._g, r), _device=dev)
+                      for r in range(self.world)]
+
+    def _ptrs(self, name, per_rank):
+        if len(per_rank) != self.world:
+            raise ValueError(f"{name}: {len(per_rank)} ranks given, the group has {self.world}")
+        flat = []
+        for r, ts in enumerate(per_rank):
+            _check_list(f"{name}[{r}]", ts, self.sizes, self.device)
+            flat.extend(ts)
+        return (ctypes.c_void_p * len(flat))(*[x.data_ptr() for x in flat])
+
+    def push(self, grads, s: float, use_zre: bool = True, stream=None):
+        """grads[r][i]: rank r's state change of tensor i."""
+        self._gp = self._ptrs("grads", grads)
+        rc = _lib.tlc_loopback_push(self._g, ctypes.cast(self._gp, ctypes.c_void_p), ctypes.c_float(s),
+                                    int(bool(use_zre)), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_loopback_push")
+
+    def pull(self, outs, s: float, use_zre: bool = True, stream=None):
+        """outs[r][i]: rank r's full-size output of tensor i (accumulated)."""
+        self._op = self._ptrs("outs", outs)
+        rc = _lib.tlc_loopback_pull(self._g, ctypes.cast(self._op, ctypes.c_void_p), ctypes.c_float(s),
+                                    int(bool(use_zre)), _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_loopback_pull")
+
+    def close(self):
+        for x in getattr(self, "ranks", []):
+            x.close()
+        if self._g:
+            _lib.tlc_loopback_destroy(self._g)
+            self._g = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ instrumentation
@@ -561,6 +646,8 @@ def tlc_int8_decompress(codes: torch.Tensor, hdr: torch.Tensor, n: int, out: tor
     _check_dev("out", out, torch.float32)
     _check_dev("codes", codes, torch.int8)
     _check_dev("hdr", hdr, torch.uint8)
+    if out.numel() < n or codes.numel() < n:
+        raise ValueError(f"out / codes must hold n = {n} elements")
     rc = _lib.tlc_int8_decompress(codes.data_ptr(), hdr.data_ptr(), n, out.data_ptr(), int(mode),
                                   _stream_ptr(stream))
     if rc != TLC_OK:

@@ -471,11 +471,14 @@ constexpr int kK5mG = TLC_K5M_G;                    // sources whose loads are i
 
 // Dynamic shared memory, sized for W sources: E[W][kT5] bytes, then
 // V[W][5][256] words (V[w][i][b] = M_w * (digit_i(b) - 1): +0 for a zero trit).
-struct K5mHead {
+struct alignas(16) K5mHead {   // E follows it: 16-byte stores into E need sizeof % 16 == 0
     int ok[kMaxSources];
+    unsigned int stat[kMaxSources];   // each source's header status at the tile start
+    int poison;                       // the tile's mean is NaN (reading R24)
     unsigned int warp_sum[kK5Threads / 32];
 };
 constexpr int kK5mSegCache = kSegCache;               // owned contexts (all 150 of BERT-large at W = 1)
+static_assert(sizeof(K5mHead) % 16 == 0, "E[] must stay 16-byte aligned");
 __host__ __device__ constexpr size_t k5m_smem_bytes(int W) {
     return sizeof(K5mHead) + (size_t)W * kT5 + (size_t)W * 5 * 256 * sizeof(uint32_t);
 }
@@ -516,6 +519,15 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
         const uint64_t J0 = lt * kT5;
         const int tl = (int)tmin<uint64_t>(kT5, P - J0);
         __syncthreads();                                   // previous tile's readers are done
+        // R24: a context with a failed push (a source header not OK: NONFINITE/RANGE from its
+        // compression, FORMAT from K4) has a NaN mean -- as an fp32 sum would -- so the owner's
+        // pull compression raises NONFINITE, which every rank then sees.  One load per
+        // source, broadcast through shared memory so the decision is uniform in the CTA.
+        if (threadIdx.x < W) sm.stat[threadIdx.x] = get_seg(X, threadIdx.x * A.count + q).hdr->status;
+        if (threadIdx.x == 0) sm.poison = 0;
+        __syncthreads();
+        bool poison = false;
+        for (int w = 0; w < W; w++) poison |= sm.stat[w] != TLC_OK;
         // sources in groups of kK5mG: every source's header, seek and payload-window loads of a
         // group are in flight together (in peer-memory mode they cross NVLink), then the scans
         for (int w0 = 0; w0 < W; w0 += kK5mG) {
@@ -527,11 +539,11 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
             for (int g = 0; g < kK5mG; g++) {
                 const int w = w0 + g;
                 okw[g] = false;
-                if (w >= W) continue;
+                if (w >= W || poison) continue;
                 const Seg R = get_seg(X, w * A.count + q);
                 hw[g] = R.hdr;
                 pw[g] = R.payload;
-                okw[g] = R.hdr->status == TLC_OK;          // uniform
+                okw[g] = true;                              // every source OK (not poisoned)
                 zw[g] = (R.hdr->flags & TLC_FLAG_ZRE) != 0;
                 if (okw[g] && zw[g]) expand_load(Xw[g], R.payload, R.hdr->payload_len, seek + R.k5, lt, ntiles);
             }
@@ -550,11 +562,12 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
                 } else {
                     bad = __syncthreads_or(copy_quartic(E[w], pw[g] + J0, tl));
                 }
-                if (bad && threadIdx.x == 0) { raise_format(hw[g]); sm.ok[w] = 0; }
+                if (bad && threadIdx.x == 0) { raise_format(hw[g]); sm.ok[w] = 0; sm.poison = 1; }
             }
         }
-        cur = q;
+        cur = poison ? -1 : q;                                // tables not rebuilt when poisoned
         __syncthreads();
+        poison |= sm.poison != 0;                            // a literal > 242 found in this tile
 #pragma unroll 1                                         // unrolled: 0.43 vs 0.37 ms (BERT-large W = 1)
         for (int k = 0; k < kK5BytesPerThread / 4; k++) {
             const int jl = 4 * threadIdx.x + 4 * kK5Threads * k;
@@ -582,7 +595,8 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
                 float r[4];
 #pragma unroll
                 for (int c = 0; c < 4; c++)
-                    r[c] = !any ? 0.0f : (pow2 ? __fmul_rn(acc[i][c], rW) : __fdiv_rn(acc[i][c], Wf));
+                    r[c] = poison ? __int_as_float(0x7fc00000)
+                                  : !any ? 0.0f : (pow2 ? __fmul_rn(acc[i][c], rW) : __fdiv_rn(acc[i][c], Wf));
                 // partition i's positions e = i*P + J0 + jl < n (its row base recomputed here:
                 // keeping five row pointers live spilled at 80 registers)
                 const uint64_t e0 = (uint64_t)i * P + J0;

@@ -33,6 +33,7 @@
 struct tlc_comm {
     ncclComm_t nccl;
     int rank, world, device;
+    int loopback;      // a virtual rank of a tlc_loopback group: no NCCL, no other process
 };
 
 namespace tlc {
@@ -51,10 +52,11 @@ struct Ctx {
     size_t owned_off;   // offset in the owner's flat owned buffer (valid on the owner)
 };
 
-// worst (largest) status over a header array -> *out (atomicMax)
-__global__ void tlc_status_kernel(const tlc_header *__restrict__ h, int count, unsigned int *out) {
+// worst status over a list of header pointers (peer-memory mode: the headers live on
+// the producing ranks)
+__global__ void tlc_status_list_kernel(const tlc_header *const *__restrict__ h, int count, unsigned int *out) {
     unsigned int m = 0;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) m = max(m, h[i].status);
+    for (int i = threadIdx.x; i < count; i += blockDim.x) m = max(m, h[i]->status);
     m = __reduce_max_sync(0xffffffffu, m);
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
@@ -160,10 +162,73 @@ struct tlc_exchange {
     unsigned long long *d_epoch = nullptr;           // barrier epochs issued (device counter)
     std::vector<const float *> last_grads;
     std::vector<float *> last_outs;
+    // every header whose status the exchange reports: the pushes this rank aggregates
+    // (from every rank) and the pulls it applies (from every owner)
+    const tlc_header **d_status_list = nullptr;
+    int status_count = 0;
+    int phase = 0;                                   // 0: next call is push, 1: pull
 };
 
 static int cuda_ok(cudaError_t e) { return e == cudaSuccess ? TLC_OK : TLC_ERR_CUDA; }
 static int nccl_ok(ncclResult_t r) { return r == ncclSuccess ? TLC_OK : TLC_ERR_NCCL; }
+
+// The headers tlc_exchange_status reports on: this rank's own push headers, and the
+// pull header of every context (on its owner in peer-memory mode, the received copy with
+// NCCL), which by reading R24 carries every rank's push failure as NONFINITE -- so every
+// rank reports the same worst status for a step.  With NCCL the received push headers
+// of the owned contexts are added (FORMAT from the owner's scan lands there).  Peer
+// mode reads no other rank's push header: after pull that rank may already be writing
+// the next step's.
+static int upload_status_list(tlc_exchange *x) {
+    const int W = x->W, me = x->me, C = (int)x->ctx.size(), nown = (int)x->owned[me].size();
+    std::vector<const tlc_header *> h;
+    h.reserve((size_t)W * nown + 2 * C);
+    for (int k = 0; k < C; k++) {
+        const Ctx &c = x->ctx[k];
+        h.push_back(x->push_hdr_send + x->hdr_start[c.owner] + c.slot);
+        h.push_back((x->p2p ? static_cast<const tlc_header *>(x->peer[c.owner][3]) : x->pull_hdr) +
+                    x->hdr_start[c.owner] + c.slot);
+    }
+    if (!x->p2p)
+        for (int i = 0; i < W * nown; i++) h.push_back(x->push_hdr_recv + i);
+    x->status_count = (int)h.size();
+    if (h.empty()) return TLC_OK;
+    return cuda_ok(cudaMemcpy(x->d_status_list, h.data(), h.size() * sizeof(void *), cudaMemcpyHostToDevice));
+}
+
+// Peer-memory mode: `peer[w]` = rank w's {push_send, push headers, pull buffer, pull
+// headers, flag slots} as addressable from this device (CUDA IPC mappings of other
+// processes' buffers, or plain device pointers for the virtual ranks of a loopback
+// group).  The owner's aggregation then reads row w*|A|+q straight from rank w's send
+// buffer, and the apply table is rebuilt on the next pull with the owners' pull buffers.
+static int set_peers(tlc_exchange *x, const std::vector<std::array<void *, 5>> &peer) {
+    const int W = x->W, me = x->me;
+    x->peer = peer;
+    std::vector<unsigned long long *> pf(W);
+    for (int w = 0; w < W; w++) pf[w] = static_cast<unsigned long long *>(x->peer[w][4]);
+    int rc = cuda_ok(cudaMemcpy(x->d_peer_flags, pf.data(), W * sizeof(void *), cudaMemcpyHostToDevice));
+    const int nown = (int)x->owned[me].size();
+    if (rc == TLC_OK && nown) {
+        std::vector<tlc_tensor_desc> xs((size_t)W * nown);
+        for (int q = 0; q < nown; q++) {
+            const Ctx &c = x->ctx[x->owned[me][q]];
+            for (int w = 0; w < W; w++) {
+                tlc_tensor_desc &e = xs[(size_t)w * nown + q];
+                e = tlc_tensor_desc{};
+                e.payload = static_cast<uint8_t *>(x->peer[w][0]) + x->region_start[me] + c.region_off;
+                e.hdr = static_cast<tlc_header *>(x->peer[w][1]) + x->hdr_start[me] + c.slot;
+                e.n = c.n;
+            }
+        }
+        rc = x->x_tab.update(xs.data());
+    }
+    if (rc == TLC_OK) {
+        x->p2p = 1;
+        x->last_outs.clear();   // the apply table is rebuilt with peer pointers
+        rc = upload_status_list(x);
+    }
+    return rc;
+}
 
 extern "C" {
 
@@ -193,7 +258,7 @@ int tlc_comm_init(tlc_comm **c, const void *unique_id, int rank, int world, int 
 }
 
 int tlc_comm_destroy(tlc_comm *c) {
-    if (!c) return TLC_ERR_ARG;
+    if (!c || c->loopback) return TLC_ERR_ARG;     // a loopback group owns its virtual comms
     const int rc = nccl_ok(ncclCommDestroy(c->nccl));
     delete c;
     return rc;
@@ -223,7 +288,7 @@ int tlc_exchange_destroy(tlc_exchange *x) {
     for (void *p : x->opened) cudaIpcCloseMemHandle(p);
     void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
                    x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags,
-                   x->d_epoch};
+                   x->d_epoch, (void *)x->d_status_list};
     for (void *p : dev)
         if (p) cudaFree(p);
     x->push_tab.release();
@@ -297,7 +362,15 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     alloc((void **)&x->d_epoch, sizeof(unsigned long long));
     if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->d_epoch, 0, sizeof(unsigned long long)));
     alloc((void **)&x->d_peer_flags, x->W * sizeof(unsigned long long *));
+    alloc((void **)&x->d_status_list, ((size_t)x->W * nown + 2 * C) * sizeof(tlc_header *));
     if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->flags, 0, 2 * x->W * sizeof(unsigned long long)));
+    // headers start zeroed (status OK, length 0): a header is only ever read after the
+    // phase that writes it, but the status report must never see stale allocator bytes
+    if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->push_hdr_send, 0, std::max<size_t>((size_t)C * sizeof(tlc_header), 256)));
+    if (rc == TLC_OK)
+        rc = cuda_ok(cudaMemset(x->push_hdr_recv, 0, std::max<size_t>((size_t)x->W * nown * sizeof(tlc_header), 256)));
+    if (rc == TLC_OK) rc = cuda_ok(cudaMemset(x->pull_hdr, 0, std::max<size_t>((size_t)C * sizeof(tlc_header), 256)));
+    if (rc == TLC_OK) rc = upload_status_list(x);
     if (rc == TLC_OK) {
         // error buffers start at zero (R20)
         rc = cuda_ok(cudaMemset(x->push_err, 0, std::max<size_t>(x->total_elems * sizeof(float), 256)));
@@ -360,44 +433,21 @@ int tlc_exchange_ipc_handles(tlc_exchange *x, void *out) {
 
 int tlc_exchange_ipc_open(tlc_exchange *x, const void *all) {
     // all: W x 5 handles in rank order (the all-gather of tlc_exchange_ipc_handles)
-    if (!x || !all || x->p2p) return TLC_ERR_ARG;
+    if (!x || !all || x->p2p || x->comm->loopback) return TLC_ERR_ARG;
     const int W = x->W, me = x->me;
-    x->peer.assign(W, {});
+    std::vector<std::array<void *, 5>> peer(W);
     void *mine[5] = {x->push_send, x->push_hdr_send, x->pull_buf, x->pull_hdr, x->flags};
     for (int w = 0; w < W; w++)
         for (int k = 0; k < 5; k++) {
-            if (w == me) { x->peer[w][k] = mine[k]; continue; }
+            if (w == me) { peer[w][k] = mine[k]; continue; }
             cudaIpcMemHandle_t h;
             std::memcpy(&h, static_cast<const char *>(all) + 64 * (5 * w + k), 64);
             void *p = nullptr;
             if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return TLC_ERR_CUDA;
             x->opened.push_back(p);
-            x->peer[w][k] = p;
+            peer[w][k] = p;
         }
-    std::vector<unsigned long long *> pf(W);
-    for (int w = 0; w < W; w++) pf[w] = static_cast<unsigned long long *>(x->peer[w][4]);
-    int rc = cuda_ok(cudaMemcpy(x->d_peer_flags, pf.data(), W * sizeof(void *), cudaMemcpyHostToDevice));
-    // the owner's aggregation reads row w*|A|+q straight from rank w's send buffer
-    const int nown = (int)x->owned[me].size();
-    if (rc == TLC_OK && nown) {
-        std::vector<tlc_tensor_desc> xs((size_t)W * nown);
-        for (int q = 0; q < nown; q++) {
-            const Ctx &c = x->ctx[x->owned[me][q]];
-            for (int w = 0; w < W; w++) {
-                tlc_tensor_desc &e = xs[(size_t)w * nown + q];
-                e = tlc_tensor_desc{};
-                e.payload = static_cast<uint8_t *>(x->peer[w][0]) + x->region_start[me] + c.region_off;
-                e.hdr = static_cast<tlc_header *>(x->peer[w][1]) + x->hdr_start[me] + c.slot;
-                e.n = c.n;
-            }
-        }
-        rc = x->x_tab.update(xs.data());
-    }
-    if (rc == TLC_OK) {
-        x->p2p = 1;
-        x->last_outs.clear();   // the apply table is rebuilt with peer pointers
-    }
-    return rc;
+    return set_peers(x, peer);
 }
 
 // Stream capture (CUDA graphs) is supported by the peer-memory transport only;
@@ -486,15 +536,21 @@ uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction) {
     return b;
 }
 
-int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream) {
-    if (!x || !grads || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (int rc0 = capture_ok(x, st)) return rc0;
+}  // extern "C"
+
+// ------------------------------------------------------------------ the four phases
+// push = (1) compress + transport + (2) owner aggregate; pull = (3) owner compress +
+// transport + (4) apply.  The loopback group runs each phase for every virtual rank
+// before the next phase, which is the order the flag barriers enforce across GPUs.
+static int check_ptrs(const tlc_exchange *x, const void *const *p) {
+    for (size_t i = 0; i < x->tensor_sizes.size(); i++)
+        if (!p[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
+    return TLC_OK;
+}
+
+// (1) compress every context with this rank's push error buffer into the send layout
+static int phase_push_compress(tlc_exchange *x, const float *const *grads, float s, int use_zre, cudaStream_t st) {
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
-    for (int i = 0; i < T; i++)
-        if (!grads[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
-    int rc = TLC_OK;
-    // (1) compress every context with this rank's push error buffer into the send layout
     bool same = x->last_grads.size() == (size_t)T;
     for (int i = 0; same && i < T; i++) same = x->last_grads[i] == grads[i];
     if (!same) {
@@ -509,77 +565,29 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
             d[k].n = c.n;
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;   // table may be in use
-        rc = x->push_tab.d ? x->push_tab.update(d.data()) : x->push_tab.create(d.data(), C, true, nullptr);
+        const int rc = x->push_tab.d ? x->push_tab.update(d.data()) : x->push_tab.create(d.data(), C, true, nullptr);
         if (rc != TLC_OK) return rc;
         x->last_grads.assign(grads, grads + T);
     }
-    if ((rc = launch_compress_table(x->push_tab.T, s, use_zre ? 1 : 0, x->push_tab.ws, st)) != TLC_OK) return rc;
-    // (2) every owner receives its contexts' payloads and headers from every rank
-    const int nown = (int)x->owned[x->me].size();
-    const size_t own_region = x->region_bytes[x->me];
-    ncclComm_t nc = x->comm->nccl;
-    if (x->p2p) {
-        // peer memory: no copy -- once every rank's pushes are written, the owner's
-        // scan and aggregation kernels read them from the producing GPU over NVLink
-        if ((rc = flag_barrier(x, 0, st)) != TLC_OK) return rc;
-        if (x->owned_elems &&
-            (rc = launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st)) != TLC_OK)
-            return rc;
-        return TLC_OK;
-    }
-    if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
-    for (int o = 0; o < x->W; o++) {
-        if (x->region_bytes[o] == 0) continue;
-        ncclSend(x->push_send + x->region_start[o], x->region_bytes[o], ncclUint8, o, nc, st);
-        ncclSend(x->push_hdr_send + x->hdr_start[o], x->owned[o].size() * sizeof(tlc_header), ncclUint8, o, nc, st);
-    }
-    if (own_region)
-        for (int w = 0; w < x->W; w++) {
-            ncclRecv(x->push_recv + (size_t)w * own_region, own_region, ncclUint8, w, nc, st);
-            ncclRecv(x->push_hdr_recv + (size_t)w * nown, nown * sizeof(tlc_header), ncclUint8, w, nc, st);
-        }
-    if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
-    // (3) owner: fused decompress-aggregate of the W pushes of every owned context,
-    //     rank-ordered sum from +0 of the nonzero trits, then / W (R15), written once
-    if (x->owned_elems &&
-        (rc = launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st)) != TLC_OK)
-        return rc;
-    return TLC_OK;
+    return launch_compress_table(x->push_tab.T, s, use_zre ? 1 : 0, x->push_tab.ws, st);
 }
 
-int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream) {
-    if (!x || !outs || !(s >= 1.0f && s < 2.0f)) return TLC_ERR_ARG;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (int rc0 = capture_ok(x, st)) return rc0;
+// (2) owner: fused decompress-aggregate of the W pushes of every owned context,
+//     rank-ordered sum from +0 of the nonzero trits, then / W (R15), written once
+static int phase_aggregate(tlc_exchange *x, cudaStream_t st) {
+    if (!x->owned_elems) return TLC_OK;
+    return launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st);
+}
+
+// (3) the owner compresses its shard of the model delta ONCE (shared pull)
+static int phase_pull_compress(tlc_exchange *x, float s, int use_zre, cudaStream_t st) {
+    if (!x->owned_elems) return TLC_OK;
+    return launch_compress_table(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st);
+}
+
+// (4) every rank applies every context to its full-size output (ACCUMULATE, R16)
+static int phase_apply(tlc_exchange *x, float *const *outs, cudaStream_t st) {
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
-    for (int i = 0; i < T; i++)
-        if (!outs[i] && x->tensor_sizes[i]) return TLC_ERR_ARG;
-    int rc = TLC_OK;
-    // (1) the owner compresses its shard of the model delta ONCE (shared pull)
-    if (x->owned_elems &&
-        (rc = launch_compress_table(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st)) != TLC_OK)
-        return rc;
-    // (2) all-gather of the owners' regions (grouped send/recv, sizes differ per owner);
-    //     in peer-memory mode a barrier, then the apply kernels read the owners' regions
-    ncclComm_t nc = x->comm->nccl;
-    if (x->p2p) {
-        if ((rc = flag_barrier(x, 1, st)) != TLC_OK) return rc;
-    } else {
-    if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
-    for (int o = 0; o < x->W; o++) {
-        if (o == x->me) continue;
-        if (x->region_bytes[x->me]) {
-            ncclSend(x->pull_buf + x->region_start[x->me], x->region_bytes[x->me], ncclUint8, o, nc, st);
-            ncclSend(x->pull_hdr + x->hdr_start[x->me], x->owned[x->me].size() * sizeof(tlc_header), ncclUint8, o, nc, st);
-        }
-        if (x->region_bytes[o]) {
-            ncclRecv(x->pull_buf + x->region_start[o], x->region_bytes[o], ncclUint8, o, nc, st);
-            ncclRecv(x->pull_hdr + x->hdr_start[o], x->owned[o].size() * sizeof(tlc_header), ncclUint8, o, nc, st);
-        }
-    }
-    if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
-    }
-    // (3) every rank applies every context to its full-size output (ACCUMULATE, R16)
     bool same = x->last_outs.size() == (size_t)T;
     for (int i = 0; same && i < T; i++) same = x->last_outs[i] == outs[i];
     if (!same) {
@@ -595,24 +603,97 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
             d[k].n = c.n;
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;
-        rc = x->apply_tab.d ? x->apply_tab.update(d.data()) : x->apply_tab.create(d.data(), C, false, nullptr);
+        const int rc = x->apply_tab.d ? x->apply_tab.update(d.data()) : x->apply_tab.create(d.data(), C, false, nullptr);
         if (rc != TLC_OK) return rc;
         x->last_outs.assign(outs, outs + T);
     }
     return launch_decompress_table(x->apply_tab.T, TLC_MODE_ACCUMULATE, x->apply_tab.ws, st);
 }
 
+extern "C" {
+
+int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream) {
+    if (!x || !grads || !(s >= 1.0f && s < 2.0f) || x->comm->loopback) return TLC_ERR_ARG;
+    if (x->phase != 0) return TLC_ERR_ARG;        // push and pull alternate (buffer reuse, see tlc.h)
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc0 = capture_ok(x, st)) return rc0;
+    int rc = check_ptrs(x, reinterpret_cast<const void *const *>(grads));
+    if (rc == TLC_OK) rc = phase_push_compress(x, grads, s, use_zre, st);
+    if (rc != TLC_OK) return rc;
+    // every owner receives its contexts' payloads and headers from every rank
+    if (x->p2p) {
+        // peer memory: no copy -- once every rank's pushes are written, the owner's
+        // scan and aggregation kernels read them from the producing GPU over NVLink
+        if ((rc = flag_barrier(x, 0, st)) != TLC_OK) return rc;
+    } else {
+        const int nown = (int)x->owned[x->me].size();
+        const size_t own_region = x->region_bytes[x->me];
+        ncclComm_t nc = x->comm->nccl;
+        if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
+        for (int o = 0; o < x->W; o++) {
+            if (x->region_bytes[o] == 0) continue;
+            ncclSend(x->push_send + x->region_start[o], x->region_bytes[o], ncclUint8, o, nc, st);
+            ncclSend(x->push_hdr_send + x->hdr_start[o], x->owned[o].size() * sizeof(tlc_header), ncclUint8, o, nc, st);
+        }
+        if (own_region)
+            for (int w = 0; w < x->W; w++) {
+                ncclRecv(x->push_recv + (size_t)w * own_region, own_region, ncclUint8, w, nc, st);
+                ncclRecv(x->push_hdr_recv + (size_t)w * nown, nown * sizeof(tlc_header), ncclUint8, w, nc, st);
+            }
+        if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
+    }
+    if ((rc = phase_aggregate(x, st)) != TLC_OK) return rc;
+    x->phase = 1;
+    return TLC_OK;
+}
+
+int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream) {
+    if (!x || !outs || !(s >= 1.0f && s < 2.0f) || x->comm->loopback) return TLC_ERR_ARG;
+    if (x->phase != 1) return TLC_ERR_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc0 = capture_ok(x, st)) return rc0;
+    int rc = check_ptrs(x, reinterpret_cast<const void *const *>(outs));
+    if (rc == TLC_OK) rc = phase_pull_compress(x, s, use_zre, st);
+    if (rc != TLC_OK) return rc;
+    // all-gather of the owners' regions (grouped send/recv, sizes differ per owner);
+    // in peer-memory mode a barrier, then the apply kernels read the owners' regions
+    if (x->p2p) {
+        if ((rc = flag_barrier(x, 1, st)) != TLC_OK) return rc;
+    } else {
+        ncclComm_t nc = x->comm->nccl;
+        if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
+        for (int o = 0; o < x->W; o++) {
+            if (o == x->me) continue;
+            if (x->region_bytes[x->me]) {
+                ncclSend(x->pull_buf + x->region_start[x->me], x->region_bytes[x->me], ncclUint8, o, nc, st);
+                ncclSend(x->pull_hdr + x->hdr_start[x->me], x->owned[x->me].size() * sizeof(tlc_header), ncclUint8,
+                         o, nc, st);
+            }
+            if (x->region_bytes[o]) {
+                ncclRecv(x->pull_buf + x->region_start[o], x->region_bytes[o], ncclUint8, o, nc, st);
+                ncclRecv(x->pull_hdr + x->hdr_start[o], x->owned[o].size() * sizeof(tlc_header), ncclUint8, o, nc, st);
+            }
+        }
+        if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
+    }
+    if ((rc = phase_apply(x, outs, st)) != TLC_OK) return rc;
+    x->phase = 0;
+    return TLC_OK;
+}
+
+}  // extern "C"
+
 static int exchange_status_enqueue(tlc_exchange *x, unsigned int *dst, cudaStream_t st) {
-    // worst device status over every received header (push and pull)
+    // worst device status over every header this rank consumed (push and pull)
     int rc = cuda_ok(cudaMemsetAsync(x->d_status, 0, sizeof(unsigned int), st));
-    const int nown = (int)x->owned[x->me].size();
-    if (rc == TLC_OK && nown && !x->p2p) tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_recv, x->W * nown, x->d_status);
-    if (rc == TLC_OK && x->p2p && !x->ctx.empty())   // peer-memory mode: this rank's own pushes
-        tlc_status_kernel<<<1, 256, 0, st>>>(x->push_hdr_send, (int)x->ctx.size(), x->d_status);
-    if (rc == TLC_OK && !x->ctx.empty()) tlc_status_kernel<<<1, 256, 0, st>>>(x->pull_hdr, (int)x->ctx.size(), x->d_status);
+    if (rc == TLC_OK && x->status_count)
+        tlc_status_list_kernel<<<1, 256, 0, st>>>(x->d_status_list, x->status_count, x->d_status);
+    if (rc == TLC_OK) rc = cuda_ok(cudaPeekAtLastError());
     if (rc == TLC_OK) rc = cuda_ok(cudaMemcpyAsync(dst, x->d_status, sizeof(unsigned int), cudaMemcpyDefault, st));
     return rc;
 }
+
+extern "C" {
 
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream) {
     // synchronizes `stream`
@@ -626,6 +707,95 @@ int tlc_exchange_status(tlc_exchange *x, unsigned int *status_out, void *stream)
 int tlc_exchange_status_async(tlc_exchange *x, unsigned int *dst, void *stream) {
     if (!x || !dst) return TLC_ERR_ARG;
     return exchange_status_enqueue(x, dst, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ loopback group
+// W virtual ranks in one process on one device: each has its own tlc_exchange (own
+// push / pull error buffers, owned buffer, send and pull regions) and sees the others'
+// buffers as plain device pointers (peer-memory mode without IPC); stream order
+// replaces the flag barriers.  Push and pull run the same kernels as the multi-GPU
+// transports -- K1-K3 per rank, K4 + K5m per owner reading every rank's payloads,
+// K1-K3 per owner, K4 + K5 per rank reading every owner's payloads.
+struct tlc_loopback {
+    int W = 0;
+    std::vector<tlc_comm *> comms;
+    std::vector<tlc_exchange *> xs;
+    int phase = 0;
+};
+
+extern "C" {
+
+int tlc_loopback_destroy(tlc_loopback *g) {
+    if (!g) return TLC_ERR_ARG;
+    for (tlc_exchange *x : g->xs)
+        if (x) tlc_exchange_destroy(x);
+    for (tlc_comm *c : g->comms) delete c;
+    delete g;
+    return TLC_OK;
+}
+
+int tlc_loopback_create(tlc_loopback **out, int world, int num_tensors, const uint64_t *sizes, int device) {
+    if (!out || world < 1 || world > 8 || num_tensors < 1 || !sizes) return TLC_ERR_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return TLC_ERR_CUDA;
+    auto *g = new tlc_loopback{};
+    g->W = world;
+    int rc = TLC_OK;
+    for (int r = 0; r < world && rc == TLC_OK; r++) {
+        auto *c = new tlc_comm{};
+        c->nccl = nullptr;
+        c->rank = r;
+        c->world = world;
+        c->device = device;
+        c->loopback = 1;
+        g->comms.push_back(c);
+        tlc_exchange *x = nullptr;
+        rc = tlc_exchange_create(&x, c, num_tensors, sizes);
+        if (rc == TLC_OK) g->xs.push_back(x);
+    }
+    if (rc == TLC_OK) {
+        std::vector<std::array<void *, 5>> peer(world);
+        for (int w = 0; w < world; w++) {
+            tlc_exchange *y = g->xs[w];
+            peer[w] = {y->push_send, y->push_hdr_send, y->pull_buf, y->pull_hdr, y->flags};
+        }
+        for (int r = 0; r < world && rc == TLC_OK; r++) rc = set_peers(g->xs[r], peer);
+    }
+    if (rc != TLC_OK) {
+        tlc_loopback_destroy(g);
+        return rc;
+    }
+    *out = g;
+    return TLC_OK;
+}
+
+tlc_exchange *tlc_loopback_rank(tlc_loopback *g, int rank) {
+    return (g && rank >= 0 && rank < g->W) ? g->xs[rank] : nullptr;
+}
+
+int tlc_loopback_push(tlc_loopback *g, const float *const *grads, float s, int use_zre, void *stream) {
+    if (!g || !grads || !(s >= 1.0f && s < 2.0f) || g->phase != 0) return TLC_ERR_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t T = g->xs[0]->tensor_sizes.size();
+    int rc = TLC_OK;
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = check_ptrs(g->xs[r], reinterpret_cast<const void *const *>(grads + r * T));
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = phase_push_compress(g->xs[r], grads + r * T, s, use_zre, st);
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = phase_aggregate(g->xs[r], st);
+    if (rc == TLC_OK) g->phase = 1;
+    return rc;
+}
+
+int tlc_loopback_pull(tlc_loopback *g, float *const *outs, float s, int use_zre, void *stream) {
+    if (!g || !outs || !(s >= 1.0f && s < 2.0f) || g->phase != 1) return TLC_ERR_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t T = g->xs[0]->tensor_sizes.size();
+    int rc = TLC_OK;
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = check_ptrs(g->xs[r], reinterpret_cast<const void *const *>(outs + r * T));
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = phase_pull_compress(g->xs[r], s, use_zre, st);
+    for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = phase_apply(g->xs[r], outs + r * T, st);
+    if (rc == TLC_OK) g->phase = 0;
+    return rc;
 }
 
 }  // extern "C"

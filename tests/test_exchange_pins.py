@@ -195,3 +195,32 @@ def test_round_f32_against_numpy_on_float64_exact_values():
     assert _round_f32(Fraction(1) + Fraction(1, 2 ** 24)) == f32(1.0)                # tie -> even
     assert _round_f32(Fraction(1) + Fraction(3, 2 ** 24)) == f32(1.0 + 2 ** -22)       # tie -> even (up)
     assert _round_f32(Fraction(1, 2 ** 149)).view(np.uint32) == 1                      # smallest subnormal
+
+
+def test_failed_push_poisons_only_its_context():
+    """Reading R24: a NaN in one rank's push gives that context a NaN mean (an fp32 sum
+    with a NaN term is NaN), its shared pull fails with NONFINITE and is applied nowhere;
+    every other context is exactly what it is without the failure."""
+    W, sizes = 3, [40, 40, 40]
+    grads = [[synth.gaussian(40, 99, r, t) for t in range(3)] for r in range(W)]
+    ref = X.VirtualPS(sizes, W)
+    ref_means, _ = ref.push(grads, 1.5)
+    bad = [[g.copy() for g in gr] for gr in grads]
+    bad[1][2][5] = np.nan
+    ps = X.VirtualPS(sizes, W)
+    means, sent = ps.push(bad, 1.5)
+    c_bad = [c for c, (t, _, _, _) in enumerate(ps.ctx) if t == 2][0]
+    assert sent[1][c_bad].status == 2                                  # NONFINITE (R6)
+    assert np.array_equal(ps.push_err[1][c_bad], np.zeros(40, f32))     # err untouched (R6)
+    for c in range(len(ps.ctx)):
+        if c == c_bad:
+            assert np.isnan(means[c]).all()
+        else:
+            assert np.array_equal(means[c].view(np.uint32), ref_means[c].view(np.uint32))
+    outs = [[np.zeros(40, f32) for _ in sizes] for _ in range(W)]
+    shared = ps.pull(means, outs, 1.5)
+    assert shared[c_bad].status == 2
+    assert np.array_equal(ps.pull_err[c_bad], np.zeros(40, f32))
+    for r in range(W):
+        assert np.array_equal(outs[r][2], np.zeros(40, f32))
+        assert not np.array_equal(outs[r][0], np.zeros(40, f32))
