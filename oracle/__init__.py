@@ -19,6 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "tlc_oracle.c")
 _LIB = os.path.join(_HERE, "libtlc_oracle.so")
+_LIB_OMP = os.path.join(_HERE, "libtlc_oracle_omp.so")
 
 # Status values (defined independently of include/tlc.h).
 OK, ERR_ARG, ERR_NONFINITE, ERR_RANGE, ERR_FORMAT = 0, 1, 2, 3, 4
@@ -26,22 +27,33 @@ OK, ERR_ARG, ERR_NONFINITE, ERR_RANGE, ERR_FORMAT = 0, 1, 2, 3, 4
 CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math"]
 
 
-def build(force: bool = False) -> str:
-    """Compile tlc_oracle.c with gcc (no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile tlc_oracle.c with gcc (no FMA contraction, no fast-math); omp=True builds
+    the same source with -fopenmp (element-wise loops on all host cores, bench.py's
+    cpu_baseline only)."""
+    out = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, *(["-fopenmp"] if omp else []), "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
 
 
 _lib = None
+_omp = False
+
+
+def use_openmp(on: bool) -> None:
+    """Switch the functions below to the -fopenmp build (True) or the plain one."""
+    global _lib, _omp
+    if bool(on) != _omp:
+        _omp, _lib = bool(on), None
 
 
 def lib():
     global _lib
     if _lib is None:
-        L = ctypes.CDLL(build())
+        L = ctypes.CDLL(build(omp=_omp))
         P, U64, F, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_float, ctypes.c_int
         sig = {
             "tlc_o_accumulate": (None, [P, P, U64, P]),

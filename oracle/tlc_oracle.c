@@ -20,6 +20,13 @@
  * Every step runs over the whole tensor before the next starts, in the order
  * the paper lists them; no fusion, no blocking.
  *
+ * The element-wise loops carry "#pragma omp parallel for".  The default build
+ * (no -fopenmp) ignores them; oracle.build(omp=True) compiles the same source
+ * with -fopenmp for bench.py's cpu_baseline on all host cores.  Results are
+ * identical: every element's operations are independent, and the one reduction
+ * (the max of Eq. 1) is exact and order-free.  The zero-run coder (Sec. 3.3)
+ * stays serial in both builds.
+ *
  * Pinning (see tests/test_oracle_pins.py): every function is pinned by values
  * the paper or SPEC prints, closed forms, invariants or brute force.  The only
  * unpinned quantities are the paper's Table 2 s-rows (need real ResNet-110
@@ -44,6 +51,7 @@ enum {
 /* "accumulates the input tensor into a local buffer": u = buffer + T_in.      */
 void tlc_o_accumulate(const float *t, const float *buf, uint64_t n, float *u)
 {
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++)
         u[i] = buf[i] + t[i];
 }
@@ -54,12 +62,17 @@ void tlc_o_accumulate(const float *t, const float *buf, uint64_t n, float *u)
 int tlc_o_scale(const float *u, uint64_t n, float s, float *M_out, float *maxabs_out)
 {
     float a = 0.0f;
+    int bad = 0;
+    /* max is exact and order-free, so the -fopenmp build's reduction gives the same a */
+#pragma omp parallel for reduction(max : a) reduction(| : bad)
     for (uint64_t i = 0; i < n; i++) {
         if (isnan(u[i]) || isinf(u[i]))
-            return O_ERR_NONFINITE;
-        if (fabsf(u[i]) > a)
+            bad = 1;
+        else if (fabsf(u[i]) > a)
             a = fabsf(u[i]);
     }
+    if (bad)
+        return O_ERR_NONFINITE;
     float M = a * s;
     if (isinf(M))
         return O_ERR_RANGE;
@@ -73,6 +86,7 @@ int tlc_o_scale(const float *u, uint64_t n, float s, float *M_out, float *maxabs
 /* when every u is zero; then every value is 0 (R5).                   */
 void tlc_o_quantize(const float *u, uint64_t n, float M, int8_t *q)
 {
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++) {
         if (M == 0.0f)
             q[i] = 0;
@@ -84,6 +98,7 @@ void tlc_o_quantize(const float *u, uint64_t n, float M, int8_t *q)
 /* Eq. 3: T_out = M * T_quantized.                                    */
 void tlc_o_dequantize(const int8_t *q, uint64_t n, float M, float *out)
 {
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++)
         out[i] = M * (float)q[i];
 }
@@ -93,6 +108,7 @@ void tlc_o_dequantize(const int8_t *q, uint64_t n, float M, float *out)
 /* buffer": buffer = u - M * q  (R7, R8).                         */
 void tlc_o_residual(const float *u, const int8_t *q, uint64_t n, float M, float *buf)
 {
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++)
         buf[i] = u[i] - M * (float)q[i];
 }
@@ -114,6 +130,7 @@ void tlc_o_quartic_encode(const int8_t *q, uint64_t n, uint8_t *out)
     uint64_t L = 5 * P;
     uint8_t *a = (uint8_t *)malloc(L ? L : 1);
     /* step 1 "Element-wise add 1", step 2 "Type cast it to an unsigned 8-bit integer array" */
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++)
         a[i] = (uint8_t)(q[i] + 1);
     /* step 3 "Flatten it into a 1-D array": q is already flat (row-major).   */
@@ -124,6 +141,7 @@ void tlc_o_quartic_encode(const int8_t *q, uint64_t n, uint8_t *out)
     /* -- contiguous partitions p_k = a[k*P .. (k+1)*P) (R9).                 */
     const uint8_t *p0 = a, *p1 = a + P, *p2 = a + 2 * P, *p3 = a + 3 * P, *p4 = a + 4 * P;
     /* step 6 "Compute a = p0*81 + p1*27 + p2*9 + p3*3 + p4"                  */
+#pragma omp parallel for
     for (uint64_t j = 0; j < P; j++)
         out[j] = (uint8_t)(p0[j] * 81 + p1[j] * 27 + p2[j] * 9 + p3[j] * 3 + p4[j]);
     free(a);
@@ -143,9 +161,11 @@ int tlc_o_quartic_decode(const uint8_t *B, uint64_t P, uint64_t n, int8_t *q)
     /* step 1 "Restore p0..p4 by dividing a by a power of 3 and taking the    */
     /* remainder"; step 2 "Concatenate p0..p4" -- p_k lands at a[k*P + j].     */
     for (int k = 0; k < 5; k++)
+#pragma omp parallel for
         for (uint64_t j = 0; j < P; j++)
             a[(uint64_t)k * P + j] = (uint8_t)((B[j] / pow3[k]) % 3);
     /* step 3 "Unpad, reshape, and type cast"; step 4 "Element-wise subtract 1" */
+#pragma omp parallel for
     for (uint64_t i = 0; i < n; i++)
         q[i] = (int8_t)((int)a[i] - 1);
     free(a);
@@ -272,6 +292,7 @@ int tlc_o_decompress(const uint8_t *payload, uint64_t len, int zre_flag, float M
         if (mode == 0) {
             tlc_o_dequantize(q, n, M, out);
         } else {
+#pragma omp parallel for
             for (uint64_t i = 0; i < n; i++)
                 if (q[i] != 0)
                     out[i] = out[i] + M * (float)q[i];

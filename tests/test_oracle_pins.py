@@ -390,3 +390,33 @@ def test_malformed_scale_is_format():
     for M in (-1.0, -0.0, float("nan"), float("inf")):
         st, _ = O.decompress(np.array([175], np.uint8), True, f32(M), 5)
         assert st == O.ERR_FORMAT
+
+
+def test_openmp_build_is_bitwise_identical():
+    """bench.py's cpu_baseline times the -fopenmp build of the same oracle source; it must
+    compute exactly what the plain build computes (independent element-wise loops, exact
+    max), including the NONFINITE decision and the untouched buffer."""
+    import synth
+
+    results = []
+    for omp in (False, True):
+        O.use_openmp(omp)
+        try:
+            r = []
+            for n, s in ((1, 1.0), (1000, 1.9), (300_007, 1.75)):
+                t = synth.gaussian(n, 77, n)
+                buf = (0.5 * synth.gaussian(n, 78, n)).astype(np.float32)
+                c = O.compress(t, buf, s)
+                st, out = O.decompress(c.payload, True, c.M, n)
+                acc = buf.copy()
+                st2, acc = O.decompress(c.payload, True, c.M, n, out=acc, accumulate=True)
+                bad = t.copy()
+                bad[n // 2] = np.nan
+                b2 = buf.copy()
+                cb = O.compress(bad, b2, s)
+                r.append((c.payload.tobytes(), float(c.M), buf.tobytes(), out.tobytes(), acc.tobytes(), st, st2,
+                          cb.status, b2.tobytes()))
+            results.append(r)
+        finally:
+            O.use_openmp(False)
+    assert results[0] == results[1]
