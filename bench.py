@@ -44,8 +44,9 @@ def parse():
     ap.add_argument("--s", type=float, default=1.75)
     ap.add_argument("--no-zre", action="store_true")
     ap.add_argument("--inputs", type=int, default=2, help="rotating state-change tensors")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--cpu-steps", type=int, default=2, help="timed oracle round trips at the config size")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: seconds the timed oracle steps may take before they shrink to a sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the ResNet-110 (configs[1]) side measurement")
@@ -57,6 +58,8 @@ def parse():
     ap.add_argument("--xchg", choices=["p2p", "nccl"], default="p2p",
                     help="exchange transport: peer-memory kernels over NVLink, or NCCL send/recv")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the C3 families / s grid / 2^20..2^30 size sweep side measurement")
     ap.add_argument("--no-codecs", action="store_true",
                     help="skip the compared-design codecs side measurement (Stoch 3-value + QE, 8-bit int)")
     return ap.parse_args()
@@ -157,29 +160,72 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_roundtrips(n_sample: int, s: float, zre: bool, seconds: float = None, reps: int = None):
-    """Time the CPU oracle (as it stands, single thread) on compress+decompress round
-    trips of an n_sample-element tensor of the same workload family."""
+def host_info():
+    """Host CPU of the box the oracle runs on: logical CPUs usable here and the model."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cores": cores, "cpu_model": model}
+
+
+def oracle_config(n: int, s: float, zre: bool, omp: bool, steps: int, warmup: int = 1, budget_s: float = None):
+    """Time the CPU oracle (oracle/tlc_oracle.c as it stands) on compress + decompress round
+    trips of the workload itself: an n-element N(0,1) fp32 state change, two rotating
+    inputs, the error buffer carried (steady state).  omp=True: the -fopenmp build of the
+    same source (element-wise loops on every host core, zero-run coding serial).  If a
+    time budget is given and a warm-up round trip shows the steps would exceed it, the
+    timed steps run on a leading sample of the tensor instead (stated in `sample`)."""
     import numpy as np
 
     import oracle as O
     import synth
 
-    ts = [synth.gaussian(n_sample, 3, k) for k in range(2)]
-    buf = np.zeros(n_sample, np.float32)
-    c = O.compress(ts[0], buf, s, zre)         # untimed warm-up (builds/loads the lib)
-    done, t0 = 0, time.perf_counter()
-    while True:
-        c = O.compress(ts[done % 2], buf, s, zre)
-        st, out = O.decompress(c.payload, zre, c.M, n_sample)
-        done += 1
-        el = time.perf_counter() - t0
-        if (reps is not None and done >= reps) or (seconds is not None and el >= seconds):
-            break
-    return {"value": 4.0 * n_sample * done / el / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{done} compress+decompress round trips of a {n_sample:,}-element N(0,1) fp32 "
-                      f"tensor (same generator, s={s}, error buffer carried), single thread, "
-                      f"{el:.1f} s", "seconds": el, "bits_per_value": 8.0 * c.payload_len / n_sample}
+    O.use_openmp(omp)
+    try:
+        ts = [synth.gaussian(n, 3, k) for k in range(2)]
+        buf = np.zeros(n, np.float32)
+        t_w = []
+        for k in range(max(1, warmup)):                      # untimed; page-faults the buffers
+            t0 = time.perf_counter()
+            c = O.compress(ts[k % 2], buf, s, zre)
+            O.decompress(c.payload, zre, c.M, n)
+            t_w.append(time.perf_counter() - t0)
+        m = n
+        if budget_s is not None and t_w[-1] * steps > budget_s:
+            m = max(1 << 16, int(n * budget_s / (t_w[-1] * steps)) // 1024 * 1024)
+            ts = [x[:m].copy() for x in ts]
+            buf = buf[:m].copy()
+        tc = td = 0.0
+        for k in range(steps):
+            t0 = time.perf_counter()
+            c = O.compress(ts[k % 2], buf, s, zre)
+            t1 = time.perf_counter()
+            st, out = O.decompress(c.payload, zre, c.M, m)
+            td += time.perf_counter() - t1
+            tc += t1 - t0
+            assert c.status == 0 and st == 0
+    finally:
+        O.use_openmp(False)
+    h = host_info()
+    threads = h["cores"] if omp else 1
+    el = tc + td
+    return {"value": 4.0 * m * steps / el / 1e9, "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": (f"{steps} compress+decompress round trips of the {n:,}-element workload tensor"
+                       if m == n else f"{steps} round trips of the leading {m:,} of the {n:,} elements "
+                                      f"(budget {budget_s:.0f} s)") +
+                      f" (N(0,1), s={s}, error buffer carried), "
+                      + (f"-fopenmp build on {threads} threads (element-wise loops; ZRE serial)" if omp
+                         else "plain build, 1 thread") + f", {el:.1f} s",
+            "same_config": m == n, "n_timed": m, "seconds": el, "steps": steps,
+            "compress_GBps": 4.0 * m * steps / tc / 1e9, "decompress_GBps": 4.0 * m * steps / td / 1e9,
+            "cpu_model": h["cpu_model"], "host_cores": h["cores"], "bits_per_value": 8.0 * c.payload_len / m}
 
 
 def run_reference(args):
@@ -187,19 +233,19 @@ def run_reference(args):
     if rank != 0:
         return 0
     zre = not args.no_zre
-    for _ in range(args.warmup):
-        oracle_roundtrips(args.cpu_sample, args.s, zre, reps=1)
-    r = oracle_roundtrips(args.cpu_sample, args.s, zre, reps=max(1, args.steps))
+    r = oracle_config(args.n, args.s, zre, omp=True, steps=max(1, args.steps), warmup=max(1, args.warmup),
+                      budget_s=args.ref_budget)
     ms = 1000.0 * r["seconds"] / max(1, args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: N(0,1) fp32 state changes (numpy PCG64), error buffer carried",
-        "config": {"workload": workload_name(args.n, args.s, zre) + f"; each step a bounded "
-                   f"{args.cpu_sample:,}-element sample on the host", "n": args.n, "s": args.s},
+        "config": {"workload": workload_name(args.n, args.s, zre) + ("" if r["same_config"] else
+                   f"; each step a bounded {r['n_timed']:,}-element sample on the host"), "n": args.n, "s": args.s},
         "bits_per_value": r["bits_per_value"],
-        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                           "compress_GBps", "decompress_GBps", "same_config")},
         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -280,6 +326,105 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
                      "l2": "back-to-back replays, working set L2-resident"},
             "bits_per_value": 8.0 * Z / N, "kernel_launches_per_step": 5, "kernel_us_cold": kern,
             "host_launch_calls_during_replay": T.tlc_launch_count() - l0}
+
+
+# ------------------------------------------------------------------ C3 families / s grid / size sweep
+C3_ALG = {  # algorithmic HBM bytes per launch of the codec kernels
+    "k1_absmax": lambda n, P, Z: 8.0 * n,
+    "k2_quant_qe": lambda n, P, Z: 12.0 * n + P,
+    "k3_zre": lambda n, P, Z: float(P + Z),
+    "k4_zre_scan": lambda n, P, Z: float(Z),
+    "k5_expand_dequant": lambda n, P, Z: 4.0 * n + Z,
+}
+
+
+def measure_c3_sweep(T, dev, configs, steps=10, warmup=8, flush_below=1 << 27):
+    """SURVEY 8(d) C3 side measurements next to the headline: the four input families at
+    the headline size (zeros, dense and runs with a fresh error buffer every step; gauss
+    carried to steady state), the s grid, and the 2^20..2^30 size sweep.  A step is one
+    tlc_compress + tlc_decompress timed with its own CUDA-event pair on the launching
+    stream; per-kernel device times come from a second, profiled pass (library events).
+    Tensors of n < 2^27 fit the 126 MB L2 with their error buffer and output, so the L2 is
+    flushed (512 MiB write) before each of their steps, outside the events."""
+    import torch
+
+    import synth
+
+    peak, _ = load_peaks()
+    stream = torch.cuda.current_stream(dev)
+    flush = None
+    res = []
+    for label, fam, n, s in configs:
+        ts = [synth.family_torch(fam, n, s, dev, 3, k) for k in range(2 if fam == "gauss" else 1)]
+        err = torch.zeros(n, dtype=torch.float32, device=dev)
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+        payload = torch.empty(T.tlc_max_payload_bytes(n), dtype=torch.uint8, device=dev)
+        hdr = T.new_header(dev)
+        ws_c = torch.empty(T.tlc_compress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+        ws_d = torch.empty(T.tlc_decompress_workspace_bytes(n), dtype=torch.uint8, device=dev)
+        fresh = fam != "gauss"
+        cold = n < flush_below
+        if cold and flush is None:
+            flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+        def step(k):
+            T.tlc_compress(ts[k % len(ts)], err, s, True, payload, hdr, ws_c, stream)
+            T.tlc_decompress(payload, hdr, n, out, T.TLC_MODE_OVERWRITE, ws_d, stream)
+
+        def prep(k):
+            if fresh:
+                err.zero_()
+            if cold:
+                flush.fill_(k & 0xff)
+
+        for k in range(warmup):
+            prep(k)
+            step(k)
+        torch.cuda.synchronize(dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for k in range(steps):
+            prep(k)
+            evs[k][0].record(stream)
+            step(k)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        ms = sorted(a.elapsed_time(b) for a, b in evs)
+        ms_med = ms[len(ms) // 2]
+        T.tlc_prof_collect()
+        T.tlc_prof_enable(True)
+        for k in range(steps):
+            prep(k)
+            step(k)
+        T.tlc_prof_enable(False)
+        prof = T.tlc_prof_collect()
+        h = T.parse_header(hdr)
+        P, Z = (n + 4) // 5, h["payload_len"]
+        kern = {}
+        for name, (cnt, tot) in prof.items():
+            avg = tot / max(cnt, 1)
+            b = C3_ALG[name](n, P, Z) if name in C3_ALG else None
+            kern[name] = {"avg_ms": round(avg, 5), "alg_GBps": round(b / (avg / 1e3) / 1e9, 1) if b else None}
+        k2 = kern.get("k2_quant_qe", {}).get("alg_GBps")
+        res.append({"label": label, "family": fam, "n": n, "s": s, "status": h["status"],
+                    "error_buffer": "fresh (zeroed before every step)" if fresh else "carried (steady state)",
+                    "l2": "flushed before every step" if cold else "inputs larger than L2",
+                    "value": 4.0 * n / (ms_med / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms_med,
+                    "ms_min": ms[0], "ms_max": ms[-1], "bits_per_value": 8.0 * Z / n,
+                    "step_alg_frac": (24.0 * n + 2 * P + 3 * Z) / (ms_med / 1e3) / 1e9 / peak,
+                    "k2_frac": (k2 / peak) if k2 else None, "kernels": kern})
+        del ts, err, out, payload, ws_c, ws_d
+        torch.cuda.empty_cache()
+    return {"what": "C3 side measurements (SURVEY 8(d)): families at the headline size, s grid, size sweep; "
+                    "value = fp32-input GB/s (median step), step_alg_frac = (24n + 2P + 3Z) bytes per step / "
+                    "step time / measured HBM peak, k2_frac = K2's (12n + P) / its time / peak",
+            "steps": steps, "warmup": warmup, "runs": res}
+
+
+def c3_sweep_configs(n_head, s_head):
+    cfg = [(f"family {f}", f, n_head, s_head) for f in ("zeros", "dense", "runs")]
+    cfg += [(f"gauss s={sv}", "gauss", n_head, sv) for sv in (1.0, 1.5, 1.9)]
+    cfg += [(f"gauss n=2^{e}", "gauss", 1 << e, s_head) for e in (20, 22, 24, 26, 30)]
+    return cfg
 
 
 # ------------------------------------------------------------------ exchange step (row e)
@@ -734,14 +879,26 @@ def run_tlc(args):
     if rank == 0 and world == 1 and not args.no_codecs:
         codecs = measure_codecs(T, dev, ts)
 
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        del ts, err, out, payload, ws_c, ws_d
+        torch.cuda.empty_cache()
+        sweep = measure_c3_sweep(T, dev, c3_sweep_configs(n, s))
+
     c2 = None
     if rank == 0 and not args.no_c2:
         c2 = [measure_resnet110(T, dev, sv) for sv in (1.0, 1.75, 1.9)]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = oracle_roundtrips(args.cpu_sample, s, zre, seconds=args.cpu_seconds)
-        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # the oracle at the config size, compress and decompress timed separately: the
+        # -fopenmp build on every host core (the baseline), and the plain build on one
+        r = oracle_config(n, s, zre, omp=True, steps=args.cpu_steps, budget_s=60.0)
+        r1 = oracle_config(n, s, zre, omp=False, steps=1, warmup=1, budget_s=30.0)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "host_cores",
+                                 "compress_GBps", "decompress_GBps", "same_config")}
+        cpu["single_thread"] = {k: r1[k] for k in ("value", "sample", "compress_GBps", "decompress_GBps",
+                                                    "same_config")}
 
     if rank == 0:
         line = {
@@ -750,7 +907,7 @@ def run_tlc(args):
             "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: N(0,1) fp32 state changes (numpy PCG64, synth/), "
-                    f"{len(ts)} rotating tensors per rank, error buffer carried across steps",
+                    f"{args.inputs} rotating tensors per rank, error buffer carried across steps",
             "config": {"workload": workload_name(n, s, zre), "n": n, "s": s, "use_zre": zre,
                        "family": "gauss-steady",
                        "l2": "inputs larger than L2 (t, err, out 1 GiB each vs 126 MB L2); no flush",
@@ -766,6 +923,7 @@ def run_tlc(args):
             "c2_resnet110": c2,
             "xchg_w1": xw1,
             "next3_codecs": codecs,
+            "c3_sweep": sweep,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

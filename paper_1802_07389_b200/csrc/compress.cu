@@ -626,8 +626,10 @@ constexpr uint32_t kRowNotKept = 1u << 31;
 // and, for k > 0, the flush code remainder R_k % 14 (bits 0-3) and the output
 // offset relative to the end of literal 0's bytes (bits 16-31); literal 0's
 // position is in the row's metadata, its bytes depend on the row's carry.
+constexpr uint32_t kK3Stage = (uint32_t)(kLargeItems.c3 / kK3Workers);   // phase-3 stage per warp
+static_assert(kK3Stage >= kK3WarpRow + 1 + 15, "a row's output (<= row + 1 bytes) fits the stage");
 struct K3Smem {
-    uint8_t chunk[kLargeItems.c3];                       // the chunk's quartic bytes
+    uint8_t chunk[kLargeItems.c3];                       // the chunk's quartic bytes; phase-3 stages
     uint32_t lit[2][kScanWarps][kK3LitCap];               // literal lists, row after row
     uint4 rowmeta[2][kScanWarps][kK3RowsPerWarp];         // (L | base << 16, rest | cout << 16, p0, -)
     unsigned long long bar;
@@ -662,9 +664,18 @@ __device__ __forceinline__ uint32_t row_literals(const uint32_t (&w)[8], uint32_
 // chunks, one flush code if R % 14 > 0, the literal itself.
 __device__ __forceinline__ uint32_t lit_cost(uint32_t R) { return R / kMaxRun + (R % kMaxRun != 0) + 1u; }
 
-// Load [pos, min(pos+32, hi)) from global memory as 8 words, padding with 121.
+// Load [pos, min(pos+32, hi)) from global memory as 8 words, padding with 121.  A full
+// 16-byte-aligned segment takes two 16-byte loads (byte loads from lanes 32 bytes apart
+// touched 32 sectors per instruction).
 __device__ __forceinline__ int load_seg_g(const uint8_t *bytes, uint64_t pos, uint64_t hi, uint32_t (&w)[8]) {
     const int len = pos < hi ? (int)tmin<uint64_t>(kK3Seg, hi - pos) : 0;
+    if (len == kK3Seg && aligned16(bytes + pos)) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(bytes + pos));
+        const uint4 b = __ldg(reinterpret_cast<const uint4 *>(bytes + pos) + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        return len;
+    }
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         uint32_t x = 0;
@@ -819,6 +830,8 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
             const uint32_t rwhi = (uint32_t)(cj.whi - cj.lo);
             if (threadIdx.x == 0) {
                 const uint32_t nb = (uint32_t)((cj.hi - cj.lo + 15) & ~uint64_t(15));
+                // the previous phase 3 wrote its stages here with generic stores
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&sm.bar, nb);
                 bulk_load(sm.chunk, scratch + S.bytes_off + cj.lo, nb, &sm.bar);
             }
@@ -936,7 +949,13 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     }
                     off += cost0 + (meta.y & 0xffffu);
                     carry = meta.y >> 16;
-                } else {                                  // not kept: per-lane emission from the bytes
+                } else {
+                    // not kept (a dense row: its list did not fit): every lane emits its
+                    // bytes into the warp's stage in shared memory (the chunk buffer is free
+                    // in phase 3), prefilled with 255 for the full chunks, placed congruent
+                    // to the output modulo 16; the warp then copies the row's output out with
+                    // 16-byte stores (byte stores from lanes 32 bytes apart wrote 32 sectors
+                    // per instruction: 0.31 ms on dense stochastic trits)
                     const int len = load_seg_g(bytes, row + kK3Seg * lane, pend.whi, w);
                     const uint32_t mask = literal_mask(w);
                     const WarpRow wr = warp_row(mask, len, mask_summary(mask, len), carry, row_len);
@@ -946,21 +965,15 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                         if (lane >= d) x += y;
                     }
-                    uint32_t o = x - wr.count;
-                    uint32_t c = wr.carry_in;
-                    int prev = -1;
-                    for (uint32_t m = mask; m; m &= m - 1u) {
-                        const int q = (int)ctz32(m);
-                        const uint32_t R = (uint32_t)(q - prev - 1) + c;
-                        c = 0;
-                        o += R / kMaxRun;
-                        if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
-                        uint32_t word = w[0];             // select, not a dynamic index
-#pragma unroll
-                        for (int k = 1; k < 8; k++) word = (k == (q >> 2)) ? w[k] : word;
-                        out[o++] = (uint8_t)(word >> (8 * (q & 3)));
-                        prev = q;
-                    }
+                    uint8_t *stage = sm.chunk + (size_t)wk * kK3Stage;
+                    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 15u);
+                    for (uint32_t q = lane; q < (sh + wr.row_count + 15u) / 16u; q += 32)
+                        reinterpret_cast<uint4 *>(stage)[q] = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    __syncwarp();
+                    lane_emit(w, mask, wr.carry_in, stage + sh, x - wr.count);
+                    __syncwarp();
+                    warp_copy_congruent(out, stage + sh, wr.row_count);
+                    __syncwarp();                         // the stage is reused by the next row
                     off += wr.row_count;
                     carry = wr.carry_out;
                 }

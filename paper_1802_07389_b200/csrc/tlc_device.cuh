@@ -327,6 +327,44 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
     return row_summary(r.mixbal != 0, lead, r.row_count, r.carry_out, row_len);
 }
 
+// ZRE bytes of one lane's 32 quartic bytes of a warp row, given the zero groups
+// pending before them (carry_in, from warp_row): per literal (bit of `mask`), the
+// code of the zero groups before it that do not fill a chunk of 14 (full chunks are
+// skipped -- their 255 bytes are the caller's prefill), then the literal itself
+// (P:545-546).  Fully unrolled so each byte is extracted with a static shift.
+// Writes dst[o, ...) and returns the end offset.
+__host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], uint32_t mask, uint32_t carry_in,
+                                                       uint8_t *dst, uint32_t o) {
+    int prev = -1;
+    uint32_t c = carry_in;
+#pragma unroll
+    for (int m = 0; m < 32; m++) {
+        if ((mask >> m) & 1u) {
+            const uint32_t R = (uint32_t)(m - prev - 1) + c;
+            c = 0;
+            o += R / kMaxRun;
+            const uint32_t rem = R % kMaxRun;
+            if (rem) dst[o++] = run_code(rem);
+            dst[o++] = (uint8_t)(w[m >> 2] >> (8 * (m & 3)));
+            prev = m;
+        }
+    }
+    return o;
+}
+
+// A warp copies n bytes from shared memory to global memory where src and dst are
+// congruent modulo 16: head and tail bytes singly, the middle with 16-byte stores.
+__device__ __forceinline__ void warp_copy_congruent(uint8_t *dst, const uint8_t *src, uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t head = tmin<uint32_t>(n, (16u - (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u);
+    if (lane < head) dst[lane] = src[lane];
+    const uint32_t nv = (n - head) / 16u;
+    for (uint32_t q = lane; q < nv; q += 32)
+        reinterpret_cast<uint4 *>(dst + head)[q] = reinterpret_cast<const uint4 *>(src + head)[q];
+    const uint32_t t0 = head + 16u * nv;
+    if (t0 + lane < n) dst[t0 + lane] = src[t0 + lane];
+}
+
 // A warp stores code 255 to payload[a, b): head and tail bytes singly, the
 // 16-byte-aligned middle with vector stores.  Callers __syncwarp() before
 // overwriting any of these bytes.

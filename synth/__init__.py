@@ -159,6 +159,51 @@ def family(name: str, n: int, s: float, seed: int = 3) -> np.ndarray:
     raise ValueError(name)
 
 
+def family_torch(name: str, n: int, s: float, device, seed: int = 3, step: int = 0):
+    """Device-side draw of a C3 family (bench-only, for the 2^20..2^30 sweep): the same
+    distributions as ``family`` -- gauss N(0,1); zeros; dense |t| in [s/2 + 2^-20, 1]
+    with random sign and one element exactly +1; runs: all-zero quartic groups in runs
+    of 1..100 and 14k-1/14k/14k+1 between 1-3 separator groups whose partition-0
+    element is +-1 -- from torch's seeded Philox generator (other streams than the
+    numpy generators; no parity use)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(int(np.random.SeedSequence([seed, n, step, len(name)]).generate_state(1)[0]))
+    if name == "gauss":
+        return torch.randn(n, generator=g, device=device, dtype=torch.float32)
+    if name == "zeros":
+        return torch.zeros(n, device=device, dtype=torch.float32)
+    if name == "dense":
+        lo = float(np.float32(s) / np.float32(2) + np.float32(2.0 ** -20))
+        t = torch.rand(n, generator=g, device=device, dtype=torch.float32) * (1.0 - lo) + lo
+        t = t.clamp_(min=lo, max=1.0)
+        t *= torch.randint(0, 2, (n,), generator=g, device=device, dtype=torch.int8).float() * 2 - 1
+        t[n // 2] = 1.0
+        return t
+    if name == "runs":
+        P = -(-n // 5)
+        menu = torch.tensor(list(range(1, 101)) + [14 * k + d for k in range(1, 40) for d in (-1, 0, 1)],
+                            device=device)
+        # blocks of (run of zero groups, 1-3 separators); enough blocks to cover P
+        K = P // 40 + 16
+        run = menu[torch.randint(0, menu.numel(), (K,), generator=g, device=device)]
+        sep = torch.randint(1, 4, (K,), generator=g, device=device)
+        start = torch.cumsum(run + sep, 0) - sep                     # first separator of each block
+        groups = torch.zeros(P + 4, device=device, dtype=torch.float32)
+        for k in range(3):
+            idx = start + k
+            ok = (k < sep) & (idx < P)
+            sign = torch.randint(0, 2, (K,), generator=g, device=device).float() * 2 - 1
+            groups[idx[ok]] = sign[ok]
+        t = torch.zeros(n, device=device, dtype=torch.float32)
+        t[:P] = groups[:P]                                           # partition 0 of each group
+        if not bool(t.any()):
+            t[0] = 1.0
+        return t
+    raise ValueError(name)
+
+
 def blobs(n_train: int, n_test: int, dim: int, classes: int, std: float, *key: int):
     """Desk-scale classification task of the training simulator (the
     stand-in for CIFAR-10): class c is centred at a seeded random unit-norm vector

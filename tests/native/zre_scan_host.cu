@@ -111,6 +111,24 @@ void emit_row_list(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint
     if (carry > 0 && row + r.row_len == P) out[off] = run_code(carry);
 }
 
+// K3 phase 3 for a row whose literal list was not kept (dense rows): every lane
+// emits its own bytes with lane_emit into a stage prefilled with 255, at its
+// exclusive-scanned offset; the row's output is then copied out.
+void emit_row_lanes(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint8_t *out, uint64_t &off) {
+    uint8_t stage[LANES * SEG + 16];
+    std::memset(stage, 0xff, sizeof stage);
+    uint32_t o = 0;
+    for (int l = 0; l < LANES; l++) {
+        const uint32_t end = lane_emit(r.w[l], r.mask[l], r.carry_in[l], stage, o);
+        if (r.len[l] > 0 && end > o + r.count[l]) std::abort();   // lane_emit never writes past its count
+        o += r.count[l];
+    }
+    std::memcpy(out + off, stage, r.row_count);
+    off += r.row_count;
+    carry = r.carry_out;
+    if (carry > 0 && row + r.row_len == P) out[off] = run_code(carry);
+}
+
 void load_row(const uint8_t *B, uint64_t row, uint64_t whi, Row &r) {
     r.row_len = (uint32_t)std::min<uint64_t>((uint64_t)LANES * SEG, whi - row);
     for (int l = 0; l < LANES; l++) {
@@ -121,7 +139,8 @@ void load_row(const uint8_t *B, uint64_t row, uint64_t whi, Row &r) {
 }
 }  // namespace
 
-extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out) {
+extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out,
+                                      int lane_mode) {
     uint64_t chunk = (P + nchunks_req - 1) / nchunks_req;
     chunk = (chunk + SEG - 1) / SEG * SEG;
     const uint64_t nch = (P + chunk - 1) / chunk;
@@ -175,11 +194,16 @@ extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
                 load_row(B, row, whi, r);
                 warp_row_host(r, carry);
-                emit_row_list(r, row, P, carry, out, off);
+                if (lane_mode) emit_row_lanes(r, row, P, carry, out, off);
+                else emit_row_list(r, row, P, carry, out, off);
             }
         }
     }
     return total;
+}
+
+extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out) {
+    return zre_scan_sim_mode(B, P, warps, nchunks_req, out, 0);
 }
 
 // K4's SWAR expansion length of a payload word (tlc_device.cuh word_len), host form

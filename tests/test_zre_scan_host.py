@@ -29,11 +29,14 @@ def sim():
     L = ctypes.CDLL(LIB)
     L.zre_scan_sim.restype = ctypes.c_uint64
     L.zre_scan_sim.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p]
+    L.zre_scan_sim_mode.restype = ctypes.c_uint64
+    L.zre_scan_sim_mode.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
+                                    ctypes.c_void_p, ctypes.c_int]
 
-    def run(B, threads, nchunks):
+    def run(B, threads, nchunks, lane_mode=0):
         B = np.ascontiguousarray(B, dtype=np.uint8)
         out = np.full(B.size + 16, 0xEE, dtype=np.uint8)
-        z = L.zre_scan_sim(B.ctypes.data, B.size, threads, nchunks, out.ctypes.data)
+        z = L.zre_scan_sim_mode(B.ctypes.data, B.size, threads, nchunks, out.ctypes.data, lane_mode)
         assert np.all(out[z:] == 0xEE), "bytes emitted past the computed payload length"
         return out[:z]
 
@@ -47,7 +50,9 @@ def _streams():
     yield np.array([5], np.uint8)
     for L in (13, 14, 15, 27, 28, 29, 200, 4096, 4097):
         yield np.full(L, 121, np.uint8)
-    for p in (0.5, 0.9, 0.97, 0.995):
+    dense = g.integers(0, 242, 5000).astype(np.uint8)       # no zero group at all (dense family)
+    yield np.where(dense >= 121, dense + 1, dense).astype(np.uint8)
+    for p in (0.1, 0.5, 0.9, 0.97, 0.995):
         for L in (1, 7, 8, 9, 100, 2047, 2048, 2049, 20000):
             yield np.where(g.random(L) < p, 121, g.integers(0, 243, L)).astype(np.uint8)
     # run lengths 1..100 and 14k-1/14k/14k+1 separated by literals
@@ -58,13 +63,16 @@ def _streams():
     yield np.array(parts, np.uint8)
 
 
+@pytest.mark.parametrize("lane_mode", [0, 1])
 @pytest.mark.parametrize("threads", [1, 2, 3, 8])
-def test_scan_matches_oracle_zre(sim, threads):  # threads = warps per CTA
+def test_scan_matches_oracle_zre(sim, threads, lane_mode):  # threads = warps per CTA
+    """lane_mode 0: rows emitted from their kept literal lists; 1: the dense-row form,
+    every lane's bytes emitted by lane_emit into a 255-prefilled stage."""
     for i, B in enumerate(_streams()):
         ref = O.zre_encode(B)
         for nchunks in (1, 2, 3, 7, 64):
-            got = sim(B, threads, nchunks)
-            assert got.tolist() == ref.tolist(), (threads, nchunks, i, B.size)
+            got = sim(B, threads, nchunks, lane_mode)
+            assert got.tolist() == ref.tolist(), (threads, nchunks, i, B.size, lane_mode)
 
 
 def test_word_len_swar_matches_bytewise(sim):
