@@ -652,6 +652,49 @@ def measure_exchange_graph(T, dev, world, rank, model, s, steps, warmup, dist=No
     return ms, sum(sizes), status
 
 
+def measure_allreduce(dev, world, rank, model, steps, warmup, dist, graph=False):
+    """The paper's baseline, "32-bit float": the same per-rank gradient set
+    averaged uncompressed -- one ncclAllReduce (sum) of the flat fp32 set, then / W --
+    timed like the exchange (events on the stream, max over ranks).  graph=True captures
+    the step in a CUDA graph (the ResNet-110 case, as its exchange is)."""
+    import torch
+
+    import synth
+
+    sizes = synth.MODELS[model]
+    flat = torch.cat(synth.model_step_torch(model, 0, rank, dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        dist.all_reduce(flat)
+        flat.div_(world)
+
+    for _ in range(max(3, warmup)):
+        step()
+    g = None
+    if graph:
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        g.replay() if g is not None else step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del g, flat
+    torch.cuda.empty_cache()
+    return float(t.item()), sum(sizes)
+
+
 def run_exchange_leg(args, T, dev, world, rank, dist, e2e_steps=None):
     import torch
 
@@ -940,8 +983,11 @@ def run_exchange_main(args, T, dev, world, rank, dist):
     clocks.start()
     r, ms, value = run_exchange_leg(args, T, dev, world, rank, dist)
     clocks.stop()
-    c4 = []
+    ar_ms, _ = measure_allreduce(dev, world, rank, args.model, args.steps, args.warmup, dist)
+    c4, ar4_ms = [], None
     if not args.no_c2:
+        ar4_ms, _ = measure_allreduce(dev, world, rank, "resnet110", max(args.steps, 50), args.warmup, dist,
+                                      graph=True)
         for s4 in (1.0, 1.75, 1.9):
             ms4, n4, st4 = measure_exchange_graph(T, dev, world, rank, "resnet110", s4, max(args.steps, 50),
                                                   args.warmup, dist)
@@ -949,7 +995,8 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms4 = float(t.item())
             c4.append({"s": s4, "ms_per_step": ms4, "value": world * 4.0 * n4 / (ms4 / 1e3) / 1e9, "unit": "GB/s",
-                       "status": st4})
+                       "status": st4, "allreduce_fp32_ms_per_step": ar4_ms,
+                       "speedup_vs_allreduce": ar4_ms / ms4})
     if rank == 0:
         pct_nvlink = r["wire"] / 2 / (ms / 1e3) / 1e9 / NVLINK_GBS   # per direction
         line = {
@@ -971,6 +1018,11 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             "wire_bytes_per_rank_per_step": r["wire"],
             "wire_definition": "bytes rank 0 received from other ranks per step (push + pull)",
             "nvlink_frac": pct_nvlink,
+            "allreduce_fp32": {"what": "the paper's '32-bit float' baseline (P:621-622) on the same tensors: "
+                                       "ncclAllReduce(sum) of the flat fp32 gradient set + /W, events, max over ranks",
+                               "ms_per_step": ar_ms, "value": world * 4.0 * r["N"] / (ar_ms / 1e3) / 1e9,
+                               "unit": "GB/s"},
+            "speedup_vs_allreduce": ar_ms / ms,
             "roofline": exchange_roofline(r),
             "kernel_ms_per_step_rank0": r["kernel_ms"],
             "kernels_rank0": r["kernels"],

@@ -856,12 +856,14 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                     continue;
                 }
                 bool stored = false;
-                const uint32_t L = row_literals(w, lit + used, keep ? kK3LitCap - used : 0u, stored);
+                // once a list has not fit, the warp's later rows of the chunk take the mask
+                // form directly (they could not be kept in order anyway)
+                const uint32_t L = keep ? row_literals(w, lit + used, kK3LitCap - used, stored) : 0u;
                 if (!stored) {                                        // list space exhausted: mask form
                     keep = false;
                     const uint32_t mask = literal_mask(w);
                     wagg = compose(wagg, warp_row_summary(mask, len, mask_summary(mask, len), row_len));
-                    if (lane == 0) sm.rowmeta[jb][wk][r] = make_uint4(kRowNotKept | L, 0u, 0u, 0u);
+                    if (lane == 0) sm.rowmeta[jb][wk][r] = make_uint4(kRowNotKept | 1u, 0u, 0u, 0u);   // L != 0
                     continue;
                 }
                 // literal k > 0 is preceded by R_k = p_k - p_{k-1} - 1 zero groups and costs

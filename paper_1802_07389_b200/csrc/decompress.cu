@@ -49,6 +49,11 @@ __device__ __forceinline__ uint32_t pay16(const uint8_t *__restrict__ p, uint64_
     return sum;
 }
 
+// rows of 32 lanes x 16 bytes per warp and chunk (the large item size; small chunks use fewer)
+constexpr int kK4Rows = (int)(kLargeItems.c4 / kScanWarps / (32 * kK4Seg));
+static_assert(kK4Rows * kScanWarps * 32 * kK4Seg == (int)kLargeItems.c4, "whole rows per warp");
+static_assert(kSmallItems.c4 <= kLargeItems.c4, "small chunks need no more rows");
+
 __global__ void __launch_bounds__(kK4Threads)
 tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, unsigned long long *seek) {
     __shared__ unsigned long long s_warp[kScanWarps];
@@ -93,12 +98,19 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         const uint64_t sub = ((hi - lo + kScanWarps - 1) / kScanWarps + kK4Seg - 1) / kK4Seg * kK4Seg;
         const uint64_t wlo = tmin<uint64_t>(hi, lo + warp * sub), whi = tmin<uint64_t>(hi, wlo + sub);
 
-        // ---- phase 1: expansion length of each warp's sub-range, then of the chunk
-        uint64_t wsum = 0;
+        // ---- phase 1: expansion length of each warp's sub-range, then of the chunk.  The
+        // rows' loads are all issued before any reduction, and every lane keeps its rows'
+        // sums for phase 3 (which then reloads bytes only where an output tile starts).
         uint32_t wv[4];
         int nb;
-        for (uint64_t row = wlo; row < whi; row += kWRow) {
-            uint32_t sum = pay16(S.payload, row + (uint64_t)kK4Seg * lane, whi, wv, nb);
+        uint32_t rsum[kK4Rows];
+#pragma unroll
+        for (int r = 0; r < kK4Rows; r++)
+            rsum[r] = pay16(S.payload, wlo + (uint64_t)r * kWRow + (uint64_t)kK4Seg * lane, whi, wv, nb);
+        uint64_t wsum = 0;
+#pragma unroll
+        for (int r = 0; r < kK4Rows; r++) {
+            uint32_t sum = rsum[r];
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
             wsum += sum;
@@ -128,9 +140,12 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
         // ---- phase 3: seek entries (payload byte covering J0 = k*kT5, offset inside it).  A
         // lane's 16 bytes expand to at most 16*14 < kT5 positions: at most one J0 falls in them.
         uint64_t q0 = run + before;                       // position of the warp's first byte
-        for (uint64_t row = wlo; row < whi; row += kWRow) {
+#pragma unroll
+        for (int r = 0; r < kK4Rows; r++) {
+            const uint64_t row = wlo + (uint64_t)r * kWRow;
+            if (row >= whi) break;                        // warp-uniform
             const uint64_t pos0 = row + (uint64_t)kK4Seg * lane;
-            const uint32_t sum = pay16(S.payload, pos0, whi, wv, nb);
+            const uint32_t sum = rsum[r];
             uint32_t x = sum;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -140,6 +155,7 @@ tlc_zre_scan_kernel(const SegTable T, Ctrl *ctrl, unsigned long long *states, un
             uint64_t q = q0 + (x - sum);
             const uint64_t kt = (q + kT5 - 1) / kT5, J0 = kt * kT5;
             if (J0 < q + sum && kt < num_out_tiles) {
+                pay16(S.payload, pos0, whi, wv, nb);      // this lane's bytes again (L2)
 #pragma unroll
                 for (int k = 0; k < kK4Seg; k++) {
                     if (k >= nb) break;

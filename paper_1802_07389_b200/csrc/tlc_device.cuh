@@ -329,24 +329,36 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
 
 // ZRE bytes of one lane's 32 quartic bytes of a warp row, given the zero groups
 // pending before them (carry_in, from warp_row): per literal (bit of `mask`), the
-// code of the zero groups before it that do not fill a chunk of 14 (full chunks are
+// code of the pending zero groups that do not fill a chunk of 14 (full chunks are
 // skipped -- their 255 bytes are the caller's prefill), then the literal itself
-// (P:545-546).  Fully unrolled so each byte is extracted with a static shift.
-// Writes dst[o, ...) and returns the end offset.
+// (P:545-546).  Word by word: a word of four literals with nothing pending is stored
+// as is (dense data: 0.78 -> ~0.1 K instructions per lane and row); other words go
+// byte by byte.  Writes dst[o, ...) and returns the end offset.
 __host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], uint32_t mask, uint32_t carry_in,
                                                        uint8_t *dst, uint32_t o) {
-    int prev = -1;
-    uint32_t c = carry_in;
+    uint32_t c = carry_in;                                   // zero groups pending
 #pragma unroll
-    for (int m = 0; m < 32; m++) {
-        if ((mask >> m) & 1u) {
-            const uint32_t R = (uint32_t)(m - prev - 1) + c;
-            c = 0;
-            o += R / kMaxRun;
-            const uint32_t rem = R % kMaxRun;
-            if (rem) dst[o++] = run_code(rem);
-            dst[o++] = (uint8_t)(w[m >> 2] >> (8 * (m & 3)));
-            prev = m;
+    for (int k = 0; k < 8; k++) {
+        const uint32_t mk = (mask >> (4 * k)) & 0xfu;
+        if (mk == 0xfu && c == 0) {
+            dst[o] = (uint8_t)w[k];
+            dst[o + 1] = (uint8_t)(w[k] >> 8);
+            dst[o + 2] = (uint8_t)(w[k] >> 16);
+            dst[o + 3] = (uint8_t)(w[k] >> 24);
+            o += 4;
+            continue;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if ((mk >> q) & 1u) {
+                o += c / kMaxRun;
+                const uint32_t rem = c % kMaxRun;
+                if (rem) dst[o++] = run_code(rem);
+                c = 0;
+                dst[o++] = (uint8_t)(w[k] >> (8 * q));
+            } else {
+                c++;
+            }
         }
     }
     return o;

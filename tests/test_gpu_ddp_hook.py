@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 S, STEPS = 1.75, 4
 
 
-def _worker(rank, world, port, q, p2p):
+def _worker(rank, world, port, q, p2p, batch=False, nan_step=-1):
     import torch
     import torch.distributed as dist
     from torch.nn.parallel import DistributedDataParallel as DDP
@@ -28,70 +28,105 @@ def _worker(rank, world, port, q, p2p):
         model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 300),
                                     torch.nn.ReLU(), torch.nn.Linear(300, 10)).to(dev)
         ddp = DDP(model, device_ids=[rank], bucket_cap_mb=0.1)
-        state = TLCHookState(s=S, p2p=p2p)
-        rec = []
+        state = TLCHookState(s=S, p2p=p2p, batch=batch)
+        steps = []
 
         def hook(st, bucket):
             inp = bucket.buffer().detach().clone()
+            if rank == 1 and len(steps) == nan_step and bucket.index() == 0:
+                bucket.buffer()[3] = float("nan")           # one rank's gradient goes non-finite
+                inp = bucket.buffer().detach().clone()
             fut = tlc_hook(st, bucket)
-            rec.append((len(rec), bucket.index(), inp.cpu().numpy(), fut.value().detach().clone().cpu().numpy()))
+            steps[-1].append((bucket.index(), inp, fut))
             return fut
 
         ddp.register_comm_hook(state, hook)
         opt = torch.optim.SGD(ddp.parameters(), lr=0.01)
         g = torch.Generator(device="cpu").manual_seed(100 + rank)
-        grads_ok = True
+        rec = []
         for step in range(STEPS):
             x = torch.randn(32, 64, generator=g).to(dev)
             opt.zero_grad()
+            steps.append([])
             loss = ddp(x).square().mean()
             loss.backward()
             torch.cuda.synchronize()
-            opt.step()
+            rec.append([(i, inp.cpu().numpy(), f.value().detach().clone().cpu().numpy()) for i, inp, f in steps[-1]])
+            if step != nan_step:
+                opt.step()
         params = [p.detach().cpu().numpy() for p in model.parameters()]
-        q.put((rank, rec, params, grads_ok))
+        q.put((rank, rec, params))
         state.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("p2p", [False, True])
-def test_ddp_hook_matches_oracle(p2p):
-    import torch
+def _launch(world, p2p, batch=False, nan_step=-1):
     import torch.multiprocessing as mp
 
-    from oracle import exchange as X
-
-    world = 2
-    if torch.cuda.device_count() < world:
-        pytest.skip("needs 2 GPUs")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, p2p)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, p2p, batch, nan_step)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict((r, (rec, params)) for r, rec, params, _ in (q.get(timeout=600) for _ in range(world)))
+    res = dict((r, (rec, params)) for r, rec, params in (q.get(timeout=600) for _ in range(world)))
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    return res
+
+
+def _oracle_check(res, world, batch, nan_step=-1):
+    from oracle import exchange as X
+
     rec0, rec1 = res[0][0], res[1][0]
-    assert len(rec0) == len(rec1) and len(rec0) >= STEPS
+    assert len(rec0) == len(rec1) == STEPS
     ps = {}
-    for (i0, b0, in0, out0), (i1, b1, in1, out1) in zip(rec0, rec1):
-        assert b0 == b1 and in0.size == in1.size
-        key = b0
-        if key not in ps or ps[key][0] != in0.size:
-            ps[key] = (in0.size, X.VirtualPS([in0.size], world))
-        vp = ps[key][1]
-        means, _ = vp.push([[in0.astype(np.float32)], [in1.astype(np.float32)]], S)
-        outs = [[np.zeros(in0.size, np.float32)] for _ in range(world)]
-        vp.pull(means, outs, S)
-        assert np.array_equal(out0.view(np.uint32), outs[0][0].view(np.uint32)), ("rank 0", i0, b0)
-        assert np.array_equal(out1.view(np.uint32), outs[1][0].view(np.uint32)), ("rank 1", i1, b1)
+    for step, (b0s, b1s) in enumerate(zip(rec0, rec1)):
+        assert [b[0] for b in b0s] == [b[0] for b in b1s]
+        groups = [sorted(zip(b0s, b1s), key=lambda e: e[0][0])] if batch else [[e] for e in zip(b0s, b1s)]
+        for grp in groups:
+            sizes = tuple(a[1].size for a, _ in grp)
+            key = sizes if batch else grp[0][0][0]
+            if key not in ps or ps[key][0] != sizes:
+                ps[key] = (sizes, X.VirtualPS(list(sizes), world))
+            vp = ps[key][1]
+            means, _ = vp.push([[a[1].astype(np.float32) for a, _ in grp], [b[1].astype(np.float32) for _, b in grp]], S)
+            outs = [[np.zeros(n, np.float32) for n in sizes] for _ in range(world)]
+            shared = vp.pull(means, outs, S)
+            failed = any(p.status for p in shared)
+            for k, (a, b) in enumerate(grp):
+                if failed:                                   # R24: every rank gets NaN
+                    assert np.isnan(a[2]).all() and np.isnan(b[2]).all(), (step, k)
+                    continue
+                assert np.array_equal(a[2].view(np.uint32), outs[0][k].view(np.uint32)), ("rank 0", step, a[0])
+                assert np.array_equal(b[2].view(np.uint32), outs[1][k].view(np.uint32)), ("rank 1", step, b[0])
+            if step == nan_step:
+                assert failed
     # identical reduced gradients -> identical parameters on both ranks
     for a, b in zip(res[0][1], res[1][1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("p2p,batch", [(False, False), (True, False), (True, True)])
+def test_ddp_hook_matches_oracle(p2p, batch):
+    import torch
+
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs 2 GPUs")
+    _oracle_check(_launch(world, p2p, batch), world, batch)
+
+
+@pytest.mark.parametrize("batch", [False, True])
+def test_ddp_hook_nonfinite_gradient_is_nan_on_every_rank(batch):
+    import torch
+
+    world = 2
+    if torch.cuda.device_count() < world:
+        pytest.skip("needs 2 GPUs")
+    _oracle_check(_launch(world, True, batch, nan_step=1), world, batch, nan_step=1)
