@@ -71,6 +71,10 @@ typedef struct tlc_header {
 /* Library version (major*10000 + minor*100 + patch). */
 int tlc_version(void);
 
+/* 16 hex digits: sha256 of the csrc/ and include/ sources and the nvcc flags this
+ * library was built from (build.py rebuilds whenever it differs from the tree). */
+const char *tlc_build_id(void);
+
 /* Human-readable name of a tlc_status value; never NULL. */
 const char *tlc_status_string(int status);
 
@@ -94,7 +98,8 @@ size_t tlc_decompress_workspace_bytes(uint64_t n);
  *                 compression context.  Zero-initialised by the
  *                 caller before the first call (R20); one writer at a time
  *                 (S:167).  Left unmodified when a data error is raised.
- *                 Must not alias t or payload.
+ *                 Must not overlap t, payload or hdr (TLC_ERR_ARG: any two of
+ *                 the ranges t[n], err[n], payload[payload_cap], hdr share a byte).
  *  n        number of elements, >= 1.
  *  s        sparsity multiplier, fp32, 1 <= s < 2.
  *  use_zre  nonzero: apply zero-run encoding (step 4); 0: payload = quartic bytes.
@@ -281,6 +286,14 @@ float *tlc_exchange_owned_buffer(tlc_exchange *x);
 float *tlc_exchange_push_error(tlc_exchange *x);
 float *tlc_exchange_pull_error(tlc_exchange *x);
 uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction /* 0 push, 1 pull */);
+/* tlc_exchange_bind_error_buffers: make caller-owned DEVICE buffers the exchange's
+ * error-accumulation state (the contexts of P:400-404 are training state to
+ * checkpoint): push_err[tlc_exchange_push_error's length = every context] and
+ * pull_err[tlc_exchange_owned_elements] (either may be NULL: unchanged).  Their
+ * contents are used as they are (zero them for a fresh start, R20, or restore a
+ * checkpoint); the caller keeps them alive and unaliased until the exchange is
+ * destroyed.  Synchronizes the device. */
+int tlc_exchange_bind_error_buffers(tlc_exchange *x, float *push_err, float *pull_err);
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream);
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream);
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status, void *stream);
@@ -319,10 +332,53 @@ tlc_exchange *tlc_loopback_rank(tlc_loopback *group, int rank);
 int tlc_loopback_push(tlc_loopback *group, const float *const *grads, float s, int use_zre, void *stream);
 int tlc_loopback_pull(tlc_loopback *group, float *const *outs, float s, int use_zre, void *stream);
 
+/* Standalone aggregation: the server's "average the gradients" over
+ * `world` (1..8) compressed copies of a list of `count` tensors, for callers that
+ * move the payloads themselves (e.g. a single-server simulator).  outs: HOST
+ * array of count descriptors (out = fp32[n] DEVICE output, n); srcs: HOST array
+ * of world x count descriptors, rank-major (srcs[w*count + i]: payload and hdr
+ * of rank w's compression of tensor i, n).  tlc_aggregate_run overwrites every
+ * out with fl(fold_w M_w q_w / world): the rank-ordered fp32 sum from +0 of the
+ * nonzero dequantized trits, then the IEEE quotient (R15), in one fused pass
+ * (K4 scan + K5m); a tensor with any source whose header is not OK gets NaN
+ * (R24).  Enqueues on `stream`; the descriptors are fixed at create. */
+typedef struct tlc_aggregate tlc_aggregate;
+int tlc_aggregate_create(tlc_aggregate **agg, int world, int count, const tlc_tensor_desc *outs,
+                         const tlc_tensor_desc *srcs);
+int tlc_aggregate_run(tlc_aggregate *agg, void *stream);
+int tlc_aggregate_destroy(tlc_aggregate *agg);
+
 /* Bytes this rank received from other ranks in the last push (out[0]) and pull
  * (out[1]): capacity regions + headers with NCCL; exactly the payload_len (+
  * header) bytes read over NVLink in peer-memory mode.  Synchronizes the device. */
 int tlc_exchange_traffic(tlc_exchange *x, uint64_t *out);
+
+/* ---------------------------------------------------------------------------
+ * 3LC1 blobs (host memory only): one compressed tensor as
+ * "3LC1" | version 1 | codec (0 = 3LC pipeline incl. Stoch 3-value + QE, 2 =
+ * 8-bit int) | flags (bit 0 = ZRE) | rank | rank x u64 dims | f32 M |
+ * u64 payload_len | payload, little-endian -- the file format of oracle-parity
+ * dumps.  Bits/value counts the payload only (R14).
+ *
+ * tlc_blob_size   bytes of a blob with `rank` dims and payload_len payload bytes
+ *                 (0 if rank is outside 0..255).
+ * tlc_blob_write  hdr: a HOST copy of a successful compression's header
+ *                 (status OK, n = product of dims); payload: host, hdr->
+ *                 payload_len bytes; writes tlc_blob_size(...) bytes to `out`
+ *                 (TLC_ERR_CAPACITY if out_cap is short) and their count to
+ *                 *written.
+ * tlc_blob_read   parses `len` bytes: fills *hdr (M, flags, n = product of dims,
+ *                 payload_len, status 0), *rank and dims[0..rank) (dims_cap
+ *                 entries available, else TLC_ERR_CAPACITY), and the payload's
+ *                 offset in the blob.  TLC_ERR_FORMAT for a bad magic / version
+ *                 / codec / flags, a truncated or overlong blob, or a payload
+ *                 length impossible for n ("malformed header").
+ */
+uint64_t tlc_blob_size(int rank, uint64_t payload_len);
+int tlc_blob_write(const tlc_header *hdr, int rank, const uint64_t *dims, const uint8_t *payload,
+                   uint8_t *out, uint64_t out_cap, uint64_t *written);
+int tlc_blob_read(const uint8_t *blob, uint64_t len, tlc_header *hdr, int *rank, uint64_t *dims,
+                  int dims_cap, uint64_t *payload_offset);
 
 /* ---------------------------------------------------------------------------
  * Instrumentation (host-side, not part of the method).

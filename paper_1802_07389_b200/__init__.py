@@ -15,7 +15,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtlc.so")
+# TLC_LIB: a development build of the same sources (tools/, e.g. a -DTLC_K6C_TRACE variant)
+LIB_PATH = os.environ.get("TLC_LIB") or os.path.join(_HERE, "libtlc.so")
 
 TLC_OK, TLC_ERR_ARG, TLC_ERR_NONFINITE, TLC_ERR_RANGE, TLC_ERR_FORMAT, TLC_ERR_CAPACITY, \
     TLC_ERR_CUDA, TLC_ERR_NCCL = range(8)
@@ -40,6 +41,7 @@ def _load():
     P, U64, SZ, F, I = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_float, ctypes.c_int
     sig = {
         "tlc_version": (I, []),
+        "tlc_build_id": (ctypes.c_char_p, []),
         "tlc_status_string": (ctypes.c_char_p, [I]),
         "tlc_quartic_bytes": (U64, [U64]),
         "tlc_max_payload_bytes": (U64, [U64]),
@@ -67,6 +69,7 @@ def _load():
         "tlc_exchange_push_error": (P, [P]),
         "tlc_exchange_pull_error": (P, [P]),
         "tlc_exchange_wire_bytes": (U64, [P, I]),
+        "tlc_exchange_bind_error_buffers": (I, [P, P, P]),
         "tlc_exchange_push": (I, [P, P, F, I, P]),
         "tlc_exchange_pull": (I, [P, P, F, I, P]),
         "tlc_exchange_status": (I, [P, P, P]),
@@ -83,6 +86,12 @@ def _load():
         "tlc_int8_workspace_bytes": (SZ, [U64]),
         "tlc_int8_compress": (I, [P, U64, P, P, P, SZ, P]),
         "tlc_int8_decompress": (I, [P, P, U64, P, I, P]),
+        "tlc_aggregate_create": (I, [P, I, I, P, P]),
+        "tlc_aggregate_run": (I, [P, P]),
+        "tlc_aggregate_destroy": (I, [P]),
+        "tlc_blob_size": (U64, [I, U64]),
+        "tlc_blob_write": (I, [P, I, P, P, P, U64, P]),
+        "tlc_blob_read": (I, [P, U64, P, P, P, I, P]),
         "tlc_launch_count": (ctypes.c_ulonglong, []),
         "tlc_prof_enable": (None, [I]),
         "tlc_prof_collect": (I, [P, I]),
@@ -103,6 +112,10 @@ def lib():
 # ------------------------------------------------------------------ sizes / strings
 def tlc_version() -> int:
     return _lib.tlc_version()
+
+
+def tlc_build_id() -> str:
+    return _lib.tlc_build_id().decode()
 
 
 def tlc_status_string(code: int) -> str:
@@ -165,6 +178,44 @@ def parse_header(hdr: torch.Tensor) -> dict:
     raw = bytes(hdr.detach().to("cpu").numpy().tobytes())
     M, flags, n, plen, status, _ = struct.unpack("<fIQQII", raw)
     return {"M": M, "flags": flags, "n": n, "payload_len": plen, "status": status}
+
+
+class Header(ctypes.Structure):
+    """struct tlc_header (include/tlc.h), host copy."""
+    _fields_ = [("M", ctypes.c_float), ("flags", ctypes.c_uint32), ("n", ctypes.c_uint64),
+                ("payload_len", ctypes.c_uint64), ("status", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+def tlc_blob_write(hdr: dict, dims, payload: bytes) -> bytes:
+    """3LC1 blob of a compressed tensor: `hdr` as parse_header() returns it,
+    `payload` its payload_len bytes (host).  Marshalling only: the C ABI writes the bytes."""
+    h = Header(float(hdr["M"]), int(hdr["flags"]), int(hdr["n"]), int(hdr["payload_len"]), int(hdr["status"]), 0)
+    d = (ctypes.c_uint64 * max(1, len(dims)))(*[int(x) for x in dims])
+    pb = bytes(payload)
+    cap = int(_lib.tlc_blob_size(len(dims), len(pb)))
+    out = (ctypes.c_uint8 * max(cap, 1))()
+    wr = ctypes.c_uint64()
+    src = ctypes.create_string_buffer(pb, max(1, len(pb)))
+    rc = _lib.tlc_blob_write(ctypes.byref(h), len(dims), ctypes.cast(d, ctypes.c_void_p), src, out, cap,
+                             ctypes.byref(wr))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_blob_write")
+    return bytes(out)[: wr.value]
+
+
+def tlc_blob_read(blob: bytes):
+    """(header dict, dims, payload bytes) of a 3LC1 blob; TlcError(FORMAT) if malformed."""
+    b = bytes(blob)
+    h = Header()
+    rank = ctypes.c_int()
+    dims = (ctypes.c_uint64 * 255)()
+    off = ctypes.c_uint64()
+    src = ctypes.create_string_buffer(b, max(1, len(b)))
+    rc = _lib.tlc_blob_read(src, len(b), ctypes.byref(h), ctypes.byref(rank), dims, 255, ctypes.byref(off))
+    if rc != TLC_OK:
+        raise TlcError(rc, "tlc_blob_read")
+    hd = {"M": h.M, "flags": h.flags, "n": h.n, "payload_len": h.payload_len, "status": h.status}
+    return hd, [int(dims[i]) for i in range(rank.value)], b[off.value: off.value + h.payload_len]
 
 
 # ------------------------------------------------------------------ the ABI calls
@@ -466,6 +517,26 @@ class Exchange:
             raise TlcError(rc, "tlc_exchange_traffic")
         return int(out[0]), int(out[1])
 
+    def bind_error_buffers(self, push_err: torch.Tensor | None = None, pull_err: torch.Tensor | None = None):
+        """Use caller-owned fp32 device tensors as the push / pull error buffers (checkpointable
+        training state; contents used as they are).  The exchange keeps references to them."""
+        if push_err is not None:
+            _check_dev("push_err", push_err, torch.float32)
+            if push_err.numel() != self.push_err.numel() or push_err.device != self.device:
+                raise ValueError(f"push_err must hold {self.push_err.numel()} values on {self.device}")
+        if pull_err is not None:
+            _check_dev("pull_err", pull_err, torch.float32)
+            if pull_err.numel() != self.owned_elements or pull_err.device != self.device:
+                raise ValueError(f"pull_err must hold {self.owned_elements} values on {self.device}")
+        rc = _lib.tlc_exchange_bind_error_buffers(self._x, push_err.data_ptr() if push_err is not None else None,
+                                                  pull_err.data_ptr() if pull_err is not None else None)
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_exchange_bind_error_buffers")
+        if push_err is not None:
+            self.push_err = push_err
+        if pull_err is not None and self.owned_elements:
+            self.pull_err = pull_err
+
     def wire_bytes(self, direction: int) -> int:
         return int(_lib.tlc_exchange_wire_bytes(self._x, int(direction)))
 
@@ -559,6 +630,43 @@ class Loopback:
         if self._g:
             _lib.tlc_loopback_destroy(self._g)
             self._g = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Aggregate:
+    """tlc_aggregate: outs[i] <- mean over W ranks of the decompressed sources[w][i] (rank-
+    ordered fp32 fold of the nonzero trits, then IEEE / W; R15), one fused launch pair.
+    sources[w] = (payloads, headers) of rank w, as TensorSet keeps them."""
+
+    def __init__(self, outs, sources):
+        self.W, self.outs = len(sources), list(outs)
+        rows_o = [(None, None, o, None, None, o.numel()) for o in self.outs]
+        rows_s = []
+        for pays, hdrs in sources:
+            if len(pays) != len(self.outs) or len(hdrs) != len(self.outs):
+                raise ValueError("every rank needs one payload and header per output")
+            rows_s += [(None, None, None, p, h, o.numel()) for p, h, o in zip(pays, hdrs, self.outs)]
+        ao, asrc = _descs(rows_o), _descs(rows_s)
+        self._a = ctypes.c_void_p()
+        rc = _lib.tlc_aggregate_create(ctypes.byref(self._a), self.W, len(self.outs), ctypes.cast(ao, ctypes.c_void_p),
+                                       ctypes.cast(asrc, ctypes.c_void_p))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_aggregate_create")
+
+    def run(self, stream=None):
+        rc = _lib.tlc_aggregate_run(self._a, _stream_ptr(stream))
+        if rc != TLC_OK:
+            raise TlcError(rc, "tlc_aggregate_run")
+
+    def close(self):
+        if self._a:
+            _lib.tlc_aggregate_destroy(self._a)
+            self._a = ctypes.c_void_p()
 
     def __del__(self):
         try:

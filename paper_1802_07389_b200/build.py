@@ -39,11 +39,32 @@ def _inputs():
             [os.path.join(ROOT, "include", "tlc.h"), os.path.abspath(__file__)])
 
 
+def source_id(defines=()) -> str:
+    """sha256 (16 hex digits) of every source, header and flag that goes into libtlc.so;
+    compiled in as TLC_BUILD_ID and returned by tlc_build_id()."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in _inputs():
+        h.update(os.path.basename(p).encode() + b"\0" + open(p, "rb").read() + b"\0")
+    h.update(" ".join(ARCH + FLAGS + [f"-D{d}" for d in defines]).encode())
+    return h.hexdigest()[:16]
+
+
+def _lib_id(path):
+    """The TLC_BUILD_ID embedded in a built library (read from the file, not dlopen'ed, so a
+    process that builds and then imports the package loads the fresh library)."""
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        return None
+    k = data.find(b"TLC_BUILD_ID:")
+    return data[k + 13: k + 29].decode(errors="replace") if k >= 0 else None
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in _inputs() if os.path.exists(p))
+    """Rebuild unless the library carries the id of the current sources."""
+    return _lib_id(LIB) != source_id()
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
@@ -53,9 +74,11 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     objs = []
     bdir = os.path.join(HERE, "build", os.path.basename(out).replace(".so", ""))
     os.makedirs(bdir, exist_ok=True)
+    bid = source_id(defines)
     for s in SOURCES:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], f"-DTLC_BUILD_ID=\"{bid}\"",
+               "-I", os.path.join(ROOT, "include"),
                "-I", os.path.join(_nccl_dir(), "include"), "-c", os.path.join(CSRC, s), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

@@ -301,26 +301,6 @@ struct BulkSmem {
     unsigned long long bar[kBulkStages];
 };
 
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "TLC_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra TLC_WAIT_%=;\n\t}" ::"r"(smem_addr(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, unsigned long long *b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
-}
-
 // kAligned: P % 4 == 0, every partition segment starts 16-byte aligned.  Otherwise the
 // copy engine fetched the aligned superset starting sh_i = (i P) mod 4 elements early:
 // shared reads are scalar at offset sh_i and err goes back with 32-bit stores.
@@ -627,7 +607,7 @@ constexpr uint32_t kRowNotKept = 1u << 31;
 // offset relative to the end of literal 0's bytes (bits 16-31); literal 0's
 // position is in the row's metadata, its bytes depend on the row's carry.
 constexpr uint32_t kK3Stage = (uint32_t)(kLargeItems.c3 / kK3Workers);   // phase-3 stage per warp
-static_assert(kK3Stage >= kK3WarpRow + 1 + 15, "a row's output (<= row + 1 bytes) fits the stage");
+static_assert(kK3Stage >= pad_stage_bytes(kK3WarpRow + 1 + 3), "a row's output (<= row + 1 bytes) fits the stage");
 struct K3Smem {
     uint8_t chunk[kLargeItems.c3];                       // the chunk's quartic bytes; phase-3 stages
     uint32_t lit[2][kScanWarps][kK3LitCap];               // literal lists, row after row
@@ -967,14 +947,13 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                         if (lane >= d) x += y;
                     }
-                    uint8_t *stage = sm.chunk + (size_t)wk * kK3Stage;
-                    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 15u);
-                    for (uint32_t q = lane; q < (sh + wr.row_count + 15u) / 16u; q += 32)
-                        reinterpret_cast<uint4 *>(stage)[q] = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    const PadStage stage{sm.chunk + (size_t)wk * kK3Stage};
+                    const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 3u);
+                    pad_stage_fill(stage, sh + wr.row_count);
                     __syncwarp();
-                    lane_emit(w, mask, wr.carry_in, stage + sh, x - wr.count);
+                    lane_emit(w, mask, wr.carry_in, stage, sh + x - wr.count);
                     __syncwarp();
-                    warp_copy_congruent(out, stage + sh, wr.row_count);
+                    warp_copy_padded(out, stage, sh, wr.row_count);
                     __syncwarp();                         // the stage is reused by the next row
                     off += wr.row_count;
                     carry = wr.carry_out;

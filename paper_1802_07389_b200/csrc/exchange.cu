@@ -150,7 +150,9 @@ struct tlc_exchange {
     unsigned int *d_status = nullptr;
     // segment tables: push compress (all contexts), aggregation (owned contexts A and
     // the W x |A| received payloads X), pull compress (owned), apply (all contexts)
-    Table push_tab, pullc_tab, apply_tab, a_tab, x_tab;
+    // push / apply tables cached for the two most recent pointer sets (a caller that
+    // double-buffers its gradients or outputs alternates between two without re-uploads)
+    Table push_tab[2], pullc_tab, apply_tab[2], a_tab, x_tab;
     // peer-memory mode (tlc_exchange_ipc_*): the owner's kernels read the pushed
     // payloads and every rank reads the pulled payloads straight from the producing
     // rank's buffers over NVLink; two flag barriers per step order the phases
@@ -160,8 +162,10 @@ struct tlc_exchange {
     std::vector<void *> opened;                      // peer mappings to close
     std::vector<std::array<void *, 5>> peer;         // per rank: push_send, push_hdr, pull_buf, pull_hdr, flags
     unsigned long long *d_epoch = nullptr;           // barrier epochs issued (device counter)
-    std::vector<const float *> last_grads;
-    std::vector<float *> last_outs;
+    std::vector<const float *> push_key[2];
+    std::vector<float *> apply_key[2];
+    int push_mru = 0, apply_mru = 0;
+    float *own_push_err = nullptr, *own_pull_err = nullptr;   // library-allocated (freed at destroy)
     // every header whose status the exchange reports: the pushes this rank aggregates
     // (from every rank) and the pulls it applies (from every owner)
     const tlc_header **d_status_list = nullptr;
@@ -224,7 +228,8 @@ static int set_peers(tlc_exchange *x, const std::vector<std::array<void *, 5>> &
     }
     if (rc == TLC_OK) {
         x->p2p = 1;
-        x->last_outs.clear();   // the apply table is rebuilt with peer pointers
+        x->apply_key[0].clear();   // the apply tables are rebuilt with peer pointers
+        x->apply_key[1].clear();
         rc = upload_status_list(x);
     }
     return rc;
@@ -286,14 +291,16 @@ int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap,
 int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
     for (void *p : x->opened) cudaIpcCloseMemHandle(p);
-    void *dev[] = {x->push_err, x->owned_buf, x->pull_err, x->push_send, x->push_recv, x->pull_buf,
+    void *dev[] = {x->own_push_err, x->owned_buf, x->own_pull_err, x->push_send, x->push_recv, x->pull_buf,
                    x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags,
                    x->d_epoch, (void *)x->d_status_list};
     for (void *p : dev)
         if (p) cudaFree(p);
-    x->push_tab.release();
+    x->push_tab[0].release();
+    x->push_tab[1].release();
     x->pullc_tab.release();
-    x->apply_tab.release();
+    x->apply_tab[0].release();
+    x->apply_tab[1].release();
     x->a_tab.release();
     x->x_tab.release();
     delete x;
@@ -348,9 +355,11 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     auto alloc = [&](void **p, size_t bytes) {
         if (rc == TLC_OK && cudaMalloc(p, std::max<size_t>(bytes, 256)) != cudaSuccess) rc = TLC_ERR_CUDA;
     };
-    alloc((void **)&x->push_err, x->total_elems * sizeof(float));
+    alloc((void **)&x->own_push_err, x->total_elems * sizeof(float));
     alloc((void **)&x->owned_buf, x->owned_elems * sizeof(float));
-    alloc((void **)&x->pull_err, x->owned_elems * sizeof(float));
+    alloc((void **)&x->own_pull_err, x->owned_elems * sizeof(float));
+    x->push_err = x->own_push_err;
+    x->pull_err = x->own_pull_err;
     alloc((void **)&x->push_send, x->total_region);
     alloc((void **)&x->push_recv, (size_t)x->W * own_region);
     alloc((void **)&x->pull_buf, x->total_region);
@@ -414,6 +423,36 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
         return rc;
     }
     *out = x;
+    return TLC_OK;
+}
+
+int tlc_exchange_bind_error_buffers(tlc_exchange *x, float *push_err, float *pull_err) {
+    // caller-owned error buffers (training state to checkpoint): push_err holds
+    // tlc_exchange_push_error's layout (every context, fp32), pull_err this rank's owned
+    // contexts; NULL keeps the current buffer.  Synchronizes the device.
+    if (!x || (!push_err && !pull_err)) return TLC_ERR_ARG;
+    if (cudaDeviceSynchronize() != cudaSuccess) return TLC_ERR_CUDA;
+    if (push_err) {
+        x->push_err = push_err;
+        x->push_key[0].clear();                       // push tables are rebuilt on the next push
+        x->push_key[1].clear();
+    }
+    if (pull_err && x->owned_elems) {
+        x->pull_err = pull_err;
+        const int nown = (int)x->owned[x->me].size();
+        std::vector<tlc_tensor_desc> pullc(nown);
+        for (int q = 0; q < nown; q++) {
+            const Ctx &c = x->ctx[x->owned[x->me][q]];
+            tlc_tensor_desc &d = pullc[q];
+            d = tlc_tensor_desc{};
+            d.t = x->owned_buf + c.owned_off;
+            d.err = x->pull_err + c.owned_off;
+            d.payload = x->pull_buf + x->region_start[x->me] + c.region_off;
+            d.hdr = x->pull_hdr + x->hdr_start[x->me] + c.slot;
+            d.n = c.n;
+        }
+        return x->pullc_tab.update(pullc.data());
+    }
     return TLC_OK;
 }
 
@@ -551,9 +590,11 @@ static int check_ptrs(const tlc_exchange *x, const void *const *p) {
 // (1) compress every context with this rank's push error buffer into the send layout
 static int phase_push_compress(tlc_exchange *x, const float *const *grads, float s, int use_zre, cudaStream_t st) {
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
-    bool same = x->last_grads.size() == (size_t)T;
-    for (int i = 0; same && i < T; i++) same = x->last_grads[i] == grads[i];
-    if (!same) {
+    int slot = -1;
+    for (int k = 0; k < 2 && slot < 0; k++)
+        if (x->push_key[k].size() == (size_t)T && std::equal(grads, grads + T, x->push_key[k].begin())) slot = k;
+    if (slot < 0) {
+        slot = x->push_key[x->push_mru].empty() ? x->push_mru : 1 - x->push_mru;   // the least recently used
         std::vector<tlc_tensor_desc> d(C);
         for (int k = 0; k < C; k++) {
             const Ctx &c = x->ctx[k];
@@ -565,11 +606,13 @@ static int phase_push_compress(tlc_exchange *x, const float *const *grads, float
             d[k].n = c.n;
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;   // table may be in use
-        const int rc = x->push_tab.d ? x->push_tab.update(d.data()) : x->push_tab.create(d.data(), C, true, nullptr);
+        Table &tb = x->push_tab[slot];
+        const int rc = tb.d ? tb.update(d.data()) : tb.create(d.data(), C, true, nullptr);
         if (rc != TLC_OK) return rc;
-        x->last_grads.assign(grads, grads + T);
+        x->push_key[slot].assign(grads, grads + T);
     }
-    return launch_compress_table(x->push_tab.T, s, use_zre ? 1 : 0, x->push_tab.ws, st);
+    x->push_mru = slot;
+    return launch_compress_table(x->push_tab[slot].T, s, use_zre ? 1 : 0, x->push_tab[slot].ws, st);
 }
 
 // (2) owner: fused decompress-aggregate of the W pushes of every owned context,
@@ -588,9 +631,11 @@ static int phase_pull_compress(tlc_exchange *x, float s, int use_zre, cudaStream
 // (4) every rank applies every context to its full-size output (ACCUMULATE, R16)
 static int phase_apply(tlc_exchange *x, float *const *outs, cudaStream_t st) {
     const int T = (int)x->tensor_sizes.size(), C = (int)x->ctx.size();
-    bool same = x->last_outs.size() == (size_t)T;
-    for (int i = 0; same && i < T; i++) same = x->last_outs[i] == outs[i];
-    if (!same) {
+    int slot = -1;
+    for (int k = 0; k < 2 && slot < 0; k++)
+        if (x->apply_key[k].size() == (size_t)T && std::equal(outs, outs + T, x->apply_key[k].begin())) slot = k;
+    if (slot < 0) {
+        slot = x->apply_key[x->apply_mru].empty() ? x->apply_mru : 1 - x->apply_mru;
         std::vector<tlc_tensor_desc> d(C);
         for (int k = 0; k < C; k++) {
             const Ctx &c = x->ctx[k];
@@ -603,11 +648,13 @@ static int phase_apply(tlc_exchange *x, float *const *outs, cudaStream_t st) {
             d[k].n = c.n;
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;
-        const int rc = x->apply_tab.d ? x->apply_tab.update(d.data()) : x->apply_tab.create(d.data(), C, false, nullptr);
+        Table &tb = x->apply_tab[slot];
+        const int rc = tb.d ? tb.update(d.data()) : tb.create(d.data(), C, false, nullptr);
         if (rc != TLC_OK) return rc;
-        x->last_outs.assign(outs, outs + T);
+        x->apply_key[slot].assign(outs, outs + T);
     }
-    return launch_decompress_table(x->apply_tab.T, TLC_MODE_ACCUMULATE, x->apply_tab.ws, st);
+    x->apply_mru = slot;
+    return launch_decompress_table(x->apply_tab[slot].T, TLC_MODE_ACCUMULATE, x->apply_tab[slot].ws, st);
 }
 
 extern "C" {
@@ -796,6 +843,57 @@ int tlc_loopback_pull(tlc_loopback *g, float *const *outs, float s, int use_zre,
     for (int r = 0; r < g->W && rc == TLC_OK; r++) rc = phase_apply(g->xs[r], outs + r * T, st);
     if (rc == TLC_OK) g->phase = 0;
     return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ standalone aggregation
+// The server's "average the gradients" (reading R15; R24 for failed sources) over
+// W compressed copies of a tensor list, outside any exchange: the owner-side fused
+// decompress-aggregate (K4 + K5m) of the parameter server, for callers that move the
+// payloads themselves (the desk-scale simulator's single server, psim.py).
+struct tlc_aggregate {
+    int W = 0;
+    Table a_tab, x_tab;
+};
+
+extern "C" {
+
+int tlc_aggregate_destroy(tlc_aggregate *g) {
+    if (!g) return TLC_ERR_ARG;
+    g->a_tab.release();
+    g->x_tab.release();
+    delete g;
+    return TLC_OK;
+}
+
+int tlc_aggregate_create(tlc_aggregate **out, int world, int count, const tlc_tensor_desc *outs,
+                         const tlc_tensor_desc *srcs) {
+    if (!out || world < 1 || world > 8 || count < 1 || !outs || !srcs) return TLC_ERR_ARG;
+    for (int i = 0; i < count; i++) {
+        if (!outs[i].out || outs[i].n == 0) return TLC_ERR_ARG;
+        for (int w = 0; w < world; w++) {
+            const tlc_tensor_desc &d = srcs[(size_t)w * count + i];
+            if (!d.payload || !d.hdr || d.n != outs[i].n) return TLC_ERR_ARG;
+        }
+    }
+    auto *g = new tlc_aggregate{};
+    g->W = world;
+    std::vector<tlc_tensor_desc> a(outs, outs + count);
+    for (int i = 0; i < count; i++) a[i].hdr = srcs[i].hdr;      // only n / out are used through A
+    int rc = g->a_tab.create(a.data(), count, false, nullptr);
+    if (rc == TLC_OK) rc = g->x_tab.create(srcs, world * count, false, nullptr);
+    if (rc != TLC_OK) {
+        tlc_aggregate_destroy(g);
+        return rc;
+    }
+    *out = g;
+    return TLC_OK;
+}
+
+int tlc_aggregate_run(tlc_aggregate *g, void *stream) {
+    if (!g) return TLC_ERR_ARG;
+    return launch_aggregate(g->a_tab.T, g->x_tab.T, g->W, g->x_tab.ws, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

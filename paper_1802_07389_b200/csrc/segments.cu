@@ -92,6 +92,10 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
             return TLC_ERR_CUDA;
         for (int k = 0; k < 5; k++) T.first[k] = d_first + (size_t)k * cnt;
     }
+    if (with_scratch && cnt > 1 && T.max_n <= kSmallMaxN) {
+        const int rc = small_plan_build(T, host, &d_small, sl_layout);
+        if (rc != TLC_OK) return rc;
+    }
     if (shared_ws) {
         ws = shared_ws;
     } else {
@@ -131,6 +135,10 @@ int Table::upload() {
     T.rest_list = d_bulk ? d_bulk + T.n_bulk : nullptr;
     T.n_rest = d_bulk ? rest.size() : 0;
     T.bulk_nozre_ok = nozre_ok ? 1 : 0;
+    if (T.sl) {
+        const int rc = small_plan_refresh(T, host, sl_layout);   // the slices carry the pointers
+        if (rc != TLC_OK) return rc;
+    }
     return cudaMemcpy(d, host.data(), host.size() * sizeof(Seg), cudaMemcpyHostToDevice) == cudaSuccess
                ? TLC_OK : TLC_ERR_CUDA;
 }
@@ -153,6 +161,8 @@ void Table::release() {
     if (d_bulk) cudaFree(d_bulk);
     d_bulk = nullptr;
     if (own_ws && ws) cudaFree(ws);
+    if (d_small) cudaFree(d_small);
+    d_small = nullptr;
     d = nullptr;
     ws = nullptr;
 }

@@ -21,6 +21,7 @@
 // Same results, byte for byte, as the large path (the payload, err, header and output
 // are defined by the method, not by the kernels).
 #include <cstdlib>
+#include <vector>
 
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
@@ -205,6 +206,344 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
     }
 }
 
+// ============================================================== K6c
+// The small-table compressor as ONE cooperative launch over all SMs (tables of many
+// small tensors: the 110 ResNet-110 layers).  K6 gave each tensor one CTA, so the 35
+// tensors of 36,864 values each streamed ~440 KB through a single SM (22 us, DRAM 9 %).
+// Here every tensor is cut into slices of kSlice quartic positions (5 * kSlice values),
+// the slices are dealt to the CTAs in contiguous runs of about equal size, and the method
+// runs in three phases separated by two grid barriers:
+//   A  t and err of the CTA's slices -> shared memory with cp.async (every load in
+//      flight at once), u = err + t (step 1), the max key of each slice, atomicMax into
+//      its tensor's key (Eq. 1 needs the whole tensor's max);
+//   B  M per tensor (Eq. 1, R6), quantize from shared memory writing err (Eq. 2, steps
+//      a, b), quartic bytes into shared memory (step 3), the run summary of every slice
+//      (one warp per slice) published for its tensor's later slices;
+//   C  each slice composes the summaries of its tensor's earlier slices (<= 15) into
+//      its output offset and carry and emits its zero-run bytes (step 4) through a
+//      255-prefilled stage; the tensor's last slice writes the length.
+// Results are identical to K6 / K1-K5 (the payload, err and header are defined by the
+// method).  A tensor's key is reset to 0 after barrier 2 for the next launch.
+constexpr uint32_t kSlice = 512;                        // quartic positions per slice
+constexpr int kSlots = kSmWarps;                        // <= 16 slices per CTA (one warp each)
+constexpr uint32_t kStage = 544;                        // per-warp padded stage: <= kSlice + 1 bytes + 3
+static_assert(kStage >= pad_stage_bytes(kSlice + 1 + 3), "a slice's output fits the stage");
+
+// All CTAs of the (cooperative) launch: arrive, then wait until every CTA has arrived.
+// The counter only grows; each barrier waits for the next multiple of the grid size.
+__device__ __forceinline__ void grid_barrier(unsigned long long *ctr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long G = gridDim.x;
+        const unsigned long long old = atomicAdd(ctr, 1ull);
+        const unsigned long long target = (old / G + 1) * G;
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// Phase A's copy of one partition row of a slice: elements [i*P + j0, +m) of t (or err),
+// fetched as the 16-byte-aligned superset of its bytes (a bulk copy needs 16-byte
+// addresses and sizes; the granules around a valid byte lie in the same mapped page).
+struct RowCopy {
+    uint32_t dst, bytes, shift;      // smem byte offset, superset bytes, elements before the row
+};
+__device__ __forceinline__ RowCopy row_copy(const float *base, uint32_t e0, uint32_t m, uint32_t dst) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base + e0), a0 = a & ~uintptr_t(15);
+    const uintptr_t a1 = (a + 4ull * m + 15) & ~uintptr_t(15);
+    return RowCopy{dst, (uint32_t)(a1 - a0), (uint32_t)((a - a0) >> 2)};
+}
+// bytes one slice row can take in the stage: 4 * kSlice + two partial granules
+constexpr uint32_t kRowBytes = 4 * kSlice + 32;
+
+#ifdef TLC_K6C_TRACE
+// development instrumentation: %globaltimer at the phase boundaries of every CTA
+__device__ unsigned long long g_k6c_trace[1024][8];
+#define K6C_TRACE(slot)                                                                     \
+    do {                                                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                        \
+            unsigned long long t_;                                                          \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+            g_k6c_trace[blockIdx.x][slot] = t_;                                             \
+        }                                                                                   \
+    } while (0)
+#else
+#define K6C_TRACE(slot) do {} while (0)
+#endif
+
+__global__ void __launch_bounds__(kSmThreads, 1)
+tlc_small_coop_compress_kernel(const SegTable T, float s, int use_zre) {
+    extern __shared__ __align__(16) uint8_t sm_raw[];        // bulk-copy destinations: 16-byte aligned
+    __shared__ SliceRec s_sl[kSlots];
+    __shared__ uint32_t s_row[kSlots][5][2];               // t / err row: smem offset (bytes) | shift << 24
+    __shared__ unsigned int s_key[kSlots];
+    __shared__ float s_M[kSlots];
+    __shared__ unsigned int s_st[kSlots];
+    __shared__ __align__(8) unsigned long long s_bar;
+    K6C_TRACE(0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t c0 = T.sl_cta[blockIdx.x], ns = T.sl_cta[blockIdx.x + 1] - c0;
+    // the CTA's slice records (pointers included) in one round trip
+    if (threadIdx.x < ns * (sizeof(SliceRec) / 16))
+        reinterpret_cast<uint4 *>(s_sl)[threadIdx.x] = reinterpret_cast<const uint4 *>(T.sl + c0)[threadIdx.x];
+    if (threadIdx.x < kSlots) s_key[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint8_t *stage = sm_raw + (size_t)ns * 10 * kRowBytes + (size_t)warp * kStage;
+    uint8_t *Bs = sm_raw + (size_t)ns * 10 * kRowBytes + kSmWarps * kStage;   // kSlots x kSlice quartic bytes
+
+    // ---- A: every row of t and err of every slice with one bulk copy each (the copy
+    // engine keeps them all in flight); u = err + t; per-slice max keys
+    if (threadIdx.x == 0) {
+        uint32_t total = 0;
+        for (uint32_t r = 0; r < ns * 10; r++) {
+            const SliceRec &sl = s_sl[r / 10];
+            const uint32_t i = (r % 10) >> 1, e0 = i * sl.P + sl.j0;
+            const uint32_t m = e0 < sl.n ? min(sl.len, sl.n - e0) : 0u;
+            const RowCopy rc = m ? row_copy((r & 1) ? sl.err : sl.t, e0, m, r * kRowBytes) : RowCopy{r * kRowBytes, 0u, 0u};
+            s_row[r / 10][i][r & 1] = rc.dst | (rc.shift << 24);
+            total += rc.bytes;
+        }
+        mbar_expect_tx(&s_bar, total);
+    }
+    __syncthreads();
+    if (threadIdx.x < ns * 10) {
+        const uint32_t r = threadIdx.x;
+        const SliceRec &sl = s_sl[r / 10];
+        const uint32_t i = (r % 10) >> 1, e0 = i * sl.P + sl.j0;
+        const uint32_t m = e0 < sl.n ? min(sl.len, sl.n - e0) : 0u;
+        if (m) {
+            const float *src = (r & 1) ? sl.err : sl.t;
+            const RowCopy rc = row_copy(src, e0, m, r * kRowBytes);
+            bulk_load(sm_raw + rc.dst, reinterpret_cast<const void *>(reinterpret_cast<uintptr_t>(src + e0) & ~uintptr_t(15)),
+                      rc.bytes, &s_bar);
+        }
+    }
+    mbar_wait(&s_bar, 0);
+    K6C_TRACE(1);
+    const uint32_t jj = threadIdx.x;                        // thread j: quartic position j0 + j of each slice
+    static_assert(kSlice == kSmThreads, "one quartic position per thread and slice");
+    for (uint32_t k = 0; k < ns; k++) {
+        const SliceRec &sl = s_sl[k];
+        unsigned int m = 0;
+        if (jj < sl.len) {
+#pragma unroll
+            for (uint32_t i = 0; i < 5; i++) {
+                const uint32_t e = i * sl.P + sl.j0 + jj;
+                float *tu = reinterpret_cast<float *>(sm_raw + (s_row[k][i][0] & 0xffffffu)) + (s_row[k][i][0] >> 24) + jj;
+                float x = 0.0f;                                   // pad positions: digit 0 below
+                if (e < sl.n) {
+                    const float ev = reinterpret_cast<const float *>(sm_raw + (s_row[k][i][1] & 0xffffffu))[(s_row[k][i][1] >> 24) + jj];
+                    x = __fadd_rn(ev, *tu);                       // step (1)
+                    m = max(m, __float_as_uint(x) & 0x7fffffffu);
+                }
+                *tu = x;                                          // u replaces t in place
+            }
+        }
+        m = __reduce_max_sync(0xffffffffu, m);
+        if (lane == 0 && m) atomicMax(&s_key[k], m);
+    }
+    __syncthreads();
+    if (threadIdx.x < ns && s_key[threadIdx.x]) atomicMax(T.sl_key + s_sl[threadIdx.x].seg, s_key[threadIdx.x]);
+    K6C_TRACE(2);
+    grid_barrier(T.sl_bar);
+    K6C_TRACE(3);
+
+    // ---- B: M (Eq. 1), quantization + residual (Eq. 2, steps a, b), quartic bytes (step 3)
+    if (threadIdx.x < ns) {
+        float M;
+        s_st[threadIdx.x] = scale_from_key(__ldcg(T.sl_key + s_sl[threadIdx.x].seg), s, M);
+        s_M[threadIdx.x] = M;
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < ns; k++) {
+        const SliceRec &sl = s_sl[k];
+        const unsigned int st = s_st[k];
+        if (sl.k == 0 && threadIdx.x == 0) {                      // the tensor's first slice: header
+            tlc_header *h = sl.hdr;
+            h->M = s_M[k];
+            h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+            h->n = sl.n;
+            h->status = st;
+            h->reserved = 0;
+            if (!use_zre || st != TLC_OK) h->payload_len = (st == TLC_OK) ? sl.P : 0;
+        }
+        if (st != TLC_OK) continue;                               // err untouched (R6)
+        const Quant Q(s_M[k]);
+        if (jj < sl.len) {
+            uint32_t b = 0;
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const uint32_t e = (uint32_t)i * sl.P + sl.j0 + jj;
+                uint32_t d = 0;                                   // pad digit (R10)
+                if (e < sl.n) {
+                    const float x = reinterpret_cast<const float *>(sm_raw + (s_row[k][i][0] & 0xffffffu))[(s_row[k][i][0] >> 24) + jj];
+                    const int q = Q.q(x);                         // Eq. 2
+                    __stcs(sl.err + e, Q.residual(x, q));         // steps (a), (b)
+                    d = (uint32_t)(q + 1);
+                }
+                b = b * 3u + d;                                   // steps 1, 4, 6
+            }
+            Bs[k * kSlice + jj] = (uint8_t)b;
+            if (!use_zre) sl.payload[sl.j0 + jj] = (uint8_t)b;
+        }
+    }
+    __syncthreads();
+    // run summary of slice `warp` (one warp row of <= kSlice bytes), kept in registers for C
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mask = 0;
+    int len_l = 0;
+    RunSum lane_sum = run_identity();
+    const bool mine = use_zre && (uint32_t)warp < ns && s_st[warp] == TLC_OK;
+    uint32_t row_len = 0;
+    if (mine) {
+        row_len = s_sl[warp].len;
+        const uint32_t rel = 32u * lane;
+        len_l = rel < row_len ? (int)min(32u, row_len - rel) : 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int mm = 4 * k + q;
+                x |= (uint32_t)(mm < len_l ? Bs[warp * kSlice + rel + mm] : kZeroGroup) << (8 * q);
+            }
+            w[k] = x;
+        }
+        mask = literal_mask(w);
+        lane_sum = mask_summary(mask, len_l);
+        const RunSum rs = warp_row_summary(mask, len_l, lane_sum, row_len);
+        if (lane == 0) st_relaxed_u64(T.sl_sum + c0 + warp, pack(rs));
+    }
+    K6C_TRACE(4);
+    grid_barrier(T.sl_bar);
+    K6C_TRACE(5);
+
+    // ---- C: offsets from the tensor's earlier slices, zero-run emission (step 4)
+    if (mine) {
+        const SliceRec &sl = s_sl[warp];
+        const uint32_t kk = sl.k;
+        const unsigned long long pv = lane < (int)kk ? ld_relaxed_u64(T.sl_sum + sl.first + lane) : 0ull;
+        RunSum acc = lane < (int)kk ? unpack(pv) : run_identity();
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {                      // in-order tree: lane 0 = slices 0..kk-1
+            const RunSum o = unpack(__shfl_down_sync(0xffffffffu, pack(acc), d));
+            if (lane + d < 32) acc = compose(acc, o);
+        }
+        acc = unpack(__shfl_sync(0xffffffffu, pack(acc), 0));
+        uint64_t o0;
+        uint32_t c_in;
+        run_eval(acc, 0, o0, c_in);
+        const WarpRow wr = warp_row(mask, len_l, lane_sum, c_in, row_len);
+        uint32_t x = wr.count;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        uint8_t *out = sl.payload + o0;
+        const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 3u);
+        const PadStage pst{stage};
+        pad_stage_fill(pst, sh + wr.row_count);
+        __syncwarp();
+        lane_emit(w, mask, wr.carry_in, pst, sh + x - wr.count);
+        __syncwarp();
+        warp_copy_padded(out, pst, sh, wr.row_count);
+        if (sl.last && lane == 0) {                              // the tensor's last slice
+            if (wr.carry_out > 0) out[wr.row_count] = run_code(wr.carry_out);
+            sl.hdr->payload_len = o0 + wr.row_count + (wr.carry_out > 0);
+        }
+    }
+    // every read of the keys happened before barrier 2: reset them for the next launch
+    if (threadIdx.x < ns && s_sl[threadIdx.x].k == 0) T.sl_key[s_sl[threadIdx.x].seg] = 0;
+    __syncthreads();
+    K6C_TRACE(6);
+}
+
+int small_plan_build(SegTable &T, const std::vector<Seg> &host, void **d_small, std::vector<uint4> &layout) {
+    // slices in segment order, then contiguous runs of about total/G values per CTA
+    layout.clear();
+    std::vector<uint32_t> w;                                      // values per slice
+    std::vector<uint32_t> first;
+    for (int si = 0; si < (int)host.size(); si++) {
+        const Seg &S = host[si];
+        const uint32_t P = (uint32_t)S.P, nsl = (P + kSlice - 1) / kSlice;
+        for (uint32_t k = 0; k < nsl; k++) {
+            const uint32_t j0 = k * kSlice, len = min(kSlice, P - j0);
+            layout.push_back(make_uint4((uint32_t)si, j0, len, k | ((k + 1 == nsl ? 1u : 0u) << 16)));
+            w.push_back(5 * len);
+        }
+    }
+    const int G = (int)tmin<uint64_t>((uint64_t)num_sms(), layout.size());
+    uint64_t total = 0;
+    for (uint32_t x : w) total += x;
+    std::vector<uint32_t> cta(G + 1, 0);
+    uint64_t acc = 0;
+    int g = 0;
+    for (size_t k = 0; k < layout.size(); k++) {
+        // open the next CTA's run once this one has reached its share (and slices remain)
+        while (g + 1 < G && acc >= (total * (uint64_t)(g + 1)) / G && cta[g + 1] == 0 && k > cta[g]) cta[++g] = (uint32_t)k;
+        acc += w[k];
+    }
+    for (int q = g + 1; q <= G; q++) cta[q] = (uint32_t)layout.size();
+    uint32_t max_ns = 0;
+    for (int q = 0; q < G; q++) max_ns = max(max_ns, cta[q + 1] - cta[q]);
+    if (max_ns > (uint32_t)kSlots) { layout.clear(); return TLC_OK; }   // too many slices per CTA: K6
+    const size_t smem = (size_t)max_ns * 10 * kRowBytes + kSmWarps * kStage + kSlots * kSlice;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem + 4096 > (size_t)optin) { layout.clear(); return TLC_OK; }   // does not fit: K6
+    const size_t b_sl = align256(layout.size() * sizeof(SliceRec)), b_cta = align256((G + 1) * sizeof(uint32_t));
+    const size_t b_key = align256(host.size() * sizeof(unsigned int));
+    const size_t b_sum = align256(layout.size() * sizeof(unsigned long long)), b_bar = 256;
+    char *d = nullptr;
+    if (cudaMalloc((void **)&d, b_sl + b_cta + b_key + b_sum + b_bar) != cudaSuccess) return TLC_ERR_CUDA;
+    *d_small = d;
+    if (cudaMemcpy(d + b_sl, cta.data(), cta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemset(d + b_sl + b_cta, 0, b_key + b_sum + b_bar) != cudaSuccess)
+        return TLC_ERR_CUDA;
+    T.sl = reinterpret_cast<const SliceRec *>(d);
+    T.sl_cta = reinterpret_cast<const uint32_t *>(d + b_sl);
+    T.sl_key = reinterpret_cast<unsigned int *>(d + b_sl + b_cta);
+    T.sl_sum = reinterpret_cast<unsigned long long *>(d + b_sl + b_cta + b_key);
+    T.sl_bar = reinterpret_cast<unsigned long long *>(d + b_sl + b_cta + b_key + b_sum);
+    T.sl_grid = G;
+    T.sl_smem = (uint32_t)smem;
+    return TLC_OK;
+}
+
+int small_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout) {
+    std::vector<SliceRec> rec(layout.size());
+    uint32_t first = 0;
+    for (size_t q = 0; q < layout.size(); q++) {
+        const uint4 &L = layout[q];
+        const Seg &S = host[L.x];
+        if ((L.w & 0xffffu) == 0) first = (uint32_t)q;
+        rec[q] = SliceRec{S.t, S.err, S.payload, S.hdr, (uint32_t)S.n, (uint32_t)S.P, L.y, L.z,
+                          first, L.w & 0xffffu, L.w >> 16, L.x};
+    }
+    return cudaMemcpy(const_cast<SliceRec *>(T.sl), rec.data(), rec.size() * sizeof(SliceRec),
+                      cudaMemcpyHostToDevice) == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+// K6c is opt-in (TLC_COOP=1): on the ResNet-110 table it measured 31 us against K6's 22 us
+// (tools/k6c_trace.py: every phase takes 3-5 us)
+static bool coop_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_COOP");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 // A tensor's decode is split into parts of kSmPart quartic positions, one CTA each (the
 // 36,864-value ResNet-110 tensors would otherwise keep one SM busy while most idle): every
 // part scans the whole payload (<= P bytes, on chip) and expands / decodes only its range.
@@ -214,12 +553,12 @@ template <int kMode>
 __global__ void __launch_bounds__(kSmThreads)
 tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
     extern __shared__ __align__(16) uint8_t sm_raw[];
-    __shared__ uint32_t V[5][256];
-    __shared__ uint16_t lut[256];
+    __shared__ uint16_t dig[256];                                // digit_i(b) at bits 2i
     __shared__ uint32_t s_wsum[kSmWarps + 1];
     __shared__ int s_bad;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t items = (uint64_t)T.count * parts;
+    bool table = false;
     for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
         const int si = (int)(item / parts);
         const uint32_t part = (uint32_t)(item % parts);
@@ -227,40 +566,53 @@ tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
         tlc_header *hdr = S.hdr;
         const uint32_t jr0 = part * kSmPart;
         if (jr0 >= S.P) continue;                                // no positions in this part
-        if (!header_valid(hdr, S.n)) {                           // uniform over the CTA
+        const bool hv = header_valid(hdr, S.n);
+        if (!table) {
+            // Decoding step 1 for the 243 byte values, once per CTA (no dependence on M), built
+            // while the segment and header loads above are in flight: Eq. 3 is then
+            // M * (d - 1) in {-M, +0, M}, taken by selection (the same bits as the product)
+            for (int v = threadIdx.x; v < 256; v += kSmThreads) {
+                uint32_t r = v < 243 ? v : 121, pk = 0;
+#pragma unroll
+                for (int i = 4; i >= 0; i--) {
+                    pk |= (r % 3u) << (2 * i);
+                    r /= 3u;
+                }
+                dig[v] = (uint16_t)pk;
+            }
+            __syncthreads();
+            table = true;
+        }
+        if (!hv) {                                               // uniform over the CTA
             if (threadIdx.x == 0 && part == 0 && hdr->status == TLC_OK) raise_format(hdr);
             continue;
         }
         const uint32_t n = (uint32_t)S.n, P = (uint32_t)S.P, Z = (uint32_t)hdr->payload_len;
         const uint32_t jr1 = min(P, jr0 + kSmPart), pl = jr1 - jr0;
         const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
-        const float M = hdr->M;
+        const float M = hdr->M, negM = -M;
         uint8_t *E = sm_raw;                                     // quartic bytes [jr0, jr1)
-        uint8_t *Y = sm_raw + kSmPart;                           // the payload (ZRE)
         if (threadIdx.x == 0) s_bad = 0;
-        // value table: Eq. 3 per partition, V[i][b] = M * (digit_i(b) - 1)
-        for (int v = threadIdx.x; v < 256; v += kSmThreads) {
-            uint32_t wd = 0, r = v < 243 ? v : 121;
-#pragma unroll
-            for (int i = 4; i >= 0; i--) {
-                const uint32_t d = r % 3u;
-                r /= 3u;
-                wd |= (uint32_t)(d != 1) << i;
-                V[i][v] = __float_as_uint(__fmul_rn(M, (float)((int)d - 1)));
-            }
-            lut[v] = (uint16_t)wd;
-        }
-        __syncthreads();
         if (zre) {
-            for (uint32_t q = threadIdx.x; q < Z; q += kSmThreads) Y[q] = S.payload[q];
-            __syncthreads();
-            // expansion lengths of bytes [16t, 16t+16), block exclusive scan
+            // this thread's 16 payload bytes straight to registers (one 16-byte load when
+            // aligned), expansion lengths by SWAR, block exclusive scan
             constexpr int kPer = 16;
             static_assert((kSmallMaxN + 4) / 5 <= kPer * kSmThreads, "every payload byte has a thread");
-            uint32_t lens = 0;
             const uint32_t b0 = kPer * threadIdx.x;
+            uint32_t wv[4] = {0, 0, 0, 0}, lens = 0;
+            if (b0 + kPer <= Z && aligned16(S.payload)) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(S.payload + b0));
+                wv[0] = v.x; wv[1] = v.y; wv[2] = v.z; wv[3] = v.w;
+                lens = word_len(wv[0]) + word_len(wv[1]) + word_len(wv[2]) + word_len(wv[3]);
+            } else {
 #pragma unroll
-            for (int k = 0; k < kPer; k++) lens += b0 + k < Z ? zre_len(Y[b0 + k]) : 0u;
+                for (int k = 0; k < kPer; k++)
+                    if (b0 + k < Z) {
+                        const uint32_t b = S.payload[b0 + k];
+                        wv[k >> 2] |= b << (8 * (k & 3));
+                        lens += zre_len(b);
+                    }
+            }
             uint32_t x = lens;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -287,12 +639,13 @@ tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
                 continue;
             }
             uint32_t p = s_wsum[warp] + x - lens;
+            if (p < jr1 && p + lens > jr0) {
 #pragma unroll
-            for (int k = 0; k < kPer; k++) {
-                if (b0 + k >= Z || p >= jr1) break;
-                const uint32_t b = Y[b0 + k];
-                if (b < kFirstRunCode && p >= jr0) E[p - jr0] = (uint8_t)b;   // literal
-                p += zre_len(b);
+                for (int k = 0; k < kPer; k++) {
+                    const uint32_t b = (wv[k >> 2] >> (8 * (k & 3))) & 0xffu;
+                    if (b0 + k < Z && b < kFirstRunCode && p >= jr0 && p < jr1) E[p - jr0] = (uint8_t)b;   // literal
+                    p += b0 + k < Z ? zre_len(b) : 0u;
+                }
             }
         } else {
             for (uint32_t q = threadIdx.x; q < pl; q += kSmThreads) {
@@ -308,30 +661,27 @@ tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
             }
         }
         __syncthreads();
-        // ---- decoding steps 1-4 and Eq. 3
+        // ---- decoding steps 1-4 and Eq. 3: out = M * (d - 1) (bits of the fp32 product)
         for (uint32_t jl = threadIdx.x; jl < pl; jl += kSmThreads) {
-            const uint32_t b = E[jl];
-            const uint32_t nz = lut[b];
+            const uint32_t pk = dig[E[jl]];
 #pragma unroll
             for (int i = 0; i < 5; i++) {
                 const uint32_t e = (uint32_t)(i * P) + jr0 + jl;
                 if (e >= n) break;
-                const float v = __uint_as_float(V[i][b]);
+                const uint32_t d = (pk >> (2 * i)) & 3u;
+                const float v = d == 2u ? M : (d == 0u ? negM : 0.0f);
                 if (kMode == TLC_MODE_OVERWRITE) __stcs(S.out + e, v);
-                else if ((nz >> i) & 1u) S.out[e] = __fadd_rn(S.out[e], v);   // q != 0 (R16)
+                else if (d != 1u) S.out[e] = __fadd_rn(S.out[e], v);   // q != 0 (R16)
             }
         }
-        __syncthreads();                                         // tables / buffers reuse
+        __syncthreads();                                         // E reuse
     }
 }
 
 static size_t small_smem_compress(uint64_t max_n) {
     return 4 * ((max_n + 3) & ~3ull) + ((max_n + 4) / 5 + 16);
 }
-static size_t small_smem_decompress(uint64_t max_n) {
-    const uint64_t P = (max_n + 4) / 5;
-    return kSmPart + ((P + 15) & ~15ull);
-}
+static size_t small_smem_decompress(uint64_t) { return kSmPart; }
 
 // TLC_NO_SMALL=1 routes small tables through K1-K5 (A/B measurements)
 bool small_enabled() {
@@ -346,6 +696,30 @@ bool small_enabled() {
 bool small_table(const SegTable &T) { return T.max_n <= kSmallMaxN && small_enabled(); }
 
 int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st) {
+    if (T.sl && coop_enabled()) {
+        static bool cattr = false;
+        if (!cattr) {
+            int dev = 0, optin = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncSetAttribute(tlc_small_coop_compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - 4096);
+            cattr = true;
+        }
+        KernelScope ks(kK6s, st);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(T.sl_grid);
+        cfg.blockDim = dim3(kSmThreads);
+        cfg.dynamicSmemBytes = T.sl_smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;   // every CTA co-resident: the grid barriers
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, tlc_small_coop_compress_kernel, T, s, use_zre);
+        return e == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+    }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tlc_small_compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -377,3 +751,10 @@ int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
 }
 
 }  // namespace tlc
+
+#ifdef TLC_K6C_TRACE
+extern "C" int tlc_debug_k6c_trace(void *host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, tlc::g_k6c_trace, bytes < sizeof(tlc::g_k6c_trace) ? bytes : sizeof(tlc::g_k6c_trace)) ==
+                   cudaSuccess ? 0 : 1;
+}
+#endif

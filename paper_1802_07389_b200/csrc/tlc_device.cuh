@@ -40,6 +40,28 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned l
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- mbarriers and bulk copies
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TLC_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra TLC_WAIT_%=;\n\t}" ::"r"(smem_addr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+
+
 // Streaming loads of data read exactly once by this kernel.
 __device__ __forceinline__ float ld_stream(const float *p) { return __ldcs(p); }
 __device__ __forceinline__ float4 ld_stream4(const float4 *p) { return __ldcs(p); }
@@ -328,26 +350,44 @@ __device__ __forceinline__ RunSum warp_row_summary(uint32_t mask, int len, const
 }
 
 // ZRE bytes of one lane's 32 quartic bytes of a warp row, given the zero groups
-// pending before them (carry_in, from warp_row): per literal (bit of `mask`), the
+// pending before them (carry_in < 14, from warp_row): per literal (bit of `mask`), the
 // code of the pending zero groups that do not fill a chunk of 14 (full chunks are
 // skipped -- their 255 bytes are the caller's prefill), then the literal itself
-// (P:545-546).  Word by word: a word of four literals with nothing pending is stored
-// as is (dense data: 0.78 -> ~0.1 K instructions per lane and row); other words go
-// byte by byte.  Writes dst[o, ...) and returns the end offset.
-__host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], uint32_t mask, uint32_t carry_in,
-                                                       uint8_t *dst, uint32_t o) {
-    uint32_t c = carry_in;                                   // zero groups pending
+// (P:545-546).  Writes dst[o, ...) and returns the end offset.
+//
+// Common case ("simple": no run of 14 or more zero groups before a literal of the lane):
+// every literal m lands at o + (literals before m) + (codes up to m), a code right
+// before literal m whose preceding run is non-empty -- one running offset, no division,
+// the same instructions in every lane (SIMT: a per-byte branchy loop made the warp run
+// both paths).  A word of four literals without codes is stored as a unit when the
+// whole warp has one there.  The codes' values (run lengths) follow in a short loop
+// over the code bits.  Other lanes take the general byte loop.
+__host__ __device__ __forceinline__ bool lane_simple(uint32_t mask, uint32_t carry_in) {
+    if (!mask) return true;
+    const uint32_t lead = ctz32(mask), hi = msb32(mask);
+    if (lead + carry_in >= kMaxRun) return false;
+    uint32_t y = hi > lead ? ((~mask) & (((2u << hi) - 1u) ^ ((2u << lead) - 1u))) : 0u;
+    y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 6;             // a run of >= 14 zero groups
+    return y == 0;
+}
+
+// vote among the lanes currently executing together (lane_emit's lanes may have split on
+// lane_simple); only ever used where p itself makes the voted path correct for the lane
+__host__ __device__ __forceinline__ bool warp_all(bool p) {
+#ifdef __CUDA_ARCH__
+    return __all_sync(__activemask(), p);
+#else
+    return p;                                // host emulation: lanes run one at a time
+#endif
+}
+
+// The general form: one byte at a time, zero groups pending in c.
+template <class Dst>
+__host__ __device__ __forceinline__ uint32_t lane_emit_bytes(const uint32_t (&w)[8], uint32_t mask, uint32_t c,
+                                                             Dst dst, uint32_t o) {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const uint32_t mk = (mask >> (4 * k)) & 0xfu;
-        if (mk == 0xfu && c == 0) {
-            dst[o] = (uint8_t)w[k];
-            dst[o + 1] = (uint8_t)(w[k] >> 8);
-            dst[o + 2] = (uint8_t)(w[k] >> 16);
-            dst[o + 3] = (uint8_t)(w[k] >> 24);
-            o += 4;
-            continue;
-        }
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             if ((mk >> q) & 1u) {
@@ -362,6 +402,120 @@ __host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], u
         }
     }
     return o;
+}
+
+// Variants (A/B by -DTLC_EMIT_V; the host harness checks all three against the oracle):
+//  1  a word of four literals with nothing pending is stored as a unit, other words go
+//     byte by byte (divergent: a warp runs both paths when its lanes differ);
+//  2  simple lanes: one running offset, predicated byte stores (a serial add chain);
+//  3  simple lanes: every byte's offset from popcounts of the masks below it (no chain).
+#ifndef TLC_EMIT_V
+#define TLC_EMIT_V 1
+#endif
+template <int V = TLC_EMIT_V, class Dst>
+__host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], uint32_t mask, uint32_t carry_in,
+                                                       Dst dst, uint32_t o) {
+    if (V == 1) {
+        uint32_t c = carry_in;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t mk = (mask >> (4 * k)) & 0xfu;
+            if (mk == 0xfu && c == 0) {
+                dst[o] = (uint8_t)w[k];
+                dst[o + 1] = (uint8_t)(w[k] >> 8);
+                dst[o + 2] = (uint8_t)(w[k] >> 16);
+                dst[o + 3] = (uint8_t)(w[k] >> 24);
+                o += 4;
+                continue;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if ((mk >> q) & 1u) {
+                    o += c / kMaxRun;
+                    const uint32_t rem = c % kMaxRun;
+                    if (rem) dst[o++] = run_code(rem);
+                    c = 0;
+                    dst[o++] = (uint8_t)(w[k] >> (8 * q));
+                } else {
+                    c++;
+                }
+            }
+        }
+        return o;
+    }
+    if (!lane_simple(mask, carry_in)) return lane_emit_bytes(w, mask, carry_in, dst, o);
+    // code flags: a literal whose previous byte is a zero group, or the lane's first
+    // byte when zero groups are pending from before the lane
+    const uint32_t cf = mask & ((~mask << 1) | (carry_in ? 1u : 0u));
+    if (V == 2) {
+        uint32_t off = o;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t nib = (mask >> (4 * k)) & 0xfu, cnib = (cf >> (4 * k)) & 0xfu;
+            if (warp_all(nib == 0xfu && cnib == 0u)) {
+                dst[off] = (uint8_t)w[k];
+                dst[off + 1] = (uint8_t)(w[k] >> 8);
+                dst[off + 2] = (uint8_t)(w[k] >> 16);
+                dst[off + 3] = (uint8_t)(w[k] >> 24);
+                off += 4;
+                continue;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                off += (cnib >> q) & 1u;
+                if ((nib >> q) & 1u) dst[off] = (uint8_t)(w[k] >> (8 * q));
+                off += (nib >> q) & 1u;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t lt = (1u << (4 * k)) - 1u;
+            const uint32_t base = o + popc32(mask & lt) + popc32(cf & lt);
+            const uint32_t nib = (mask >> (4 * k)) & 0xfu, cnib = (cf >> (4 * k)) & 0xfu;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if ((nib >> q) & 1u)
+                    dst[base + popc32(nib & ((1u << q) - 1u)) + popc32(cnib & ((2u << q) - 1u))] =
+                        (uint8_t)(w[k] >> (8 * q));
+        }
+    }
+    for (uint32_t cm = cf; cm; cm &= cm - 1u) {
+        const uint32_t m = ctz32(cm), lt = (1u << m) - 1u, below = mask & lt;
+        const uint32_t R = below ? m - msb32(below) - 1u : m + carry_in;   // 1..13
+        dst[o + popc32(below) + popc32(cf & lt)] = run_code(R);
+    }
+    return o + popc32(mask) + popc32(cf);
+}
+
+// The warp's emission stage in shared memory with 4 bytes of padding after every 128:
+// a lane of a dense row writes near byte 32*lane, i.e. word 8*lane, and 32 lanes hit
+// only 4 banks (8-way conflicts on every byte store); with the padding lane l's word is
+// 8*l + l/4, 32 distinct banks.  Logical byte q lives at q + 4*(q/128).
+struct PadStage {
+    uint8_t *p;
+    __host__ __device__ __forceinline__ uint8_t &operator[](uint32_t q) const { return p[q + ((q >> 7) << 2)]; }
+};
+__host__ __device__ constexpr uint32_t pad_stage_bytes(uint32_t n) { return n + ((n + 127) >> 7) * 4; }
+
+// Prefill logical bytes [0, n) of a padded stage with 255 (32-bit stores).
+__device__ __forceinline__ void pad_stage_fill(const PadStage &st, uint32_t n) {
+    for (uint32_t q = 4 * (threadIdx.x & 31); q < n; q += 128)
+        *reinterpret_cast<uint32_t *>(&st[q]) = ~0u;
+}
+
+// A warp copies logical bytes [a, a+n) of a padded stage to dst, where dst is congruent
+// to stage byte a modulo 4: head and tail bytes singly, the middle with 32-bit stores
+// (a 4-byte-aligned logical word never straddles a padding gap).
+__device__ __forceinline__ void warp_copy_padded(uint8_t *dst, const PadStage &st, uint32_t a, uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t head = tmin<uint32_t>(n, (4u - (uint32_t)(reinterpret_cast<uintptr_t>(dst) & 3u)) & 3u);
+    if (lane < head) dst[lane] = st[a + lane];
+    const uint32_t nw = (n - head) / 4u;
+    for (uint32_t q = lane; q < nw; q += 32)
+        reinterpret_cast<uint32_t *>(dst + head)[q] = *reinterpret_cast<const uint32_t *>(&st[a + head + 4 * q]);
+    const uint32_t t0 = head + 4u * nw;
+    if (t0 + lane < n) dst[t0 + lane] = st[a + t0 + lane];
 }
 
 // A warp copies n bytes from shared memory to global memory where src and dst are

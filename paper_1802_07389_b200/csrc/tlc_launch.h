@@ -106,6 +106,19 @@ struct Seg {
     uint32_t flags, pad;
 };
 
+// A slice of a small tensor (K6c): quartic positions [j0, j0+len) of segment `seg` with
+// the segment's pointers and sizes, its index k among the segment's slices (the first at
+// global slice id `first`), last = 1 for the segment's last slice.
+struct SliceRec {
+    const float *t;
+    float *err;
+    uint8_t *payload;
+    tlc_header *hdr;
+    uint32_t n, P, j0, len;
+    uint32_t first, k, last, seg;
+};
+static_assert(sizeof(SliceRec) == 64, "slice records are 64 bytes");
+
 struct SegTable {
     const Seg *d;                   // device table when count > 1
     Seg one;                        // the segment when count == 1
@@ -119,6 +132,15 @@ struct SegTable {
     const uint64_t *rest_list;      // device: the other K2 tiles (the register kernel's, when bulk runs)
     uint64_t n_rest;
     int bulk_nozre_ok;              // every listed segment's payload is 4-byte aligned
+    // small tables (K6c, small.cu): slices of <= kSlice quartic positions of the segments,
+    // contiguous runs of them per CTA of one cooperative launch (sl == nullptr: no plan)
+    const struct SliceRec *sl;      // every slice with its tensor's pointers (refreshed at upload)
+    const uint32_t *sl_cta;         // first slice of every CTA (sl_grid + 1 entries)
+    unsigned int *sl_key;           // per segment max key, zero between launches
+    unsigned long long *sl_sum;     // per slice ZRE run summary
+    unsigned long long *sl_bar;     // grid barrier counter (monotonic)
+    int sl_grid;
+    uint32_t sl_smem;               // dynamic shared memory of the launch
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -160,6 +182,8 @@ struct Table {
     void *ws = nullptr;
     size_t ws_bytes = 0;
     bool own_ws = false;
+    void *d_small = nullptr;        // the K6c plan and its state (small tables only)
+    std::vector<uint4> sl_layout;   // K6c slices on the host: (seg, j0, len, k | last << 16)
     int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);
     int update(const tlc_tensor_desc *descs);
     int upload();
@@ -170,6 +194,10 @@ int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t 
 // Small tensors (small.cu): one CTA per tensor, one launch per direction.
 bool small_enabled();
 bool small_table(const SegTable &T);
+// K6c plan of a small table (slices, CTA runs, state); leaves T.sl null when the table does
+// not fit one cooperative wave (K6, one CTA per tensor, then runs instead)
+int small_plan_build(SegTable &T, const std::vector<Seg> &host, void **d_small, std::vector<uint4> &layout);
+int small_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout);
 int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st);
 int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st);
 

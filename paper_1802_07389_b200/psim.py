@@ -10,8 +10,10 @@ Step (S:451-454):
      synthetic Gaussian-blob task (synth.blobs) against its model replica;
   2. push: every worker compresses each compressed tensor (ndim >= 2, R19; biases go
      uncompressed, P:656-659) with its own push context;
-  3. the server averages: decompress-accumulate the W payloads in worker order from +0
-     (R15, R16), then / W; uncompressed tensors are summed in worker order, then / W;
+  3. the server averages: the library's fused aggregation (tlc_aggregate: K4 + K5m) folds
+     the W payloads in worker order from +0 and divides by W (R15, R16); the compared
+     designs decompress-accumulate in worker order, uncompressed tensors are summed in
+     worker order, then / W (IEEE, in torch);
   4. the server applies momentum SGD (0.9, cosine learning-rate decay) to the
      global model; the model delta is the update (R18, S:491);
   5. pull: the server compresses each delta ONCE with its pull context; every worker
@@ -20,7 +22,8 @@ Step (S:451-454):
 
 Codecs: "3lc" (tlc_batch compress / decompress; s, use_zre), "stoch" (Stoch 3-value + QE,
 tlc_stoch_compress), "int8" (8-bit int), "none" (32-bit float).
-Every compression, decompression and aggregation runs in libtlc's kernels; torch supplies
+Every compression, decompression and 3LC / Stoch aggregation (fold and / W) runs in libtlc's
+kernels (the 8-bit and fp32 baselines' / W is a torch division); torch supplies
 the model's forward/backward, the optimizer arithmetic and device memory.
 """
 from __future__ import annotations
@@ -30,7 +33,7 @@ import math
 
 import torch
 
-from . import (TLC_MODE_ACCUMULATE, TensorSet, new_header, parse_header, tlc_decompress, tlc_int8_compress,
+from . import (TLC_MODE_ACCUMULATE, Aggregate, TensorSet, new_header, parse_header, tlc_decompress, tlc_int8_compress,
                tlc_int8_decompress, tlc_int8_workspace_bytes, tlc_max_payload_bytes, tlc_stoch_compress,
                workspace)
 
@@ -78,10 +81,16 @@ class Sim:
         W = c.workers
         if c.codec == "3lc":
             self.push_ctx = [TensorSet(self.sizes, dev) for _ in range(W)]
+            # the server's aggregation: the library's fused fold + / W over the W push payloads
+            self.means = [torch.empty(n, dtype=torch.float32, device=dev) for n in self.sizes]
+            self.agg = Aggregate(self.means, [(x.payloads, x.hdrs) for x in self.push_ctx])
         elif c.codec == "stoch":
             self.push_pay = [[torch.empty(max(1, tlc_max_payload_bytes(n)), dtype=torch.uint8, device=dev)
                               for n in self.sizes] for _ in range(W)]
             self.push_hdr = [[new_header(dev) for _ in self.sizes] for _ in range(W)]
+            # Stoch 3-value + QE payloads decode like 3LC's (M = m): the same fused aggregation
+            self.means = [torch.empty(n, dtype=torch.float32, device=dev) for n in self.sizes]
+            self.agg = Aggregate(self.means, list(zip(self.push_pay, self.push_hdr)))
         elif c.codec == "int8":
             self.push_codes = [[torch.empty(n, dtype=torch.int8, device=dev) for n in self.sizes] for _ in range(W)]
             self.push_hdr = [[new_header(dev) for _ in self.sizes] for _ in range(W)]
@@ -134,14 +143,12 @@ class Sim:
             if c.codec == "3lc":
                 ctx = self.push_ctx[w]
                 ctx.compress(gw, c.s, c.use_zre)
-                ctx.decompress(sums, TLC_MODE_ACCUMULATE)
                 hs = ctx.headers()
                 push_bytes += sum(h["payload_len"] for h in hs)
             elif c.codec == "stoch":
                 for k, g in enumerate(gw):
                     seed = (c.seed << 20) ^ (w << 8) ^ k
                     tlc_stoch_compress(g, seed, self.step_no, c.use_zre, self.push_pay[w][k], self.push_hdr[w][k])
-                    tlc_decompress(self.push_pay[w][k], self.push_hdr[w][k], g.numel(), sums[k], TLC_MODE_ACCUMULATE)
                 push_bytes += sum(parse_header(h)["payload_len"] for h in self.push_hdr[w])
             elif c.codec == "int8":
                 for k, g in enumerate(gw):
@@ -154,9 +161,15 @@ class Sim:
                 for k, g in enumerate(gw):
                     sums[k] += g
                 push_bytes += 4 * sum(g.numel() for g in gw)
-        # / W as an IEEE fp32 division (R15): an elementwise tensor divisor -- torch turns division by a
-        # Python scalar into multiplication by its reciprocal, which differs for W = 3, 5, ...
-        means = [torch.div(s, torch.full_like(s, float(W))) for s in sums]
+        if c.codec in ("3lc", "stoch"):
+            # R15 in the library: rank-ordered fold from +0 of the nonzero trits, then the IEEE / W
+            self.agg.run()
+            means = [m.clone() for m in self.means]
+        else:
+            # 8-bit int / 32-bit float were summed into sums above in worker order; / W as an
+            # IEEE fp32 division: an elementwise tensor divisor -- torch turns division by a
+            # Python scalar into multiplication by its reciprocal, which differs for W = 3, 5, ...
+            means = [torch.div(s, torch.full_like(s, float(W))) for s in sums]
         plain_means = []
         for i in self.plain:
             acc = torch.zeros_like(grads[0][i])

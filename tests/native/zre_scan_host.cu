@@ -114,16 +114,24 @@ void emit_row_list(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint
 // K3 phase 3 for a row whose literal list was not kept (dense rows): every lane
 // emits its own bytes with lane_emit into a stage prefilled with 255, at its
 // exclusive-scanned offset; the row's output is then copied out.
-void emit_row_lanes(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint8_t *out, uint64_t &off) {
-    uint8_t stage[LANES * SEG + 16];
+void emit_row_lanes(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uint8_t *out, uint64_t &off,
+                    int lane_mode) {
+    uint8_t stage[pad_stage_bytes(LANES * SEG + 16)];
     std::memset(stage, 0xff, sizeof stage);
+    const PadStage pst{stage};
     uint32_t o = 0;
     for (int l = 0; l < LANES; l++) {
-        const uint32_t end = lane_emit(r.w[l], r.mask[l], r.carry_in[l], stage, o);
+        const uint32_t end = lane_mode == 4 ? lane_emit<1>(r.w[l], r.mask[l], r.carry_in[l], pst, o)
+                             : lane_mode == 3 ? lane_emit<3>(r.w[l], r.mask[l], r.carry_in[l], stage, o)
+                             : lane_mode == 2 ? lane_emit<2>(r.w[l], r.mask[l], r.carry_in[l], stage, o)
+                                              : lane_emit<1>(r.w[l], r.mask[l], r.carry_in[l], stage, o);
         if (r.len[l] > 0 && end > o + r.count[l]) std::abort();   // lane_emit never writes past its count
         o += r.count[l];
     }
-    std::memcpy(out + off, stage, r.row_count);
+    if (lane_mode == 4)
+        for (uint32_t q = 0; q < r.row_count; q++) out[off + q] = pst[q];   // the padded layout, logical order
+    else
+        std::memcpy(out + off, stage, r.row_count);
     off += r.row_count;
     carry = r.carry_out;
     if (carry > 0 && row + r.row_len == P) out[off] = run_code(carry);
@@ -194,7 +202,7 @@ extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, u
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
                 load_row(B, row, whi, r);
                 warp_row_host(r, carry);
-                if (lane_mode) emit_row_lanes(r, row, P, carry, out, off);
+                if (lane_mode) emit_row_lanes(r, row, P, carry, out, off, lane_mode);
                 else emit_row_list(r, row, P, carry, out, off);
             }
         }

@@ -57,6 +57,31 @@ def test_argument_validation_without_gpu(T):
     assert lib.tlc_compress(fake, fake + 4096, 0, 1.0, 1, fake, 2, fake, fake, 1 << 20, None) == T.TLC_ERR_ARG
     assert lib.tlc_compress(fake, fake + 4096, 10, 2.0, 1, fake, 2, fake, fake, 1 << 20, None) == T.TLC_ERR_ARG
     assert lib.tlc_compress(fake, fake + 4096, 10, 0.99, 1, fake, 2, fake, fake, 1 << 20, None) == T.TLC_ERR_ARG
-    assert lib.tlc_compress(fake, fake + 4096, 10, 1.0, 1, fake, 1, fake, fake, 1 << 20, None) == T.TLC_ERR_CAPACITY
-    assert lib.tlc_compress(fake, fake + 4096, 10, 1.0, 1, fake, 2, fake, fake, 8, None) == T.TLC_ERR_CAPACITY
+    pay, hdr = fake + 8192, fake + 12288
+    assert lib.tlc_compress(fake, fake + 4096, 10, 1.0, 1, pay, 1, hdr, fake, 1 << 20, None) == T.TLC_ERR_CAPACITY
+    assert lib.tlc_compress(fake, fake + 4096, 10, 1.0, 1, pay, 2, hdr, fake, 8, None) == T.TLC_ERR_CAPACITY
     assert lib.tlc_decompress(fake, fake, 10, fake, 7, fake, 1 << 20, None) == T.TLC_ERR_ARG
+
+
+def test_build_id_matches_sources(T):
+    """The loaded libtlc.so was built from this tree: its embedded id is the hash of the
+    current csrc/, include/ and flags (build.py rebuilds on any difference)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_b", os.path.join(ROOT, "paper_1802_07389_b200", "build.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
+    assert T.tlc_build_id() == B.source_id()
+    assert not B.stale()
+
+
+def test_overlapping_ranges_rejected_without_gpu(T):
+    lib = T.lib()
+    n = 1000
+    t, err, pay, hdr, ws = 1 << 24, 2 << 24, 3 << 24, 4 << 24, 5 << 24
+    ok = [t, err, n, 1.5, 1, pay, 200, hdr, ws, 1 << 24, None]
+    for k, v in [(1, t + 4 * 999), (1, t - 4 * 999), (5, t + 16), (5, err + 3996), (7, t + 64), (7, pay + 100),
+                 (7, err)]:
+        a = list(ok)
+        a[k] = v
+        assert lib.tlc_compress(*a) == T.TLC_ERR_ARG, (k, v)

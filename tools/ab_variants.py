@@ -20,7 +20,10 @@ class Ent(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("launches", ctypes.c_ulonglong), ("total_ms", ctypes.c_double)]
 
 
-def run(path, n=1 << 28, s=1.75, steps=30, warm=45, keep=False):
+def run(path, n=1 << 28, s=None, steps=30, warm=45, keep=False, family=None):
+    """family (env FAMILY: gauss | dense | runs | zeros) and s (env S) select the C3 input."""
+    s = float(os.environ.get("S", "1.75")) if s is None else s
+    family = family or os.environ.get("FAMILY", "gauss")
     L = ctypes.CDLL(path)
     P, U64, SZ = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_size_t
     L.tlc_compress.argtypes = [P, P, U64, ctypes.c_float, ctypes.c_int, P, U64, P, P, SZ, P]
@@ -29,7 +32,8 @@ def run(path, n=1 << 28, s=1.75, steps=30, warm=45, keep=False):
     L.tlc_decompress_workspace_bytes.restype = SZ
     L.tlc_prof_collect.argtypes = [P, ctypes.c_int]
     dev = torch.device("cuda")
-    ts = [torch.from_numpy(synth.gaussian(n, 3, k)).to(dev) for k in range(2)]
+    ts = ([torch.from_numpy(synth.gaussian(n, 3, k)).to(dev) for k in range(2)] if family == "gauss" else
+          [synth.family_torch(family, n, s, dev, 3, k) for k in range(2)])
     err = torch.zeros(n, device=dev)
     out = torch.empty(n, device=dev)
     cap = (n + 4) // 5
@@ -40,6 +44,8 @@ def run(path, n=1 << 28, s=1.75, steps=30, warm=45, keep=False):
     st = torch.cuda.current_stream().cuda_stream
 
     def step(k):
+        if family != "gauss":
+            err.zero_()
         L.tlc_compress(ts[k % 2].data_ptr(), err.data_ptr(), n, s, 1, pay.data_ptr(), cap, hdr.data_ptr(),
                        wc.data_ptr(), wc.numel(), st)
         L.tlc_decompress(pay.data_ptr(), hdr.data_ptr(), n, out.data_ptr(), 0, wd.data_ptr(), wd.numel(), st)

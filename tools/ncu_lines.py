@@ -50,6 +50,7 @@ def main():
     lm = line_map(cubin, fn, outer)
     inst = collections.Counter()
     samp = collections.Counter()
+    data = [r for r in data if r[ie].strip().isdigit() or r[ie].strip() == ""]   # repeated header rows
     for i, r in enumerate(data):
         key = lm.get(16 * i, "?")
         inst[key] += int(r[ie] or 0)
