@@ -926,6 +926,7 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                             o = cost0 + (u >> 16);
                             rem = u & 0xfu;
                         }
+                        TLC_CHECK(off + o + (rem ? 1 : 0) < pend.P);
                         if (rem) out[o++] = run_code(rem);
                         out[o] = (uint8_t)(u >> 8);
                     }
@@ -947,18 +948,22 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                         const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
                         if (lane >= d) x += y;
                     }
-                    const PadStage stage{sm.chunk + (size_t)wk * kK3Stage};
+                    const PadStage stage{sm.chunk + (size_t)wk * kK3Stage, kK3Stage};
                     const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 3u);
                     pad_stage_fill(stage, sh + wr.row_count);
                     __syncwarp();
                     lane_emit(w, mask, wr.carry_in, stage, sh + x - wr.count);
                     __syncwarp();
+                    TLC_CHECK(off + wr.row_count <= pend.P);
                     warp_copy_padded(out, stage, sh, wr.row_count);
                     __syncwarp();                         // the stage is reused by the next row
                     off += wr.row_count;
                     carry = wr.carry_out;
                 }
-                if (lane == 0 && carry > 0 && row + row_len == pend.P) S.payload[off] = run_code(carry);
+                if (lane == 0 && carry > 0 && row + row_len == pend.P) {
+                    TLC_CHECK(off < pend.P);
+                    S.payload[off] = run_code(carry);
+                }
             }
             if (warp == 0) K3_TRACE(pend.id, 5);
         }
@@ -1031,6 +1036,36 @@ static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_e
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
+// A second stream per device (and two events) for the table path's K2 register-tail kernel:
+// it needs only K1's keys, so it runs beside the bulk table kernel instead of after it.
+// Stream capture records the fork and the join as graph edges.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream *side_stream() {
+    static SideStream ss[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream &x = ss[dev & 63];
+    if (!x.s) {
+        cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    }
+    return &x;
+}
+
+// TLC_NO_FORK=1 keeps the K2 tail on the caller's stream (A/B)
+static bool fork_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_NO_FORK");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
     if (small_table(T)) return launch_small_compress(T, s, use_zre, st);    // one launch, on chip
     const int sms = num_sms();
@@ -1060,19 +1095,31 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
             tile_begin = nbulk * kBulkPos / T.sz.t2;
         } else if (use_bulk() && T.count > 1 && T.n_bulk && (use_zre || T.bulk_nozre_ok) &&
                    T.sz.t2 == kLargeItems.t2) {
+            skip_bulk = 1;
+        }
+        const uint64_t nreg = skip_bulk ? T.n_rest : T.n2 - tile_begin;
+        if (!g_k2_blocks) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
+        const int rgrid = (int)tmax<uint64_t>(1, tmin<uint64_t>(nreg, (uint64_t)sms * tmax(1, g_k2_blocks)));
+        const bool fork = skip_bulk && nreg > 0 && fork_enabled();
+        SideStream *ss = fork ? side_stream() : nullptr;
+        if (fork) {
+            // the ragged tail tiles of the table (register kernel) beside the bulk kernel
+            cudaEventRecord(ss->fork, st);
+            cudaStreamWaitEvent(ss->s, ss->fork, 0);
+            tlc_quant_qe_kernel<<<rgrid, kK2Threads, 0, ss->s>>>(T, maxkey, s, use_zre, scratch, tile_begin, skip_bulk);
+            cudaEventRecord(ss->join, ss->s);
+        }
+        if (skip_bulk) {
             // large tables only: below 32M values (ResNet-50) the register kernel at 2 CTAs/SM
             // measured faster (0.44 vs 0.49 ms per W=1 exchange step) than the 1-CTA/SM bulk one
             const int grid = (int)tmin<uint64_t>(T.n_bulk * (T.sz.t2 / kBulkPos), (uint64_t)sms);
             launch_pdl(tlc_quant_qe_bulk_table_kernel, grid, kK2TThreads, sizeof(BulkSmem), st, T, maxkey, s, use_zre,
                        scratch);
-            skip_bulk = 1;
         }
-        const uint64_t nreg = skip_bulk ? T.n_rest : T.n2 - tile_begin;
-        if (nreg > 0) {
-            if (!g_k2_blocks)
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k2_blocks, tlc_quant_qe_kernel, kK2Threads, 0);
-            const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(nreg, (uint64_t)sms * tmax(1, g_k2_blocks)));
-            launch_pdl(tlc_quant_qe_kernel, grid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin,
+        if (fork) {
+            cudaStreamWaitEvent(st, ss->join, 0);
+        } else if (nreg > 0) {
+            launch_pdl(tlc_quant_qe_kernel, rgrid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin,
                        skip_bulk);
         }
     });

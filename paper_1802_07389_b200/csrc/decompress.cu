@@ -16,6 +16,7 @@
 //     128-bit stores to the five partitions (or, in ACCUMULATE mode, a
 //     read-modify-write of the elements whose q != 0, R16).
 #include <algorithm>
+#include <cstdlib>
 
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
@@ -632,6 +633,264 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
     }
 }
 
+// ---------------------------------------------------------------- K5m, sources in parallel
+// The kernel above expands the W sources of a tile one after another with the whole CTA,
+// so a tile pays W dependent global round trips (seek entries, then the window; over
+// NVLink in peer mode) and 2W block barriers: per owner its time hardly fell as W grew
+// (loopback, BERT-large: 0.35 / 0.24 / 0.19 / 0.20 ms per owner at W = 1 / 2 / 4 / 8).
+// ncu (W = 8): 85 M warp instructions per owner, mostly every thread walking all its
+// byte slots of every source window (window_nonzero, per-byte loads) though a window at
+// s = 1.9 holds a few hundred bytes.  Here the CTA splits into WP groups (WP = W rounded
+// up to a power of two), group g expands source g -- all groups at once, one round trip
+// per tile -- in passes of 16 bytes per thread over only the bytes the window has.
+// Loopback, BERT-large, s = 1.9, per owner: 0.195 / 0.108 / 0.080 ms at W = 2 / 4 / 8
+// (sequential: 0.242 / 0.192 / 0.202; profiles/r02n_loopback.txt).
+// The fold (rank order from +0, skip-zero, IEEE / W, R15; NaN for a failed source, R24)
+// is the same as above.
+template <int WP>
+__global__ void __launch_bounds__(kK5Threads, 3)
+tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
+    constexpr int TP = kK5Threads / WP;                  // threads per source
+    constexpr int BPT = kT5 / TP;                        // window bytes per thread (16 * WP)
+    constexpr int NV = BPT / 16;                         // 16-byte loads per thread
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ uint64_t s_first[kK5mSegCache];
+    __shared__ unsigned int s_stat[kMaxSources];
+    __shared__ int s_ok[kMaxSources], s_nz[kMaxSources], s_poison;
+    __shared__ unsigned int s_wsum[kK5Threads / 32];
+    __shared__ float s_M[kMaxSources];
+    seg_index_load<5, kK5mSegCache>(A, s_first);
+    pdl_wait();                                          // K4's seek entries
+    uint8_t(*E)[kT5] = reinterpret_cast<uint8_t(*)[kT5]>(smem_raw);
+    uint32_t(*V)[5][256] = reinterpret_cast<uint32_t(*)[5][256]>(smem_raw + (size_t)WP * kT5);
+    const bool pow2 = (W & (W - 1)) == 0;
+    const float Wf = (float)W, rW = 1.0f / (float)W;
+    const int g = threadIdx.x / TP, tg = threadIdx.x % TP, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int cur = -1;
+    for (uint64_t tile = blockIdx.x; tile < A.n5; tile += gridDim.x) {
+        const int q = find_seg_c<5, kK5mSegCache>(A, tile, s_first);
+        const Seg S = get_seg(A, q);
+        const uint64_t P = S.P, n = S.n, lt = tile - S.k5, ntiles = (P + kT5 - 1) / kT5;
+        const uint64_t J0 = lt * kT5;
+        const int tl = (int)tmin<uint64_t>(kT5, P - J0);
+        // every thread of group g reads source g's row (the same addresses: broadcast)
+        const bool src = g < W;
+        Seg R{};
+        unsigned int st = TLC_OK, flags = 0;
+        uint64_t Z = 0;
+        if (src) {
+            R = get_seg(X, g * A.count + q);
+            st = R.hdr->status;
+            flags = R.hdr->flags;
+            Z = R.hdr->payload_len;
+        }
+        __syncthreads();                                   // previous tile's readers of E / V / flags
+        if (tg == 0 && src) {
+            s_stat[g] = st;
+            s_M[g] = R.hdr->M;
+            s_nz[g] = 0;
+        }
+        if (threadIdx.x == 0) s_poison = 0;
+        __syncthreads();
+        bool poison = false;
+        for (int w = 0; w < W; w++) poison |= s_stat[w] != TLC_OK;   // R24
+        // ---- expansion of source g's window into E[g] (all groups at once).  A group reads the
+        // window in passes of 16 bytes per thread (16*TP bytes), as many as the window needs --
+        // one for a sparse window, up to kT5/(16*TP) + 1 for a dense one -- so idle byte slots
+        // cost nothing; each pass scans its expansion lengths within the group and scatters the
+        // literals.  Groups synchronise on their own named barrier (id 1 + g).
+        const bool zre = (flags & TLC_FLAG_ZRE) != 0;
+        const bool act0 = src && !poison;
+        int wl = 0, sh = 0, skip = 0;
+        uint64_t bi = 0;
+        if (act0 && zre) {
+            const unsigned long long sk = seek[R.k5 + lt];
+            bi = sk >> 4;
+            skip = (int)(sk & 15);
+            const uint64_t be = lt + 1 < ntiles ? (seek[R.k5 + lt + 1] >> 4) : Z - 1;
+            wl = (int)(be - bi) + 1;                           // <= kT5 + 1
+            sh = (int)(bi & 15);                               // passes start at the granule of bi
+        }
+        auto group_sync = [&]() {
+            if (TP == 32) __syncwarp();
+            else asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(TP) : "memory");
+        };
+        // pass 0 doubles as the nonzero test: a window without a literal but 121 adds +0 only
+        if (act0) {
+            uint8_t *Eg = E[g];
+            if (q != cur) {                                    // Eq. 3 values of source g (new context)
+                const float M = s_M[g];
+                for (int v = tg; v < 256; v += TP) {
+                    uint32_t r = v < 243 ? v : 121;
+#pragma unroll
+                    for (int i = 4; i >= 0; i--) {
+                        V[g][i][v] = __float_as_uint(__fmul_rn(M, (float)((int)(r % 3u) - 1)));
+                        r /= 3u;
+                    }
+                }
+            }
+            for (int k = 16 * tg; k < kT5; k += 16 * TP)      // 121 prefill
+                *reinterpret_cast<uint4 *>(Eg + k) = make_uint4(0x79797979u, 0x79797979u, 0x79797979u, 0x79797979u);
+            bool nz = false;
+            if (zre) {
+                const uint8_t *gbase = R.payload + (bi & ~15ull);
+                const bool pal = (reinterpret_cast<uintptr_t>(R.payload) & 15u) == 0;
+                int pos = -skip;                               // tile position of the pass's first byte
+                group_sync();                                  // prefill before any scatter
+                for (int base = 0; base < wl + sh; base += 16 * TP) {   // uniform within the group
+                    const int r0 = base + 16 * tg - sh;        // window offset of this thread's 16 bytes
+                    uint32_t wd[4];
+                    if (pal && r0 >= 0 && r0 + 15 < wl) {
+                        const uint4 xv = __ldg(reinterpret_cast<const uint4 *>(gbase + base + 16 * tg));
+                        wd[0] = xv.x; wd[1] = xv.y; wd[2] = xv.z; wd[3] = xv.w;
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; h++) {
+                            uint32_t y = 0;
+#pragma unroll
+                            for (int c = 0; c < 4; c++) {
+                                const int rr = r0 + 4 * h + c;
+                                if (rr >= 0 && rr < wl) y |= (uint32_t)R.payload[bi + rr] << (8 * c);
+                            }
+                            wd[h] = y;
+                        }
+                    }
+                    uint32_t lens = 0;
+                    if (r0 >= 0 && r0 + 15 < wl) {
+                        lens = word_len(wd[0]) + word_len(wd[1]) + word_len(wd[2]) + word_len(wd[3]);
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 16; m++)
+                            if (r0 + m >= 0 && r0 + m < wl) lens += zre_len((wd[m >> 2] >> (8 * (m & 3))) & 0xffu);
+                    }
+                    // exclusive scan within the group: the warp, then its earlier warps
+                    uint32_t x = lens;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    uint32_t wofs = 0, tot = __shfl_sync(0xffffffffu, x, 31);
+                    if (TP > 32) {
+                        if (lane == 31) s_wsum[warp] = x;
+                        group_sync();
+                        tot = 0;
+                        for (int k = g * (TP / 32); k < (g + 1) * (TP / 32); k++) {
+                            const uint32_t v = s_wsum[k];
+                            wofs += k < warp ? v : 0u;
+                            tot += v;
+                        }
+                    }
+                    int p = pos + (int)(wofs + x - lens);
+#pragma unroll
+                    for (int m = 0; m < 16; m++) {
+                        const int r = r0 + m;
+                        if (r < 0 || r >= wl) continue;
+                        const uint32_t b = (wd[m >> 2] >> (8 * (m & 3))) & 0xffu;
+                        const uint32_t l = zre_len(b);
+                        if (l == 1) {
+                            nz |= b != kZeroGroup;
+                            TLC_CHECK(!(p >= 0 && p < tl) || p < kT5);
+                            if (p >= 0 && p < tl) Eg[p] = (uint8_t)b;   // literal byte
+                        }
+                        p += (int)l;
+                    }
+                    pos += (int)tot;
+                    if (TP > 32) group_sync();                 // s_wsum reuse by the next pass
+                }
+            } else {
+                // quartic bytes as sent (a literal > 242 is FORMAT)
+                group_sync();                                  // prefill done (bytes past tl stay 121)
+                bool bad = false;
+                for (int jl = tg; jl < tl; jl += TP) {
+                    uint8_t b = R.payload[J0 + jl];
+                    if (b > 242) { bad = true; b = kZeroGroup; }
+                    Eg[jl] = b;
+                }
+                nz = true;
+                if (bad) {
+                    raise_format(R.hdr);
+                    s_poison = 1;
+                }
+            }
+            if (nz) s_nz[g] = 1;
+        }
+        __syncthreads();                                     // every group's E, V and nonzero flag
+        if (threadIdx.x < W) s_ok[threadIdx.x] = !poison && s_nz[threadIdx.x];
+        cur = poison ? -1 : q;
+        __syncthreads();
+        poison |= s_poison != 0;
+#pragma unroll 1
+        for (int k = 0; k < kK5BytesPerThread / 4; k++) {
+            const int jl = 4 * threadIdx.x + 4 * kK5Threads * k;
+            if (jl >= tl) break;
+            float acc[5][4];
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0 (R15)
+            bool any = false;
+            for (int w = 0; w < W; w++) {                          // rank order
+                if (!s_ok[w]) continue;
+                const uint32_t w4 = *reinterpret_cast<const uint32_t *>(E[w] + jl);
+                if (w4 == 0x79797979u) continue;                 // all trits zero: adds +0 only
+                any = true;
+                const uint32_t b[4] = {w4 & 0xffu, (w4 >> 8) & 0xffu, (w4 >> 16) & 0xffu, w4 >> 24};
+#pragma unroll
+                for (int i = 0; i < 5; i++)
+#pragma unroll
+                    for (int c = 0; c < 4; c++) acc[i][c] = __fadd_rn(acc[i][c], __uint_as_float(V[w][i][b[c]]));
+            }
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                float r[4];
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    r[c] = poison ? __int_as_float(0x7fc00000)
+                                  : !any ? 0.0f : (pow2 ? __fmul_rn(acc[i][c], rW) : __fdiv_rn(acc[i][c], Wf));
+                const uint64_t e0 = (uint64_t)i * P + J0;
+                const int lim = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
+                float *o = S.out + e0 + jl;
+                if (((reinterpret_cast<uintptr_t>(o) & 15u) == 0) && jl + 3 < lim) {
+                    __stcs(reinterpret_cast<float4 *>(o), make_float4(r[0], r[1], r[2], r[3]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if (jl + c < lim) o[c] = r[c];
+                }
+            }
+        }
+    }
+}
+
+template <int WP>
+__host__ __device__ constexpr size_t k5p_smem_bytes() { return (size_t)WP * kT5 + (size_t)WP * 5 * 256 * sizeof(uint32_t); }
+
+template <int WP>
+static void launch_par(const SegTable &A, const SegTable &X, int W, const unsigned long long *seek, cudaStream_t st) {
+    static bool attr = false;
+    static int per_sm = 0;
+    if (!attr) {
+        cudaFuncSetAttribute(tlc_aggregate_par_kernel<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)k5p_smem_bytes<WP>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_par_kernel<WP>, kK5Threads,
+                                                      k5p_smem_bytes<WP>());
+        attr = true;
+    }
+    const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)num_sms() * tmax(1, per_sm)));
+    launch_pdl(tlc_aggregate_par_kernel<WP>, grid, kK5Threads, k5p_smem_bytes<WP>(), st, A, X, W, seek);
+}
+
+// TLC_K5M_SEQ=1 runs the sources-in-sequence kernel at every W (A/B)
+static bool k5m_seq() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K5M_SEQ");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st) {
     // X: K4 over every received payload (validation + seek entries), then one fused pass
     if (W < 1 || W > kMaxSources) return TLC_ERR_ARG;
@@ -648,13 +907,20 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(X.n4, (uint64_t)sms * 8));
         tlc_zre_scan_kernel<<<grid, kK4Threads, 0, st>>>(X, ctrl, states, seek);
     }
+    KernelScope ks(kK6, st);
+    // W = 1: the sequential kernel (one source either way; 0.346 vs 0.374 ms, BERT-large)
+    if (!k5m_seq() && W > 1) {
+        if (W == 2) launch_par<2>(A, X, W, seek, st);
+        else if (W <= 4) launch_par<4>(A, X, W, seek, st);
+        else launch_par<8>(A, X, W, seek, st);
+        return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+    }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k5m_smem_bytes(kMaxSources));
         attr = true;
     }
-    KernelScope ks(kK6, st);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_kernel, kK5Threads, k5m_smem_bytes(W));
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * tmax(1, per_sm)));

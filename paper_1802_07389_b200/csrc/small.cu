@@ -193,6 +193,7 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
                 const uint32_t R = (uint32_t)(q - prev - 1) + c;
                 c = 0;
                 o += R / kMaxRun;
+                TLC_CHECK(s_off[warp] + o + (R % kMaxRun ? 1 : 0) < P);
                 if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
                 uint32_t word = w[0];
 #pragma unroll
@@ -201,6 +202,7 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
                 prev = q;
             }
         }
+        TLC_CHECK(!(threadIdx.x == 0 && s_carry[nrows] > 0) || total < P);
         if (threadIdx.x == 0 && s_carry[nrows] > 0) S.payload[total] = run_code(s_carry[nrows]);
         __syncthreads();                                         // shared memory reuse
     }
@@ -449,7 +451,8 @@ tlc_small_coop_compress_kernel(const SegTable T, float s, int use_zre) {
         }
         uint8_t *out = sl.payload + o0;
         const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(out) & 3u);
-        const PadStage pst{stage};
+        const PadStage pst{stage, kStage};
+        TLC_CHECK(o0 + wr.row_count + (sl.last && wr.carry_out > 0) <= sl.P);
         pad_stage_fill(pst, sh + wr.row_count);
         __syncwarp();
         lane_emit(w, mask, wr.carry_in, pst, sh + x - wr.count);

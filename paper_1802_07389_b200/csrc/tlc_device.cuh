@@ -12,6 +12,23 @@
 
 namespace tlc {
 
+// ---------------------------------------------------------------- device checks
+// -DTLC_DEVICE_CHECKS (a test build, tests/test_gpu_device_checks.py): bounds of every
+// data-dependent store index are asserted on the device; a violation prints its site and
+// traps.  compute-sanitizer is not available on the GPU pool this was built on.
+#ifdef TLC_DEVICE_CHECKS
+#include <cstdio>
+#define TLC_CHECK(c)                                                                      \
+    do {                                                                                  \
+        if (!(c)) {                                                                       \
+            printf("TLC_CHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__);            \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define TLC_CHECK(c) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------- constants
 constexpr uint8_t kZeroGroup = 121;        // five zero trits
 constexpr uint8_t kFirstRunCode = 243;     // 243+(k-2), 2 <= k <= 14
@@ -494,7 +511,13 @@ __host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], u
 // 8*l + l/4, 32 distinct banks.  Logical byte q lives at q + 4*(q/128).
 struct PadStage {
     uint8_t *p;
-    __host__ __device__ __forceinline__ uint8_t &operator[](uint32_t q) const { return p[q + ((q >> 7) << 2)]; }
+    uint32_t cap;                    // physical bytes (checked in TLC_DEVICE_CHECKS builds)
+    __host__ __device__ __forceinline__ uint8_t &operator[](uint32_t q) const {
+#if defined(TLC_DEVICE_CHECKS) && defined(__CUDA_ARCH__)
+        TLC_CHECK(q + ((q >> 7) << 2) < cap);
+#endif
+        return p[q + ((q >> 7) << 2)];
+    }
 };
 __host__ __device__ constexpr uint32_t pad_stage_bytes(uint32_t n) { return n + ((n + 127) >> 7) * 4; }
 
