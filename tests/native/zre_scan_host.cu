@@ -121,14 +121,15 @@ void emit_row_lanes(const Row &r, uint64_t row, uint64_t P, uint32_t &carry, uin
     const PadStage pst{stage};
     uint32_t o = 0;
     for (int l = 0; l < LANES; l++) {
-        const uint32_t end = lane_mode == 4 ? lane_emit<1>(r.w[l], r.mask[l], r.carry_in[l], pst, o)
+        const uint32_t end = lane_mode == 5 ? lane_emit<4>(r.w[l], r.mask[l], r.carry_in[l], pst, o)
+                             : lane_mode == 4 ? lane_emit<1>(r.w[l], r.mask[l], r.carry_in[l], pst, o)
                              : lane_mode == 3 ? lane_emit<3>(r.w[l], r.mask[l], r.carry_in[l], stage, o)
                              : lane_mode == 2 ? lane_emit<2>(r.w[l], r.mask[l], r.carry_in[l], stage, o)
                                               : lane_emit<1>(r.w[l], r.mask[l], r.carry_in[l], stage, o);
         if (r.len[l] > 0 && end > o + r.count[l]) std::abort();   // lane_emit never writes past its count
         o += r.count[l];
     }
-    if (lane_mode == 4)
+    if (lane_mode >= 4)
         for (uint32_t q = 0; q < r.row_count; q++) out[off + q] = pst[q];   // the padded layout, logical order
     else
         std::memcpy(out + off, stage, r.row_count);

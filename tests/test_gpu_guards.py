@@ -82,7 +82,8 @@ def test_corrupt_payloads_write_nothing_outside(bad):
     if bad == "truncate":
         hdr[16:24] = torch.tensor(list(int(h["payload_len"] - 3).to_bytes(8, "little")), dtype=torch.uint8)
     elif bad == "overrun":
-        pay[0] = 255
+        k = int((pay[: h["payload_len"]] < 243).nonzero()[0])    # a literal becomes a 14-run code
+        pay[k] = 255
     elif bad == "literal":
         hdr[4] = 0
         hdr[16:24] = torch.tensor(list(P.to_bytes(8, "little")), dtype=torch.uint8)

@@ -63,12 +63,12 @@ def _streams():
     yield np.array(parts, np.uint8)
 
 
-@pytest.mark.parametrize("lane_mode", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("lane_mode", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("threads", [1, 2, 3, 8])
 def test_scan_matches_oracle_zre(sim, threads, lane_mode):  # threads = warps per CTA
     """lane_mode 0: rows emitted from their kept literal lists; 1-3: the dense-row form,
     every lane's bytes emitted by lane_emit (variant 1, 2 or 3) into a 255-prefilled stage;
-    4: variant 1 into the bank-padded stage (PadStage) K3 and K6c use."""
+    4: variant 1 into the bank-padded stage (PadStage) K3 and K6c use; 5: variant 4 into it."""
     for i, B in enumerate(_streams()):
         ref = O.zre_encode(B)
         for nchunks in (1, 2, 3, 7, 64):

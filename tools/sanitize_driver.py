@@ -50,7 +50,7 @@ for bad in ("truncate", "overrun", "literal"):
     if bad == "truncate":
         hh[16:24] = torch.tensor(list(int(hd["payload_len"] - 3).to_bytes(8, "little")), dtype=torch.uint8)
     elif bad == "overrun":
-        q[0] = 255
+        q[int((q[: hd["payload_len"]] < 243).nonzero()[0])] = 255     # a literal becomes a 14-run code
     else:
         hh[4] = 0                                               # claim no ZRE: bytes > 242 are invalid
         hh[16:24] = torch.tensor(list(int(-(-n // 5)).to_bytes(8, "little")), dtype=torch.uint8)
