@@ -658,8 +658,6 @@ template <int WP>
 __global__ void __launch_bounds__(kK5Threads, 3)
 tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
     constexpr int TP = kK5Threads / WP;                  // threads per source
-    constexpr int BPT = kT5 / TP;                        // window bytes per thread (16 * WP)
-    constexpr int NV = BPT / 16;                         // 16-byte loads per thread
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint64_t s_first[kK5mSegCache];
     __shared__ unsigned int s_stat[kMaxSources];

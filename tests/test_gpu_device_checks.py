@@ -23,7 +23,8 @@ def test_suites_under_device_checks():
     for coop in ("0", "1"):
         env = dict(os.environ, TLC_LIB=lib, TLC_COOP=coop)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_guards.py",
-                            "tests/test_gpu_parity.py::test_parity_sizes", "tests/test_gpu_parity.py::test_parity_families",
+                            "tests/test_gpu_parity.py::test_parity_sizes", "tests/test_gpu_parity.py::test_parity_runs_many_tiles",
+                            "tests/test_gpu_parity.py::test_corrupt_payloads_raise_format",
                             "tests/test_gpu_batched.py", "tests/test_gpu_exchange_loopback.py::test_loopback_matches_oracle",
                             "tests/test_gpu_codecs.py"],
                            cwd=ROOT, env=env, capture_output=True, text=True, timeout=1800)
