@@ -24,7 +24,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     width, depth, batch, steps = 4096, 6, 64, 20
     res = {}
-    for mode in ("allreduce", "tlc_p2p", "tlc_nccl"):
+    for mode in ("allreduce", "tlc_p2p", "tlc_p2p_batch", "tlc_nccl"):
         torch.manual_seed(0)
         layers = []
         for _ in range(depth):
@@ -33,7 +33,7 @@ def main():
         ddp = DDP(model, device_ids=[local])
         state = None
         if mode != "allreduce":
-            state = TLCHookState(s=1.75, p2p=(mode == "tlc_p2p"))
+            state = TLCHookState(s=1.75, p2p=mode.startswith("tlc_p2p"), batch=mode.endswith("batch"))
             ddp.register_comm_hook(state, tlc_hook)
         opt = torch.optim.SGD(ddp.parameters(), lr=1e-4)
         x = torch.randn(batch, width, device=dev)
