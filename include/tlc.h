@@ -294,6 +294,14 @@ uint64_t tlc_exchange_wire_bytes(const tlc_exchange *x, int direction /* 0 push,
  * checkpoint); the caller keeps them alive and unaliased until the exchange is
  * destroyed.  Synchronizes the device. */
 int tlc_exchange_bind_error_buffers(tlc_exchange *x, float *push_err, float *pull_err);
+/* tlc_exchange_set_transport: the NCCL transport's mode (between steps, not in peer-memory
+ * or loopback mode).  0 (default): every owner's whole capacity region (ceil(n/5) bytes
+ * per context) and the headers move each direction, no host synchronization.  1 (exact,
+ * "sizes first"): each rank packs its payloads, the packing offsets are all-gathered
+ * (ncclAllGather), the host waits for them once per direction, then grouped
+ * ncclSend/ncclRecv move exactly the payload bytes, unpacked on the receiver.  Same
+ * results bit for bit.  Push/pull in mode 1 synchronize `stream` once each. */
+int tlc_exchange_set_transport(tlc_exchange *x, int mode);
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream);
 int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre, void *stream);
 int tlc_exchange_status(tlc_exchange *x, unsigned int *status, void *stream);

@@ -70,6 +70,7 @@ def _load():
         "tlc_exchange_pull_error": (P, [P]),
         "tlc_exchange_wire_bytes": (U64, [P, I]),
         "tlc_exchange_bind_error_buffers": (I, [P, P, P]),
+        "tlc_exchange_set_transport": (I, [P, I]),
         "tlc_exchange_push": (I, [P, P, F, I, P]),
         "tlc_exchange_pull": (I, [P, P, F, I, P]),
         "tlc_exchange_status": (I, [P, P, P]),
@@ -456,10 +457,12 @@ def _check_list(name, ts, sizes, device):
 class Exchange:
     """3LC parameter-server push/pull for a fixed tensor list (include/tlc.h)."""
 
-    def __init__(self, comm: Comm | None, sizes, p2p: bool = False, group=None, _handle=None, _device=None):
+    def __init__(self, comm: Comm | None, sizes, p2p: bool = False, group=None, _handle=None, _device=None,
+                 exact: bool = False):
         """p2p=True: peer-memory mode -- the compressed payloads are read by the consuming
         kernels straight from the producing GPU over NVLink (CUDA IPC mappings set up
-        here through torch.distributed); otherwise NCCL send/recv moves them.
+        here through torch.distributed); otherwise NCCL send/recv moves them: whole capacity
+        regions, or with exact=True the payload bytes after a sizes all-gather.
         (_handle: a virtual rank of a Loopback group, owned by the group.)"""
         import numpy as np
 
@@ -482,6 +485,10 @@ class Exchange:
         self.pull_err = _as_tensor(_lib.tlc_exchange_pull_error(self._x), self.owned_elements, self.device)
         self.push_err = _as_tensor(_lib.tlc_exchange_push_error(self._x), sum(self.sizes), self.device)
         self.p2p = bool(p2p) or _handle is not None
+        if exact and not self.p2p:
+            rc = _lib.tlc_exchange_set_transport(self._x, 1)
+            if rc != TLC_OK:
+                raise TlcError(rc, "tlc_exchange_set_transport")
         if p2p:
             mine = (ctypes.c_ubyte * 320)()
             rc = _lib.tlc_exchange_ipc_handles(self._x, ctypes.cast(mine, ctypes.c_void_p))

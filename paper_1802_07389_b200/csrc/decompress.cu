@@ -834,6 +834,8 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
         cur = poison ? -1 : q;
         __syncthreads();
         poison |= s_poison != 0;
+        uint32_t okmask = 0;                                       // sources with a nonzero trit here
+        for (int w = 0; w < W; w++) okmask |= (uint32_t)(s_ok[w] != 0) << w;
 #pragma unroll 1
         for (int k = 0; k < kK5BytesPerThread / 4; k++) {
             const int jl = 4 * threadIdx.x + 4 * kK5Threads * k;
@@ -844,8 +846,8 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
 #pragma unroll
                 for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0 (R15)
             bool any = false;
-            for (int w = 0; w < W; w++) {                          // rank order
-                if (!s_ok[w]) continue;
+            for (uint32_t m = okmask; m; m &= m - 1u) {            // rank order (ascending bits)
+                const int w = (int)ctz32(m);
                 const uint32_t w4 = *reinterpret_cast<const uint32_t *>(E[w] + jl);
                 if (w4 == 0x79797979u) continue;                 // all trits zero: adds +0 only
                 any = true;

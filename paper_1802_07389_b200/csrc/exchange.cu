@@ -52,6 +52,40 @@ struct Ctx {
     size_t owned_off;   // offset in the owner's flat owned buffer (valid on the owner)
 };
 
+// Exact transport.  Packing: the payloads of `count` contexts whose headers are the
+// consecutive hdr[0..count) (a region's contexts in slot order: the layout of the header
+// arrays) are laid end to end; off[k] = packed offset, off[count] = total, len[k] = bytes
+// (payload_len, 0 for a failed compression).  Tiny: one thread.
+__global__ void tlc_pack_offsets_kernel(const tlc_header *hdr, int count, uint64_t *off, uint64_t *len) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        uint64_t o = 0;
+        for (int k = 0; k < count; k++) {
+            const uint64_t l = hdr[k].status == TLC_OK ? hdr[k].payload_len : 0;
+            off[k] = o;
+            len[k] = l;
+            o += l;
+        }
+        off[count] = o;
+    }
+}
+// copy len[k] bytes src_base + src_off[k] -> dst_base + dst_off[k] for every item k (one
+// block per item; 16-byte steps where both ends are aligned)
+__global__ void tlc_copy_items_kernel(const uint8_t *src_base, const uint64_t *src_off, uint8_t *dst_base,
+                                      const uint64_t *dst_off, const uint64_t *len, int count) {
+    for (int k = blockIdx.x; k < count; k += gridDim.x) {
+        const uint8_t *src = src_base + src_off[k];
+        uint8_t *dst = dst_base + dst_off[k];
+        const uint64_t n = len[k];
+        if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0) {
+            for (uint64_t i = 16 * threadIdx.x; i + 16 <= n; i += 16 * blockDim.x)
+                *reinterpret_cast<uint4 *>(dst + i) = *reinterpret_cast<const uint4 *>(src + i);
+            for (uint64_t i = (n & ~15ull) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+        } else {
+            for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+        }
+    }
+}
+
 // worst status over a list of header pointers (peer-memory mode: the headers live on
 // the producing ranks)
 __global__ void tlc_status_list_kernel(const tlc_header *const *__restrict__ h, int count, unsigned int *out) {
@@ -171,6 +205,19 @@ struct tlc_exchange {
     const tlc_header **d_status_list = nullptr;
     int status_count = 0;
     int phase = 0;                                   // 0: next call is push, 1: pull
+    // NCCL "exact" transport (tlc_exchange_set_transport): payloads packed per owner, the
+    // byte counts all-gathered first (one host sync per direction), then only those bytes sent
+    int exact = 0;
+    uint8_t *pack = nullptr;                         // packed send (push: by owner; pull: own region)
+    uint8_t *pack_recv = nullptr;                    // packed receive, W slots of the larger region
+    // device: [0, C+1) packed offsets, [C+1, 2C+1) lengths, [2C+1, 2C+1+C) capacity offsets of
+    // the contexts in owner-major order; then the W x (C+1) all-gathered offsets; then the
+    // unpack items (src, dst, len: 3 x W x C)
+    uint64_t *d_pk = nullptr, *d_all = nullptr, *d_items = nullptr;
+    uint64_t *h_all = nullptr;                       // pinned host copy of the all-gathered offsets
+    std::vector<uint64_t> h_items;
+    size_t max_region = 0;
+    uint64_t last_recv[2] = {0, 0};                  // bytes received in the last push / pull (exact mode)
 };
 
 static int cuda_ok(cudaError_t e) { return e == cudaSuccess ? TLC_OK : TLC_ERR_CUDA; }
@@ -291,6 +338,10 @@ int tlc_plan_compute(int num_tensors, const uint64_t *sizes, int world, int cap,
 int tlc_exchange_destroy(tlc_exchange *x) {
     if (!x) return TLC_ERR_ARG;
     for (void *p : x->opened) cudaIpcCloseMemHandle(p);
+    if (x->h_all) cudaFreeHost(x->h_all);
+    void *dev2[] = {x->pack, x->pack_recv, x->d_pk, x->d_all, x->d_items};
+    for (void *p : dev2)
+        if (p) cudaFree(p);
     void *dev[] = {x->own_push_err, x->owned_buf, x->own_pull_err, x->push_send, x->push_recv, x->pull_buf,
                    x->push_hdr_send, x->push_hdr_recv, x->pull_hdr, x->d_status, x->flags, x->d_peer_flags,
                    x->d_epoch, (void *)x->d_status_list};
@@ -512,6 +563,11 @@ int tlc_exchange_traffic(tlc_exchange *x, uint64_t *out) {
     if (cudaDeviceSynchronize() != cudaSuccess) return TLC_ERR_CUDA;
     const int W = x->W, me = x->me;
     const int nown = (int)x->owned[me].size();
+    if (x->exact) {
+        out[0] = x->last_recv[0];
+        out[1] = x->last_recv[1];
+        return TLC_OK;
+    }
     if (!x->p2p) {
         out[0] = (uint64_t)(W - 1) * (x->region_bytes[me] + nown * sizeof(tlc_header));
         uint64_t b = 0;
@@ -657,7 +713,172 @@ static int phase_apply(tlc_exchange *x, float *const *outs, cudaStream_t st) {
     return launch_decompress_table(x->apply_tab[slot].T, TLC_MODE_ACCUMULATE, x->apply_tab[slot].ws, st);
 }
 
+// ------------------------------------------------------------------ NCCL exact transport
+// Sizes first: pack the payloads, all-gather the packing offsets, one host
+// sync, then grouped send/recv of exactly the payload bytes, and unpack into the capacity
+// layout the aggregation / apply tables read.
+static int exact_alloc(tlc_exchange *x) {
+    const int W = x->W, C = (int)x->ctx.size();
+    for (int o = 0; o < W; o++) x->max_region = std::max(x->max_region, x->region_bytes[o]);
+    int rc = TLC_OK;
+    auto alloc = [&](void **p, size_t bytes) {
+        if (rc == TLC_OK && cudaMalloc(p, std::max<size_t>(bytes, 256)) != cudaSuccess) rc = TLC_ERR_CUDA;
+    };
+    alloc((void **)&x->pack, x->total_region);
+    alloc((void **)&x->pack_recv, (size_t)W * x->max_region);
+    alloc((void **)&x->d_pk, (3 * (size_t)C + 1) * sizeof(uint64_t));
+    alloc((void **)&x->d_all, (size_t)W * (C + 1) * sizeof(uint64_t));
+    alloc((void **)&x->d_items, 3 * (size_t)W * C * sizeof(uint64_t));
+    if (rc == TLC_OK && cudaMallocHost((void **)&x->h_all, (size_t)W * (C + 1) * sizeof(uint64_t)) != cudaSuccess)
+        rc = TLC_ERR_CUDA;
+    if (rc != TLC_OK) return rc;
+    // capacity offsets of the contexts in owner-major (header) order
+    std::vector<uint64_t> cap(C);
+    for (int o = 0; o < W; o++)
+        for (int q = 0; q < (int)x->owned[o].size(); q++) {
+            const Ctx &c = x->ctx[x->owned[o][q]];
+            cap[x->hdr_start[o] + q] = x->region_start[o] + c.region_off;
+        }
+    if (C) rc = cuda_ok(cudaMemcpy(x->d_pk + 2 * C + 1, cap.data(), C * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    return rc;
+}
+
+// pack `count` contexts whose headers are hdr[0..count) and whose capacity offsets in `src`
+// are cap[0..count); all-gather the offsets; wait for them on the host (h_all)
+static int exact_pack_gather(tlc_exchange *x, const tlc_header *hdr, const uint64_t *cap, const uint8_t *src,
+                             int count, cudaStream_t st) {
+    const int C = (int)x->ctx.size();
+    uint64_t *off = x->d_pk, *len = x->d_pk + C + 1;
+    tlc_pack_offsets_kernel<<<1, 32, 0, st>>>(hdr, count, off, len);
+    if (count)
+        tlc_copy_items_kernel<<<std::min(count, num_sms() * 4), 256, 0, st>>>(src, cap, x->pack, off, len, count);
+    int rc = cuda_ok(cudaPeekAtLastError());
+    if (rc == TLC_OK) rc = nccl_ok(ncclAllGather(off, x->d_all, C + 1, ncclUint64, x->comm->nccl, st));
+    if (rc == TLC_OK)
+        rc = cuda_ok(cudaMemcpyAsync(x->h_all, x->d_all, (size_t)x->W * (C + 1) * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, st));
+    if (rc == TLC_OK) rc = cuda_ok(cudaStreamSynchronize(st));   // the counts are host arguments
+    return rc;
+}
+
+// unpack items: (src offset in pack_recv, dst offset in dst_base, length)
+static int exact_unpack(tlc_exchange *x, uint8_t *dst_base, cudaStream_t st) {
+    const int k = (int)(x->h_items.size() / 3);
+    if (!k) return TLC_OK;
+    int rc = cuda_ok(cudaMemcpyAsync(x->d_items, x->h_items.data(), x->h_items.size() * sizeof(uint64_t),
+                                     cudaMemcpyHostToDevice, st));
+    if (rc != TLC_OK) return rc;
+    tlc_copy_items_kernel<<<std::min(k, num_sms() * 4), 256, 0, st>>>(x->pack_recv, x->d_items, dst_base,
+                                                                      x->d_items + k, x->d_items + 2 * k, k);
+    return cuda_ok(cudaPeekAtLastError());
+}
+
+static int exact_push(tlc_exchange *x, cudaStream_t st) {
+    const int W = x->W, C = (int)x->ctx.size(), me = x->me, nown = (int)x->owned[me].size();
+    int rc = exact_pack_gather(x, x->push_hdr_send, x->d_pk + 2 * C + 1, x->push_send, C, st);
+    if (rc != TLC_OK) return rc;
+    const uint64_t *mine = x->h_all + (size_t)me * (C + 1);
+    ncclComm_t nc = x->comm->nccl;
+    uint64_t recvd = 0;
+    if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
+    for (int o = 0; o < W; o++) {
+        const int f = (int)x->hdr_start[o], no = (int)x->owned[o].size();
+        if (!no) continue;
+        const uint64_t b = mine[f + no] - mine[f];
+        if (b) ncclSend(x->pack + mine[f], b, ncclUint8, o, nc, st);
+        ncclSend(x->push_hdr_send + f, no * sizeof(tlc_header), ncclUint8, o, nc, st);
+    }
+    if (nown) {
+        const int f = (int)x->hdr_start[me];
+        for (int w = 0; w < W; w++) {
+            const uint64_t *ow = x->h_all + (size_t)w * (C + 1);
+            const uint64_t b = ow[f + nown] - ow[f];
+            if (b) ncclRecv(x->pack_recv + (size_t)w * x->max_region, b, ncclUint8, w, nc, st);
+            ncclRecv(x->push_hdr_recv + (size_t)w * nown, nown * sizeof(tlc_header), ncclUint8, w, nc, st);
+            if (w != me) recvd += b + nown * sizeof(tlc_header);
+        }
+    }
+    if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
+    x->last_recv[0] = recvd;
+    // unpack every sender's payloads of my contexts into the capacity layout of push_recv
+    x->h_items.clear();
+    if (nown) {
+        const int f = (int)x->hdr_start[me];
+        std::vector<uint64_t> so, dof, ln;
+        for (int w = 0; w < W; w++) {
+            const uint64_t *ow = x->h_all + (size_t)w * (C + 1);
+            for (int q = 0; q < nown; q++) {
+                const uint64_t l = ow[f + q + 1] - ow[f + q];
+                if (!l) continue;
+                so.push_back((size_t)w * x->max_region + (ow[f + q] - ow[f]));
+                dof.push_back((size_t)w * x->region_bytes[me] + x->ctx[x->owned[me][q]].region_off);
+                ln.push_back(l);
+            }
+        }
+        x->h_items = so;
+        x->h_items.insert(x->h_items.end(), dof.begin(), dof.end());
+        x->h_items.insert(x->h_items.end(), ln.begin(), ln.end());
+    }
+    return exact_unpack(x, x->push_recv, st);
+}
+
+static int exact_pull(tlc_exchange *x, cudaStream_t st) {
+    const int W = x->W, C = (int)x->ctx.size(), me = x->me, nown = (int)x->owned[me].size();
+    const int fme = (int)x->hdr_start[me];
+    int rc = exact_pack_gather(x, x->pull_hdr + fme, x->d_pk + 2 * C + 1 + fme, x->pull_buf, nown, st);
+    if (rc != TLC_OK) return rc;
+    ncclComm_t nc = x->comm->nccl;
+    const uint64_t mine = x->h_all[(size_t)me * (C + 1) + nown];
+    uint64_t recvd = 0;
+    if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;
+    for (int o = 0; o < W; o++) {
+        if (o == me) continue;
+        const int no = (int)x->owned[o].size();
+        if (nown) {
+            if (mine) ncclSend(x->pack, mine, ncclUint8, o, nc, st);
+            ncclSend(x->pull_hdr + fme, nown * sizeof(tlc_header), ncclUint8, o, nc, st);
+        }
+        if (no) {
+            const uint64_t b = x->h_all[(size_t)o * (C + 1) + no];
+            if (b) ncclRecv(x->pack_recv + (size_t)o * x->max_region, b, ncclUint8, o, nc, st);
+            ncclRecv(x->pull_hdr + x->hdr_start[o], no * sizeof(tlc_header), ncclUint8, o, nc, st);
+            recvd += b + no * sizeof(tlc_header);
+        }
+    }
+    if ((rc = nccl_ok(ncclGroupEnd())) != TLC_OK) return rc;
+    x->last_recv[1] = recvd;
+    // unpack every owner's shared pull payloads into the capacity layout of pull_buf
+    std::vector<uint64_t> so, dof, ln;
+    for (int o = 0; o < W; o++) {
+        if (o == me) continue;
+        const uint64_t *oo = x->h_all + (size_t)o * (C + 1);
+        for (int q = 0; q < (int)x->owned[o].size(); q++) {
+            const uint64_t l = oo[q + 1] - oo[q];
+            if (!l) continue;
+            so.push_back((size_t)o * x->max_region + oo[q]);
+            dof.push_back(x->region_start[o] + x->ctx[x->owned[o][q]].region_off);
+            ln.push_back(l);
+        }
+    }
+    x->h_items = so;
+    x->h_items.insert(x->h_items.end(), dof.begin(), dof.end());
+    x->h_items.insert(x->h_items.end(), ln.begin(), ln.end());
+    return exact_unpack(x, x->pull_buf, st);
+}
+
 extern "C" {
+
+int tlc_exchange_set_transport(tlc_exchange *x, int mode) {
+    // NCCL transports: 0 = capacity regions (no host sync), 1 = exact payload bytes after a
+    // sizes all-gather (one host sync per direction).  Not for peer-memory or loopback.
+    if (!x || x->p2p || x->comm->loopback || (mode != 0 && mode != 1) || x->phase != 0) return TLC_ERR_ARG;
+    if (mode == 1 && !x->pack) {
+        const int rc = exact_alloc(x);
+        if (rc != TLC_OK) return rc;
+    }
+    x->exact = mode;
+    return TLC_OK;
+}
 
 int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int use_zre, void *stream) {
     if (!x || !grads || !(s >= 1.0f && s < 2.0f) || x->comm->loopback) return TLC_ERR_ARG;
@@ -672,6 +893,8 @@ int tlc_exchange_push(tlc_exchange *x, const float *const *grads, float s, int u
         // peer memory: no copy -- once every rank's pushes are written, the owner's
         // scan and aggregation kernels read them from the producing GPU over NVLink
         if ((rc = flag_barrier(x, 0, st)) != TLC_OK) return rc;
+    } else if (x->exact) {
+        if ((rc = exact_push(x, st)) != TLC_OK) return rc;
     } else {
         const int nown = (int)x->owned[x->me].size();
         const size_t own_region = x->region_bytes[x->me];
@@ -706,6 +929,8 @@ int tlc_exchange_pull(tlc_exchange *x, float *const *outs, float s, int use_zre,
     // in peer-memory mode a barrier, then the apply kernels read the owners' regions
     if (x->p2p) {
         if ((rc = flag_barrier(x, 1, st)) != TLC_OK) return rc;
+    } else if (x->exact) {
+        if ((rc = exact_pull(x, st)) != TLC_OK) return rc;
     } else {
         ncclComm_t nc = x->comm->nccl;
         if ((rc = nccl_ok(ncclGroupStart())) != TLC_OK) return rc;

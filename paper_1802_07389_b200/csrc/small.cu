@@ -550,22 +550,25 @@ static bool coop_enabled() {
 // A tensor's decode is split into parts of kSmPart quartic positions, one CTA each (the
 // 36,864-value ResNet-110 tensors would otherwise keep one SM busy while most idle): every
 // part scans the whole payload (<= P bytes, on chip) and expands / decodes only its range.
-constexpr uint32_t kSmPart = 2048;
+constexpr uint32_t kSmPart = (uint32_t)kT5;   // the K5 tile: parts are numbered like K5's tiles (Seg::k5)
 
 template <int kMode>
 __global__ void __launch_bounds__(kSmThreads)
-tlc_small_decompress_kernel(const SegTable T, uint32_t parts) {
+tlc_small_decompress_kernel(const SegTable T) {
     extern __shared__ __align__(16) uint8_t sm_raw[];
     __shared__ uint16_t dig[256];                                // digit_i(b) at bits 2i
     __shared__ uint32_t s_wsum[kSmWarps + 1];
     __shared__ int s_bad;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t items = (uint64_t)T.count * parts;
+    // exactly the parts that exist (K5's tile numbering): no CTA for the empty parts of the
+    // smaller tensors (round 1 launched count x max-parts CTAs, most of them idle)
+    __shared__ uint64_t s_first[kSegCache];
+    seg_index_load<5>(T, s_first);
     bool table = false;
-    for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
-        const int si = (int)(item / parts);
-        const uint32_t part = (uint32_t)(item % parts);
+    for (uint64_t item = blockIdx.x; item < T.n5; item += gridDim.x) {
+        const int si = find_seg_c<5>(T, item, s_first);
         const Seg S = get_seg(T, si);
+        const uint32_t part = (uint32_t)(item - S.k5);
         tlc_header *hdr = S.hdr;
         const uint32_t jr0 = part * kSmPart;
         if (jr0 >= S.P) continue;                                // no positions in this part
@@ -745,11 +748,10 @@ int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
         attr = true;
     }
     KernelScope ks(kK7s, st);
-    const uint32_t parts = (uint32_t)(((T.max_n + 4) / 5 + kSmPart - 1) / kSmPart);
-    const int grid = (int)tmin<uint64_t>((uint64_t)T.count * parts, 65535);
+    const int grid = (int)tmin<uint64_t>(T.n5, 65535);
     const size_t smem = small_smem_decompress(T.max_n);
-    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T, parts);
-    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T, parts);
+    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T);
+    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 

@@ -6,6 +6,9 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#ifdef TLC_DEVICE_CHECKS
+#include <cstdio>
+#endif
 
 #include "../../include/tlc.h"
 #include "tlc_launch.h"
@@ -17,7 +20,6 @@ namespace tlc {
 // data-dependent store index are asserted on the device; a violation prints its site and
 // traps.  compute-sanitizer is not available on the GPU pool this was built on.
 #ifdef TLC_DEVICE_CHECKS
-#include <cstdio>
 #define TLC_CHECK(c)                                                                      \
     do {                                                                                  \
         if (!(c)) {                                                                       \
@@ -425,7 +427,8 @@ __host__ __device__ __forceinline__ uint32_t lane_emit_bytes(const uint32_t (&w)
 //  1  a word of four literals with nothing pending is stored as a unit, other words go
 //     byte by byte (divergent: a warp runs both paths when its lanes differ);
 //  2  simple lanes: one running offset, predicated byte stores (a serial add chain);
-//  3  simple lanes: every byte's offset from popcounts of the masks below it (no chain).
+//  3  simple lanes: every byte's offset from popcounts of the masks below it (no chain);
+//  4  variant 1 for simple lanes without the division (pending zero groups < 14).
 #ifndef TLC_EMIT_V
 #define TLC_EMIT_V 1
 #endif
@@ -461,6 +464,34 @@ __host__ __device__ __forceinline__ uint32_t lane_emit(const uint32_t (&w)[8], u
         return o;
     }
     if (!lane_simple(mask, carry_in)) return lane_emit_bytes(w, mask, carry_in, dst, o);
+    if (V == 4) {
+        // variant 1's word fast path; simple lanes never hold 14 pending zero groups, so a
+        // flush is one code of the pending count c (< 14), no division
+        uint32_t c = carry_in;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t mk = (mask >> (4 * k)) & 0xfu;
+            if (mk == 0xfu && c == 0) {
+                dst[o] = (uint8_t)w[k];
+                dst[o + 1] = (uint8_t)(w[k] >> 8);
+                dst[o + 2] = (uint8_t)(w[k] >> 16);
+                dst[o + 3] = (uint8_t)(w[k] >> 24);
+                o += 4;
+                continue;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if ((mk >> q) & 1u) {
+                    if (c) dst[o++] = run_code(c);
+                    c = 0;
+                    dst[o++] = (uint8_t)(w[k] >> (8 * q));
+                } else {
+                    c++;
+                }
+            }
+        }
+        return o;
+    }
     // code flags: a literal whose previous byte is a zero group, or the lane's first
     // byte when zero groups are pending from before the lane
     const uint32_t cf = mask & ((~mask << 1) | (carry_in ? 1u : 0u));

@@ -33,7 +33,7 @@ def _grads(r, step, sizes=SIZES, kind="gauss"):
     return [synth.gaussian(n, 95, r, t, step) for t, n in enumerate(sizes)]
 
 
-def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False, kind="gauss"):
+def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False, kind="gauss", exact=False):
     """One rank's exchange; returns per-step means (owned flat) and final state.
     graph=True: step 0 runs eagerly (it uploads the descriptor tables), then push and
     pull are captured once as CUDA graphs over fixed gradient buffers and replayed."""
@@ -43,7 +43,7 @@ def _run_rank(rank, world, steps, sizes=SIZES, p2p=False, graph=False, kind="gau
 
     dev = torch.device("cuda", torch.cuda.current_device())
     comm = T.Comm(rank, world, dev)
-    x = T.Exchange(comm, sizes, p2p=p2p)
+    x = T.Exchange(comm, sizes, p2p=p2p, exact=exact)
     outs = [torch.zeros(n, device=dev) for n in sizes]
     gs = [torch.empty(n, device=dev) for n in sizes]
     owned_per_step = []
@@ -103,12 +103,13 @@ def _check(world, results, sizes=SIZES, steps=STEPS, kind="gauss"):
             assert np.array_equal(res["outs"][t].view(np.uint32), outs[r][t].view(np.uint32)), ("out", r, t)
 
 
-@pytest.mark.parametrize("p2p,graph", [(False, False), (True, False), (True, True)])
-def test_exchange_w1_in_process(p2p, graph):
+@pytest.mark.parametrize("p2p,graph,exact", [(False, False, False), (False, False, True), (True, False, False),
+                                            (True, True, False)])
+def test_exchange_w1_in_process(p2p, graph, exact):
     import torch
 
     assert torch.cuda.is_available()
-    _check(1, [_run_rank(0, 1, STEPS, p2p=p2p, graph=graph)])
+    _check(1, [_run_rank(0, 1, STEPS, p2p=p2p, graph=graph, exact=exact)])
 
 
 def test_exchange_w1_sparse_gradients():
@@ -117,7 +118,7 @@ def test_exchange_w1_sparse_gradients():
     _check(1, [_run_rank(0, 1, STEPS, p2p=True, kind="sparse")], kind="sparse")
 
 
-def _mp_worker(rank, world, port, q, p2p, graph=False, kind="gauss"):
+def _mp_worker(rank, world, port, q, p2p, graph=False, kind="gauss", exact=False):
     import torch
     import torch.distributed as dist
 
@@ -125,16 +126,17 @@ def _mp_worker(rank, world, port, q, p2p, graph=False, kind="gauss"):
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
-        res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph, kind=kind)
+        res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph, kind=kind, exact=exact)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("p2p,graph,kind", [(False, False, "gauss"), (True, False, "gauss"), (True, True, "gauss"),
-                                            (True, False, "sparse")])
+@pytest.mark.parametrize("p2p,graph,kind,exact", [(False, False, "gauss", False), (False, False, "sparse", True),
+                                                  (True, False, "gauss", False), (True, True, "gauss", False),
+                                                  (True, False, "sparse", False)])
 @pytest.mark.parametrize("world", [2, 4])
-def test_exchange_multi_gpu(world, p2p, graph, kind):
+def test_exchange_multi_gpu(world, p2p, graph, kind, exact):
     import torch
     import torch.multiprocessing as mp
 
@@ -146,7 +148,7 @@ def test_exchange_multi_gpu(world, p2p, graph, kind):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph, kind)) for r in range(world)]
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph, kind, exact)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
