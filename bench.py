@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--model", default="bert-large", help="tensor list of the exchange workload")
     ap.add_argument("--xs", type=float, default=1.9, help="s of the exchange workload (configs[4])")
     ap.add_argument("--no-xchg-w1", action="store_true", help="skip the N=1 exchange side measurement")
-    ap.add_argument("--xchg", choices=["p2p", "nccl"], default="p2p",
-                    help="exchange transport: peer-memory kernels over NVLink, or NCCL send/recv")
+    ap.add_argument("--xchg", choices=["p2p", "nccl", "nccl-exact"], default="p2p",
+                    help="exchange transport: peer-memory kernels over NVLink, NCCL send/recv of capacity "
+                         "regions, or NCCL with a sizes all-gather and exact payload bytes")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the C3 families / s grid / 2^20..2^30 size sweep side measurement")
@@ -512,7 +513,7 @@ def measure_codecs(T, dev, ts, steps=20, warmup=3):
             "steps": steps, "designs": res}
 
 
-def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True, e2e_steps=0):
+def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2p=True, e2e_steps=0, exact=False):
     """BASELINE configs[4]: the model's ndim>=2 gradient tensors exchanged through
     the parameter-server push/pull (tlc_exchange_push + tlc_exchange_pull, delta =
     mean) on `world` ranks; every rank holds its own full state change (weak
@@ -526,7 +527,7 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2
     grads = [synth.model_step_torch(model, k, rank, dev) for k in range(2)]
     outs = [torch.zeros(n, dtype=torch.float32, device=dev) for n in sizes]
     comm = T.Comm(rank, world, dev)
-    x = T.Exchange(comm, sizes, p2p=p2p)
+    x = T.Exchange(comm, sizes, p2p=p2p, exact=exact)
     stream = torch.cuda.current_stream(dev)
 
     def step(k):
@@ -707,7 +708,7 @@ def run_exchange_leg(args, T, dev, world, rank, dist, e2e_steps=None):
     import torch
 
     r = measure_exchange(T, dev, world, rank, args.model, args.xs, args.steps, args.warmup,
-                         dist if world > 1 else None, p2p=args.xchg == "p2p",
+                         dist if world > 1 else None, p2p=args.xchg == "p2p", exact=args.xchg == "nccl-exact",
                          e2e_steps=e2e_steps if e2e_steps is not None else (0 if args.no_e2e else args.e2e_steps))
     ms = r["ms"]
     ems = r["e2e"]["ms"] if r["e2e"] else None
@@ -1024,7 +1025,10 @@ def run_exchange_main(args, T, dev, world, rank, dist):
                                    f"(owner compresses once, every rank applies) at s={args.xs}, "
                                    f"{r['N']:,} values per rank; transport: "
                                    + ("kernels read peers' payloads over NVLink (CUDA IPC), flag barriers"
-                                      if args.xchg == "p2p" else "NCCL grouped send/recv"),
+                                      if args.xchg == "p2p" else
+                                      "NCCL sizes all-gather + grouped send/recv of exact payload bytes"
+                                      if args.xchg == "nccl-exact" else
+                                      "NCCL grouped send/recv of capacity regions"),
                        "n_per_rank": r["N"], "s": args.xs, "contexts": r["contexts"],
                        "l2": "inputs larger than L2 (1.34 GB of state changes per rank); no flush",
                        "parallelism": f"ps{world} (sharded parameter server, {args.xchg})"},
