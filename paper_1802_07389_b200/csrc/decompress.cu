@@ -654,8 +654,14 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
 // (sequential: 0.242 / 0.192 / 0.202; profiles/r02n_loopback.txt).
 // The fold (rank order from +0, skip-zero, IEEE / W, R15; NaN for a failed source, R24)
 // is the same as above.
+// 4 CTAs/SM where shared memory allows it (W <= 4): per owner 0.180 -> 0.168 ms at W = 2,
+// 0.099 -> 0.093 at W = 4 (loopback, profiles/r02y_k5m_minb_ab.txt); W = 8 is held to 3 by its
+// shared memory either way
+#ifndef TLC_K5P_MINB
+#define TLC_K5P_MINB 4
+#endif
 template <int WP>
-__global__ void __launch_bounds__(kK5Threads, 3)
+__global__ void __launch_bounds__(kK5Threads, WP == 8 ? 3 : TLC_K5P_MINB)
 tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
     constexpr int TP = kK5Threads / WP;                  // threads per source
     extern __shared__ __align__(16) uint8_t smem_raw[];

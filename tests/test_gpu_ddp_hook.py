@@ -130,3 +130,42 @@ def test_ddp_hook_nonfinite_gradient_is_nan_on_every_rank(batch):
     if torch.cuda.device_count() < world:
         pytest.skip("needs 2 GPUs")
     _oracle_check(_launch(world, True, batch, nan_step=1), world, batch, nan_step=1)
+
+
+@pytest.mark.parametrize("batch", [False, True])
+def test_ddp_hook_world1_on_one_gpu(batch):
+    """The hook's code path on one GPU (DDP with a world of 1, NCCL process group): every
+    bucket's reduced gradient equals the oracle's W = 1 exchange of it (compress, decompress as
+    the mean, shared pull), step after step with the error buffers carried; the batched schedule
+    exchanges all buckets of a step together."""
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_worker, args=(0, 1, port, q, True, batch, -1))
+    p.start()
+    r, rec, params = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    from oracle import exchange as X
+
+    assert len(rec) == STEPS
+    ps = {}
+    for step, bs in enumerate(rec):
+        groups = [sorted(bs, key=lambda e: e[0])] if batch else [[e] for e in bs]
+        for grp in groups:
+            sizes = tuple(b[1].size for b in grp)
+            key = sizes if batch else grp[0][0]
+            if key not in ps or ps[key][0] != sizes:
+                ps[key] = (sizes, X.VirtualPS(list(sizes), 1))
+            vp = ps[key][1]
+            means, _ = vp.push([[b[1].astype(np.float32) for b in grp]], S)
+            outs = [[np.zeros(n, np.float32) for n in sizes]]
+            vp.pull(means, outs, S)
+            for k, b in enumerate(grp):
+                assert np.array_equal(b[2].view(np.uint32), outs[0][k].view(np.uint32)), (step, b[0])
+    assert all(np.isfinite(a).all() for a in params)
