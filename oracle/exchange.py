@@ -58,9 +58,11 @@ class VirtualPS:
     """State of a W-rank exchange: push error buffers per (rank, context), pull error
     buffers per context (held by its owner)."""
 
-    def __init__(self, sizes, W):
+    def __init__(self, sizes, W, ctx=None):
+        """ctx: an explicit list of (tensor, lo, hi, owner) contexts instead of plan(sizes, W)
+        (tests replay a few contexts of a large plan on their own: contexts are independent)."""
         self.sizes, self.W = [int(n) for n in sizes], W
-        self.ctx = plan(self.sizes, W)
+        self.ctx = [tuple(c) for c in ctx] if ctx is not None else plan(self.sizes, W)
         self.push_err = [[np.zeros(hi - lo, f32) for (_, lo, hi, _) in self.ctx] for _ in range(W)]
         self.pull_err = [np.zeros(hi - lo, f32) for (_, lo, hi, _) in self.ctx]
 

@@ -162,3 +162,61 @@ def test_loopback_phase_order_and_arguments():
         g.ranks[0].push(gs[0], 1.5)                       # a virtual rank is driven by its group
     torch.cuda.synchronize()
     g.close()
+
+
+def test_loopback_bert_large_full_size_sampled():
+    """The bench's exchange workload at full size (BASELINE configs[4]: BERT-large, 150 tensors,
+    335,869,952 values per rank, s = 1.9) with W = 4 virtual ranks, two steps: every rank's
+    outputs bitwise identical (the shared pull), and for five sampled contexts (the largest, the
+    smallest and three random) every rank's push error, the owner's mean, pull error and every
+    rank's output equal to the oracle replaying those contexts alone (contexts are independent:
+    X2-X6 per context)."""
+    import torch
+
+    import paper_1802_07389_b200 as T
+    import synth
+    from oracle import exchange as X
+
+    W, s, steps = 4, 1.9, 2
+    dev = torch.device("cuda", 0)
+    sizes = synth.BERT_LARGE_SIZES
+    g = T.Loopback(W, sizes, dev)
+    ctxs = g.ranks[0].contexts()
+    rng = np.random.default_rng(11)
+    lens = [c["hi"] - c["lo"] for c in ctxs]
+    pick = sorted({int(np.argmax(lens)), int(np.argmin(lens)), *rng.choice(len(ctxs), 3, replace=False).tolist()})
+    sub = [(k, 0, lens[c], ctxs[c]["owner"]) for k, c in enumerate(pick)]
+    ps = X.VirtualPS([lens[c] for c in pick], W, ctx=sub)
+    outs = [[torch.zeros(n, device=dev) for n in sizes] for _ in range(W)]
+    ref_outs = [[np.zeros(lens[c], f32) for c in pick] for _ in range(W)]
+    for step in range(steps):
+        grads = [synth.model_step_torch("bert-large", step, r, dev) for r in range(W)]
+        g.push(grads, s)
+        torch.cuda.synchronize()
+        sub_grads = [[grads[r][ctxs[c]["tensor"]][ctxs[c]["lo"]:ctxs[c]["hi"]].cpu().numpy() for c in pick]
+                     for r in range(W)]
+        means, _ = ps.push(sub_grads, s)
+        for k, c in enumerate(pick):
+            o = ctxs[c]["owner"]
+            oo = g.ranks[o].contexts()[c]["owned_off"]
+            m = g.ranks[o].owned[oo: oo + lens[c]].cpu().numpy()
+            assert np.array_equal(m.view(np.uint32), means[k].view(np.uint32)), ("mean", step, c)
+        g.pull(outs, s)
+        torch.cuda.synchronize()
+        ps.pull(means, ref_outs, s)
+        del grads
+    for r in range(1, W):
+        for t in range(len(sizes)):
+            assert torch.equal(outs[r][t].view(torch.int32), outs[0][t].view(torch.int32)), (r, t)
+    for k, c in enumerate(pick):
+        cx = ctxs[c]
+        for r in range(W):
+            pe = g.ranks[r].push_err[cx["elem_off"]: cx["elem_off"] + lens[c]].cpu().numpy()
+            assert np.array_equal(pe.view(np.uint32), ps.push_err[r][k].view(np.uint32)), ("push_err", r, c)
+            o = outs[r][cx["tensor"]][cx["lo"]: cx["hi"]].cpu().numpy()
+            assert np.array_equal(o.view(np.uint32), ref_outs[r][k].view(np.uint32)), ("out", r, c)
+        own = g.ranks[cx["owner"]]
+        oo = own.contexts()[c]["owned_off"]
+        pl = own.pull_err[oo: oo + lens[c]].cpu().numpy()
+        assert np.array_equal(pl.view(np.uint32), ps.pull_err[k].view(np.uint32)), ("pull_err", c)
+    g.close()
