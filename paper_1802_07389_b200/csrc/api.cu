@@ -82,6 +82,9 @@ int tlc_stoch_compress(const float *t, uint64_t n, uint64_t seed, uint64_t step,
                        uint64_t payload_cap, tlc_header *hdr, void *ws, size_t ws_bytes, void *stream) {
     if (!t || !payload || !hdr || !ws || n == 0) return TLC_ERR_ARG;
     if (n >= (1ull << 42)) return TLC_ERR_ARG;
+    if (overlap(payload, payload_cap, t, 4 * n) || overlap(hdr, sizeof(tlc_header), t, 4 * n) ||
+        overlap(hdr, sizeof(tlc_header), payload, payload_cap))
+        return TLC_ERR_ARG;
     if (payload_cap < tlc_max_payload_bytes(n)) return TLC_ERR_CAPACITY;
     if (ws_bytes < compress_workspace_bytes(n)) return TLC_ERR_CAPACITY;
     if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return TLC_ERR_ARG;
@@ -101,6 +104,9 @@ int tlc_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr
                       void *stream) {
     if (!t || !codes || !hdr || !ws || n == 0) return TLC_ERR_ARG;
     if (n >= (1ull << 42)) return TLC_ERR_ARG;
+    if (overlap(codes, n, t, 4 * n) || overlap(hdr, sizeof(tlc_header), t, 4 * n) ||
+        overlap(hdr, sizeof(tlc_header), codes, n))
+        return TLC_ERR_ARG;
     if (ws_bytes < tlc_int8_workspace_bytes(n)) return TLC_ERR_CAPACITY;
     if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return TLC_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(hdr) & 7u) != 0) return TLC_ERR_ARG;

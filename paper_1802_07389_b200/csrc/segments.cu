@@ -92,7 +92,7 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
             return TLC_ERR_CUDA;
         for (int k = 0; k < 5; k++) T.first[k] = d_first + (size_t)k * cnt;
     }
-    if (with_scratch && cnt > 1 && T.max_n <= kSmallMaxN) {
+    if (with_scratch && cnt > 1 && T.max_n <= kSmallMaxN && small_coop_enabled()) {
         const int rc = small_plan_build(T, host, &d_small, sl_layout);
         if (rc != TLC_OK) return rc;
     }

@@ -538,7 +538,7 @@ int small_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const st
 
 // K6c is opt-in (TLC_COOP=1): on the ResNet-110 table it measured 31 us against K6's 22 us
 // (tools/k6c_trace.py: every phase takes 3-5 us)
-static bool coop_enabled() {
+bool small_coop_enabled() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("TLC_COOP");
@@ -702,7 +702,7 @@ bool small_enabled() {
 bool small_table(const SegTable &T) { return T.max_n <= kSmallMaxN && small_enabled(); }
 
 int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st) {
-    if (T.sl && coop_enabled()) {
+    if (T.sl && small_coop_enabled()) {
         static bool cattr = false;
         if (!cattr) {
             int dev = 0, optin = 0;

@@ -193,6 +193,7 @@ int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t 
 
 // Small tensors (small.cu): one CTA per tensor, one launch per direction.
 bool small_enabled();
+bool small_coop_enabled();   // TLC_COOP=1: small tables take K6c (its plan is only built then)
 bool small_table(const SegTable &T);
 // K6c plan of a small table (slices, CTA runs, state); leaves T.sl null when the table does
 // not fit one cooperative wave (K6, one CTA per tensor, then runs instead)
