@@ -4,6 +4,7 @@ kernel's share of the step, and profiles/ncu_traffic.json (read by bench.py for
 roofline.traffic).
 
   python tools/launch_summary.py gpurun_out/launches.csv <first-id> <last-id> <out-prefix>
+  (first-id -1: the last two steps of the list)
 
 The ids select whole compress+decompress steps of the C3 tensor (n = 2^28)."""
 import collections
@@ -27,6 +28,9 @@ def main(path, lo, hi, prefix):
             continue
         d = launch.setdefault(int(r[ii]), {"name": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", ""))
+    if lo < 0:                        # "auto": the last two C3 steps (from the second-last K1 on)
+        k1 = [i for i, d in launch.items() if d["name"].split("(")[0].split("::")[-1].split("<")[0] == "tlc_absmax_kernel"]
+        lo, hi = k1[-2], max(launch)
     sel = [(i, d) for i, d in launch.items() if lo <= i <= hi]
     agg = collections.OrderedDict()
     out_rows = []
