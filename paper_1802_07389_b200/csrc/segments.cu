@@ -92,6 +92,10 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
             return TLC_ERR_CUDA;
         for (int k = 0; k < 5; k++) T.first[k] = d_first + (size_t)k * cnt;
     }
+    if (T.max_n <= kSmallMaxN) {
+        const int rc = small_group_plan_build(T, host, &d_grp, grp_layout);
+        if (rc != TLC_OK) return rc;
+    }
     if (with_scratch && cnt > 1 && T.max_n <= kSmallMaxN && small_coop_enabled()) {
         const int rc = small_plan_build(T, host, &d_small, sl_layout);
         if (rc != TLC_OK) return rc;
@@ -139,6 +143,10 @@ int Table::upload() {
         const int rc = small_plan_refresh(T, host, sl_layout);   // the slices carry the pointers
         if (rc != TLC_OK) return rc;
     }
+    if (T.grp) {
+        const int rc = small_group_plan_refresh(T, host, grp_layout);
+        if (rc != TLC_OK) return rc;
+    }
     return cudaMemcpy(d, host.data(), host.size() * sizeof(Seg), cudaMemcpyHostToDevice) == cudaSuccess
                ? TLC_OK : TLC_ERR_CUDA;
 }
@@ -163,6 +171,8 @@ void Table::release() {
     if (own_ws && ws) cudaFree(ws);
     if (d_small) cudaFree(d_small);
     d_small = nullptr;
+    if (d_grp) cudaFree(d_grp);
+    d_grp = nullptr;
     d = nullptr;
     ws = nullptr;
 }

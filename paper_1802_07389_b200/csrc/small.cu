@@ -20,6 +20,7 @@
 //
 // Same results, byte for byte, as the large path (the payload, err, header and output
 // are defined by the method, not by the kernels).
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -45,6 +46,26 @@ __device__ __forceinline__ unsigned int block_max(unsigned int m, unsigned int *
     __syncthreads();
     return s_red[kSmWarps];
 }
+
+#ifdef TLC_K6C_TRACE
+// development instrumentation: %globaltimer at the phase boundaries of every CTA (K6, K6x, K6c)
+__device__ unsigned long long g_k6c_trace[1024][8];
+#define K6C_TRACE(slot)                                                                     \
+    do {                                                                                    \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                        \
+            unsigned long long t_;                                                          \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+            g_k6c_trace[blockIdx.x][slot] = t_;                                             \
+            if (slot == 0) {                                                                \
+                unsigned int sm_;                                                           \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                           \
+                g_k6c_trace[blockIdx.x][7] = sm_;                                           \
+            }                                                                               \
+        }                                                                                   \
+    } while (0)
+#else
+#define K6C_TRACE(slot) do {} while (0)
+#endif
 
 template <class QT>
 __device__ __forceinline__ void small_quantize(const Seg &S, const float *u, uint8_t *dst, const QT &Q) {
@@ -75,6 +96,7 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
     __shared__ uint32_t s_off[kSmWarps + 1], s_carry[kSmWarps + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int si = blockIdx.x; si < T.count; si += gridDim.x) {
+        K6C_TRACE(0);
         const Seg S = get_seg(T, si);
         const uint32_t n = (uint32_t)S.n, P = (uint32_t)S.P;
         float *u = reinterpret_cast<float *>(sm_raw);
@@ -114,6 +136,7 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
             m = max(m, __float_as_uint(x) & 0x7fffffffu);
         }
         m = block_max(m, s_red);                                 // also orders the u stores
+        K6C_TRACE(1);
         float M;
         const unsigned int status = scale_from_key(m, s, M);     // Eq. 1, R6
         if (threadIdx.x == 0) {
@@ -133,6 +156,7 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
         else small_quantize(S, u, dst, Q);
         if (!use_zre) { __syncthreads(); continue; }
         __syncthreads();
+        K6C_TRACE(2);
         // ---- step (4): zero-run encoding, one warp per 1 KiB row
         const uint32_t nrows = (P + kK3WarpRowS - 1) / kK3WarpRowS;
         uint32_t w[8], mask = 0;
@@ -173,10 +197,12 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
             S.hdr->payload_len = s_off[nrows] + (s_carry[nrows] > 0);
         }
         __syncthreads();
+        K6C_TRACE(3);
         // full chunks (255) everywhere first; flush codes and literals overwrite
         const uint32_t total = s_off[nrows];
         for (uint32_t q = threadIdx.x; q < total; q += kSmThreads) S.payload[q] = 0xff;
         __syncthreads();
+        K6C_TRACE(4);
         if ((uint32_t)warp < nrows) {
             const WarpRow wr = warp_row(mask, len, lane_sum, s_carry[warp], row_len);
             uint32_t x = wr.count;
@@ -205,7 +231,494 @@ tlc_small_compress_kernel(const SegTable T, float s, int use_zre) {
         TLC_CHECK(!(threadIdx.x == 0 && s_carry[nrows] > 0) || total < P);
         if (threadIdx.x == 0 && s_carry[nrows] > 0) S.payload[total] = run_code(s_carry[nrows]);
         __syncthreads();                                         // shared memory reuse
+        K6C_TRACE(5);
     }
+}
+
+// ============================================================== K6g (clusters)
+// K6 with each tensor cut into slices of whole 1 KiB ZRE rows (at most kGRows rows, at most
+// CL slices), the slices of one tensor in one thread-block cluster of CL CTAs, several small
+// tensors sharing a cluster (host plan, small_group_plan_build).  One SM stores at most
+// ~61 GB/s and loads ~130-200 GB/s (profiles/r03l_sm_bw.txt), so the 36,864-value layers of
+// ResNet-110 (442 KB each) are too much for one CTA: K6's CTA spends 12 us on one of them
+// (profiles/r03k_trace.txt).  The group's CTAs exchange their max keys (cluster barrier 1)
+// and their ZRE run summaries (cluster barrier 2) by stores into each other's shared memory
+// (DSMEM) before the barriers, so nothing remote is touched after the second barrier and
+// every global store -- err, payload, header -- comes after it (a release barrier waits for
+// outstanding stores).  Same results bit for bit as K6.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store v into the same shared variable of CTA `rank` of this cluster
+__device__ __forceinline__ void dsmem_store_u64(unsigned long long *local, uint32_t rank, unsigned long long v) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_store_u32(unsigned int *local, uint32_t rank, unsigned int v) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+constexpr int kGThreads = 256;
+constexpr int kGWarps = kGThreads / 32;
+
+template <int NW>
+__device__ __forceinline__ unsigned int block_max_n(unsigned int m, unsigned int *s_red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) s_red[warp] = m;
+    __syncthreads();
+    if (warp == 0) {
+        m = __reduce_max_sync(0xffffffffu, lane < NW ? s_red[lane] : 0u);
+        if (lane == 0) s_red[NW] = m;
+    }
+    __syncthreads();
+    return s_red[NW];
+}
+
+// thread x < 40 of the 16-byte-aligned case: element (i, jj) of partition i's scalar head
+// (slots 0-3, up to the first 16-byte boundary) or tail (slots 4-7, after the float4 groups)
+__device__ __forceinline__ bool slice_edge(uint32_t x, uint32_t P, uint32_t j0, uint32_t len, uint32_t n,
+                                           uint32_t &i, uint32_t &jj) {
+    if (x >= 40) return false;
+    i = x >> 3;
+    const uint32_t r = x & 7, e0 = i * P + j0;
+    const uint32_t lim = e0 >= n ? 0u : min(len, n - e0);
+    const uint32_t hd = min((4u - (e0 & 3u)) & 3u, lim), body = hd + (lim - hd) / 4 * 4;
+    jj = r < 4 ? r : body + (r - 4);
+    return r < 4 ? r < hd : jj < lim;
+}
+
+template <class QT>
+__device__ __forceinline__ void slice_quantize(float *u, uint8_t *B, uint32_t j0, uint32_t len, uint32_t Ls,
+                                               const uint32_t (&sh)[5], uint32_t P, uint32_t n, const QT &Q) {
+    for (uint32_t jj = threadIdx.x; jj < len; jj += kGThreads) {
+        float x[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) x[i] = u[(uint32_t)i * Ls + sh[i] + jj];   // all five loads first
+        uint32_t b = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const bool in = (uint32_t)i * P + j0 + jj < n;
+            const int q = in ? Q.q(x[i]) : 0;                      // Eq. 2
+            x[i] = Q.residual(x[i], q);                            // steps (a), (b): u becomes err
+            b = b * 3u + (in ? (uint32_t)(q + 1) : 0u);            // steps 1, 4, 6; pad digit (R10)
+        }
+#pragma unroll
+        for (int i = 0; i < 5; i++) u[(uint32_t)i * Ls + sh[i] + jj] = x[i];
+        B[jj] = (uint8_t)b;
+    }
+}
+
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)),
+                 "r"(bytes) : "memory");
+}
+
+// plan record: GrpRec (tlc_launch.h).  BULK: t and err rows arrive by bulk copies (every
+// partition row of the slice in flight at once; one SM keeps ~40 KB in flight with
+// registers, profiles/r03o_trace.txt) into rows of Ls floats placed so that the 16-byte
+// aligned interiors land 16-byte aligned (row i starts at i*Ls + (e0_i & 3)), and err leaves
+// by bulk stores from the same rows.
+template <int CL, bool BULK>
+__global__ void __launch_bounds__(kGThreads, 2)
+tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
+    extern __shared__ __align__(16) uint8_t sm_raw[];
+    __shared__ unsigned int s_red[kGWarps + 1];
+    __shared__ unsigned long long s_row[kGWarps];
+    __shared__ uint32_t s_off[kGWarps + 1], s_carry[kGWarps + 1];
+    __shared__ unsigned int s_keys[CL];
+    __shared__ unsigned long long s_aggs[CL];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    K6C_TRACE(0);
+    const GrpRec S = T.grp[blockIdx.x];                        // one 64-byte record: no table walk
+    const bool idle = S.seg == ~0u;
+    const uint32_t g0 = S.g0, gcnt = S.gcnt, grank = S.grank;
+    const uint32_t n = S.n, P = S.P, j0 = S.j0, len = idle ? 0u : S.len;
+    const bool vec = aligned16(S.t) && aligned16(S.err);
+    const bool bulk = BULK && vec;
+    const uint32_t Ls = bulk ? ((len + 3) & ~3u) + 4 : len;   // floats per partition row
+    float *u = reinterpret_cast<float *>(sm_raw);             // u[i * Ls + sh_i + j - j0]
+    float *tt = u + 5 * Ls;                                    // BULK: T_in rows
+    uint8_t *B = reinterpret_cast<uint8_t *>(u + (bulk ? 10 : 5) * Ls);
+    B = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(B) + 15) & ~uintptr_t(15));
+    // ---- step (1): u = buffer + T_in of the slice into shared memory; its max key.
+    // Partition i of the slice is the global run [e0_i = i*P + j0, +lim_i): a scalar head up
+    // to a 16-byte boundary, float4 groups, a scalar tail.
+    unsigned int m = 0;
+    uint32_t hd[5], gc[5], sh[5], lim[5], gmax = 0;
+#pragma unroll
+    for (int i = 0; i < 5; i++) {
+        const uint32_t e0 = (uint32_t)i * P + j0;
+        lim[i] = e0 >= n ? 0u : min(len, n - e0);
+        sh[i] = bulk ? (e0 & 3u) : 0u;
+        hd[i] = vec ? min((4u - (e0 & 3u)) & 3u, lim[i]) : lim[i];
+        gc[i] = (lim[i] - hd[i]) / 4;
+        gmax = max(gmax, gc[i]);
+    }
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int i = 0; i < 5; i++) bytes += 32u * gc[i];
+            mbar_expect_tx(&s_mbar, bytes);
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+                if (gc[i]) {
+                    const uint32_t o = (uint32_t)i * Ls + sh[i] + hd[i], e = (uint32_t)i * P + j0 + hd[i];
+                    bulk_load(u + o, S.err + e, 16u * gc[i], &s_mbar);
+                    bulk_load(tt + o, S.t + e, 16u * gc[i], &s_mbar);
+                }
+        }
+        uint32_t jj, i;                                        // heads and tails (< 8 per row)
+        if (slice_edge(threadIdx.x - 32u, P, j0, len, n, i, jj)) {
+            const uint32_t e = i * P + j0 + jj, o = i * Ls + (((i * P + j0) & 3u)) + jj;
+            u[o] = __ldcs(S.err + e);
+            tt[o] = ld_stream(S.t + e);
+        }
+        mbar_wait(&s_mbar, 0);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 5; i++)
+            for (uint32_t jj = threadIdx.x; jj < lim[i]; jj += kGThreads) {
+                const uint32_t o = (uint32_t)i * Ls + sh[i] + jj;
+                const float x = __fadd_rn(u[o], tt[o]);
+                u[o] = x;
+                m = max(m, __float_as_uint(x) & 0x7fffffffu);
+            }
+    } else {
+        for (uint32_t k = threadIdx.x; k < gmax; k += kGThreads) {
+            float4 tv[5], ev[5];
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+                if (k < gc[i]) {
+                    const uint32_t g = ((uint32_t)i * P + j0 + hd[i]) / 4 + k;
+                    tv[i] = ld_stream4(reinterpret_cast<const float4 *>(S.t) + g);
+                    ev[i] = __ldcs(reinterpret_cast<const float4 *>(S.err) + g);
+                }
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+                if (k < gc[i]) {
+                    float *d = u + (uint32_t)i * Ls + hd[i] + 4 * k;
+                    d[0] = __fadd_rn(ev[i].x, tv[i].x); d[1] = __fadd_rn(ev[i].y, tv[i].y);
+                    d[2] = __fadd_rn(ev[i].z, tv[i].z); d[3] = __fadd_rn(ev[i].w, tv[i].w);
+                    m = max(m, max(max(__float_as_uint(d[0]) & 0x7fffffffu, __float_as_uint(d[1]) & 0x7fffffffu),
+                                   max(__float_as_uint(d[2]) & 0x7fffffffu, __float_as_uint(d[3]) & 0x7fffffffu)));
+                }
+        }
+        if (vec) {                                             // heads and tails: < 4 + 4 per partition
+            uint32_t jj, i;
+            if (slice_edge(threadIdx.x, P, j0, len, n, i, jj)) {
+                const uint32_t e = i * P + j0 + jj;
+                const float x = __fadd_rn(__ldcs(S.err + e), ld_stream(S.t + e));
+                u[i * Ls + jj] = x;
+                m = max(m, __float_as_uint(x) & 0x7fffffffu);
+            }
+        } else {
+            for (uint32_t i = 0; i < 5; i++) {
+                const uint32_t e0 = i * P + j0;
+                for (uint32_t jj = threadIdx.x; jj < lim[i]; jj += kGThreads) {
+                    const float x = __fadd_rn(__ldcs(S.err + e0 + jj), ld_stream(S.t + e0 + jj));
+                    u[i * Ls + jj] = x;
+                    m = max(m, __float_as_uint(x) & 0x7fffffffu);
+                }
+            }
+        }
+    }
+    m = block_max_n<kGWarps>(m, s_red);
+    K6C_TRACE(1);
+    // the key to every CTA of the group (its own copy included)
+    if (!idle && threadIdx.x < gcnt) dsmem_store_u32(&s_keys[grank], g0 + threadIdx.x, m);
+    cluster_sync_all();                                        // 1: the group's keys
+    K6C_TRACE(2);
+    if (idle) {
+        cluster_sync_all();
+        return;
+    }
+    for (uint32_t q = 0; q < gcnt; q++) m = max(m, s_keys[q]);
+    float M;
+    const unsigned int status = scale_from_key(m, s, M);      // Eq. 1, R6
+    const Quant Q(M);
+    // ---- Eq. 2, steps (a),(b) in shared memory (u becomes err), quartic steps 1-6
+    if (status == TLC_OK) {
+        if (Q.mode == 1) slice_quantize(u, B, j0, len, Ls, sh, P, n, QuantCmp(Q));
+        else slice_quantize(u, B, j0, len, Ls, sh, P, n, Q);
+        if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // u rows -> bulk stores
+    }
+    __syncthreads();
+    K6C_TRACE(3);
+    // ---- step (4): run summaries of the slice's rows (one warp per 1 KiB row)
+    const uint32_t nrows = (len + kK3WarpRowS - 1) / kK3WarpRowS;
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mask = 0;
+    int lenl = 0;
+    RunSum lane_sum = run_identity();
+    uint32_t row_len = 0;
+    if (status == TLC_OK && use_zre && (uint32_t)warp < nrows) {
+        const uint32_t base = (uint32_t)warp * kK3WarpRowS;
+        row_len = min(kK3WarpRowS, len - base);
+        const uint32_t rel = base + 32u * lane;
+        lenl = rel < len ? (int)min(32u, len - rel) : 0;
+        // 32 bytes per lane as two 16-byte loads (B is 16-byte aligned, padded by 32 bytes)
+        if (lenl > 0) {
+            const uint4 a = *reinterpret_cast<const uint4 *>(B + rel), b = *reinterpret_cast<const uint4 *>(B + rel + 16);
+            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        }
+        if (lenl < 32) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (4 * k + q >= lenl) w[k] = (w[k] & ~(0xffu << (8 * q))) | ((uint32_t)kZeroGroup << (8 * q));
+            }
+        }
+        mask = literal_mask(w);
+        lane_sum = mask_summary(mask, lenl);
+        const RunSum rs = warp_row_summary(mask, lenl, lane_sum, row_len);
+        if (lane == 0) s_row[warp] = pack(rs);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && use_zre && status == TLC_OK) {    // the slice's summary to the later slices
+        RunSum acc = run_identity();
+        for (uint32_t r = 0; r < nrows; r++) acc = compose(acc, unpack(s_row[r]));
+        const unsigned long long v = pack(acc);
+        for (uint32_t q = grank + 1; q < gcnt; q++) dsmem_store_u64(&s_aggs[grank], g0 + q, v);
+    }
+    K6C_TRACE(4);
+    cluster_sync_all();                                        // 2: the earlier slices' summaries
+    K6C_TRACE(5);
+    const bool last = grank + 1 == gcnt;                       // holds the tensor's last row
+    if (status != TLC_OK) {                                    // err untouched (R6)
+        if (grank == 0 && threadIdx.x == 0) {
+            S.hdr->M = M; S.hdr->flags = use_zre ? TLC_FLAG_ZRE : 0u; S.hdr->n = n;
+            S.hdr->payload_len = 0; S.hdr->status = status; S.hdr->reserved = 0;
+        }
+        return;
+    }
+    // the residuals (steps a, b) from shared memory to err first (bulk: in flight meanwhile)
+    if (bulk) {
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+                if (gc[i]) {
+                    const uint32_t o = (uint32_t)i * Ls + sh[i] + hd[i];
+                    bulk_store(S.err + (uint32_t)i * P + j0 + hd[i], u + o, 16u * gc[i]);
+                }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        uint32_t jj, i;
+        if (slice_edge(threadIdx.x - 32u, P, j0, len, n, i, jj))
+            __stcs(S.err + i * P + j0 + jj, u[i * Ls + ((i * P + j0) & 3u) + jj]);
+    }
+    if (!use_zre) {
+        for (uint32_t jj = threadIdx.x; jj < len; jj += kGThreads) S.payload[j0 + jj] = B[jj];
+    } else {
+        if (threadIdx.x == 0) {                                // rows in order: offset, carry
+            RunSum acc = run_identity();
+            for (uint32_t q = 0; q < grank; q++) acc = compose(acc, unpack(s_aggs[q]));
+            for (uint32_t r = 0; r <= nrows; r++) {
+                uint64_t o;
+                uint32_t c;
+                run_eval(acc, 0, o, c);
+                s_off[r] = (uint32_t)o;
+                s_carry[r] = c;
+                if (r < nrows) acc = compose(acc, unpack(s_row[r]));
+            }
+            if (last) S.hdr->payload_len = s_off[nrows] + (s_carry[nrows] > 0);
+        }
+        __syncthreads();
+        if ((uint32_t)warp < nrows) {
+            // every lane writes its whole output range [x - count, x): full chunks (255), flush
+            // codes and literals in order (no prefill pass, no block barrier)
+            const WarpRow wr = warp_row(mask, lenl, lane_sum, s_carry[warp], row_len);
+            uint32_t x = wr.count;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            uint8_t *out = S.payload + s_off[warp];
+            uint32_t o = x - wr.count, c = wr.carry_in;
+            int prev = -1;
+            for (uint32_t mk = mask; mk; mk &= mk - 1u) {
+                const int q = (int)ctz32(mk);
+                const uint32_t R = (uint32_t)(q - prev - 1) + c;
+                c = 0;
+                for (uint32_t f = R / kMaxRun; f; f--) out[o++] = 0xff;
+                TLC_CHECK(s_off[warp] + o + (R % kMaxRun ? 1 : 0) < P);
+                if (R % kMaxRun) out[o++] = run_code(R % kMaxRun);
+                uint32_t word = w[0];
+#pragma unroll
+                for (int k = 1; k < 8; k++) word = (k == (q >> 2)) ? w[k] : word;
+                out[o++] = (uint8_t)(word >> (8 * (q & 3)));
+                prev = q;
+            }
+            while (o < x) out[o++] = 0xff;                     // chunks completed in the trailing run
+        }
+        if (last && threadIdx.x == 0 && s_carry[nrows] > 0) {
+            TLC_CHECK(s_off[nrows] < P);
+            S.payload[s_off[nrows]] = run_code(s_carry[nrows]);
+        }
+    }
+    if (!bulk) {
+        for (uint32_t k = threadIdx.x; k < gmax; k += kGThreads) {
+#pragma unroll
+            for (int i = 0; i < 5; i++)
+                if (k < gc[i]) {
+                    const float *d = u + (uint32_t)i * Ls + hd[i] + 4 * k;
+                    __stcs(reinterpret_cast<float4 *>(S.err) + ((uint32_t)i * P + j0 + hd[i]) / 4 + k,
+                           make_float4(d[0], d[1], d[2], d[3]));
+                }
+        }
+        if (vec) {
+            uint32_t jj, i;
+            if (slice_edge(threadIdx.x, P, j0, len, n, i, jj)) __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
+        } else {
+            for (uint32_t i = 0; i < 5; i++)
+                for (uint32_t jj = threadIdx.x; jj < lim[i]; jj += kGThreads)
+                    __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
+        }
+    }
+    if (grank == 0 && threadIdx.x == 0) {
+        tlc_header *h = S.hdr;
+        h->M = M;
+        h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+        h->n = n;
+        if (!use_zre) h->payload_len = P;
+        h->status = status;
+        h->reserved = 0;
+    }
+    if (bulk && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem in use
+    K6C_TRACE(6);
+}
+
+// TLC_K6G=0 keeps one CTA per tensor (K6); 4 (default): clusters of 4, slices of <= 2 rows;
+// 8: clusters of 8, slices of 1 row (A/B)
+static int group_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K6G");
+        v = e ? atoi(e) : 4;
+        if (v != 0 && v != 4 && v != 8 && v != 2) v = 4;
+    }
+    return v;
+}
+
+int small_group_plan_build(SegTable &T, const std::vector<Seg> &host, GrpRec **d_grp, std::vector<uint4> &layout) {
+    T.grp = nullptr;
+    const int CL = group_mode();
+    if (CL == 0) return TLC_OK;
+    const uint32_t max_rows = CL == 8 ? 1u : 2u;               // rows per slice
+    struct Group { int seg; uint32_t k; };
+    std::vector<Group> groups;
+    for (int i = 0; i < (int)host.size(); i++) {
+        const uint32_t rows = (uint32_t)((host[i].P + kK3WarpRowS - 1) / kK3WarpRowS);
+        const uint32_t k = std::min<uint32_t>((uint32_t)CL, (rows + max_rows - 1) / max_rows);
+        groups.push_back({i, std::max<uint32_t>(k, 1u)});
+    }
+    std::stable_sort(groups.begin(), groups.end(), [](const Group &a, const Group &b) { return a.k > b.k; });
+    // best fit: open clusters by free slots
+    std::vector<std::vector<uint4>> clusters;
+    std::vector<std::vector<int>> open(CL + 1);              // open[f]: clusters with f free slots
+    uint32_t max_len = 0;
+    for (const Group &g : groups) {
+        int c = -1;
+        for (int f = (int)g.k; f < CL && c < 0; f++)
+            if (!open[f].empty()) { c = open[f].back(); open[f].pop_back(); }
+        if (c < 0) { c = (int)clusters.size(); clusters.emplace_back(); }
+        std::vector<uint4> &cl = clusters[c];
+        const Seg &S = host[g.seg];
+        const uint32_t P = (uint32_t)S.P, rows = (P + kK3WarpRowS - 1) / kK3WarpRowS;
+        const uint32_t base = rows / g.k, extra = rows % g.k, first = (uint32_t)cl.size();
+        uint32_t r0 = 0;
+        for (uint32_t q = 0; q < g.k; q++) {
+            const uint32_t nr = base + (q < extra ? 1u : 0u);
+            const uint32_t j0 = r0 * kK3WarpRowS, j1 = std::min(P, (r0 + nr) * kK3WarpRowS);
+            cl.push_back(make_uint4((uint32_t)g.seg, j0, j1 - j0, first | (g.k << 8) | (q << 16)));
+            max_len = std::max(max_len, j1 - j0);
+            r0 += nr;
+        }
+        const int f = CL - (int)cl.size();
+        if (f > 0) open[f].push_back(c);
+    }
+    layout.clear();
+    for (auto &cl : clusters) {
+        for (const uint4 &r : cl) layout.push_back(r);
+        for (size_t q = cl.size(); q < (size_t)CL; q++) layout.push_back(make_uint4(~0u, 0, 0, 0));
+    }
+    if (cudaMalloc((void **)d_grp, layout.size() * sizeof(GrpRec)) != cudaSuccess) return TLC_ERR_CUDA;
+    T.grp = *d_grp;
+    T.grp_grid = (int)layout.size();
+    T.grp_cl = CL;
+    T.grp_maxlen = max_len;
+    return TLC_OK;
+}
+
+int small_group_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout) {
+    std::vector<GrpRec> recs(layout.size());
+    for (size_t c = 0; c < layout.size(); c++) {
+        const uint4 &l = layout[c];
+        GrpRec &r = recs[c];
+        r = GrpRec{};
+        r.seg = l.x;
+        if (l.x == ~0u) continue;
+        const Seg &S = host[l.x];
+        r.t = S.t; r.err = S.err; r.payload = S.payload; r.hdr = S.hdr;
+        r.n = (uint32_t)S.n; r.P = (uint32_t)S.P; r.j0 = l.y; r.len = l.z;
+        r.g0 = l.w & 0xffu; r.gcnt = (l.w >> 8) & 0xffu; r.grank = (l.w >> 16) & 0xffu;
+    }
+    return cudaMemcpy(const_cast<GrpRec *>(T.grp), recs.data(), recs.size() * sizeof(GrpRec),
+                      cudaMemcpyHostToDevice) == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
+// TLC_K6G_BULK=1: K6g moves t and err in by bulk copies and err out by bulk stores instead
+// of through registers (A/B: 19.3 vs 20.1 us cold at s = 1.75 in favour of registers,
+// profiles/r03t_c2.txt; cp.async 16-byte copies were slower than both, r03r)
+static bool group_bulk() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K6G_BULK");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <int CL, bool BULK>
+static int launch_group(const SegTable &T, float s, int use_zre, cudaStream_t st) {
+    // u (and the T_in rows when copied in bulk), then B
+    const uint32_t smem = (BULK ? 2u : 1u) * 4u * 5u * (((T.grp_maxlen + 3) & ~3u) + 4u) + T.grp_maxlen + 64u;
+    static uint32_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(tlc_small_group_compress_kernel<CL, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = smem;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(T.grp_grid);
+    cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = CL;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tlc_small_group_compress_kernel<CL, BULK>, T, s, use_zre) == cudaSuccess
+               ? TLC_OK : TLC_ERR_CUDA;
 }
 
 // ============================================================== K6c
@@ -262,20 +775,6 @@ __device__ __forceinline__ RowCopy row_copy(const float *base, uint32_t e0, uint
 // bytes one slice row can take in the stage: 4 * kSlice + two partial granules
 constexpr uint32_t kRowBytes = 4 * kSlice + 32;
 
-#ifdef TLC_K6C_TRACE
-// development instrumentation: %globaltimer at the phase boundaries of every CTA
-__device__ unsigned long long g_k6c_trace[1024][8];
-#define K6C_TRACE(slot)                                                                     \
-    do {                                                                                    \
-        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                        \
-            unsigned long long t_;                                                          \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
-            g_k6c_trace[blockIdx.x][slot] = t_;                                             \
-        }                                                                                   \
-    } while (0)
-#else
-#define K6C_TRACE(slot) do {} while (0)
-#endif
 
 __global__ void __launch_bounds__(kSmThreads, 1)
 tlc_small_coop_compress_kernel(const SegTable T, float s, int use_zre) {
@@ -547,14 +1046,15 @@ bool small_coop_enabled() {
     return v == 1;
 }
 
-// A tensor's decode is split into parts of kSmPart quartic positions, one CTA each (the
-// 36,864-value ResNet-110 tensors would otherwise keep one SM busy while most idle): every
-// part scans the whole payload (<= P bytes, on chip) and expands / decodes only its range.
+// A tensor's decode is split into parts of kSmPart >> sub_log2 quartic positions, one CTA
+// each (the 36,864-value ResNet-110 tensors would otherwise keep one SM busy while most
+// idle; one SM stores at most ~61 GB/s, profiles/r03l_sm_bw.txt): every part scans the
+// whole payload (<= P bytes, on chip) and expands / decodes only its range.
 constexpr uint32_t kSmPart = (uint32_t)kT5;   // the K5 tile: parts are numbered like K5's tiles (Seg::k5)
 
 template <int kMode>
 __global__ void __launch_bounds__(kSmThreads)
-tlc_small_decompress_kernel(const SegTable T) {
+tlc_small_decompress_kernel(const SegTable T, int sub_log2) {
     extern __shared__ __align__(16) uint8_t sm_raw[];
     __shared__ uint16_t dig[256];                                // digit_i(b) at bits 2i
     __shared__ uint32_t s_wsum[kSmWarps + 1];
@@ -565,12 +1065,15 @@ tlc_small_decompress_kernel(const SegTable T) {
     __shared__ uint64_t s_first[kSegCache];
     seg_index_load<5>(T, s_first);
     bool table = false;
-    for (uint64_t item = blockIdx.x; item < T.n5; item += gridDim.x) {
+    const uint32_t sub_len = kSmPart >> sub_log2;
+    for (uint64_t it = blockIdx.x; it < (T.n5 << sub_log2); it += gridDim.x) {
+        const uint64_t item = it >> sub_log2;                    // K5 tile, and the sub-part of it
+        const uint32_t sub = (uint32_t)(it & ((1u << sub_log2) - 1u));
         const int si = find_seg_c<5>(T, item, s_first);
         const Seg S = get_seg(T, si);
-        const uint32_t part = (uint32_t)(item - S.k5);
+        const uint32_t part = (uint32_t)(item - S.k5) * (1u << sub_log2) + sub;
         tlc_header *hdr = S.hdr;
-        const uint32_t jr0 = part * kSmPart;
+        const uint32_t jr0 = part * sub_len;
         if (jr0 >= S.P) continue;                                // no positions in this part
         const bool hv = header_valid(hdr, S.n);
         if (!table) {
@@ -594,7 +1097,7 @@ tlc_small_decompress_kernel(const SegTable T) {
             continue;
         }
         const uint32_t n = (uint32_t)S.n, P = (uint32_t)S.P, Z = (uint32_t)hdr->payload_len;
-        const uint32_t jr1 = min(P, jr0 + kSmPart), pl = jr1 - jr0;
+        const uint32_t jr1 = min(P, jr0 + sub_len), pl = jr1 - jr0;
         const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
         const float M = hdr->M, negM = -M;
         uint8_t *E = sm_raw;                                     // quartic bytes [jr0, jr1)
@@ -726,6 +1229,13 @@ int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t 
         const cudaError_t e = cudaLaunchKernelEx(&cfg, tlc_small_coop_compress_kernel, T, s, use_zre);
         return e == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
     }
+    if (T.grp) {
+        KernelScope ks(kK6s, st);
+        const bool b = group_bulk();
+        if (T.grp_cl == 8) return b ? launch_group<8, true>(T, s, use_zre, st) : launch_group<8, false>(T, s, use_zre, st);
+        if (T.grp_cl == 2) return b ? launch_group<2, true>(T, s, use_zre, st) : launch_group<2, false>(T, s, use_zre, st);
+        return b ? launch_group<4, true>(T, s, use_zre, st) : launch_group<4, false>(T, s, use_zre, st);
+    }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tlc_small_compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -738,6 +1248,16 @@ int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t 
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 
+// K7 parts per K5 tile, log2 (TLC_K7_SUB=0..3 for A/B; default 1: 2048 positions per CTA)
+static int k7_sub_log2() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K7_SUB");
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;
+    }
+    return v;
+}
+
 int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
@@ -748,10 +1268,11 @@ int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
         attr = true;
     }
     KernelScope ks(kK7s, st);
-    const int grid = (int)tmin<uint64_t>(T.n5, 65535);
+    const int sl = k7_sub_log2();
+    const int grid = (int)tmin<uint64_t>(T.n5 << sl, 65535);
     const size_t smem = small_smem_decompress(T.max_n);
-    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T);
-    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T);
+    if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_kernel<0><<<grid, kSmThreads, smem, st>>>(T, sl);
+    else tlc_small_decompress_kernel<1><<<grid, kSmThreads, smem, st>>>(T, sl);
     return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
 }
 

@@ -119,6 +119,19 @@ struct SliceRec {
 };
 static_assert(sizeof(SliceRec) == 64, "slice records are 64 bytes");
 
+// A CTA of the K6g cluster launch (small.cu): quartic positions [j0, j0+len) of segment `seg`
+// (~0u: an idle CTA) with the segment's pointers and sizes; the tensor's slices sit at cluster
+// ranks g0 .. g0+gcnt-1, this one at g0+grank.
+struct GrpRec {
+    const float *t;
+    float *err;
+    uint8_t *payload;
+    tlc_header *hdr;
+    uint32_t n, P, j0, len;
+    uint32_t g0, gcnt, grank, seg;
+};
+static_assert(sizeof(GrpRec) == 64, "group records are 64 bytes");
+
 struct SegTable {
     const Seg *d;                   // device table when count > 1
     Seg one;                        // the segment when count == 1
@@ -141,6 +154,12 @@ struct SegTable {
     unsigned long long *sl_bar;     // grid barrier counter (monotonic)
     int sl_grid;
     uint32_t sl_smem;               // dynamic shared memory of the launch
+    // small tables (K6g, small.cu): one record per CTA of a cluster launch (refreshed at
+    // upload: the records carry the pointers); grp == nullptr: no plan
+    const GrpRec *grp;
+    int grp_grid;                   // CTAs (a multiple of grp_cl)
+    int grp_cl;                     // cluster size
+    uint32_t grp_maxlen;            // longest slice (quartic positions)
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -183,6 +202,8 @@ struct Table {
     size_t ws_bytes = 0;
     bool own_ws = false;
     void *d_small = nullptr;        // the K6c plan and its state (small tables only)
+    GrpRec *d_grp = nullptr;        // the K6g plan (small tables only)
+    std::vector<uint4> grp_layout;  // K6g CTAs on the host: (seg, j0, len, g0 | gcnt << 8 | grank << 16)
     std::vector<uint4> sl_layout;   // K6c slices on the host: (seg, j0, len, k | last << 16)
     int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);
     int update(const tlc_tensor_desc *descs);
@@ -200,6 +221,11 @@ bool small_table(const SegTable &T);
 int small_plan_build(SegTable &T, const std::vector<Seg> &host, void **d_small, std::vector<uint4> &layout);
 int small_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout);
 int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st);
+// K6g plan of a small table: every tensor cut into up to `cl` slices of whole 1 KiB ZRE rows,
+// the slices of one tensor in one thread-block cluster, clusters packed best-fit; depends on
+// the sizes only (the kernel takes the pointers from the table).  No-op when K6g is off.
+int small_group_plan_build(SegTable &T, const std::vector<Seg> &host, GrpRec **d_grp, std::vector<uint4> &layout);
+int small_group_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout);
 int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st);
 
 // K1 alone: per-segment max key of |err + t| (has_err) or |t| into maxkey[].
