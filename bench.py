@@ -321,7 +321,7 @@ def measure_resnet110(T, dev, s, steps=200, warmup=10):
     N = sum(sizes)
     Z = sum(h["payload_len"] for h in ctx.headers())
     return {"workload": "C2: ResNet-110 gradient set, 110 tensors, 1,719,856 values, one tlc_batch "
-                        "(small-table kernels: K6 compress + K7 decompress, one launch each) in a CUDA "
+                        "(small-table kernels: K6g compress (clusters of 4) + K7 decompress, one launch each) in a CUDA "
                         "graph, error feedback carried", "s": s,
             "value": 4.0 * N / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "l2": "flushed (512 MiB write) before every timed step",

@@ -28,9 +28,10 @@ def main(path, lo, hi, prefix):
             continue
         d = launch.setdefault(int(r[ii]), {"name": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", ""))
-    if lo < 0:                        # "auto": the last two C3 steps (from the second-last K1 on)
-        k1 = [i for i, d in launch.items() if d["name"].split("(")[0].split("::")[-1].split("<")[0] == "tlc_absmax_kernel"]
-        lo, hi = k1[-2], max(launch)
+    if lo < 0:                        # "auto": the last two COMPLETE C3 steps (K1 .. the K1 before the last K5)
+        base = {i: d["name"].split("(")[0].split("::")[-1].split("<")[0] for i, d in launch.items()}
+        hi = max(i for i, b in base.items() if b == "tlc_expand_dequant_kernel")
+        lo = [i for i, b in base.items() if b == "tlc_absmax_kernel" and i < hi][-2]
     sel = [(i, d) for i, d in launch.items() if lo <= i <= hi]
     agg = collections.OrderedDict()
     out_rows = []
