@@ -614,6 +614,9 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2
     # K5m's 4 n_own of means, the pull's K1 + K2 over the owned contexts
     n_own = sum(hi - lo for (_, lo, hi, ow) in plan if ow == rank)
     step_bytes = 8 * N + k2_push + 4 * n_own + 8 * n_own + k2_pull
+    if "k12_absmax_quant" in prof:
+        # K12 reads t and err from HBM once (its quantize items hit L2): no K1 terms
+        step_bytes = k2_push + 4 * n_own + k2_pull
     return {"ms": ms, "kernel_ms": kern_ms, "launches": launches, "wire": wire, "N": N, "status": status,
             "contexts": len(plan), "e2e": e2e, "k2_alg_bytes_per_step": k2_push + k2_pull,
             "step_alg_bytes": step_bytes,
@@ -728,23 +731,28 @@ def exchange_roofline(r, step_ms=None):
     """roofline object of the exchange step's dominant kernel (K2 over the segment table,
     push + pull launches) on this rank: algorithmic bytes per step / its device time per step;
     step_frac: the step's streaming bytes (a lower bound) / step time / peak."""
-    dom = "k2_quant_qe"
+    dom = "k12_absmax_quant" if "k12_absmax_quant" in r["kernels"] else "k2_quant_qe"
     k = r["kernels"].get(dom)
     if not k or not k["ms_per_step"]:
         return None
+    fused = dom == "k12_absmax_quant"
     peak, peak_src = load_peaks()
     achieved = r["k2_alg_bytes_per_step"] / (k["ms_per_step"] / 1e3) / 1e9
     sf = (r["step_alg_bytes"] / ((step_ms or r["ms"]) / 1e3) / 1e9 / peak) if r.get("step_alg_bytes") else None
     return {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "step_frac": sf, "step_alg_bytes": r.get("step_alg_bytes"),
-            "step_alg_bytes_formula": "8N + sum(12 n_c + ceil(n_c/5)) (push K1, K2) + 4 n_own (K5m means) + "
-                                      "8 n_own + sum_own(12 n_c + ceil(n_c/5)) (pull K1, K2); payload bytes and "
-                                      "the apply's skip-zero read-modify-writes omitted (lower bound); rank 0",
+            "step_alg_bytes_formula": ("sum(12 n_c + ceil(n_c/5)) (push K12: t, err read once) + 4 n_own (K5m "
+                                       "means) + sum_own(12 n_c + ceil(n_c/5)) (pull K12)" if fused else
+                                       "8N + sum(12 n_c + ceil(n_c/5)) (push K1, K2) + 4 n_own (K5m means) + "
+                                       "8 n_own + sum_own(12 n_c + ceil(n_c/5)) (pull K1, K2)") +
+                                      "; payload bytes and the apply's skip-zero read-modify-writes omitted "
+                                      "(lower bound); rank 0",
             "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
             "launches_per_step": k["launches_per_step"],
             "alg_bytes_per_launch": r["k2_alg_bytes_per_step"] / k["launches_per_step"],
             "alg_bytes_formula": "sum over compressed contexts of 12 n_c + ceil(n_c/5): all contexts (push) "
-                                 "+ the contexts this rank owns (pull), per step; rank 0"}
+                                 "+ the contexts this rank owns (pull), per step; rank 0" +
+                                 ("; K12 = K1 and K2 fused, t and err read from HBM once" if fused else "")}
 
 
 # ------------------------------------------------------------------ the GPU leg

@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <vector>
+
 #include "tlc_device.cuh"
 #include "tlc_launch.h"
 
@@ -132,17 +134,35 @@ tlc_absmax_kernel(const SegTable T, unsigned int *__restrict__ maxkey) {
 // ============================================================== K2
 constexpr int kK2Threads = 256;
 
+// K2's loads of t and err (read once): streaming (.cs, LP = 0), or through an L2 cache-policy
+// operand (LP = 1: K12's quantize items demote the lines its max items kept, TLC_K12_HINT=2)
+template <int LP>
+__device__ __forceinline__ float4 ldq4(const float4 *p, uint64_t pol) {
+    if (LP == 0) return __ldcs(p);
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+template <int LP>
+__device__ __forceinline__ float ldq(const float *p, uint64_t pol) {
+    if (LP == 0) return __ldcs(p);
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // One quartic position j, any alignment: the five strided elements e = i*P + j
 // (partition i), residuals stored, byte returned (pad positions -> digit 0).
-template <class QT>
+template <class QT, int LP = 0>
 __device__ __forceinline__ uint32_t quant_qe_one(const float *__restrict__ t, float *__restrict__ err,
-                                                 uint64_t n, uint64_t P, uint64_t j, const QT &Q) {
+                                                 uint64_t n, uint64_t P, uint64_t j, const QT &Q, uint64_t pol = 0) {
     float tv[5], ev[5];
 #pragma unroll
     for (int i = 0; i < 5; i++) {
         const uint64_t e = (uint64_t)i * P + j;
-        tv[i] = e < n ? ld_stream(t + e) : 0.0f;
-        ev[i] = e < n ? __ldcs(err + e) : 0.0f;
+        tv[i] = e < n ? ldq<LP>(t + e, pol) : 0.0f;
+        ev[i] = e < n ? ldq<LP>(err + e, pol) : 0.0f;
     }
     uint32_t b = 0;
 #pragma unroll
@@ -158,15 +178,15 @@ __device__ __forceinline__ uint32_t quant_qe_one(const float *__restrict__ t, fl
 
 // One group of 4 consecutive quartic positions 4g..4g+3 whose 20 elements all
 // exist: one float4 of t and of err per partition.
-template <class QT>
+template <class QT, int LP = 0>
 __device__ __forceinline__ void quant_qe_group(const float4 *__restrict__ t4, float4 *__restrict__ e4,
                                                uint32_t *__restrict__ b4, uint64_t P4, uint64_t g,
-                                               const QT &Q) {
+                                               const QT &Q, uint64_t pol = 0) {
     float4 tv[5], ev[5];
 #pragma unroll
     for (int i = 0; i < 5; i++) {
-        tv[i] = ld_stream4(t4 + g + i * P4);
-        ev[i] = __ldcs(e4 + g + i * P4);
+        tv[i] = ldq4<LP>(t4 + g + i * P4, pol);
+        ev[i] = ldq4<LP>(e4 + g + i * P4, pol);
     }
     uint32_t by[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -188,10 +208,10 @@ __device__ __forceinline__ void quant_qe_group(const float4 *__restrict__ t4, fl
 
 // Four quartic positions j + 256k (k = 0..3), any alignment: all 40 loads are
 // issued before any arithmetic so that 160 bytes per thread are in flight.
-template <class QT>
+template <class QT, int LP = 0>
 __device__ __forceinline__ void quant_qe_four(const float *__restrict__ t, float *__restrict__ err, uint64_t n,
                                               uint64_t P, uint64_t j, uint64_t jend, uint8_t *__restrict__ bytes,
-                                              const QT &Q) {
+                                              const QT &Q, uint64_t pol = 0) {
     float tv[4][5], ev[4][5];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -200,8 +220,8 @@ __device__ __forceinline__ void quant_qe_four(const float *__restrict__ t, float
         for (int i = 0; i < 5; i++) {
             const uint64_t e = (uint64_t)i * P + jj;
             const bool ok = jj < jend && e < n;
-            tv[k][i] = ok ? ld_stream(t + e) : 0.0f;
-            ev[k][i] = ok ? __ldcs(err + e) : 0.0f;
+            tv[k][i] = ok ? ldq<LP>(t + e, pol) : 0.0f;
+            ev[k][i] = ok ? ldq<LP>(err + e, pol) : 0.0f;
         }
     }
 #pragma unroll
@@ -221,8 +241,9 @@ __device__ __forceinline__ void quant_qe_four(const float *__restrict__ t, float
     }
 }
 
-template <class QT>
-__device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, uint64_t t2, const QT &Q) {
+template <class QT, int LP = 0>
+__device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint64_t j0, uint64_t t2, const QT &Q,
+                                              uint64_t pol = 0) {
     const uint64_t P = S.P, n = S.n;
     const uint64_t jend = tmin<uint64_t>(P, j0 + t2);
     if (S.flags & kSegVec2) {
@@ -232,12 +253,13 @@ __device__ __forceinline__ void quant_qe_tile(const Seg &S, uint8_t *bytes, uint
         const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
         float4 *e4 = reinterpret_cast<float4 *>(S.err);
         uint32_t *b4 = reinterpret_cast<uint32_t *>(bytes);
-        for (uint64_t g = g0 + threadIdx.x; g < g1; g += kK2Threads) quant_qe_group(t4, e4, b4, P / 4, g, Q);
+        for (uint64_t g = g0 + threadIdx.x; g < g1; g += kK2Threads)
+            quant_qe_group<QT, LP>(t4, e4, b4, P / 4, g, Q, pol);
         for (uint64_t j = 4 * g1 + threadIdx.x; j < jend; j += kK2Threads)
-            bytes[j] = (uint8_t)quant_qe_one(S.t, S.err, n, P, j, Q);
+            bytes[j] = (uint8_t)quant_qe_one<QT, LP>(S.t, S.err, n, P, j, Q, pol);
     } else {
         for (uint64_t j = j0 + threadIdx.x; j < jend; j += 4 * kK2Threads)
-            quant_qe_four(S.t, S.err, n, P, j, jend, bytes, Q);
+            quant_qe_four<QT, LP>(S.t, S.err, n, P, j, jend, bytes, Q, pol);
     }
 }
 
@@ -277,6 +299,264 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int u
     }
 }
 
+// ============================================================== K12
+// K1 and K2 fused for tables of several tensors (the exchange's push and pull tables, BERT-
+// large's 150 tensors): one persistent launch takes work items in order from a counter; the
+// host list (k12_plan_build) interleaves the max tiles (K1) and the quantize tiles (K2) of
+// consecutive windows of tensors of <= ~32 MB of t + err: K1(w0) K1(w1) K2(w0) K1(w2) K2(w1)
+// ...  A window's K2 tiles then re-read t and err while they are still in the 126 MB L2
+// (K1 of the next window is the only traffic in between), so HBM sees 12n + P/5 per
+// compress instead of K1's 8n plus K2's 12n + P/5.  A quantize item waits (one thread,
+// acquire load) until every max item of its tensor has folded its key; max items never
+// wait, and every item waits only on items dispensed before it, so the smallest unfinished
+// item can always run: no deadlock.  Same tiles, keys and arithmetic as K1 + K2: the same
+// bits.
+constexpr int kK12Threads = 256;
+static_assert(kK12Threads == kK2Threads, "the quantize items run K2's tile code");
+
+// L2 policy of the max items' loads: 0 normal (default), 1 evict_last through a cache-policy
+// operand (A/B, TLC_K12_HINT=1)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <int HINT>
+__device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol) {
+    float4 v;
+    if (HINT >= 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+template <int HINT>
+__device__ __forceinline__ float ld_keep(const float *p, uint64_t pol) {
+    float v;
+    if (HINT >= 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+// max key of the elements of K2 tile [j0, j0 + t2) (all five partitions).  The tile's part of
+// partition i is the run [i P + j0, i P + jend) of the flat arrays: aligned float4 groups
+// covering it (elements outside the run masked out: the key is a max, so any cover works),
+// all five runs' loads in flight together.
+template <int HINT>
+__device__ __forceinline__ unsigned int absmax_tile(const Seg &S, uint64_t j0, uint64_t t2) {
+    const uint64_t P = S.P, n = S.n;
+    const uint64_t jend = tmin<uint64_t>(P, j0 + t2);
+    unsigned int m = 0;
+    const uint64_t pol = HINT >= 1 ? policy_evict_last() : 0;
+    if (S.flags & kSegVec1) {
+        const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
+        const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
+        uint64_t lo[5], hi[5], g0[5];
+        uint32_t ng = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            lo[i] = tmin<uint64_t>(n, (uint64_t)i * P + j0);
+            hi[i] = tmin<uint64_t>(n, (uint64_t)i * P + jend);
+            g0[i] = lo[i] / 4;
+            ng = max(ng, (uint32_t)(hi[i] / 4 > g0[i] ? hi[i] / 4 - g0[i] : 0));
+        }
+        // whole float4 inside [4 g0, hi) (the head's extra elements masked), then the tail
+        // elements past the last whole float4 (< 4 per partition) one by one
+        if (threadIdx.x < 20) {
+            const int i = threadIdx.x >> 2;
+            const uint64_t l = i == 0 ? lo[0] : i == 1 ? lo[1] : i == 2 ? lo[2] : i == 3 ? lo[3] : lo[4];
+            const uint64_t h = i == 0 ? hi[0] : i == 1 ? hi[1] : i == 2 ? hi[2] : i == 3 ? hi[3] : hi[4];
+            const uint64_t e = h / 4 * 4 + (threadIdx.x & 3);
+            if (e >= l && e < h) m = max(m, absmax_key(ld_keep<HINT>(S.t + e, pol), ld_keep<HINT>(S.err + e, pol)));
+        }
+        for (uint32_t k = threadIdx.x; k < ng; k += kK12Threads) {
+            float4 tv[5], ev[5];
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const uint64_t g = g0[i] + k;
+                const bool ok = g < hi[i] / 4;
+                tv[i] = ok ? ld_keep4<HINT>(t4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ev[i] = ok ? ld_keep4<HINT>(e4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const uint64_t e = 4 * (g0[i] + k);
+                const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
+                const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (e + c >= lo[i] && e + c < hi[i]) m = max(m, absmax_key(tt[c], ee[c]));
+            }
+        }
+        return m;
+    }
+    for (uint64_t j = j0 + threadIdx.x; j < jend; j += kK12Threads) {
+        float tv[5], ev[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + j;
+            tv[i] = e < n ? ld_keep<HINT>(S.t + e, pol) : 0.0f;
+            ev[i] = e < n ? ld_keep<HINT>(S.err + e, pol) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; i++) m = max(m, absmax_key(tv[i], ev[i]));   // pads: key 0
+    }
+    return m;
+}
+
+// K2 on a complete tile of a tensor whose partitions are not 16-byte aligned to each other
+// (P % 4 != 0; t and err 16-byte aligned): a warp takes 31 groups of four positions at a time;
+// for each partition its lanes load the 32 aligned float4 of t and err covering the 124
+// elements (shift sh = (i P + j0) mod 4), stage them in the warp's shared memory, read their
+// four elements back at the shift, and return the residuals through the stage: whole float4
+// stores, scalar ones for the two partial float4 at the ends (their other elements belong to
+// neighbouring groups).  Every element of the tile's supersets exists (the caller checks).
+constexpr int kUGroups = 31;
+template <class QT, int LP>
+__device__ __forceinline__ void quant_qe_tile_unaligned(const Seg &S, uint8_t *bytes, uint64_t j0, uint64_t jend,
+                                                        float *wbuf, const QT &Q, uint64_t pol) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t P = S.P;
+    const uint32_t ngr = (uint32_t)((jend - j0) / 4);      // groups of the tile (complete)
+    const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
+    const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
+    float4 *o4 = reinterpret_cast<float4 *>(S.err);
+    float *wt = wbuf, *we = wbuf + 128;                      // this warp's stage: 128 floats of t, of err
+    for (uint32_t c0 = warp * kUGroups; c0 < ngr; c0 += (kK12Threads / 32) * kUGroups) {
+        const uint32_t g = c0 + lane;                         // this lane's group (lane 31: none)
+        const bool mine = lane < kUGroups && g < ngr;
+        float4 tv[5], ev[5];
+        uint64_t A[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            A[i] = ((uint64_t)i * P + j0 + 4ull * c0) / 4;   // first aligned float4 of the window
+            tv[i] = ldq4<LP>(t4 + A[i] + lane, pol);
+            ev[i] = ldq4<LP>(e4 + A[i] + lane, pol);
+        }
+        uint32_t by[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint32_t sh = (uint32_t)(((uint64_t)i * P + j0) & 3);
+            reinterpret_cast<float4 *>(wt)[lane] = tv[i];
+            reinterpret_cast<float4 *>(we)[lane] = ev[i];
+            __syncwarp();
+            float r[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const float u = __fadd_rn(we[sh + 4 * lane + c], wt[sh + 4 * lane + c]);   // step (1)
+                const int q = Q.q(u);                        // Eq. 2
+                r[c] = Q.residual(u, q);                     // steps (a),(b)
+                by[c] = by[c] * 3u + (uint32_t)(q + 1);      // steps 1, 6
+            }
+            __syncwarp();
+            if (mine)
+#pragma unroll
+                for (int c = 0; c < 4; c++) we[sh + 4 * lane + c] = r[c];
+            __syncwarp();
+            // lane l writes float4 l of the window: whole for 1 <= l <= 30 (inside the 31 groups
+            // when they are all there), element-wise at the ends and past the tile's last group
+            const uint32_t e_lo = sh, e_hi = sh + 4 * (ngr - c0 < (uint32_t)kUGroups ? ngr - c0 : (uint32_t)kUGroups);
+            const float4 w = reinterpret_cast<const float4 *>(we)[lane];
+            if (4 * lane >= e_lo && 4 * lane + 4 <= e_hi) {
+                __stcs(o4 + A[i] + lane, w);
+            } else {
+                float *eo = S.err + 4 * (A[i] + lane);
+                const float ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (4 * lane + c >= e_lo && 4 * lane + c < e_hi) __stcs(eo + c, ww[c]);
+            }
+            __syncwarp();
+        }
+        if (mine) reinterpret_cast<uint32_t *>(bytes + j0)[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
+    }
+}
+
+template <int HINT>
+__global__ void __launch_bounds__(kK12Threads, 2)
+tlc_absmax_quant_kernel(const SegTable T, unsigned int *__restrict__ maxkey, unsigned int *__restrict__ done,
+                        Ctrl *ctrl, float s, int use_zre, uint8_t *__restrict__ scratch) {
+    __shared__ uint64_t s_first[kSegCache];
+    __shared__ unsigned int s_red[kK12Threads / 32];
+    __shared__ uint32_t s_it[2];
+    __shared__ unsigned int s_key;
+    __shared__ __align__(16) float s_stage[(kK12Threads / 32) * 256];   // per-warp realignment stages
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_it[0] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);
+    seg_index_load<2>(T, s_first);                          // (ends with a block barrier)
+    for (int b = 0;; b ^= 1) {
+        const uint32_t it = s_it[b];
+        if (it >= T.k12_n) break;
+        if (threadIdx.x == 0) s_it[b ^ 1] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);   // the next, early
+        const uint32_t item = T.k12[it];
+        const uint64_t tile = item >> 1;
+        const int si = find_seg_c<2>(T, tile, s_first);
+        const Seg S = get_seg(T, si);
+        const uint64_t lt = tile - S.k2;
+        if ((item & 1u) == 0) {
+            // ---- K1 on this tile: max of bits(u) & 0x7fffffff, folded into the tensor's key
+            unsigned int m = absmax_tile<HINT>(S, lt * T.sz.t2, T.sz.t2);
+            m = __reduce_max_sync(0xffffffffu, m);
+            if (lane == 0) s_red[warp] = m;
+            __syncthreads();
+            if (warp == 0) {
+                m = __reduce_max_sync(0xffffffffu, lane < kK12Threads / 32 ? s_red[lane] : 0u);
+                if (lane == 0) {
+                    atomicMax(maxkey + si, m);
+                    __threadfence();                        // the key before the count (release)
+                    atomicAdd(done + si, 1u);
+                }
+            }
+        } else {
+            // ---- K2 on this tile once every max tile of the tensor is in
+            if (threadIdx.x == 0) {
+                const unsigned int need = (unsigned int)((S.P + T.sz.t2 - 1) / T.sz.t2);
+                while (ld_acquire_u32(done + si) < need) __nanosleep(64);
+                s_key = ld_relaxed_u32(maxkey + si);
+            }
+            __syncthreads();
+            float M;
+            const unsigned int status = scale_from_key(s_key, s, M);   // Eq. 1, R6
+            if (lt == 0 && threadIdx.x == 0) {
+                tlc_header *h = S.hdr;
+                h->M = M;
+                h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+                h->n = S.n;
+                h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;   // ZRE: set by K3
+                h->status = status;
+                h->reserved = 0;
+            }
+            if (status == TLC_OK) {                          // else err untouched (R6)
+                uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
+                const Quant Q(M);
+                constexpr int LP = HINT == 2 ? 1 : 0;
+                const uint64_t pol = LP ? policy_evict_first() : 0;
+                const uint64_t j0 = lt * T.sz.t2, jend = tmin<uint64_t>(S.P, j0 + T.sz.t2);
+                // complete tile: whole groups, and partition 4's 128-float windows inside the tensor
+                const bool whole = (jend - j0) % 4 == 0 &&
+                                   ((4 * S.P + jend) & ~uint64_t(3)) + 4 * kUGroups + 4 <= S.n;
+                if (!(S.flags & kSegVec2) && (S.flags & kSegVec1) && whole && (use_zre || aligned4(S.payload))) {
+                    float *wbuf = s_stage + (threadIdx.x >> 5) * 256;
+                    if (Q.mode == 1) quant_qe_tile_unaligned<QuantCmp, LP>(S, bytes, j0, jend, wbuf, QuantCmp(Q), pol);
+                    else quant_qe_tile_unaligned<Quant, LP>(S, bytes, j0, jend, wbuf, Q, pol);
+                } else {
+                    if (Q.mode == 1) quant_qe_tile<QuantCmp, LP>(S, bytes, j0, T.sz.t2, QuantCmp(Q), pol);
+                    else quant_qe_tile<Quant, LP>(S, bytes, j0, T.sz.t2, Q, pol);
+                }
+            }
+        }
+        __syncthreads();                                     // s_it[b ^ 1], s_red, s_key
+    }
+}
+
 // ---- K2 bulk path: the same computation on tiles staged in shared memory by the
 // Blackwell bulk-copy (TMA) engine.  One CTA per SM keeps kBulkStages tiles of
 // t and err (10 contiguous 4 KiB partition segments each) in flight behind
@@ -305,7 +585,7 @@ struct BulkSmem {
 // copy engine fetched the aligned superset starting sh_i = (i P) mod 4 elements early:
 // shared reads are scalar at offset sh_i and err goes back with 32-bit stores.
 template <bool kAligned, class QT>
-__device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, float *err, uint64_t P, uint64_t j0,
+__device__ __forceinline__ void bulk_compute(const float *buf, float *err, uint64_t P, uint64_t j0,
                                              uint8_t *bytes, const QT &Q) {
     const int g = threadIdx.x;                       // group: positions j0 + 4g .. j0 + 4g + 3
     uint32_t by[4] = {0, 0, 0, 0};
@@ -314,15 +594,15 @@ __device__ __forceinline__ void bulk_compute(const BulkSmem &sm, int stage, floa
         const int sh = kAligned ? 0 : (int)(((uint64_t)i * P) & 3);
         float tt[4], ee[4];
         if (kAligned) {
-            const float4 tv = *reinterpret_cast<const float4 *>(&sm.buf[stage][i * kBulkPos + 4 * g]);
-            const float4 ev = *reinterpret_cast<const float4 *>(&sm.buf[stage][(5 + i) * kBulkPos + 4 * g]);
+            const float4 tv = *reinterpret_cast<const float4 *>(&buf[i * kBulkPos + 4 * g]);
+            const float4 ev = *reinterpret_cast<const float4 *>(&buf[(5 + i) * kBulkPos + 4 * g]);
             tt[0] = tv.x; tt[1] = tv.y; tt[2] = tv.z; tt[3] = tv.w;
             ee[0] = ev.x; ee[1] = ev.y; ee[2] = ev.z; ee[3] = ev.w;
         } else {
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                tt[c] = sm.buf[stage][i * kBulkRow + sh + 4 * g + c];
-                ee[c] = sm.buf[stage][(5 + i) * kBulkRow + sh + 4 * g + c];
+                tt[c] = buf[i * kBulkRow + sh + 4 * g + c];
+                ee[c] = buf[(5 + i) * kBulkRow + sh + 4 * g + c];
             }
         }
         float r[4];
@@ -394,8 +674,8 @@ tlc_quant_qe_bulk_kernel(const SegTable T, const unsigned int *maxkey, float s, 
         const int st = (int)(k % kBulkStages);
         mbar_wait(&sm.bar[st], (uint32_t)((k / kBulkStages) & 1));
         const uint64_t j0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kBulkPos;
-        if (Q.mode == 1) bulk_compute<kAligned>(sm, st, S.err, P, j0, bytes, QuantCmp(Q));
-        else bulk_compute<kAligned>(sm, st, S.err, P, j0, bytes, Q);
+        if (Q.mode == 1) bulk_compute<kAligned>(sm.buf[st], S.err, P, j0, bytes, QuantCmp(Q));
+        else bulk_compute<kAligned>(sm.buf[st], S.err, P, j0, bytes, Q);
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
     }
@@ -534,11 +814,11 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
         if (status == TLC_OK) {                          // else err untouched (R6)
             const Quant Q(M);
             if ((it.P & 3) == 0) {
-                if (Q.mode == 1) bulk_compute<true>(sm, st, it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
-                else bulk_compute<true>(sm, st, it.err, it.P, it.j0, it.bytes, Q);
+                if (Q.mode == 1) bulk_compute<true>(sm.buf[st], it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
+                else bulk_compute<true>(sm.buf[st], it.err, it.P, it.j0, it.bytes, Q);
             } else {
-                if (Q.mode == 1) bulk_compute<false>(sm, st, it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
-                else bulk_compute<false>(sm, st, it.err, it.P, it.j0, it.bytes, Q);
+                if (Q.mode == 1) bulk_compute<false>(sm.buf[st], it.err, it.P, it.j0, it.bytes, QuantCmp(Q));
+                else bulk_compute<false>(sm.buf[st], it.err, it.P, it.j0, it.bytes, Q);
             }
         }
 #ifdef TLC_K2T_WS
@@ -1013,7 +1293,7 @@ void launch_absmax(const SegTable &T, unsigned int *maxkey, bool has_err, cudaSt
 // K1 (max key), then `k2` (the quantizer + quartic pass of the codec), then K3 (ZRE).
 template <class K2Launch>
 static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_err, void *ws, cudaStream_t st,
-                             const K2Launch &k2) {
+                             const K2Launch &k2, bool fused_k1 = false) {
     const WsLayout L = ws_layout(T, 0);
     char *base = reinterpret_cast<char *>(ws);
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
@@ -1022,7 +1302,7 @@ static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_e
     uint8_t *scratch = reinterpret_cast<uint8_t *>(base + L.bytes);
     const int sms = num_sms();
     if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
-    launch_absmax(T, maxkey, has_err, st);
+    if (!fused_k1) launch_absmax(T, maxkey, has_err, st);   // K12 folds K1 into its items
     k2(maxkey, scratch);
     if (use_zre) {
         KernelScope ks(kK3, st);
@@ -1066,9 +1346,85 @@ static bool fork_enabled() {
     return v == 1;
 }
 
+// K12 is opt-in (TLC_K12=1; measured in round 2): it cuts K2's HBM reads
+// (profiles/r04a: 2.66 instead of 4.3 GB per compress of 64 x 4M values) and is 14 % faster
+// than K1 + K2 on tables of 16-byte aligned partitions (P % 4 == 0), but its register-staged
+// quantize loses to the bulk-copy K2 on unaligned partitions (+20 %), and BERT-large's
+// exchange (mostly P % 4 != 0) is 10 % slower with it (profiles/r04f, r04g).
+// TLC_K12_WIN=<M values> sets the window (default 4: 32 MB of t + err); TLC_K12_HINT: L2
+// policy of the max items' loads (1 default: evict_last; 0 none; 2 also evict_first on the
+// quantize items' loads).
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e && e[0] ? atoi(e) : dflt;
+}
+static int k12_mode() {
+    static int v = -1;
+    if (v < 0) v = env_int("TLC_K12", 0) != 0 ? 1 : 0;
+    return v;
+}
+static bool k12_enabled() { return k12_mode() != 0; }
+
+int k12_plan_build(SegTable &T, const std::vector<Seg> &host, uint32_t **d_k12) {
+    T.k12 = nullptr;
+    T.k12_n = 0;
+    if (!k12_enabled() || host.size() < 2) return TLC_OK;
+    const uint64_t win = (uint64_t)tmax(1, env_int("TLC_K12_WIN", 4)) << 20;   // values per window
+    std::vector<std::pair<size_t, size_t>> wins;            // [first, last) tensors
+    for (size_t i = 0; i < host.size();) {
+        size_t j = i;
+        uint64_t sum = 0;
+        while (j < host.size() && (j == i || sum + host[j].n <= win)) sum += host[j++].n;
+        wins.push_back({i, j});
+        i = j;
+    }
+    const uint64_t upos = T.sz.t2, R = 1;                    // items are K2 tiles
+    std::vector<uint32_t> items;
+    auto emit = [&](size_t w, uint32_t kind) {
+        for (size_t i = wins[w].first; i < wins[w].second; i++) {
+            const uint64_t nt = (host[i].P + upos - 1) / upos;
+            for (uint64_t lt = 0; lt < nt; lt++) items.push_back((uint32_t)((host[i].k2 * R + lt) << 1) | kind);
+        }
+    };
+    emit(0, 0u);
+    for (size_t w = 0; w < wins.size(); w++) {              // K1(w+1) then K2(w)
+        if (w + 1 < wins.size()) emit(w + 1, 0u);
+        emit(w, 1u);
+    }
+    if (T.n2 * R >= (1ull << 31)) return TLC_OK;            // item ids are 31-bit units: keep K1 + K2
+    const size_t nitems = items.size();
+    if (cudaMalloc((void **)d_k12, items.size() * sizeof(uint32_t)) != cudaSuccess) return TLC_ERR_CUDA;
+    if (cudaMemcpy(*d_k12, items.data(), items.size() * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess)
+        return TLC_ERR_CUDA;
+    T.k12 = *d_k12;
+    T.k12_n = (uint32_t)nitems;
+    return TLC_OK;
+}
+
+static int g_k12_blocks = 0;
+
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
     if (small_table(T)) return launch_small_compress(T, s, use_zre, st);    // one launch, on chip
     const int sms = num_sms();
+    if (T.k12 && k12_enabled()) {
+        static const int hint = env_int("TLC_K12_HINT", 1);
+        const WsLayout L = ws_layout(T, 0);
+        char *base = reinterpret_cast<char *>(ws);
+        unsigned int *done = reinterpret_cast<unsigned int *>(base + L.k12done);
+        Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
+        return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
+            KernelScope ks(kK12, st);
+            if (!g_k12_blocks)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k12_blocks, tlc_absmax_quant_kernel<0>, kK12Threads, 0);
+            const int grid = (int)tmin<uint64_t>(T.k12_n, (uint64_t)sms * tmax(1, g_k12_blocks));
+            if (hint == 2)
+                tlc_absmax_quant_kernel<2><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+            else if (hint == 1)
+                tlc_absmax_quant_kernel<1><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+            else
+                tlc_absmax_quant_kernel<0><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+        }, true);
+    }
     return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
         KernelScope ks(kK2, st);
         const uint64_t nbulk = use_bulk() ? bulk_tiles(T, use_zre) : 0;

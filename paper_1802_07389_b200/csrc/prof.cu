@@ -20,7 +20,8 @@ static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe", "k3_zre"
                                             "k5m_aggregate", "k9_flag_barrier",
                                             "k8_scale_mean", "k2s_stoch_qe",
                                             "kq8_int8_quant", "kd8_int8_dequant",
-                                            "k6_small_compress", "k7_small_decompress"};
+                                            "k6_small_compress", "k7_small_decompress",
+                                            "k12_absmax_quant"};
 
 namespace {
 struct Rec {

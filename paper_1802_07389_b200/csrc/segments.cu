@@ -48,8 +48,9 @@ WsLayout ws_layout(const SegTable &T, uint64_t scratch_bytes) {
     size_t p = 0;
     L.ctrl = p;   p += sizeof(Ctrl);
     L.maxkey = p; p += align256((size_t)T.count * sizeof(unsigned int));
+    L.k12done = p; p += T.k12 ? align256((size_t)T.count * sizeof(unsigned int)) : 0;
     L.k3st = p;   p += align256(T.n3 * sizeof(unsigned long long));
-    L.memset_c = p;                                   // ctrl + max keys + K3 states
+    L.memset_c = p;                                   // ctrl + max keys + K12 counts + K3 states
     L.k4st = p;   p += align256(T.n4 * sizeof(unsigned long long));
     L.memset_d = T.n4 * sizeof(unsigned long long);   // K4 states (ctrl separately)
     L.seek = p;   p += align256(T.n5 * sizeof(unsigned long long));
@@ -79,6 +80,10 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
     T.count = cnt;
     T.n1 = c1; T.n2 = c2; T.n3 = c3; T.n4 = c4; T.n5 = c5;
     for (int i = 0; i < cnt; i++) T.max_n = tmax<uint64_t>(T.max_n, host[i].n);
+    if (with_scratch && T.max_n > kSmallMaxN) {                     // compress tables
+        const int rc = k12_plan_build(T, host, &d_k12);
+        if (rc != TLC_OK) return rc;
+    }
     ws_bytes = ws_layout(T, with_scratch ? scratch : 0).total;
     if (cudaMalloc((void **)&d, cnt * sizeof(Seg)) != cudaSuccess) return TLC_ERR_CUDA;
     if (cudaMalloc((void **)&d_first, 5 * (size_t)cnt * sizeof(uint64_t)) != cudaSuccess) return TLC_ERR_CUDA;
@@ -173,6 +178,8 @@ void Table::release() {
     d_small = nullptr;
     if (d_grp) cudaFree(d_grp);
     d_grp = nullptr;
+    if (d_k12) cudaFree(d_k12);
+    d_k12 = nullptr;
     d = nullptr;
     ws = nullptr;
 }

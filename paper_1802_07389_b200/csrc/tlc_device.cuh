@@ -42,11 +42,22 @@ constexpr uint32_t kMaxRun = 14;
 struct Ctrl {
     unsigned long long k3_counter;   // dynamic K3 chunk ids (forward-progress ordering)
     unsigned long long k4_counter;   // dynamic K4 chunk ids
-    unsigned int pad[60];
+    unsigned long long k12_counter;  // dynamic K12 work items
+    unsigned int pad[58];
 };
 static_assert(sizeof(Ctrl) == 256, "ctrl is one 256-byte block");
 
 // ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

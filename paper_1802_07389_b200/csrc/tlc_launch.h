@@ -54,7 +54,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 // Kernel ids for launch counting / profiling (prof.cu).
 enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7,
-                kK2s = 8, kKq8 = 9, kKd8 = 10, kK6s = 11, kK7s = 12, kNumKernelIds = 13 };
+                kK2s = 8, kKq8 = 9, kKd8 = 10, kK6s = 11, kK7s = 12, kK12 = 13, kNumKernelIds = 14 };
 
 struct Ctrl;
 
@@ -156,6 +156,10 @@ struct SegTable {
     uint32_t sl_smem;               // dynamic shared memory of the launch
     // small tables (K6g, small.cu): one record per CTA of a cluster launch (refreshed at
     // upload: the records carry the pointers); grp == nullptr: no plan
+    // tables of several tensors (K12, compress.cu): the fused K1/K2 work list, K1 and K2 tiles
+    // of consecutive L2-sized windows of tensors interleaved (k12 == nullptr: no plan)
+    const uint32_t *k12;            // item = K2 tile index << 1 | (1: quantize, 0: max)
+    uint32_t k12_n;
     const GrpRec *grp;
     int grp_grid;                   // CTAs (a multiple of grp_cl)
     int grp_cl;                     // cluster size
@@ -165,7 +169,7 @@ struct SegTable {
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
 // chunk states, K5 seek entries, quartic scratch.
 struct WsLayout {
-    size_t ctrl, maxkey, k3st, k4st, seek, bytes, memset_c, memset_d, total;
+    size_t ctrl, maxkey, k12done, k3st, k4st, seek, bytes, memset_c, memset_d, total;
 };
 
 WsLayout ws_layout(const SegTable &T, uint64_t scratch_bytes);
@@ -174,6 +178,9 @@ inline ItemSizes item_sizes(uint64_t total_elems) { return total_elems < kSmallT
 SegTable single_table(const float *t, float *err, float *out, uint8_t *payload, tlc_header *hdr, uint64_t n,
                       uint64_t &scratch);
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st);
+// K12 work list of a table of several tensors (sizes only); no-op when K12 is off or the
+// table is small or a single tensor
+int k12_plan_build(SegTable &T, const std::vector<Seg> &host, uint32_t **d_k12);
 int launch_compress(const float *t, float *err, uint64_t n, float s, int use_zre, uint8_t *payload,
                     tlc_header *hdr, void *ws, cudaStream_t st);
 size_t compress_workspace_bytes(uint64_t n);
@@ -203,6 +210,7 @@ struct Table {
     bool own_ws = false;
     void *d_small = nullptr;        // the K6c plan and its state (small tables only)
     GrpRec *d_grp = nullptr;        // the K6g plan (small tables only)
+    uint32_t *d_k12 = nullptr;      // the K12 work list (tables of several tensors)
     std::vector<uint4> grp_layout;  // K6g CTAs on the host: (seg, j0, len, g0 | gcnt << 8 | grank << 16)
     std::vector<uint4> sl_layout;   // K6c slices on the host: (seg, j0, len, k | last << 16)
     int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);

@@ -29,3 +29,25 @@ def test_cooperative_small_table_path():
                         "tests/test_gpu_exchange_loopback.py::test_loopback_matches_oracle"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"TLC_K6G": "0"}, {"TLC_K6G_BULK": "1"}, {"TLC_K6G": "8"}])
+def test_small_table_compressor_variants(env):
+    """K6g (clusters of 4 CTAs per tensor group) is the small-table compressor; K6 (one CTA per
+    tensor, TLC_K6G=0), K6g with bulk-copy staging (TLC_K6G_BULK=1) and clusters of 8 with
+    one-row slices (TLC_K6G=8) stay selectable and must give the oracle's bytes too."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_batched.py",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_graph_replay"],
+                       cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_fused_max_quantize_table_path():
+    """TLC_K12=1: K1 and K2 fused over L2-sized windows of tensors (compress.cu K12, opt-in) --
+    batches, the loopback exchange with contexts above the small-table bound (aligned and
+    unaligned partitions) and the full-size BERT-large sample must give the oracle's bytes."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_batched.py",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_large_contexts",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_bert_large_full_size_sampled"],
+                       cwd=ROOT, env=dict(os.environ, TLC_K12="1"), capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
