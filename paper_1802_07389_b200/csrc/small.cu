@@ -266,6 +266,24 @@ __device__ __forceinline__ void dsmem_store_u32(unsigned int *local, uint32_t ra
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
+// DSMEM store that completes `bytes` of the receiving CTA's mbarrier transaction count
+__device__ __forceinline__ void st_async_u32(unsigned int *local_dst, uint32_t rank, unsigned int v,
+                                             unsigned long long *local_mbar) {
+    uint32_t ra, rm;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local_dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(smem_addr(local_mbar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 ::"r"(ra), "r"(v), "r"(rm) : "memory");
+}
+__device__ __forceinline__ void st_async_u64(unsigned long long *local_dst, uint32_t rank, unsigned long long v,
+                                             unsigned long long *local_mbar) {
+    uint32_t ra, rm;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(local_dst)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rm) : "r"(smem_addr(local_mbar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(ra), "l"(v), "r"(rm) : "memory");
+}
+
 constexpr int kGThreads = 256;
 constexpr int kGWarps = kGThreads / 32;
 
@@ -327,7 +345,13 @@ __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_
 // registers, profiles/r03o_trace.txt) into rows of Ls floats placed so that the 16-byte
 // aligned interiors land 16-byte aligned (row i starts at i*Ls + (e0_i & 3)), and err leaves
 // by bulk stores from the same rows.
-template <int CL, bool BULK>
+// AS (default): the keys and the run summaries travel by st.async into the receivers' shared
+// memory, each receiver waiting on its own mbarrier for exactly the bytes it is owed; the only
+// cluster barrier is the one that publishes the mbarriers' initialisation (arrived at the
+// start, waited on before the first remote store), so err is stored right after the
+// quantization and nobody waits for the slowest member of the cluster.  !AS: two cluster
+// barriers, every global store after the second (TLC_K6G_SYNC=1, A/B).
+template <int CL, bool BULK, bool AS>
 __global__ void __launch_bounds__(kGThreads, 2)
 tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
     extern __shared__ __align__(16) uint8_t sm_raw[];
@@ -337,11 +361,24 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
     __shared__ unsigned int s_keys[CL];
     __shared__ unsigned long long s_aggs[CL];
     __shared__ __align__(8) unsigned long long s_mbar;
+    __shared__ __align__(8) unsigned long long s_mb_keys, s_mb_aggs;   // AS: incoming keys / summaries
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     K6C_TRACE(0);
     const GrpRec S = T.grp[blockIdx.x];                        // one 64-byte record: no table walk
     const bool idle = S.seg == ~0u;
     const uint32_t g0 = S.g0, gcnt = S.gcnt, grank = S.grank;
+    if (AS) {
+        if (threadIdx.x == 0) {
+            mbar_init(&s_mb_keys, 1);
+            mbar_init(&s_mb_aggs, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            // the bytes this CTA is owed: every other member's key, every earlier slice's summary
+            mbar_expect_tx(&s_mb_keys, idle ? 0u : 4u * (gcnt - 1));
+            mbar_expect_tx(&s_mb_aggs, idle || !use_zre ? 0u : 8u * grank);
+        }
+        __syncthreads();
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // waited on below
+    }
     const uint32_t n = S.n, P = S.P, j0 = S.j0, len = idle ? 0u : S.len;
     const bool vec = aligned16(S.t) && aligned16(S.err);
     const bool bulk = BULK && vec;
@@ -440,14 +477,25 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
     }
     m = block_max_n<kGWarps>(m, s_red);
     K6C_TRACE(1);
-    // the key to every CTA of the group (its own copy included)
-    if (!idle && threadIdx.x < gcnt) dsmem_store_u32(&s_keys[grank], g0 + threadIdx.x, m);
-    cluster_sync_all();                                        // 1: the group's keys
-    K6C_TRACE(2);
-    if (idle) {
-        cluster_sync_all();
-        return;
+    if (AS) {
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every member's mbarriers are live
+        if (idle) return;
+        if (threadIdx.x < gcnt) {
+            if (threadIdx.x == grank) s_keys[grank] = m;
+            else st_async_u32(&s_keys[grank], g0 + threadIdx.x, m, &s_mb_keys);
+        }
+        mbar_wait(&s_mb_keys, 0);
+        __syncthreads();                                       // the local key
+    } else {
+        // the key to every CTA of the group (its own copy included)
+        if (!idle && threadIdx.x < gcnt) dsmem_store_u32(&s_keys[grank], g0 + threadIdx.x, m);
+        cluster_sync_all();                                    // 1: the group's keys
+        if (idle) {
+            cluster_sync_all();
+            return;
+        }
     }
+    K6C_TRACE(2);
     for (uint32_t q = 0; q < gcnt; q++) m = max(m, s_keys[q]);
     float M;
     const unsigned int status = scale_from_key(m, s, M);      // Eq. 1, R6
@@ -460,6 +508,42 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
     }
     __syncthreads();
     K6C_TRACE(3);
+    // the residuals (steps a, b) from shared memory to err: now (AS) or after the last barrier
+    auto store_err = [&]() {
+        if (bulk) {
+            if (threadIdx.x == 0) {
+#pragma unroll
+                for (int i = 0; i < 5; i++)
+                    if (gc[i]) {
+                        const uint32_t o = (uint32_t)i * Ls + sh[i] + hd[i];
+                        bulk_store(S.err + (uint32_t)i * P + j0 + hd[i], u + o, 16u * gc[i]);
+                    }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            uint32_t jj, i;
+            if (slice_edge(threadIdx.x - 32u, P, j0, len, n, i, jj))
+                __stcs(S.err + i * P + j0 + jj, u[i * Ls + ((i * P + j0) & 3u) + jj]);
+        } else {
+            for (uint32_t k = threadIdx.x; k < gmax; k += kGThreads) {
+#pragma unroll
+                for (int i = 0; i < 5; i++)
+                    if (k < gc[i]) {
+                        const float *d = u + (uint32_t)i * Ls + hd[i] + 4 * k;
+                        __stcs(reinterpret_cast<float4 *>(S.err) + ((uint32_t)i * P + j0 + hd[i]) / 4 + k,
+                               make_float4(d[0], d[1], d[2], d[3]));
+                    }
+            }
+            if (vec) {
+                uint32_t jj, i;
+                if (slice_edge(threadIdx.x, P, j0, len, n, i, jj)) __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
+            } else {
+                for (uint32_t i = 0; i < 5; i++)
+                    for (uint32_t jj = threadIdx.x; jj < lim[i]; jj += kGThreads)
+                        __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
+            }
+        }
+    };
+    if (AS && status == TLC_OK) store_err();
     // ---- step (4): run summaries of the slice's rows (one warp per 1 KiB row)
     const uint32_t nrows = (len + kK3WarpRowS - 1) / kK3WarpRowS;
     uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mask = 0;
@@ -494,10 +578,16 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
         RunSum acc = run_identity();
         for (uint32_t r = 0; r < nrows; r++) acc = compose(acc, unpack(s_row[r]));
         const unsigned long long v = pack(acc);
-        for (uint32_t q = grank + 1; q < gcnt; q++) dsmem_store_u64(&s_aggs[grank], g0 + q, v);
+        for (uint32_t q = grank + 1; q < gcnt; q++) {
+            if (AS) st_async_u64(&s_aggs[grank], g0 + q, v, &s_mb_aggs);
+            else dsmem_store_u64(&s_aggs[grank], g0 + q, v);
+        }
     }
     K6C_TRACE(4);
-    cluster_sync_all();                                        // 2: the earlier slices' summaries
+    // the earlier slices' summaries (a failed compress sends none: the whole group has the
+    // same key, hence the same status, and nothing is owed to it)
+    if (AS) { if (status == TLC_OK) mbar_wait(&s_mb_aggs, 0); }
+    else cluster_sync_all();                                   // 2: the earlier slices' summaries
     K6C_TRACE(5);
     const bool last = grank + 1 == gcnt;                       // holds the tensor's last row
     if (status != TLC_OK) {                                    // err untouched (R6)
@@ -507,21 +597,7 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
         }
         return;
     }
-    // the residuals (steps a, b) from shared memory to err first (bulk: in flight meanwhile)
-    if (bulk) {
-        if (threadIdx.x == 0) {
-#pragma unroll
-            for (int i = 0; i < 5; i++)
-                if (gc[i]) {
-                    const uint32_t o = (uint32_t)i * Ls + sh[i] + hd[i];
-                    bulk_store(S.err + (uint32_t)i * P + j0 + hd[i], u + o, 16u * gc[i]);
-                }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        uint32_t jj, i;
-        if (slice_edge(threadIdx.x - 32u, P, j0, len, n, i, jj))
-            __stcs(S.err + i * P + j0 + jj, u[i * Ls + ((i * P + j0) & 3u) + jj]);
-    }
+    if (!AS) store_err();                                      // err first (bulk: in flight meanwhile)
     if (!use_zre) {
         for (uint32_t jj = threadIdx.x; jj < len; jj += kGThreads) S.payload[j0 + jj] = B[jj];
     } else {
@@ -570,25 +646,6 @@ tlc_small_group_compress_kernel(const SegTable T, float s, int use_zre) {
         if (last && threadIdx.x == 0 && s_carry[nrows] > 0) {
             TLC_CHECK(s_off[nrows] < P);
             S.payload[s_off[nrows]] = run_code(s_carry[nrows]);
-        }
-    }
-    if (!bulk) {
-        for (uint32_t k = threadIdx.x; k < gmax; k += kGThreads) {
-#pragma unroll
-            for (int i = 0; i < 5; i++)
-                if (k < gc[i]) {
-                    const float *d = u + (uint32_t)i * Ls + hd[i] + 4 * k;
-                    __stcs(reinterpret_cast<float4 *>(S.err) + ((uint32_t)i * P + j0 + hd[i]) / 4 + k,
-                           make_float4(d[0], d[1], d[2], d[3]));
-                }
-        }
-        if (vec) {
-            uint32_t jj, i;
-            if (slice_edge(threadIdx.x, P, j0, len, n, i, jj)) __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
-        } else {
-            for (uint32_t i = 0; i < 5; i++)
-                for (uint32_t jj = threadIdx.x; jj < lim[i]; jj += kGThreads)
-                    __stcs(S.err + i * P + j0 + jj, u[i * Ls + jj]);
         }
     }
     if (grank == 0 && threadIdx.x == 0) {
@@ -695,13 +752,23 @@ static bool group_bulk() {
     return v == 1;
 }
 
-template <int CL, bool BULK>
+// TLC_K6G_SYNC=1: K6g's two cluster barriers instead of st.async + mbarriers (A/B)
+static bool group_async() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K6G_SYNC");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <int CL, bool BULK, bool AS>
 static int launch_group(const SegTable &T, float s, int use_zre, cudaStream_t st) {
     // u (and the T_in rows when copied in bulk), then B
     const uint32_t smem = (BULK ? 2u : 1u) * 4u * 5u * (((T.grp_maxlen + 3) & ~3u) + 4u) + T.grp_maxlen + 64u;
     static uint32_t attr = 0;
     if (smem > attr) {
-        cudaFuncSetAttribute(tlc_small_group_compress_kernel<CL, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tlc_small_group_compress_kernel<CL, BULK, AS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = smem;
     }
@@ -717,7 +784,7 @@ static int launch_group(const SegTable &T, float s, int use_zre, cudaStream_t st
     a[0].val.clusterDim.z = 1;
     cfg.attrs = a;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tlc_small_group_compress_kernel<CL, BULK>, T, s, use_zre) == cudaSuccess
+    return cudaLaunchKernelEx(&cfg, tlc_small_group_compress_kernel<CL, BULK, AS>, T, s, use_zre) == cudaSuccess
                ? TLC_OK : TLC_ERR_CUDA;
 }
 
@@ -1231,10 +1298,15 @@ int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t 
     }
     if (T.grp) {
         KernelScope ks(kK6s, st);
-        const bool b = group_bulk();
-        if (T.grp_cl == 8) return b ? launch_group<8, true>(T, s, use_zre, st) : launch_group<8, false>(T, s, use_zre, st);
-        if (T.grp_cl == 2) return b ? launch_group<2, true>(T, s, use_zre, st) : launch_group<2, false>(T, s, use_zre, st);
-        return b ? launch_group<4, true>(T, s, use_zre, st) : launch_group<4, false>(T, s, use_zre, st);
+        const bool b = group_bulk(), a = group_async();
+        if (T.grp_cl == 8)
+            return b ? (a ? launch_group<8, true, true>(T, s, use_zre, st) : launch_group<8, true, false>(T, s, use_zre, st))
+                     : (a ? launch_group<8, false, true>(T, s, use_zre, st) : launch_group<8, false, false>(T, s, use_zre, st));
+        if (T.grp_cl == 2)
+            return b ? (a ? launch_group<2, true, true>(T, s, use_zre, st) : launch_group<2, true, false>(T, s, use_zre, st))
+                     : (a ? launch_group<2, false, true>(T, s, use_zre, st) : launch_group<2, false, false>(T, s, use_zre, st));
+        return b ? (a ? launch_group<4, true, true>(T, s, use_zre, st) : launch_group<4, true, false>(T, s, use_zre, st))
+                 : (a ? launch_group<4, false, true>(T, s, use_zre, st) : launch_group<4, false, false>(T, s, use_zre, st));
     }
     static bool attr = false;
     if (!attr) {
