@@ -98,7 +98,8 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
         for (int k = 0; k < 5; k++) T.first[k] = d_first + (size_t)k * cnt;
     }
     if (T.max_n <= kSmallMaxN) {
-        const int rc = small_group_plan_build(T, host, &d_grp, grp_layout);
+        int rc = small_group_plan_build(T, host, &d_grp, grp_layout);
+        if (rc == TLC_OK) rc = small_dec_plan_build(T, host, &d_dec, dec_layout);
         if (rc != TLC_OK) return rc;
     }
     if (with_scratch && cnt > 1 && T.max_n <= kSmallMaxN && small_coop_enabled()) {
@@ -152,6 +153,10 @@ int Table::upload() {
         const int rc = small_group_plan_refresh(T, host, grp_layout);
         if (rc != TLC_OK) return rc;
     }
+    if (T.dec) {
+        const int rc = small_dec_plan_refresh(T, host, dec_layout);
+        if (rc != TLC_OK) return rc;
+    }
     return cudaMemcpy(d, host.data(), host.size() * sizeof(Seg), cudaMemcpyHostToDevice) == cudaSuccess
                ? TLC_OK : TLC_ERR_CUDA;
 }
@@ -180,6 +185,8 @@ void Table::release() {
     d_grp = nullptr;
     if (d_k12) cudaFree(d_k12);
     d_k12 = nullptr;
+    if (d_dec) cudaFree(d_dec);
+    d_dec = nullptr;
     d = nullptr;
     ws = nullptr;
 }

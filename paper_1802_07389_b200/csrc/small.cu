@@ -1254,6 +1254,159 @@ tlc_small_decompress_kernel(const SegTable T, int sub_log2) {
     }
 }
 
+// K7 over per-CTA records (default for small tables): the CTA's part, pointers and sizes
+// in one 48-byte record, so the header load is the first global access instead of the third
+// (no first-item table, no segment descriptor); otherwise the same steps as above.
+template <int kMode>
+__global__ void __launch_bounds__(kSmThreads)
+tlc_small_decompress_rec_kernel(const SegTable T) {
+    extern __shared__ __align__(16) uint8_t sm_raw[];
+    __shared__ uint16_t dig[256];                                // digit_i(b) at bits 2i
+    __shared__ uint32_t s_wsum[kSmWarps + 1];
+    __shared__ int s_bad;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const DecRec R = T.dec[blockIdx.x];
+    tlc_header *hdr = R.hdr;
+    const uint32_t n = R.n, P = R.P, jr0 = R.jr0, pl = R.pl;
+    const bool hv = header_valid(hdr, n);
+    // decoding step 1 for the 243 byte values while the header is in flight (as above)
+    for (int v = threadIdx.x; v < 256; v += kSmThreads) {
+        uint32_t r = v < 243 ? v : 121, pk = 0;
+#pragma unroll
+        for (int i = 4; i >= 0; i--) {
+            pk |= (r % 3u) << (2 * i);
+            r /= 3u;
+        }
+        dig[v] = (uint16_t)pk;
+    }
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if (!hv) {                                                   // uniform over the CTA
+        if (threadIdx.x == 0 && R.first && hdr->status == TLC_OK) raise_format(hdr);
+        return;
+    }
+    const uint32_t Z = (uint32_t)hdr->payload_len, jr1 = jr0 + pl;
+    const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
+    const float M = hdr->M, negM = -M;
+    uint8_t *E = sm_raw;                                         // quartic bytes [jr0, jr1)
+    if (zre) {
+        constexpr int kPer = 16;
+        const uint32_t b0 = kPer * threadIdx.x;
+        uint32_t wv[4] = {0, 0, 0, 0}, lens = 0;
+        if (b0 + kPer <= Z && aligned16(R.payload)) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(R.payload + b0));
+            wv[0] = v.x; wv[1] = v.y; wv[2] = v.z; wv[3] = v.w;
+            lens = word_len(wv[0]) + word_len(wv[1]) + word_len(wv[2]) + word_len(wv[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPer; k++)
+                if (b0 + k < Z) {
+                    const uint32_t b = R.payload[b0 + k];
+                    wv[k >> 2] |= b << (8 * (k & 3));
+                    lens += zre_len(b);
+                }
+        }
+        uint32_t x = lens;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_wsum[warp] = x;
+        for (uint32_t q = 16 * threadIdx.x; q < pl; q += 16 * kSmThreads) {   // 121 prefill
+            if (q + 16 <= pl) *reinterpret_cast<uint4 *>(E + q) = make_uint4(0x79797979u, 0x79797979u,
+                                                                             0x79797979u, 0x79797979u);
+            else for (uint32_t r = q; r < pl; r++) E[r] = kZeroGroup;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int k = 0; k < kSmWarps; k++) { const uint32_t v = s_wsum[k]; s_wsum[k] = acc; acc += v; }
+            s_wsum[kSmWarps] = acc;
+            if (acc != P) s_bad = 1;
+        }
+        __syncthreads();
+        if (s_bad) {
+            if (threadIdx.x == 0 && R.first) raise_format(hdr);
+            return;
+        }
+        uint32_t p = s_wsum[warp] + x - lens;
+        if (p < jr1 && p + lens > jr0) {
+#pragma unroll
+            for (int k = 0; k < kPer; k++) {
+                const uint32_t b = (wv[k >> 2] >> (8 * (k & 3))) & 0xffu;
+                if (b0 + k < Z && b < kFirstRunCode && p >= jr0 && p < jr1) E[p - jr0] = (uint8_t)b;   // literal
+                p += b0 + k < Z ? zre_len(b) : 0u;
+            }
+        }
+    } else {
+        for (uint32_t q = threadIdx.x; q < pl; q += kSmThreads) {
+            const uint8_t b = R.payload[jr0 + q];
+            if (b > 242) s_bad = 1;
+            E[q] = b;
+        }
+        __syncthreads();
+        if (s_bad) {
+            if (threadIdx.x == 0) raise_format(hdr);
+            return;
+        }
+    }
+    __syncthreads();
+    // ---- decoding steps 1-4 and Eq. 3: out = M * (d - 1) (bits of the fp32 product)
+    for (uint32_t jl = threadIdx.x; jl < pl; jl += kSmThreads) {
+        const uint32_t pk = dig[E[jl]];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint32_t e = (uint32_t)(i * P) + jr0 + jl;
+            if (e >= n) break;
+            const uint32_t d = (pk >> (2 * i)) & 3u;
+            const float v = d == 2u ? M : (d == 0u ? negM : 0.0f);
+            if (kMode == TLC_MODE_OVERWRITE) __stcs(R.out + e, v);
+            else if (d != 1u) R.out[e] = __fadd_rn(R.out[e], v);   // q != 0 (R16)
+        }
+    }
+}
+
+// TLC_K7_REC=0: K7 walks the segment table instead of taking per-CTA records (A/B)
+static bool dec_rec_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_K7_REC");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+int small_dec_plan_build(SegTable &T, const std::vector<Seg> &host, DecRec **d_dec, std::vector<uint4> &layout) {
+    T.dec = nullptr;
+    if (!dec_rec_enabled()) return TLC_OK;
+    constexpr uint32_t part = kSmPart >> 1;                      // 2048 positions per CTA (as sub_log2 = 1)
+    layout.clear();
+    for (size_t i = 0; i < host.size(); i++) {
+        const uint32_t P = (uint32_t)host[i].P;
+        for (uint32_t j = 0; j < P; j += part) layout.push_back(make_uint4((uint32_t)i, j, std::min(part, P - j), j == 0));
+    }
+    if (layout.empty() || layout.size() > 65535) return TLC_OK;
+    if (cudaMalloc((void **)d_dec, layout.size() * sizeof(DecRec)) != cudaSuccess) return TLC_ERR_CUDA;
+    T.dec = *d_dec;
+    T.dec_grid = (int)layout.size();
+    return TLC_OK;
+}
+
+int small_dec_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout) {
+    std::vector<DecRec> recs(layout.size());
+    for (size_t c = 0; c < layout.size(); c++) {
+        const uint4 &l = layout[c];
+        const Seg &S = host[l.x];
+        DecRec &r = recs[c];
+        r = DecRec{};
+        r.payload = S.payload; r.hdr = S.hdr; r.out = S.out;
+        r.n = (uint32_t)S.n; r.P = (uint32_t)S.P; r.jr0 = l.y; r.pl = l.z; r.first = l.w; r.seg = l.x;
+    }
+    return cudaMemcpy(const_cast<DecRec *>(T.dec), recs.data(), recs.size() * sizeof(DecRec),
+                      cudaMemcpyHostToDevice) == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+}
+
 static size_t small_smem_compress(uint64_t max_n) {
     return 4 * ((max_n + 3) & ~3ull) + ((max_n + 4) / 5 + 16);
 }
@@ -1340,6 +1493,11 @@ int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
         attr = true;
     }
     KernelScope ks(kK7s, st);
+    if (T.dec) {
+        if (mode == TLC_MODE_OVERWRITE) tlc_small_decompress_rec_kernel<0><<<T.dec_grid, kSmThreads, kSmPart, st>>>(T);
+        else tlc_small_decompress_rec_kernel<1><<<T.dec_grid, kSmThreads, kSmPart, st>>>(T);
+        return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
+    }
     const int sl = k7_sub_log2();
     const int grid = (int)tmin<uint64_t>(T.n5 << sl, 65535);
     const size_t smem = small_smem_decompress(T.max_n);

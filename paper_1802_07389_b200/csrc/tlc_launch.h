@@ -132,6 +132,17 @@ struct GrpRec {
 };
 static_assert(sizeof(GrpRec) == 64, "group records are 64 bytes");
 
+// A CTA of the K7 record launch (small.cu): quartic positions [jr0, jr0+pl) of a segment's
+// decode, with the segment's pointers and sizes; first = 1 for the segment's first part.
+struct DecRec {
+    const uint8_t *payload;
+    tlc_header *hdr;
+    float *out;
+    uint32_t n, P, jr0, pl;
+    uint32_t first, seg;
+};
+static_assert(sizeof(DecRec) == 48, "decode records are 48 bytes");
+
 struct SegTable {
     const Seg *d;                   // device table when count > 1
     Seg one;                        // the segment when count == 1
@@ -160,6 +171,8 @@ struct SegTable {
     // of consecutive L2-sized windows of tensors interleaved (k12 == nullptr: no plan)
     const uint32_t *k12;            // item = K2 tile index << 1 | (1: quantize, 0: max)
     uint32_t k12_n;
+    const DecRec *dec;              // K7 records (small tables; nullptr: K7 walks the table)
+    int dec_grid;
     const GrpRec *grp;
     int grp_grid;                   // CTAs (a multiple of grp_cl)
     int grp_cl;                     // cluster size
@@ -212,6 +225,8 @@ struct Table {
     GrpRec *d_grp = nullptr;        // the K6g plan (small tables only)
     uint32_t *d_k12 = nullptr;      // the K12 work list (tables of several tensors)
     std::vector<uint4> grp_layout;  // K6g CTAs on the host: (seg, j0, len, g0 | gcnt << 8 | grank << 16)
+    DecRec *d_dec = nullptr;        // the K7 records (small tables only)
+    std::vector<uint4> dec_layout;  // K7 CTAs on the host: (seg, jr0, pl, first)
     std::vector<uint4> sl_layout;   // K6c slices on the host: (seg, j0, len, k | last << 16)
     int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);
     int update(const tlc_tensor_desc *descs);
@@ -234,6 +249,8 @@ int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t 
 // the sizes only (the kernel takes the pointers from the table).  No-op when K6g is off.
 int small_group_plan_build(SegTable &T, const std::vector<Seg> &host, GrpRec **d_grp, std::vector<uint4> &layout);
 int small_group_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout);
+int small_dec_plan_build(SegTable &T, const std::vector<Seg> &host, DecRec **d_dec, std::vector<uint4> &layout);
+int small_dec_plan_refresh(const SegTable &T, const std::vector<Seg> &host, const std::vector<uint4> &layout);
 int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st);
 
 // K1 alone: per-segment max key of |err + t| (has_err) or |t| into maxkey[].

@@ -31,7 +31,8 @@ def test_cooperative_small_table_path():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"TLC_K6G": "0"}, {"TLC_K6G_BULK": "1"}, {"TLC_K6G": "8"}, {"TLC_K6G_SYNC": "1"}])
+@pytest.mark.parametrize("env", [{"TLC_K6G": "0"}, {"TLC_K6G_BULK": "1"}, {"TLC_K6G": "8"}, {"TLC_K6G_SYNC": "1"},
+                                 {"TLC_K7_REC": "0"}])
 def test_small_table_compressor_variants(env):
     """K6g (clusters of 4 CTAs per tensor group) is the small-table compressor; K6 (one CTA per
     tensor, TLC_K6G=0), K6g with bulk-copy staging (TLC_K6G_BULK=1) and clusters of 8 with
