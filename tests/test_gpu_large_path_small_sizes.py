@@ -34,9 +34,12 @@ def test_cooperative_small_table_path():
 @pytest.mark.parametrize("env", [{"TLC_K6G": "0"}, {"TLC_K6G_BULK": "1"}, {"TLC_K6G": "8"}, {"TLC_K6G_SYNC": "1"},
                                  {"TLC_K7_REC": "0"}])
 def test_small_table_compressor_variants(env):
-    """K6g (clusters of 4 CTAs per tensor group) is the small-table compressor; K6 (one CTA per
-    tensor, TLC_K6G=0), K6g with bulk-copy staging (TLC_K6G_BULK=1) and clusters of 8 with
-    one-row slices (TLC_K6G=8) stay selectable and must give the oracle's bytes too."""
+    """K6g (clusters of 4 CTAs per tensor group, st.async + mbarriers) is the small-table
+    compressor and K7 takes per-CTA records; K6 (one CTA per tensor, TLC_K6G=0), K6g with
+    bulk-copy staging (TLC_K6G_BULK=1), clusters of 8 with one-row slices (TLC_K6G=8), K6g with
+    two cluster barriers (TLC_K6G_SYNC=1) and the table-walking K7 (TLC_K7_REC=0) stay
+    selectable and must give the oracle's bytes too (test_gpu_batched: ResNet-110 and mixed
+    small tables, corrupt payloads, graphs)."""
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_batched.py",
                         "tests/test_gpu_exchange_loopback.py::test_loopback_graph_replay"],
                        cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
