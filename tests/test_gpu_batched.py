@@ -59,6 +59,20 @@ def test_resnet110_batched(T, s):
     _run_steps(T, sizes, 3, s, True, lambda k, n, step: synth.layer_gradient(n, mus[k], 2, 0, k, step))
 
 
+# small tables (every n <= 40,960): K6g cuts a tensor of r ZRE rows (1 KiB of quartic bytes
+# each) into min(4, ceil(r/2)) slices -- these sizes give groups of 1, 2, 3 and 4 slices with
+# uneven last rows, packed together into clusters of 4 -- and K7 takes 2048-position parts
+SMALL_GROUP_SIZES = [1, 2, 7, 432, 5120, 5121, 10240, 10241, 15361, 20481, 30721, 40960, 36864,
+                     9216, 2304, 640, 4608, 18432, 25603, 35839]
+
+
+@pytest.mark.parametrize("use_zre", [True, False])
+@pytest.mark.parametrize("s", [1.0, 1.9])
+def test_small_table_group_shapes(T, s, use_zre):
+    _run_steps(T, SMALL_GROUP_SIZES, 2, s, use_zre, lambda k, n, step: synth.runs_adversarial(n, 1.0, 9, k, step)
+               if k % 3 == 0 else synth.gaussian(n, 9, k, step))
+
+
 def test_mixed_sizes(T):
     sizes = list(range(1, 12)) + [69, 70, 71, 1000, 5 * 2048 + 3, 163_840, 163_841, 400_003, 5 * 65536 + 7]
     for use_zre in (True, False):
