@@ -182,6 +182,7 @@ struct K5Smem {
     alignas(16) uint8_t E[kT5];          // expanded quartic bytes of the tile
     uint32_t V[5][256];                  // Eq. 3 output bits of partition i for byte value b
     uint16_t lut[256];                   // per byte: bit i = (digit_i != 1)
+    uint16_t dig[256];                   // per byte: digit_i at bits 2i (no dependence on M)
     unsigned int warp_sum[kK5Threads / 32];
 };
 
@@ -341,7 +342,21 @@ __global__ void __launch_bounds__(kK5Threads, TLC_K5_MINB)   // <= 85 registers:
 tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     __shared__ K5Smem sm;
     __shared__ uint64_t s_first[kSegCache];
-    seg_index_load<5>(T, s_first);
+    // Decoding step 1, "dividing a by a power of 3 and taking the remainder", for
+    // the 243 byte values, once per CTA: the digits and the nonzero mask do not depend on M
+    for (int v = threadIdx.x; v < 256; v += kK5Threads) {
+        uint32_t w = 0, pk = 0, r = v < 243 ? v : 121;
+#pragma unroll
+        for (int i = 4; i >= 0; i--) {
+            const uint32_t d = r % 3u;
+            r /= 3u;
+            w |= (uint32_t)(d != 1) << i;
+            pk |= d << (2 * i);
+        }
+        sm.lut[v] = (uint16_t)w;
+        sm.dig[v] = (uint16_t)pk;
+    }
+    seg_index_load<5>(T, s_first);                       // (ends with __syncthreads)
     pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
     for (uint64_t tile = blockIdx.x; tile < T.n5; tile += gridDim.x) {
@@ -356,19 +371,16 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
         const uint8_t *__restrict__ payload = S.payload;
         __syncthreads();   // previous tile's readers of sm.E / sm.V are done
         if (si != cur) {
-            // Decoding step 1, "dividing a by a power of 3 and taking the remainder"
-            // (P:514-515), for the 243 byte values, and Eq. 3 per partition:
-            // V[i][b] = M * (digit_i(b) - 1) -- the same single fp32 multiply.
+            // Eq. 3 per partition: V[i][b] = M * (digit_i(b) - 1), taken as a selection
+            // of {-M, +0, M} -- the bits of the fp32 product (M >= +0, validated by K4)
+            const uint32_t mb = __float_as_uint(M), nmb = __float_as_uint(-M);
             for (int v = threadIdx.x; v < 256; v += kK5Threads) {
-                uint32_t w = 0, r = v < 243 ? v : 121;
+                const uint32_t pk = sm.dig[v];
 #pragma unroll
-                for (int i = 4; i >= 0; i--) {
-                    const uint32_t d = r % 3u;
-                    r /= 3u;
-                    w |= (uint32_t)(d != 1) << i;
-                    sm.V[i][v] = __float_as_uint(__fmul_rn(M, (float)((int)d - 1)));
+                for (int i = 0; i < 5; i++) {
+                    const uint32_t d = (pk >> (2 * i)) & 3u;
+                    sm.V[i][v] = d == 2u ? mb : (d == 0u ? nmb : 0u);
                 }
-                sm.lut[v] = (uint16_t)w;
             }
             cur = si;
         }
