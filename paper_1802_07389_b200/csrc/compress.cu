@@ -1306,10 +1306,11 @@ static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_e
     k2(maxkey, scratch);
     if (use_zre) {
         KernelScope ks(kK3, st);
-        if (!g_k3_blocks) {
+        static PerDevice k3attr;
+        if (k3attr.first())
             cudaFuncSetAttribute(tlc_zre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K3Smem));
+        if (!g_k3_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k3_blocks, tlc_zre_kernel, kK3Threads, sizeof(K3Smem));
-        }
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(T.n3, (uint64_t)sms * tmin(16, tmax(1, g_k3_blocks))));
         launch_pdl(tlc_zre_kernel, grid, kK3Threads, sizeof(K3Smem), st, T, maxkey, s, scratch, ctrl, states);
     }
@@ -1430,15 +1431,14 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
         const uint64_t nbulk = use_bulk() ? bulk_tiles(T, use_zre) : 0;
         uint64_t tile_begin = 0;
         int skip_bulk = 0;
-        static bool attr = false;
-        if (!attr) {
+        static PerDevice attr;
+        if (attr.first()) {
             cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BulkSmem));
             cudaFuncSetAttribute(tlc_quant_qe_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BulkSmem));
             cudaFuncSetAttribute(tlc_quant_qe_bulk_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(BulkSmem));
-            attr = true;
         }
         if (nbulk) {
             const int grid = (int)tmin<uint64_t>(nbulk, (uint64_t)sms);

@@ -910,14 +910,14 @@ __host__ __device__ constexpr size_t k5p_smem_bytes() { return (size_t)WP * kT5 
 
 template <int WP>
 static void launch_par(const SegTable &A, const SegTable &X, int W, const unsigned long long *seek, cudaStream_t st) {
-    static bool attr = false;
+    static PerDevice attr;
     static int per_sm = 0;
-    if (!attr) {
+    if (attr.first()) {
         cudaFuncSetAttribute(tlc_aggregate_par_kernel<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k5p_smem_bytes<WP>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_par_kernel<WP>, kK5Threads,
-                                                      k5p_smem_bytes<WP>());
-        attr = true;
+        if (!per_sm)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_par_kernel<WP>, kK5Threads,
+                                                          k5p_smem_bytes<WP>());
     }
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)num_sms() * tmax(1, per_sm)));
     launch_pdl(tlc_aggregate_par_kernel<WP>, grid, kK5Threads, k5p_smem_bytes<WP>(), st, A, X, W, seek);
@@ -957,12 +957,10 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
         else launch_par<8>(A, X, W, seek, st);
         return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
     }
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first())
         cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k5m_smem_bytes(kMaxSources));
-        attr = true;
-    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_kernel, kK5Threads, k5m_smem_bytes(W));
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)sms * tmax(1, per_sm)));

@@ -25,19 +25,19 @@ static const char *kNames[kNumKernelIds] = {"k1_absmax", "k2_quant_qe", "k3_zre"
 
 namespace {
 struct Rec {
-    int id;
+    int id, dev;
     cudaEvent_t a, b;
 };
 std::atomic<unsigned long long> g_launches{0};
 std::atomic<bool> g_on{false};
 std::mutex g_mu;
 std::vector<Rec> g_recs;
-std::vector<cudaEvent_t> g_pool;
+std::vector<cudaEvent_t> g_pool[64];                 // per device: an event records only on its device's streams
 
-cudaEvent_t get_event() {
-    if (!g_pool.empty()) {
-        cudaEvent_t e = g_pool.back();
-        g_pool.pop_back();
+cudaEvent_t get_event(int dev) {
+    if (!g_pool[dev].empty()) {
+        cudaEvent_t e = g_pool[dev].back();
+        g_pool[dev].pop_back();
         return e;
     }
     cudaEvent_t e;
@@ -50,7 +50,8 @@ KernelScope::KernelScope(int id, cudaStream_t st) : id_(id), st_(st), a_(nullptr
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (g_on.load(std::memory_order_relaxed)) {
         std::lock_guard<std::mutex> lk(g_mu);
-        a_ = get_event();
+        dev_ = cur_device();
+        a_ = get_event(dev_);
         cudaEventRecord((cudaEvent_t)a_, st_);
     }
 }
@@ -58,9 +59,9 @@ KernelScope::KernelScope(int id, cudaStream_t st) : id_(id), st_(st), a_(nullptr
 KernelScope::~KernelScope() {
     if (a_) {
         std::lock_guard<std::mutex> lk(g_mu);
-        cudaEvent_t b = get_event();
+        cudaEvent_t b = get_event(dev_);
         cudaEventRecord(b, st_);
-        g_recs.push_back(Rec{id_, (cudaEvent_t)a_, b});
+        g_recs.push_back(Rec{id_, dev_, (cudaEvent_t)a_, b});
     }
 }
 
@@ -96,8 +97,8 @@ int tlc_prof_collect(tlc_prof_entry *out, int cap) {
         cudaEventElapsedTime(&t, r.a, r.b);
         ms[r.id] += t;
         cnt[r.id] += 1;
-        g_pool.push_back(r.a);
-        g_pool.push_back(r.b);
+        g_pool[r.dev].push_back(r.a);
+        g_pool[r.dev].push_back(r.b);
     }
     g_recs.clear();
     int k = 0;

@@ -766,11 +766,12 @@ template <int CL, bool BULK, bool AS>
 static int launch_group(const SegTable &T, float s, int use_zre, cudaStream_t st) {
     // u (and the T_in rows when copied in bulk), then B
     const uint32_t smem = (BULK ? 2u : 1u) * 4u * 5u * (((T.grp_maxlen + 3) & ~3u) + 4u) + T.grp_maxlen + 64u;
-    static uint32_t attr = 0;
-    if (smem > attr) {
+    static uint32_t attr[64] = {};                             // per device (tlc_launch.h PerDevice)
+    const int dv = cur_device();
+    if (smem > attr[dv]) {
         cudaFuncSetAttribute(tlc_small_group_compress_kernel<CL, BULK, AS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attr = smem;
+        attr[dv] = smem;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(T.grp_grid);
@@ -1426,14 +1427,13 @@ bool small_table(const SegTable &T) { return T.max_n <= kSmallMaxN && small_enab
 
 int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t st) {
     if (T.sl && small_coop_enabled()) {
-        static bool cattr = false;
-        if (!cattr) {
+        static PerDevice cattr;
+        if (cattr.first()) {
             int dev = 0, optin = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
             cudaFuncSetAttribute(tlc_small_coop_compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - 4096);
-            cattr = true;
         }
         KernelScope ks(kK6s, st);
         cudaLaunchConfig_t cfg{};
@@ -1461,12 +1461,10 @@ int launch_small_compress(const SegTable &T, float s, int use_zre, cudaStream_t 
         return b ? (a ? launch_group<4, true, true>(T, s, use_zre, st) : launch_group<4, true, false>(T, s, use_zre, st))
                  : (a ? launch_group<4, false, true>(T, s, use_zre, st) : launch_group<4, false, false>(T, s, use_zre, st));
     }
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first())
         cudaFuncSetAttribute(tlc_small_compress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)small_smem_compress(kSmallMaxN));
-        attr = true;
-    }
     KernelScope ks(kK6s, st);
     const int grid = (int)tmin<uint64_t>((uint64_t)T.count, 65535);
     tlc_small_compress_kernel<<<grid, kSmThreads, small_smem_compress(T.max_n), st>>>(T, s, use_zre);
@@ -1484,13 +1482,12 @@ static int k7_sub_log2() {
 }
 
 int launch_small_decompress(const SegTable &T, int mode, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr;
+    if (attr.first()) {
         cudaFuncSetAttribute(tlc_small_decompress_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)small_smem_decompress(kSmallMaxN));
         cudaFuncSetAttribute(tlc_small_decompress_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)small_smem_decompress(kSmallMaxN));
-        attr = true;
     }
     KernelScope ks(kK7s, st);
     if (T.dec) {

@@ -52,6 +52,24 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Once per device: a kernel's attributes (cudaFuncSetAttribute, e.g. its dynamic shared
+// memory limit) belong to the current device's context, so a process driving several GPUs
+// sets them on each.
+inline int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+}
+struct PerDevice {
+    bool done[64] = {};
+    bool first() {
+        const int d = cur_device();
+        if (done[d]) return false;
+        done[d] = true;
+        return true;
+    }
+};
+
 // Kernel ids for launch counting / profiling (prof.cu).
 enum KernelId { kK1 = 0, kK2 = 1, kK3 = 2, kK4 = 3, kK5 = 4, kK6 = 5, kK7 = 6, kK8 = 7,
                 kK2s = 8, kKq8 = 9, kKd8 = 10, kK6s = 11, kK7s = 12, kK12 = 13, kNumKernelIds = 14 };
@@ -68,6 +86,7 @@ class KernelScope {
     int id_;
     cudaStream_t st_;
     void *a_;
+    int dev_ = 0;
 };
 
 // ---------------------------------------------------------------- segments
