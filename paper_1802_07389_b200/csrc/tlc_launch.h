@@ -103,7 +103,10 @@ struct ItemSizes {
     uint64_t c3;    // K3 chunk: quartic bytes (8 warps x rows of 1 KiB)
     uint64_t c4;    // K4 chunk: payload bytes (capacity based)
 };
-constexpr ItemSizes kLargeItems{65536, 4096, 32768, 16384};
+#ifndef TLC_K4_CHUNK
+#define TLC_K4_CHUNK 16384                 // K4 chunk of large tables (A/B builds: 32768, 65536)
+#endif
+constexpr ItemSizes kLargeItems{65536, 4096, 32768, TLC_K4_CHUNK};
 constexpr ItemSizes kSmallItems{8192, 1024, 8192, 4096};
 constexpr uint64_t kSmallTableElems = 32ull << 20;   // tables below 32M values use kSmallItems
 constexpr uint64_t kT5 = 4096;      // K5 tile: quartic positions per output tile
