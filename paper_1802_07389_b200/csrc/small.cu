@@ -1381,7 +1381,9 @@ static bool dec_rec_enabled() {
 int small_dec_plan_build(SegTable &T, const std::vector<Seg> &host, DecRec **d_dec, std::vector<uint4> &layout) {
     T.dec = nullptr;
     if (!dec_rec_enabled()) return TLC_OK;
-    constexpr uint32_t part = kSmPart >> 1;                      // 2048 positions per CTA (as sub_log2 = 1)
+    // 2048 positions per CTA (as sub_log2 = 1); TLC_K7_PART=1024 / 4096 for A/B
+    const char *pe = getenv("TLC_K7_PART");
+    const uint32_t part = pe && (atoi(pe) == 1024 || atoi(pe) == 4096) ? (uint32_t)atoi(pe) : kSmPart >> 1;
     layout.clear();
     for (size_t i = 0; i < host.size(); i++) {
         const uint32_t P = (uint32_t)host[i].P;
