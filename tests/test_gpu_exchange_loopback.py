@@ -128,6 +128,17 @@ def test_loopback_large_contexts(W):
     _check(W, _run_group(W, SIZES_LARGE, 1.75, "gauss"), SIZES_LARGE, 1.75, "gauss")
 
 
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_loopback_resnet110_small_tables(W):
+    """BASELINE configs[3] (C4): ResNet-110's 110 layers -- every context is a small tensor, so
+    the pushes and the owners' pulls are compressed by K6g (clusters) and the applies
+    decompressed by K7 over records; owners' means, error buffers and outputs bit for bit."""
+    import synth
+
+    sizes = synth.RESNET110_SIZES
+    _check(W, _run_group(W, sizes, 1.75, "gauss", steps=2), sizes, 1.75, "gauss", steps=2)
+
+
 @pytest.mark.parametrize("W", [1, 5])
 def test_loopback_graph_replay(W):
     _check(W, _run_group(W, SIZES_SMALL, 1.75, "gauss", graph=True), SIZES_SMALL, 1.75, "gauss")
