@@ -614,6 +614,11 @@ def measure_exchange(T, dev, world, rank, model, s, steps, warmup, dist=None, p2
     # K5m's 4 n_own of means, the pull's K1 + K2 over the owned contexts
     n_own = sum(hi - lo for (_, lo, hi, ow) in plan if ow == rank)
     step_bytes = 8 * N + k2_push + 4 * n_own + 8 * n_own + k2_pull
+    keyed = n_own > 0 and "k1_absmax" in prof and prof["k1_absmax"][0] / steps < 1.5
+    if keyed:
+        # the pull compress's K1 folded into K5m (one K1 launch per step): K5m reads the pull
+        # error buffer (4 n_own) instead of K1 reading mean and error buffer (8 n_own)
+        step_bytes = 8 * N + k2_push + 4 * n_own + 4 * n_own + k2_pull
     if "k12_absmax_quant" in prof:
         # K12 reads t and err from HBM once (its quantize items hit L2): no K1 terms
         step_bytes = k2_push + 4 * n_own + k2_pull
@@ -744,7 +749,8 @@ def exchange_roofline(r, step_ms=None):
             "step_alg_bytes_formula": ("sum(12 n_c + ceil(n_c/5)) (push K12: t, err read once) + 4 n_own (K5m "
                                        "means) + sum_own(12 n_c + ceil(n_c/5)) (pull K12)" if fused else
                                        "8N + sum(12 n_c + ceil(n_c/5)) (push K1, K2) + 4 n_own (K5m means) + "
-                                       "8 n_own + sum_own(12 n_c + ceil(n_c/5)) (pull K1, K2)") +
+                                       "8 n_own (pull K1; 4 n_own when K5m folds the pull's keys, reading the "
+                                       "pull error buffer) + sum_own(12 n_c + ceil(n_c/5)) (pull K2)") +
                                       "; payload bytes and the apply's skip-zero read-modify-writes omitted "
                                       "(lower bound); rank 0",
             "frac": achieved / peak, "traffic": None, "peak_source": peak_src,

@@ -1293,7 +1293,7 @@ void launch_absmax(const SegTable &T, unsigned int *maxkey, bool has_err, cudaSt
 // K1 (max key), then `k2` (the quantizer + quartic pass of the codec), then K3 (ZRE).
 template <class K2Launch>
 static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_err, void *ws, cudaStream_t st,
-                             const K2Launch &k2, bool fused_k1 = false) {
+                             const K2Launch &k2, bool fused_k1 = false, bool zeroed = false) {
     const WsLayout L = ws_layout(T, 0);
     char *base = reinterpret_cast<char *>(ws);
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
@@ -1301,8 +1301,8 @@ static int compress_pipeline(const SegTable &T, float s, int use_zre, bool has_e
     unsigned long long *states = reinterpret_cast<unsigned long long *>(base + L.k3st);
     uint8_t *scratch = reinterpret_cast<uint8_t *>(base + L.bytes);
     const int sms = num_sms();
-    if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
-    if (!fused_k1) launch_absmax(T, maxkey, has_err, st);   // K12 folds K1 into its items
+    if (!zeroed && cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
+    if (!fused_k1) launch_absmax(T, maxkey, has_err, st);   // K12 / the keyed aggregate fold K1 in
     k2(maxkey, scratch);
     if (use_zre) {
         KernelScope ks(kK3, st);
@@ -1404,7 +1404,27 @@ int k12_plan_build(SegTable &T, const std::vector<Seg> &host, uint32_t **d_k12) 
 
 static int g_k12_blocks = 0;
 
+static int launch_compress_table_impl(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st, bool keyed);
+
 int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+    return launch_compress_table_impl(T, s, use_zre, ws, st, false);
+}
+
+bool compress_runs_k1(const SegTable &T) { return !small_table(T) && !(T.k12 && k12_enabled()); }
+
+int prepare_keyed_compress(const SegTable &T, void *ws, cudaStream_t st, unsigned int **keys) {
+    const WsLayout L = ws_layout(T, 0);
+    if (cudaMemsetAsync(ws, 0, L.memset_c, st) != cudaSuccess) return TLC_ERR_CUDA;
+    *keys = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(ws) + L.maxkey);
+    return TLC_OK;
+}
+
+int launch_compress_table_keyed(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st) {
+    if (!compress_runs_k1(T)) return TLC_ERR_ARG;
+    return launch_compress_table_impl(T, s, use_zre, ws, st, true);
+}
+
+static int launch_compress_table_impl(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st, bool keyed) {
     if (small_table(T)) return launch_small_compress(T, s, use_zre, st);    // one launch, on chip
     const int sms = num_sms();
     if (T.k12 && k12_enabled()) {
@@ -1478,7 +1498,7 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
             launch_pdl(tlc_quant_qe_kernel, rgrid, kK2Threads, 0, st, T, maxkey, s, use_zre, scratch, tile_begin,
                        skip_bulk);
         }
-    });
+    }, keyed, keyed);
 }
 
 // "Stoch 3-value + QE": K1 over t alone (m = max|t|, s = 1), the

@@ -672,9 +672,10 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
 #ifndef TLC_K5P_MINB
 #define TLC_K5P_MINB 4
 #endif
-template <int WP>
-__global__ void __launch_bounds__(kK5Threads, WP == 8 ? 3 : TLC_K5P_MINB)
-tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek) {
+template <int WP, bool KEYED>
+__global__ void __launch_bounds__(kK5Threads, (WP == 8 || KEYED) ? 3 : TLC_K5P_MINB)
+tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsigned long long *seek,
+                         const SegTable K, unsigned int *__restrict__ keys) {
     constexpr int TP = kK5Threads / WP;                  // threads per source
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ uint64_t s_first[kK5mSegCache];
@@ -701,6 +702,10 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
         const uint64_t P = S.P, n = S.n, lt = tile - S.k5, ntiles = (P + kT5 - 1) / kT5;
         const uint64_t J0 = lt * kT5;
         const int tl = (int)tmin<uint64_t>(kT5, P - J0);
+        // keys: the max key of u = err + mean over this tile (K1 of the owner's pull compress,
+        // which then skips K1), err = the pull table's error buffer of the same context
+        const float *kerr = KEYED ? get_seg(K, q).err : nullptr;
+        unsigned int kmax = 0;
         // every thread of group g reads source g's row (the same addresses: broadcast)
         const bool src = g < W;
         Seg R{};
@@ -863,6 +868,24 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
             for (int i = 0; i < 5; i++)
 #pragma unroll
                 for (int c = 0; c < 4; c++) acc[i][c] = 0.0f;     // +0 (R15)
+            // KEYED: the err values of this step's 20 elements, loaded before the fold so their
+            // latency hides behind it
+            float ev[5][4];
+            if (KEYED) {
+#pragma unroll
+                for (int i = 0; i < 5; i++) {
+                    const uint64_t e0 = (uint64_t)i * P + J0;
+                    const int lim = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
+                    const float *ep = kerr + e0 + jl;
+                    if (((reinterpret_cast<uintptr_t>(ep) & 15u) == 0) && jl + 3 < lim) {
+                        const float4 v = __ldcg(reinterpret_cast<const float4 *>(ep));
+                        ev[i][0] = v.x; ev[i][1] = v.y; ev[i][2] = v.z; ev[i][3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; c++) ev[i][c] = jl + c < lim ? __ldcg(ep + c) : 0.0f;
+                    }
+                }
+            }
             bool any = false;
             for (uint32_t m = okmask; m; m &= m - 1u) {            // rank order (ascending bits)
                 const int w = (int)ctz32(m);
@@ -901,6 +924,21 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
                         if (jl + c < lim) o[c] = r[c];
                 }
             }
+            if (KEYED) {                                           // step (1) and K1's key, fused
+#pragma unroll
+                for (int i = 0; i < 5; i++) {
+                    const uint64_t e0 = (uint64_t)i * P + J0;
+                    const int lim = e0 >= n ? 0 : (int)tmin<uint64_t>(tl, n - e0);
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        if (jl + c < lim)
+                            kmax = max(kmax, __float_as_uint(__fadd_rn(ev[i][c], acc[i][c])) & 0x7fffffffu);
+                }
+            }
+        }
+        if (KEYED) {
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            if (lane == 0 && kmax) atomicMax(keys + q, kmax);
         }
     }
 }
@@ -908,19 +946,27 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
 template <int WP>
 __host__ __device__ constexpr size_t k5p_smem_bytes() { return (size_t)WP * kT5 + (size_t)WP * 5 * 256 * sizeof(uint32_t); }
 
-template <int WP>
-static void launch_par(const SegTable &A, const SegTable &X, int W, const unsigned long long *seek, cudaStream_t st) {
+template <int WP, bool KEYED>
+static void launch_par_k(const SegTable &A, const SegTable &X, int W, const unsigned long long *seek, cudaStream_t st,
+                         const SegTable &K, unsigned int *keys) {
     static PerDevice attr;
     static int per_sm = 0;
     if (attr.first()) {
-        cudaFuncSetAttribute(tlc_aggregate_par_kernel<WP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tlc_aggregate_par_kernel<WP, KEYED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)k5p_smem_bytes<WP>());
         if (!per_sm)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_par_kernel<WP>, kK5Threads,
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tlc_aggregate_par_kernel<WP, KEYED>, kK5Threads,
                                                           k5p_smem_bytes<WP>());
     }
     const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(A.n5, (uint64_t)num_sms() * tmax(1, per_sm)));
-    launch_pdl(tlc_aggregate_par_kernel<WP>, grid, kK5Threads, k5p_smem_bytes<WP>(), st, A, X, W, seek);
+    launch_pdl(tlc_aggregate_par_kernel<WP, KEYED>, grid, kK5Threads, k5p_smem_bytes<WP>(), st, A, X, W, seek, K,
+               keys);
+}
+template <int WP>
+static void launch_par(const SegTable &A, const SegTable &X, int W, const unsigned long long *seek, cudaStream_t st,
+                       const SegTable *K, unsigned int *keys) {
+    if (K && keys) launch_par_k<WP, true>(A, X, W, seek, st, *K, keys);
+    else launch_par_k<WP, false>(A, X, W, seek, st, A, nullptr);
 }
 
 // TLC_K5M_SEQ=1 runs the sources-in-sequence kernel at every W (A/B)
@@ -933,7 +979,10 @@ static bool k5m_seq() {
     return v == 1;
 }
 
-int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st) {
+bool aggregate_keyable(int W) { return W > 1 && W <= kMaxSources && !k5m_seq(); }
+
+int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st, const SegTable *K,
+                     unsigned int *keys) {
     // X: K4 over every received payload (validation + seek entries), then one fused pass
     if (W < 1 || W > kMaxSources) return TLC_ERR_ARG;
     const WsLayout L = ws_layout(X, 0);
@@ -952,11 +1001,12 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
     KernelScope ks(kK6, st);
     // W = 1: the sequential kernel (one source either way; 0.346 vs 0.374 ms, BERT-large)
     if (!k5m_seq() && W > 1) {
-        if (W == 2) launch_par<2>(A, X, W, seek, st);
-        else if (W <= 4) launch_par<4>(A, X, W, seek, st);
-        else launch_par<8>(A, X, W, seek, st);
+        if (W == 2) launch_par<2>(A, X, W, seek, st, K, keys);
+        else if (W <= 4) launch_par<4>(A, X, W, seek, st, K, keys);
+        else launch_par<8>(A, X, W, seek, st, K, keys);
         return cudaPeekAtLastError() == cudaSuccess ? TLC_OK : TLC_ERR_CUDA;
     }
+    if (keys) return TLC_ERR_ARG;                                // keyed only with the parallel kernel
     static PerDevice attr;
     if (attr.first())
         cudaFuncSetAttribute(tlc_aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

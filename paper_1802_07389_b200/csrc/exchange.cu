@@ -187,6 +187,7 @@ struct tlc_exchange {
     // push / apply tables cached for the two most recent pointer sets (a caller that
     // double-buffers its gradients or outputs alternates between two without re-uploads)
     Table push_tab[2], pullc_tab, apply_tab[2], a_tab, x_tab;
+    bool keyed = false;                // this step's K5m folded the pull compress's max keys
     // peer-memory mode (tlc_exchange_ipc_*): the owner's kernels read the pushed
     // payloads and every rank reads the pulled payloads straight from the producing
     // rank's buffers over NVLink; two flag barriers per step order the phases
@@ -673,14 +674,37 @@ static int phase_push_compress(tlc_exchange *x, const float *const *grads, float
 
 // (2) owner: fused decompress-aggregate of the W pushes of every owned context,
 //     rank-ordered sum from +0 of the nonzero trits, then / W (R15), written once
+// TLC_NO_KEYED=1: the pull compress runs its own K1 instead of taking the keys the fused
+// aggregate folded while it wrote the means (A/B)
+static bool keyed_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_NO_KEYED");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int phase_aggregate(tlc_exchange *x, cudaStream_t st) {
+    x->keyed = false;
     if (!x->owned_elems) return TLC_OK;
+    // the pull compress's K1 (max |pull_err + mean| per owned context) folded into K5m, which
+    // has the means in registers as it writes them: one launch and 8 n_own bytes less
+    if (keyed_enabled() && aggregate_keyable(x->W) && compress_runs_k1(x->pullc_tab.T) &&
+        x->pullc_tab.count == x->a_tab.count) {
+        unsigned int *keys = nullptr;
+        int rc = prepare_keyed_compress(x->pullc_tab.T, x->pullc_tab.ws, st, &keys);
+        if (rc == TLC_OK) rc = launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st, &x->pullc_tab.T, keys);
+        x->keyed = rc == TLC_OK;
+        return rc;
+    }
     return launch_aggregate(x->a_tab.T, x->x_tab.T, x->W, x->x_tab.ws, st);
 }
 
 // (3) the owner compresses its shard of the model delta ONCE (shared pull)
 static int phase_pull_compress(tlc_exchange *x, float s, int use_zre, cudaStream_t st) {
     if (!x->owned_elems) return TLC_OK;
+    if (x->keyed) return launch_compress_table_keyed(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st);
     return launch_compress_table(x->pullc_tab.T, s, use_zre ? 1 : 0, x->pullc_tab.ws, st);
 }
 

@@ -284,6 +284,15 @@ int launch_stoch_compress_table(const SegTable &T, uint64_t seed, uint64_t step,
                                 cudaStream_t st);
 int launch_int8_compress(const float *t, uint64_t n, int8_t *codes, tlc_header *hdr, void *ws, cudaStream_t st);
 int launch_int8_decompress(const int8_t *codes, tlc_header *hdr, uint64_t n, float *out, int mode, cudaStream_t st);
-int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st);
+// keys (optional, W >= 2): K1's max keys of u = K.err + mean per context of A (K = the
+// owner's pull compress table, same context order), folded by atomicMax into `keys`
+int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cudaStream_t st,
+                     const SegTable *K = nullptr, unsigned int *keys = nullptr);
+// the compress path of a table takes its max keys from elsewhere (K1 skipped, workspace
+// control block, keys and scan states zeroed by prepare_keyed_compress beforehand)
+int prepare_keyed_compress(const SegTable &T, void *ws, cudaStream_t st, unsigned int **keys);
+int launch_compress_table_keyed(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st);
+bool compress_runs_k1(const SegTable &T);
+bool aggregate_keyable(int W);                 // the parallel K5m (W >= 2) can fold the keys
 
 }  // namespace tlc
