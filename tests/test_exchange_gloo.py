@@ -5,7 +5,7 @@ with the oracle as the codec; every rank must end bit-identical to the
 single-process W-virtual-rank oracle.  The product's plan is computed by
 libtlc on each rank (host code, no GPU) and must agree across ranks."""
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -44,9 +44,7 @@ def _recv_payload(src):
 
 
 def _worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     try:
         import oracle as O
         import paper_1802_07389_b200 as T
@@ -95,10 +93,8 @@ def _worker(rank, world, port, q):
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
+    # rendezvous through a file (FileStore): no port to race for with other processes
+    p = os.path.join(tempfile.mkdtemp(prefix="tlc_rdv_"), "store")
     return p
 
 

@@ -3,7 +3,7 @@ the hook receives and returns is recorded; the returned reduced gradients must e
 bit for bit, the W-virtual-rank oracle (oracle/exchange.py) run on the recorded
 per-rank bucket gradients, step after step (error buffers carried per bucket)."""
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -19,10 +19,9 @@ def _worker(rank, world, port, q, p2p, batch=False, nan_step=-1):
 
     from paper_1802_07389_b200.ddp import TLCHookState, tlc_hook
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    dist.init_process_group("nccl", init_method="file://" + port, rank=rank, world_size=world, device_id=dev)
     try:
         torch.manual_seed(0)
         model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 300),
@@ -64,10 +63,8 @@ def _worker(rank, world, port, q, p2p, batch=False, nan_step=-1):
 def _launch(world, p2p, batch=False, nan_step=-1):
     import torch.multiprocessing as mp
 
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
+    # rendezvous through a file (FileStore): no port to race for with other processes
+    port = os.path.join(tempfile.mkdtemp(prefix="tlc_rdv_"), "store")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q, p2p, batch, nan_step)) for r in range(world)]
@@ -140,10 +137,8 @@ def test_ddp_hook_world1_on_one_gpu(batch):
     exchanges all buckets of a step together."""
     import torch.multiprocessing as mp
 
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
+    # rendezvous through a file (FileStore): no port to race for with other processes
+    port = os.path.join(tempfile.mkdtemp(prefix="tlc_rdv_"), "store")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = ctx.Process(target=_worker, args=(0, 1, port, q, True, batch, -1))

@@ -4,7 +4,7 @@ push / pull error buffer, bit for bit, eagerly and (peer-memory transport) repla
 from CUDA graphs.  W = 1 runs in-process; W = 2, 4 spawn one process per GPU when the
 box has them."""
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -122,9 +122,9 @@ def _mp_worker(rank, world, port, q, p2p, graph=False, kind="gauss", exact=False
     import torch
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    dist.init_process_group("nccl", init_method="file://" + port, rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
     try:
         res = _run_rank(rank, world, STEPS, p2p=p2p, graph=graph, kind=kind, exact=exact)
         q.put((rank, res))
@@ -142,10 +142,8 @@ def test_exchange_multi_gpu(world, p2p, graph, kind, exact):
 
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
+    # rendezvous through a file (FileStore): no port to race for with other processes
+    port = os.path.join(tempfile.mkdtemp(prefix="tlc_rdv_"), "store")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_mp_worker, args=(r, world, port, q, p2p, graph, kind, exact)) for r in range(world)]
