@@ -558,10 +558,18 @@ struct PadStage {
 #if defined(TLC_DEVICE_CHECKS) && defined(__CUDA_ARCH__)
         TLC_CHECK(q + ((q >> 7) << 2) < cap);
 #endif
+#ifdef TLC_NO_PAD
+        return p[q];                                   // A/B: unpadded stage
+#else
         return p[q + ((q >> 7) << 2)];
+#endif
     }
 };
+#ifdef TLC_NO_PAD
+__host__ __device__ constexpr uint32_t pad_stage_bytes(uint32_t n) { return n; }
+#else
 __host__ __device__ constexpr uint32_t pad_stage_bytes(uint32_t n) { return n + ((n + 127) >> 7) * 4; }
+#endif
 
 // Prefill logical bytes [0, n) of a padded stage with 255 (32-bit stores).
 __device__ __forceinline__ void pad_stage_fill(const PadStage &st, uint32_t n) {
