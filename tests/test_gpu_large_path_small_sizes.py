@@ -55,3 +55,14 @@ def test_fused_max_quantize_table_path():
                         "tests/test_gpu_exchange_loopback.py::test_loopback_bert_large_full_size_sampled"],
                        cwd=ROOT, env=dict(os.environ, TLC_K12="1"), capture_output=True, text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_unkeyed_pull_compress():
+    """TLC_NO_KEYED=1: the owner's pull compress runs its own K1 instead of taking the max keys
+    the parallel K5m folds while writing the means; both must give the oracle's bytes."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_matches_oracle",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_large_contexts",
+                        "tests/test_gpu_exchange_loopback.py::test_loopback_failed_push_poisons_context"],
+                       cwd=ROOT, env=dict(os.environ, TLC_NO_KEYED="1"), capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
