@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the ResNet-110 (configs[1]) side measurement")
+    ap.add_argument("--no-r50", action="store_true",
+                    help="N > 1: skip the ResNet-50 exchange (the other model of configs[4])")
     ap.add_argument("--mode", choices=["auto", "codec", "exchange"], default="auto",
                     help="auto: codec step at N=1, parameter-server exchange step at N>1")
     ap.add_argument("--model", default="bert-large", help="tensor list of the exchange workload")
@@ -1026,6 +1028,20 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             c4.append({"s": s4, "ms_per_step": ms4, "value": world * 4.0 * n4 / (ms4 / 1e3) / 1e9, "unit": "GB/s",
                        "status": st4, "allreduce_fp32_ms_per_step": ar4_ms,
                        "speedup_vs_allreduce": ar4_ms / ms4})
+    r50 = None
+    if not args.no_r50 and args.model != "resnet50":
+        # configs[4]'s other model: ResNet-50's gradient set (161 tensors, ~25.6 M values per rank)
+        rr = measure_exchange(T, dev, world, rank, "resnet50", args.xs, args.steps, args.warmup, dist,
+                              p2p=args.xchg == "p2p", exact=args.xchg == "nccl-exact", e2e_steps=0)
+        t = torch.tensor([rr["ms"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms50 = float(t.item())
+        ar50, _ = measure_allreduce(dev, world, rank, "resnet50", args.steps, args.warmup, dist)
+        r50 = {"workload": f"configs[4]: ResNet-50 gradient exchange (push + pull at s={args.xs}, "
+                           f"{rr['N']:,} values per rank, {rr['contexts']} contexts), same transport",
+               "ms_per_step": ms50, "value": world * 4.0 * rr["N"] / (ms50 / 1e3) / 1e9, "unit": "GB/s",
+               "status": rr["status"], "allreduce_fp32_ms_per_step": ar50, "speedup_vs_allreduce": ar50 / ms50,
+               "kernels_rank0": rr["kernels"]}
     if rank == 0:
         pct_nvlink = r["wire"] / 2 / (ms / 1e3) / 1e9 / NVLINK_GBS   # per direction
         line = {
@@ -1060,6 +1076,7 @@ def run_exchange_main(args, T, dev, world, rank, dist):
             "kernels_rank0": r["kernels"],
             "gpu_launches": r["launches"],
             "exchange_status": r["status"],
+            "resnet50": r50,
             "c4_resnet110": ({"workload": "configs[3]: ResNet-110 gradient set (110 tensors, 1,719,856 values per "
                                           "rank) PS push + pull, peer-memory transport, one CUDA graph per step, "
                                           "max over ranks; working set L2-resident",
