@@ -299,264 +299,6 @@ tlc_quant_qe_kernel(const SegTable T, const unsigned int *maxkey, float s, int u
     }
 }
 
-// ============================================================== K12
-// K1 and K2 fused for tables of several tensors (the exchange's push and pull tables, BERT-
-// large's 150 tensors): one persistent launch takes work items in order from a counter; the
-// host list (k12_plan_build) interleaves the max tiles (K1) and the quantize tiles (K2) of
-// consecutive windows of tensors of <= ~32 MB of t + err: K1(w0) K1(w1) K2(w0) K1(w2) K2(w1)
-// ...  A window's K2 tiles then re-read t and err while they are still in the 126 MB L2
-// (K1 of the next window is the only traffic in between), so HBM sees 12n + P/5 per
-// compress instead of K1's 8n plus K2's 12n + P/5.  A quantize item waits (one thread,
-// acquire load) until every max item of its tensor has folded its key; max items never
-// wait, and every item waits only on items dispensed before it, so the smallest unfinished
-// item can always run: no deadlock.  Same tiles, keys and arithmetic as K1 + K2: the same
-// bits.
-constexpr int kK12Threads = 256;
-static_assert(kK12Threads == kK2Threads, "the quantize items run K2's tile code");
-
-// L2 policy of the max items' loads: 0 normal (default), 1 evict_last through a cache-policy
-// operand (A/B, TLC_K12_HINT=1)
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-template <int HINT>
-__device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol) {
-    float4 v;
-    if (HINT >= 1)
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-}
-template <int HINT>
-__device__ __forceinline__ float ld_keep(const float *p, uint64_t pol) {
-    float v;
-    if (HINT >= 1)
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-
-// max key of the elements of K2 tile [j0, j0 + t2) (all five partitions).  The tile's part of
-// partition i is the run [i P + j0, i P + jend) of the flat arrays: aligned float4 groups
-// covering it (elements outside the run masked out: the key is a max, so any cover works),
-// all five runs' loads in flight together.
-template <int HINT>
-__device__ __forceinline__ unsigned int absmax_tile(const Seg &S, uint64_t j0, uint64_t t2) {
-    const uint64_t P = S.P, n = S.n;
-    const uint64_t jend = tmin<uint64_t>(P, j0 + t2);
-    unsigned int m = 0;
-    const uint64_t pol = HINT >= 1 ? policy_evict_last() : 0;
-    if (S.flags & kSegVec1) {
-        const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
-        const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
-        uint64_t lo[5], hi[5], g0[5];
-        uint32_t ng = 0;
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            lo[i] = tmin<uint64_t>(n, (uint64_t)i * P + j0);
-            hi[i] = tmin<uint64_t>(n, (uint64_t)i * P + jend);
-            g0[i] = lo[i] / 4;
-            ng = max(ng, (uint32_t)(hi[i] / 4 > g0[i] ? hi[i] / 4 - g0[i] : 0));
-        }
-        // whole float4 inside [4 g0, hi) (the head's extra elements masked), then the tail
-        // elements past the last whole float4 (< 4 per partition) one by one
-        if (threadIdx.x < 20) {
-            const int i = threadIdx.x >> 2;
-            const uint64_t l = i == 0 ? lo[0] : i == 1 ? lo[1] : i == 2 ? lo[2] : i == 3 ? lo[3] : lo[4];
-            const uint64_t h = i == 0 ? hi[0] : i == 1 ? hi[1] : i == 2 ? hi[2] : i == 3 ? hi[3] : hi[4];
-            const uint64_t e = h / 4 * 4 + (threadIdx.x & 3);
-            if (e >= l && e < h) m = max(m, absmax_key(ld_keep<HINT>(S.t + e, pol), ld_keep<HINT>(S.err + e, pol)));
-        }
-        for (uint32_t k = threadIdx.x; k < ng; k += kK12Threads) {
-            float4 tv[5], ev[5];
-#pragma unroll
-            for (int i = 0; i < 5; i++) {
-                const uint64_t g = g0[i] + k;
-                const bool ok = g < hi[i] / 4;
-                tv[i] = ok ? ld_keep4<HINT>(t4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
-                ev[i] = ok ? ld_keep4<HINT>(e4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int i = 0; i < 5; i++) {
-                const uint64_t e = 4 * (g0[i] + k);
-                const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
-                const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    if (e + c >= lo[i] && e + c < hi[i]) m = max(m, absmax_key(tt[c], ee[c]));
-            }
-        }
-        return m;
-    }
-    for (uint64_t j = j0 + threadIdx.x; j < jend; j += kK12Threads) {
-        float tv[5], ev[5];
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint64_t e = (uint64_t)i * P + j;
-            tv[i] = e < n ? ld_keep<HINT>(S.t + e, pol) : 0.0f;
-            ev[i] = e < n ? ld_keep<HINT>(S.err + e, pol) : 0.0f;
-        }
-#pragma unroll
-        for (int i = 0; i < 5; i++) m = max(m, absmax_key(tv[i], ev[i]));   // pads: key 0
-    }
-    return m;
-}
-
-// K2 on a complete tile of a tensor whose partitions are not 16-byte aligned to each other
-// (P % 4 != 0; t and err 16-byte aligned): a warp takes 31 groups of four positions at a time;
-// for each partition its lanes load the 32 aligned float4 of t and err covering the 124
-// elements (shift sh = (i P + j0) mod 4), stage them in the warp's shared memory, read their
-// four elements back at the shift, and return the residuals through the stage: whole float4
-// stores, scalar ones for the two partial float4 at the ends (their other elements belong to
-// neighbouring groups).  Every element of the tile's supersets exists (the caller checks).
-constexpr int kUGroups = 31;
-template <class QT, int LP>
-__device__ __forceinline__ void quant_qe_tile_unaligned(const Seg &S, uint8_t *bytes, uint64_t j0, uint64_t jend,
-                                                        float *wbuf, const QT &Q, uint64_t pol) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t P = S.P;
-    const uint32_t ngr = (uint32_t)((jend - j0) / 4);      // groups of the tile (complete)
-    const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
-    const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
-    float4 *o4 = reinterpret_cast<float4 *>(S.err);
-    float *wt = wbuf, *we = wbuf + 128;                      // this warp's stage: 128 floats of t, of err
-    for (uint32_t c0 = warp * kUGroups; c0 < ngr; c0 += (kK12Threads / 32) * kUGroups) {
-        const uint32_t g = c0 + lane;                         // this lane's group (lane 31: none)
-        const bool mine = lane < kUGroups && g < ngr;
-        float4 tv[5], ev[5];
-        uint64_t A[5];
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            A[i] = ((uint64_t)i * P + j0 + 4ull * c0) / 4;   // first aligned float4 of the window
-            tv[i] = ldq4<LP>(t4 + A[i] + lane, pol);
-            ev[i] = ldq4<LP>(e4 + A[i] + lane, pol);
-        }
-        uint32_t by[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < 5; i++) {
-            const uint32_t sh = (uint32_t)(((uint64_t)i * P + j0) & 3);
-            reinterpret_cast<float4 *>(wt)[lane] = tv[i];
-            reinterpret_cast<float4 *>(we)[lane] = ev[i];
-            __syncwarp();
-            float r[4];
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const float u = __fadd_rn(we[sh + 4 * lane + c], wt[sh + 4 * lane + c]);   // step (1)
-                const int q = Q.q(u);                        // Eq. 2
-                r[c] = Q.residual(u, q);                     // steps (a),(b)
-                by[c] = by[c] * 3u + (uint32_t)(q + 1);      // steps 1, 6
-            }
-            __syncwarp();
-            if (mine)
-#pragma unroll
-                for (int c = 0; c < 4; c++) we[sh + 4 * lane + c] = r[c];
-            __syncwarp();
-            // lane l writes float4 l of the window: whole for 1 <= l <= 30 (inside the 31 groups
-            // when they are all there), element-wise at the ends and past the tile's last group
-            const uint32_t e_lo = sh, e_hi = sh + 4 * (ngr - c0 < (uint32_t)kUGroups ? ngr - c0 : (uint32_t)kUGroups);
-            const float4 w = reinterpret_cast<const float4 *>(we)[lane];
-            if (4 * lane >= e_lo && 4 * lane + 4 <= e_hi) {
-                __stcs(o4 + A[i] + lane, w);
-            } else {
-                float *eo = S.err + 4 * (A[i] + lane);
-                const float ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    if (4 * lane + c >= e_lo && 4 * lane + c < e_hi) __stcs(eo + c, ww[c]);
-            }
-            __syncwarp();
-        }
-        if (mine) reinterpret_cast<uint32_t *>(bytes + j0)[g] = by[0] | (by[1] << 8) | (by[2] << 16) | (by[3] << 24);
-    }
-}
-
-template <int HINT>
-__global__ void __launch_bounds__(kK12Threads, 2)
-tlc_absmax_quant_kernel(const SegTable T, unsigned int *__restrict__ maxkey, unsigned int *__restrict__ done,
-                        Ctrl *ctrl, float s, int use_zre, uint8_t *__restrict__ scratch) {
-    __shared__ uint64_t s_first[kSegCache];
-    __shared__ unsigned int s_red[kK12Threads / 32];
-    __shared__ uint32_t s_it[2];
-    __shared__ unsigned int s_key;
-    __shared__ __align__(16) float s_stage[(kK12Threads / 32) * 256];   // per-warp realignment stages
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_it[0] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);
-    seg_index_load<2>(T, s_first);                          // (ends with a block barrier)
-    for (int b = 0;; b ^= 1) {
-        const uint32_t it = s_it[b];
-        if (it >= T.k12_n) break;
-        if (threadIdx.x == 0) s_it[b ^ 1] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);   // the next, early
-        const uint32_t item = T.k12[it];
-        const uint64_t tile = item >> 1;
-        const int si = find_seg_c<2>(T, tile, s_first);
-        const Seg S = get_seg(T, si);
-        const uint64_t lt = tile - S.k2;
-        if ((item & 1u) == 0) {
-            // ---- K1 on this tile: max of bits(u) & 0x7fffffff, folded into the tensor's key
-            unsigned int m = absmax_tile<HINT>(S, lt * T.sz.t2, T.sz.t2);
-            m = __reduce_max_sync(0xffffffffu, m);
-            if (lane == 0) s_red[warp] = m;
-            __syncthreads();
-            if (warp == 0) {
-                m = __reduce_max_sync(0xffffffffu, lane < kK12Threads / 32 ? s_red[lane] : 0u);
-                if (lane == 0) {
-                    atomicMax(maxkey + si, m);
-                    __threadfence();                        // the key before the count (release)
-                    atomicAdd(done + si, 1u);
-                }
-            }
-        } else {
-            // ---- K2 on this tile once every max tile of the tensor is in
-            if (threadIdx.x == 0) {
-                const unsigned int need = (unsigned int)((S.P + T.sz.t2 - 1) / T.sz.t2);
-                while (ld_acquire_u32(done + si) < need) __nanosleep(64);
-                s_key = ld_relaxed_u32(maxkey + si);
-            }
-            __syncthreads();
-            float M;
-            const unsigned int status = scale_from_key(s_key, s, M);   // Eq. 1, R6
-            if (lt == 0 && threadIdx.x == 0) {
-                tlc_header *h = S.hdr;
-                h->M = M;
-                h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
-                h->n = S.n;
-                h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;   // ZRE: set by K3
-                h->status = status;
-                h->reserved = 0;
-            }
-            if (status == TLC_OK) {                          // else err untouched (R6)
-                uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
-                const Quant Q(M);
-                constexpr int LP = HINT == 2 ? 1 : 0;
-                const uint64_t pol = LP ? policy_evict_first() : 0;
-                const uint64_t j0 = lt * T.sz.t2, jend = tmin<uint64_t>(S.P, j0 + T.sz.t2);
-                // complete tile: whole groups, and partition 4's 128-float windows inside the tensor
-                const bool whole = (jend - j0) % 4 == 0 &&
-                                   ((4 * S.P + jend) & ~uint64_t(3)) + 4 * kUGroups + 4 <= S.n;
-                if (!(S.flags & kSegVec2) && (S.flags & kSegVec1) && whole && (use_zre || aligned4(S.payload))) {
-                    float *wbuf = s_stage + (threadIdx.x >> 5) * 256;
-                    if (Q.mode == 1) quant_qe_tile_unaligned<QuantCmp, LP>(S, bytes, j0, jend, wbuf, QuantCmp(Q), pol);
-                    else quant_qe_tile_unaligned<Quant, LP>(S, bytes, j0, jend, wbuf, Q, pol);
-                } else {
-                    if (Q.mode == 1) quant_qe_tile<QuantCmp, LP>(S, bytes, j0, T.sz.t2, QuantCmp(Q), pol);
-                    else quant_qe_tile<Quant, LP>(S, bytes, j0, T.sz.t2, Q, pol);
-                }
-            }
-        }
-        __syncthreads();                                     // s_it[b ^ 1], s_red, s_key
-    }
-}
-
 // ---- K2 bulk path: the same computation on tiles staged in shared memory by the
 // Blackwell bulk-copy (TMA) engine.  One CTA per SM keeps kBulkStages tiles of
 // t and err (10 contiguous 4 KiB partition segments each) in flight behind
@@ -829,6 +571,239 @@ tlc_quant_qe_bulk_table_kernel(const SegTable T, const unsigned int *maxkey, flo
         __syncthreads();                                 // every thread is done with this stage
         if (threadIdx.x == 0 && k + kBulkStages < mine) issue(k + kBulkStages);
 #endif
+    }
+}
+
+// ============================================================== K12
+// K1 and K2 fused for tables of several tensors (the exchange's push and pull tables, BERT-
+// large's 150 tensors): one persistent launch takes work items in order from a counter; the
+// host list (k12_plan_build) interleaves the max tiles (K1) and the quantize tiles (K2) of
+// consecutive windows of tensors of <= ~32 MB of t + err: K1(w0) K1(w1) K2(w0) K1(w2) K2(w1)
+// ...  A window's K2 tiles then re-read t and err while they are still in the 126 MB L2
+// (K1 of the next window is the only traffic in between), so HBM sees 12n + P/5 per
+// compress instead of K1's 8n plus K2's 12n + P/5.  A quantize item waits (one thread,
+// acquire load) until every max item of its tensor has folded its key; max items never
+// wait, and every item waits only on items dispensed before it, so the smallest unfinished
+// item can always run: no deadlock.  Same tiles, keys and arithmetic as K1 + K2: the same
+// bits.
+constexpr int kK12Threads = 256;
+static_assert(kK12Threads == kK2Threads, "the quantize items run K2's tile code");
+
+// L2 policy of the max items' loads: 0 normal (default), 1 evict_last through a cache-policy
+// operand (A/B, TLC_K12_HINT=1)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <int HINT>
+__device__ __forceinline__ float4 ld_keep4(const float4 *p, uint64_t pol) {
+    float4 v;
+    if (HINT >= 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+template <int HINT>
+__device__ __forceinline__ float ld_keep(const float *p, uint64_t pol) {
+    float v;
+    if (HINT >= 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
+// max key of the elements of K2 tile [j0, j0 + t2) (all five partitions).  The tile's part of
+// partition i is the run [i P + j0, i P + jend) of the flat arrays: aligned float4 groups
+// covering it (elements outside the run masked out: the key is a max, so any cover works),
+// all five runs' loads in flight together.
+template <int HINT>
+__device__ __forceinline__ unsigned int absmax_tile(const Seg &S, uint64_t j0, uint64_t t2) {
+    const uint64_t P = S.P, n = S.n;
+    const uint64_t jend = tmin<uint64_t>(P, j0 + t2);
+    unsigned int m = 0;
+    const uint64_t pol = HINT >= 1 ? policy_evict_last() : 0;
+    if (S.flags & kSegVec1) {
+        const float4 *t4 = reinterpret_cast<const float4 *>(S.t);
+        const float4 *e4 = reinterpret_cast<const float4 *>(S.err);
+        uint64_t lo[5], hi[5], g0[5];
+        uint32_t ng = 0;
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            lo[i] = tmin<uint64_t>(n, (uint64_t)i * P + j0);
+            hi[i] = tmin<uint64_t>(n, (uint64_t)i * P + jend);
+            g0[i] = lo[i] / 4;
+            ng = max(ng, (uint32_t)(hi[i] / 4 > g0[i] ? hi[i] / 4 - g0[i] : 0));
+        }
+        // whole float4 inside [4 g0, hi) (the head's extra elements masked), then the tail
+        // elements past the last whole float4 (< 4 per partition) one by one
+        if (threadIdx.x < 20) {
+            const int i = threadIdx.x >> 2;
+            const uint64_t l = i == 0 ? lo[0] : i == 1 ? lo[1] : i == 2 ? lo[2] : i == 3 ? lo[3] : lo[4];
+            const uint64_t h = i == 0 ? hi[0] : i == 1 ? hi[1] : i == 2 ? hi[2] : i == 3 ? hi[3] : hi[4];
+            const uint64_t e = h / 4 * 4 + (threadIdx.x & 3);
+            if (e >= l && e < h) m = max(m, absmax_key(ld_keep<HINT>(S.t + e, pol), ld_keep<HINT>(S.err + e, pol)));
+        }
+        for (uint32_t k = threadIdx.x; k < ng; k += kK12Threads) {
+            float4 tv[5], ev[5];
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const uint64_t g = g0[i] + k;
+                const bool ok = g < hi[i] / 4;
+                tv[i] = ok ? ld_keep4<HINT>(t4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ev[i] = ok ? ld_keep4<HINT>(e4 + g, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 5; i++) {
+                const uint64_t e = 4 * (g0[i] + k);
+                const float tt[4] = {tv[i].x, tv[i].y, tv[i].z, tv[i].w};
+                const float ee[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (e + c >= lo[i] && e + c < hi[i]) m = max(m, absmax_key(tt[c], ee[c]));
+            }
+        }
+        return m;
+    }
+    for (uint64_t j = j0 + threadIdx.x; j < jend; j += kK12Threads) {
+        float tv[5], ev[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            const uint64_t e = (uint64_t)i * P + j;
+            tv[i] = e < n ? ld_keep<HINT>(S.t + e, pol) : 0.0f;
+            ev[i] = e < n ? ld_keep<HINT>(S.err + e, pol) : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; i++) m = max(m, absmax_key(tv[i], ev[i]));   // pads: key 0
+    }
+    return m;
+}
+
+template <int HINT>
+__global__ void __launch_bounds__(kK12Threads, 2)
+tlc_absmax_quant_kernel(const SegTable T, unsigned int *__restrict__ maxkey, unsigned int *__restrict__ done,
+                        Ctrl *ctrl, float s, int use_zre, uint8_t *__restrict__ scratch) {
+    __shared__ uint64_t s_first[kSegCache];
+    __shared__ unsigned int s_red[kK12Threads / 32];
+    __shared__ uint32_t s_it[2];
+    __shared__ unsigned int s_key;
+    extern __shared__ __align__(128) float s_buf[];             // 2 stages of 10 superset rows (bulk copies)
+    __shared__ __align__(8) unsigned long long s_bar[2];
+    uint32_t bphase = 0;                                          // the stages' mbarrier phases (CTA-uniform)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        s_it[0] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    seg_index_load<2>(T, s_first);                          // (ends with a block barrier)
+    for (int b = 0;; b ^= 1) {
+        const uint32_t it = s_it[b];
+        if (it >= T.k12_n) break;
+        if (threadIdx.x == 0) s_it[b ^ 1] = (uint32_t)atomicAdd(&ctrl->k12_counter, 1ull);   // the next, early
+        const uint32_t item = T.k12[it];
+        const uint64_t tile = item >> 1;
+        const int si = find_seg_c<2>(T, tile, s_first);
+        const Seg S = get_seg(T, si);
+        const uint64_t lt = tile - S.k2;
+        if ((item & 1u) == 0) {
+            // ---- K1 on this tile: max of bits(u) & 0x7fffffff, folded into the tensor's key
+            unsigned int m = absmax_tile<HINT>(S, lt * T.sz.t2, T.sz.t2);
+            m = __reduce_max_sync(0xffffffffu, m);
+            if (lane == 0) s_red[warp] = m;
+            __syncthreads();
+            if (warp == 0) {
+                m = __reduce_max_sync(0xffffffffu, lane < kK12Threads / 32 ? s_red[lane] : 0u);
+                if (lane == 0) {
+                    atomicMax(maxkey + si, m);
+                    __threadfence();                        // the key before the count (release)
+                    atomicAdd(done + si, 1u);
+                }
+            }
+        } else {
+            // ---- K2 on this tile once every max tile of the tensor is in
+            if (threadIdx.x == 0) {
+                const unsigned int need = (unsigned int)((S.P + T.sz.t2 - 1) / T.sz.t2);
+                while (ld_acquire_u32(done + si) < need) __nanosleep(64);
+                s_key = ld_relaxed_u32(maxkey + si);
+            }
+            __syncthreads();
+            float M;
+            const unsigned int status = scale_from_key(s_key, s, M);   // Eq. 1, R6
+            if (lt == 0 && threadIdx.x == 0) {
+                tlc_header *h = S.hdr;
+                h->M = M;
+                h->flags = use_zre ? TLC_FLAG_ZRE : 0u;
+                h->n = S.n;
+                h->payload_len = (status == TLC_OK && !use_zre) ? S.P : 0;   // ZRE: set by K3
+                h->status = status;
+                h->reserved = 0;
+            }
+            if (status == TLC_OK) {                          // else err untouched (R6)
+                uint8_t *bytes = use_zre ? scratch + S.bytes_off : S.payload;
+                const Quant Q(M);
+                constexpr int LP = HINT == 2 ? 1 : 0;
+                const uint64_t pol = LP ? policy_evict_first() : 0;
+                const uint64_t j0 = lt * T.sz.t2, jend = tmin<uint64_t>(S.P, j0 + T.sz.t2);
+                if (!(S.flags & kSegVec2) && (S.flags & kSegVec1) && (use_zre || aligned4(S.payload))) {
+                    // partitions not aligned to each other: the bulk-copy engine stages each
+                    // 1024-position sub-tile's ten rows as 16-byte aligned supersets (two stages,
+                    // the next sub-tile in flight while this one is quantized), then K2's bulk
+                    // compute; a sub-tile whose superset would cross the tensor's end goes
+                    // through the register path
+                    const uint64_t P = S.P, n = S.n;
+                    const int nsub = (int)((jend - j0 + kBulkPos - 1) / kBulkPos);
+                    auto whole = [&](int k) {
+                        const uint64_t js = j0 + (uint64_t)k * kBulkPos;
+                        return js + kBulkPos <= P && ((4 * P + js) & ~uint64_t(3)) + kBulkRow <= n;
+                    };
+                    auto issue = [&](int k) {                    // thread 0
+                        const int st = k & 1;
+                        const uint64_t js = j0 + (uint64_t)k * kBulkPos;
+                        mbar_expect_tx(&s_bar[st], 10 * kBulkPartU);
+#pragma unroll
+                        for (int i = 0; i < 5; i++) {
+                            const uint64_t a = ((uint64_t)i * P + js) & ~uint64_t(3);
+                            bulk_load(s_buf + (size_t)st * 10 * kBulkRow + i * kBulkRow, S.t + a, kBulkPartU, &s_bar[st]);
+                            bulk_load(s_buf + (size_t)st * 10 * kBulkRow + (5 + i) * kBulkRow, S.err + a, kBulkPartU,
+                                      &s_bar[st]);
+                        }
+                    };
+                    if (threadIdx.x == 0)
+                        for (int k = 0; k < 2 && k < nsub; k++)
+                            if (whole(k)) issue(k);
+                    for (int k = 0; k < nsub; k++) {
+                        const int st = k & 1;
+                        const uint64_t js = j0 + (uint64_t)k * kBulkPos;
+                        if (whole(k)) {
+                            mbar_wait(&s_bar[st], (bphase >> st) & 1u);
+                            bphase ^= 1u << st;
+                            const float *buf = s_buf + (size_t)st * 10 * kBulkRow;
+                            if (Q.mode == 1) bulk_compute<false>(buf, S.err, P, js, bytes, QuantCmp(Q));
+                            else bulk_compute<false>(buf, S.err, P, js, bytes, Q);
+                        } else {
+                            if (Q.mode == 1) quant_qe_tile<QuantCmp, LP>(S, bytes, js, kBulkPos, QuantCmp(Q), pol);
+                            else quant_qe_tile<Quant, LP>(S, bytes, js, kBulkPos, Q, pol);
+                        }
+                        __syncthreads();                         // the stage is free again
+                        if (threadIdx.x == 0 && k + 2 < nsub && whole(k + 2)) issue(k + 2);
+                    }
+                } else {
+                    if (Q.mode == 1) quant_qe_tile<QuantCmp, LP>(S, bytes, j0, T.sz.t2, QuantCmp(Q), pol);
+                    else quant_qe_tile<Quant, LP>(S, bytes, j0, T.sz.t2, Q, pol);
+                }
+            }
+        }
+        __syncthreads();                                     // s_it[b ^ 1], s_red, s_key
     }
 }
 
@@ -1435,15 +1410,22 @@ static int launch_compress_table_impl(const SegTable &T, float s, int use_zre, v
         Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
         return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
             KernelScope ks(kK12, st);
+            constexpr size_t smem = 2 * 10 * kBulkRow * sizeof(float);   // two bulk stages
+            static PerDevice k12attr;
+            if (k12attr.first()) {
+                cudaFuncSetAttribute(tlc_absmax_quant_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(tlc_absmax_quant_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(tlc_absmax_quant_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            }
             if (!g_k12_blocks)
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k12_blocks, tlc_absmax_quant_kernel<0>, kK12Threads, 0);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k12_blocks, tlc_absmax_quant_kernel<0>, kK12Threads, smem);
             const int grid = (int)tmin<uint64_t>(T.k12_n, (uint64_t)sms * tmax(1, g_k12_blocks));
             if (hint == 2)
-                tlc_absmax_quant_kernel<2><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+                tlc_absmax_quant_kernel<2><<<grid, kK12Threads, smem, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
             else if (hint == 1)
-                tlc_absmax_quant_kernel<1><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+                tlc_absmax_quant_kernel<1><<<grid, kK12Threads, smem, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
             else
-                tlc_absmax_quant_kernel<0><<<grid, kK12Threads, 0, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
+                tlc_absmax_quant_kernel<0><<<grid, kK12Threads, smem, st>>>(T, maxkey, done, ctrl, s, use_zre, scratch);
         }, true);
     }
     return compress_pipeline(T, s, use_zre, true, ws, st, [&](unsigned int *maxkey, uint8_t *scratch) {
