@@ -1385,7 +1385,8 @@ int launch_compress_table(const SegTable &T, float s, int use_zre, void *ws, cud
     return launch_compress_table_impl(T, s, use_zre, ws, st, false);
 }
 
-bool compress_runs_k1(const SegTable &T) { return !small_table(T) && !(T.k12 && k12_enabled()); }
+// the keyed pull compress (keys folded by K5m) runs K2 after them: any table off the small path
+bool compress_runs_k1(const SegTable &T) { return !small_table(T); }
 
 int prepare_keyed_compress(const SegTable &T, void *ws, cudaStream_t st, unsigned int **keys) {
     const WsLayout L = ws_layout(T, 0);
@@ -1402,7 +1403,7 @@ int launch_compress_table_keyed(const SegTable &T, float s, int use_zre, void *w
 static int launch_compress_table_impl(const SegTable &T, float s, int use_zre, void *ws, cudaStream_t st, bool keyed) {
     if (small_table(T)) return launch_small_compress(T, s, use_zre, st);    // one launch, on chip
     const int sms = num_sms();
-    if (T.k12 && k12_enabled()) {
+    if (T.k12 && k12_enabled() && !keyed) {
         static const int hint = env_int("TLC_K12_HINT", 1);
         const WsLayout L = ws_layout(T, 0);
         char *base = reinterpret_cast<char *>(ws);
