@@ -848,6 +848,8 @@ __device__ __forceinline__ bool plain_lane(const uint32_t (&w)[8]) {
 }
 
 constexpr int kK3RowsPerWarp = (int)(kLargeItems.c3 / kScanWarps / kK3WarpRow);   // rows of a sub-range
+static_assert(kT5 % kK3WarpRow == 0 && kLargeItems.c3 % kT5 == 0 && kSmallItems.c3 % kT5 == 0,
+              "K5 tile starts are warp-row starts (K3 writes the producer seek entries there)");
 #ifndef TLC_K3_LITCAP
 #define TLC_K3_LITCAP 512
 #endif
@@ -969,7 +971,9 @@ __device__ __forceinline__ K3Chunk k3_chunk(const SegTable &T, uint64_t id, cons
     c.nch = (S.P + T.sz.c3 - 1) / T.sz.c3;
     c.lo = c.lc * T.sz.c3;
     c.hi = tmin<uint64_t>(S.P, c.lo + T.sz.c3);
-    const uint64_t sub = ((c.hi - c.lo + kK3Workers - 1) / kK3Workers + kK3Seg - 1) / kK3Seg * kK3Seg;
+    // whole 1 KiB rows per warp: every quartic position that is a multiple of kT5 (a K5 tile
+    // start) is then the start of some warp's row, where phase 3 knows (offset, carry)
+    const uint64_t sub = ((c.hi - c.lo + kK3Workers - 1) / kK3Workers + kK3WarpRow - 1) / kK3WarpRow * kK3WarpRow;
     c.wlo = warp < kK3Workers ? tmin<uint64_t>(c.hi, c.lo + warp * sub) : c.hi;
     c.whi = tmin<uint64_t>(c.hi, c.wlo + sub);
     return c;
@@ -1163,6 +1167,10 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 const uint4 meta = sm.rowmeta[ib][wk][r];
                 const uint32_t L = meta.x & 0xffffu;
                 uint8_t *out = S.payload + off;
+                // K5 tile start: the payload byte covering position `row` is the next one
+                // emitted (the pending run's code, 255 or the literal), `carry` positions into
+                // its expansion -- the entry K4 would derive from the payload
+                if (S.seek && lane == 0 && row % kT5 == 0) S.seek[row / kT5] = (off << 4) | carry;
                 if (L == 0) {                             // no literal: the run grows by row_len
                     const uint32_t x = carry + row_len;
                     off += x / kMaxRun;

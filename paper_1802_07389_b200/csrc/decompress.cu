@@ -399,12 +399,12 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
             // skip-zero (R16): a tile whose payload window holds no literal but 121 leaves
             // out untouched -- the expansion and the decode are skipped
             ExpandWin X;
-            expand_load(X, payload, Z, seek + S.k5, lt, ntiles);
+            expand_load(X, payload, Z, S.seek ? S.seek : seek + S.k5, lt, ntiles);
             if (!__syncthreads_or(window_nonzero(X))) continue;
             expand_scan<true>(sm.E, sm.warp_sum, X, tl);
         }
         const bool bad = (kMode != TLC_MODE_OVERWRITE && zre)
-                             ? false : expand_tile(sm.E, sm.warp_sum, payload, zre, Z, seek + S.k5, lt, ntiles, J0, tl);
+                             ? false : expand_tile(sm.E, sm.warp_sum, payload, zre, Z, S.seek ? S.seek : seek + S.k5, lt, ntiles, J0, tl);
         if (bad) {                                         // literal > 242 without ZRE
             if (threadIdx.x == 0) raise_format(S.hdr);
             continue;
@@ -581,7 +581,7 @@ tlc_aggregate_kernel(const SegTable A, const SegTable X, int W, const unsigned l
                 pw[g] = R.payload;
                 okw[g] = true;                              // every source OK (not poisoned)
                 zw[g] = (R.hdr->flags & TLC_FLAG_ZRE) != 0;
-                if (okw[g] && zw[g]) expand_load(Xw[g], R.payload, R.hdr->payload_len, seek + R.k5, lt, ntiles);
+                if (okw[g] && zw[g]) expand_load(Xw[g], R.payload, R.hdr->payload_len, R.seek ? R.seek : seek + R.k5, lt, ntiles);
             }
 #pragma unroll
             for (int g = 0; g < kK5mG; g++) {
@@ -737,10 +737,11 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
         int wl = 0, sh = 0, skip = 0;
         uint64_t bi = 0;
         if (act0 && zre) {
-            const unsigned long long sk = seek[R.k5 + lt];
+            const unsigned long long *sp = R.seek ? R.seek : seek + R.k5;   // producer's or K4's
+            const unsigned long long sk = sp[lt];
             bi = sk >> 4;
             skip = (int)(sk & 15);
-            const uint64_t be = lt + 1 < ntiles ? (seek[R.k5 + lt + 1] >> 4) : Z - 1;
+            const uint64_t be = lt + 1 < ntiles ? (sp[lt + 1] >> 4) : Z - 1;
             wl = (int)(be - bi) + 1;                           // <= kT5 + 1
             sh = (int)(bi & 15);                               // passes start at the granule of bi
         }
@@ -993,7 +994,7 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
     if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
     if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
     const int sms = num_sms();
-    {
+    if (!X.all_seek) {                       // producer seek entries: no scan (payloads from K3)
         KernelScope ks(kK4, st);
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(X.n4, (uint64_t)sms * 8));
         tlc_zre_scan_kernel<<<grid, kK4Threads, 0, st>>>(X, ctrl, states, seek);
@@ -1031,7 +1032,7 @@ int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t 
     if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
     if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
     const int sms = num_sms();
-    {
+    if (!T.all_seek) {                       // producer seek entries: no scan (payloads from K3)
         KernelScope ks(kK4, st);
         if (!g_k4_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k4_blocks, tlc_zre_scan_kernel, kK4Threads, 0);

@@ -219,7 +219,32 @@ struct tlc_exchange {
     std::vector<uint64_t> h_items;
     size_t max_region = 0;
     uint64_t last_recv[2] = {0, 0};                  // bytes received in the last push / pull (exact mode)
+    // producer seek entries: behind the payload regions of push_send and pull_buf (at
+    // seek_base), tile_off[k] entries in for context k; written by the producing K3, read by
+    // the consumers' K5m / K5 over peer memory instead of running K4 (TLC_NO_PRODSEEK=1: off)
+    size_t seek_base = 0;
+    std::vector<uint64_t> tile_off;
+    bool push_seeks = false;                         // the push compress runs K3 (not K6g)
+    std::vector<char> pull_seeks;                    // per owner: its pull compress runs K3
 };
+
+static bool prodseek_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("TLC_NO_PRODSEEK");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// Seg::seek pointers of a table over contexts ks: base + tile_off[k] (base == nullptr: none)
+static std::vector<unsigned long long *> seek_ptrs(const tlc_exchange *x, const std::vector<int> &ks,
+                                                   const std::vector<uint8_t *> &bases) {
+    std::vector<unsigned long long *> v(ks.size(), nullptr);
+    for (size_t i = 0; i < ks.size(); i++)
+        if (bases[i]) v[i] = reinterpret_cast<unsigned long long *>(bases[i] + x->seek_base) + x->tile_off[ks[i]];
+    return v;
+}
 
 static int cuda_ok(cudaError_t e) { return e == cudaSuccess ? TLC_OK : TLC_ERR_CUDA; }
 static int nccl_ok(ncclResult_t r) { return r == ncclSuccess ? TLC_OK : TLC_ERR_NCCL; }
@@ -272,6 +297,15 @@ static int set_peers(tlc_exchange *x, const std::vector<std::array<void *, 5>> &
                 e.n = c.n;
             }
         }
+        // rank w's K3 wrote the seek entries of its pushes behind its send buffer
+        std::vector<int> ks((size_t)W * nown);
+        std::vector<uint8_t *> bases((size_t)W * nown, nullptr);
+        for (int w = 0; w < W; w++)
+            for (int q = 0; q < nown; q++) {
+                ks[(size_t)w * nown + q] = x->owned[me][q];
+                if (x->push_seeks) bases[(size_t)w * nown + q] = static_cast<uint8_t *>(x->peer[w][0]);
+            }
+        x->x_tab.seekp = seek_ptrs(x, ks, bases);
         rc = x->x_tab.update(xs.data());
     }
     if (rc == TLC_OK) {
@@ -412,9 +446,26 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
     alloc((void **)&x->own_pull_err, x->owned_elems * sizeof(float));
     x->push_err = x->own_push_err;
     x->pull_err = x->own_pull_err;
-    alloc((void **)&x->push_send, x->total_region);
+    x->tile_off.assign(C + 1, 0);
+    for (int k = 0; k < C; k++) x->tile_off[k + 1] = x->tile_off[k] + ((x->ctx[k].n + 4) / 5 + kT5 - 1) / kT5;
+    x->seek_base = align256(x->total_region);
+    const size_t seek_bytes = x->tile_off[C] * sizeof(unsigned long long);
+    {
+        // a table whose tensors are all small takes K6g (no K3, no seek entries)
+        auto runs_k3 = [&](const std::vector<int> &ks) {
+            uint64_t mx = 0;
+            for (int k : ks) mx = tmax<uint64_t>(mx, x->ctx[k].n);
+            return prodseek_enabled() && !ks.empty() && (mx > kSmallMaxN || !small_enabled());
+        };
+        std::vector<int> all(C);
+        for (int k = 0; k < C; k++) all[k] = k;
+        x->push_seeks = runs_k3(all);
+        x->pull_seeks.assign(x->W, 0);
+        for (int o = 0; o < x->W; o++) x->pull_seeks[o] = runs_k3(x->owned[o]) ? 1 : 0;
+    }
+    alloc((void **)&x->push_send, x->seek_base + seek_bytes);
     alloc((void **)&x->push_recv, (size_t)x->W * own_region);
-    alloc((void **)&x->pull_buf, x->total_region);
+    alloc((void **)&x->pull_buf, x->seek_base + seek_bytes);
     alloc((void **)&x->push_hdr_send, (size_t)C * sizeof(tlc_header));
     alloc((void **)&x->push_hdr_recv, (size_t)x->W * nown * sizeof(tlc_header));
     alloc((void **)&x->pull_hdr, (size_t)C * sizeof(tlc_header));
@@ -450,6 +501,7 @@ int tlc_exchange_create(tlc_exchange **out, tlc_comm *comm, int num_tensors, con
             d.hdr = x->pull_hdr + x->hdr_start[x->me] + c.slot;
             d.n = c.n;
         }
+        x->pullc_tab.seekp = seek_ptrs(x, x->owned[x->me], std::vector<uint8_t *>(nown, x->pull_buf));
         rc = x->pullc_tab.create(pullc.data(), nown, true, nullptr);
         std::vector<tlc_tensor_desc> xs((size_t)x->W * nown);
         for (int q = 0; q < nown; q++) {
@@ -664,6 +716,9 @@ static int phase_push_compress(tlc_exchange *x, const float *const *grads, float
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;   // table may be in use
         Table &tb = x->push_tab[slot];
+        std::vector<int> ks(C);
+        for (int k = 0; k < C; k++) ks[k] = k;
+        tb.seekp = seek_ptrs(x, ks, std::vector<uint8_t *>(C, x->push_seeks ? x->push_send : nullptr));
         const int rc = tb.d ? tb.update(d.data()) : tb.create(d.data(), C, true, nullptr);
         if (rc != TLC_OK) return rc;
         x->push_key[slot].assign(grads, grads + T);
@@ -729,6 +784,15 @@ static int phase_apply(tlc_exchange *x, float *const *outs, cudaStream_t st) {
         }
         if (cudaStreamSynchronize(st) != cudaSuccess) return TLC_ERR_CUDA;
         Table &tb = x->apply_tab[slot];
+        // peer memory: every owner's K3 wrote its pulls' seek entries behind its pull buffer
+        std::vector<int> ks(C);
+        std::vector<uint8_t *> bases(C, nullptr);
+        for (int k = 0; k < C; k++) {
+            ks[k] = k;
+            const int o = x->ctx[k].owner;
+            if (x->p2p && x->pull_seeks[o]) bases[k] = static_cast<uint8_t *>(x->peer[o][2]);
+        }
+        tb.seekp = seek_ptrs(x, ks, bases);
         const int rc = tb.d ? tb.update(d.data()) : tb.create(d.data(), C, false, nullptr);
         if (rc != TLC_OK) return rc;
         x->apply_key[slot].assign(outs, outs + T);

@@ -117,6 +117,12 @@ int Table::create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void
 
 int Table::upload() {
     for (Seg &s : host) s.flags = seg_flags(s);
+    bool all = !host.empty();
+    for (size_t i = 0; i < host.size(); i++) {
+        host[i].seek = i < seekp.size() ? seekp[i] : nullptr;
+        all = all && host[i].seek;
+    }
+    T.all_seek = all ? 1 : 0;
     T.d = d;
     if (count == 1) T.one = host[0];
     // the K2 tiles the bulk-copy kernel takes (count > 1; one tensor uses a tile range)

@@ -126,6 +126,11 @@ struct Seg {
     uint64_t k1, k2, k3, k4, k5;    // first global item of each kernel
     uint64_t bytes_off;             // quartic scratch offset (compress with ZRE)
     uint32_t flags, pad;
+    // seek entries of the segment's K5 tiles written by the producer (nullptr: none).  A
+    // compress table's K3 writes them as it emits the payload; a decompress table whose
+    // segments all carry them (payloads produced by this library's K3 in the same exchange,
+    // read over peer memory) skips K4 and K5 reads them instead of the workspace's.
+    unsigned long long *seek;
 };
 
 // A slice of a small tensor (K6c): quartic positions [j0, j0+len) of segment `seg` with
@@ -199,6 +204,7 @@ struct SegTable {
     int grp_grid;                   // CTAs (a multiple of grp_cl)
     int grp_cl;                     // cluster size
     uint32_t grp_maxlen;            // longest slice (quartic positions)
+    int all_seek;                   // every segment carries producer seek entries (Seg::seek)
 };
 
 // Workspace layout of one table: control block, per-segment max keys, K3 / K4
@@ -250,6 +256,7 @@ struct Table {
     DecRec *d_dec = nullptr;        // the K7 records (small tables only)
     std::vector<uint4> dec_layout;  // K7 CTAs on the host: (seg, jr0, pl, first)
     std::vector<uint4> sl_layout;   // K6c slices on the host: (seg, j0, len, k | last << 16)
+    std::vector<unsigned long long *> seekp;   // per segment Seg::seek (empty: none), kept across update()
     int create(const tlc_tensor_desc *descs, int cnt, bool with_scratch, void *shared_ws);
     int update(const tlc_tensor_desc *descs);
     int upload();

@@ -128,6 +128,35 @@ def test_loopback_large_contexts(W):
     _check(W, _run_group(W, SIZES_LARGE, 1.75, "gauss"), SIZES_LARGE, 1.75, "gauss")
 
 
+@pytest.mark.parametrize("W", [2, 3])
+def test_loopback_producer_seeks_skip_k4(W):
+    """Peer-memory consumers read the seek entries the producing K3 wrote (its phase 3 knows
+    the payload offset and run carry at every K5 tile start) and launch no K4: the owners'
+    K5m and every rank's apply still match the oracle bit for bit.  The contexts' last K3
+    chunks are partial with K5 tile starts inside them (K3 gives every warp whole rows)."""
+    import os
+
+    import paper_1802_07389_b200 as T
+
+    # W = 2: P = 28709 (its last 8 KiB chunk holds 4133 bytes, the tile start 28672 inside);
+    # W = 3: two shards of P = 14355 (tile start 12288 inside a 6163-byte last chunk)
+    sizes = [5 * (3 * 8192 + 4096 + 37), 5 * (4096 + 1) + 3, 40_961 * 3, 2304]
+    T.tlc_prof_collect()
+    T.tlc_prof_enable(True)
+    try:
+        res = _run_group(W, sizes, 1.5, "gauss", steps=2)
+    finally:
+        T.tlc_prof_enable(False)
+    prof = T.tlc_prof_collect()
+    _check(W, res, sizes, 1.5, "gauss", steps=2)
+    k4 = prof.get("k4_zre_scan", (0, 0.0))[0]
+    if os.environ.get("TLC_NO_PRODSEEK") == "1":
+        assert k4 > 0, prof
+    else:
+        assert k4 == 0, prof
+        assert prof.get("k3_zre", (0, 0.0))[0] > 0, prof
+
+
 @pytest.mark.parametrize("W", [2, 4, 8])
 def test_loopback_resnet110_small_tables(W):
     """BASELINE configs[3] (C4): ResNet-110's 110 layers -- every context is a small tensor, so
