@@ -313,9 +313,12 @@ int tlc_exchange_status_async(tlc_exchange *x, unsigned int *dst, void *stream);
  * memory `out`), the caller all-gathers them in rank order (W x 320 bytes) and
  * every rank calls tlc_exchange_ipc_open.  From then on push/pull move no data
  * with NCCL: a flag barrier over peer memory orders the phases, and the owner's
- * scan + fused aggregation kernels (and every rank's apply kernels) read the
- * compressed payloads -- exactly their payload_len bytes -- straight from the
- * producing GPU over NVLink.  Results are identical to the NCCL mode. */
+ * fused aggregation kernels (and every rank's apply kernels) read the compressed
+ * payloads -- exactly their payload_len bytes -- straight from the producing GPU
+ * over NVLink, with the seek entries (8 bytes per 4096 quartic positions) the
+ * producer's zero-run encoder wrote behind its buffers, so no consumer rescans a
+ * payload (env TLC_NO_PRODSEEK=1: the consumers scan).  Results are identical to
+ * the NCCL mode. */
 int tlc_exchange_ipc_handles(tlc_exchange *x, void *out);
 int tlc_exchange_ipc_open(tlc_exchange *x, const void *all);
 
