@@ -222,12 +222,13 @@ struct ExpandWin {
     int skip, wl, sh;
 };
 
-__device__ __forceinline__ void expand_load(ExpandWin &X, const uint8_t *payload, uint64_t Z,
-                                            const unsigned long long *seek, uint64_t lt, uint64_t ntiles) {
-    const unsigned long long sk = seek[lt];
+// sk = the tile's seek entry, sk1 = the next tile's (ignored for the last tile, lt + 1 = ntiles)
+__device__ __forceinline__ void expand_load_at(ExpandWin &X, const uint8_t *payload, uint64_t Z,
+                                               unsigned long long sk, unsigned long long sk1, uint64_t lt,
+                                               uint64_t ntiles) {
     const uint64_t bi = sk >> 4;                          // payload byte covering J0
     X.skip = (int)(sk & 15);                              // J0 - (first position of that byte)
-    const uint64_t be = lt + 1 < ntiles ? (seek[lt + 1] >> 4) : Z - 1;   // last byte needed
+    const uint64_t be = lt + 1 < ntiles ? (sk1 >> 4) : Z - 1;   // last byte needed
     X.wl = (int)(be - bi) + 1;                            // <= kT5 + 1
     // thread owns window bytes [16*tid, 16*tid+16) relative to w0 = bi rounded down
     // to 4; the last thread also owns the next 4 bytes, so the <= kT5 bytes from bi
@@ -251,6 +252,11 @@ __device__ __forceinline__ void expand_load(ExpandWin &X, const uint8_t *payload
             X.wd[h] = x;
         }
     }
+}
+
+__device__ __forceinline__ void expand_load(ExpandWin &X, const uint8_t *payload, uint64_t Z,
+                                            const unsigned long long *seek, uint64_t lt, uint64_t ntiles) {
+    expand_load_at(X, payload, Z, seek[lt], lt + 1 < ntiles ? seek[lt + 1] : 0ull, lt, ntiles);
 }
 
 // true if this thread's window bytes hold a literal other than 121, i.e. a nonzero trit
@@ -363,11 +369,19 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
         const int si = find_seg_c<5>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         const tlc_header *hdr = S.hdr;
+        const uint64_t lt = tile - S.k5, ntiles = (S.P + kT5 - 1) / kT5;
+        // ACCUMULATE (the exchange's apply): the seek entries are loaded beside the header, not
+        // after it -- over peer memory both are the owner's (one remote round trip fewer)
+        unsigned long long sk0 = 0, sk1 = 0;
+        if (kMode != TLC_MODE_OVERWRITE) {
+            const unsigned long long *sp = S.seek ? S.seek : seek + S.k5;
+            sk0 = sp[lt];
+            if (lt + 1 < ntiles) sk1 = sp[lt + 1];
+        }
         if (hdr->status != TLC_OK) continue;             // uniform: FORMAT from K4 or a failed compress
         const float M = hdr->M;
         const bool zre = (hdr->flags & TLC_FLAG_ZRE) != 0;
         const uint64_t Z = hdr->payload_len, P = S.P, n = S.n;
-        const uint64_t lt = tile - S.k5, ntiles = (P + kT5 - 1) / kT5;
         const uint8_t *__restrict__ payload = S.payload;
         __syncthreads();   // previous tile's readers of sm.E / sm.V are done
         if (si != cur) {
@@ -399,7 +413,7 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
             // skip-zero (R16): a tile whose payload window holds no literal but 121 leaves
             // out untouched -- the expansion and the decode are skipped
             ExpandWin X;
-            expand_load(X, payload, Z, S.seek ? S.seek : seek + S.k5, lt, ntiles);
+            expand_load_at(X, payload, Z, sk0, sk1, lt, ntiles);
             if (!__syncthreads_or(window_nonzero(X))) continue;
             expand_scan<true>(sm.E, sm.warp_sum, X, tl);
         }
@@ -711,8 +725,14 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
         Seg R{};
         unsigned int st = TLC_OK, flags = 0;
         uint64_t Z = 0;
+        unsigned long long sk0 = 0, sk1 = 0;
         if (src) {
             R = get_seg(X, g * A.count + q);
+            // the seek entries are loaded beside the header, not after it (over peer memory they
+            // are the producer's: one remote round trip fewer per tile); used only with ZRE
+            const unsigned long long *sp = R.seek ? R.seek : seek + R.k5;   // producer's or K4's
+            sk0 = sp[lt];
+            if (lt + 1 < ntiles) sk1 = sp[lt + 1];
             st = R.hdr->status;
             flags = R.hdr->flags;
             Z = R.hdr->payload_len;
@@ -737,11 +757,9 @@ tlc_aggregate_par_kernel(const SegTable A, const SegTable X, int W, const unsign
         int wl = 0, sh = 0, skip = 0;
         uint64_t bi = 0;
         if (act0 && zre) {
-            const unsigned long long *sp = R.seek ? R.seek : seek + R.k5;   // producer's or K4's
-            const unsigned long long sk = sp[lt];
-            bi = sk >> 4;
-            skip = (int)(sk & 15);
-            const uint64_t be = lt + 1 < ntiles ? (sp[lt + 1] >> 4) : Z - 1;
+            bi = sk0 >> 4;
+            skip = (int)(sk0 & 15);
+            const uint64_t be = lt + 1 < ntiles ? (sk1 >> 4) : Z - 1;
             wl = (int)(be - bi) + 1;                           // <= kT5 + 1
             sh = (int)(bi & 15);                               // passes start at the granule of bi
         }
