@@ -1167,9 +1167,10 @@ tlc_zre_kernel(const SegTable T, const unsigned int *maxkey, float s,
                 const uint4 meta = sm.rowmeta[ib][wk][r];
                 const uint32_t L = meta.x & 0xffffu;
                 uint8_t *out = S.payload + off;
-                // K5 tile start: the payload byte covering position `row` is the next one
-                // emitted (the pending run's code, 255 or the literal), `carry` positions into
-                // its expansion -- the entry K4 would derive from the payload
+                // K5 tile start: the next byte emitted starts `carry` positions before `row`
+                // (the pending run's 255 or flush code, or the literal when carry = 0) -- K4's
+                // entry, except that a literal at `row` after pending zero groups is reached
+                // through their flush code, fully skipped (reading R25)
                 if (S.seek && lane == 0 && row % kT5 == 0) S.seek[row / kT5] = (off << 4) | carry;
                 if (L == 0) {                             // no literal: the run grows by row_len
                     const uint32_t x = carry + row_len;

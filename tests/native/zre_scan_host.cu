@@ -148,16 +148,17 @@ void load_row(const uint8_t *B, uint64_t row, uint64_t whi, Row &r) {
 }
 }  // namespace
 
-extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out,
-                                      int lane_mode) {
-    uint64_t chunk = (P + nchunks_req - 1) / nchunks_req;
-    chunk = (chunk + SEG - 1) / SEG * SEG;
+// sub_round: granule of a warp's sub-range (SEG, or a whole row as K3 does since it writes
+// seek entries); seek != nullptr: at every row start that is a multiple of 4096 (a K5 tile
+// start) record (payload offset << 4) | carry, as K3's phase 3 does
+static uint64_t scan_impl(const uint8_t *B, uint64_t P, int warps, uint64_t chunk, uint8_t *out, int lane_mode,
+                          uint64_t sub_round, uint64_t *seek) {
     const uint64_t nch = (P + chunk - 1) / chunk;
     std::vector<RunSum> agg(nch);
     std::vector<std::vector<RunSum>> wagg(nch, std::vector<RunSum>(warps));
     auto bounds = [&](uint64_t b, int w, uint64_t &wlo, uint64_t &whi) {
         const uint64_t lo = b * chunk, hi = std::min(P, lo + chunk);
-        const uint64_t sub = ((hi - lo + warps - 1) / warps + SEG - 1) / SEG * SEG;
+        const uint64_t sub = ((hi - lo + warps - 1) / warps + sub_round - 1) / sub_round * sub_round;
         wlo = std::min(hi, lo + w * sub);
         whi = std::min(hi, wlo + sub);
     };
@@ -201,6 +202,7 @@ extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, u
             uint64_t wlo, whi;
             bounds(b, w, wlo, whi);
             for (uint64_t row = wlo; row < whi; row += (uint64_t)LANES * SEG) {
+                if (seek && row % 4096 == 0) seek[row / 4096] = (off << 4) | carry;
                 load_row(B, row, whi, r);
                 warp_row_host(r, carry);
                 if (lane_mode) emit_row_lanes(r, row, P, carry, out, off, lane_mode);
@@ -209,6 +211,20 @@ extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, u
         }
     }
     return total;
+}
+
+extern "C" uint64_t zre_scan_sim_mode(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out,
+                                      int lane_mode) {
+    uint64_t chunk = (P + nchunks_req - 1) / nchunks_req;
+    chunk = (chunk + SEG - 1) / SEG * SEG;
+    return scan_impl(B, P, warps, chunk, out, lane_mode, SEG, nullptr);
+}
+
+// K3's decomposition as built (chunks of `chunk` bytes, a multiple of 4096; warps take whole
+// 1 KiB rows) with the producer seek entries of every K5 tile written to seek[ceil(P/4096)]
+extern "C" uint64_t zre_seek_sim(const uint8_t *B, uint64_t P, int warps, uint64_t chunk, uint8_t *out,
+                                 uint64_t *seek) {
+    return scan_impl(B, P, warps, chunk, out, 0, (uint64_t)LANES * SEG, seek);
 }
 
 extern "C" uint64_t zre_scan_sim(const uint8_t *B, uint64_t P, int warps, uint64_t nchunks_req, uint8_t *out) {

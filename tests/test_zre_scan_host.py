@@ -99,3 +99,51 @@ def test_word_len_swar_matches_bytewise(sim):
     g = np.random.default_rng(5)
     for w in g.integers(0, 2**32, 20000, dtype=np.uint64):
         assert L.tlc_word_len(int(w)) == ref(int(w))
+
+
+def test_producer_seek_entries_match_payload_scan(sim):
+    """The seek entries K3 writes for the peer-memory consumers (exchange): K3's decomposition
+    as built (chunks of 8 or 32 KiB, warps on whole 1 KiB rows), recording (payload offset << 4)
+    | run carry at every row start that is a multiple of 4096.  K5 needs a byte index i and a
+    skip with start(i) + skip = J0 and skip <= len(i), len(b) = b >= 243 ? b - 241 : 1 (inverse
+    of P:545-546), start walked here over the oracle's encoding byte by byte.  K4's entry is the
+    byte covering J0; K3's equals it except where J0 holds a literal after c > 0 pending zero
+    groups: then it names the flush code of those c groups (emitted next) with skip = c, its
+    whole expansion (DESIGN reading R25) -- checked to be exactly that case."""
+    L = sim.lib
+    L.zre_seek_sim.restype = ctypes.c_uint64
+    L.zre_seek_sim.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint64,
+                               ctypes.c_void_p, ctypes.c_void_p]
+    g = synth.rng(73)
+    cases = []
+    for p in (0.0, 0.5, 0.9, 0.99, 1.0):
+        for n in (4096, 4097, 3 * 8192 + 4096 + 37, 2 * 32768 + 5 * 4096 + 100, 5 * 32768 + 11):
+            cases.append(np.where(g.random(n) < p, 121, g.integers(0, 243, n)).astype(np.uint8))
+    runs = []                                          # runs straddling tile starts at every carry
+    for r in list(range(1, 30)) + [4095, 4096, 4097, 14 * 300 + 3]:
+        runs += [121] * r + [int(g.integers(0, 121))]
+    cases.append(np.array(runs, np.uint8))
+    alt = 0
+    for B in cases:
+        ref = O.zre_encode(B)
+        lens = np.where(ref >= 243, ref.astype(np.int64) - 241, 1)
+        start = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        assert int(lens.sum()) == B.size
+        ntiles = -(-B.size // 4096)
+        want = []
+        for k in range(ntiles):
+            i = int(np.searchsorted(start, 4096 * k, side="right")) - 1
+            want.append((i << 4) | (4096 * k - int(start[i])))
+        for chunk in (8192, 32768):
+            out = np.full(B.size + 16, 0xEE, np.uint8)
+            seek = np.full(ntiles, 0xFFFFFFFFFFFFFFFF, np.uint64)
+            z = L.zre_seek_sim(B.ctypes.data, B.size, 8, chunk, out.ctypes.data, seek.ctypes.data)
+            assert out[:z].tolist() == ref.tolist(), (B.size, chunk)
+            for k, (got, w) in enumerate(zip(seek.tolist(), want)):
+                i, skip = got >> 4, got & 15
+                assert int(start[i]) + skip == 4096 * k and skip <= int(lens[i]), (B.size, chunk, k)
+                if got != w:                       # a fully skipped flush code before J0's literal
+                    assert skip == int(lens[i]) and (w >> 4) == i + 1 and (w & 15) == 0, (B.size, chunk, k)
+                    assert B[4096 * k] != 121 and B[4096 * k - 1] == 121, (B.size, chunk, k)
+                    alt += 1
+    assert alt > 0                                  # the flush-code form was exercised
