@@ -1009,10 +1009,11 @@ int launch_aggregate(const SegTable &A, const SegTable &X, int W, void *xws, cud
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
     unsigned long long *states = reinterpret_cast<unsigned long long *>(base + L.k4st);
     unsigned long long *seek = reinterpret_cast<unsigned long long *>(base + L.seek);
-    if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
-    if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
     const int sms = num_sms();
     if (!X.all_seek) {                       // producer seek entries: no scan (payloads from K3)
+        // K4's counter and chunk states (K5 / K5m use neither: no memsets without K4)
+        if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
+        if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
         KernelScope ks(kK4, st);
         const int grid = (int)tmax<uint64_t>(1, tmin<uint64_t>(X.n4, (uint64_t)sms * 8));
         tlc_zre_scan_kernel<<<grid, kK4Threads, 0, st>>>(X, ctrl, states, seek);
@@ -1047,10 +1048,11 @@ int launch_decompress_table(const SegTable &T, int mode, void *ws, cudaStream_t 
     Ctrl *ctrl = reinterpret_cast<Ctrl *>(base + L.ctrl);
     unsigned long long *states = reinterpret_cast<unsigned long long *>(base + L.k4st);
     unsigned long long *seek = reinterpret_cast<unsigned long long *>(base + L.seek);
-    if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
-    if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
     const int sms = num_sms();
     if (!T.all_seek) {                       // producer seek entries: no scan (payloads from K3)
+        // K4's counter and chunk states (K5 / K5m use neither: no memsets without K4)
+        if (cudaMemsetAsync(base + L.ctrl, 0, sizeof(Ctrl), st) != cudaSuccess) return TLC_ERR_CUDA;
+        if (cudaMemsetAsync(states, 0, L.memset_d, st) != cudaSuccess) return TLC_ERR_CUDA;
         KernelScope ks(kK4, st);
         if (!g_k4_blocks)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_k4_blocks, tlc_zre_scan_kernel, kK4Threads, 0);
