@@ -365,7 +365,20 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     seg_index_load<5>(T, s_first);                       // (ends with __syncthreads)
     pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
-    for (uint64_t tile = blockIdx.x; tile < T.n5; tile += gridDim.x) {
+    // ACCUMULATE (the exchange's apply over a table of contexts): contiguous runs of tiles per
+    // CTA, so the value tables V are rebuilt only when the context changes (with a grid stride
+    // of ~450 tiles almost every tile of a 150-context table changed it; K5m does the same).
+    // OVERWRITE keeps the grid stride (C3: one tensor, at the store roofline).
+#ifndef TLC_K5A_STRIDE
+    constexpr bool kRuns = kMode != TLC_MODE_OVERWRITE;
+#else
+    constexpr bool kRuns = false;
+#endif
+    const uint64_t per = kRuns ? (T.n5 + gridDim.x - 1) / gridDim.x : 1;
+    const uint64_t t_begin = kRuns ? per * blockIdx.x : blockIdx.x;
+    const uint64_t t_end = kRuns ? tmin<uint64_t>(T.n5, per * (blockIdx.x + 1)) : T.n5;
+    const uint64_t t_step = kRuns ? 1 : gridDim.x;
+    for (uint64_t tile = t_begin; tile < t_end; tile += t_step) {
         const int si = find_seg_c<5>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         const tlc_header *hdr = S.hdr;
