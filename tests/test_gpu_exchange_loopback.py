@@ -1,5 +1,6 @@
 """The multi-source exchange on ONE GPU: a loopback group (tlc_loopback_*) of W virtual
-ranks runs the real push -> K4 -> K5m -> pull -> apply kernels -- every owner's fused
+ranks runs the real push -> K5m -> pull -> apply kernels (K4 only under TLC_NO_PRODSEEK=1:
+the consumers read the seek entries the producers' K3 wrote) -- every owner's fused
 aggregation reading all W ranks' payloads, every rank's apply reading all owners'
 payloads -- and is compared bit for bit with the W-virtual-rank oracle
 (oracle/exchange.py, X1-X6): every owner's mean after every step, every push and pull
