@@ -365,20 +365,23 @@ tlc_expand_dequant_kernel(const SegTable T, const unsigned long long *seek) {
     seg_index_load<5>(T, s_first);                       // (ends with __syncthreads)
     pdl_wait();                                          // K4's seek entries and header checks
     int cur = -1;
-    // ACCUMULATE (the exchange's apply over a table of contexts): contiguous runs of tiles per
-    // CTA, so the value tables V are rebuilt only when the context changes (with a grid stride
-    // of ~450 tiles almost every tile of a 150-context table changed it; K5m does the same).
-    // OVERWRITE keeps the grid stride (C3: one tensor, at the store roofline).
-#ifndef TLC_K5A_STRIDE
-    constexpr bool kRuns = kMode != TLC_MODE_OVERWRITE;
-#else
-    constexpr bool kRuns = false;
+    // ACCUMULATE (the exchange's apply over a table of contexts): runs of R consecutive tiles
+    // dealt to the CTAs cyclically, so the value tables V are rebuilt at most once per run (with
+    // a plain grid stride of ~450 tiles nearly every tile of a 150-context table rebuilt them),
+    // while dense and sparse contexts still spread over all CTAs (N = 4 apply 0.207 ms vs 0.224
+    // with whole contiguous ranges per CTA and 0.251 with the stride).  OVERWRITE: grid stride.
+#ifndef TLC_K5A_RUN
+#define TLC_K5A_RUN 8
 #endif
-    const uint64_t per = kRuns ? (T.n5 + gridDim.x - 1) / gridDim.x : 1;
-    const uint64_t t_begin = kRuns ? per * blockIdx.x : blockIdx.x;
-    const uint64_t t_end = kRuns ? tmin<uint64_t>(T.n5, per * (blockIdx.x + 1)) : T.n5;
-    const uint64_t t_step = kRuns ? 1 : gridDim.x;
-    for (uint64_t tile = t_begin; tile < t_end; tile += t_step) {
+    // (a table with fewer than TLC_K5A_RUN tiles per CTA takes shorter runs: every CTA busy)
+    const uint64_t R = kMode != TLC_MODE_OVERWRITE
+                           ? tmax<uint64_t>(1, tmin<uint64_t>(TLC_K5A_RUN, (T.n5 + gridDim.x - 1) / gridDim.x))
+                           : 1u;
+    for (uint64_t it = 0;; it++) {
+        const uint64_t run = blockIdx.x + (it / R) * gridDim.x;
+        if (run * R >= T.n5) break;
+        const uint64_t tile = run * R + it % R;
+        if (tile >= T.n5) continue;
         const int si = find_seg_c<5>(T, tile, s_first);
         const Seg S = get_seg(T, si);
         const tlc_header *hdr = S.hdr;
